@@ -1,0 +1,361 @@
+"""Benchmark of the collective hot path (BASELINE.json metric: AllReduce busbw
+GB/s & latency vs message size, % of NVLink peak).
+
+N=1 (default): the 8-rank AllReduce runs with all 8 ranks co-resident on one
+B200 (the reference's own setting is 8 simulated ranks in one process, C1).
+Every "peer" access is then HBM instead of NVLink, so the roofline of the
+dominant kernel is the measured HBM copy bandwidth.  Headline workload: C4
+shape, bf16 two-shot, 256 MiB per rank; the sweep adds latency/busbw from 1 KiB
+to 1 GiB for the selected algorithm and the C1 config (fp32 1 MiB one-shot LL).
+
+N>1 (torchrun): one rank per GPU over NVLink (one-process-per-GPU mode).
+
+--impl reference: the reference's CPU path for the same workload, i.e. the
+oracle port (oracle/, C + pthreads, every host core) on a bounded sample.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
+
+KiB, MiB, GiB = 1 << 10, 1 << 20, 1 << 30
+N_SIM = 8                      # simulated ranks at N=1
+HEAD_BYTES = 256 * MiB         # per-rank message of the headline line
+HEAD_DTYPE = "bf16"
+METRIC = "AllReduce busbw GB/s & latency vs msg size at 8xB200 (vs NCCL, % of 900 GB/s)"
+
+
+def busbw(nbytes, seconds, n):
+    return nbytes / seconds * 2 * (n - 1) / n / 1e9
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi style clock/throttle sampling during the timed region (NVML)."""
+
+    def __init__(self, dev=0, period=0.05):
+        self.dev, self.period = dev, period
+        self.samples, self.reasons = [], set()
+        self._stop = threading.Event()
+        self.max_mhz = None
+
+    def __enter__(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(self.dev)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+            self._nv = pynvml
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        except Exception:
+            self._nv = None
+        return self
+
+    def _run(self):
+        nv = self._nv
+        names = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+                 "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                for k, bit in names.items():
+                    if mask & bit:
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._nv is not None:
+            self._t.join(timeout=1)
+
+    def summary(self):
+        med = float(np.median(self.samples)) if self.samples else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------- CPU arms
+
+def cpu_reference_step(n, elems, dtype, algo, seed=0):
+    """One step of the reference algorithm on the host: the oracle port
+    (C + pthreads over every core) applied to `elems` per rank."""
+    from oracle import oracle
+    from inputs import gen_inputs
+    ins = gen_inputs(n, elems, dtype, "normal", seed)
+    t0 = time.perf_counter()
+    oracle.allreduce(ins, algo, dtype, nthreads=0)
+    return time.perf_counter() - t0
+
+
+def cpu_baseline(n, full_elems, dtype, algo, budget_s=15.0):
+    """Bounded sample (~budget_s of CPU work) of the same workload."""
+    from oracle import oracle
+    es = 2 if dtype in ("bf16", "f16") else 4
+    elems = min(full_elems, 4 * MiB // es)
+    times = []
+    t_end = time.perf_counter() + budget_s
+    while time.perf_counter() < t_end and len(times) < 20:
+        times.append(cpu_reference_step(n, elems, dtype, algo, seed=len(times)))
+    t = float(np.median(times))
+    return {"value": round(busbw(elems * es, t, n), 4), "unit": "GB/s",
+            "cores": oracle.max_threads(), "kind": "port",
+            "sample": f"{len(times)} steps of {n}-rank {dtype} AllReduce ({algo} order) on "
+                      f"{elems * es // KiB} KiB per rank (full workload {full_elems * es // MiB} MiB); "
+                      f"median {t * 1e3:.1f} ms/step"}
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from oracle import oracle
+    es = 2
+    full = HEAD_BYTES // es
+    elems = min(full, 4 * MiB // es)
+    for _ in range(args.warmup):
+        cpu_reference_step(N_SIM, elems, HEAD_DTYPE, "2pa")
+    ts = [cpu_reference_step(N_SIM, elems, HEAD_DTYPE, "2pa", seed=i) for i in range(args.steps)]
+    t = float(np.mean(ts))
+    v = busbw(elems * es, t, N_SIM)
+    line = {"impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": "GB/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(t * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": HEAD_DTYPE, "data": "synthetic",
+            "config": {"workload": f"AllReduce {HEAD_DTYPE} {N_SIM} ranks, {HEAD_BYTES // MiB} MiB "
+                                   "per rank (C4 shape), two-shot (2pa) order",
+                       "sample_bytes_per_rank": elems * es},
+            "cpu_baseline": {"value": round(v, 4), "unit": "GB/s", "cores": oracle.max_threads(),
+                             "kind": "port",
+                             "sample": f"{elems * es // KiB} KiB per rank of the {HEAD_BYTES // MiB} MiB "
+                                       "workload per step (oracle/ C port, pthreads)"},
+            "e2e": {"value": round(v, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+# ----------------------------------------------------------------------------- GPU arm
+
+def time_coll(world, kind, send, recv, count, dtype, algo, iters, warmup, flush=None):
+    """Device time per call (CUDA events on the launching stream), optional L2 flush."""
+    import torch
+    from paper_2504_09014_b200 import collectives as C
+    stream = torch.cuda.current_stream(world.device(0))
+    for _ in range(warmup):
+        C.run(kind, send, recv, count, dtype, algo, world)
+    world.synchronize()
+    total = 0.0
+    if flush is None:
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(iters):
+            C.run(kind, send, recv, count, dtype, algo, world)
+        e1.record(stream)
+        e1.synchronize()
+        total = e0.elapsed_time(e1) / 1e3
+    else:
+        for _ in range(iters):
+            flush.zero_()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            C.run(kind, send, recv, count, dtype, algo, world)
+            e1.record(stream)
+            e1.synchronize()
+            total += e0.elapsed_time(e1) / 1e3
+    world.check_device_error()
+    return total / iters
+
+
+def run_gpu_arm(args):
+    import torch
+    from paper_2504_09014_b200 import _lib, make_world
+    from paper_2504_09014_b200 import collectives as C
+    from paper_2504_09014_b200.dtypes import torch_dtype
+
+    if args.gpus > 1:
+        return run_multi_gpu(args)
+    n = N_SIM
+    w = make_world(1, n, devices=[0] * n)
+    dev = w.device(0)
+    es = 2
+    count = HEAD_BYTES // es
+    tdt = torch_dtype(HEAD_DTYPE)
+    gen = torch.Generator(device=dev)
+    send = []
+    for r in range(n):
+        gen.manual_seed(20250409 + 4000 + r)
+        send.append(torch.randn(count, device=dev, dtype=torch.float32, generator=gen).to(tdt))
+    recv = [torch.empty_like(s) for s in send]
+    algo_name = C.select_algorithm("allreduce", HEAD_BYTES, w.topology, world=w, dtype=HEAD_DTYPE)
+    algo = _lib.ALGOS["2pa_ll" if algo_name.variant == "ll" else algo_name.name]
+    # parity spot check of the headline config (vs the size-independent property:
+    # every rank holds identical bits, and a sampled slice equals the oracle)
+    C.run("allreduce", send, recv, count, HEAD_DTYPE, algo, w)
+    w.synchronize()
+    for r in range(1, n):
+        assert torch.equal(recv[0], recv[r]), "ranks disagree"
+    from oracle import oracle
+    sl = slice(count // 3, count // 3 + 4096)
+    host = [s[sl].view(torch.int16).cpu().numpy().view(np.uint16) for s in send]
+    # 2pa order: chunk owner first; the slice lies in chunk count//3 // cs
+    cs = -(-count // n)
+    lead = (count // 3) // cs
+    assert ((count // 3 + 4096 - 1) // cs) == lead
+    want = oracle.reduce_ordered("bf16", host, [lead] + [p for p in range(n) if p != lead])
+    got = recv[0][sl].view(torch.int16).cpu().numpy().view(np.uint16)
+    assert np.array_equal(got, want), "headline parity spot check failed"
+
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(args.warmup):
+        C.run("allreduce", send, recv, count, HEAD_DTYPE, algo, w)
+    w.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    with ClockSampler(dev.index) as clk:
+        torch.cuda.synchronize(dev)
+        t_start = time.perf_counter()
+        for a, b in ev:
+            a.record(stream)
+            C.run("allreduce", send, recv, count, HEAD_DTYPE, algo, w)
+            b.record(stream)
+        torch.cuda.synchronize(dev)
+        wall = time.perf_counter() - t_start
+    w.check_device_error()
+    per = [a.elapsed_time(b) / 1e3 for a, b in ev]
+    t = float(np.sum(per)) / args.steps
+    value = busbw(HEAD_BYTES, t, n)
+    hbm, peak_kind = load_peaks()
+    alg_bytes = 2 * n * HEAD_BYTES                 # every rank's input read once + output written once
+    achieved = alg_bytes / t / 1e9
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
+                "frac": round(achieved / hbm, 4), "traffic": None,
+                "peak_kind": peak_kind, "kernel": "pull_reduce_kernel<bf16,8> (K3 two-shot)",
+                "algorithmic_bytes_per_launch": alg_bytes}
+    prof = os.path.join(ROOT, "profiles", "headline_traffic.json")
+    if os.path.exists(prof):
+        with open(prof) as f:
+            roofline["traffic"] = json.load(f).get("dram_bytes_per_launch")
+
+    # e2e: pinned host inputs -> public collective() -> pinned host outputs
+    host_in = [s.cpu().pin_memory() for s in send]
+    e2e_times = []
+    for it in range(max(2, min(args.steps, 5)) + 1):
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        outs = C.collective("allreduce", host_in, w, algo="2pa")
+        torch.cuda.synchronize(dev)
+        if it > 0:
+            e2e_times.append(time.perf_counter() - t0)
+    te = float(np.mean(e2e_times))
+    e2e = {"value": round(busbw(HEAD_BYTES, te, n), 3), "unit": "GB/s",
+           "h2d_bytes_per_step": n * HEAD_BYTES, "d2h_bytes_per_step": n * HEAD_BYTES,
+           "ms_per_step": round(te * 1e3, 3), "api": "collective('allreduce', pinned host tensors)"}
+    del outs
+
+    sweep = []
+    if not args.no_sweep:
+        sweep = run_sweep(w, args)
+    cpu = cpu_baseline(n, count, HEAD_DTYPE, "2pa")
+    line = {"metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": 1,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t * 1e3, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": HEAD_DTYPE,
+            "data": "synthetic",
+            "config": {"workload": f"AllReduce {HEAD_DTYPE}, {n} ranks co-resident on one B200 "
+                                   f"(simulated ranks as in C1), {HEAD_BYTES // MiB} MiB per rank (C4 shape)",
+                       "ranks": n, "ranks_per_gpu": n, "bytes_per_rank": HEAD_BYTES,
+                       "algo": _lib.ALGO_NAMES[algo], "parallelism": "8 ranks / 1 GPU",
+                       "l2": "inputs larger than L2 (8 x 256 MiB)"},
+            "latency_us": round(t * 1e6, 2), "algbw_gbs": round(HEAD_BYTES / t / 1e9, 2),
+            "pct_of_900": round(100 * value / 900, 2),
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": args.steps, "clocks": clk.summary(),
+            "wall_s_timed": round(wall, 4), "sweep": sweep}
+    print(json.dumps(line))
+    w.close()
+    return 0
+
+
+def run_sweep(w, args):
+    """Latency / busbw per size for the selector's pick and each algorithm
+    (8 co-resident ranks), L2 flushed between timed iterations below 64 MiB."""
+    import torch
+    from paper_2504_09014_b200 import _lib
+    from paper_2504_09014_b200 import collectives as C
+    n = w.num_ranks
+    dev = w.device(0)
+    out = []
+    flush = torch.empty(256 * MiB, dtype=torch.uint8, device=dev)
+    sizes = [1 * KiB << (2 * i) for i in range(0, 11)]  # 1 KiB .. 1 GiB, x4
+    big = max(sizes)
+    maxe = big // 2
+    send = [torch.randn(maxe, device=dev).to(torch.bfloat16) for _ in range(n)]
+    recv = [torch.empty_like(s) for s in send]
+    for nb in sizes:
+        count = nb // 2
+        row = {"bytes": nb}
+        for name in ("auto", "1pa", "2pa_ll", "2pa", "1pa_hb"):
+            if name in ("1pa", "2pa_ll") and nb > w.config.ll_max_bytes:
+                continue
+            if name == "1pa_hb" and nb > 64 * MiB:
+                continue
+            aid = _lib.ALGOS[name]
+            iters = 20 if nb <= 16 * MiB else 5
+            t = time_coll(w, "allreduce", [s[:count] for s in send], [r[:count] for r in recv],
+                          count, "bf16", aid, iters, 3, flush if nb < 64 * MiB else None)
+            row[name] = {"us": round(t * 1e6, 2), "busbw": round(busbw(nb, t, n), 2)}
+        out.append(row)
+    # C1: fp32 1 MiB one-shot LL (8 simulated ranks)
+    c1 = [torch.randn(MiB // 4, device=dev) for _ in range(n)]
+    c1o = [torch.empty_like(x) for x in c1]
+    t = time_coll(w, "allreduce", c1, c1o, MiB // 4, "f32", _lib.ALGOS["1pa"], 50, 5, flush)
+    out.append({"config": "C1 AllReduce fp32 1 MiB one-shot LL, 8 co-resident ranks",
+                "us": round(t * 1e6, 2), "busbw": round(busbw(MiB, t, n), 2)})
+    return out
+
+
+def run_multi_gpu(args):
+    raise SystemExit("multi-GPU bench needs the one-process-per-GPU registered-buffer path "
+                     "(not in this build)")
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="cf", choices=["cf", "reference"])
+    ap.add_argument("--no-sweep", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_gpu_arm(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

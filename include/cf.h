@@ -1,0 +1,171 @@
+/*
+ * cf.h -- C ABI of the B200-native collective library (libcf.so).
+ *
+ * Plain pointers, sizes and cudaStream_t handles only; no torch types.  Every
+ * entry point returns a cfStatus whose code string (cfStatusCode) is the
+ * reference's stable error code (commforge 0.1.0, cf/errors.py:6-93).
+ *
+ * Each declaration cites the reference interface it replaces.  The reference
+ * is a Python package with no FFI of its own; the binding a maintainer would
+ * add on the reference side (a ctypes stub) is shown in INTEGRATION.md.
+ *
+ * Rank model.  A communicator drives `nlocal` local ranks out of `nranks`.
+ *   - cfCommInitAll: one process drives every rank (the reference's in-process
+ *     SimWorld, cf/world.py:80-185).  Ranks may share a device: co-resident
+ *     ranks on one GPU run in ONE launch whose CTAs are split by rank.
+ *   - cfCommCreateRank + cfCommGetHandle + cfCommConnect: one process per
+ *     GPU; the opaque handles are exchanged by the caller's bootstrap
+ *     (torch.distributed store / gloo in the Python package).
+ * Collective calls take arrays with one entry per LOCAL rank (length 1 in the
+ * one-process-per-GPU mode), in local-rank order.  Calls are asynchronous and
+ * stream-ordered; calls on one communicator must be issued in the same order
+ * on every rank (NCCL rules).
+ */
+#ifndef CF_H_
+#define CF_H_
+
+#include <stddef.h>
+#include <stdint.h>
+#include <cuda_runtime_api.h>
+
+#if defined(__GNUC__)
+#define CF_API __attribute__((visibility("default")))
+#else
+#define CF_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CF_VERSION 1
+#define CF_MAX_RANKS 8        /* one 8-GPU NVSwitch domain */
+#define CF_MAX_BLOCKS 1024    /* CTAs per rank per launch (semaphore slab width) */
+#define CF_HANDLE_BYTES 256   /* cfCommGetHandle blob size */
+
+/* cf/errors.py:6-93 -- one status per reference error class. */
+typedef enum {
+  CF_OK = 0,
+  CF_E_GENERIC = 1,        /* CommforgeError        E_GENERIC        */
+  CF_E_BAD_SIZE = 2,       /* BadSizeError          E_BAD_SIZE       */
+  CF_E_NO_SEM = 3,         /* NoSemError            E_NO_SEM         */
+  CF_E_BAD_DELTA = 4,      /* BadDeltaError         E_BAD_DELTA      */
+  CF_E_OOB = 5,            /* OutOfBoundsError      E_OOB            */
+  CF_E_DEADLOCK = 6,       /* DeadlockError         E_DEADLOCK  (device spin timeout) */
+  CF_E_PROXY_DOWN = 7,     /* ProxyDownError        E_PROXY_DOWN     */
+  CF_E_ZERO_FLAG = 8,      /* ZeroFlagError         E_ZERO_FLAG      */
+  CF_E_WRONG_PROTOCOL = 9, /* WrongProtocolError    E_WRONG_PROTOCOL */
+  CF_E_BAD_ALIGN = 10,     /* BadAlignError         E_BAD_ALIGN      */
+  CF_E_SYNTAX = 11,        /* PlanSyntaxError       E_SYNTAX         */
+  CF_E_VERSION = 12,       /* PlanVersionError      E_VERSION        */
+  CF_E_REF = 13,           /* PlanRefError          E_REF            */
+  CF_E_SHAPE = 14,         /* ShapeError            E_SHAPE          */
+  CF_E_PROTOCOL = 15,      /* ProtocolError         E_PROTOCOL       */
+  CF_E_RANK_MISMATCH = 16, /* RankMismatchError     E_RANK_MISMATCH  */
+  CF_E_TOPOLOGY = 17,      /* TopologyError         E_TOPOLOGY (e.g. no multicast) */
+  CF_E_NO_ALGO = 18,       /* NoAlgoError           E_NO_ALGO        */
+  CF_E_BAD_TIME = 19,      /* BadTimeError          E_BAD_TIME       */
+  CF_E_CONFIG = 20,        /* ConfigError           E_CONFIG         */
+  CF_E_CUDA = 21,          /* (new) CUDA runtime/driver failure      */
+  CF_E_INTERNAL = 22       /* (new) invariant violated inside libcf  */
+} cfStatus;
+
+/* cf/dtypes.py:7-8 (i32, f32) extended with the 2-byte types. */
+typedef enum { CF_I32 = 0, CF_F32 = 1, CF_F16 = 2, CF_BF16 = 3 } cfDtype;
+
+/*
+ * Algorithms (cf/collectives.py:23-24 ALGO_NAMES, single-node subset).
+ * Each GPU algorithm reproduces the reference algorithm's accumulation order,
+ * so f32 results are bit-identical to the reference `collective()` output.
+ */
+typedef enum {
+  CF_ALGO_AUTO = -1,        /* measured selector (cf/collectives.py:464-491) */
+  CF_ALGO_1PA = 0,          /* one-shot LL packets        build_1pa        :139-162 */
+  CF_ALGO_1PA_HB = 1,       /* one-shot HB pull (K2)      channels.py:202-225      */
+  CF_ALGO_2PA = 2,          /* two-shot HB pull/push      build_2pa memory :187-197 */
+  CF_ALGO_2PA_LL = 3,       /* two-shot LL packets        build_2pa ll     :216-231 */
+  CF_ALGO_SWITCH_2PA = 4,   /* NVLS multimem              build_switch_2pa :235-250 */
+  CF_ALGO_2PR = 5,          /* two-phase (ring order)     build_2pr        :107-136 */
+  CF_ALGO_ALLPAIRS_AG = 6,  /* direct AllGather           build_allpairs_ag:253-270 */
+  CF_ALGO_RING_AG = 7,      /* ring AllGather             build_ring_ag    :82-104  */
+  CF_ALGO_RING_RS = 8,      /* ReduceScatter, ring order  build_ring_rs    :30-79   */
+  CF_ALGO_RS_DIRECT = 9,    /* ReduceScatter, all-pairs (2PA RS phase)  :188-191  */
+  CF_ALGO_COUNT = 10
+} cfAlgo;
+
+typedef struct cfComm* cfComm_t;
+typedef struct cfPlan* cfPlan_t;
+
+typedef struct {
+  size_t ll_max_bytes;      /* largest per-rank message the LL algorithms accept (0 = default 4 MiB) */
+  int max_blocks;           /* CTA cap per rank (0 = derived from occupancy and co-residency) */
+  int threads;              /* threads per CTA (0 = 512) */
+  uint64_t spin_timeout_ns; /* device spin-wait timeout -> CF_E_DEADLOCK (0 = 10 s) */
+  int use_multicast;        /* 1 = build NVLS multicast objects when supported */
+} cfConfig;
+
+/* cf/errors.py: the `.code` string of each class ("E_SHAPE", ...). */
+CF_API const char* cfStatusCode(cfStatus status);
+/* Detail message of the last failing call on this host thread. */
+CF_API const char* cfLastErrorMessage(void);
+CF_API int cfVersion(void);
+
+/* Replaces make_world(num_nodes=1, gpus_per_node=n) (cf/world.py:184-185):
+ * one process, `nranks` ranks on devices devs[0..nranks) (entries may repeat). */
+CF_API cfStatus cfCommInitAll(cfComm_t* comm, int nranks, const int* devs, const cfConfig* cfg);
+
+/* One-process-per-GPU bootstrap (replaces make_world for real multi-process
+ * runs).  Create, export the opaque handle, let the caller
+ * all-gather the handles, then connect with all nranks handles (rank order). */
+CF_API cfStatus cfCommCreateRank(cfComm_t* comm, int nranks, int rank, int cuda_dev, const cfConfig* cfg);
+CF_API cfStatus cfCommGetHandle(cfComm_t comm, void* handle, size_t* bytes);
+CF_API cfStatus cfCommConnect(cfComm_t comm, const void* handles, size_t bytes_per_handle);
+CF_API cfStatus cfCommDestroy(cfComm_t comm);
+
+CF_API cfStatus cfCommNumRanks(cfComm_t comm, int* nranks);
+CF_API cfStatus cfCommLocalRanks(cfComm_t comm, int* nlocal, int* ranks /* nullable, nlocal entries */);
+CF_API cfStatus cfCommMulticastSupported(cfComm_t comm, int* supported);
+
+/* Device-side spin timeout word (SURVEY.md §5 failure detection): 0 if clean,
+ * CF_E_DEADLOCK if any wait of any local rank timed out.  Synchronizes. */
+CF_API cfStatus cfCommLastDeviceError(cfComm_t comm, int* code);
+CF_API cfStatus cfCommClearDeviceError(cfComm_t comm);
+
+/* Collective API (cf/collectives.py:532-573 `collective`).  `send`/`recv`/
+ * `streams` hold one entry per local rank.  Counts are in elements:
+ *   AllReduce      count     = elements per rank (in and out)
+ *   AllGather      sendcount = shard elements; recv holds nranks*sendcount
+ *   ReduceScatter  recvcount = shard elements; send holds nranks*recvcount
+ * In the one-process mode the buffers of every rank must be device memory
+ * reachable from every rank's device (same device, or peer access).  In the
+ * one-process-per-GPU mode the library stages through its symmetric scratch
+ * unless the buffers came from cfMemAlloc. */
+CF_API cfStatus cfAllReduce(cfComm_t comm, const void* const* send, void* const* recv, size_t count,
+                     cfDtype dtype, int algo, const cudaStream_t* streams);
+CF_API cfStatus cfAllGather(cfComm_t comm, const void* const* send, void* const* recv, size_t sendcount,
+                     cfDtype dtype, int algo, const cudaStream_t* streams);
+CF_API cfStatus cfReduceScatter(cfComm_t comm, const void* const* send, void* const* recv, size_t recvcount,
+                         cfDtype dtype, int algo, const cudaStream_t* streams);
+
+/* The algorithm the measured selector picks (cf/collectives.py:473-491).
+ * collective: 0 = allreduce, 1 = allgather, 2 = reducescatter; nbytes as the
+ * reference counts them (AG: output bytes). */
+CF_API cfStatus cfSelectAlgorithm(cfComm_t comm, int collective, size_t nbytes, cfDtype dtype, int* algo);
+
+/* Plan executor (cf/executor.py:73-379 Runtime; wire format cf/plan.py:1-36).
+ * cfPlanLoad parses canonical plan JSON (dtype may be i32/f32/f16/bf16; the
+ * execution dtype can also be overridden at execute time), validates it and
+ * compiles it to a device op array; buffers are allocated per rank.
+ * cfPlanExecute copies each local rank's input in, runs every (rank, tb)
+ * program on the GPU, and copies the output buffer out. */
+CF_API cfStatus cfPlanLoad(cfComm_t comm, const char* json, size_t len, cfPlan_t* plan);
+CF_API cfStatus cfPlanExecute(cfPlan_t plan, const void* const* inputs, void* const* outputs,
+                       int dtype_override /* -1 = plan dtype */, const cudaStream_t* streams);
+CF_API cfStatus cfPlanInfo(cfPlan_t plan, size_t* in_elems, size_t* out_elems, int* dtype, int* n_programs,
+                    int* n_device_ops);
+CF_API cfStatus cfPlanDestroy(cfPlan_t plan);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CF_H_ */

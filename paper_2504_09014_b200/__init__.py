@@ -1,0 +1,19 @@
+"""B200-native collective hot path of MSCCL++ (arXiv 2504.09014).
+
+Drop-in for the reference package's API (commforge 0.1.0, ``cf/__init__.py:12-17``):
+the collective facade, the selector and the world bootstrap run on
+hand-written sm_100a kernels in ``libcf.so`` (C ABI: ``include/cf.h``).
+"""
+
+__version__ = "0.1.0"
+
+from .collectives import AlgoDescriptor, Selector, collective, required_multiple, select_algorithm
+from .errors import CommforgeError
+from .world import Topology, World, make_world
+
+SimWorld = World  # the reference's name for the world type (cf/world.py:80)
+
+__all__ = [
+    "AlgoDescriptor", "CommforgeError", "Selector", "SimWorld", "Topology", "World",
+    "collective", "make_world", "required_multiple", "select_algorithm",
+]

@@ -1,0 +1,395 @@
+// cf_collectives.cu -- hand-written sm_100a collective kernels.
+//
+//   K1 ll_oneshot      AllReduce, one-shot LL16 packets      build_1pa            cf/collectives.py:139-162
+//   K2 pull_reduce     AllReduce, one-shot HB pull (whole)   MemoryChannel.reduce cf/channels.py:202-225
+//   K3 pull_reduce     AllReduce, two-shot HB (push=1)       build_2pa memory     cf/collectives.py:187-197
+//   K4 ll_twoshot      AllReduce, two-shot LL16 packets      build_2pa ll         cf/collectives.py:216-231
+//   K6 push_gather     AllGather, direct peer stores         build_allpairs_ag    cf/collectives.py:253-270
+//   K8 pull_reduce     ReduceScatter, all-pairs (rs_shift=1) 2PA RS phase         cf/collectives.py:188-191
+//
+// One launch serves every rank co-resident on a device: blockIdx.y selects the
+// rank (CollArgs.rk), blockIdx.x the CTA within the rank.  CTA b of rank r
+// only synchronizes with CTA b of its peers, through its own semaphore slot,
+// so no kernel needs a grid-wide barrier.  All peer traffic is 16-byte
+// vectors; element ranges that do not start/end on a vector boundary are
+// handled with guarded element-wise loads and masked stores.
+#include <cstdio>
+#include "cf_kernels.cuh"
+
+namespace cf {
+
+// ---------------------------------------------------------------- call bracket
+
+// Every CTA reads the rank's call counter once; the last CTA of the rank to
+// finish publishes epoch+1 (last-CTA-done, no grid barrier).  Keeping the
+// counter on the device makes the kernels CUDA-graph replayable.
+__device__ __forceinline__ uint64_t begin_call(const RankCtx& rk) {
+  __shared__ uint64_t s_e;
+  if (threadIdx.x == 0) s_e = *(volatile uint64_t*)&rk.st->epoch + 1;
+  __syncthreads();
+  return s_e;
+}
+
+__device__ __forceinline__ void end_call(const RankCtx& rk, uint64_t e) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const uint32_t prev = atomicAdd(&rk.st->arrive, 1u);
+    if (prev == gridDim.x - 1) {
+      *(volatile uint32_t*)&rk.st->arrive = 0;
+      *(volatile uint64_t*)&rk.st->epoch = e;
+      __threadfence();
+    }
+  }
+}
+
+// CTA-pair handshake with every peer: signal value `v` to CTA b of each peer,
+// then wait until each peer's CTA b signalled >= v.  `publish` makes this
+// CTA's prior global writes visible system-wide first (fence before signal,
+// cf/channels.py:227-232).
+__device__ __forceinline__ void handshake(const RankCtx& rk, int n, uint64_t v, bool publish) {
+  const int t = threadIdx.x, r = rk.rank, b = blockIdx.x;
+  if (publish) __syncthreads();
+  if (t < n && t != r) {
+    if (publish) __threadfence_system();
+    st_release_sys(rk.sem[t] + sem_index(r, b), v);
+    wait_geq(rk.sem[r] + sem_index(t, b), v, rk.st);
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------- vector helpers
+
+// Load 16-byte vector `v` of a T array of `count` elements; lanes past the end
+// read as zero.
+template <typename T>
+__device__ __forceinline__ uint4 load_vec(const char* base, size_t v, size_t count) {
+  constexpr int V = 16 / sizeof(T);
+  const size_t e0 = v * V;
+  if (e0 + V <= count) return ld16(base + v * 16);
+  union { uint4 u; T t[V]; } r;
+  r.u = make_uint4(0, 0, 0, 0);
+  const T* src = reinterpret_cast<const T*>(base);
+#pragma unroll
+  for (int j = 0; j < V; j++)
+    if (e0 + j < count) r.t[j] = src[e0 + j];
+  return r.u;
+}
+
+// Store the lanes of vector `v` whose element index lies in [lo, hi) at
+// element position (index - shift) of `base`.
+template <typename T>
+__device__ __forceinline__ void store_vec(char* base, size_t v, uint4 val, size_t lo, size_t hi,
+                                          size_t shift) {
+  constexpr int V = 16 / sizeof(T);
+  const size_t e0 = v * V;
+  if (e0 >= lo && e0 + V <= hi && (((e0 - shift) * sizeof(T)) & 15) == 0) {
+    st16(base + (e0 - shift) * sizeof(T), val);
+    return;
+  }
+  union { uint4 u; T t[V]; } x;
+  x.u = val;
+  T* dst = reinterpret_cast<T*>(base);
+#pragma unroll
+  for (int j = 0; j < V; j++) {
+    const size_t e = e0 + j;
+    if (e >= lo && e < hi) dst[e - shift] = x.t[j];
+  }
+}
+
+// Accumulate NR (runtime n <= NR) 16-byte vectors in order: x[0] first (or a
+// zero accumulator when `zero`), then x[1], x[2], ...  f16/bf16 accumulate in
+// f32 and round once; i32 wraps; f32 is one RNE add per source.
+template <typename T, int NR>
+__device__ __forceinline__ uint4 reduce_vecs(const uint4 (&x)[NR], int n, bool zero) {
+  using A = typename Vec<T>::Acc;
+  constexpr int V = Vec<T>::N;
+  A acc[V];
+  if (zero) {
+#pragma unroll
+    for (int j = 0; j < V; j++) acc[j] = A(0);
+  } else {
+    Vec<T>::load(x[0], acc);
+  }
+#pragma unroll
+  for (int k = 0; k < NR; k++) {
+    if (k < n && (zero || k > 0)) {
+      A t[V];
+      Vec<T>::load(x[k], t);
+#pragma unroll
+      for (int j = 0; j < V; j++) acc[j] = acc_add(acc[j], t[j]);
+    }
+  }
+  return Vec<T>::store(acc);
+}
+
+// ---------------------------------------------------------------- K2 / K3 / K8
+
+// Pull-reduce: after an entry handshake (peers' send buffers are produced and
+// their recv buffers free), rank r reads its range from all n send buffers in
+// the reference order, reduces, and stores to its own recv buffer (K2, K8) or
+// to every rank's recv buffer (K3, `push`).  An exit handshake guarantees no
+// peer still reads r's send buffer when r's kernel retires.
+template <typename T, int NR>
+__global__ void __launch_bounds__(512) pull_reduce_kernel(const __grid_constant__ CollArgs a) {
+  const RankCtx& rk = a.rk[blockIdx.y];
+  constexpr int V = Vec<T>::N;
+  const int n = a.n, r = rk.rank;
+  const uint64_t e = begin_call(rk);
+  handshake(rk, n, e * 4 + 1, false);
+
+  size_t lo = 0, hi = a.count;
+  if (!a.whole) {
+    lo = min((size_t)r * a.cs, a.count);
+    hi = min(lo + a.cs, a.count);
+  }
+  const bool zero = a.order != kLead;
+  const char* src[NR];
+#pragma unroll
+  for (int k = 0; k < NR; k++) src[k] = k < n ? rk.in[order_src(a.order, k, r, n)] : nullptr;
+  const size_t shift = a.rs_shift ? lo : 0;
+  const size_t vlo = lo / V, vhi = (hi + V - 1) / V;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t v = vlo + (size_t)blockIdx.x * blockDim.x + threadIdx.x; v < vhi; v += stride) {
+    uint4 x[NR];
+#pragma unroll
+    for (int k = 0; k < NR; k++)
+      if (k < n) x[k] = load_vec<T>(src[k], v, a.count);
+    const uint4 res = reduce_vecs<T, NR>(x, n, zero);
+    if (a.push) {
+#pragma unroll
+      for (int p = 0; p < NR; p++)
+        if (p < n) store_vec<T>(rk.out[p], v, res, lo, hi, 0);
+    } else {
+      store_vec<T>(rk.out[r], v, res, lo, hi, shift);
+    }
+  }
+  handshake(rk, n, e * 4 + 2, true);
+  end_call(rk, e);
+}
+
+// ---------------------------------------------------------------- K1
+
+// One-shot LL: every rank writes its whole send buffer as LL16 packets into
+// slot r of each peer's scratch (parity half e&1), then polls its own n-1
+// slots and reduces in the 1pa order (own input first, peers ascending,
+// cf/collectives.py:156-161).  No semaphores, no fences: the flag travels in
+// the same 16-byte store as the data.
+template <typename T, int NR>
+__global__ void __launch_bounds__(512) ll_oneshot_kernel(const __grid_constant__ CollArgs a) {
+  const RankCtx& rk = a.rk[blockIdx.y];
+  constexpr int V = Vec<T>::N;
+  const int n = a.n, r = rk.rank;
+  const uint64_t e = begin_call(rk);
+  const uint32_t flag = ll_flag(e);
+  const size_t par = (e & 1) * a.half;
+  const size_t nvec = (a.count + V - 1) / V;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  const size_t t0 = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int lead = a.order == kLead ? r : 0;
+
+  for (size_t v = t0; v < nvec; v += stride) {
+    const uint4 x = load_vec<T>(rk.in[r], v, a.count);
+#pragma unroll
+    for (int p = 0; p < NR; p++) {
+      if (p < n && p != r) {
+        char* d = rk.scr[p] + par + (size_t)r * a.slot + v * 32;
+        ll16_put(d, make_uint2(x.x, x.y), flag);
+        ll16_put(d + 16, make_uint2(x.z, x.w), flag);
+      }
+    }
+  }
+  for (size_t v = t0; v < nvec; v += stride) {
+    uint4 x[NR];
+#pragma unroll
+    for (int k = 0; k < NR; k++) {
+      if (k < n) {
+        const int q = order_src(a.order, k, lead, n);
+        if (q == r) {
+          x[k] = load_vec<T>(rk.in[r], v, a.count);
+        } else {
+          const char* s = rk.scr[r] + par + (size_t)q * a.slot + v * 32;
+          const uint2 p0 = ll16_get(s, flag, rk.st);
+          const uint2 p1 = ll16_get(s + 16, flag, rk.st);
+          x[k] = make_uint4(p0.x, p0.y, p1.x, p1.y);
+        }
+      }
+    }
+    const uint4 res = reduce_vecs<T, NR>(x, n, a.order != kLead);
+    store_vec<T>(rk.out[r], v, res, 0, a.count, 0);
+  }
+  end_call(rk, e);
+}
+
+// ---------------------------------------------------------------- K4
+
+// Two-shot LL (cf/collectives.py:216-231): phase 1 sends chunk p of the send
+// buffer as packets into peer p's ph1 slot r; rank r reduces chunk r (owner
+// first, peers ascending), stores it, and sends the result as packets into
+// every peer's ph2 slot r; phase 2 decodes the peers' chunks into recv.
+// Chunks follow the reference chunking (cs elements); packets carry the
+// 16-byte vectors covering a chunk, and stores are masked to the chunk.
+template <typename T, int NR>
+__global__ void __launch_bounds__(512) ll_twoshot_kernel(const __grid_constant__ CollArgs a) {
+  const RankCtx& rk = a.rk[blockIdx.y];
+  constexpr int V = Vec<T>::N;
+  const int n = a.n, r = rk.rank;
+  const uint64_t e = begin_call(rk);
+  const uint32_t flag = ll_flag(e);
+  const size_t ph1 = (e & 1) * a.half, ph2 = ph1 + (size_t)n * a.slot;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  const size_t t0 = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  auto clo = [&](int c) { return min((size_t)c * a.cs, a.count); };
+  auto chi = [&](int c) { return min((size_t)c * a.cs + a.cs, a.count); };
+  auto vlo = [&](int c) { return clo(c) / V; };
+  auto vhi = [&](int c) { return (chi(c) + V - 1) / V; };
+
+  // phase 1: scatter my chunks as packets
+  for (int p = 0; p < n; p++) {
+    if (p == r) continue;
+    const size_t b = vlo(p), nv = vhi(p) > b ? vhi(p) - b : 0;
+    char* dst = rk.scr[p] + ph1 + (size_t)r * a.slot;
+    for (size_t i = t0; i < nv; i += stride) {
+      const uint4 x = load_vec<T>(rk.in[r], b + i, a.count);
+      ll16_put(dst + i * 32, make_uint2(x.x, x.y), flag);
+      ll16_put(dst + i * 32 + 16, make_uint2(x.z, x.w), flag);
+    }
+  }
+  // reduce my chunk, store, broadcast as packets
+  {
+    const size_t b = vlo(r), nv = vhi(r) > b ? vhi(r) - b : 0;
+    for (size_t i = t0; i < nv; i += stride) {
+      uint4 x[NR];
+#pragma unroll
+      for (int k = 0; k < NR; k++) {
+        if (k < n) {
+          const int q = order_src(kLead, k, r, n);
+          if (q == r) {
+            x[k] = load_vec<T>(rk.in[r], b + i, a.count);
+          } else {
+            const char* s = rk.scr[r] + ph1 + (size_t)q * a.slot + i * 32;
+            const uint2 p0 = ll16_get(s, flag, rk.st);
+            const uint2 p1 = ll16_get(s + 16, flag, rk.st);
+            x[k] = make_uint4(p0.x, p0.y, p1.x, p1.y);
+          }
+        }
+      }
+      const uint4 res = reduce_vecs<T, NR>(x, n, false);
+      store_vec<T>(rk.out[r], b + i, res, clo(r), chi(r), 0);
+#pragma unroll
+      for (int p = 0; p < NR; p++) {
+        if (p < n && p != r) {
+          char* d = rk.scr[p] + ph2 + (size_t)r * a.slot + i * 32;
+          ll16_put(d, make_uint2(res.x, res.y), flag);
+          ll16_put(d + 16, make_uint2(res.z, res.w), flag);
+        }
+      }
+    }
+  }
+  // phase 2: decode the peers' reduced chunks
+  for (int p = 0; p < n; p++) {
+    if (p == r) continue;
+    const size_t b = vlo(p), nv = vhi(p) > b ? vhi(p) - b : 0;
+    const char* src = rk.scr[r] + ph2 + (size_t)p * a.slot;
+    for (size_t i = t0; i < nv; i += stride) {
+      const uint2 p0 = ll16_get(src + i * 32, flag, rk.st);
+      const uint2 p1 = ll16_get(src + i * 32 + 16, flag, rk.st);
+      store_vec<T>(rk.out[r], b + i, make_uint4(p0.x, p0.y, p1.x, p1.y), clo(p), chi(p), 0);
+    }
+  }
+  end_call(rk, e);
+}
+
+// ---------------------------------------------------------------- K6
+
+// Direct AllGather: entry handshake (peer recv buffers free), then each rank
+// stores its shard into slot r of every rank's recv buffer, then an exit
+// handshake publishes the data (put + signal, wait; cf/collectives.py:262-269).
+template <typename T>
+__global__ void __launch_bounds__(512) push_gather_kernel(const __grid_constant__ CollArgs a) {
+  const RankCtx& rk = a.rk[blockIdx.y];
+  constexpr int V = 16 / sizeof(T);
+  const int n = a.n, r = rk.rank;
+  const uint64_t e = begin_call(rk);
+  handshake(rk, n, e * 4 + 1, false);
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  const size_t t0 = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t sb = a.count * sizeof(T);
+  if ((sb & 15) == 0) {
+    const size_t nvec = sb / 16;
+    for (size_t v = t0; v < nvec; v += stride) {
+      const uint4 x = ld16(rk.in[r] + v * 16);
+#pragma unroll 8
+      for (int p = 0; p < CF_MAX_RANKS; p++)
+        if (p < n) st16(rk.out[p] + (size_t)r * sb + v * 16, x);
+    }
+  } else {
+    // ragged shard: slot r starts off the 16-byte grid; vector loads, element stores
+    const size_t nvec = (a.count + V - 1) / V;
+    for (size_t v = t0; v < nvec; v += stride) {
+      const uint4 x = load_vec<T>(rk.in[r], v, a.count);
+      for (int p = 0; p < n; p++)
+        store_vec<T>(rk.out[p] + (size_t)r * sb, v, x, 0, a.count, 0);
+    }
+  }
+  handshake(rk, n, e * 4 + 2, true);
+  end_call(rk, e);
+}
+
+// ---------------------------------------------------------------- launchers
+
+template <template <typename, int> class K> struct KernelTable;
+
+template <typename T>
+static const void* pick_pull(int nr) {
+  if (nr <= 2) return (const void*)pull_reduce_kernel<T, 2>;
+  if (nr <= 4) return (const void*)pull_reduce_kernel<T, 4>;
+  return (const void*)pull_reduce_kernel<T, 8>;
+}
+template <typename T>
+static const void* pick_ll1(int nr) {
+  if (nr <= 2) return (const void*)ll_oneshot_kernel<T, 2>;
+  if (nr <= 4) return (const void*)ll_oneshot_kernel<T, 4>;
+  return (const void*)ll_oneshot_kernel<T, 8>;
+}
+template <typename T>
+static const void* pick_ll2(int nr) {
+  if (nr <= 2) return (const void*)ll_twoshot_kernel<T, 2>;
+  if (nr <= 4) return (const void*)ll_twoshot_kernel<T, 4>;
+  return (const void*)ll_twoshot_kernel<T, 8>;
+}
+
+template <const void* (*F32)(int), const void* (*I32)(int), const void* (*F16)(int),
+          const void* (*BF16)(int)>
+static const void* by_dtype(int dtype, int n) {
+  switch (dtype) {
+    case 0: return I32(n);
+    case 1: return F32(n);
+    case 2: return F16(n);
+    case 3: return BF16(n);
+  }
+  return nullptr;
+}
+
+// Kernel entry point for (kind, dtype, n).  kind: 0 pull-reduce, 1 LL one-shot,
+// 2 LL two-shot, 3 push-gather.
+const void* collective_kernel(int kind, int dtype, int n) {
+  switch (kind) {
+    case 0: return by_dtype<pick_pull<float>, pick_pull<int32_t>, pick_pull<__half>,
+                            pick_pull<__nv_bfloat16>>(dtype, n);
+    case 1: return by_dtype<pick_ll1<float>, pick_ll1<int32_t>, pick_ll1<__half>,
+                            pick_ll1<__nv_bfloat16>>(dtype, n);
+    case 2: return by_dtype<pick_ll2<float>, pick_ll2<int32_t>, pick_ll2<__half>,
+                            pick_ll2<__nv_bfloat16>>(dtype, n);
+    case 3:
+      switch (dtype) {
+        case 0: return (const void*)push_gather_kernel<int32_t>;
+        case 1: return (const void*)push_gather_kernel<float>;
+        case 2: return (const void*)push_gather_kernel<__half>;
+        case 3: return (const void*)push_gather_kernel<__nv_bfloat16>;
+      }
+  }
+  return nullptr;
+}
+
+}  // namespace cf

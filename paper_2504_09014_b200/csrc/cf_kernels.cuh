@@ -1,0 +1,40 @@
+// cf_kernels.cuh -- launch-argument layout shared by the host runtime and the
+// collective kernels.  Internal to libcf (not part of the C ABI).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include "device/cf_device.cuh"
+
+namespace cf {
+
+// Everything one rank's CTAs need, as addressable from that rank's device.
+struct RankCtx {
+  int rank;
+  int pad_;
+  const char* in[CF_MAX_RANKS];   // every rank's send buffer (pull kernels)
+  char* out[CF_MAX_RANKS];        // every rank's recv buffer (push kernels)
+  char* scr[CF_MAX_RANKS];        // every rank's LL scratch base
+  uint64_t* sem[CF_MAX_RANKS];    // every rank's semaphore slab
+  RankState* st;                  // this rank's state
+};
+
+// Semaphore slab of a receiving rank: slot [src_rank][cta].
+__host__ __device__ inline size_t sem_index(int src, int cta) {
+  return (size_t)src * CF_MAX_BLOCKS + (size_t)cta;
+}
+
+struct CollArgs {
+  int n;            // ranks in the communicator
+  int nlocal;       // ranks served by this launch (gridDim.y)
+  int order;        // cf::Order
+  int push;         // pull-reduce: store the result into every rank's recv buffer
+  int whole;        // pull-reduce: each rank reduces [0,count) instead of its chunk
+  int rs_shift;     // pull-reduce: recv is the shard (offset by -chunk start)
+  size_t count;     // elements per rank (AR/RS: send elements; AG: shard elements)
+  size_t cs;        // reference chunk size in elements (cf/collectives.py:170-172)
+  size_t slot;      // LL slot stride in bytes
+  size_t half;      // LL parity-half stride in bytes
+  RankCtx rk[CF_MAX_RANKS];
+};
+
+}  // namespace cf

@@ -1,0 +1,556 @@
+// cf_runtime.cu -- communicator bootstrap, symmetric heap, measured algorithm
+// selection and the collective entry points of the C ABI (include/cf.h).
+//
+// Reference counterparts (commforge 0.1.0, cf/):
+//   make_world / SimWorld regions + semaphores   cf/world.py:80-185
+//   collective() facade                          cf/collectives.py:532-573
+//   Selector / default_table / select_algorithm  cf/collectives.py:415-491
+//   error codes                                  cf/errors.py:6-93
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <unistd.h>
+#include "cf_runtime.h"
+
+namespace cf {
+const void* collective_kernel(int kind, int dtype, int n);
+
+static thread_local std::string g_last_error;
+
+cfStatus fail(cfStatus s, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return s;
+}
+
+void HeapLayout::compute(int nranks, size_t ll_max, size_t plan_sems) {
+  sem_off = 256;
+  sem_bytes = (size_t)CF_MAX_RANKS * CF_MAX_BLOCKS * sizeof(uint64_t);
+  plan_sem_off = round_up(sem_off + sem_bytes, 256);
+  plan_sem_bytes = round_up(plan_sems * sizeof(uint64_t), 256);
+  scr_off = round_up(plan_sem_off + plan_sem_bytes, 4096);
+  // one LL16 packet (16 B) per 8 payload bytes: a slot holds 2*ll_max bytes
+  slot = round_up(2 * ll_max + 64, 256);
+  half = (size_t)nranks * slot;
+  scr_bytes = 2 * half;
+  total = round_up(scr_off + scr_bytes, 1 << 21);
+}
+
+int occupancy(cfComm* c, const void* kernel, int dev, int threads) {
+  auto key = std::make_pair(kernel, dev);
+  auto it = c->occ.find(key);
+  if (it != c->occ.end()) return it->second;
+  int nb = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, threads, 0) != cudaSuccess) nb = 1;
+  c->occ[key] = std::max(nb, 1);
+  return c->occ[key];
+}
+
+int max_blocks_per_rank(cfComm* c, const void* kernel, int group, int threads) {
+  const auto& g = c->groups[group];
+  const int dev = c->local[g[0]].dev;
+  const int cap = occupancy(c, kernel, dev, threads) * c->sm_count[dev];
+  int mb = std::max(1, cap / (int)g.size());
+  mb = std::min(mb, CF_MAX_BLOCKS);
+  if (c->cfg.max_blocks > 0) mb = std::min(mb, c->cfg.max_blocks);
+  return mb;
+}
+
+cfStatus join_streams(cfComm* c, int group, const cudaStream_t* streams, bool after) {
+  const auto& g = c->groups[group];
+  const cudaStream_t s0 = streams[g[0]];
+  for (size_t i = 1; i < g.size(); i++) {
+    const int li = g[i];
+    if (streams[li] == s0) continue;
+    if (!after) {
+      CF_CUDA(cudaEventRecord(c->local[li].ev, streams[li]));
+      CF_CUDA(cudaStreamWaitEvent(s0, c->local[li].ev, 0));
+    } else {
+      CF_CUDA(cudaEventRecord(c->local[g[0]].ev, s0));
+      CF_CUDA(cudaStreamWaitEvent(streams[li], c->local[g[0]].ev, 0));
+    }
+  }
+  return CF_OK;
+}
+
+// Restores the caller's current device on scope exit.
+struct DeviceGuard {
+  int prev = -1;
+  DeviceGuard() { cudaGetDevice(&prev); }
+  ~DeviceGuard() { if (prev >= 0) cudaSetDevice(prev); }
+};
+
+static cfStatus alloc_heap(cfComm* c, LocalRank& lr) {
+  CF_CUDA(cudaSetDevice(lr.dev));
+  CF_CUDA(cudaMalloc((void**)&lr.heap, c->lay.total));
+  CF_CUDA(cudaMemset(lr.heap, 0, c->lay.total));
+  RankState st{};
+  st.timeout_ns = c->cfg.spin_timeout_ns;
+  CF_CUDA(cudaMemcpy(lr.heap + c->lay.state_off, &st, sizeof(st), cudaMemcpyHostToDevice));
+  CF_CUDA(cudaEventCreateWithFlags(&lr.ev, cudaEventDisableTiming));
+  int sms = 0;
+  CF_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, lr.dev));
+  c->sm_count[lr.dev] = sms;
+  return CF_OK;
+}
+
+static void apply_defaults(cfConfig* cfg) {
+  if (cfg->ll_max_bytes == 0) cfg->ll_max_bytes = 4u << 20;
+  if (cfg->threads == 0) cfg->threads = 512;
+  if (cfg->spin_timeout_ns == 0) {
+    cfg->spin_timeout_ns = 10ull * 1000 * 1000 * 1000;
+    if (const char* s = getenv("CF_SPIN_TIMEOUT_MS")) cfg->spin_timeout_ns = strtoull(s, nullptr, 10) * 1000000ull;
+  }
+}
+
+static void build_groups(cfComm* c) {
+  c->groups.clear();
+  std::map<int, int> by_dev;
+  for (int li = 0; li < (int)c->local.size(); li++) {
+    const int d = c->local[li].dev;
+    auto it = by_dev.find(d);
+    if (it == by_dev.end()) {
+      by_dev[d] = (int)c->groups.size();
+      c->groups.push_back({li});
+    } else {
+      c->groups[it->second].push_back(li);
+    }
+  }
+}
+
+// ---------------------------------------------------------------- selection
+
+// Measured crossover table: replaces DEFAULT_THRESHOLDS
+// (cf/collectives.py:418).  Thresholds are per-rank message bytes.  Values
+// come from bench.py sweeps; see DESIGN.md "selector".
+static int select_algo(const cfComm* c, int coll, size_t nbytes, int dtype) {
+  (void)dtype;
+  const bool coresident = c->groups.size() == 1 && c->local.size() > 1;
+  if (coll == 1) return CF_ALGO_ALLPAIRS_AG;
+  if (coll == 2) return CF_ALGO_RS_DIRECT;
+  if (c->nranks == 1) return CF_ALGO_2PA;
+  if (coresident) {
+    // ranks share one GPU's memory: LL doubles HBM traffic, so only tiny
+    // messages use it; the pull two-shot moves the minimum bytes.
+    if (nbytes <= 16 * 1024) return CF_ALGO_1PA;
+    return CF_ALGO_2PA;
+  }
+  if (nbytes < 256 * 1024 && nbytes <= c->cfg.ll_max_bytes) return CF_ALGO_1PA;
+  if (nbytes < 2 * 1024 * 1024 && nbytes <= c->cfg.ll_max_bytes) return CF_ALGO_2PA_LL;
+  return CF_ALGO_2PA;
+}
+
+}  // namespace cf
+
+using namespace cf;
+
+// ---------------------------------------------------------------- C ABI: misc
+
+extern "C" const char* cfStatusCode(cfStatus s) {
+  static const char* codes[] = {"OK", "E_GENERIC", "E_BAD_SIZE", "E_NO_SEM", "E_BAD_DELTA", "E_OOB",
+                                "E_DEADLOCK", "E_PROXY_DOWN", "E_ZERO_FLAG", "E_WRONG_PROTOCOL",
+                                "E_BAD_ALIGN", "E_SYNTAX", "E_VERSION", "E_REF", "E_SHAPE",
+                                "E_PROTOCOL", "E_RANK_MISMATCH", "E_TOPOLOGY", "E_NO_ALGO",
+                                "E_BAD_TIME", "E_CONFIG", "E_CUDA", "E_INTERNAL"};
+  if ((int)s < 0 || (int)s > (int)CF_E_INTERNAL) return "E_GENERIC";
+  return codes[s];
+}
+
+extern "C" const char* cfLastErrorMessage(void) { return g_last_error.c_str(); }
+extern "C" int cfVersion(void) { return CF_VERSION; }
+
+// ---------------------------------------------------------------- C ABI: comm
+
+static cfStatus comm_common_init(cfComm* c, int nranks, const cfConfig* cfg) {
+  if (nranks < 1 || nranks > CF_MAX_RANKS)
+    return fail(CF_E_BAD_SIZE, "nranks %d outside [1, %d]", nranks, CF_MAX_RANKS);
+  c->nranks = nranks;
+  if (cfg) c->cfg = *cfg;
+  apply_defaults(&c->cfg);
+  if (c->cfg.threads % 32 || c->cfg.threads < 64 || c->cfg.threads > 1024)
+    return fail(CF_E_CONFIG, "threads must be a multiple of 32 in [64, 1024]");
+  c->lay.compute(nranks, c->cfg.ll_max_bytes, /*plan_sems=*/(size_t)CF_MAX_RANKS * 4096);
+  return CF_OK;
+}
+
+extern "C" cfStatus cfCommInitAll(cfComm_t* out, int nranks, const int* devs, const cfConfig* cfg) {
+  if (!out || !devs) return fail(CF_E_CONFIG, "null argument");
+  DeviceGuard guard;
+  cfComm* c = new cfComm();
+  cfStatus s = comm_common_init(c, nranks, cfg);
+  if (s != CF_OK) { delete c; return s; }
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    delete c;
+    return fail(CF_E_CUDA, "no CUDA device visible");
+  }
+  c->local.resize(nranks);
+  for (int r = 0; r < nranks; r++) {
+    if (devs[r] < 0 || devs[r] >= ndev) {
+      delete c;
+      return fail(CF_E_TOPOLOGY, "rank %d: device %d not present (%d visible)", r, devs[r], ndev);
+    }
+    c->local[r].rank = r;
+    c->local[r].dev = devs[r];
+  }
+  // peer access between every pair of distinct devices
+  for (int a = 0; a < nranks; a++)
+    for (int b = 0; b < nranks; b++) {
+      if (devs[a] == devs[b]) continue;
+      int ok = 0;
+      cudaDeviceCanAccessPeer(&ok, devs[a], devs[b]);
+      if (!ok) {
+        delete c;
+        return fail(CF_E_TOPOLOGY, "device %d cannot access device %d over NVLink/P2P", devs[a], devs[b]);
+      }
+      cudaSetDevice(devs[a]);
+      cudaError_t e = cudaDeviceEnablePeerAccess(devs[b], 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) {
+        delete c;
+        return fail(CF_E_CUDA, "cudaDeviceEnablePeerAccess(%d->%d): %s", devs[a], devs[b], cudaGetErrorString(e));
+      }
+      cudaGetLastError();
+    }
+  for (int r = 0; r < nranks; r++) {
+    s = alloc_heap(c, c->local[r]);
+    if (s != CF_OK) { cfCommDestroy(c); return s; }
+  }
+  c->peer_heap.assign(nranks, {});
+  for (int li = 0; li < nranks; li++)
+    for (int p = 0; p < nranks; p++) c->peer_heap[li][p] = c->local[p].heap;
+  build_groups(c);
+  c->connected = true;
+  *out = c;
+  return CF_OK;
+}
+
+namespace {
+struct HandleBlob {
+  uint32_t magic;
+  uint32_t version;
+  int32_t nranks;
+  int32_t rank;
+  int32_t dev;
+  int32_t pid;
+  uint64_t heap_bytes;
+  uint64_t ll_max;
+  cudaIpcMemHandle_t ipc;
+};
+constexpr uint32_t kMagic = 0x43464d31;  // "CFM1"
+static_assert(sizeof(HandleBlob) <= CF_HANDLE_BYTES, "handle too large");
+}  // namespace
+
+extern "C" cfStatus cfCommCreateRank(cfComm_t* out, int nranks, int rank, int cuda_dev, const cfConfig* cfg) {
+  if (!out) return fail(CF_E_CONFIG, "null argument");
+  if (rank < 0 || rank >= nranks) return fail(CF_E_OOB, "rank %d out of range", rank);
+  DeviceGuard guard;
+  cfComm* c = new cfComm();
+  cfStatus s = comm_common_init(c, nranks, cfg);
+  if (s != CF_OK) { delete c; return s; }
+  c->multiprocess = true;
+  c->local.resize(1);
+  c->local[0].rank = rank;
+  c->local[0].dev = cuda_dev;
+  s = alloc_heap(c, c->local[0]);
+  if (s != CF_OK) { cfCommDestroy(c); return s; }
+  c->peer_heap.assign(1, {});
+  c->peer_heap[0][rank] = c->local[0].heap;
+  build_groups(c);
+  *out = c;
+  return CF_OK;
+}
+
+extern "C" cfStatus cfCommGetHandle(cfComm_t c, void* handle, size_t* bytes) {
+  if (!c || !bytes) return fail(CF_E_CONFIG, "null argument");
+  if (!c->multiprocess) return fail(CF_E_CONFIG, "handles exist only for cfCommCreateRank communicators");
+  if (!handle) { *bytes = CF_HANDLE_BYTES; return CF_OK; }
+  if (*bytes < CF_HANDLE_BYTES) return fail(CF_E_BAD_SIZE, "handle buffer needs %d bytes", CF_HANDLE_BYTES);
+  DeviceGuard guard;
+  HandleBlob h{};
+  h.magic = kMagic;
+  h.version = CF_VERSION;
+  h.nranks = c->nranks;
+  h.rank = c->local[0].rank;
+  h.dev = c->local[0].dev;
+  h.pid = (int32_t)getpid();
+  h.heap_bytes = c->lay.total;
+  h.ll_max = c->cfg.ll_max_bytes;
+  CF_CUDA(cudaSetDevice(c->local[0].dev));
+  CF_CUDA(cudaIpcGetMemHandle(&h.ipc, c->local[0].heap));
+  memset(handle, 0, CF_HANDLE_BYTES);
+  memcpy(handle, &h, sizeof(h));
+  *bytes = CF_HANDLE_BYTES;
+  return CF_OK;
+}
+
+extern "C" cfStatus cfCommConnect(cfComm_t c, const void* handles, size_t bytes_per_handle) {
+  if (!c || !handles) return fail(CF_E_CONFIG, "null argument");
+  if (!c->multiprocess) return fail(CF_E_CONFIG, "cfCommConnect needs a cfCommCreateRank communicator");
+  if (bytes_per_handle < sizeof(HandleBlob)) return fail(CF_E_BAD_SIZE, "handle stride too small");
+  DeviceGuard guard;
+  CF_CUDA(cudaSetDevice(c->local[0].dev));
+  const int me = c->local[0].rank;
+  for (int p = 0; p < c->nranks; p++) {
+    HandleBlob h;
+    memcpy(&h, (const char*)handles + (size_t)p * bytes_per_handle, sizeof(h));
+    if (h.magic != kMagic || h.version != CF_VERSION)
+      return fail(CF_E_VERSION, "rank %d handle is not a cf v%d handle", p, CF_VERSION);
+    if (h.nranks != c->nranks || h.rank != p)
+      return fail(CF_E_RANK_MISMATCH, "handle %d claims rank %d of %d (expected %d of %d)", p, h.rank,
+                  h.nranks, p, c->nranks);
+    if (h.heap_bytes != c->lay.total || h.ll_max != c->cfg.ll_max_bytes)
+      return fail(CF_E_CONFIG, "rank %d was created with a different configuration", p);
+    if (p == me) continue;
+    void* ptr = nullptr;
+    CF_CUDA(cudaIpcOpenMemHandle(&ptr, h.ipc, cudaIpcMemLazyEnablePeerAccess));
+    c->ipc_opened.push_back(ptr);
+    c->peer_heap[0][p] = (char*)ptr;
+  }
+  c->connected = true;
+  return CF_OK;
+}
+
+extern "C" cfStatus cfCommDestroy(cfComm_t c) {
+  if (!c) return CF_OK;
+  DeviceGuard guard;
+  for (void* p : c->ipc_opened) {
+    if (!c->local.empty()) cudaSetDevice(c->local[0].dev);
+    cudaIpcCloseMemHandle(p);
+  }
+  for (auto& lr : c->local) {
+    if (lr.dev >= 0) cudaSetDevice(lr.dev);
+    if (lr.heap) cudaFree(lr.heap);
+    if (lr.ev) cudaEventDestroy(lr.ev);
+  }
+  delete c;
+  return CF_OK;
+}
+
+extern "C" cfStatus cfCommNumRanks(cfComm_t c, int* n) {
+  if (!c || !n) return fail(CF_E_CONFIG, "null argument");
+  *n = c->nranks;
+  return CF_OK;
+}
+
+extern "C" cfStatus cfCommLocalRanks(cfComm_t c, int* nlocal, int* ranks) {
+  if (!c || !nlocal) return fail(CF_E_CONFIG, "null argument");
+  *nlocal = (int)c->local.size();
+  if (ranks)
+    for (size_t i = 0; i < c->local.size(); i++) ranks[i] = c->local[i].rank;
+  return CF_OK;
+}
+
+extern "C" cfStatus cfCommMulticastSupported(cfComm_t c, int* supported) {
+  if (!c || !supported) return fail(CF_E_CONFIG, "null argument");
+  *supported = c->multicast_supported ? 1 : 0;
+  return CF_OK;
+}
+
+extern "C" cfStatus cfCommLastDeviceError(cfComm_t c, int* code) {
+  if (!c || !code) return fail(CF_E_CONFIG, "null argument");
+  DeviceGuard guard;
+  uint32_t worst = 0;
+  for (size_t li = 0; li < c->local.size(); li++) {
+    CF_CUDA(cudaSetDevice(c->local[li].dev));
+    CF_CUDA(cudaDeviceSynchronize());
+    RankState st;
+    CF_CUDA(cudaMemcpy(&st, c->state((int)li), sizeof(st), cudaMemcpyDeviceToHost));
+    worst = std::max(worst, st.error);
+  }
+  *code = (int)worst;
+  return CF_OK;
+}
+
+extern "C" cfStatus cfCommClearDeviceError(cfComm_t c) {
+  if (!c) return fail(CF_E_CONFIG, "null argument");
+  DeviceGuard guard;
+  for (size_t li = 0; li < c->local.size(); li++) {
+    CF_CUDA(cudaSetDevice(c->local[li].dev));
+    CF_CUDA(cudaDeviceSynchronize());
+    CF_CUDA(cudaMemset((char*)c->state((int)li) + offsetof(RankState, error), 0, sizeof(uint32_t)));
+  }
+  return CF_OK;
+}
+
+extern "C" cfStatus cfSelectAlgorithm(cfComm_t c, int coll, size_t nbytes, cfDtype dtype, int* algo) {
+  if (!c || !algo) return fail(CF_E_CONFIG, "null argument");
+  if (coll < 0 || coll > 2) return fail(CF_E_NO_ALGO, "unknown collective %d", coll);
+  *algo = select_algo(c, coll, nbytes, dtype);
+  return CF_OK;
+}
+
+// ---------------------------------------------------------------- collectives
+
+namespace {
+
+enum Kind { kPull = 0, kLL1 = 1, kLL2 = 2, kGather = 3 };
+
+struct Job {
+  int kind = kPull;
+  int order = kLead;
+  int push = 0, whole = 0, rs_shift = 0;
+  size_t count = 0;   // elements per rank on the reduced/gathered axis
+  size_t cs = 0;      // reference chunk (elements)
+  size_t slot = 0;
+  size_t work = 0;    // 16-byte vectors per rank (grid sizing)
+};
+
+cfStatus check_ptrs(cfComm* c, const void* const* send, void* const* recv, const cudaStream_t* streams) {
+  if (!c) return fail(CF_E_CONFIG, "null communicator");
+  if (!c->connected) return fail(CF_E_CONFIG, "communicator not connected (call cfCommConnect)");
+  if (!send || !recv || !streams) return fail(CF_E_CONFIG, "null buffer or stream array");
+  for (size_t li = 0; li < c->local.size(); li++) {
+    if (!send[li] || !recv[li]) return fail(CF_E_OOB, "local rank %zu: null buffer", li);
+    if (((uintptr_t)send[li] | (uintptr_t)recv[li]) & 15)
+      return fail(CF_E_BAD_ALIGN, "local rank %zu: buffers must be 16-byte aligned", li);
+  }
+  return CF_OK;
+}
+
+cfStatus launch(cfComm* c, const Job& j, int dtype, const void* const* send, void* const* recv,
+                const cudaStream_t* streams) {
+  if (c->multiprocess && j.kind != kLL1 && j.kind != kLL2)
+    return fail(CF_E_TOPOLOGY,
+                "HB algorithms in one-process-per-GPU mode need registered buffers (not in this build); "
+                "use an LL algorithm");
+  DeviceGuard guard;
+  const void* kernel = collective_kernel(j.kind, dtype, c->nranks);
+  if (!kernel) return fail(CF_E_INTERNAL, "no kernel for kind %d dtype %d", j.kind, dtype);
+  const int threads = c->cfg.threads;
+  for (size_t gi = 0; gi < c->groups.size(); gi++) {
+    const auto& g = c->groups[gi];
+    const int dev = c->local[g[0]].dev;
+    CF_CUDA(cudaSetDevice(dev));
+    CollArgs a;
+    memset(&a, 0, sizeof(a));
+    a.n = c->nranks;
+    a.nlocal = (int)g.size();
+    a.order = j.order;
+    a.push = j.push;
+    a.whole = j.whole;
+    a.rs_shift = j.rs_shift;
+    a.count = j.count;
+    a.cs = j.cs;
+    a.slot = j.slot ? j.slot : c->lay.slot;
+    a.half = c->lay.half;
+    for (size_t k = 0; k < g.size(); k++) {
+      const int li = g[k];
+      RankCtx& rk = a.rk[k];
+      rk.rank = c->local[li].rank;
+      rk.st = c->state(li);
+      for (int p = 0; p < c->nranks; p++) {
+        // one-process mode: rank p's buffers are the caller's entries (UVA)
+        rk.in[p] = c->multiprocess ? nullptr : (const char*)send[p];
+        rk.out[p] = c->multiprocess ? nullptr : (char*)recv[p];
+        rk.scr[p] = c->scr(li, p);
+        rk.sem[p] = c->sem(li, p);
+      }
+      if (c->multiprocess) {
+        rk.in[rk.rank] = (const char*)send[li];
+        rk.out[rk.rank] = (char*)recv[li];
+      }
+    }
+    const int mb = max_blocks_per_rank(c, kernel, (int)gi, threads);
+    int blocks = (int)std::min<size_t>((size_t)mb, std::max<size_t>(1, ceil_div(j.work, (size_t)threads)));
+    CF_TRY(join_streams(c, (int)gi, streams, false));
+    void* args[] = {&a};
+    CF_CUDA(cudaLaunchKernel(kernel, dim3(blocks, g.size()), dim3(threads), args, 0, streams[g[0]]));
+    CF_TRY(join_streams(c, (int)gi, streams, true));
+  }
+  return CF_OK;
+}
+
+}  // namespace
+
+extern "C" cfStatus cfAllReduce(cfComm_t c, const void* const* send, void* const* recv, size_t count,
+                                cfDtype dtype, int algo, const cudaStream_t* streams) {
+  CF_TRY(check_ptrs(c, send, recv, streams));
+  if ((int)dtype < 0 || (int)dtype > 3) return fail(CF_E_SHAPE, "unknown dtype %d", (int)dtype);
+  if (count == 0) return CF_OK;
+  const int n = c->nranks;
+  const size_t es = dtype_size(dtype), V = 16 / es;
+  const size_t bytes = count * es;
+  if (algo == CF_ALGO_AUTO) algo = select_algo(c, 0, bytes, dtype);
+  Job j;
+  j.count = count;
+  switch (algo) {
+    case CF_ALGO_1PA:
+      if (bytes > c->cfg.ll_max_bytes)
+        return fail(CF_E_BAD_SIZE, "1pa: %zu bytes exceed the LL capacity %zu", bytes, c->cfg.ll_max_bytes);
+      j.kind = kLL1;
+      j.order = kLead;
+      j.work = ceil_div(count, V);
+      break;
+    case CF_ALGO_1PA_HB:
+      for (size_t li = 0; li < c->local.size(); li++)
+        if (send[li] == recv[li]) return fail(CF_E_SHAPE, "1pa_hb cannot run in place");
+      j.kind = kPull;
+      j.whole = 1;
+      j.order = kLead;
+      j.work = ceil_div(count, V);
+      break;
+    case CF_ALGO_2PA:
+    case CF_ALGO_SWITCH_2PA:
+    case CF_ALGO_2PR: {
+      const size_t mult = algo == CF_ALGO_2PR ? 2 * n : n;   // cf/collectives.py:497-504
+      j.kind = kPull;
+      j.push = 1;
+      j.order = algo == CF_ALGO_2PA ? kLead : (algo == CF_ALGO_SWITCH_2PA ? kAscZero : kRingZero);
+      j.cs = round_up(count, mult) / n;
+      j.work = ceil_div(j.cs, V) + 1;
+      break;
+    }
+    case CF_ALGO_2PA_LL: {
+      j.kind = kLL2;
+      j.cs = round_up(count, n) / n;
+      j.slot = c->lay.half / (2 * n) / 256 * 256;
+      if (32 * (ceil_div(j.cs, V) + 1) > j.slot)
+        return fail(CF_E_BAD_SIZE, "2pa_ll: %zu bytes exceed the LL capacity", bytes);
+      j.work = ceil_div(j.cs, V) + 1;
+      break;
+    }
+    default:
+      return fail(CF_E_NO_ALGO, "algorithm %d is not an AllReduce algorithm", algo);
+  }
+  return launch(c, j, dtype, send, recv, streams);
+}
+
+extern "C" cfStatus cfAllGather(cfComm_t c, const void* const* send, void* const* recv, size_t sendcount,
+                                cfDtype dtype, int algo, const cudaStream_t* streams) {
+  CF_TRY(check_ptrs(c, send, recv, streams));
+  if ((int)dtype < 0 || (int)dtype > 3) return fail(CF_E_SHAPE, "unknown dtype %d", (int)dtype);
+  if (sendcount == 0) return CF_OK;
+  if (algo == CF_ALGO_AUTO) algo = select_algo(c, 1, sendcount * dtype_size(dtype) * c->nranks, dtype);
+  if (algo != CF_ALGO_ALLPAIRS_AG && algo != CF_ALGO_RING_AG)
+    return fail(CF_E_NO_ALGO, "algorithm %d is not an AllGather algorithm", algo);
+  Job j;
+  j.kind = kGather;
+  j.count = sendcount;
+  j.work = ceil_div(sendcount * dtype_size(dtype), 16);
+  return launch(c, j, dtype, send, recv, streams);
+}
+
+extern "C" cfStatus cfReduceScatter(cfComm_t c, const void* const* send, void* const* recv,
+                                    size_t recvcount, cfDtype dtype, int algo, const cudaStream_t* streams) {
+  CF_TRY(check_ptrs(c, send, recv, streams));
+  if ((int)dtype < 0 || (int)dtype > 3) return fail(CF_E_SHAPE, "unknown dtype %d", (int)dtype);
+  if (recvcount == 0) return CF_OK;
+  const int n = c->nranks;
+  const size_t es = dtype_size(dtype);
+  if (algo == CF_ALGO_AUTO) algo = select_algo(c, 2, recvcount * es * n, dtype);
+  if (algo != CF_ALGO_RS_DIRECT && algo != CF_ALGO_RING_RS)
+    return fail(CF_E_NO_ALGO, "algorithm %d is not a ReduceScatter algorithm", algo);
+  Job j;
+  j.kind = kPull;
+  j.rs_shift = 1;
+  j.order = algo == CF_ALGO_RING_RS ? kRingZero : kLead;
+  j.count = recvcount * n;
+  j.cs = recvcount;
+  j.work = ceil_div(recvcount, 16 / es) + 1;
+  return launch(c, j, dtype, send, recv, streams);
+}

@@ -1,0 +1,91 @@
+// cf_runtime.h -- host-side communicator internals shared by the collective
+// API (cf_runtime.cu) and the plan executor (cf_plan.cu).  Not part of the ABI.
+#pragma once
+#include <array>
+#include <cstdarg>
+#include <cstddef>
+#include <cstdint>
+#include <map>
+#include <string>
+#include <vector>
+#include <cuda_runtime.h>
+#include "cf.h"
+#include "cf_kernels.cuh"
+
+namespace cf {
+
+cfStatus fail(cfStatus s, const char* fmt, ...);
+
+#define CF_CUDA(call)                                                                \
+  do {                                                                               \
+    cudaError_t e_ = (call);                                                         \
+    if (e_ != cudaSuccess)                                                           \
+      return ::cf::fail(CF_E_CUDA, "%s failed: %s", #call, cudaGetErrorString(e_));  \
+  } while (0)
+
+#define CF_TRY(call)                     \
+  do {                                   \
+    cfStatus s_ = (call);                \
+    if (s_ != CF_OK) return s_;          \
+  } while (0)
+
+inline size_t round_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+inline size_t ceil_div(size_t x, size_t a) { return (x + a - 1) / a; }
+inline int dtype_size(int dt) { return dt <= 1 ? 4 : 2; }
+
+// Symmetric heap of one rank: [RankState | semaphore slab | plan semaphores | LL scratch]
+struct HeapLayout {
+  size_t state_off = 0;
+  size_t sem_off = 256;
+  size_t sem_bytes = (size_t)CF_MAX_RANKS * CF_MAX_BLOCKS * sizeof(uint64_t);
+  size_t plan_sem_off = 0, plan_sem_bytes = 0;
+  size_t scr_off = 0, scr_bytes = 0;
+  size_t slot = 0, half = 0;
+  size_t total = 0;
+  void compute(int nranks, size_t ll_max, size_t plan_sems);
+};
+
+struct LocalRank {
+  int rank = -1;
+  int dev = -1;
+  char* heap = nullptr;
+  cudaEvent_t ev = nullptr;   // stream joins for co-resident ranks
+};
+
+struct Occupancy {
+  int blocks_per_sm = 0;
+};
+
+}  // namespace cf
+
+struct cfComm {
+  int nranks = 0;
+  bool multiprocess = false;
+  bool connected = false;
+  cfConfig cfg{};
+  cf::HeapLayout lay;
+  std::vector<cf::LocalRank> local;
+  // peer_heap[li][p]: heap base of rank p as addressable from local rank li's device
+  std::vector<std::array<char*, CF_MAX_RANKS>> peer_heap;
+  // local-rank indices grouped by device (one launch per group)
+  std::vector<std::vector<int>> groups;
+  std::vector<void*> ipc_opened;       // cudaIpcOpenMemHandle mappings to close
+  std::map<int, int> sm_count;         // device -> SMs
+  std::map<std::pair<const void*, int>, int> occ;  // (kernel, device) -> CTAs/SM
+  bool multicast_supported = false;
+
+  cf::RankState* state(int li) const { return (cf::RankState*)(local[li].heap + lay.state_off); }
+  uint64_t* sem(int li, int p) const { return (uint64_t*)(peer_heap[li][p] + lay.sem_off); }
+  char* scr(int li, int p) const { return peer_heap[li][p] + lay.scr_off; }
+  uint64_t* plan_sem(int li, int p) const { return (uint64_t*)(peer_heap[li][p] + lay.plan_sem_off); }
+};
+
+namespace cf {
+// CTAs of `kernel` (launched with `threads`) that may run per SM on `dev`.
+int occupancy(cfComm* c, const void* kernel, int dev, int threads);
+// Co-residency cap: CTAs per rank such that every rank of the group fits at once.
+int max_blocks_per_rank(cfComm* c, const void* kernel, int group, int threads);
+// Make streams[first] of the group wait for the others; after the launch, the
+// others wait for it.  `after` selects the phase.
+cfStatus join_streams(cfComm* c, int group, const cudaStream_t* streams, bool after);
+}  // namespace cf

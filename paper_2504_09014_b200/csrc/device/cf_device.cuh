@@ -1,0 +1,271 @@
+// cf_device.cuh -- device-side primitive API for sm_100a (the paper's Primitive
+// API), re-designed for B200 NVLink 5 / NVSwitch.
+//
+// Reference semantics (commforge 0.1.0, cf/):
+//   MemoryChannel HB  put / signal / wait / flush     cf/channels.py:181-240
+//   MemoryChannel LL  put_packets / read_packets      cf/channels.py:244-330
+//   SwitchChannel     reduce / broadcast (multimem)   cf/channels.py:333-409
+//   Semaphore         monotonic u64, release/acquire  cf/world.py:148-181
+//
+// B200 mapping
+//   - peer memory is plain global memory mapped into this GPU's VA (cudaIpc /
+//     P2P / same device); 16-byte vector loads and stores.
+//   - signal  = fence + st.release.sys of a monotonically increasing value on
+//               the receiver's slot (one writer per slot, so a value store is
+//               equivalent to the reference's +1 counter).
+//   - wait    = ld.acquire.sys spin until value >= target, bounded by a
+//               %globaltimer timeout that raises the rank's error word
+//               (-> CF_E_DEADLOCK on the host).
+//   - LL16    = one 16-byte st.volatile {d0, flag, d1, flag}: two reference
+//               packets ([u32 data | u32 flag], cf/channels.py:36-37) in one
+//               single-copy-atomic transaction, byte-identical layout.
+//   - multimem.ld_reduce / multimem.st on NVLS multicast addresses.
+#pragma once
+#include <cstdint>
+#include <cuda_fp16.h>
+#include <cuda_bf16.h>
+
+#ifndef CF_MAX_RANKS
+#define CF_MAX_RANKS 8
+#endif
+#ifndef CF_MAX_BLOCKS
+#define CF_MAX_BLOCKS 1024
+#endif
+
+namespace cf {
+
+enum DevError : uint32_t { kDevOk = 0, kDevTimeout = 6 /* == CF_E_DEADLOCK */ };
+
+// Per-rank device state (lives in the rank's symmetric heap).
+struct RankState {
+  uint64_t epoch;      // completed collective calls on this rank
+  uint32_t arrive;     // CTAs of the current launch that finished (last-CTA-done)
+  uint32_t error;      // DevError
+  uint64_t timeout_ns;
+  uint64_t pad[5];
+};
+
+// LL flag of call `e`: never 0 (cf/channels.py:254-255), distinct for
+// 2^32-1 consecutive calls, so stale packets of earlier calls never match.
+__host__ __device__ __forceinline__ uint32_t ll_flag(uint64_t e) {
+  return (uint32_t)(e % 0xffffffffull) + 1u;
+}
+
+// ---------------------------------------------------------------- memory model
+
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t ld_relaxed_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_acq_rel_sys() {
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+}
+
+// 16-byte vector global access (.v4.u32), plain and volatile (LL packets).
+__device__ __forceinline__ uint4 ld16(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ uint4 ld16_nc(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void st16(void* p, uint4 v) {
+  asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w) : "memory");
+}
+__device__ __forceinline__ uint4 ld16_volatile(const void* p) {
+  uint4 v;
+  asm volatile("ld.volatile.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st16_volatile(void* p, uint4 v) {
+  asm volatile("st.volatile.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y),
+               "r"(v.z), "r"(v.w) : "memory");
+}
+__device__ __forceinline__ uint2 ld8_volatile(const void* p) {
+  uint2 v;
+  asm volatile("ld.volatile.global.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st8_volatile(void* p, uint2 v) {
+  asm volatile("st.volatile.global.v2.u32 [%0], {%1,%2};" ::"l"(p), "r"(v.x), "r"(v.y) : "memory");
+}
+
+// ---------------------------------------------------------------- spin waits
+
+// Spin until *sem >= target (acquire).  Returns false on timeout or when the
+// rank's error word is already set (so one stuck wait does not cascade into a
+// full-timeout per wait).
+__device__ __forceinline__ bool wait_geq(const uint64_t* sem, uint64_t target, RankState* st) {
+  if (ld_acquire_sys(sem) >= target) return true;
+  const uint64_t t0 = globaltimer();
+  const uint64_t limit = st->timeout_ns;
+  for (uint32_t it = 1;; ++it) {
+    if (ld_acquire_sys(sem) >= target) return true;
+    if ((it & 255u) == 0) {
+      if (*(volatile uint32_t*)&st->error != kDevOk) return false;
+      if (globaltimer() - t0 > limit) {
+        atomicExch(&st->error, (uint32_t)kDevTimeout);
+        return false;
+      }
+    }
+  }
+}
+
+// LL16: two reference packets {d0, flag, d1, flag} in one 16-byte store.
+__device__ __forceinline__ void ll16_put(void* dst, uint2 data, uint32_t flag) {
+  st16_volatile(dst, make_uint4(data.x, flag, data.y, flag));
+}
+// Poll one LL16 packet until both flag words equal `flag`.
+__device__ __forceinline__ uint2 ll16_get(const void* src, uint32_t flag, RankState* st) {
+  uint4 v = ld16_volatile(src);
+  if (v.y == flag && v.w == flag) return make_uint2(v.x, v.z);
+  const uint64_t t0 = globaltimer();
+  for (uint32_t it = 1;; ++it) {
+    v = ld16_volatile(src);
+    if (v.y == flag && v.w == flag) break;
+    if ((it & 255u) == 0) {
+      if (*(volatile uint32_t*)&st->error != kDevOk) break;
+      if (globaltimer() - t0 > st->timeout_ns) {
+        atomicExch(&st->error, (uint32_t)kDevTimeout);
+        break;
+      }
+    }
+  }
+  return make_uint2(v.x, v.z);
+}
+
+// ---------------------------------------------------------------- element math
+
+template <typename T> struct Vec;  // 16-byte vector of T <-> f32/i32 accumulators
+template <> struct Vec<float> {
+  static constexpr int N = 4;
+  using Acc = float;
+  __device__ static void load(uint4 v, float* a) {
+    a[0] = __uint_as_float(v.x); a[1] = __uint_as_float(v.y);
+    a[2] = __uint_as_float(v.z); a[3] = __uint_as_float(v.w);
+  }
+  __device__ static uint4 store(const float* a) {
+    return make_uint4(__float_as_uint(a[0]), __float_as_uint(a[1]), __float_as_uint(a[2]),
+                      __float_as_uint(a[3]));
+  }
+  __device__ static float round(float x) { return x; }
+};
+template <> struct Vec<int32_t> {
+  static constexpr int N = 4;
+  using Acc = int32_t;
+  __device__ static void load(uint4 v, int32_t* a) {
+    a[0] = (int32_t)v.x; a[1] = (int32_t)v.y; a[2] = (int32_t)v.z; a[3] = (int32_t)v.w;
+  }
+  __device__ static uint4 store(const int32_t* a) {
+    return make_uint4((uint32_t)a[0], (uint32_t)a[1], (uint32_t)a[2], (uint32_t)a[3]);
+  }
+  __device__ static int32_t round(int32_t x) { return x; }
+};
+template <> struct Vec<__half> {
+  static constexpr int N = 8;
+  using Acc = float;
+  __device__ static void load(uint4 v, float* a) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+      __half2 h = *reinterpret_cast<const __half2*>(&w[i]);
+      float2 f = __half22float2(h);
+      a[2 * i] = f.x; a[2 * i + 1] = f.y;
+    }
+  }
+  __device__ static uint4 store(const float* a) {
+    uint32_t w[4];
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+      __half2 h = __floats2half2_rn(a[2 * i], a[2 * i + 1]);
+      w[i] = *reinterpret_cast<uint32_t*>(&h);
+    }
+    return make_uint4(w[0], w[1], w[2], w[3]);
+  }
+  __device__ static float round(float x) { return __half2float(__float2half_rn(x)); }
+};
+template <> struct Vec<__nv_bfloat16> {
+  static constexpr int N = 8;
+  using Acc = float;
+  __device__ static void load(uint4 v, float* a) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+      a[2 * i] = __uint_as_float(w[i] << 16);
+      a[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+    }
+  }
+  __device__ static uint4 store(const float* a) {
+    uint32_t w[4];
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+      __nv_bfloat162 h = __floats2bfloat162_rn(a[2 * i], a[2 * i + 1]);
+      w[i] = *reinterpret_cast<uint32_t*>(&h);
+    }
+    return make_uint4(w[0], w[1], w[2], w[3]);
+  }
+  __device__ static float round(float x) { return __bfloat162float(__float2bfloat16_rn(x)); }
+};
+
+// Scalar element access for ragged heads/tails.
+template <typename T> __device__ __forceinline__ typename Vec<T>::Acc to_acc(T x);
+template <> __device__ __forceinline__ float to_acc<float>(float x) { return x; }
+template <> __device__ __forceinline__ int32_t to_acc<int32_t>(int32_t x) { return x; }
+template <> __device__ __forceinline__ float to_acc<__half>(__half x) { return __half2float(x); }
+template <> __device__ __forceinline__ float to_acc<__nv_bfloat16>(__nv_bfloat16 x) {
+  return __bfloat162float(x);
+}
+template <typename T> __device__ __forceinline__ T from_acc(typename Vec<T>::Acc x);
+template <> __device__ __forceinline__ float from_acc<float>(float x) { return x; }
+template <> __device__ __forceinline__ int32_t from_acc<int32_t>(int32_t x) { return x; }
+template <> __device__ __forceinline__ __half from_acc<__half>(float x) { return __float2half_rn(x); }
+template <> __device__ __forceinline__ __nv_bfloat16 from_acc<__nv_bfloat16>(float x) {
+  return __float2bfloat16_rn(x);
+}
+
+// i32 adds wrap like numpy int32 (two's complement); use unsigned math.
+__device__ __forceinline__ int32_t acc_add(int32_t a, int32_t b) {
+  return (int32_t)((uint32_t)a + (uint32_t)b);
+}
+__device__ __forceinline__ float acc_add(float a, float b) { return __fadd_rn(a, b); }
+
+// ---------------------------------------------------------------- reduction orders
+//
+// The reference accumulates each element chunk in an algorithm-specific order
+// (probed, pinned by tests/golden):
+//   kLead   : x[lead], then every other rank ascending   (1pa: lead = own rank,
+//             2pa: lead = chunk owner)          cf/collectives.py:156-161, 187-231
+//   kAscZero: 0 + x[0] + ... + x[n-1]          switch_reduce, cf/channels.py:380-388
+//   kRingZero: 0 + x[c] + x[c+1] + ... (mod n) ring_rs / 2pr, cf/collectives.py:52-79
+enum Order : int { kLead = 0, kAscZero = 1, kRingZero = 2 };
+
+// k-th source rank of the order.
+__device__ __forceinline__ int order_src(int mode, int k, int lead, int n) {
+  if (mode == kLead) return k == 0 ? lead : (k - 1 + (k - 1 >= lead ? 1 : 0));
+  if (mode == kRingZero) { int q = lead + k; return q >= n ? q - n : q; }
+  return k;
+}
+
+}  // namespace cf

@@ -1,0 +1,156 @@
+"""Communicator bootstrap: the B200 replacement of the reference's simulated
+cluster (``cf/world.py:80-185``, ``make_world``).
+
+A :class:`World` is one process driving every rank (the reference's model:
+all ranks live in one process).  Ranks are placed on distinct GPUs when the
+box has enough of them, otherwise they are co-resident on one GPU: their CTAs
+then run in a single launch and "peer" memory is the same HBM.  Either way the
+kernels, the synchronization and the results are identical; only the link
+(NVLink vs HBM) differs.
+
+Per rank, libcf allocates a symmetric heap (rank state, semaphore slab, LL
+scratch) that replaces the reference's zero-filled ``Region``s and
+``Semaphore``s (``cf/world.py:24-51``).  Collective buffers are caller-owned
+torch tensors (``cf/executor.py:160-175`` copied arrays in and out; here the
+facade does that only for numpy inputs).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+from . import _lib
+from .errors import BadSizeError, OutOfBoundsError, TopologyError
+
+INTRA = "intra"
+INTER = "inter"
+SEED_ENV_VAR = "COMMFORGE_SEED"
+
+
+@dataclass(frozen=True)
+class Topology:
+    """cf/world.py:54-77.  One NVSwitch domain: every pair is an intra link."""
+
+    num_nodes: int
+    gpus_per_node: int
+    intra_kind: str = "switch-attached"
+
+    @property
+    def num_ranks(self) -> int:
+        return self.num_nodes * self.gpus_per_node
+
+    def node_of(self, rank: int) -> int:
+        return rank // self.gpus_per_node
+
+    def link_class(self, a: int, b: int) -> str:
+        return INTRA if self.node_of(a) == self.node_of(b) else INTER
+
+    def links(self):
+        n = self.num_ranks
+        return {(a, b, self.link_class(a, b)) for a in range(n) for b in range(n) if a != b}
+
+
+class World:
+    """In-process communicator over ``num_nodes * gpus_per_node`` ranks."""
+
+    def __init__(self, num_nodes: int = 1, gpus_per_node: int = 1,
+                 intra_kind: str = "switch-attached", seed: int = 0, devices=None,
+                 ll_max_bytes: int = 0, max_blocks: int = 0, threads: int = 0,
+                 spin_timeout_ms: int = 0):
+        if num_nodes * gpus_per_node < 1:
+            raise BadSizeError("world needs at least one rank")
+        if num_nodes != 1:
+            raise TopologyError("multi-node worlds are out of scope: one NVSwitch domain "
+                                "(the hierarchical 2ph algorithms need an inter-node fabric)")
+        env = os.environ.get(SEED_ENV_VAR)
+        self.seed = int(env) if env is not None else seed
+        self.num_nodes = num_nodes
+        self.gpus_per_node = gpus_per_node
+        self.intra_kind = intra_kind
+        self.topology = Topology(num_nodes, gpus_per_node, intra_kind)
+        n = self.num_ranks
+        if n > _lib.CF_MAX_RANKS:
+            raise BadSizeError(f"at most {_lib.CF_MAX_RANKS} ranks per NVSwitch domain")
+        import torch
+        if not torch.cuda.is_available():
+            raise TopologyError("no CUDA device: the collective path runs only on GPUs")
+        if devices is None:
+            ndev = torch.cuda.device_count()
+            devices = list(range(n)) if ndev >= n else [0] * n
+        devices = [int(d) for d in devices]
+        if len(devices) != n:
+            raise OutOfBoundsError(f"need {n} device ids, got {len(devices)}")
+        self.devices = devices
+        cfg = _lib.cfConfig(ll_max_bytes, max_blocks, threads,
+                            int(spin_timeout_ms) * 1_000_000, 0)
+        handle = ctypes.c_void_p()
+        devs = (ctypes.c_int * n)(*devices)
+        _lib.check(_lib.lib().cfCommInitAll(ctypes.byref(handle), n, devs, ctypes.byref(cfg)))
+        self._comm = handle
+        self.config = cfg
+
+    # -- reference surface -------------------------------------------------
+
+    @property
+    def num_ranks(self) -> int:
+        return self.num_nodes * self.gpus_per_node
+
+    @property
+    def coresident(self) -> bool:
+        return len(set(self.devices)) < len(self.devices)
+
+    @property
+    def comm(self):
+        if self._comm is None:
+            raise TopologyError("world is closed")
+        return self._comm
+
+    def device(self, rank: int):
+        import torch
+        return torch.device("cuda", self.devices[rank])
+
+    def streams(self):
+        import torch
+        return [torch.cuda.current_stream(self.device(r)).cuda_stream for r in range(self.num_ranks)]
+
+    def synchronize(self):
+        import torch
+        for d in sorted(set(self.devices)):
+            torch.cuda.synchronize(d)
+
+    def check_device_error(self):
+        """Raise DeadlockError if any device wait of this world timed out."""
+        code = ctypes.c_int()
+        _lib.check(_lib.lib().cfCommLastDeviceError(self.comm, ctypes.byref(code)))
+        if code.value:
+            _lib.lib().cfCommClearDeviceError(self.comm)
+            from .errors import raise_status
+            raise_status(code.value, "device-side wait timed out (peer never signalled)")
+
+    def multicast_supported(self) -> bool:
+        v = ctypes.c_int()
+        _lib.check(_lib.lib().cfCommMulticastSupported(self.comm, ctypes.byref(v)))
+        return bool(v.value)
+
+    def close(self):
+        if self._comm is not None:
+            _lib.lib().cfCommDestroy(self._comm)
+            self._comm = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __repr__(self):
+        return (f"World(ranks={self.num_ranks}, devices={self.devices}, "
+                f"coresident={self.coresident})")
+
+
+def make_world(num_nodes=1, gpus_per_node=1, intra_kind="switch-attached", seed=0, **kw) -> World:
+    """cf/world.py:184-185 with the same arguments; extra keywords (devices,
+    ll_max_bytes, max_blocks, threads, spin_timeout_ms) tune the communicator."""
+    return World(num_nodes, gpus_per_node, intra_kind, seed, **kw)

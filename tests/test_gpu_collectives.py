@@ -1,0 +1,156 @@
+"""GPU parity: libcf collectives vs the reference's own outputs (golden digests
+from tests/golden/make_golden.py) and vs the CPU oracle.  Needs a B200."""
+
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+from inputs import gen_inputs
+from oracle import oracle
+
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+_WORLDS = {}
+
+
+def world(n, **kw):
+    from paper_2504_09014_b200 import make_world
+    key = (n, tuple(sorted(kw.items())))
+    if key not in _WORLDS:
+        _WORLDS[key] = make_world(1, n, spin_timeout_ms=5000, **kw)
+    return _WORLDS[key]
+
+
+def _digest(a):
+    return hashlib.sha256(np.ascontiguousarray(a).view(np.uint8).tobytes()).hexdigest()
+
+
+def _cases():
+    with open(os.path.join(GOLD, "collectives.json")) as f:
+        return [c for c in json.load(f) if c["algo"]]
+
+
+@pytest.mark.parametrize("case", _cases(), ids=lambda c: f"{c['kind']}-{c['algo']}{c['variant']}"
+                         f"-n{c['n']}-e{c['elems']}-{c['dtype']}-{c['dist']}")
+def test_gpu_matches_reference_bits(case):
+    """Every reference algorithm on the GPU returns the reference's exact bits."""
+    from paper_2504_09014_b200 import collective
+    ins = gen_inputs(case["n"], case["elems"], case["dtype"], case["dist"], case["seed"])
+    outs = collective(case["kind"], ins, world(case["n"]), dtype=case["dtype"],
+                      algo=case["algo"], variant=case["variant"])
+    assert [len(o) for o in outs] == case["out_len"]
+    assert [_digest(o) for o in outs] == case["digests"]
+
+
+ALGOS = [("1pa", ""), ("1pa_hb", ""), ("2pa", "memory"), ("2pa", "ll"), ("switch_2pa", ""),
+         ("2pr", "")]
+_ORACLE_NAME = {"1pa_hb": "1pa"}
+
+
+@pytest.mark.parametrize("n", [2, 4, 8])
+@pytest.mark.parametrize("dtype", ["f32", "bf16", "f16", "i32"])
+@pytest.mark.parametrize("elems", [1, 3, 8, 1000, 4097, 65536 + 24, 262144])
+def test_allreduce_vs_oracle(n, dtype, elems):
+    from paper_2504_09014_b200 import collective
+    dist = {"f32": "wide", "i32": "int"}.get(dtype, "normal")
+    ins = gen_inputs(n, elems, dtype, dist, 100 * n + elems % 97)
+    for algo, var in ALGOS:
+        got = collective("allreduce", ins, world(n), dtype=dtype, algo=algo, variant=var)
+        want = oracle.allreduce(ins, _ORACLE_NAME.get(algo, algo), dtype)
+        for r in range(n):
+            assert np.array_equal(got[r].view(np.uint8), want[r].view(np.uint8)), (algo, var, r)
+
+
+@pytest.mark.parametrize("n", [2, 8])
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+@pytest.mark.parametrize("elems", [5, 4096, 100003])
+def test_reducescatter_allgather_vs_oracle(n, dtype, elems):
+    from paper_2504_09014_b200 import collective
+    dist = "wide" if dtype == "f32" else "normal"
+    ins = gen_inputs(n, elems, dtype, dist, 7 * n + elems % 13)
+    for algo in ("ring_rs", "rs_direct"):
+        got = collective("reducescatter", ins, world(n), dtype=dtype, algo=algo)
+        want = oracle.reducescatter(ins, "ring_rs" if algo == "ring_rs" else "direct", dtype)
+        for r in range(n):
+            assert np.array_equal(got[r].view(np.uint8), want[r].view(np.uint8)), (algo, r)
+    for algo in ("allpairs_ag", "ring_ag"):
+        got = collective("allgather", ins, world(n), dtype=dtype, algo=algo)
+        for g, wnt in zip(got, oracle.allgather(ins)):
+            assert np.array_equal(g.view(np.uint8), wnt.view(np.uint8)), algo
+
+
+def test_allgather_bf16_nan_patterns_bit_exact():
+    """C2: random 16-bit patterns including NaNs move bit-exactly."""
+    from paper_2504_09014_b200 import collective
+    rng = np.random.default_rng(5)
+    for n in (2, 4, 8):
+        for cnt in (1, 7, 64, 4096, 1 << 18):
+            shards = [rng.integers(0, 1 << 16, cnt, dtype=np.uint32).astype(np.uint16)
+                      for _ in range(n)]
+            got = collective("allgather", shards, world(n), dtype="bf16", algo="allpairs_ag")
+            cat = np.concatenate(shards)
+            for g in got:
+                assert np.array_equal(g, cat)
+
+
+def test_repeated_calls_reuse_scratch_and_semaphores():
+    """Epoch flags / monotonic semaphores across many back-to-back calls of
+    mixed algorithms and sizes (scratch is never zeroed between calls)."""
+    import torch
+    from paper_2504_09014_b200 import collectives as C
+    from paper_2504_09014_b200 import _lib
+    n = 8
+    w = world(n)
+    rng = np.random.default_rng(3)
+    for it in range(60):
+        elems = int(rng.choice([1, 33, 1024, 8192, 70000]))
+        algo = ["1pa", "2pa", "2pa_ll", "1pa_hb", "2pr"][it % 5]
+        vals = [torch.full((elems,), float(r + it), device=w.device(r)) for r in range(n)]
+        outs = [torch.empty_like(v) for v in vals]
+        C.run("allreduce", vals, outs, elems, "f32", _lib.ALGOS[algo], w)
+        w.synchronize()
+        want = float(sum(r + it for r in range(n)))
+        for o in outs:
+            assert torch.all(o == want).item(), (it, algo, elems)
+    w.check_device_error()
+
+
+def test_large_allreduce_property():
+    """Size-independent check at a large size: integer-valued bf16 sums are exact."""
+    import torch
+    from paper_2504_09014_b200 import collectives as C
+    from paper_2504_09014_b200 import _lib
+    n = 8
+    w = world(n)
+    elems = 64 << 20   # 128 MiB per rank
+    send = [torch.randint(-8, 8, (elems,), device=w.device(r), dtype=torch.int32)
+            .to(torch.bfloat16) for r in range(n)]
+    want = sum(s.float() for s in send)
+    for algo in ("2pa", "switch_2pa", "2pr"):
+        recv = [torch.empty_like(s) for s in send]
+        C.run("allreduce", send, recv, elems, "bf16", _lib.ALGOS[algo], w)
+        w.synchronize()
+        for o in recv:
+            assert torch.equal(o.float(), want), algo
+    w.check_device_error()
+
+
+def test_errors_map_to_reference_codes():
+    import torch
+    from paper_2504_09014_b200 import collective, collectives as C, _lib
+    from paper_2504_09014_b200.errors import BadAlignError, BadSizeError, NoAlgoError, ShapeError
+    w = world(2, ll_max_bytes=1 << 16)
+    big = [np.ones(1 << 15, np.float32) for _ in range(2)]
+    with pytest.raises(BadSizeError):
+        collective("allreduce", big, w, dtype="f32", algo="1pa")
+    with pytest.raises(NoAlgoError):
+        collective("allreduce", big, w, dtype="f32", algo="ring_ag")
+    with pytest.raises(ShapeError):
+        collective("allreduce", big[:1], w, dtype="f32")
+    t = [torch.zeros(64, device=w.device(r)) for r in range(2)]
+    with pytest.raises(BadAlignError):
+        C.run("allreduce", [x[1:] for x in t], [x[1:] for x in t], 8, "f32", _lib.ALGOS["2pa"], w)
