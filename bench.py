@@ -53,7 +53,7 @@ def load_peaks():
 class ClockSampler:
     """nvidia-smi style clock/throttle sampling during the timed region (NVML)."""
 
-    def __init__(self, dev=0, period=0.05):
+    def __init__(self, dev=0, period=0.002):
         self.dev, self.period = dev, period
         self.samples, self.reasons = [], set()
         self._stop = threading.Event()
@@ -160,36 +160,54 @@ def run_reference_arm(args):
 
 # ----------------------------------------------------------------------------- GPU arm
 
-def time_coll(world, kind, send, recv, count, dtype, algo, iters, warmup, flush=None):
-    """Device time per call (CUDA events on the launching stream), optional L2 flush."""
+def time_coll(world, kind, send, recv, count, dtype, algo, iters, warmup, flush=None, reps=3):
+    """Device time per call: `iters` calls captured in one CUDA graph (no host
+    launch overhead), replayed `reps` times, CUDA events on the replay stream.
+    With `flush`, each call is preceded by an L2 flush (memset of a buffer
+    larger than L2) and the time of a flush-only graph is subtracted."""
     import torch
     from paper_2504_09014_b200 import collectives as C
-    stream = torch.cuda.current_stream(world.device(0))
+    dev = world.device(0)
     for _ in range(warmup):
         C.run(kind, send, recv, count, dtype, algo, world)
     world.synchronize()
-    total = 0.0
-    if flush is None:
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(iters):
-            C.run(kind, send, recv, count, dtype, algo, world)
-        e1.record(stream)
-        e1.synchronize()
-        total = e0.elapsed_time(e1) / 1e3
-    else:
-        for _ in range(iters):
-            flush.zero_()
+
+    def capture(with_coll):
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream(dev)
+        s.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(g, stream=s):
+                for _ in range(iters):
+                    if flush is not None:
+                        flush.zero_()
+                    if with_coll:
+                        C.run(kind, send, recv, count, dtype, algo, world)
+        torch.cuda.synchronize(dev)
+        return g
+
+    def replay(g):
+        g.replay()
+        torch.cuda.synchronize(dev)
+        best = None
+        for _ in range(reps):
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            C.run(kind, send, recv, count, dtype, algo, world)
-            e1.record(stream)
+            st = torch.cuda.current_stream(dev)
+            e0.record(st)
+            g.replay()
+            e1.record(st)
             e1.synchronize()
-            total += e0.elapsed_time(e1) / 1e3
+            t = e0.elapsed_time(e1) / 1e3
+            best = t if best is None else min(best, t)
+        return best
+
+    g = capture(True)
+    t = replay(g)
+    if flush is not None:
+        t -= replay(capture(False))
     world.check_device_error()
-    return total / iters
+    return max(t, 0.0) / iters
 
 
 def run_gpu_arm(args):
@@ -264,11 +282,12 @@ def run_gpu_arm(args):
 
     # e2e: pinned host inputs -> public collective() -> pinned host outputs
     host_in = [s.cpu().pin_memory() for s in send]
+    host_out = [torch.empty_like(h).pin_memory() for h in host_in]
     e2e_times = []
     for it in range(max(2, min(args.steps, 5)) + 1):
         torch.cuda.synchronize(dev)
         t0 = time.perf_counter()
-        outs = C.collective("allreduce", host_in, w, algo="2pa")
+        outs = C.collective("allreduce", host_in, w, algo="2pa", outputs=host_out)
         torch.cuda.synchronize(dev)
         if it > 0:
             e2e_times.append(time.perf_counter() - t0)

@@ -138,8 +138,8 @@ CF_API cfStatus cfCommClearDeviceError(cfComm_t comm);
  *   ReduceScatter  recvcount = shard elements; send holds nranks*recvcount
  * In the one-process mode the buffers of every rank must be device memory
  * reachable from every rank's device (same device, or peer access).  In the
- * one-process-per-GPU mode the library stages through its symmetric scratch
- * unless the buffers came from cfMemAlloc. */
+ * one-process-per-GPU mode only the LL algorithms run in this version (they
+ * touch no peer user buffer). */
 CF_API cfStatus cfAllReduce(cfComm_t comm, const void* const* send, void* const* recv, size_t count,
                      cfDtype dtype, int algo, const cudaStream_t* streams);
 CF_API cfStatus cfAllGather(cfComm_t comm, const void* const* send, void* const* recv, size_t sendcount,
@@ -153,16 +153,19 @@ CF_API cfStatus cfReduceScatter(cfComm_t comm, const void* const* send, void* co
 CF_API cfStatus cfSelectAlgorithm(cfComm_t comm, int collective, size_t nbytes, cfDtype dtype, int* algo);
 
 /* Plan executor (cf/executor.py:73-379 Runtime; wire format cf/plan.py:1-36).
- * cfPlanLoad parses canonical plan JSON (dtype may be i32/f32/f16/bf16; the
- * execution dtype can also be overridden at execute time), validates it and
- * compiles it to a device op array; buffers are allocated per rank.
- * cfPlanExecute copies each local rank's input in, runs every (rank, tb)
- * program on the GPU, and copies the output buffer out. */
-CF_API cfStatus cfPlanLoad(cfComm_t comm, const char* json, size_t len, cfPlan_t* plan);
+ * cfPlanLoad parses canonical plan JSON (dtype i32/f32/f16/bf16, or forced by
+ * dtype_override >= 0), validates it, compiles it to a device op array and
+ * allocates the plan's buffers per rank.  cfPlanExecute runs every (rank, tb)
+ * program on the GPU with the caller's per-local-rank input/output buffers
+ * bound zero-copy as the plan's input/output buffers (sizes: the declared
+ * elems).  One-process communicators only in this version. */
+CF_API cfStatus cfPlanLoad(cfComm_t comm, const char* json, size_t len, int dtype_override, cfPlan_t* plan);
 CF_API cfStatus cfPlanExecute(cfPlan_t plan, const void* const* inputs, void* const* outputs,
-                       int dtype_override /* -1 = plan dtype */, const cudaStream_t* streams);
+                              const cudaStream_t* streams);
 CF_API cfStatus cfPlanInfo(cfPlan_t plan, size_t* in_elems, size_t* out_elems, int* dtype, int* n_programs,
-                    int* n_device_ops);
+                           int* n_device_ops);
+/* Device spin-timeout word of the plan's ranks (0 or CF_E_DEADLOCK).  Synchronizes. */
+CF_API cfStatus cfPlanLastDeviceError(cfPlan_t plan, int* code);
 CF_API cfStatus cfPlanDestroy(cfPlan_t plan);
 
 #ifdef __cplusplus

@@ -30,7 +30,7 @@ EXPORTS = (
     "cfCommGetHandle", "cfCommConnect", "cfCommDestroy", "cfCommNumRanks", "cfCommLocalRanks",
     "cfCommMulticastSupported", "cfCommLastDeviceError", "cfCommClearDeviceError", "cfAllReduce",
     "cfAllGather", "cfReduceScatter", "cfSelectAlgorithm", "cfPlanLoad", "cfPlanExecute",
-    "cfPlanInfo", "cfPlanDestroy",
+    "cfPlanInfo", "cfPlanLastDeviceError", "cfPlanDestroy",
 )
 
 
@@ -65,8 +65,9 @@ _PROTOS = {
     "cfAllGather": ([vp, P(vp), P(vp), sz, i32, i32, P(vp)], i32),
     "cfReduceScatter": ([vp, P(vp), P(vp), sz, i32, i32, P(vp)], i32),
     "cfSelectAlgorithm": ([vp, i32, sz, i32, P(i32)], i32),
-    "cfPlanLoad": ([vp, ctypes.c_char_p, sz, P(vp)], i32),
-    "cfPlanExecute": ([vp, P(vp), P(vp), i32, P(vp)], i32),
+    "cfPlanLoad": ([vp, ctypes.c_char_p, sz, i32, P(vp)], i32),
+    "cfPlanExecute": ([vp, P(vp), P(vp), P(vp)], i32),
+    "cfPlanLastDeviceError": ([vp, P(i32)], i32),
     "cfPlanInfo": ([vp, P(sz), P(sz), P(i32), P(i32), P(i32)], i32),
     "cfPlanDestroy": ([vp], i32),
 }

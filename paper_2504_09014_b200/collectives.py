@@ -183,11 +183,13 @@ def run(kind: str, send, recv, count: int, dtype: str, algo: int, world) -> None
 
 def collective(kind: str, inputs, world, selector: Selector | None = None, dtype: str = "i32",
                algo: str | None = None, variant: str = "", mode: str = "round-robin",
-               seed: int | None = None):
+               seed: int | None = None, outputs=None):
     """Select, run on the GPUs, return per-rank outputs (cf/collectives.py:532-573).
 
     `mode` and `seed` drive the reference's simulated scheduler; real GPUs
-    schedule themselves, so they are accepted and ignored.
+    schedule themselves, so they are accepted and ignored.  `outputs`
+    (extension): per-rank host torch tensors to receive the results when the
+    inputs are host torch tensors (e.g. pinned buffers reused across calls).
     """
     import torch
     if kind not in _COLL:
@@ -249,7 +251,8 @@ def collective(kind: str, inputs, world, selector: Selector | None = None, dtype
         outs = recv
     if host_tensors:
         pin = inputs[0].is_pinned()
-        host = [torch.empty(o.shape, dtype=o.dtype, pin_memory=pin) for o in outs]
+        host = outputs if outputs is not None else \
+            [torch.empty(o.shape, dtype=o.dtype, pin_memory=pin) for o in outs]
         for h, o in zip(host, outs):
             h.copy_(o, non_blocking=pin)
         world.synchronize()

@@ -83,8 +83,9 @@ __device__ __forceinline__ void store_vec(char* base, size_t v, uint4 val, size_
                                           size_t shift) {
   constexpr int V = 16 / sizeof(T);
   const size_t e0 = v * V;
-  if (e0 >= lo && e0 + V <= hi && (((e0 - shift) * sizeof(T)) & 15) == 0) {
-    st16(base + (e0 - shift) * sizeof(T), val);
+  char* p = base + (e0 - shift) * sizeof(T);
+  if (e0 >= lo && e0 + V <= hi && ((uintptr_t)p & 15) == 0) {
+    st16(p, val);
     return;
   }
   union { uint4 u; T t[V]; } x;

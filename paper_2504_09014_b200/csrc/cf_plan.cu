@@ -1,0 +1,898 @@
+// cf_plan.cu -- plan loading: validation, lowering of reference plan ops to
+// the device op array, fusion, sync classification, buffer binding, and the
+// cfPlan* entry points (replaces Runtime, cf/executor.py:73-178).
+//
+// Op semantics follow the reference executor exactly (cf/executor.py:237-379):
+//   put / put_with_signal : chan.src's src range -> chan.dst's dst range (+ signal)
+//   put_packets           : chan.src's payload -> LL packets in chan.dst's buffer
+//   read_packets          : own packets -> own dst (size taken from src)
+//   reduce  memory chan   : own dst += chan.dst's src      switch: own dst = sum_r src@r
+//   copy    memory chan   : own dst  = chan.dst's src      switch: src -> dst@r for all r
+//   reduce_put            : chan.dst's dst = own src + own src2
+//   flush                 : no-op (puts are executed by the issuing CTAs themselves)
+// Fusions (same results, fewer passes over memory):
+//   reduce chains on one destination -> one n-source reduce, plan order kept
+//   copy feeding such a chain         -> first source of the chain
+//   puts of the reduced range         -> extra destinations of the reduce
+//   (the SURVEY.md Appendix B pattern "pull-reduce then push").
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <set>
+#include "cf_plan.h"
+#include "cf_runtime.h"
+
+namespace cf {
+namespace plan {
+cfStatus parse(const char* text, size_t len, int dtype_override, Plan& P);
+const char* op_name(int k);
+const void* plan_kernel_for(int dtype);
+
+namespace {
+
+// host-side op under construction
+struct R {
+  int buf, rank;
+  long long off;     // elements
+  bool packet;       // packet-space range (2 bytes of packet per payload byte)
+};
+struct HOp {
+  int code = D_NOP;
+  int flags = 0;
+  long long size = 0;
+  uint32_t llflag = 0;
+  int chan = -1, peer = -1;
+  std::vector<int> members;   // device_barrier tbs
+  std::vector<R> src, dst;
+  int plan_index = -1;
+};
+
+struct Group {
+  int dev;
+  std::vector<int> progs;     // indices into compiled program list (sorted by rank, tb)
+  DevOp* d_ops = nullptr;
+  int32_t* d_meta = nullptr;  // begin | end | rank
+  char** d_bufptr = nullptr;
+  int32_t* d_zero = nullptr;
+  int nops = 0;
+};
+
+}  // namespace
+}  // namespace plan
+}  // namespace cf
+
+struct cfPlan {
+  cfComm* comm = nullptr;
+  cf::plan::Plan ir;
+  int dtype = 0, es = 4, K = 1, threads = 512;
+  int in_buf = -1, out_buf = -1;
+  bool input_private = false;
+  uint32_t flag_stride = 2;
+  std::vector<std::vector<cf::plan::DevOp>> prog_ops;  // per compiled program
+  std::vector<int> prog_rank, prog_tb;
+  std::vector<char*> heap;            // per rank plan heap
+  std::vector<size_t> buf_off;        // per buffer: offset in the heap (all ranks alike)
+  size_t state_off = 0, lanes_off = 0, bars_off = 0, heap_bytes = 0;
+  int nbars = 0;
+  std::vector<std::vector<int>> zero_bufs;  // per rank
+  std::vector<cf::plan::Group> groups;
+  int n_device_ops = 0;
+};
+
+namespace cf {
+namespace plan {
+namespace {
+
+struct Fail {
+  cfStatus s;
+  std::string m;
+};
+[[noreturn]] void bad(cfStatus s, const std::string& m) { throw Fail{s, m}; }
+
+std::string where(int pi, int oi) {
+  return "programs[" + std::to_string(pi) + "].ops[" + std::to_string(oi) + "]";
+}
+
+// ------------------------------------------------------------------ validation helpers
+
+void check_ref(const Plan& P, const Ref& r, int rank, bool packet, long long size, const std::string& w) {
+  const Buf& b = P.bufs[r.buf];
+  if (b.rank != -1 && b.rank != rank)
+    bad(CF_E_OOB, w + ": buffer '" + b.id + "' not present on rank " + std::to_string(rank));
+  const long long limit = packet ? b.elems / 2 : b.elems;
+  if (r.off < 0 || size < 0 || r.off + size > limit)
+    bad(CF_E_OOB, w + ": [" + std::to_string(r.off) + "," + std::to_string(r.off + size) + ") exceeds " +
+                      (packet ? "packet capacity " : "elems ") + std::to_string(limit) + " of buffer '" + b.id + "'");
+}
+
+void check_rank(const Plan& P, int r, const std::string& w) {
+  if (r < 0 || r >= P.nranks) bad(CF_E_OOB, w + ": rank " + std::to_string(r) + " out of range");
+}
+
+// ------------------------------------------------------------------ lowering to HOps
+
+std::vector<HOp> lower_program(const Plan& P, int pi, int es) {
+  const Prog& G = P.progs[pi];
+  std::vector<HOp> out;
+  const int rank = G.rank;
+  for (size_t oi = 0; oi < G.ops.size(); oi++) {
+    const Op& op = G.ops[oi];
+    const std::string w = where(pi, (int)oi);
+    const Chan* ch = op.chan >= 0 ? &P.chans[op.chan] : nullptr;
+    auto need_chan = [&](bool allow_switch) {
+      if (!ch) bad(CF_E_SHAPE, w + ": " + op_name(op.kind) + " requires a channel");
+      if (!allow_switch && ch->type == C_SWITCH)
+        bad(CF_E_PROTOCOL, w + ": " + op_name(op.kind) + " needs a port or memory channel");
+      if (ch->type != C_SWITCH) { check_rank(P, ch->src, w); check_rank(P, ch->dst, w); }
+      else for (int r : ch->ranks) check_rank(P, r, w);
+    };
+    auto need = [&](bool have, const char* what) {
+      if (!have) bad(CF_E_SHAPE, w + ": " + op_name(op.kind) + " needs " + what);
+    };
+    HOp h;
+    h.plan_index = (int)oi;
+    switch (op.kind) {
+      case P_PUT:
+      case P_PUT_WITH_SIGNAL: {
+        need_chan(false);
+        need(op.has_src && op.has_dst, "src and dst");
+        check_ref(P, op.src, ch->src, false, op.src.size, w);
+        check_ref(P, op.dst, ch->dst, false, op.src.size, w);
+        h.code = D_COPY;
+        h.size = op.src.size;
+        h.src = {{op.src.buf, ch->src, op.src.off, false}};
+        h.dst = {{op.dst.buf, ch->dst, op.dst.off, false}};
+        if (h.size > 0) out.push_back(h);
+        if (op.kind == P_PUT_WITH_SIGNAL) {
+          HOp s;
+          s.code = D_SIGNAL;
+          s.chan = op.chan;
+          s.peer = ch->dst;
+          s.plan_index = (int)oi;
+          out.push_back(s);
+        }
+        break;
+      }
+      case P_SIGNAL:
+        need_chan(false);
+        h.code = D_SIGNAL;
+        h.chan = op.chan;
+        h.peer = ch->dst;
+        out.push_back(h);
+        break;
+      case P_WAIT:
+        need_chan(false);
+        h.code = D_WAIT;
+        h.chan = op.chan;
+        out.push_back(h);
+        break;
+      case P_FLUSH:
+        need_chan(true);
+        break;
+      case P_PUT_PACKETS: {
+        need_chan(false);
+        need(op.has_src && op.has_dst, "src and dst");
+        if (!op.has_flag || op.flag == 0) bad(CF_E_ZERO_FLAG, w + ": LL flag must be nonzero");
+        if (op.flag < 0 || op.flag > 0x7fffffff) bad(CF_E_SHAPE, w + ": LL flag out of range");
+        if ((op.src.size * es) % 4) bad(CF_E_BAD_ALIGN, w + ": LL payload must be a multiple of 4 bytes");
+        check_ref(P, op.src, ch->src, false, op.src.size, w);
+        check_ref(P, op.dst, ch->dst, true, op.src.size, w);
+        h.code = D_PUT_PACKETS;
+        h.size = op.src.size;
+        h.llflag = (uint32_t)op.flag;
+        h.src = {{op.src.buf, ch->src, op.src.off, false}};
+        h.dst = {{op.dst.buf, ch->dst, op.dst.off, true}};
+        if (h.size > 0) out.push_back(h);
+        break;
+      }
+      case P_READ_PACKETS: {
+        need(op.has_src && op.has_dst, "src and dst");
+        if (!op.has_flag || op.flag == 0) bad(CF_E_ZERO_FLAG, w + ": LL flag must be nonzero");
+        if (op.flag < 0 || op.flag > 0x7fffffff) bad(CF_E_SHAPE, w + ": LL flag out of range");
+        if ((op.src.size * es) % 4) bad(CF_E_BAD_ALIGN, w + ": LL payload must be a multiple of 4 bytes");
+        check_ref(P, op.src, rank, true, op.src.size, w);
+        check_ref(P, op.dst, rank, false, op.src.size, w);
+        h.code = D_READ_PACKETS;
+        h.size = op.src.size;
+        h.llflag = (uint32_t)op.flag;
+        h.src = {{op.src.buf, rank, op.src.off, true}};
+        h.dst = {{op.dst.buf, rank, op.dst.off, false}};
+        if (h.size > 0) out.push_back(h);
+        break;
+      }
+      case P_REDUCE: {
+        need(op.has_src && op.has_dst, "src and dst");
+        h.code = D_MULTI;
+        h.size = op.src.size;
+        check_ref(P, op.dst, rank, false, h.size, w);
+        if (ch && ch->type == C_SWITCH) {
+          need_chan(true);
+          if ((int)ch->ranks.size() > kMaxSrc) bad(CF_E_SHAPE, w + ": switch channel wider than 16 ranks");
+          h.flags = F_ZERO;
+          for (int r : ch->ranks) {
+            check_ref(P, op.src, r, false, h.size, w);
+            h.src.push_back({op.src.buf, r, op.src.off, false});
+          }
+        } else {
+          const int peer = (ch && ch->type == C_MEMORY) ? ch->dst : rank;
+          if (ch) need_chan(false);
+          check_ref(P, op.src, peer, false, h.size, w);
+          h.flags = F_ROUND_EACH;
+          h.src = {{op.dst.buf, rank, op.dst.off, false}, {op.src.buf, peer, op.src.off, false}};
+        }
+        h.dst = {{op.dst.buf, rank, op.dst.off, false}};
+        if (h.size > 0) out.push_back(h);
+        break;
+      }
+      case P_COPY: {
+        need(op.has_src && op.has_dst, "src and dst");
+        h.code = D_COPY;
+        h.size = op.src.size;
+        if (ch && ch->type == C_SWITCH) {
+          need_chan(true);
+          if ((int)ch->ranks.size() > kMaxDst) bad(CF_E_SHAPE, w + ": switch broadcast wider than 8 ranks");
+          check_ref(P, op.src, rank, false, h.size, w);
+          h.src = {{op.src.buf, rank, op.src.off, false}};
+          for (int r : ch->ranks) {
+            check_ref(P, op.dst, r, false, h.size, w);
+            h.dst.push_back({op.dst.buf, r, op.dst.off, false});
+          }
+        } else {
+          const int peer = (ch && ch->type == C_MEMORY) ? ch->dst : rank;
+          if (ch) need_chan(false);
+          check_ref(P, op.src, peer, false, h.size, w);
+          check_ref(P, op.dst, rank, false, h.size, w);
+          h.src = {{op.src.buf, peer, op.src.off, false}};
+          h.dst = {{op.dst.buf, rank, op.dst.off, false}};
+        }
+        if (h.size > 0) out.push_back(h);
+        break;
+      }
+      case P_REDUCE_PUT: {
+        need_chan(false);
+        need(op.has_src && op.has_dst && op.has_src2, "src, src2 and dst");
+        h.code = D_MULTI;
+        h.size = op.src.size;
+        h.flags = F_ROUND_EACH;
+        check_ref(P, op.src, rank, false, h.size, w);
+        check_ref(P, op.src2, rank, false, h.size, w);
+        check_ref(P, op.dst, ch->dst, false, h.size, w);
+        h.src = {{op.src.buf, rank, op.src.off, false}, {op.src2.buf, rank, op.src2.off, false}};
+        h.dst = {{op.dst.buf, ch->dst, op.dst.off, false}};
+        if (h.size > 0) out.push_back(h);
+        break;
+      }
+      case P_TB_SYNC:
+        h.code = D_SYNC_CTA;
+        out.push_back(h);
+        break;
+      case P_DEVICE_BARRIER:
+        h.code = D_DEV_BARRIER;
+        h.members = op.group;
+        out.push_back(h);
+        break;
+      default:
+        bad(CF_E_SYNTAX, w + ": unknown op");
+    }
+  }
+  return out;
+}
+
+// ------------------------------------------------------------------ fusion
+
+bool same_ref(const R& a, const R& b) {
+  return a.buf == b.buf && a.rank == b.rank && a.off == b.off && a.packet == b.packet;
+}
+
+// byte interval of a ref
+void span(const R& r, long long size, int es, long long& lo, long long& hi) {
+  const int mul = r.packet ? 2 : 1;
+  lo = r.off * es * mul;
+  hi = (r.off + size) * es * mul;
+}
+
+bool overlaps(const R& a, long long asz, const R& b, long long bsz, int es) {
+  if (a.buf != b.buf || a.rank != b.rank) return false;
+  long long alo, ahi, blo, bhi;
+  span(a, asz, es, alo, ahi);
+  span(b, bsz, es, blo, bhi);
+  return alo < bhi && blo < ahi;
+}
+
+bool is_data(const HOp& h) {
+  return h.code == D_MULTI || h.code == D_COPY || h.code == D_PUT_PACKETS || h.code == D_READ_PACKETS;
+}
+
+bool touches(const HOp& h, const R& r, long long size, int es, bool writes_only) {
+  if (!is_data(h)) return false;
+  for (auto& d : h.dst)
+    if (overlaps(d, h.size, r, size, es)) return true;
+  if (!writes_only)
+    for (auto& s : h.src)
+      if (overlaps(s, h.size, r, size, es)) return true;
+  return false;
+}
+
+// accumulate form: dst[0] += ...  (srcs[0] is the destination itself)
+bool accumulate_form(const HOp& h) {
+  return h.code == D_MULTI && h.dst.size() == 1 && !(h.flags & F_ZERO) && !h.src.empty() &&
+         same_ref(h.src[0], h.dst[0]);
+}
+
+void fuse(std::vector<HOp>& ops, int es) {
+  bool changed = true;
+  while (changed) {
+    changed = false;
+    for (size_t i = 0; i < ops.size() && !changed; i++) {
+      HOp& a = ops[i];
+      // (1) reduce chain: A(dst D, D + ...) [sync]* B(dst D, D + ...)
+      if (accumulate_form(a) || (a.code == D_MULTI && a.dst.size() == 1 && !(a.flags & F_ZERO))) {
+        size_t k = i + 1;
+        while (k < ops.size() && ops[k].code == D_SYNC_CTA) k++;
+        if (k < ops.size() && accumulate_form(ops[k]) && same_ref(ops[k].dst[0], a.dst[0]) &&
+            ops[k].size == a.size && ops[k].flags == a.flags &&
+            a.src.size() + ops[k].src.size() - 1 <= (size_t)kMaxSrc) {
+          for (size_t s = 1; s < ops[k].src.size(); s++) a.src.push_back(ops[k].src[s]);
+          ops.erase(ops.begin() + i + 1, ops.begin() + k + 1);
+          changed = true;
+          break;
+        }
+      }
+      // (2) copy S0 -> D feeding a later accumulate chain on D
+      if (a.code == D_COPY && a.dst.size() == 1 && a.src.size() == 1) {
+        for (size_t k = i + 1; k < ops.size(); k++) {
+          HOp& b = ops[k];
+          if (accumulate_form(b) && same_ref(b.dst[0], a.dst[0]) && b.size == a.size) {
+            b.src[0] = a.src[0];
+            ops.erase(ops.begin() + i);
+            changed = true;
+            break;
+          }
+          if (b.code == D_WAIT || b.code == D_DEV_BARRIER || b.code == D_SYNC_GROUP) break;
+          if (touches(b, a.dst[0], a.size, es, false) || touches(b, a.src[0], a.size, es, true)) break;
+        }
+        if (changed) break;
+      }
+      // (3) puts of the reduced range become extra destinations of the reduce
+      if (a.code == D_MULTI && a.dst.size() < (size_t)kMaxDst) {
+        for (size_t k = i + 1; k < ops.size(); k++) {
+          HOp& b = ops[k];
+          if (b.code == D_SYNC_CTA || b.code == D_SIGNAL) continue;
+          if (b.code == D_COPY && b.src.size() == 1 && b.dst.size() == 1 && same_ref(b.src[0], a.dst[0]) &&
+              b.size == a.size) {
+            bool clash = false;
+            for (auto& d : a.dst) clash |= overlaps(d, a.size, b.dst[0], b.size, es);
+            for (auto& s : a.src) clash |= overlaps(s, a.size, b.dst[0], b.size, es);
+            if (!clash) {
+              a.dst.push_back(b.dst[0]);
+              ops.erase(ops.begin() + k);
+              changed = true;
+            }
+          }
+          break;
+        }
+        if (changed) break;
+      }
+    }
+  }
+  // collapse runs of syncs
+  std::vector<HOp> out;
+  for (auto& h : ops) {
+    if (h.code == D_SYNC_CTA && !out.empty() && out.back().code == D_SYNC_CTA) continue;
+    out.push_back(h);
+  }
+  ops.swap(out);
+}
+
+// ------------------------------------------------------------------ sync classification
+
+// Two data ops touch the same bytes in the same per-element layout, so one
+// CTA slice covers the same elements in both.
+bool aligned_pair(const HOp& a, const HOp& b, int es) {
+  auto refs = [](const HOp& h) {
+    std::vector<std::pair<R, bool>> v;
+    for (auto& s : h.src) v.push_back({s, false});
+    for (auto& d : h.dst) v.push_back({d, true});
+    return v;
+  };
+  for (auto& ra : refs(a))
+    for (auto& rb : refs(b)) {
+      if (!ra.second && !rb.second) continue;  // read/read
+      if (!overlaps(ra.first, a.size, rb.first, b.size, es)) continue;
+      if (!(a.size == b.size && ra.first.off == rb.first.off && ra.first.packet == rb.first.packet))
+        return false;
+    }
+  return true;
+}
+
+void classify_syncs(std::vector<HOp>& ops, int K, int es) {
+  if (K == 1) return;
+  int last_group = -1;
+  for (int s = 0; s < (int)ops.size(); s++) {
+    if (ops[s].code == D_WAIT || ops[s].code == D_DEV_BARRIER) last_group = s;
+    if (ops[s].code != D_SYNC_CTA) continue;
+    bool group = false;
+    for (int i = last_group + 1; i < s && !group; i++) {
+      if (!is_data(ops[i])) continue;
+      for (int k = s + 1; k < (int)ops.size() && !group; k++)
+        if (is_data(ops[k]) && !aligned_pair(ops[i], ops[k], es)) group = true;
+    }
+    if (group) {
+      ops[s].code = D_SYNC_GROUP;
+      last_group = s;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ zero / private analysis
+
+struct Interval {
+  long long lo, hi;
+};
+bool covered(const std::vector<Interval>& iv, long long lo, long long hi) {
+  // iv sorted/merged on insert
+  for (auto& x : iv)
+    if (x.lo <= lo && hi <= x.hi) return true;
+  return false;
+}
+void add_interval(std::vector<Interval>& iv, long long lo, long long hi) {
+  iv.push_back({lo, hi});
+  std::sort(iv.begin(), iv.end(), [](const Interval& a, const Interval& b) { return a.lo < b.lo; });
+  std::vector<Interval> m;
+  for (auto& x : iv) {
+    if (!m.empty() && x.lo <= m.back().hi) m.back().hi = std::max(m.back().hi, x.hi);
+    else m.push_back(x);
+  }
+  iv.swap(m);
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ load
+
+cfStatus load(cfComm* c, const char* json, size_t len, int dtype_override, cfPlan** out) {
+  std::unique_ptr<cfPlan> pl(new cfPlan());
+  pl->comm = c;
+  CF_TRY(parse(json, len, dtype_override, pl->ir));
+  Plan& P = pl->ir;
+  try {
+    if (!P.lowered) bad(CF_E_SHAPE, "cannot execute a pre-lowering document; lower it first");
+    if (P.nranks != c->nranks)
+      bad(CF_E_RANK_MISMATCH, "plan wants " + std::to_string(P.nranks) + " ranks, world has " +
+                                  std::to_string(c->nranks));
+    if (c->multiprocess) bad(CF_E_TOPOLOGY, "plan execution needs a one-process world in this build");
+    if ((int)P.bufs.size() > kMaxBufs) bad(CF_E_SHAPE, "plans are limited to 16 buffers");
+    for (size_t b = 0; b < P.bufs.size(); b++) {
+      if (P.bufs[b].elems <= 0) bad(CF_E_BAD_SIZE, "buffer '" + P.bufs[b].id + "' has non-positive elems");
+      if (P.bufs[b].rank < -1 || P.bufs[b].rank >= P.nranks) bad(CF_E_OOB, "buffer '" + P.bufs[b].id + "' rank out of range");
+      if (P.bufs[b].kind == B_INPUT) { if (pl->in_buf >= 0) bad(CF_E_SHAPE, "plan must declare exactly one input buffer, found 2"); pl->in_buf = (int)b; }
+      if (P.bufs[b].kind == B_OUTPUT) { if (pl->out_buf >= 0) bad(CF_E_SHAPE, "plan must declare exactly one output buffer, found 2"); pl->out_buf = (int)b; }
+    }
+    if (pl->in_buf < 0) bad(CF_E_SHAPE, "plan must declare exactly one input buffer, found 0");
+    if (pl->out_buf < 0) bad(CF_E_SHAPE, "plan must declare exactly one output buffer, found 0");
+    if (P.bufs[pl->in_buf].rank != -1 || P.bufs[pl->out_buf].rank != -1)
+      bad(CF_E_SHAPE, "input and output buffers must exist on every rank");
+    for (auto& g : P.progs) check_rank(P, g.rank, "program");
+    for (size_t i = 0; i < P.progs.size(); i++)
+      for (size_t k = i + 1; k < P.progs.size(); k++)
+        if (P.progs[i].rank == P.progs[k].rank && P.progs[i].tb == P.progs[k].tb)
+          bad(CF_E_SHAPE, "duplicate program for rank " + std::to_string(P.progs[i].rank) + " tb " +
+                              std::to_string(P.progs[i].tb));
+  } catch (const Fail& f) {
+    return fail(f.s, "%s", f.m.c_str());
+  }
+  pl->dtype = P.dtype;
+  pl->es = dtype_size(P.dtype);
+  const int es = pl->es, n = P.nranks;
+
+  // programs sorted by (rank, tb); ranks without a program get an empty one so
+  // the call-bracketing rank barrier always has a participant.
+  std::vector<int> order(P.progs.size());
+  for (size_t i = 0; i < order.size(); i++) order[i] = (int)i;
+  std::sort(order.begin(), order.end(), [&](int a, int b) {
+    return std::make_pair(P.progs[a].rank, P.progs[a].tb) < std::make_pair(P.progs[b].rank, P.progs[b].tb);
+  });
+  std::vector<std::vector<HOp>> hops;
+  std::vector<int> prank, ptb;
+  try {
+    int next = 0;
+    for (int r = 0; r < n; r++) {
+      bool any = false;
+      while (next < (int)order.size() && P.progs[order[next]].rank == r) {
+        hops.push_back(lower_program(P, order[next], es));
+        prank.push_back(r);
+        ptb.push_back(P.progs[order[next]].tb);
+        next++;
+        any = true;
+      }
+      if (!any) { hops.emplace_back(); prank.push_back(r); ptb.push_back(1 << 30); }
+    }
+  } catch (const Fail& f) {
+    return fail(f.s, "%s", f.m.c_str());
+  }
+  for (auto& h : hops) fuse(h, es);
+
+  // CTAs per program: enough threads for the largest data op, all programs
+  // of a device co-resident.
+  long long max_bytes = 0;
+  for (auto& h : hops)
+    for (auto& o : h)
+      if (is_data(o)) max_bytes = std::max(max_bytes, o.size * es);
+  const void* kernel = plan_kernel_for(pl->dtype);
+  int cap = INT32_MAX, progs_per_dev_max = 1;
+  {
+    std::map<int, int> per_dev;
+    for (int r : prank) per_dev[c->local[r].dev]++;
+    for (auto& kv : per_dev) {
+      progs_per_dev_max = std::max(progs_per_dev_max, kv.second);
+      cap = std::min(cap, occupancy(c, kernel, kv.first, pl->threads) * c->sm_count[kv.first] / kv.second);
+    }
+  }
+  if (cap < 1) return fail(CF_E_CONFIG, "plan has more programs per device than co-resident CTAs");
+  const long long per_cta = (long long)pl->threads * 16 * 4;
+  pl->K = (int)std::max(1LL, std::min<long long>({(max_bytes + per_cta - 1) / per_cta, (long long)cap, 32LL}));
+  const int K = pl->K;
+
+  try {
+    for (auto& h : hops) classify_syncs(h, K, es);
+  } catch (const Fail& f) {
+    return fail(f.s, "%s", f.m.c_str());
+  }
+
+  // signals per call per channel; waits restricted to one program per channel
+  std::vector<long long> sig(P.chans.size(), 0);
+  std::vector<int> waiter(P.chans.size(), -1);
+  long long max_flag = 1;
+  for (size_t p = 0; p < hops.size(); p++)
+    for (auto& o : hops[p]) {
+      if (o.code == D_SIGNAL) sig[o.chan]++;
+      if (o.code == D_WAIT) {
+        if (waiter[o.chan] >= 0 && waiter[o.chan] != (int)p)
+          return fail(CF_E_PROTOCOL, "channel '%s' is waited on by more than one thread block",
+                      P.chans[o.chan].id.c_str());
+        waiter[o.chan] = (int)p;
+      }
+      if (o.code == D_PUT_PACKETS || o.code == D_READ_PACKETS) max_flag = std::max<long long>(max_flag, o.llflag);
+    }
+  pl->flag_stride = (uint32_t)(max_flag + 1);
+
+  // barrier counters: one per program for group syncs, one per device_barrier key
+  int nbar = 0;
+  std::map<std::pair<int, std::vector<int>>, int> bar_key;
+  std::map<std::pair<int, std::vector<int>>, std::map<int, int>> bar_count;  // key -> program -> count
+  std::vector<int> gbar(hops.size(), -1);
+  for (size_t p = 0; p < hops.size(); p++) {
+    int gsyncs = 0, m = 0;
+    for (auto& o : hops[p]) gsyncs += o.code == D_SYNC_GROUP;
+    if (gsyncs) gbar[p] = nbar++;
+    std::map<std::pair<int, std::vector<int>>, int> occ;
+    for (auto& o : hops[p]) {
+      if (o.code == D_SYNC_GROUP) {
+        o.chan = gbar[p];
+        o.peer = ++m;                      // m
+        o.members.assign(1, gsyncs);       // per_call stash
+      } else if (o.code == D_DEV_BARRIER) {
+        std::vector<int> mem = o.members;
+        if (mem.empty())
+          for (size_t q = 0; q < hops.size(); q++)
+            if (prank[q] == prank[p] && ptb[q] != (1 << 30)) mem.push_back(ptb[q]);
+        std::sort(mem.begin(), mem.end());
+        auto key = std::make_pair(prank[p], mem);
+        if (!bar_key.count(key)) bar_key[key] = nbar++;
+        o.chan = bar_key[key];
+        o.peer = ++occ[key];
+        bar_count[key][(int)p] = o.peer;
+        o.members = mem;
+      }
+    }
+  }
+  for (auto& kv : bar_count) {
+    const auto& mem = kv.first.second;
+    int per_call = -1;
+    for (auto& pc : kv.second) {
+      if (per_call >= 0 && pc.second != per_call)
+        return fail(CF_E_PROTOCOL, "device_barrier members disagree on the barrier count");
+      per_call = pc.second;
+    }
+    for (int tb : mem) {
+      bool found = false;
+      for (size_t q = 0; q < hops.size(); q++) found |= prank[q] == kv.first.first && ptb[q] == tb;
+      if (!found) return fail(CF_E_OOB, "device_barrier names tb %d, which has no program", tb);
+    }
+    if ((int)kv.second.size() != (int)mem.size())
+      return fail(CF_E_PROTOCOL, "device_barrier member without a matching barrier");
+  }
+  pl->nbars = nbar;
+
+  // zeroing and private-input analysis
+  std::vector<std::set<int>> zero(n);
+  for (size_t p = 0; p < hops.size(); p++) {
+    std::map<std::pair<int, int>, std::vector<Interval>> written;
+    for (auto& o : hops[p]) {
+      if (!is_data(o)) continue;
+      for (auto& s : o.src) {
+        if (s.packet || s.buf == pl->in_buf) continue;
+        long long lo, hi;
+        span(s, o.size, es, lo, hi);
+        auto& iv = written[{s.buf, s.rank}];
+        if (s.rank != prank[p] || !covered(iv, lo, hi)) zero[s.rank].insert(s.buf);
+      }
+      for (auto& d : o.dst) {
+        if (d.buf == pl->in_buf) pl->input_private = true;
+        if (d.packet) continue;
+        long long lo, hi;
+        span(d, o.size, es, lo, hi);
+        add_interval(written[{d.buf, d.rank}], lo, hi);
+      }
+    }
+  }
+  pl->zero_bufs.assign(n, {});
+  for (int r = 0; r < n; r++)
+    for (int b : zero[r]) {
+      if (P.bufs[b].rank != -1 && P.bufs[b].rank != r) continue;
+      if ((int)pl->zero_bufs[r].size() < kMaxZero) pl->zero_bufs[r].push_back(b);
+    }
+
+  // encode device ops
+  for (size_t p = 0; p < hops.size(); p++) {
+    std::vector<DevOp> dv;
+    std::map<int, int> wm;
+    for (auto& o : hops[p]) {
+      DevOp d;
+      memset(&d, 0, sizeof(d));
+      d.code = (uint8_t)o.code;
+      d.size = (uint64_t)o.size;
+      d.llflag = o.llflag;
+      d.flags = (uint8_t)(o.flags & (F_ZERO | F_ROUND_EACH));
+      d.nsrc = (uint8_t)o.src.size();
+      d.ndst = (uint8_t)o.dst.size();
+      bool vec = true;
+      for (size_t k = 0; k < o.src.size(); k++) {
+        d.src[k] = {o.src[k].buf, o.src[k].rank, (uint64_t)(o.src[k].off * es * (o.src[k].packet ? 2 : 1))};
+        vec &= (d.src[k].off % 16) == 0;
+      }
+      for (size_t k = 0; k < o.dst.size(); k++) {
+        d.dst[k] = {o.dst[k].buf, o.dst[k].rank, (uint64_t)(o.dst[k].off * es * (o.dst[k].packet ? 2 : 1))};
+        vec &= (d.dst[k].off % 16) == 0;
+      }
+      if (vec) d.flags |= F_VEC;
+      if (o.code == D_PUT_PACKETS || o.code == D_READ_PACKETS) {
+        const R& pay = o.code == D_PUT_PACKETS ? o.src[0] : o.dst[0];
+        if ((pay.off * es) % 8 == 0 && (o.size * es) % 8 == 0) d.flags |= F_LL16;
+      }
+      switch (o.code) {
+        case D_SIGNAL:
+          d.id = o.chan;
+          d.peer = o.peer;
+          break;
+        case D_WAIT:
+          d.id = o.chan;
+          d.m = (uint64_t)(++wm[o.chan]);
+          d.per_call = (uint64_t)sig[o.chan];
+          break;
+        case D_SYNC_GROUP:
+          d.id = o.chan;
+          d.m = (uint64_t)o.peer;
+          d.per_call = (uint64_t)o.members[0];
+          d.members = (uint64_t)K;
+          break;
+        case D_DEV_BARRIER:
+          d.id = o.chan;
+          d.m = (uint64_t)o.peer;
+          d.per_call = (uint64_t)bar_count[{prank[p], o.members}][(int)p];
+          d.members = (uint64_t)(o.members.size() * K);
+          break;
+        default:
+          break;
+      }
+      dv.push_back(d);
+    }
+    pl->n_device_ops += (int)dv.size();
+    pl->prog_ops.push_back(dv);
+  }
+  pl->prog_rank = prank;
+  pl->prog_tb = ptb;
+
+  // per-rank plan heap: [PlanState | lanes | bars | buffers]
+  pl->state_off = 0;
+  pl->lanes_off = round_up(sizeof(PlanState), 256);
+  pl->bars_off = round_up(pl->lanes_off + P.chans.size() * K * sizeof(uint64_t) + 8, 256);
+  size_t off = round_up(pl->bars_off + (size_t)(nbar + 1) * sizeof(uint64_t), 256);
+  pl->buf_off.assign(P.bufs.size(), 0);
+  for (size_t b = 0; b < P.bufs.size(); b++) {
+    if ((int)b == pl->out_buf || ((int)b == pl->in_buf && !pl->input_private)) continue;
+    pl->buf_off[b] = off;
+    off += round_up((size_t)P.bufs[b].elems * es, 256);
+  }
+  pl->heap_bytes = round_up(off, 4096);
+  int prev_dev = -1;
+  cudaGetDevice(&prev_dev);
+  pl->heap.assign(n, nullptr);
+  for (int r = 0; r < n; r++) {
+    if (cudaSetDevice(c->local[r].dev) != cudaSuccess || cudaMalloc((void**)&pl->heap[r], pl->heap_bytes) != cudaSuccess ||
+        cudaMemset(pl->heap[r], 0, pl->heap_bytes) != cudaSuccess) {
+      cudaSetDevice(prev_dev);
+      cfPlanDestroy(pl.release());
+      return fail(CF_E_CUDA, "plan heap allocation failed");
+    }
+    PlanState st;
+    memset(&st, 0, sizeof(st));
+    st.base.timeout_ns = c->cfg.spin_timeout_ns;
+    cudaMemcpy(pl->heap[r] + pl->state_off, &st, sizeof(st), cudaMemcpyHostToDevice);
+  }
+  // device tables per device group
+  for (size_t gi = 0; gi < c->groups.size(); gi++) {
+    Group G;
+    G.dev = c->local[c->groups[gi][0]].dev;
+    std::set<int> ranks;
+    for (int li : c->groups[gi]) ranks.insert(c->local[li].rank);
+    std::vector<DevOp> all;
+    std::vector<int32_t> meta;
+    std::vector<int32_t> beg, end, rk;
+    for (size_t p = 0; p < pl->prog_ops.size(); p++) {
+      if (!ranks.count(prank[p])) continue;
+      G.progs.push_back((int)p);
+      beg.push_back((int32_t)all.size());
+      all.insert(all.end(), pl->prog_ops[p].begin(), pl->prog_ops[p].end());
+      end.push_back((int32_t)all.size());
+      rk.push_back(prank[p]);
+    }
+    meta = beg;
+    meta.insert(meta.end(), end.begin(), end.end());
+    meta.insert(meta.end(), rk.begin(), rk.end());
+    std::vector<char*> bp((size_t)P.bufs.size() * n, nullptr);
+    for (size_t b = 0; b < P.bufs.size(); b++)
+      for (int r = 0; r < n; r++) bp[b * n + r] = pl->heap[r] + pl->buf_off[b];
+    std::vector<int32_t> zl((size_t)n * kMaxZero, -1);
+    for (int r = 0; r < n; r++)
+      for (size_t z = 0; z < pl->zero_bufs[r].size(); z++) zl[(size_t)r * kMaxZero + z] = pl->zero_bufs[r][z];
+    cudaSetDevice(G.dev);
+    bool ok = cudaMalloc((void**)&G.d_ops, std::max<size_t>(1, all.size()) * sizeof(DevOp)) == cudaSuccess &&
+              cudaMalloc((void**)&G.d_meta, std::max<size_t>(1, meta.size()) * sizeof(int32_t)) == cudaSuccess &&
+              cudaMalloc((void**)&G.d_bufptr, bp.size() * sizeof(char*) + 8) == cudaSuccess &&
+              cudaMalloc((void**)&G.d_zero, zl.size() * sizeof(int32_t)) == cudaSuccess;
+    if (ok && !all.empty()) ok = cudaMemcpy(G.d_ops, all.data(), all.size() * sizeof(DevOp), cudaMemcpyHostToDevice) == cudaSuccess;
+    if (ok && !meta.empty()) ok = cudaMemcpy(G.d_meta, meta.data(), meta.size() * sizeof(int32_t), cudaMemcpyHostToDevice) == cudaSuccess;
+    if (ok) ok = cudaMemcpy(G.d_bufptr, bp.data(), bp.size() * sizeof(char*), cudaMemcpyHostToDevice) == cudaSuccess;
+    if (ok) ok = cudaMemcpy(G.d_zero, zl.data(), zl.size() * sizeof(int32_t), cudaMemcpyHostToDevice) == cudaSuccess;
+    G.nops = (int)all.size();
+    pl->groups.push_back(G);
+    if (!ok) {
+      cudaSetDevice(prev_dev);
+      cfPlanDestroy(pl.release());
+      return fail(CF_E_CUDA, "plan table upload failed");
+    }
+  }
+  cudaSetDevice(prev_dev);
+  *out = pl.release();
+  return CF_OK;
+}
+
+}  // namespace plan
+}  // namespace cf
+
+using namespace cf;
+using namespace cf::plan;
+
+extern "C" cfStatus cfPlanLoad(cfComm_t comm, const char* json, size_t len, int dtype_override, cfPlan_t* plan) {
+  if (!comm || !json || !plan) return fail(CF_E_CONFIG, "null argument");
+  if (!comm->connected) return fail(CF_E_CONFIG, "communicator not connected");
+  if (dtype_override < -1 || dtype_override > 3) return fail(CF_E_SHAPE, "unknown dtype %d", dtype_override);
+  return cf::plan::load(comm, json, len, dtype_override, plan);
+}
+
+extern "C" cfStatus cfPlanExecute(cfPlan_t pl, const void* const* inputs, void* const* outputs,
+                                  const cudaStream_t* streams) {
+  if (!pl || !inputs || !outputs || !streams) return fail(CF_E_CONFIG, "null argument");
+  cfComm* c = pl->comm;
+  const int n = pl->ir.nranks;
+  for (size_t li = 0; li < c->local.size(); li++) {
+    if (!inputs[li] || !outputs[li]) return fail(CF_E_OOB, "local rank %zu: null buffer", li);
+    if (((uintptr_t)inputs[li] | (uintptr_t)outputs[li]) & 15)
+      return fail(CF_E_BAD_ALIGN, "local rank %zu: buffers must be 16-byte aligned", li);
+  }
+  int prev = -1;
+  cudaGetDevice(&prev);
+  const void* kernel = plan_kernel_for(pl->dtype);
+  for (size_t gi = 0; gi < pl->groups.size(); gi++) {
+    Group& G = pl->groups[gi];
+    PlanArgs a;
+    memset(&a, 0, sizeof(a));
+    const int np = (int)G.progs.size();
+    a.ops = G.d_ops;
+    a.prog_begin = G.d_meta;
+    a.prog_end = G.d_meta + np;
+    a.prog_rank = G.d_meta + 2 * np;
+    a.bufptr = G.d_bufptr;
+    a.zero_list = G.d_zero;
+    a.n = n;
+    a.K = pl->K;
+    a.nprog = np;
+    a.nbuf = (int)pl->ir.bufs.size();
+    a.in_buf = pl->in_buf;
+    a.out_buf = pl->out_buf;
+    a.input_private = pl->input_private ? 1 : 0;
+    a.flag_stride = pl->flag_stride;
+    for (size_t b = 0; b < pl->ir.bufs.size(); b++) a.buf_bytes[b] = (uint64_t)pl->ir.bufs[b].elems * pl->es;
+    for (int r = 0; r < n; r++) {
+      a.io_in[r] = (char*)inputs[r];     // one-process world: local index == rank
+      a.io_out[r] = (char*)outputs[r];
+      a.st[r] = (PlanState*)(pl->heap[r] + pl->state_off);
+      a.lanes[r] = (uint64_t*)(pl->heap[r] + pl->lanes_off);
+      a.bars[r] = (uint64_t*)(pl->heap[r] + pl->bars_off);
+      a.rank_ctas[r] = 0;
+      a.rank_leader[r] = -1;
+    }
+    for (int p = 0; p < np; p++) {
+      const int r = pl->prog_rank[G.progs[p]];
+      if (a.rank_leader[r] < 0) a.rank_leader[r] = p * pl->K;
+      a.rank_ctas[r] += pl->K;
+    }
+    cudaSetDevice(G.dev);
+    cfStatus s = join_streams(c, (int)gi, streams, false);
+    if (s != CF_OK) { cudaSetDevice(prev); return s; }
+    void* args[] = {&a};
+    cudaError_t e = cudaLaunchKernel(kernel, dim3(np * pl->K), dim3(pl->threads), args, 0, streams[c->groups[gi][0]]);
+    if (e != cudaSuccess) {
+      cudaSetDevice(prev);
+      return fail(CF_E_CUDA, "plan kernel launch: %s", cudaGetErrorString(e));
+    }
+    s = join_streams(c, (int)gi, streams, true);
+    if (s != CF_OK) { cudaSetDevice(prev); return s; }
+  }
+  cudaSetDevice(prev);
+  return CF_OK;
+}
+
+extern "C" cfStatus cfPlanInfo(cfPlan_t pl, size_t* in_elems, size_t* out_elems, int* dtype, int* n_programs,
+                               int* n_device_ops) {
+  if (!pl) return fail(CF_E_CONFIG, "null plan");
+  if (in_elems) *in_elems = (size_t)pl->ir.bufs[pl->in_buf].elems;
+  if (out_elems) *out_elems = (size_t)pl->ir.bufs[pl->out_buf].elems;
+  if (dtype) *dtype = pl->dtype;
+  if (n_programs) *n_programs = (int)pl->prog_ops.size();
+  if (n_device_ops) *n_device_ops = pl->n_device_ops;
+  return CF_OK;
+}
+
+extern "C" cfStatus cfPlanLastDeviceError(cfPlan_t pl, int* code) {
+  if (!pl || !code) return fail(CF_E_CONFIG, "null argument");
+  int prev = -1;
+  cudaGetDevice(&prev);
+  uint32_t worst = 0;
+  for (size_t r = 0; r < pl->heap.size(); r++) {
+    cudaSetDevice(pl->comm->local[r].dev);
+    cudaDeviceSynchronize();
+    PlanState st;
+    if (cudaMemcpy(&st, pl->heap[r] + pl->state_off, sizeof(st), cudaMemcpyDeviceToHost) != cudaSuccess) {
+      cudaSetDevice(prev);
+      return fail(CF_E_CUDA, "plan state read failed");
+    }
+    worst = std::max(worst, st.base.error);
+  }
+  cudaSetDevice(prev);
+  *code = (int)worst;
+  return CF_OK;
+}
+
+extern "C" cfStatus cfPlanDestroy(cfPlan_t pl) {
+  if (!pl) return CF_OK;
+  int prev = -1;
+  cudaGetDevice(&prev);
+  for (auto& G : pl->groups) {
+    cudaSetDevice(G.dev);
+    cudaFree(G.d_ops);
+    cudaFree(G.d_meta);
+    cudaFree(G.d_bufptr);
+    cudaFree(G.d_zero);
+  }
+  for (size_t r = 0; r < pl->heap.size(); r++)
+    if (pl->heap[r]) {
+      cudaSetDevice(pl->comm->local[r].dev);
+      cudaFree(pl->heap[r]);
+    }
+  cudaSetDevice(prev);
+  delete pl;
+  return CF_OK;
+}

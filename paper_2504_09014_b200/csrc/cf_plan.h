@@ -1,0 +1,137 @@
+// cf_plan.h -- execution-plan IR, device op array and launch arguments of the
+// GPU plan interpreter (K10).  Internal to libcf.
+//
+// Reference: plan wire format and IR   cf/plan.py:20-101, 136-291
+//            plan interpreter           cf/executor.py:73-379
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+#include "device/cf_device.cuh"
+
+namespace cf {
+namespace plan {
+
+// ---------------------------------------------------------------- host IR (cf/plan.py:38-86)
+
+enum OpKind { P_PUT, P_PUT_PACKETS, P_PUT_WITH_SIGNAL, P_SIGNAL, P_WAIT, P_FLUSH, P_READ_PACKETS,
+              P_REDUCE, P_REDUCE_PUT, P_COPY, P_TB_SYNC, P_DEVICE_BARRIER, P_NUM_OPS };
+enum BufKind { B_INPUT, B_OUTPUT, B_SCRATCH };
+enum ChanType { C_PORT, C_MEMORY, C_SWITCH };
+
+struct Ref {
+  int buf = -1;
+  long long off = 0, size = 0;
+};
+
+struct Op {
+  int kind = -1;
+  int chan = -1;
+  bool has_src = false, has_dst = false, has_src2 = false, has_arrives = false;
+  Ref src, dst, src2, arrives;
+  bool has_flag = false;
+  long long flag = 0;
+  bool has_group = false;
+  std::vector<int> group;
+};
+
+struct Buf {
+  std::string id;
+  int kind = B_SCRATCH;
+  int rank = -1;          // -1 = "all"
+  long long elems = 0;
+};
+
+struct Chan {
+  std::string id;
+  int type = C_MEMORY;
+  int src = -1, dst = -1;
+  std::vector<int> ranks;
+  int protocol = -1;      // -1 = plan protocol
+};
+
+struct Prog {
+  int rank = 0, tb = 0;
+  std::vector<Op> ops;
+};
+
+struct Plan {
+  std::string name;
+  int collective = 0, protocol = 0, dtype = 0, nranks = 0;
+  bool lowered = true;
+  std::vector<Buf> bufs;
+  std::vector<Chan> chans;
+  std::vector<Prog> progs;
+};
+
+// ---------------------------------------------------------------- device op array
+
+constexpr int kMaxSrc = 16;
+constexpr int kMaxDst = 8;
+
+enum DevCode : uint8_t {
+  D_NOP = 0,
+  D_SYNC_CTA,      // tb_sync whose dependences stay inside each CTA's slice
+  D_SYNC_GROUP,    // tb_sync across the CTAs of one program
+  D_DEV_BARRIER,   // device_barrier over member programs        cf/executor.py:208-226
+  D_SIGNAL,        // +1 on each CTA lane of the receiver         cf/channels.py:227-232
+  D_WAIT,          // every lane >= target                        cf/channels.py:234-237
+  D_MULTI,         // dst[*] = [0 +] src0 + src1 + ...            reduce / reduce_put / switch reduce
+  D_COPY,          // dst[*] = src0                               put / copy / switch broadcast
+  D_PUT_PACKETS,   // payload -> LL packets                       cf/channels.py:244-280
+  D_READ_PACKETS,  // LL packets -> payload                       cf/channels.py:303-330
+};
+enum DevFlags : uint8_t { F_ZERO = 1, F_ROUND_EACH = 2, F_VEC = 4, F_LL16 = 8 };
+
+struct DRef {
+  int32_t buf;
+  int32_t rank;
+  uint64_t off;        // bytes
+};
+
+struct DevOp {
+  uint8_t code, nsrc, ndst, flags;
+  uint32_t llflag;     // plan flag (the runtime flag also folds in the call epoch)
+  uint64_t size;       // elements (payload elements for LL ops)
+  int32_t id;          // channel index (signal/wait) or counter index (barriers)
+  int32_t peer;        // signal: receiving rank
+  uint64_t m;          // wait / barrier: 1-based occurrence within the call
+  uint64_t per_call;   // wait: signals per call on the channel; barrier: occurrences per call
+  uint64_t members;    // barrier: participating CTAs
+  DRef src[kMaxSrc];
+  DRef dst[kMaxDst];
+};
+
+// Per-rank execution state of one loaded plan (in the plan heap of the rank).
+struct PlanState {
+  RankState base;            // epoch / done counter / error word / timeout
+  uint64_t bar_arrive;       // rank barrier: local CTA arrivals (monotonic)
+  uint64_t bar_release;      // rank barrier: leader's release value
+  uint64_t rankbar[CF_MAX_RANKS];  // rank barrier: value written by each peer
+};
+
+struct PlanArgs {
+  const DevOp* ops;
+  const int32_t* prog_begin;   // per launched program
+  const int32_t* prog_end;
+  const int32_t* prog_rank;
+  char* const* bufptr;         // [nbuf * n] (plan-owned buffers; io buffers from io_in/io_out)
+  const int32_t* zero_list;    // per rank: buffers to zero each call, packed [rank][kMaxZero]
+  int n, K, nprog, nbuf;
+  int in_buf, out_buf;
+  int input_private;           // 1: plan writes its input -> copy user input into the plan buffer
+  uint32_t flag_stride;
+  uint64_t buf_bytes[16];      // byte size of each buffer (<= 16 buffers)
+  char* io_in[CF_MAX_RANKS];
+  char* io_out[CF_MAX_RANKS];
+  PlanState* st[CF_MAX_RANKS];
+  uint64_t* lanes[CF_MAX_RANKS];
+  uint64_t* bars[CF_MAX_RANKS];
+  int rank_ctas[CF_MAX_RANKS];
+  int rank_leader[CF_MAX_RANKS];
+};
+constexpr int kMaxBufs = 16;
+constexpr int kMaxZero = 16;
+
+}  // namespace plan
+}  // namespace cf

@@ -1,0 +1,316 @@
+// cf_plan_kernel.cu -- K10: the GPU plan interpreter (cf/executor.py:197-379).
+//
+// One launch per device runs every (rank, tb) program of the ranks on that
+// device.  Program p is executed by K CTAs: data ops are sliced contiguously
+// across them (element slice j of K); sync ops keep the reference's
+// per-thread-block ordering model (cf/lowering.py:11-17):
+//   tb_sync        -> __syncthreads when every dependence across it stays in
+//                     one CTA's slice (decided at load time), else a counter
+//                     barrier over the program's K CTAs
+//   signal         -> each CTA adds 1 to its own lane of the receiver's
+//                     semaphore after its own slice (release at .sys scope)
+//   wait           -> every lane of the channel >= (call-1)*signals_per_call + m
+//   device_barrier -> counter barrier over the member programs' CTAs
+// Calls are bracketed by rank-level barriers (entry: inputs produced, outputs
+// zeroed where the plan reads them before writing -- the reference zeroes
+// every region per execute, cf/executor.py:153-154; exit: nobody touches a
+// rank's buffers after it returns), so plan buffers are reused across calls
+// without host work, and LL flags are re-stamped with the call epoch.
+#include "cf_plan.h"
+
+namespace cf {
+namespace plan {
+
+__device__ __forceinline__ void red_add_release_sys(uint64_t* p, uint64_t v) {
+  asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ char* ref_ptr(const PlanArgs& a, const DRef& r) {
+  char* base;
+  if (r.buf == a.in_buf && !a.input_private) base = a.io_in[r.rank];
+  else if (r.buf == a.out_buf) base = a.io_out[r.rank];
+  else base = a.bufptr[r.buf * a.n + r.rank];
+  return base + r.off;
+}
+
+__device__ __forceinline__ uint32_t runtime_flag(uint64_t e, uint32_t stride, uint32_t f) {
+  return (uint32_t)(((e - 1) * (uint64_t)stride + f) % 0xffffffffull) + 1u;
+}
+
+// counter barrier: every participant adds 1, then waits for the call's total
+__device__ __forceinline__ void counter_barrier(uint64_t* ctr, uint64_t target, RankState* rs) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd((unsigned long long*)ctr, 1ull);
+    wait_geq(ctr, target, rs);
+  }
+  __syncthreads();
+}
+
+// All CTAs of `rank` meet; the rank's leader CTA exchanges `k` with every
+// other rank's leader, then releases its rank.
+__device__ void rank_barrier(const PlanArgs& a, int rank, uint64_t k) {
+  PlanState* ps = a.st[rank];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    atomicAdd((unsigned long long*)&ps->bar_arrive, 1ull);
+  }
+  if ((int)blockIdx.x == a.rank_leader[rank]) {
+    if (threadIdx.x == 0) wait_geq(&ps->bar_arrive, k * (uint64_t)a.rank_ctas[rank], &ps->base);
+    __syncthreads();
+    const int t = threadIdx.x;
+    if (t < a.n && t != rank) {
+      __threadfence_system();
+      st_release_sys(&a.st[t]->rankbar[rank], k);
+      wait_geq(&ps->rankbar[t], k, &ps->base);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) st_release_sys(&ps->bar_release, k);
+  } else if (threadIdx.x == 0) {
+    wait_geq(&ps->bar_release, k, &ps->base);
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------- element helpers
+
+template <typename T>
+__device__ __forceinline__ uint4 load_part(const char* p, int nval) {
+  constexpr int V = 16 / sizeof(T);
+  if (nval >= V) return ld16(p);
+  union { uint4 u; T t[V]; } r;
+  r.u = make_uint4(0, 0, 0, 0);
+  for (int i = 0; i < nval; i++) r.t[i] = reinterpret_cast<const T*>(p)[i];
+  return r.u;
+}
+template <typename T>
+__device__ __forceinline__ void store_part(char* p, uint4 v, int nval) {
+  constexpr int V = 16 / sizeof(T);
+  if (nval >= V) { st16(p, v); return; }
+  union { uint4 u; T t[V]; } x;
+  x.u = v;
+  for (int i = 0; i < nval; i++) reinterpret_cast<T*>(p)[i] = x.t[i];
+}
+
+template <typename T>
+__device__ __forceinline__ void acc_vec(typename Vec<T>::Acc* acc, uint4 x, bool round_each) {
+  constexpr int V = Vec<T>::N;
+  typename Vec<T>::Acc t[V];
+  Vec<T>::load(x, t);
+#pragma unroll
+  for (int j = 0; j < V; j++) {
+    acc[j] = acc_add(acc[j], t[j]);
+    if (round_each) acc[j] = Vec<T>::round(acc[j]);
+  }
+}
+
+// D_MULTI / D_COPY on this CTA's slice [lo, hi) of the op's elements.
+template <typename T>
+__device__ void data_op(const PlanArgs& a, const DevOp& op, int j) {
+  using A = typename Vec<T>::Acc;
+  constexpr int V = Vec<T>::N;
+  const uint64_t size = op.size;
+  const uint64_t per = ((size + a.K - 1) / a.K + V - 1) / V * V;
+  const uint64_t lo = min((uint64_t)j * per, size), hi = min(lo + per, size);
+  if (lo >= hi) return;
+  const int nsrc = op.nsrc, ndst = op.ndst;
+  const bool zero = op.flags & F_ZERO, round_each = op.flags & F_ROUND_EACH;
+  const bool multi = op.code == D_MULTI;
+  const char* src[kMaxSrc];
+  char* dst[kMaxDst];
+  for (int k = 0; k < nsrc; k++) src[k] = ref_ptr(a, op.src[k]);
+  for (int k = 0; k < ndst; k++) dst[k] = ref_ptr(a, op.dst[k]);
+  if (op.flags & F_VEC) {
+    for (uint64_t v = lo / V + threadIdx.x; v * V < hi; v += blockDim.x) {
+      const int nval = (int)min((uint64_t)V, hi - v * V);
+      const size_t boff = (size_t)v * 16;
+      uint4 res;
+      if (!multi) {
+        res = load_part<T>(src[0] + boff, nval);
+      } else {
+        A acc[V];
+        int k = 0;
+        if (zero) {
+#pragma unroll
+          for (int i = 0; i < V; i++) acc[i] = A(0);
+        } else {
+          Vec<T>::load(load_part<T>(src[0] + boff, nval), acc);
+          k = 1;
+        }
+        for (; k + 4 <= nsrc; k += 4) {   // four loads in flight per step
+          const uint4 x0 = load_part<T>(src[k] + boff, nval), x1 = load_part<T>(src[k + 1] + boff, nval);
+          const uint4 x2 = load_part<T>(src[k + 2] + boff, nval), x3 = load_part<T>(src[k + 3] + boff, nval);
+          acc_vec<T>(acc, x0, round_each);
+          acc_vec<T>(acc, x1, round_each);
+          acc_vec<T>(acc, x2, round_each);
+          acc_vec<T>(acc, x3, round_each);
+        }
+        for (; k < nsrc; k++) acc_vec<T>(acc, load_part<T>(src[k] + boff, nval), round_each);
+        res = Vec<T>::store(acc);
+      }
+      for (int d = 0; d < ndst; d++) store_part<T>(dst[d] + boff, res, nval);
+    }
+  } else {
+    for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+      const size_t boff = (size_t)i * sizeof(T);
+      T res;
+      if (!multi) {
+        res = *reinterpret_cast<const T*>(src[0] + boff);
+      } else {
+        A acc = zero ? A(0) : to_acc<T>(*reinterpret_cast<const T*>(src[0] + boff));
+        for (int k = zero ? 0 : 1; k < nsrc; k++) {
+          acc = acc_add(acc, to_acc<T>(*reinterpret_cast<const T*>(src[k] + boff)));
+          if (round_each) acc = Vec<T>::round(acc);
+        }
+        res = from_acc<T>(acc);
+      }
+      for (int d = 0; d < ndst; d++) *reinterpret_cast<T*>(dst[d] + boff) = res;
+    }
+  }
+}
+
+// LL packets (cf/channels.py:244-330).  LL16: 8 payload bytes per 16-byte
+// packet {d0, f, d1, f}; LL8: one reference packet {d, f} per 4 payload bytes.
+template <typename T>
+__device__ void packet_op(const PlanArgs& a, const DevOp& op, int j, uint64_t e, RankState* rs) {
+  constexpr int V = 16 / sizeof(T);
+  const uint64_t size = op.size;
+  const uint64_t per = ((size + a.K - 1) / a.K + V - 1) / V * V;
+  const uint64_t lo = min((uint64_t)j * per, size), hi = min(lo + per, size);
+  if (lo >= hi) return;
+  const uint32_t flag = runtime_flag(e, a.flag_stride, op.llflag);
+  const char* src = ref_ptr(a, op.src[0]);
+  char* dst = ref_ptr(a, op.dst[0]);
+  const bool put = op.code == D_PUT_PACKETS;
+  if (op.flags & F_LL16) {
+    const uint64_t u0 = lo * sizeof(T) / 8, u1 = (hi * sizeof(T) + 7) / 8;
+    for (uint64_t u = u0 + threadIdx.x; u < u1; u += blockDim.x) {
+      if (put) {
+        const uint2 d = *reinterpret_cast<const uint2*>(src + u * 8);
+        ll16_put(dst + u * 16, d, flag);
+      } else {
+        const uint2 d = ll16_get(src + u * 16, flag, rs);
+        *reinterpret_cast<uint2*>(dst + u * 8) = d;
+      }
+    }
+  } else {
+    const uint64_t u0 = lo * sizeof(T) / 4, u1 = (hi * sizeof(T) + 3) / 4;
+    for (uint64_t u = u0 + threadIdx.x; u < u1; u += blockDim.x) {
+      if (put) {
+        const uint32_t d = *reinterpret_cast<const uint32_t*>(src + u * 4);
+        st8_volatile(dst + u * 8, make_uint2(d, flag));
+      } else {
+        uint2 v = ld8_volatile(src + u * 8);
+        if (v.y != flag) {
+          const uint64_t t0 = globaltimer();
+          for (uint32_t it = 1; v.y != flag; ++it) {
+            v = ld8_volatile(src + u * 8);
+            if ((it & 255u) == 0) {
+              if (*(volatile uint32_t*)&rs->error != kDevOk) break;
+              if (globaltimer() - t0 > rs->timeout_ns) { atomicExch(&rs->error, (uint32_t)kDevTimeout); break; }
+            }
+          }
+        }
+        *reinterpret_cast<uint32_t*>(dst + u * 4) = v.x;
+      }
+    }
+  }
+}
+
+// Prologue of a call, split over the rank's CTAs: copy the user input into the
+// private input buffer (plans that write their input, e.g. ring RS) and zero
+// the buffers the plan reads before writing (cf/executor.py:153-154).
+__device__ void prologue(const PlanArgs& a, int rank) {
+  const int cta = (int)blockIdx.x - a.rank_leader[rank];
+  const int nct = a.rank_ctas[rank];
+  const size_t stride = (size_t)nct * blockDim.x;
+  const size_t t0 = (size_t)cta * blockDim.x + threadIdx.x;
+  if (a.input_private) {
+    const char* s = a.io_in[rank];
+    char* d = a.bufptr[a.in_buf * a.n + rank];
+    const size_t nb = a.buf_bytes[a.in_buf];
+    for (size_t i = t0; i < nb / 16; i += stride) st16(d + i * 16, ld16(s + i * 16));
+    for (size_t i = nb / 16 * 16 + t0; i < nb; i += stride) d[i] = s[i];
+  }
+  for (int z = 0; z < kMaxZero; z++) {
+    const int b = a.zero_list[rank * kMaxZero + z];
+    if (b < 0) break;
+    char* d = b == a.out_buf ? a.io_out[rank] : a.bufptr[b * a.n + rank];
+    const size_t nb = a.buf_bytes[b];
+    for (size_t i = t0; i < nb / 16; i += stride) st16(d + i * 16, make_uint4(0, 0, 0, 0));
+    for (size_t i = nb / 16 * 16 + t0; i < nb; i += stride) d[i] = 0;
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(512) plan_kernel(const __grid_constant__ PlanArgs a) {
+  const int pid = blockIdx.x / a.K, j = blockIdx.x % a.K;
+  const int rank = a.prog_rank[pid];
+  PlanState* ps = a.st[rank];
+  RankState* rs = &ps->base;
+  __shared__ uint64_t s_e;
+  if (threadIdx.x == 0) s_e = *(volatile uint64_t*)&rs->epoch + 1;
+  __syncthreads();
+  const uint64_t e = s_e;
+  prologue(a, rank);
+  rank_barrier(a, rank, 2 * e - 1);
+  const int end = a.prog_end[pid];
+  for (int i = a.prog_begin[pid]; i < end; i++) {
+    const DevOp& op = a.ops[i];
+    switch (op.code) {
+      case D_SYNC_CTA:
+        __syncthreads();
+        break;
+      case D_SYNC_GROUP:
+      case D_DEV_BARRIER:
+        counter_barrier(a.bars[rank] + op.id, ((e - 1) * op.per_call + op.m) * op.members, rs);
+        break;
+      case D_SIGNAL:
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          __threadfence_system();
+          red_add_release_sys(a.lanes[op.peer] + (size_t)op.id * a.K + j, 1);
+        }
+        break;
+      case D_WAIT:
+        if ((int)threadIdx.x < a.K)
+          wait_geq(a.lanes[rank] + (size_t)op.id * a.K + threadIdx.x, (e - 1) * op.per_call + op.m, rs);
+        __syncthreads();
+        break;
+      case D_MULTI:
+      case D_COPY:
+        data_op<T>(a, op, j);
+        break;
+      case D_PUT_PACKETS:
+      case D_READ_PACKETS:
+        packet_op<T>(a, op, j, e, rs);
+        break;
+      default:
+        break;
+    }
+  }
+  rank_barrier(a, rank, 2 * e);
+  if (threadIdx.x == 0) {
+    const uint32_t prev = atomicAdd(&rs->arrive, 1u);
+    if (prev == (uint32_t)a.rank_ctas[rank] - 1) {
+      *(volatile uint32_t*)&rs->arrive = 0;
+      *(volatile uint64_t*)&rs->epoch = e;
+      __threadfence();
+    }
+  }
+}
+
+const void* plan_kernel_for(int dtype) {
+  switch (dtype) {
+    case 0: return (const void*)plan_kernel<int32_t>;
+    case 1: return (const void*)plan_kernel<float>;
+    case 2: return (const void*)plan_kernel<__half>;
+    case 3: return (const void*)plan_kernel<__nv_bfloat16>;
+  }
+  return nullptr;
+}
+
+}  // namespace plan
+}  // namespace cf

@@ -1,0 +1,59 @@
+"""The C ABI library loads and exports every symbol include/cf.h declares
+(no compute calls: CPU only)."""
+
+import ctypes
+import os
+import re
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    with open(os.path.join(ROOT, "include", "cf.h")) as f:
+        text = f.read()
+    return set(re.findall(r"CF_API\s+[\w\s\*]*?\b(cf\w+)\s*\(", text))
+
+
+def test_header_declarations_match_binding_table():
+    from paper_2504_09014_b200 import _lib
+    assert _declared() == set(_lib.EXPORTS)
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2504_09014_b200 import _lib
+    lib = ctypes.CDLL(_lib.LIB_PATH)
+    missing = [s for s in _declared() if not hasattr(lib, s)]
+    assert not missing, missing
+
+
+def test_status_codes_match_reference_error_codes():
+    from paper_2504_09014_b200 import _lib, errors
+    lib = _lib.lib()
+    for i, code in enumerate(errors.STATUS_CODES):
+        assert lib.cfStatusCode(i).decode() == code
+    # every reference error class (cf/errors.py:6-93) has a status
+    ref_codes = {"E_GENERIC", "E_BAD_SIZE", "E_NO_SEM", "E_BAD_DELTA", "E_OOB", "E_DEADLOCK",
+                 "E_PROXY_DOWN", "E_ZERO_FLAG", "E_WRONG_PROTOCOL", "E_BAD_ALIGN", "E_SYNTAX",
+                 "E_VERSION", "E_REF", "E_SHAPE", "E_PROTOCOL", "E_RANK_MISMATCH", "E_TOPOLOGY",
+                 "E_NO_ALGO", "E_BAD_TIME", "E_CONFIG"}
+    assert ref_codes <= set(errors.STATUS_CODES)
+    assert lib.cfVersion() == 1
+
+
+def test_raise_status_maps_classes():
+    import pytest
+    from paper_2504_09014_b200 import errors
+    for i, code in enumerate(errors.STATUS_CODES[1:], start=1):
+        with pytest.raises(errors.CommforgeError) as ei:
+            errors.raise_status(i, "x")
+        assert ei.value.code == code
+
+
+def test_kernels_are_sm100a_cubins():
+    """libcf.so carries sm_100a SASS (no PTX-only / other-arch fallback)."""
+    import subprocess
+    from paper_2504_09014_b200 import _lib
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", _lib.LIB_PATH],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    assert all("sm_100a" in line for line in out.splitlines() if line.strip())

@@ -1,0 +1,128 @@
+"""GPU plan executor (K10) vs the reference runtime's outputs (golden digests)
+and vs the oracle's sequential plan interpreter.  Needs a B200."""
+
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+from inputs import gen_inputs
+from oracle import oracle
+
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+_WORLDS = {}
+
+
+def world(n):
+    from paper_2504_09014_b200 import make_world
+    if n not in _WORLDS:
+        _WORLDS[n] = make_world(1, n, spin_timeout_ms=4000)
+    return _WORLDS[n]
+
+
+def _digest(a):
+    return hashlib.sha256(np.ascontiguousarray(a).view(np.uint8).tobytes()).hexdigest()
+
+
+def _load(name):
+    with open(os.path.join(GOLD, "plans", name + ".json"), "rb") as f:
+        return f.read()
+
+
+def _runs():
+    with open(os.path.join(GOLD, "plan_runs.json")) as f:
+        return json.load(f)
+
+
+@pytest.mark.parametrize("run", _runs(), ids=lambda r: f"{r['plan']}-{r['dtype']}")
+def test_plan_matches_reference_runtime_bits(run):
+    from paper_2504_09014_b200 import Runtime, parse_plan
+    doc = _load(run["plan"])
+    plan = parse_plan(doc.replace(b'"dtype":"i32"', f'"dtype":"{run["dtype"]}"'.encode()))
+    ins = gen_inputs(plan.num_ranks, run["in_elems"], run["dtype"], run["dist"], run["seed"])
+    rt = Runtime(plan, world(plan.num_ranks))
+    for _ in range(3):   # repeated executions reuse buffers, lanes and flags
+        res = rt.execute(ins)
+        assert [_digest(o) for o in res.outputs] == run["digests"]
+    rt.close()
+
+
+def test_reference_golden_ring_rs_plan():
+    from paper_2504_09014_b200 import Runtime, parse_plan
+    with open(os.path.join(GOLD, "frontend", "ring_rs_n4e8_lowered.json"), "rb") as f:
+        plan = parse_plan(f.read())
+    ins = [np.full(8, r + 1, np.int32) for r in range(4)]
+    res = Runtime(plan, world(4)).execute(ins)
+    for r in range(4):
+        assert (res.outputs[r] == 10).all()   # reference test_executor.py:67-74
+
+
+def _scaled(doc: bytes, factor: int, dtype: str) -> bytes:
+    """Scale every element count / offset of a size-homogeneous library plan."""
+    d = json.loads(doc)
+    d["dtype"] = "f32"
+    for b in d["buffers"]:
+        b["elems"] *= factor
+    for p in d["programs"]:
+        for o in p["ops"]:
+            for k in ("src", "dst", "src2", "arrives"):
+                if k in o:
+                    o[k] = [o[k][0], o[k][1] * factor, o[k][2] * factor]
+    return json.dumps(d, sort_keys=True, separators=(",", ":")).encode()
+
+
+@pytest.mark.parametrize("name,factor", [("2pa_memory_n8_e64", 128), ("1pa_n8_e64", 128),
+                                         ("2pa_memory_n8_e64", 128 * 64),
+                                         ("2pa_memory_n8_e64_i2", 512),
+                                         ("switch_2pa_n8_e64", 1024), ("allpairs_ag_n8_e64", 256)])
+@pytest.mark.parametrize("dtype", ["bf16", "f16", "f32"])
+def test_c5_shaped_plans_vs_oracle(name, factor, dtype):
+    """C5: Llama-70B TP decode AllReduce [b, 8192] through lowered reference plans."""
+    from paper_2504_09014_b200 import Runtime, parse_plan
+    doc = _scaled(_load(name), factor, dtype)
+    plan = parse_plan(doc)
+    in_elems = next(b.elems for b in plan.buffers if b.kind == "input")
+    ins = gen_inputs(8, in_elems, dtype, "normal", factor, scale=0.02)
+    rt = Runtime(plan, world(8), dtype=dtype)
+    got = rt.execute(ins).outputs
+    want = oracle.run_plan(doc, ins, dtype=dtype)
+    for r in range(8):
+        assert np.array_equal(got[r].view(np.uint8), want[r].view(np.uint8)), r
+    rt.close()
+
+
+def test_wait_without_signal_raises_deadlock():
+    """reference test_executor.py:77-89, as a device spin timeout."""
+    from paper_2504_09014_b200 import Runtime, make_world
+    from paper_2504_09014_b200.errors import DeadlockError
+    from paper_2504_09014_b200.plan import (BufferDecl, ChannelDecl, ExecutionPlan, PlanOp,
+                                            ThreadBlockProgram)
+    plan = ExecutionPlan(1, "stuck", "custom", "HB", "i32", 2,
+                         [BufferDecl("in", "input", "all", 4), BufferDecl("out", "output", "all", 4)],
+                         [ChannelDecl("c0", "memory", src=0, dst=1)],
+                         [ThreadBlockProgram(1, 0, (PlanOp("wait", chan="c0"),))])
+    w = make_world(1, 2, spin_timeout_ms=300)
+    rt = Runtime(plan, w)
+    with pytest.raises(DeadlockError):
+        rt.execute([np.zeros(4, np.int32)] * 2)
+    rt.close()
+    w.close()
+
+
+def test_runtime_rejects_bad_plans():
+    from paper_2504_09014_b200 import Runtime, parse_plan
+    from paper_2504_09014_b200.errors import RankMismatchError, ShapeError
+    plan = parse_plan(_load("2pa_memory_n4_e8"))
+    with pytest.raises(RankMismatchError):
+        Runtime(plan, world(2))
+    with open(os.path.join(GOLD, "frontend", "frontend_1pa_n4e8.json"), "rb") as f:
+        pre = parse_plan(f.read())
+    with pytest.raises(ShapeError):
+        Runtime(pre, world(4))
+    rt = Runtime(plan, world(4))
+    with pytest.raises(ShapeError):
+        rt.execute([np.zeros(7, np.int32)] * 4)
