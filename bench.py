@@ -335,11 +335,12 @@ def run_sweep(w, args):
     maxe = big // 2
     send = [torch.randn(maxe, device=dev).to(torch.bfloat16) for _ in range(n)]
     recv = [torch.empty_like(s) for s in send]
+    ll_max = w.config.ll_max_bytes or 4 * MiB
     for nb in sizes:
         count = nb // 2
         row = {"bytes": nb}
         for name in ("auto", "1pa", "2pa_ll", "2pa", "1pa_hb"):
-            if name in ("1pa", "2pa_ll") and nb > w.config.ll_max_bytes:
+            if name in ("1pa", "2pa_ll") and nb > ll_max:
                 continue
             if name == "1pa_hb" and nb > 64 * MiB:
                 continue

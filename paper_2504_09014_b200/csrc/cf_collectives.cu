@@ -47,13 +47,13 @@ __device__ __forceinline__ void end_call(const RankCtx& rk, uint64_t e) {
 // then wait until each peer's CTA b signalled >= v.  `publish` makes this
 // CTA's prior global writes visible system-wide first (fence before signal,
 // cf/channels.py:227-232).
-__device__ __forceinline__ void handshake(const RankCtx& rk, int n, uint64_t v, bool publish) {
+__device__ __forceinline__ void handshake(const RankCtx& rk, int n, uint64_t v, bool publish, bool gpu) {
   const int t = threadIdx.x, r = rk.rank, b = blockIdx.x;
   if (publish) __syncthreads();
   if (t < n && t != r) {
-    if (publish) __threadfence_system();
-    st_release_sys(rk.sem[t] + sem_index(r, b), v);
-    wait_geq(rk.sem[r] + sem_index(t, b), v, rk.st);
+    if (publish) fence_publish(gpu);
+    st_release(rk.sem[t] + sem_index(r, b), v, gpu);
+    wait_geq(rk.sem[r] + sem_index(t, b), v, rk.st, gpu);
   }
   __syncthreads();
 }
@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(512) pull_reduce_kernel(const __grid_constant_
   constexpr int V = Vec<T>::N;
   const int n = a.n, r = rk.rank;
   const uint64_t e = begin_call(rk);
-  handshake(rk, n, e * 4 + 1, false);
+  handshake(rk, n, e * 4 + 1, false, a.gpu_scope);
 
   size_t lo = 0, hi = a.count;
   if (!a.whole) {
@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(512) pull_reduce_kernel(const __grid_constant_
       store_vec<T>(rk.out[r], v, res, lo, hi, shift);
     }
   }
-  handshake(rk, n, e * 4 + 2, true);
+  handshake(rk, n, e * 4 + 2, true, a.gpu_scope);
   end_call(rk, e);
 }
 
@@ -312,7 +312,7 @@ __global__ void __launch_bounds__(512) push_gather_kernel(const __grid_constant_
   constexpr int V = 16 / sizeof(T);
   const int n = a.n, r = rk.rank;
   const uint64_t e = begin_call(rk);
-  handshake(rk, n, e * 4 + 1, false);
+  handshake(rk, n, e * 4 + 1, false, a.gpu_scope);
   const size_t stride = (size_t)gridDim.x * blockDim.x;
   const size_t t0 = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   const size_t sb = a.count * sizeof(T);
@@ -333,7 +333,7 @@ __global__ void __launch_bounds__(512) push_gather_kernel(const __grid_constant_
         store_vec<T>(rk.out[p] + (size_t)r * sb, v, x, 0, a.count, 0);
     }
   }
-  handshake(rk, n, e * 4 + 2, true);
+  handshake(rk, n, e * 4 + 2, true, a.gpu_scope);
   end_call(rk, e);
 }
 

@@ -30,6 +30,7 @@ struct CollArgs {
   int push;         // pull-reduce: store the result into every rank's recv buffer
   int whole;        // pull-reduce: each rank reduces [0,count) instead of its chunk
   int rs_shift;     // pull-reduce: recv is the shard (offset by -chunk start)
+  int gpu_scope;    // every rank on this device: .gpu-scope release/acquire suffice
   size_t count;     // elements per rank (AR/RS: send elements; AG: shard elements)
   size_t cs;        // reference chunk size in elements (cf/collectives.py:170-172)
   size_t slot;      // LL slot stride in bytes

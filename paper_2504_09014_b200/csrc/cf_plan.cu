@@ -813,6 +813,7 @@ extern "C" cfStatus cfPlanExecute(cfPlan_t pl, const void* const* inputs, void* 
     a.in_buf = pl->in_buf;
     a.out_buf = pl->out_buf;
     a.input_private = pl->input_private ? 1 : 0;
+    a.gpu_scope = pl->groups.size() == 1 ? 1 : 0;
     a.flag_stride = pl->flag_stride;
     for (size_t b = 0; b < pl->ir.bufs.size(); b++) a.buf_bytes[b] = (uint64_t)pl->ir.bufs[b].elems * pl->es;
     for (int r = 0; r < n; r++) {

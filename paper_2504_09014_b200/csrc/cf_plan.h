@@ -120,6 +120,7 @@ struct PlanArgs {
   int n, K, nprog, nbuf;
   int in_buf, out_buf;
   int input_private;           // 1: plan writes its input -> copy user input into the plan buffer
+  int gpu_scope;               // every rank on this device: .gpu-scope release/acquire
   uint32_t flag_stride;
   uint64_t buf_bytes[16];      // byte size of each buffer (<= 16 buffers)
   char* io_in[CF_MAX_RANKS];

@@ -21,8 +21,9 @@
 namespace cf {
 namespace plan {
 
-__device__ __forceinline__ void red_add_release_sys(uint64_t* p, uint64_t v) {
-  asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+__device__ __forceinline__ void red_add_release(uint64_t* p, uint64_t v, bool gpu) {
+  if (gpu) asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+  else asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
 __device__ __forceinline__ char* ref_ptr(const PlanArgs& a, const DRef& r) {
@@ -43,7 +44,7 @@ __device__ __forceinline__ void counter_barrier(uint64_t* ctr, uint64_t target, 
   if (threadIdx.x == 0) {
     __threadfence();
     atomicAdd((unsigned long long*)ctr, 1ull);
-    wait_geq(ctr, target, rs);
+    wait_geq(ctr, target, rs, true);
   }
   __syncthreads();
 }
@@ -52,24 +53,25 @@ __device__ __forceinline__ void counter_barrier(uint64_t* ctr, uint64_t target, 
 // other rank's leader, then releases its rank.
 __device__ void rank_barrier(const PlanArgs& a, int rank, uint64_t k) {
   PlanState* ps = a.st[rank];
+  const bool gpu = a.gpu_scope;
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence_system();
+    fence_publish(gpu);
     atomicAdd((unsigned long long*)&ps->bar_arrive, 1ull);
   }
   if ((int)blockIdx.x == a.rank_leader[rank]) {
-    if (threadIdx.x == 0) wait_geq(&ps->bar_arrive, k * (uint64_t)a.rank_ctas[rank], &ps->base);
+    if (threadIdx.x == 0) wait_geq(&ps->bar_arrive, k * (uint64_t)a.rank_ctas[rank], &ps->base, true);
     __syncthreads();
     const int t = threadIdx.x;
     if (t < a.n && t != rank) {
-      __threadfence_system();
-      st_release_sys(&a.st[t]->rankbar[rank], k);
-      wait_geq(&ps->rankbar[t], k, &ps->base);
+      fence_publish(gpu);
+      st_release(&a.st[t]->rankbar[rank], k, gpu);
+      wait_geq(&ps->rankbar[t], k, &ps->base, gpu);
     }
     __syncthreads();
-    if (threadIdx.x == 0) st_release_sys(&ps->bar_release, k);
+    if (threadIdx.x == 0) st_release_gpu(&ps->bar_release, k);
   } else if (threadIdx.x == 0) {
-    wait_geq(&ps->bar_release, k, &ps->base);
+    wait_geq(&ps->bar_release, k, &ps->base, true);
   }
   __syncthreads();
 }
@@ -270,13 +272,14 @@ __global__ void __launch_bounds__(512) plan_kernel(const __grid_constant__ PlanA
       case D_SIGNAL:
         __syncthreads();
         if (threadIdx.x == 0) {
-          __threadfence_system();
-          red_add_release_sys(a.lanes[op.peer] + (size_t)op.id * a.K + j, 1);
+          fence_publish(a.gpu_scope);
+          red_add_release(a.lanes[op.peer] + (size_t)op.id * a.K + j, 1, a.gpu_scope);
         }
         break;
       case D_WAIT:
         if ((int)threadIdx.x < a.K)
-          wait_geq(a.lanes[rank] + (size_t)op.id * a.K + threadIdx.x, (e - 1) * op.per_call + op.m, rs);
+          wait_geq(a.lanes[rank] + (size_t)op.id * a.K + threadIdx.x, (e - 1) * op.per_call + op.m, rs,
+                   a.gpu_scope);
         __syncthreads();
         break;
       case D_MULTI:

@@ -434,6 +434,7 @@ cfStatus launch(cfComm* c, const Job& j, int dtype, const void* const* send, voi
     a.push = j.push;
     a.whole = j.whole;
     a.rs_shift = j.rs_shift;
+    a.gpu_scope = (c->groups.size() == 1 && !c->multiprocess) ? 1 : 0;
     a.count = j.count;
     a.cs = j.cs;
     a.slot = j.slot ? j.slot : c->lay.slot;

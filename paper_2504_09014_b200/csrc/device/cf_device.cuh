@@ -72,6 +72,25 @@ __device__ __forceinline__ uint64_t ld_relaxed_sys(const uint64_t* p) {
   asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ void st_release_gpu(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_acquire_gpu(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+// Scope-selected release/acquire: `gpu` when every rank of the communicator
+// lives on this device (co-resident ranks), `sys` across GPUs (NVLink peers).
+__device__ __forceinline__ void st_release(uint64_t* p, uint64_t v, bool gpu) {
+  if (gpu) st_release_gpu(p, v); else st_release_sys(p, v);
+}
+__device__ __forceinline__ uint64_t ld_acquire(const uint64_t* p, bool gpu) {
+  return gpu ? ld_acquire_gpu(p) : ld_acquire_sys(p);
+}
+__device__ __forceinline__ void fence_publish(bool gpu) {
+  if (gpu) __threadfence(); else __threadfence_system();
+}
 __device__ __forceinline__ void fence_acq_rel_sys() {
   asm volatile("fence.acq_rel.sys;" ::: "memory");
 }
@@ -117,12 +136,13 @@ __device__ __forceinline__ void st8_volatile(void* p, uint2 v) {
 // Spin until *sem >= target (acquire).  Returns false on timeout or when the
 // rank's error word is already set (so one stuck wait does not cascade into a
 // full-timeout per wait).
-__device__ __forceinline__ bool wait_geq(const uint64_t* sem, uint64_t target, RankState* st) {
-  if (ld_acquire_sys(sem) >= target) return true;
+__device__ __forceinline__ bool wait_geq(const uint64_t* sem, uint64_t target, RankState* st,
+                                         bool gpu = false) {
+  if (ld_acquire(sem, gpu) >= target) return true;
   const uint64_t t0 = globaltimer();
   const uint64_t limit = st->timeout_ns;
   for (uint32_t it = 1;; ++it) {
-    if (ld_acquire_sys(sem) >= target) return true;
+    if (ld_acquire(sem, gpu) >= target) return true;
     if ((it & 255u) == 0) {
       if (*(volatile uint32_t*)&st->error != kDevOk) return false;
       if (globaltimer() - t0 > limit) {
