@@ -360,8 +360,62 @@ def run_sweep(w, args):
 
 
 def run_multi_gpu(args):
-    raise SystemExit("multi-GPU bench needs the one-process-per-GPU registered-buffer path "
-                     "(not in this build)")
+    """N GPUs, one rank per process (torchrun): the same AllReduce over NVLink."""
+    import torch
+    import torch.distributed as dist
+    from paper_2504_09014_b200.comm import Communicator
+    from paper_2504_09014_b200.dtypes import torch_dtype
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    torch.cuda.set_device(local)
+    dist.init_process_group("gloo", init_method="env://")
+    comm = Communicator(device=local)
+    dev = torch.device("cuda", local)
+    count = HEAD_BYTES // 2
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(20250409 + 4000 + rank)
+    send = torch.randn(count, device=dev, generator=gen).to(torch_dtype(HEAD_DTYPE))
+    recv = torch.empty_like(send)
+    comm.register(send)
+    comm.register(recv)
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(args.warmup):
+        comm.all_reduce(send, recv, algo="2pa")
+    torch.cuda.synchronize(dev)
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize(dev)
+        dist.barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            comm.all_reduce(send, recv, algo="2pa")
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+    comm.check_device_error()
+    t_local = e0.elapsed_time(e1) / 1e3 / args.steps
+    times = [None] * world
+    dist.all_gather_object(times, t_local)
+    t = max(times)
+    if rank == 0:
+        value = busbw(HEAD_BYTES, t, world)
+        print(json.dumps({
+            "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t * 1e3, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": HEAD_DTYPE,
+            "data": "synthetic",
+            "config": {"workload": f"AllReduce {HEAD_DTYPE}, {world} ranks (one per GPU, NVLink), "
+                                   f"{HEAD_BYTES // MiB} MiB per rank", "ranks": world,
+                       "algo": "2pa", "parallelism": f"{world} GPUs",
+                       "l2": "inputs larger than L2"},
+            "pct_of_900": round(100 * value / 900, 2),
+            "roofline": {"bound": "nvlink", "achieved": round(value, 1), "peak": 900.0,
+                         "unit": "GB/s", "frac": round(value / 900, 4), "traffic": None},
+            "gpu_launches": args.steps, "clocks": clk.summary()}))
+    comm.close()
+    dist.destroy_process_group()
+    return 0
 
 
 def main():

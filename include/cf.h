@@ -122,6 +122,18 @@ CF_API cfStatus cfCommGetHandle(cfComm_t comm, void* handle, size_t* bytes);
 CF_API cfStatus cfCommConnect(cfComm_t comm, const void* handles, size_t bytes_per_handle);
 CF_API cfStatus cfCommDestroy(cfComm_t comm);
 
+/* Buffer registration for the one-process-per-GPU mode (the B200 counterpart
+ * of binding plan buffers to world regions, cf/executor.py:97-105): export the
+ * IPC handle of a device buffer (any cudaMalloc'd range, e.g. a torch tensor),
+ * all-gather the handles with the bootstrap, then import them so HB
+ * algorithms can read/write the peers' corresponding buffers zero-copy.
+ * Collective calls on pointers inside a registered range use the peers'
+ * ranges at the same offset.  No-ops for cfCommInitAll communicators. */
+#define CF_BUFFER_HANDLE_BYTES 128
+CF_API cfStatus cfBufferExport(cfComm_t comm, const void* ptr, size_t bytes, void* handle);
+CF_API cfStatus cfBufferImport(cfComm_t comm, const void* ptr, const void* handles, size_t bytes_per_handle);
+CF_API cfStatus cfBufferRelease(cfComm_t comm, const void* ptr);
+
 CF_API cfStatus cfCommNumRanks(cfComm_t comm, int* nranks);
 CF_API cfStatus cfCommLocalRanks(cfComm_t comm, int* nlocal, int* ranks /* nullable, nlocal entries */);
 CF_API cfStatus cfCommMulticastSupported(cfComm_t comm, int* supported);
@@ -138,8 +150,9 @@ CF_API cfStatus cfCommClearDeviceError(cfComm_t comm);
  *   ReduceScatter  recvcount = shard elements; send holds nranks*recvcount
  * In the one-process mode the buffers of every rank must be device memory
  * reachable from every rank's device (same device, or peer access).  In the
- * one-process-per-GPU mode only the LL algorithms run in this version (they
- * touch no peer user buffer). */
+ * one-process-per-GPU mode the LL algorithms take any buffers (they touch no
+ * peer user buffer); HB algorithms need buffers registered with
+ * cfBufferExport/cfBufferImport (CF_E_TOPOLOGY otherwise). */
 CF_API cfStatus cfAllReduce(cfComm_t comm, const void* const* send, void* const* recv, size_t count,
                      cfDtype dtype, int algo, const cudaStream_t* streams);
 CF_API cfStatus cfAllGather(cfComm_t comm, const void* const* send, void* const* recv, size_t sendcount,

@@ -17,6 +17,7 @@ LIB_PATH = os.path.join(_HERE, "libcf.so")
 CF_MAX_RANKS = 8
 CF_MAX_BLOCKS = 1024
 CF_HANDLE_BYTES = 256
+CF_BUFFER_HANDLE_BYTES = 128
 
 ALGOS = {
     "auto": -1, "1pa": 0, "1pa_hb": 1, "2pa": 2, "2pa_ll": 3, "switch_2pa": 4, "2pr": 5,
@@ -27,7 +28,8 @@ ALGO_NAMES = {v: k for k, v in ALGOS.items()}
 # every symbol include/cf.h declares (tests check the .so exports all of them)
 EXPORTS = (
     "cfStatusCode", "cfLastErrorMessage", "cfVersion", "cfCommInitAll", "cfCommCreateRank",
-    "cfCommGetHandle", "cfCommConnect", "cfCommDestroy", "cfCommNumRanks", "cfCommLocalRanks",
+    "cfCommGetHandle", "cfCommConnect", "cfCommDestroy", "cfBufferExport", "cfBufferImport",
+    "cfBufferRelease", "cfCommNumRanks", "cfCommLocalRanks",
     "cfCommMulticastSupported", "cfCommLastDeviceError", "cfCommClearDeviceError", "cfAllReduce",
     "cfAllGather", "cfReduceScatter", "cfSelectAlgorithm", "cfPlanLoad", "cfPlanExecute",
     "cfPlanInfo", "cfPlanLastDeviceError", "cfPlanDestroy",
@@ -56,6 +58,9 @@ _PROTOS = {
     "cfCommGetHandle": ([vp, vp, P(sz)], i32),
     "cfCommConnect": ([vp, vp, sz], i32),
     "cfCommDestroy": ([vp], i32),
+    "cfBufferExport": ([vp, vp, sz, vp], i32),
+    "cfBufferImport": ([vp, vp, vp, sz], i32),
+    "cfBufferRelease": ([vp, vp], i32),
     "cfCommNumRanks": ([vp, P(i32)], i32),
     "cfCommLocalRanks": ([vp, P(i32), P(i32)], i32),
     "cfCommMulticastSupported": ([vp, P(i32)], i32),

@@ -1,0 +1,122 @@
+"""One process per GPU: the multi-process communicator.
+
+The reference runs every rank in one process (``make_world``); a real
+8xB200 job runs one process per GPU.  Bootstrap is pluggable: any
+``torch.distributed`` process group (gloo or nccl; NCCL is never used for
+data) all-gathers the opaque handles libcf exports (``cfCommGetHandle`` for
+the symmetric heap, ``cfBufferExport`` for registered tensors).  After that
+every collective is a single libcf kernel over NVLink peer memory.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+from . import _lib
+from .collectives import _algo_id
+from .dtypes import CODES, from_torch
+from .errors import ShapeError
+
+
+def all_gather_bytes(blob: bytes, group=None) -> list:
+    """All-gather one fixed-size byte string per rank (rank order)."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    backend = dist.get_backend(group)
+    dev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else torch.device("cpu")
+    t = torch.frombuffer(bytearray(blob), dtype=torch.uint8).to(dev)
+    out = [torch.empty_like(t) for _ in range(world)]
+    dist.all_gather(out, t, group=group)
+    return [bytes(o.cpu().numpy().tobytes()) for o in out]
+
+
+class Communicator:
+    """This process's rank of an ``nranks``-GPU communicator."""
+
+    def __init__(self, group=None, device=None, ll_max_bytes: int = 0, max_blocks: int = 0,
+                 threads: int = 0, spin_timeout_ms: int = 0):
+        import torch
+        import torch.distributed as dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.nranks = dist.get_world_size(group)
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else int(device))
+        cfg = _lib.cfConfig(ll_max_bytes, max_blocks, threads, int(spin_timeout_ms) * 1_000_000, 0)
+        h = ctypes.c_void_p()
+        L = _lib.lib()
+        _lib.check(L.cfCommCreateRank(ctypes.byref(h), self.nranks, self.rank, self.device.index,
+                                      ctypes.byref(cfg)))
+        self._comm = h
+        blob = ctypes.create_string_buffer(_lib.CF_HANDLE_BYTES)
+        nbytes = ctypes.c_size_t(_lib.CF_HANDLE_BYTES)
+        _lib.check(L.cfCommGetHandle(h, blob, ctypes.byref(nbytes)))
+        handles = all_gather_bytes(blob.raw, group)
+        allh = b"".join(handles)
+        _lib.check(L.cfCommConnect(h, allh, _lib.CF_HANDLE_BYTES))
+        self._registered = {}
+
+    @property
+    def comm(self):
+        return self._comm
+
+    def register(self, tensor) -> None:
+        """Collective: every rank registers its corresponding tensor."""
+        L = _lib.lib()
+        blob = ctypes.create_string_buffer(_lib.CF_BUFFER_HANDLE_BYTES)
+        nbytes = tensor.numel() * tensor.element_size()
+        _lib.check(L.cfBufferExport(self._comm, tensor.data_ptr(), nbytes, blob))
+        allh = b"".join(all_gather_bytes(blob.raw, self.group))
+        _lib.check(L.cfBufferImport(self._comm, tensor.data_ptr(), allh, _lib.CF_BUFFER_HANDLE_BYTES))
+        self._registered[tensor.data_ptr()] = tensor
+
+    def deregister(self, tensor) -> None:
+        _lib.check(_lib.lib().cfBufferRelease(self._comm, tensor.data_ptr()))
+        self._registered.pop(tensor.data_ptr(), None)
+
+    def _call(self, fn, send, recv, count, algo, stream):
+        import torch
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        st = _lib.ptr_array([s.cuda_stream])
+        _lib.check(fn(self._comm, _lib.ptr_array([send.data_ptr()]), _lib.ptr_array([recv.data_ptr()]),
+                      int(count), CODES[from_torch(send.dtype)], int(algo), st))
+
+    def all_reduce(self, send, recv=None, algo: str = "auto", variant: str = "", stream=None):
+        import torch
+        recv = torch.empty_like(send) if recv is None else recv
+        aid = -1 if algo == "auto" else _algo_id("allreduce", algo, variant)
+        self._call(_lib.lib().cfAllReduce, send, recv, send.numel(), aid, stream)
+        return recv
+
+    def all_gather(self, send, recv=None, algo: str = "auto", stream=None):
+        import torch
+        recv = send.new_empty(send.numel() * self.nranks) if recv is None else recv
+        aid = -1 if algo == "auto" else _algo_id("allgather", algo, "")
+        self._call(_lib.lib().cfAllGather, send, recv, send.numel(), aid, stream)
+        return recv
+
+    def reduce_scatter(self, send, recv=None, algo: str = "auto", stream=None):
+        if send.numel() % self.nranks:
+            raise ShapeError("reduce_scatter input must hold nranks equal shards")
+        recv = send.new_empty(send.numel() // self.nranks) if recv is None else recv
+        aid = -1 if algo == "auto" else _algo_id("reducescatter", algo, "")
+        self._call(_lib.lib().cfReduceScatter, send, recv, recv.numel(), aid, stream)
+        return recv
+
+    def check_device_error(self):
+        code = ctypes.c_int()
+        _lib.check(_lib.lib().cfCommLastDeviceError(self._comm, ctypes.byref(code)))
+        if code.value:
+            from .errors import raise_status
+            raise_status(code.value, "device-side wait timed out")
+
+    def close(self):
+        if self._comm is not None:
+            _lib.lib().cfCommDestroy(self._comm)
+            self._comm = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(512) pull_reduce_kernel(const __grid_constant_
   constexpr int V = Vec<T>::N;
   const int n = a.n, r = rk.rank;
   const uint64_t e = begin_call(rk);
-  handshake(rk, n, e * 4 + 1, false, a.gpu_scope);
+  if (!a.single_launch) handshake(rk, n, e * 4 + 1, false, a.gpu_scope);
 
   size_t lo = 0, hi = a.count;
   if (!a.whole) {
@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(512) pull_reduce_kernel(const __grid_constant_
       store_vec<T>(rk.out[r], v, res, lo, hi, shift);
     }
   }
-  handshake(rk, n, e * 4 + 2, true, a.gpu_scope);
+  if (!a.single_launch) handshake(rk, n, e * 4 + 2, true, a.gpu_scope);
   end_call(rk, e);
 }
 
@@ -201,17 +201,33 @@ __global__ void __launch_bounds__(512) ll_oneshot_kernel(const __grid_constant__
     }
   }
   for (size_t v = t0; v < nvec; v += stride) {
+    // issue every peer's two packets first (2(n-1) loads in flight), then
+    // re-poll only the packets whose flags were not yet stamped
+    uint4 raw0[NR], raw1[NR];
+#pragma unroll
+    for (int k = 0; k < NR; k++) {
+      if (k < n) {
+        const int q = order_src(a.order, k, lead, n);
+        if (q != r) {
+          const char* s = rk.scr[r] + par + (size_t)q * a.slot + v * 32;
+          raw0[k] = ld16_volatile(s);
+          raw1[k] = ld16_volatile(s + 16);
+        }
+      }
+    }
+    const uint4 own = load_vec<T>(rk.in[r], v, a.count);
     uint4 x[NR];
 #pragma unroll
     for (int k = 0; k < NR; k++) {
       if (k < n) {
         const int q = order_src(a.order, k, lead, n);
         if (q == r) {
-          x[k] = load_vec<T>(rk.in[r], v, a.count);
+          x[k] = own;
         } else {
           const char* s = rk.scr[r] + par + (size_t)q * a.slot + v * 32;
-          const uint2 p0 = ll16_get(s, flag, rk.st);
-          const uint2 p1 = ll16_get(s + 16, flag, rk.st);
+          uint2 p0 = make_uint2(raw0[k].x, raw0[k].z), p1 = make_uint2(raw1[k].x, raw1[k].z);
+          if (raw0[k].y != flag || raw0[k].w != flag) p0 = ll16_get(s, flag, rk.st);
+          if (raw1[k].y != flag || raw1[k].w != flag) p1 = ll16_get(s + 16, flag, rk.st);
           x[k] = make_uint4(p0.x, p0.y, p1.x, p1.y);
         }
       }
@@ -312,7 +328,7 @@ __global__ void __launch_bounds__(512) push_gather_kernel(const __grid_constant_
   constexpr int V = 16 / sizeof(T);
   const int n = a.n, r = rk.rank;
   const uint64_t e = begin_call(rk);
-  handshake(rk, n, e * 4 + 1, false, a.gpu_scope);
+  if (!a.single_launch) handshake(rk, n, e * 4 + 1, false, a.gpu_scope);
   const size_t stride = (size_t)gridDim.x * blockDim.x;
   const size_t t0 = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   const size_t sb = a.count * sizeof(T);
@@ -333,7 +349,7 @@ __global__ void __launch_bounds__(512) push_gather_kernel(const __grid_constant_
         store_vec<T>(rk.out[p] + (size_t)r * sb, v, x, 0, a.count, 0);
     }
   }
-  handshake(rk, n, e * 4 + 2, true, a.gpu_scope);
+  if (!a.single_launch) handshake(rk, n, e * 4 + 2, true, a.gpu_scope);
   end_call(rk, e);
 }
 

@@ -31,6 +31,9 @@ struct CollArgs {
   int whole;        // pull-reduce: each rank reduces [0,count) instead of its chunk
   int rs_shift;     // pull-reduce: recv is the shard (offset by -chunk start)
   int gpu_scope;    // every rank on this device: .gpu-scope release/acquire suffice
+  int single_launch;// every rank runs in this one launch: stream order already provides the
+                    // entry (inputs produced, outputs free) and exit (no peer still reading)
+                    // guarantees, so the HB kernels skip their handshakes
   size_t count;     // elements per rank (AR/RS: send elements; AG: shard elements)
   size_t cs;        // reference chunk size in elements (cf/collectives.py:170-172)
   size_t slot;      // LL slot stride in bytes

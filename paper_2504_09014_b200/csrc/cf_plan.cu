@@ -814,6 +814,14 @@ extern "C" cfStatus cfPlanExecute(cfPlan_t pl, const void* const* inputs, void* 
     a.out_buf = pl->out_buf;
     a.input_private = pl->input_private ? 1 : 0;
     a.gpu_scope = pl->groups.size() == 1 ? 1 : 0;
+    // One launch holding every rank: the kernel boundary already separates
+    // calls, so only a prologue that zeroes / copies buffers peers touch needs
+    // the entry barrier, and no exit barrier is needed.
+    const bool single = pl->groups.size() == 1 && (int)c->local.size() == n;
+    bool prologue = pl->input_private;
+    for (auto& z : pl->zero_bufs) prologue |= !z.empty();
+    a.entry_barrier = (!single || prologue) ? 1 : 0;
+    a.exit_barrier = single ? 0 : 1;
     a.flag_stride = pl->flag_stride;
     for (size_t b = 0; b < pl->ir.bufs.size(); b++) a.buf_bytes[b] = (uint64_t)pl->ir.bufs[b].elems * pl->es;
     for (int r = 0; r < n; r++) {

@@ -121,6 +121,8 @@ struct PlanArgs {
   int in_buf, out_buf;
   int input_private;           // 1: plan writes its input -> copy user input into the plan buffer
   int gpu_scope;               // every rank on this device: .gpu-scope release/acquire
+  int entry_barrier;           // rank barrier after the prologue (zeroing / private input)
+  int exit_barrier;            // rank barrier at the end (not needed when one launch holds every rank)
   uint32_t flag_stride;
   uint64_t buf_bytes[16];      // byte size of each buffer (<= 16 buffers)
   char* io_in[CF_MAX_RANKS];

@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(512) plan_kernel(const __grid_constant__ PlanA
   __syncthreads();
   const uint64_t e = s_e;
   prologue(a, rank);
-  rank_barrier(a, rank, 2 * e - 1);
+  if (a.entry_barrier) rank_barrier(a, rank, 2 * e - 1);
   const int end = a.prog_end[pid];
   for (int i = a.prog_begin[pid]; i < end; i++) {
     const DevOp& op = a.ops[i];
@@ -294,7 +294,8 @@ __global__ void __launch_bounds__(512) plan_kernel(const __grid_constant__ PlanA
         break;
     }
   }
-  rank_barrier(a, rank, 2 * e);
+  if (a.exit_barrier) rank_barrier(a, rank, 2 * e);
+  __syncthreads();
   if (threadIdx.x == 0) {
     const uint32_t prev = atomicAdd(&rs->arrive, 1u);
     if (prev == (uint32_t)a.rank_ctas[rank] - 1) {

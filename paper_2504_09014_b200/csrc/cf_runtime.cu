@@ -11,6 +11,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <unistd.h>
+#include <cuda.h>
 #include "cf_runtime.h"
 
 namespace cf {
@@ -76,6 +77,17 @@ cfStatus join_streams(cfComm* c, int group, const cudaStream_t* streams, bool af
     }
   }
   return CF_OK;
+}
+
+// Driver API entry points resolved through the runtime, so libcf.so has no
+// link-time dependency on libcuda (it loads on GPU-less build hosts).
+void* driver_fn(const char* name) {
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &fn, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess)
+    return nullptr;
+  return fn;
 }
 
 // Restores the caller's current device on scope exit.
@@ -315,13 +327,14 @@ extern "C" cfStatus cfCommConnect(cfComm_t c, const void* handles, size_t bytes_
   return CF_OK;
 }
 
+static void release_reg(cfComm* c, const Registration& r);
+
 extern "C" cfStatus cfCommDestroy(cfComm_t c) {
   if (!c) return CF_OK;
   DeviceGuard guard;
-  for (void* p : c->ipc_opened) {
-    if (!c->local.empty()) cudaSetDevice(c->local[0].dev);
-    cudaIpcCloseMemHandle(p);
-  }
+  if (!c->local.empty()) cudaSetDevice(c->local[0].dev);
+  for (auto& r : c->regs) release_reg(c, r);
+  for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
   for (auto& lr : c->local) {
     if (lr.dev >= 0) cudaSetDevice(lr.dev);
     if (lr.heap) cudaFree(lr.heap);
@@ -329,6 +342,103 @@ extern "C" cfStatus cfCommDestroy(cfComm_t c) {
   }
   delete c;
   return CF_OK;
+}
+
+// ---------------------------------------------------------------- registration
+
+namespace {
+struct BufferBlob {
+  uint32_t magic;
+  int32_t rank;
+  uint64_t offset;   // ptr - allocation base
+  uint64_t bytes;
+  cudaIpcMemHandle_t ipc;
+};
+constexpr uint32_t kBufMagic = 0x43464231;  // "CFB1"
+static_assert(sizeof(BufferBlob) <= CF_BUFFER_HANDLE_BYTES, "buffer handle too large");
+}  // namespace
+
+extern "C" cfStatus cfBufferExport(cfComm_t c, const void* ptr, size_t bytes, void* handle) {
+  if (!c || !ptr || !handle) return fail(CF_E_CONFIG, "null argument");
+  memset(handle, 0, CF_BUFFER_HANDLE_BYTES);
+  if (!c->multiprocess) return CF_OK;
+  DeviceGuard guard;
+  CF_CUDA(cudaSetDevice(c->local[0].dev));
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  auto get_range = (CUresult(*)(CUdeviceptr*, size_t*, CUdeviceptr))driver_fn("cuMemGetAddressRange");
+  if (!get_range) return fail(CF_E_CUDA, "driver entry point cuMemGetAddressRange unavailable");
+  if (get_range(&base, &size, (CUdeviceptr)ptr) != CUDA_SUCCESS)
+    return fail(CF_E_CUDA, "cuMemGetAddressRange(%p) failed: not device memory", ptr);
+  if ((const char*)ptr + bytes > (const char*)base + size)
+    return fail(CF_E_OOB, "registered range exceeds its allocation");
+  BufferBlob b{};
+  b.magic = kBufMagic;
+  b.rank = c->local[0].rank;
+  b.offset = (uint64_t)((const char*)ptr - (const char*)base);
+  b.bytes = bytes;
+  CF_CUDA(cudaIpcGetMemHandle(&b.ipc, (void*)base));
+  memcpy(handle, &b, sizeof(b));
+  return CF_OK;
+}
+
+extern "C" cfStatus cfBufferImport(cfComm_t c, const void* ptr, const void* handles, size_t stride) {
+  if (!c || !ptr || !handles) return fail(CF_E_CONFIG, "null argument");
+  if (!c->multiprocess) return CF_OK;
+  if (stride < sizeof(BufferBlob)) return fail(CF_E_BAD_SIZE, "buffer handle stride too small");
+  DeviceGuard guard;
+  CF_CUDA(cudaSetDevice(c->local[0].dev));
+  const int me = c->local[0].rank;
+  Registration reg;
+  reg.ptr = (const char*)ptr;
+  for (int p = 0; p < c->nranks; p++) {
+    BufferBlob b;
+    memcpy(&b, (const char*)handles + (size_t)p * stride, sizeof(b));
+    if (b.magic != kBufMagic || b.rank != p) return fail(CF_E_RANK_MISMATCH, "buffer handle %d is not rank %d's", p, p);
+    if (p == me) {
+      reg.bytes = b.bytes;
+      reg.peer[p] = (char*)ptr;
+      continue;
+    }
+    std::string key(std::to_string(p) + ":" + std::string((const char*)&b.ipc, sizeof(b.ipc)));
+    auto it = c->ipc_cache.find(key);
+    if (it == c->ipc_cache.end()) {
+      void* mapped = nullptr;
+      CF_CUDA(cudaIpcOpenMemHandle(&mapped, b.ipc, cudaIpcMemLazyEnablePeerAccess));
+      it = c->ipc_cache.emplace(key, IpcMapping{mapped, 0}).first;
+    }
+    it->second.refs++;
+    reg.keys.push_back(key);
+    reg.peer[p] = (char*)it->second.base + b.offset;
+  }
+  for (auto& r : c->regs)
+    if (r.ptr == reg.ptr) return fail(CF_E_CONFIG, "buffer %p registered twice", ptr);
+  c->regs.push_back(reg);
+  return CF_OK;
+}
+
+static void release_reg(cfComm* c, const Registration& r) {
+  for (auto& k : r.keys) {
+    auto it = c->ipc_cache.find(k);
+    if (it != c->ipc_cache.end() && --it->second.refs == 0) {
+      cudaIpcCloseMemHandle(it->second.base);
+      c->ipc_cache.erase(it);
+    }
+  }
+}
+
+extern "C" cfStatus cfBufferRelease(cfComm_t c, const void* ptr) {
+  if (!c) return fail(CF_E_CONFIG, "null argument");
+  if (!c->multiprocess) return CF_OK;
+  DeviceGuard guard;
+  cudaSetDevice(c->local[0].dev);
+  for (size_t i = 0; i < c->regs.size(); i++)
+    if (c->regs[i].ptr == (const char*)ptr) {
+      release_reg(c, c->regs[i]);
+      c->regs.erase(c->regs.begin() + i);
+      return CF_OK;
+    }
+  return fail(CF_E_OOB, "buffer %p is not registered", ptr);
 }
 
 extern "C" cfStatus cfCommNumRanks(cfComm_t c, int* n) {
@@ -414,10 +524,18 @@ cfStatus check_ptrs(cfComm* c, const void* const* send, void* const* recv, const
 
 cfStatus launch(cfComm* c, const Job& j, int dtype, const void* const* send, void* const* recv,
                 const cudaStream_t* streams) {
-  if (c->multiprocess && j.kind != kLL1 && j.kind != kLL2)
-    return fail(CF_E_TOPOLOGY,
-                "HB algorithms in one-process-per-GPU mode need registered buffers (not in this build); "
-                "use an LL algorithm");
+  // one-process-per-GPU: peers' buffers come from the registration table
+  const bool need_in = j.kind == kPull, need_out = j.kind == kGather || (j.kind == kPull && j.push);
+  const Registration* reg_in = nullptr;
+  const Registration* reg_out = nullptr;
+  if (c->multiprocess) {
+    if (need_in && !(reg_in = c->find_reg(send[0])))
+      return fail(CF_E_TOPOLOGY, "send buffer %p is not registered (cfBufferExport/cfBufferImport); "
+                                 "HB algorithms read it from the peers", send[0]);
+    if (need_out && !(reg_out = c->find_reg(recv[0])))
+      return fail(CF_E_TOPOLOGY, "recv buffer %p is not registered (cfBufferExport/cfBufferImport); "
+                                 "HB algorithms write it from the peers", recv[0]);
+  }
   DeviceGuard guard;
   const void* kernel = collective_kernel(j.kind, dtype, c->nranks);
   if (!kernel) return fail(CF_E_INTERNAL, "no kernel for kind %d dtype %d", j.kind, dtype);
@@ -435,6 +553,7 @@ cfStatus launch(cfComm* c, const Job& j, int dtype, const void* const* send, voi
     a.whole = j.whole;
     a.rs_shift = j.rs_shift;
     a.gpu_scope = (c->groups.size() == 1 && !c->multiprocess) ? 1 : 0;
+    a.single_launch = (c->groups.size() == 1 && !c->multiprocess && (int)g.size() == c->nranks) ? 1 : 0;
     a.count = j.count;
     a.cs = j.cs;
     a.slot = j.slot ? j.slot : c->lay.slot;
@@ -452,6 +571,10 @@ cfStatus launch(cfComm* c, const Job& j, int dtype, const void* const* send, voi
         rk.sem[p] = c->sem(li, p);
       }
       if (c->multiprocess) {
+        for (int p = 0; p < c->nranks; p++) {
+          if (reg_in) rk.in[p] = reg_in->peer[p] + ((const char*)send[li] - reg_in->ptr);
+          if (reg_out) rk.out[p] = reg_out->peer[p] + ((char*)recv[li] - reg_out->ptr);
+        }
         rk.in[rk.rank] = (const char*)send[li];
         rk.out[rk.rank] = (char*)recv[li];
       }

@@ -52,8 +52,18 @@ struct LocalRank {
   cudaEvent_t ev = nullptr;   // stream joins for co-resident ranks
 };
 
-struct Occupancy {
-  int blocks_per_sm = 0;
+// A registered buffer range (one-process-per-GPU mode) and the peers' mapped
+// counterparts.
+struct Registration {
+  const char* ptr = nullptr;
+  size_t bytes = 0;
+  std::array<char*, CF_MAX_RANKS> peer{};
+  std::vector<std::string> keys;   // ipc cache keys held by this registration
+};
+
+struct IpcMapping {
+  void* base = nullptr;
+  int refs = 0;
 };
 
 }  // namespace cf
@@ -70,6 +80,8 @@ struct cfComm {
   // local-rank indices grouped by device (one launch per group)
   std::vector<std::vector<int>> groups;
   std::vector<void*> ipc_opened;       // cudaIpcOpenMemHandle mappings to close
+  std::vector<cf::Registration> regs;  // registered user buffers (multi-process)
+  std::map<std::string, cf::IpcMapping> ipc_cache;  // peer allocation -> mapping
   std::map<int, int> sm_count;         // device -> SMs
   std::map<std::pair<const void*, int>, int> occ;  // (kernel, device) -> CTAs/SM
   bool multicast_supported = false;
@@ -78,11 +90,19 @@ struct cfComm {
   uint64_t* sem(int li, int p) const { return (uint64_t*)(peer_heap[li][p] + lay.sem_off); }
   char* scr(int li, int p) const { return peer_heap[li][p] + lay.scr_off; }
   uint64_t* plan_sem(int li, int p) const { return (uint64_t*)(peer_heap[li][p] + lay.plan_sem_off); }
+  // registered range containing p (nullptr if none)
+  const cf::Registration* find_reg(const void* p) const {
+    for (auto& r : regs)
+      if ((const char*)p >= r.ptr && (const char*)p < r.ptr + r.bytes) return &r;
+    return nullptr;
+  }
 };
 
 namespace cf {
 // CTAs of `kernel` (launched with `threads`) that may run per SM on `dev`.
 int occupancy(cfComm* c, const void* kernel, int dev, int threads);
+// Driver API function by name (nullptr if unavailable).
+void* driver_fn(const char* name);
 // Co-residency cap: CTAs per rank such that every rank of the group fits at once.
 int max_blocks_per_rank(cfComm* c, const void* kernel, int group, int threads);
 // Make streams[first] of the group wait for the others; after the launch, the

@@ -1,0 +1,99 @@
+"""One process per rank (the real-deployment mode), two ranks sharing cuda:0:
+gloo bootstrap, IPC-mapped symmetric heaps, registered torch buffers, every
+collective kernel vs the oracle.  (On an 8-GPU box the same code runs one
+rank per GPU over NVLink.)"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, q):
+    try:
+        import sys
+        root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+        sys.path[:0] = [root, os.path.join(root, "tests", "golden")]
+        import torch
+        import torch.distributed as dist
+        from inputs import gen_inputs
+        from paper_2504_09014_b200.comm import Communicator
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                                world_size=world)
+        comm = Communicator(spin_timeout_ms=60000)
+        out = {}
+        for elems in (1000, 65536 + 8):
+            ins = gen_inputs(world, elems, "f32", "wide", 77 + elems)
+            send = torch.from_numpy(ins[rank]).cuda()
+            recv = torch.empty_like(send)
+            comm.register(send)
+            comm.register(recv)
+            for algo in ("1pa", "2pa", "2pa_ll", "1pa_hb"):
+                name, var = (algo, "") if algo != "2pa_ll" else ("2pa", "ll")
+                comm.all_reduce(send, recv, algo=name, variant=var)
+                torch.cuda.synchronize()
+                out[("ar", algo, elems)] = recv.cpu().numpy().copy()
+            ag = torch.empty(world * elems, device="cuda", dtype=torch.float32)
+            comm.register(ag)
+            comm.all_gather(send, ag, algo="allpairs_ag")
+            torch.cuda.synchronize()
+            out[("ag", elems)] = ag.cpu().numpy().copy()
+            rs_in = torch.from_numpy(np.concatenate([ins[rank]] * world)).cuda()
+            rs_out = torch.empty(elems, device="cuda", dtype=torch.float32)
+            comm.register(rs_in)
+            comm.reduce_scatter(rs_in, rs_out, algo="rs_direct")
+            torch.cuda.synchronize()
+            out[("rs", elems)] = rs_out.cpu().numpy().copy()
+            for t in (send, recv, ag, rs_in):
+                comm.deregister(t)
+        comm.check_device_error()
+        comm.close()
+        dist.barrier()
+        dist.destroy_process_group()
+        q.put((rank, out, None))
+    except Exception as e:  # report instead of hanging the parent
+        import traceback
+        q.put((rank, None, traceback.format_exc()))
+
+
+def test_two_processes_one_gpu_all_collectives():
+    from oracle import oracle
+    from inputs import gen_inputs
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        r, out, err = q.get(timeout=600)
+        assert err is None, err
+        res[r] = out
+    for p in procs:
+        p.join(timeout=60)
+    for elems in (1000, 65536 + 8):
+        ins = gen_inputs(world, elems, "f32", "wide", 77 + elems)
+        for algo in ("1pa", "2pa", "2pa_ll", "1pa_hb"):
+            want = oracle.allreduce(ins, {"2pa_ll": "2pa", "1pa_hb": "1pa"}.get(algo, algo), "f32")
+            for r in range(world):
+                assert np.array_equal(res[r][("ar", algo, elems)].view(np.uint32),
+                                      want[r].view(np.uint32)), (algo, r, elems)
+        cat = np.concatenate(ins)
+        rs_ins = [np.concatenate([x] * world) for x in ins]
+        rs_want = oracle.reducescatter(rs_ins, "direct", "f32")
+        for r in range(world):
+            assert np.array_equal(res[r][("ag", elems)], cat)
+            assert np.array_equal(res[r][("rs", elems)].view(np.uint32), rs_want[r].view(np.uint32))
