@@ -210,6 +210,51 @@ def time_coll(world, kind, send, recv, count, dtype, algo, iters, warmup, flush=
     return max(t, 0.0) / iters
 
 
+def time_plan(rt, send, recv, iters, warmup, flush, reps=3):
+    """time_coll for a plan Runtime (CUDA graph of `iters` executions)."""
+    import torch
+    dev = rt.world.device(0)
+    for _ in range(warmup):
+        rt.run_raw(send, recv)
+    rt.world.synchronize()
+
+    def capture(with_plan):
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream(dev)
+        s.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(g, stream=s):
+                for _ in range(iters):
+                    if flush is not None:
+                        flush.zero_()
+                    if with_plan:
+                        rt.run_raw(send, recv)
+        torch.cuda.synchronize(dev)
+        return g
+
+    def replay(g):
+        g.replay()
+        torch.cuda.synchronize(dev)
+        best = None
+        for _ in range(reps):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            st = torch.cuda.current_stream(dev)
+            e0.record(st)
+            g.replay()
+            e1.record(st)
+            e1.synchronize()
+            t = e0.elapsed_time(e1) / 1e3
+            best = t if best is None else min(best, t)
+        return best
+
+    t = replay(capture(True))
+    if flush is not None:
+        t -= replay(capture(False))
+    rt.check_device_error()
+    return max(t, 0.0) / iters
+
+
 def run_gpu_arm(args):
     import torch
     from paper_2504_09014_b200 import _lib, make_world
@@ -350,6 +395,27 @@ def run_sweep(w, args):
                           count, "bf16", aid, iters, 3, flush if nb < 64 * MiB else None)
             row[name] = {"us": round(t * 1e6, 2), "busbw": round(busbw(nb, t, n), 2)}
         out.append(row)
+    # C5: Llama-70B TP-decode AllReduce [b, 8192] bf16 through lowered reference
+    # plans (tests/golden/plans, generated by the reference's lower()), K10.
+    from paper_2504_09014_b200 import Runtime, parse_plan
+    from paper_2504_09014_b200.plan import scale_plan
+    c5 = []
+    for pname in ("2pa_memory_n8_e64", "1pa_n8_e64"):
+        with open(os.path.join(ROOT, "tests", "golden", "plans", pname + ".json"), "rb") as f:
+            base = parse_plan(f.read())
+        for b in (1, 4, 16, 64, 256):
+            plan = scale_plan(base, 128 * b)
+            rt = Runtime(plan, w, dtype="bf16")
+            xs = [torch.randn(rt.in_elems, device=dev).to(torch.bfloat16) * 0.02 for _ in range(n)]
+            ys = [torch.empty(rt.out_elems, device=dev, dtype=torch.bfloat16) for _ in range(n)]
+            t = time_plan(rt, xs, ys, 20, 3, flush)
+            nb = rt.in_elems * 2
+            c5.append({"plan": pname.split("_n8")[0], "batch": b, "bytes": nb,
+                       "us": round(t * 1e6, 2), "busbw": round(busbw(nb, t, n), 2),
+                       "device_ops": rt.n_device_ops})
+            rt.close()
+    out.append({"config": "C5 Llama-70B TP decode AllReduce via DSL plans (K10), bf16, "
+                          "8 co-resident ranks", "rows": c5})
     # C1: fp32 1 MiB one-shot LL (8 simulated ranks)
     c1 = [torch.randn(MiB // 4, device=dev) for _ in range(n)]
     c1o = [torch.empty_like(x) for x in c1]

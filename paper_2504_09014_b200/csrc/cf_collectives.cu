@@ -200,40 +200,39 @@ __global__ void __launch_bounds__(512) ll_oneshot_kernel(const __grid_constant__
       }
     }
   }
+  (void)lead;
+  using A = typename Vec<T>::Acc;
   for (size_t v = t0; v < nvec; v += stride) {
     // issue every peer's two packets first (2(n-1) loads in flight), then
+    // accumulate in the 1pa order -- own input, then peers ascending -- and
     // re-poll only the packets whose flags were not yet stamped
-    uint4 raw0[NR], raw1[NR];
+    uint4 raw0[NR - 1], raw1[NR - 1];
 #pragma unroll
-    for (int k = 0; k < NR; k++) {
-      if (k < n) {
-        const int q = order_src(a.order, k, lead, n);
-        if (q != r) {
-          const char* s = rk.scr[r] + par + (size_t)q * a.slot + v * 32;
-          raw0[k] = ld16_volatile(s);
-          raw1[k] = ld16_volatile(s + 16);
-        }
+    for (int i = 0; i < NR - 1; i++) {
+      if (i < n - 1) {
+        const int q = i + (i >= r ? 1 : 0);
+        const char* s = rk.scr[r] + par + (size_t)q * a.slot + v * 32;
+        raw0[i] = ld16_volatile(s);
+        raw1[i] = ld16_volatile(s + 16);
       }
     }
-    const uint4 own = load_vec<T>(rk.in[r], v, a.count);
-    uint4 x[NR];
+    A acc[V];
+    Vec<T>::load(load_vec<T>(rk.in[r], v, a.count), acc);
 #pragma unroll
-    for (int k = 0; k < NR; k++) {
-      if (k < n) {
-        const int q = order_src(a.order, k, lead, n);
-        if (q == r) {
-          x[k] = own;
-        } else {
-          const char* s = rk.scr[r] + par + (size_t)q * a.slot + v * 32;
-          uint2 p0 = make_uint2(raw0[k].x, raw0[k].z), p1 = make_uint2(raw1[k].x, raw1[k].z);
-          if (raw0[k].y != flag || raw0[k].w != flag) p0 = ll16_get(s, flag, rk.st);
-          if (raw1[k].y != flag || raw1[k].w != flag) p1 = ll16_get(s + 16, flag, rk.st);
-          x[k] = make_uint4(p0.x, p0.y, p1.x, p1.y);
-        }
+    for (int i = 0; i < NR - 1; i++) {
+      if (i < n - 1) {
+        const int q = i + (i >= r ? 1 : 0);
+        const char* s = rk.scr[r] + par + (size_t)q * a.slot + v * 32;
+        uint2 p0 = make_uint2(raw0[i].x, raw0[i].z), p1 = make_uint2(raw1[i].x, raw1[i].z);
+        if (raw0[i].y != flag || raw0[i].w != flag) p0 = ll16_get(s, flag, rk.st);
+        if (raw1[i].y != flag || raw1[i].w != flag) p1 = ll16_get(s + 16, flag, rk.st);
+        A t[V];
+        Vec<T>::load(make_uint4(p0.x, p0.y, p1.x, p1.y), t);
+#pragma unroll
+        for (int j = 0; j < V; j++) acc[j] = acc_add(acc[j], t[j]);
       }
     }
-    const uint4 res = reduce_vecs<T, NR>(x, n, a.order != kLead);
-    store_vec<T>(rk.out[r], v, res, 0, a.count, 0);
+    store_vec<T>(rk.out[r], v, Vec<T>::store(acc), 0, a.count, 0);
   }
   end_call(rk, e);
 }

@@ -257,7 +257,9 @@ __global__ void __launch_bounds__(512) plan_kernel(const __grid_constant__ PlanA
   __syncthreads();
   const uint64_t e = s_e;
   prologue(a, rank);
-  if (a.entry_barrier) rank_barrier(a, rank, 2 * e - 1);
+  // rank barriers are numbered consecutively across calls (monotonic counters)
+  const uint64_t per_call = (uint64_t)(a.entry_barrier + a.exit_barrier);
+  if (a.entry_barrier) rank_barrier(a, rank, (e - 1) * per_call + 1);
   const int end = a.prog_end[pid];
   for (int i = a.prog_begin[pid]; i < end; i++) {
     const DevOp& op = a.ops[i];
@@ -294,7 +296,7 @@ __global__ void __launch_bounds__(512) plan_kernel(const __grid_constant__ PlanA
         break;
     }
   }
-  if (a.exit_barrier) rank_barrier(a, rank, 2 * e);
+  if (a.exit_barrier) rank_barrier(a, rank, e * per_call);
   __syncthreads();
   if (threadIdx.x == 0) {
     const uint32_t prev = atomicAdd(&rs->arrive, 1u);

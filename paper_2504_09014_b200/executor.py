@@ -105,6 +105,13 @@ class Runtime:
                                             _lib.ptr_array([t.data_ptr() for t in recv]),
                                             _lib.ptr_array(self.world.streams())))
 
+    def check_device_error(self):
+        """Synchronize and raise DeadlockError if a device wait of this plan timed out."""
+        code = ctypes.c_int()
+        _lib.check(_lib.lib().cfPlanLastDeviceError(self._plan, ctypes.byref(code)))
+        if code.value:
+            raise DeadlockError(message="plan execution timed out on the device")
+
     def _static_trace(self):
         ev = []
         for p in sorted(self.plan.programs, key=lambda q: (q.rank, q.tb)):
