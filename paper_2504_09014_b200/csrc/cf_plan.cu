@@ -661,16 +661,57 @@ cfStatus load(cfComm* c, const char* json, size_t len, int dtype_override, cfPla
         const R& pay = o.code == D_PUT_PACKETS ? o.src[0] : o.dst[0];
         if ((pay.off * es) % 8 == 0 && (o.size * es) % 8 == 0) d.flags |= F_LL16;
       }
+      DevOp* prev = dv.empty() ? nullptr : &dv.back();
       switch (o.code) {
-        case D_SIGNAL:
-          d.id = o.chan;
-          d.peer = o.peer;
+        case D_SIGNAL:   // consecutive signals batch into one op (one thread per signal)
+          if (prev && prev->code == D_SIGNAL && prev->ndst < kMaxDst) {
+            prev->dst[prev->ndst++] = {o.chan, o.peer, 0};
+            continue;
+          }
+          d.ndst = 1;
+          d.dst[0] = {o.chan, o.peer, 0};
           break;
-        case D_WAIT:
-          d.id = o.chan;
-          d.m = (uint64_t)(++wm[o.chan]);
-          d.per_call = (uint64_t)sig[o.chan];
+        case D_WAIT: {   // consecutive waits batch into one op (polled in parallel)
+          const DRef w = {o.chan, (int32_t)sig[o.chan], (uint64_t)(++wm[o.chan])};
+          if (prev && prev->code == D_WAIT && prev->nsrc < kMaxSrc) {
+            prev->src[prev->nsrc++] = w;
+            continue;
+          }
+          d.nsrc = 1;
+          d.src[0] = w;
           break;
+        }
+        case D_PUT_PACKETS:   // same payload to several peers: one load, ndst packet stores
+          if (prev && prev->code == D_PUT_PACKETS && prev->size == d.size && prev->llflag == d.llflag &&
+              prev->ndst < kMaxDst && (prev->flags & F_LL16) == (d.flags & F_LL16) &&
+              prev->src[0].buf == d.src[0].buf && prev->src[0].rank == d.src[0].rank &&
+              prev->src[0].off == d.src[0].off) {
+            prev->dst[prev->ndst++] = d.dst[0];
+            continue;
+          }
+          break;
+        case D_READ_PACKETS: {  // several packet ranges drained together, loads in flight
+          d.llflag_k[0] = d.llflag;
+          bool ok = prev && prev->code == D_READ_PACKETS && prev->size == d.size && prev->nsrc < kMaxDst &&
+                    (prev->flags & F_LL16) == (d.flags & F_LL16);
+          if (ok) {  // no range of the batch may overlap another's (order-free merge)
+            const long long len_pkt = 2 * d.size * es, len_pay = d.size * es;
+            auto ovl = [](const DRef& x, long long lx, const DRef& y, long long ly) {
+              return x.buf == y.buf && x.rank == y.rank && (long long)x.off < (long long)y.off + ly &&
+                     (long long)y.off < (long long)x.off + lx;
+            };
+            for (int k = 0; k < prev->nsrc && ok; k++)
+              ok = !ovl(prev->dst[k], len_pay, d.dst[0], len_pay) && !ovl(prev->dst[k], len_pay, d.src[0], len_pkt) &&
+                   !ovl(d.dst[0], len_pay, prev->src[k], len_pkt);
+          }
+          if (ok) {
+            prev->llflag_k[prev->nsrc] = d.llflag;
+            prev->src[prev->nsrc++] = d.src[0];
+            prev->dst[prev->ndst++] = d.dst[0];
+            continue;
+          }
+          break;
+        }
         case D_SYNC_GROUP:
           d.id = o.chan;
           d.m = (uint64_t)o.peer;

@@ -98,8 +98,12 @@ struct DevOp {
   uint64_t m;          // wait / barrier: 1-based occurrence within the call
   uint64_t per_call;   // wait: signals per call on the channel; barrier: occurrences per call
   uint64_t members;    // barrier: participating CTAs
+  // data ops: buffer references.  Batched sync ops reuse the slots:
+  //   D_SIGNAL  dst[k] = {channel, receiving rank, -}     (ndst signals)
+  //   D_WAIT    src[k] = {channel, signals per call, m}   (nsrc waits)
   DRef src[kMaxSrc];
   DRef dst[kMaxDst];
+  uint32_t llflag_k[kMaxDst];  // D_READ_PACKETS batch: plan flag of source k
 };
 
 // Per-rank execution state of one loaded plan (in the plan heap of the rank).

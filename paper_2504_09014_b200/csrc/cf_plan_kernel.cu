@@ -182,40 +182,60 @@ __device__ void packet_op(const PlanArgs& a, const DevOp& op, int j, uint64_t e,
   const uint64_t per = ((size + a.K - 1) / a.K + V - 1) / V * V;
   const uint64_t lo = min((uint64_t)j * per, size), hi = min(lo + per, size);
   if (lo >= hi) return;
-  const uint32_t flag = runtime_flag(e, a.flag_stride, op.llflag);
-  const char* src = ref_ptr(a, op.src[0]);
-  char* dst = ref_ptr(a, op.dst[0]);
   const bool put = op.code == D_PUT_PACKETS;
+  // batched ops: a put sends one payload to ndst packet ranges (one plan op
+  // each); a read drains nsrc packet ranges into nsrc payload ranges
+  const int nb = put ? op.ndst : op.nsrc;
   if (op.flags & F_LL16) {
     const uint64_t u0 = lo * sizeof(T) / 8, u1 = (hi * sizeof(T) + 7) / 8;
-    for (uint64_t u = u0 + threadIdx.x; u < u1; u += blockDim.x) {
-      if (put) {
+    if (put) {
+      const uint32_t flag = runtime_flag(e, a.flag_stride, op.llflag);
+      const char* src = ref_ptr(a, op.src[0]);
+      for (uint64_t u = u0 + threadIdx.x; u < u1; u += blockDim.x) {
         const uint2 d = *reinterpret_cast<const uint2*>(src + u * 8);
-        ll16_put(dst + u * 16, d, flag);
-      } else {
-        const uint2 d = ll16_get(src + u * 16, flag, rs);
-        *reinterpret_cast<uint2*>(dst + u * 8) = d;
+        for (int k = 0; k < nb; k++) ll16_put(ref_ptr(a, op.dst[k]) + u * 16, d, flag);
+      }
+    } else {
+      for (uint64_t u = u0 + threadIdx.x; u < u1; u += blockDim.x) {
+        uint4 raw[kMaxDst];
+#pragma unroll
+        for (int k = 0; k < kMaxDst; k++)   // all packets in flight first
+          if (k < nb) raw[k] = ld16_volatile(ref_ptr(a, op.src[k]) + u * 16);
+#pragma unroll
+        for (int k = 0; k < kMaxDst; k++) {
+          if (k < nb) {
+            const uint32_t flag = runtime_flag(e, a.flag_stride, op.llflag_k[k]);
+            uint2 d = make_uint2(raw[k].x, raw[k].z);
+            if (raw[k].y != flag || raw[k].w != flag) d = ll16_get(ref_ptr(a, op.src[k]) + u * 16, flag, rs);
+            *reinterpret_cast<uint2*>(ref_ptr(a, op.dst[k]) + u * 8) = d;
+          }
+        }
       }
     }
   } else {
     const uint64_t u0 = lo * sizeof(T) / 4, u1 = (hi * sizeof(T) + 3) / 4;
-    for (uint64_t u = u0 + threadIdx.x; u < u1; u += blockDim.x) {
-      if (put) {
-        const uint32_t d = *reinterpret_cast<const uint32_t*>(src + u * 4);
-        st8_volatile(dst + u * 8, make_uint2(d, flag));
-      } else {
-        uint2 v = ld8_volatile(src + u * 8);
-        if (v.y != flag) {
-          const uint64_t t0 = globaltimer();
-          for (uint32_t it = 1; v.y != flag; ++it) {
-            v = ld8_volatile(src + u * 8);
-            if ((it & 255u) == 0) {
-              if (*(volatile uint32_t*)&rs->error != kDevOk) break;
-              if (globaltimer() - t0 > rs->timeout_ns) { atomicExch(&rs->error, (uint32_t)kDevTimeout); break; }
+    for (int k = 0; k < nb; k++) {
+      const char* src = ref_ptr(a, op.src[put ? 0 : k]);
+      char* dst = ref_ptr(a, op.dst[k]);
+      const uint32_t flag = runtime_flag(e, a.flag_stride, put ? op.llflag : op.llflag_k[k]);
+      for (uint64_t u = u0 + threadIdx.x; u < u1; u += blockDim.x) {
+        if (put) {
+          const uint32_t d = *reinterpret_cast<const uint32_t*>(src + u * 4);
+          st8_volatile(dst + u * 8, make_uint2(d, flag));
+        } else {
+          uint2 v = ld8_volatile(src + u * 8);
+          if (v.y != flag) {
+            const uint64_t t0 = globaltimer();
+            for (uint32_t it = 1; v.y != flag; ++it) {
+              v = ld8_volatile(src + u * 8);
+              if ((it & 255u) == 0) {
+                if (*(volatile uint32_t*)&rs->error != kDevOk) break;
+                if (globaltimer() - t0 > rs->timeout_ns) { atomicExch(&rs->error, (uint32_t)kDevTimeout); break; }
+              }
             }
           }
+          *reinterpret_cast<uint32_t*>(dst + u * 4) = v.x;
         }
-        *reinterpret_cast<uint32_t*>(dst + u * 4) = v.x;
       }
     }
   }
@@ -271,17 +291,20 @@ __global__ void __launch_bounds__(512) plan_kernel(const __grid_constant__ PlanA
       case D_DEV_BARRIER:
         counter_barrier(a.bars[rank] + op.id, ((e - 1) * op.per_call + op.m) * op.members, rs);
         break;
-      case D_SIGNAL:
+      case D_SIGNAL:   // ndst consecutive signals, one thread each
         __syncthreads();
-        if (threadIdx.x == 0) {
+        if ((int)threadIdx.x < op.ndst) {
+          const DRef& s = op.dst[threadIdx.x];
           fence_publish(a.gpu_scope);
-          red_add_release(a.lanes[op.peer] + (size_t)op.id * a.K + j, 1, a.gpu_scope);
+          red_add_release(a.lanes[s.rank] + (size_t)s.buf * a.K + j, 1, a.gpu_scope);
         }
         break;
-      case D_WAIT:
-        if ((int)threadIdx.x < a.K)
-          wait_geq(a.lanes[rank] + (size_t)op.id * a.K + threadIdx.x, (e - 1) * op.per_call + op.m, rs,
+      case D_WAIT:     // nsrc consecutive waits x K lanes, polled in parallel
+        for (int t = threadIdx.x; t < op.nsrc * a.K; t += blockDim.x) {
+          const DRef& w = op.src[t / a.K];
+          wait_geq(a.lanes[rank] + (size_t)w.buf * a.K + (t % a.K), (e - 1) * (uint64_t)w.rank + w.off, rs,
                    a.gpu_scope);
+        }
         __syncthreads();
         break;
       case D_MULTI:
