@@ -102,6 +102,7 @@ typedef struct {
   int threads;              /* threads per CTA (0 = 512) */
   uint64_t spin_timeout_ns; /* device spin-wait timeout -> CF_E_DEADLOCK (0 = 10 s) */
   int use_multicast;        /* 1 = build NVLS multicast objects when supported */
+  size_t nvls_bytes;        /* per-rank NVLS staging region (input and output halves each; 0 = 64 MiB) */
 } cfConfig;
 
 /* cf/errors.py: the `.code` string of each class ("E_SHAPE", ...). */
@@ -133,6 +134,19 @@ CF_API cfStatus cfCommDestroy(cfComm_t comm);
 CF_API cfStatus cfBufferExport(cfComm_t comm, const void* ptr, size_t bytes, void* handle);
 CF_API cfStatus cfBufferImport(cfComm_t comm, const void* ptr, const void* handles, size_t bytes_per_handle);
 CF_API cfStatus cfBufferRelease(cfComm_t comm, const void* ptr);
+
+/* NVLS (SwitchChannel multimem, cf/channels.py:333-409) for the one-process-
+ * per-GPU mode, in phases the caller separates with bootstrap barriers:
+ *   rank 0: cfNvlsCreate -> POSIX fd of the multicast object, sent to every
+ *           other rank over a Unix socket (SCM_RIGHTS);
+ *   others: cfNvlsImport(fd);
+ *   all   : barrier, cfNvlsBind (binds and maps this rank's memory), barrier.
+ * cfCommInitAll communicators over distinct devices set NVLS up internally
+ * when cfConfig.use_multicast is set and every device supports multicast. */
+CF_API cfStatus cfDeviceMulticastSupported(int cuda_dev, int* supported);
+CF_API cfStatus cfNvlsCreate(cfComm_t comm, int* fd);
+CF_API cfStatus cfNvlsImport(cfComm_t comm, int fd);
+CF_API cfStatus cfNvlsBind(cfComm_t comm);
 
 CF_API cfStatus cfCommNumRanks(cfComm_t comm, int* nranks);
 CF_API cfStatus cfCommLocalRanks(cfComm_t comm, int* nlocal, int* ranks /* nullable, nlocal entries */);

@@ -29,7 +29,8 @@ ALGO_NAMES = {v: k for k, v in ALGOS.items()}
 EXPORTS = (
     "cfStatusCode", "cfLastErrorMessage", "cfVersion", "cfCommInitAll", "cfCommCreateRank",
     "cfCommGetHandle", "cfCommConnect", "cfCommDestroy", "cfBufferExport", "cfBufferImport",
-    "cfBufferRelease", "cfCommNumRanks", "cfCommLocalRanks",
+    "cfBufferRelease", "cfDeviceMulticastSupported", "cfNvlsCreate", "cfNvlsImport", "cfNvlsBind", "cfCommNumRanks",
+    "cfCommLocalRanks",
     "cfCommMulticastSupported", "cfCommLastDeviceError", "cfCommClearDeviceError", "cfAllReduce",
     "cfAllGather", "cfReduceScatter", "cfSelectAlgorithm", "cfPlanLoad", "cfPlanExecute",
     "cfPlanInfo", "cfPlanLastDeviceError", "cfPlanDestroy",
@@ -39,7 +40,7 @@ EXPORTS = (
 class cfConfig(ctypes.Structure):
     _fields_ = [("ll_max_bytes", ctypes.c_size_t), ("max_blocks", ctypes.c_int),
                 ("threads", ctypes.c_int), ("spin_timeout_ns", ctypes.c_uint64),
-                ("use_multicast", ctypes.c_int)]
+                ("use_multicast", ctypes.c_int), ("nvls_bytes", ctypes.c_size_t)]
 
 
 _lib = None
@@ -61,6 +62,10 @@ _PROTOS = {
     "cfBufferExport": ([vp, vp, sz, vp], i32),
     "cfBufferImport": ([vp, vp, vp, sz], i32),
     "cfBufferRelease": ([vp, vp], i32),
+    "cfDeviceMulticastSupported": ([i32, P(i32)], i32),
+    "cfNvlsCreate": ([vp, P(i32)], i32),
+    "cfNvlsImport": ([vp, i32], i32),
+    "cfNvlsBind": ([vp], i32),
     "cfCommNumRanks": ([vp, P(i32)], i32),
     "cfCommLocalRanks": ([vp, P(i32), P(i32)], i32),
     "cfCommMulticastSupported": ([vp, P(i32)], i32),

@@ -103,6 +103,57 @@ class Communicator:
         self._call(_lib.lib().cfReduceScatter, send, recv, recv.numel(), aid, stream)
         return recv
 
+    def setup_nvls(self) -> bool:
+        """Collective: build the NVLS multicast object (SwitchChannel).  Rank 0
+        creates it and passes its POSIX fd to the other ranks over a Unix
+        socket (SCM_RIGHTS); every rank then binds and maps its memory.  All
+        ranks must share one host.  Returns False (on every rank) when any
+        GPU lacks multicast support."""
+        import os
+        import socket
+        import tempfile
+        import torch.distributed as dist
+        L = _lib.lib()
+        ok = self._multicast_capable()
+        flags = [None] * self.nranks
+        dist.all_gather_object(flags, ok, group=self.group)
+        if not all(flags):
+            return False
+        path = None
+        if self.rank == 0:
+            fd = ctypes.c_int(-1)
+            _lib.check(L.cfNvlsCreate(self._comm, ctypes.byref(fd)))
+            path = os.path.join(tempfile.mkdtemp(prefix="cf_nvls_"), "sock")
+            srv = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+            srv.bind(path)
+            srv.listen(self.nranks)
+        box = [path]
+        dist.broadcast_object_list(box, src=0, group=self.group)
+        if self.rank == 0:
+            for _ in range(self.nranks - 1):
+                conn, _ = srv.accept()
+                socket.send_fds(conn, [b"f"], [fd.value])
+                conn.close()
+            srv.close()
+        else:
+            cli = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+            cli.connect(box[0])
+            _, fds, _, _ = socket.recv_fds(cli, 1, 1)
+            cli.close()
+            _lib.check(L.cfNvlsImport(self._comm, fds[0]))
+            os.close(fds[0])
+        dist.barrier(group=self.group)          # every device added before any bind
+        _lib.check(L.cfNvlsBind(self._comm))
+        dist.barrier(group=self.group)
+        if self.rank == 0:
+            os.close(fd.value)
+            os.unlink(path)
+        return True
+
+    def _multicast_capable(self) -> bool:
+        from .world import device_multicast_capable
+        return device_multicast_capable(self.device.index)
+
     def check_device_error(self):
         code = ctypes.c_int()
         _lib.check(_lib.lib().cfCommLastDeviceError(self._comm, ctypes.byref(code)))

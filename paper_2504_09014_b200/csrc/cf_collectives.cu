@@ -352,6 +352,72 @@ __global__ void __launch_bounds__(512) push_gather_kernel(const __grid_constant_
   end_call(rk, e);
 }
 
+// ---------------------------------------------------------------- K5
+
+// NVLS AllReduce (build_switch_2pa, cf/collectives.py:235-250): the send
+// buffers were copied into each rank's multicast-bound input half; after the
+// entry handshake rank r's CTAs multimem.ld_reduce their slice of chunk r (the
+// NVSwitch sums the same address over every member, f16/bf16 accumulating in
+// f32) and multimem.st the result into every member's output half; the exit
+// handshake publishes it.  rk.in[rank] / rk.out[rank] hold the multicast
+// addresses of the two halves.
+template <typename T>
+__device__ __forceinline__ uint4 multimem_ld_reduce(const void* p);
+template <>
+__device__ __forceinline__ uint4 multimem_ld_reduce<float>(const void* p) {
+  uint4 v;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p) : "memory");
+  return v;
+}
+template <>
+__device__ __forceinline__ uint4 multimem_ld_reduce<__nv_bfloat16>(const void* p) {
+  uint4 v;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.bf16x2 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p) : "memory");
+  return v;
+}
+template <>
+__device__ __forceinline__ uint4 multimem_ld_reduce<__half>(const void* p) {
+  uint4 v;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.f16x2 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p) : "memory");
+  return v;
+}
+template <>
+__device__ __forceinline__ uint4 multimem_ld_reduce<int32_t>(const void* p) {
+  uint4 v;
+  const char* c = (const char*)p;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.u32 %0, [%1];" : "=r"(v.x) : "l"(c) : "memory");
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.u32 %0, [%1];" : "=r"(v.y) : "l"(c + 4) : "memory");
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.u32 %0, [%1];" : "=r"(v.z) : "l"(c + 8) : "memory");
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.u32 %0, [%1];" : "=r"(v.w) : "l"(c + 12) : "memory");
+  return v;
+}
+__device__ __forceinline__ void multimem_st16(void* p, uint4 v) {
+  asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y),
+               "r"(v.z), "r"(v.w) : "memory");
+}
+
+template <typename T>
+__global__ void __launch_bounds__(512) nvls_allreduce_kernel(const __grid_constant__ CollArgs a) {
+  const RankCtx& rk = a.rk[blockIdx.y];
+  constexpr int V = 16 / sizeof(T);
+  const int n = a.n, r = rk.rank;
+  const uint64_t e = begin_call(rk);
+  handshake(rk, n, e * 4 + 1, false, a.gpu_scope);
+  const size_t nvec = (a.count + V - 1) / V;       // staging halves are padded: whole vectors
+  const size_t cv = (nvec + n - 1) / n;
+  const size_t v0 = min((size_t)r * cv, nvec), v1 = min(v0 + cv, nvec);
+  const char* in = rk.in[r];
+  char* out = rk.out[r];
+  for (size_t v = v0 + (size_t)blockIdx.x * blockDim.x + threadIdx.x; v < v1;
+       v += (size_t)gridDim.x * blockDim.x)
+    multimem_st16(out + v * 16, multimem_ld_reduce<T>(in + v * 16));
+  handshake(rk, n, e * 4 + 2, true, a.gpu_scope);
+  end_call(rk, e);
+}
+
 // ---------------------------------------------------------------- launchers
 
 template <template <typename, int> class K> struct KernelTable;
@@ -404,6 +470,15 @@ const void* collective_kernel(int kind, int dtype, int n) {
         case 2: return (const void*)push_gather_kernel<__half>;
         case 3: return (const void*)push_gather_kernel<__nv_bfloat16>;
       }
+      break;
+    case 4:
+      switch (dtype) {
+        case 0: return (const void*)nvls_allreduce_kernel<int32_t>;
+        case 1: return (const void*)nvls_allreduce_kernel<float>;
+        case 2: return (const void*)nvls_allreduce_kernel<__half>;
+        case 3: return (const void*)nvls_allreduce_kernel<__nv_bfloat16>;
+      }
+      break;
   }
   return nullptr;
 }

@@ -113,6 +113,7 @@ static cfStatus alloc_heap(cfComm* c, LocalRank& lr) {
 
 static void apply_defaults(cfConfig* cfg) {
   if (cfg->ll_max_bytes == 0) cfg->ll_max_bytes = 4u << 20;
+  if (cfg->nvls_bytes == 0) cfg->nvls_bytes = 64u << 20;
   if (cfg->threads == 0) cfg->threads = 512;
   if (cfg->spin_timeout_ns == 0) {
     cfg->spin_timeout_ns = 10ull * 1000 * 1000 * 1000;
@@ -236,6 +237,19 @@ extern "C" cfStatus cfCommInitAll(cfComm_t* out, int nranks, const int* devs, co
   for (int li = 0; li < nranks; li++)
     for (int p = 0; p < nranks; p++) c->peer_heap[li][p] = c->local[p].heap;
   build_groups(c);
+  // NVLS needs one device per rank, each multicast-capable
+  bool mc_ok = c->groups.size() == (size_t)nranks;
+  for (int r = 0; r < nranks && mc_ok; r++) mc_ok = multicast_capable(devs[r]);
+  if (c->cfg.use_multicast && mc_ok) {
+    // a box that advertises multicast but cannot build the object (e.g. no
+    // fabric manager) keeps working: switch_2pa then runs the all-pairs kernel
+    if (nvls_setup_inprocess(c) != CF_OK) {
+      fprintf(stderr, "libcf: NVLS setup failed (%s); switch_2pa uses the all-pairs kernel\n",
+              cfLastErrorMessage());
+      nvls_teardown(c);
+    }
+  }
+  c->multicast_supported = c->nvls.enabled;
   c->connected = true;
   *out = c;
   return CF_OK;
@@ -335,6 +349,7 @@ extern "C" cfStatus cfCommDestroy(cfComm_t c) {
   if (!c->local.empty()) cudaSetDevice(c->local[0].dev);
   for (auto& r : c->regs) release_reg(c, r);
   for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
+  nvls_teardown(c);
   for (auto& lr : c->local) {
     if (lr.dev >= 0) cudaSetDevice(lr.dev);
     if (lr.heap) cudaFree(lr.heap);
@@ -589,6 +604,58 @@ cfStatus launch(cfComm* c, const Job& j, int dtype, const void* const* send, voi
   return CF_OK;
 }
 
+// K5: copy into the multicast-bound input half, multimem reduce/broadcast,
+// copy the output half out; messages larger than the staging half run in
+// pieces (AllReduce is element-wise).
+cfStatus nvls_allreduce(cfComm* c, const void* const* send, void* const* recv, size_t count, int dtype,
+                        const cudaStream_t* streams) {
+  DeviceGuard guard;
+  const size_t es = dtype_size(dtype);
+  const size_t piece = c->nvls.half / es;
+  const void* kernel = collective_kernel(4, dtype, c->nranks);
+  const int threads = c->cfg.threads;
+  for (size_t off = 0; off < count; off += piece) {
+    const size_t cnt = std::min(piece, count - off);
+    for (size_t li = 0; li < c->local.size(); li++) {
+      CF_CUDA(cudaSetDevice(c->local[li].dev));
+      CF_CUDA(cudaMemcpyAsync(c->nvls.ranks[li].uc, (const char*)send[li] + off * es, cnt * es,
+                              cudaMemcpyDeviceToDevice, streams[li]));
+    }
+    for (size_t gi = 0; gi < c->groups.size(); gi++) {
+      const auto& g = c->groups[gi];
+      CF_CUDA(cudaSetDevice(c->local[g[0]].dev));
+      CollArgs a;
+      memset(&a, 0, sizeof(a));
+      a.n = c->nranks;
+      a.nlocal = (int)g.size();
+      a.count = cnt;
+      a.gpu_scope = 0;
+      for (size_t k = 0; k < g.size(); k++) {
+        const int li = g[k];
+        RankCtx& rk = a.rk[k];
+        rk.rank = c->local[li].rank;
+        rk.st = c->state(li);
+        for (int p = 0; p < c->nranks; p++) rk.sem[p] = c->sem(li, p);
+        rk.in[rk.rank] = c->nvls.ranks[li].mc;
+        rk.out[rk.rank] = c->nvls.ranks[li].mc + c->nvls.half;
+      }
+      const size_t work = ceil_div(ceil_div(cnt * es, 16), (size_t)c->nranks);
+      const int mb = max_blocks_per_rank(c, kernel, (int)gi, threads);
+      const int blocks = (int)std::min<size_t>((size_t)mb, std::max<size_t>(1, ceil_div(work, (size_t)threads)));
+      CF_TRY(join_streams(c, (int)gi, streams, false));
+      void* args[] = {&a};
+      CF_CUDA(cudaLaunchKernel(kernel, dim3(blocks, g.size()), dim3(threads), args, 0, streams[g[0]]));
+      CF_TRY(join_streams(c, (int)gi, streams, true));
+    }
+    for (size_t li = 0; li < c->local.size(); li++) {
+      CF_CUDA(cudaSetDevice(c->local[li].dev));
+      CF_CUDA(cudaMemcpyAsync((char*)recv[li] + off * es, c->nvls.ranks[li].uc + c->nvls.half, cnt * es,
+                              cudaMemcpyDeviceToDevice, streams[li]));
+    }
+  }
+  return CF_OK;
+}
+
 }  // namespace
 
 extern "C" cfStatus cfAllReduce(cfComm_t c, const void* const* send, void* const* recv, size_t count,
@@ -600,6 +667,7 @@ extern "C" cfStatus cfAllReduce(cfComm_t c, const void* const* send, void* const
   const size_t es = dtype_size(dtype), V = 16 / es;
   const size_t bytes = count * es;
   if (algo == CF_ALGO_AUTO) algo = select_algo(c, 0, bytes, dtype);
+  if (algo == CF_ALGO_SWITCH_2PA && c->nvls.enabled) return nvls_allreduce(c, send, recv, count, dtype, streams);
   Job j;
   j.count = count;
   switch (algo) {

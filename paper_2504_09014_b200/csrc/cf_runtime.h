@@ -66,6 +66,25 @@ struct IpcMapping {
   int refs = 0;
 };
 
+// NVLS multicast staging of one local rank: physical memory bound to the
+// communicator's multicast object, mapped twice (unicast for the local
+// copy-in/out, multicast for multimem.ld_reduce / multimem.st).
+struct NvlsRank {
+  unsigned long long mem = 0;   // CUmemGenericAllocationHandle
+  char* uc = nullptr;           // [input half | output half], unicast
+  char* mc = nullptr;           // same layout, multicast
+};
+
+struct Nvls {
+  bool enabled = false;
+  size_t half = 0;              // bytes of each half (input, output)
+  size_t size = 0;              // 2*half rounded to the multicast granularity
+  size_t gran = 0;
+  unsigned long long mc = 0;    // CUmemGenericAllocationHandle of the multicast object
+  bool added = false;
+  std::vector<NvlsRank> ranks;  // per local rank
+};
+
 }  // namespace cf
 
 struct cfComm {
@@ -85,6 +104,7 @@ struct cfComm {
   std::map<int, int> sm_count;         // device -> SMs
   std::map<std::pair<const void*, int>, int> occ;  // (kernel, device) -> CTAs/SM
   bool multicast_supported = false;
+  cf::Nvls nvls;
 
   cf::RankState* state(int li) const { return (cf::RankState*)(local[li].heap + lay.state_off); }
   uint64_t* sem(int li, int p) const { return (uint64_t*)(peer_heap[li][p] + lay.sem_off); }
@@ -108,4 +128,8 @@ int max_blocks_per_rank(cfComm* c, const void* kernel, int group, int threads);
 // Make streams[first] of the group wait for the others; after the launch, the
 // others wait for it.  `after` selects the phase.
 cfStatus join_streams(cfComm* c, int group, const cudaStream_t* streams, bool after);
+// NVLS: probe support; set up for a one-process world; tear down.
+bool multicast_capable(int dev);
+cfStatus nvls_setup_inprocess(cfComm* c);
+void nvls_teardown(cfComm* c);
 }  // namespace cf

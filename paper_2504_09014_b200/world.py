@@ -58,7 +58,7 @@ class World:
     def __init__(self, num_nodes: int = 1, gpus_per_node: int = 1,
                  intra_kind: str = "switch-attached", seed: int = 0, devices=None,
                  ll_max_bytes: int = 0, max_blocks: int = 0, threads: int = 0,
-                 spin_timeout_ms: int = 0):
+                 spin_timeout_ms: int = 0, use_multicast: bool = True, nvls_bytes: int = 0):
         if num_nodes * gpus_per_node < 1:
             raise BadSizeError("world needs at least one rank")
         if num_nodes != 1:
@@ -83,8 +83,9 @@ class World:
         if len(devices) != n:
             raise OutOfBoundsError(f"need {n} device ids, got {len(devices)}")
         self.devices = devices
+        # NVLS is set up when every rank has its own multicast-capable GPU
         cfg = _lib.cfConfig(ll_max_bytes, max_blocks, threads,
-                            int(spin_timeout_ms) * 1_000_000, 0)
+                            int(spin_timeout_ms) * 1_000_000, int(bool(use_multicast)), nvls_bytes)
         handle = ctypes.c_void_p()
         devs = (ctypes.c_int * n)(*devices)
         _lib.check(_lib.lib().cfCommInitAll(ctypes.byref(handle), n, devs, ctypes.byref(cfg)))
@@ -148,6 +149,13 @@ class World:
     def __repr__(self):
         return (f"World(ranks={self.num_ranks}, devices={self.devices}, "
                 f"coresident={self.coresident})")
+
+
+def device_multicast_capable(dev: int) -> bool:
+    """CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED of a device (NVLS availability)."""
+    v = ctypes.c_int()
+    _lib.check(_lib.lib().cfDeviceMulticastSupported(int(dev), ctypes.byref(v)))
+    return bool(v.value)
 
 
 def make_world(num_nodes=1, gpus_per_node=1, intra_kind="switch-attached", seed=0, **kw) -> World:

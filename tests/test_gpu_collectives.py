@@ -154,3 +154,29 @@ def test_errors_map_to_reference_codes():
     t = [torch.zeros(64, device=w.device(r)) for r in range(2)]
     with pytest.raises(BadAlignError):
         C.run("allreduce", [x[1:] for x in t], [x[1:] for x in t], 8, "f32", _lib.ALGOS["2pa"], w)
+
+
+def test_nvls_multicast_path_single_rank():
+    """K5 plumbing on one GPU: multicast object, unicast+multicast mappings,
+    multimem.ld_reduce / multimem.st (a 1-member group returns its input),
+    staging in pieces larger than the NVLS half."""
+    from paper_2504_09014_b200 import collective, make_world
+    from paper_2504_09014_b200.world import device_multicast_capable
+    if not device_multicast_capable(0):
+        pytest.skip("cuda:0 reports no multicast (NVLS) support")
+    w = make_world(1, 1, devices=[0], nvls_bytes=1 << 20)
+    if not w.multicast_supported():
+        pytest.skip("multicast advertised but the object could not be built on this box")
+    try:
+        for dtype in ("f32", "bf16", "f16", "i32"):
+            dist = {"f32": "wide", "i32": "int"}.get(dtype, "normal")
+            for elems in (5, 4096, 3 * (1 << 20) + 3):
+                x = gen_inputs(1, elems, dtype, dist, elems)
+                got = collective("allreduce", x, w, dtype=dtype, algo="switch_2pa")
+                assert np.array_equal(got[0].view(np.uint8), x[0].view(np.uint8)), (dtype, elems)
+    finally:
+        w.close()
+
+
+def test_coresident_world_has_no_multicast():
+    assert not world(8).multicast_supported()
