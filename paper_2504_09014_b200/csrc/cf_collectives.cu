@@ -20,6 +20,10 @@ namespace cf {
 
 // ---------------------------------------------------------------- call bracket
 
+// Semaphore values are epoch * kPhases + phase (phase in [1, kPhases)) for every
+// kernel, so a slot's value only grows no matter which kernels run in between.
+constexpr uint64_t kPhases = 1ull << 20;
+
 // Every CTA reads the rank's call counter once; the last CTA of the rank to
 // finish publishes epoch+1 (last-CTA-done, no grid barrier).  Keeping the
 // counter on the device makes the kernels CUDA-graph replayable.
@@ -137,7 +141,7 @@ __global__ void __launch_bounds__(512) pull_reduce_kernel(const __grid_constant_
   constexpr int V = Vec<T>::N;
   const int n = a.n, r = rk.rank;
   const uint64_t e = begin_call(rk);
-  if (!a.single_launch) handshake(rk, n, e * 4 + 1, false, a.gpu_scope);
+  if (!a.single_launch) handshake(rk, n, e * kPhases + 1, false, a.gpu_scope);
 
   size_t lo = 0, hi = a.count;
   if (!a.whole) {
@@ -165,7 +169,7 @@ __global__ void __launch_bounds__(512) pull_reduce_kernel(const __grid_constant_
       store_vec<T>(rk.out[r], v, res, lo, hi, shift);
     }
   }
-  if (!a.single_launch) handshake(rk, n, e * 4 + 2, true, a.gpu_scope);
+  if (!a.single_launch) handshake(rk, n, e * kPhases + 2, true, a.gpu_scope);
   end_call(rk, e);
 }
 
@@ -327,7 +331,7 @@ __global__ void __launch_bounds__(512) push_gather_kernel(const __grid_constant_
   constexpr int V = 16 / sizeof(T);
   const int n = a.n, r = rk.rank;
   const uint64_t e = begin_call(rk);
-  if (!a.single_launch) handshake(rk, n, e * 4 + 1, false, a.gpu_scope);
+  if (!a.single_launch) handshake(rk, n, e * kPhases + 1, false, a.gpu_scope);
   const size_t stride = (size_t)gridDim.x * blockDim.x;
   const size_t t0 = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   const size_t sb = a.count * sizeof(T);
@@ -348,7 +352,7 @@ __global__ void __launch_bounds__(512) push_gather_kernel(const __grid_constant_
         store_vec<T>(rk.out[p] + (size_t)r * sb, v, x, 0, a.count, 0);
     }
   }
-  if (!a.single_launch) handshake(rk, n, e * 4 + 2, true, a.gpu_scope);
+  if (!a.single_launch) handshake(rk, n, e * kPhases + 2, true, a.gpu_scope);
   end_call(rk, e);
 }
 
@@ -405,7 +409,7 @@ __global__ void __launch_bounds__(512) nvls_allreduce_kernel(const __grid_consta
   constexpr int V = 16 / sizeof(T);
   const int n = a.n, r = rk.rank;
   const uint64_t e = begin_call(rk);
-  handshake(rk, n, e * 4 + 1, false, a.gpu_scope);
+  handshake(rk, n, e * kPhases + 1, false, a.gpu_scope);
   const size_t nvec = (a.count + V - 1) / V;       // staging halves are padded: whole vectors
   const size_t cv = (nvec + n - 1) / n;
   const size_t v0 = min((size_t)r * cv, nvec), v1 = min(v0 + cv, nvec);
@@ -414,7 +418,199 @@ __global__ void __launch_bounds__(512) nvls_allreduce_kernel(const __grid_consta
   for (size_t v = v0 + (size_t)blockIdx.x * blockDim.x + threadIdx.x; v < v1;
        v += (size_t)gridDim.x * blockDim.x)
     multimem_st16(out + v * 16, multimem_ld_reduce<T>(in + v * 16));
-  handshake(rk, n, e * 4 + 2, true, a.gpu_scope);
+  handshake(rk, n, e * kPhases + 2, true, a.gpu_scope);
+  end_call(rk, e);
+}
+
+// ---------------------------------------------------------------- K9 / K12 / K7 ring
+
+// CTA b's contiguous share of element range [lo, hi) (multiple of V elements).
+__device__ __forceinline__ void cta_slice(size_t lo, size_t hi, int b, int B, size_t V, size_t& s0,
+                                          size_t& s1) {
+  const size_t len = hi > lo ? hi - lo : 0;
+  const size_t per = ((len + B - 1) / B + V - 1) / V * V;
+  s0 = min(lo + (size_t)b * per, hi);
+  s1 = min(s0 + per, hi);
+}
+
+// Point-to-point stream of fixed-size units from rank r's CTA b to the next
+// rank's CTA b: kRingSlots slots in the receiver's ring region, data signals
+// on the receiver's semaphore slab, credits (acks) on the sender's ack slab.
+// Values are epoch * kPhases + sequence; the value epoch * kPhases itself is
+// the receiver's "entered this call" ready mark, so slots are never
+// overwritten while the previous call still reads them.
+struct RingLink {
+  char* my_slots;         // slots I receive into (from prev)
+  char* nx_slots;         // slots I send into (next's)
+  const uint64_t* data_in;
+  uint64_t* data_out;
+  const uint64_t* ack_in;
+  uint64_t* ack_out;
+  uint64_t base;
+  uint64_t qs, qr;
+  RankState* st;
+  bool gpu;
+
+  __device__ char* recv_slot() const { return my_slots + (qr % kRingSlots) * kRingSlot; }
+  __device__ char* send_slot() const { return nx_slots + (qs % kRingSlots) * kRingSlot; }
+  __device__ void recv_wait() {
+    if (threadIdx.x == 0) wait_geq(data_in, base + qr + 1, st, gpu);
+    __syncthreads();
+  }
+  __device__ void recv_done() {
+    __syncthreads();
+    if (threadIdx.x == 0) st_release(ack_out, base + qr + 1, gpu);
+    qr++;
+  }
+  __device__ void send_wait() {
+    if (threadIdx.x == 0) wait_geq(ack_in, base + (qs >= kRingSlots ? qs - kRingSlots + 1 : 0), st, gpu);
+    __syncthreads();
+  }
+  __device__ void send_done() {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      fence_publish(gpu);
+      st_release(data_out, base + qs + 1, gpu);
+    }
+    qs++;
+  }
+};
+
+__device__ __forceinline__ RingLink make_link(const CollArgs& a, const RankCtx& rk, uint64_t e) {
+  const int n = a.n, r = rk.rank, b = blockIdx.x;
+  const int prev = (r + n - 1) % n, next = (r + 1) % n;
+  RingLink L;
+  L.my_slots = rk.ring[r] + (size_t)b * kRingSlots * kRingSlot;
+  L.nx_slots = rk.ring[next] + (size_t)b * kRingSlots * kRingSlot;
+  L.data_in = rk.sem[r] + sem_index(prev, b);
+  L.data_out = rk.sem[next] + sem_index(r, b);
+  L.ack_in = rk.ack[r] + sem_index(next, b);
+  L.ack_out = rk.ack[prev] + sem_index(r, b);
+  L.base = e * kPhases;
+  L.qs = L.qr = 0;
+  L.st = rk.st;
+  L.gpu = a.gpu_scope;
+  // ready mark: my slots are free for this call (I finished the previous one)
+  if (threadIdx.x == 0) st_release(L.ack_out, L.base, L.gpu);
+  return L;
+}
+
+// Ring ReduceScatter (build_ring_rs, cf/collectives.py:30-79) and, with
+// `push`, the two-phase ring AllReduce (build_2pr, :107-136).  Step s sends
+// the partial of chunk (r - s) mod n to the next rank; the partial that
+// arrives is added to the own contribution (partials travel in the
+// accumulator type, f32 for f16/bf16, so rounding happens once), and after n
+// steps chunk r holds 0 + x_r + x_{r+1} + ... + x_{r-1}: the reference's
+// ring order.  The AllGather phase then forwards the finished chunks.
+template <typename T>
+__global__ void __launch_bounds__(512) ring_kernel(const __grid_constant__ CollArgs a) {
+  using A = typename Vec<T>::Acc;
+  const RankCtx& rk = a.rk[blockIdx.y];
+  const int n = a.n, r = rk.rank, b = blockIdx.x, B = gridDim.x;
+  constexpr size_t V = 16 / sizeof(T);
+  const uint64_t e = begin_call(rk);
+  RingLink L = make_link(a, rk, e);
+  const T* x = reinterpret_cast<const T*>(rk.in[r]);
+  T* y = reinterpret_cast<T*>(rk.out[r]);
+  constexpr size_t UA = kRingSlot / sizeof(A);   // elements per unit, RS phase
+  constexpr size_t UT = kRingSlot / sizeof(T);   // elements per unit, AG phase
+  auto chunk = [&](int c, size_t& s0, size_t& s1) {
+    const size_t lo = min((size_t)c * a.cs, a.count), hi = min(lo + a.cs, a.count);
+    cta_slice(lo, hi, b, B, V, s0, s1);
+  };
+  // ReduceScatter phase: n sends, n-1 receives interleaved per unit
+  for (int s = 0; s < n; s++) {
+    const int c = (r - s + n) % n;
+    size_t s0, s1;
+    chunk(c, s0, s1);
+    for (size_t u0 = s0; u0 < s1; u0 += UA) {
+      const size_t u1 = min(u0 + UA, s1);
+      if (s > 0) L.recv_wait();
+      L.send_wait();
+      const A* in_slot = reinterpret_cast<const A*>(L.recv_slot());
+      A* out_slot = reinterpret_cast<A*>(L.send_slot());
+      for (size_t i = u0 + threadIdx.x; i < u1; i += blockDim.x) {
+        A v = to_acc<T>(x[i]);
+        if (s > 0) v = acc_add(in_slot[i - u0], v);
+        out_slot[i - u0] = v;
+      }
+      if (s > 0) L.recv_done();
+      L.send_done();
+    }
+  }
+  // own chunk r completed the circle: materialize 0 + P (cf/collectives.py:74-79)
+  {
+    size_t s0, s1;
+    chunk(r, s0, s1);
+    const size_t shift = a.rs_shift ? min((size_t)r * a.cs, a.count) : 0;
+    for (size_t u0 = s0; u0 < s1; u0 += UA) {
+      const size_t u1 = min(u0 + UA, s1);
+      L.recv_wait();
+      const A* in_slot = reinterpret_cast<const A*>(L.recv_slot());
+      for (size_t i = u0 + threadIdx.x; i < u1; i += blockDim.x)
+        y[i - shift] = from_acc<T>(acc_add(A(0), in_slot[i - u0]));
+      L.recv_done();
+    }
+  }
+  if (a.push) {
+    // AllGather phase: forward finished chunks around the ring; send unit k of
+    // chunk (r - t) and receive unit k of chunk (r - 1 - t) interleaved
+    __syncthreads();
+    for (int t = 0; t < n - 1; t++) {
+      size_t a0, a1, b0, b1;
+      chunk((r - t + n) % n, a0, a1);
+      chunk((r - 1 - t + n) % n, b0, b1);
+      const size_t us = (a1 - a0 + UT - 1) / UT, ur = (b1 - b0 + UT - 1) / UT;
+      for (size_t k = 0; k < max(us, ur); k++) {
+        if (k < us) {
+          const size_t u0 = a0 + k * UT, u1 = min(u0 + UT, a1);
+          L.send_wait();
+          T* out_slot = reinterpret_cast<T*>(L.send_slot());
+          for (size_t i = u0 + threadIdx.x; i < u1; i += blockDim.x) out_slot[i - u0] = y[i];
+          L.send_done();
+        }
+        if (k < ur) {
+          const size_t u0 = b0 + k * UT, u1 = min(u0 + UT, b1);
+          L.recv_wait();
+          const T* in_slot = reinterpret_cast<const T*>(L.recv_slot());
+          for (size_t i = u0 + threadIdx.x; i < u1; i += blockDim.x) y[i] = in_slot[i - u0];
+          L.recv_done();
+        }
+      }
+    }
+  }
+  end_call(rk, e);
+}
+
+// Ring AllGather (build_ring_ag, cf/collectives.py:82-104): each rank copies
+// its shard into its own output slot, then n-1 times forwards the shard it
+// holds most recently straight into the next rank's output and signals.
+template <typename T>
+__global__ void __launch_bounds__(512) ring_gather_kernel(const __grid_constant__ CollArgs a) {
+  const RankCtx& rk = a.rk[blockIdx.y];
+  const int n = a.n, r = rk.rank, b = blockIdx.x, B = gridDim.x;
+  const int next = (r + 1) % n;
+  constexpr size_t V = 16 / sizeof(T);
+  const uint64_t e = begin_call(rk);
+  RingLink L = make_link(a, rk, e);
+  // the next rank's output is free once it entered this call
+  if (threadIdx.x == 0) wait_geq(L.ack_in, L.base, rk.st, L.gpu);
+  __syncthreads();
+  const T* x = reinterpret_cast<const T*>(rk.in[r]);
+  T* y = reinterpret_cast<T*>(rk.out[r]);
+  T* yn = reinterpret_cast<T*>(rk.out[next]);
+  const size_t cnt = a.count;
+  size_t s0, s1;
+  cta_slice(0, cnt, b, B, V, s0, s1);
+  for (size_t i = s0 + threadIdx.x; i < s1; i += blockDim.x) y[(size_t)r * cnt + i] = x[i];
+  for (int t = 0; t < n - 1; t++) {
+    const size_t off = (size_t)((r - t + n) % n) * cnt;
+    __syncthreads();
+    for (size_t i = s0 + threadIdx.x; i < s1; i += blockDim.x) yn[off + i] = y[off + i];
+    L.send_done();
+    L.recv_wait();   // shard (r - 1 - t) landed in my output
+    L.qr++;
+  }
   end_call(rk, e);
 }
 
@@ -477,6 +673,22 @@ const void* collective_kernel(int kind, int dtype, int n) {
         case 1: return (const void*)nvls_allreduce_kernel<float>;
         case 2: return (const void*)nvls_allreduce_kernel<__half>;
         case 3: return (const void*)nvls_allreduce_kernel<__nv_bfloat16>;
+      }
+      break;
+    case 5:
+      switch (dtype) {
+        case 0: return (const void*)ring_kernel<int32_t>;
+        case 1: return (const void*)ring_kernel<float>;
+        case 2: return (const void*)ring_kernel<__half>;
+        case 3: return (const void*)ring_kernel<__nv_bfloat16>;
+      }
+      break;
+    case 6:
+      switch (dtype) {
+        case 0: return (const void*)ring_gather_kernel<int32_t>;
+        case 1: return (const void*)ring_gather_kernel<float>;
+        case 2: return (const void*)ring_gather_kernel<__half>;
+        case 3: return (const void*)ring_gather_kernel<__nv_bfloat16>;
       }
       break;
   }

@@ -14,9 +14,17 @@ struct RankCtx {
   const char* in[CF_MAX_RANKS];   // every rank's send buffer (pull kernels)
   char* out[CF_MAX_RANKS];        // every rank's recv buffer (push kernels)
   char* scr[CF_MAX_RANKS];        // every rank's LL scratch base
-  uint64_t* sem[CF_MAX_RANKS];    // every rank's semaphore slab
+  uint64_t* sem[CF_MAX_RANKS];    // every rank's semaphore slab (data / handshake signals)
+  uint64_t* ack[CF_MAX_RANKS];    // every rank's ack slab (ring credits, ring "ready")
+  char* ring[CF_MAX_RANKS];       // every rank's ring slot region
   RankState* st;                  // this rank's state
 };
+
+// Ring slots: per receiving rank and CTA, kRingSlots slots of kRingSlot bytes.
+constexpr int kRingCtas = 64;
+constexpr int kRingSlots = 4;
+constexpr size_t kRingSlot = 32 * 1024;
+constexpr size_t kRingBytes = (size_t)kRingCtas * kRingSlots * kRingSlot;
 
 // Semaphore slab of a receiving rank: slot [src_rank][cta].
 __host__ __device__ inline size_t sem_index(int src, int cta) {

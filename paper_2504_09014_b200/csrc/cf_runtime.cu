@@ -29,12 +29,12 @@ cfStatus fail(cfStatus s, const char* fmt, ...) {
   return s;
 }
 
-void HeapLayout::compute(int nranks, size_t ll_max, size_t plan_sems) {
+void HeapLayout::compute(int nranks, size_t ll_max) {
   sem_off = 256;
   sem_bytes = (size_t)CF_MAX_RANKS * CF_MAX_BLOCKS * sizeof(uint64_t);
-  plan_sem_off = round_up(sem_off + sem_bytes, 256);
-  plan_sem_bytes = round_up(plan_sems * sizeof(uint64_t), 256);
-  scr_off = round_up(plan_sem_off + plan_sem_bytes, 4096);
+  ack_off = round_up(sem_off + sem_bytes, 256);
+  ring_off = round_up(ack_off + sem_bytes, 4096);
+  scr_off = round_up(ring_off + kRingBytes, 4096);
   // one LL16 packet (16 B) per 8 payload bytes: a slot holds 2*ll_max bytes
   slot = round_up(2 * ll_max + 64, 256);
   half = (size_t)nranks * slot;
@@ -187,7 +187,7 @@ static cfStatus comm_common_init(cfComm* c, int nranks, const cfConfig* cfg) {
   apply_defaults(&c->cfg);
   if (c->cfg.threads % 32 || c->cfg.threads < 64 || c->cfg.threads > 1024)
     return fail(CF_E_CONFIG, "threads must be a multiple of 32 in [64, 1024]");
-  c->lay.compute(nranks, c->cfg.ll_max_bytes, /*plan_sems=*/(size_t)CF_MAX_RANKS * 4096);
+  c->lay.compute(nranks, c->cfg.ll_max_bytes);
   return CF_OK;
 }
 
@@ -513,7 +513,7 @@ extern "C" cfStatus cfSelectAlgorithm(cfComm_t c, int coll, size_t nbytes, cfDty
 
 namespace {
 
-enum Kind { kPull = 0, kLL1 = 1, kLL2 = 2, kGather = 3 };
+enum Kind { kPull = 0, kLL1 = 1, kLL2 = 2, kGather = 3, kNvls = 4, kRing = 5, kRingGather = 6 };
 
 struct Job {
   int kind = kPull;
@@ -540,7 +540,8 @@ cfStatus check_ptrs(cfComm* c, const void* const* send, void* const* recv, const
 cfStatus launch(cfComm* c, const Job& j, int dtype, const void* const* send, void* const* recv,
                 const cudaStream_t* streams) {
   // one-process-per-GPU: peers' buffers come from the registration table
-  const bool need_in = j.kind == kPull, need_out = j.kind == kGather || (j.kind == kPull && j.push);
+  const bool need_in = j.kind == kPull;
+  const bool need_out = j.kind == kGather || j.kind == kRingGather || (j.kind == kPull && j.push);
   const Registration* reg_in = nullptr;
   const Registration* reg_out = nullptr;
   if (c->multiprocess) {
@@ -584,6 +585,8 @@ cfStatus launch(cfComm* c, const Job& j, int dtype, const void* const* send, voi
         rk.out[p] = c->multiprocess ? nullptr : (char*)recv[p];
         rk.scr[p] = c->scr(li, p);
         rk.sem[p] = c->sem(li, p);
+        rk.ack[p] = c->ack(li, p);
+        rk.ring[p] = c->ring(li, p);
       }
       if (c->multiprocess) {
         for (int p = 0; p < c->nranks; p++) {
@@ -594,7 +597,8 @@ cfStatus launch(cfComm* c, const Job& j, int dtype, const void* const* send, voi
         rk.out[rk.rank] = (char*)recv[li];
       }
     }
-    const int mb = max_blocks_per_rank(c, kernel, (int)gi, threads);
+    int mb = max_blocks_per_rank(c, kernel, (int)gi, threads);
+    if (j.kind == kRing || j.kind == kRingGather) mb = std::min(mb, kRingCtas);   // ring slot region
     int blocks = (int)std::min<size_t>((size_t)mb, std::max<size_t>(1, ceil_div(j.work, (size_t)threads)));
     CF_TRY(join_streams(c, (int)gi, streams, false));
     void* args[] = {&a};
@@ -687,16 +691,22 @@ extern "C" cfStatus cfAllReduce(cfComm_t c, const void* const* send, void* const
       j.work = ceil_div(count, V);
       break;
     case CF_ALGO_2PA:
-    case CF_ALGO_SWITCH_2PA:
-    case CF_ALGO_2PR: {
-      const size_t mult = algo == CF_ALGO_2PR ? 2 * n : n;   // cf/collectives.py:497-504
+    case CF_ALGO_SWITCH_2PA: {
+      // switch_2pa without a multicast object: the all-pairs pull in the
+      // switch's reference order (0 + ranks ascending)
       j.kind = kPull;
       j.push = 1;
-      j.order = algo == CF_ALGO_2PA ? kLead : (algo == CF_ALGO_SWITCH_2PA ? kAscZero : kRingZero);
-      j.cs = round_up(count, mult) / n;
+      j.order = algo == CF_ALGO_2PA ? kLead : kAscZero;
+      j.cs = round_up(count, n) / n;   // cf/collectives.py:497-504
       j.work = ceil_div(j.cs, V) + 1;
       break;
     }
+    case CF_ALGO_2PR:
+      j.kind = kRing;
+      j.push = 1;
+      j.cs = round_up(count, 2 * n) / n;
+      j.work = ceil_div(j.cs, V) + 1;
+      break;
     case CF_ALGO_2PA_LL: {
       j.kind = kLL2;
       j.cs = round_up(count, n) / n;
@@ -721,7 +731,7 @@ extern "C" cfStatus cfAllGather(cfComm_t c, const void* const* send, void* const
   if (algo != CF_ALGO_ALLPAIRS_AG && algo != CF_ALGO_RING_AG)
     return fail(CF_E_NO_ALGO, "algorithm %d is not an AllGather algorithm", algo);
   Job j;
-  j.kind = kGather;
+  j.kind = algo == CF_ALGO_RING_AG ? kRingGather : kGather;
   j.count = sendcount;
   j.work = ceil_div(sendcount * dtype_size(dtype), 16);
   return launch(c, j, dtype, send, recv, streams);
@@ -738,9 +748,9 @@ extern "C" cfStatus cfReduceScatter(cfComm_t c, const void* const* send, void* c
   if (algo != CF_ALGO_RS_DIRECT && algo != CF_ALGO_RING_RS)
     return fail(CF_E_NO_ALGO, "algorithm %d is not a ReduceScatter algorithm", algo);
   Job j;
-  j.kind = kPull;
+  j.kind = algo == CF_ALGO_RING_RS ? kRing : kPull;
   j.rs_shift = 1;
-  j.order = algo == CF_ALGO_RING_RS ? kRingZero : kLead;
+  j.order = kLead;
   j.count = recvcount * n;
   j.cs = recvcount;
   j.work = ceil_div(recvcount, 16 / es) + 1;

@@ -33,16 +33,18 @@ inline size_t round_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 inline size_t ceil_div(size_t x, size_t a) { return (x + a - 1) / a; }
 inline int dtype_size(int dt) { return dt <= 1 ? 4 : 2; }
 
-// Symmetric heap of one rank: [RankState | semaphore slab | plan semaphores | LL scratch]
+// Symmetric heap of one rank:
+// [RankState | semaphore slab | ack slab | ring slots | LL scratch (2 parities)]
 struct HeapLayout {
   size_t state_off = 0;
   size_t sem_off = 256;
   size_t sem_bytes = (size_t)CF_MAX_RANKS * CF_MAX_BLOCKS * sizeof(uint64_t);
-  size_t plan_sem_off = 0, plan_sem_bytes = 0;
+  size_t ack_off = 0;
+  size_t ring_off = 0;
   size_t scr_off = 0, scr_bytes = 0;
   size_t slot = 0, half = 0;
   size_t total = 0;
-  void compute(int nranks, size_t ll_max, size_t plan_sems);
+  void compute(int nranks, size_t ll_max);
 };
 
 struct LocalRank {
@@ -109,7 +111,8 @@ struct cfComm {
   cf::RankState* state(int li) const { return (cf::RankState*)(local[li].heap + lay.state_off); }
   uint64_t* sem(int li, int p) const { return (uint64_t*)(peer_heap[li][p] + lay.sem_off); }
   char* scr(int li, int p) const { return peer_heap[li][p] + lay.scr_off; }
-  uint64_t* plan_sem(int li, int p) const { return (uint64_t*)(peer_heap[li][p] + lay.plan_sem_off); }
+  uint64_t* ack(int li, int p) const { return (uint64_t*)(peer_heap[li][p] + lay.ack_off); }
+  char* ring(int li, int p) const { return peer_heap[li][p] + lay.ring_off; }
   // registered range containing p (nullptr if none)
   const cf::Registration* find_reg(const void* p) const {
     for (auto& r : regs)

@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--ranks", type=int, default=8)
     ap.add_argument("--iters", type=int, default=3)
     ap.add_argument("--plan", default="")
+    ap.add_argument("--scale", type=int, default=1)
     args = ap.parse_args()
     import torch
     from paper_2504_09014_b200 import _lib, make_world
@@ -33,8 +34,9 @@ def main():
     tdt = torch_dtype(args.dtype)
     if args.plan:
         from paper_2504_09014_b200 import Runtime, parse_plan
+        from paper_2504_09014_b200.plan import scale_plan
         with open(args.plan, "rb") as f:
-            plan = parse_plan(f.read())
+            plan = scale_plan(parse_plan(f.read()), args.scale)
         rt = Runtime(plan, w, dtype=args.dtype)
         send = [torch.randn(rt.in_elems, device=dev).to(tdt) for _ in range(n)]
         recv = [torch.empty(rt.out_elems, device=dev, dtype=tdt) for _ in range(n)]
