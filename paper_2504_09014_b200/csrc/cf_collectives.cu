@@ -518,12 +518,26 @@ __global__ void __launch_bounds__(512) ring_kernel(const __grid_constant__ CollA
     const size_t lo = min((size_t)c * a.cs, a.count), hi = min(lo + a.cs, a.count);
     cta_slice(lo, hi, b, B, V, s0, s1);
   };
-  // ReduceScatter phase: n sends, n-1 receives interleaved per unit
-  for (int s = 0; s < n; s++) {
-    const int c = (r - s + n) % n;
+  // Unit-major schedule (unit k walks through every step before unit k+1):
+  // each send after the first step is preceded by the receive that feeds it,
+  // so with kRingSlots credits the ring never stalls on a full slot ring.
+  // Sender and receiver skip the same (chunk, unit) pairs, so the per-link
+  // sequence numbers stay aligned.
+  size_t ka = 0, kt = 0;
+  for (int c = 0; c < n; c++) {
     size_t s0, s1;
     chunk(c, s0, s1);
-    for (size_t u0 = s0; u0 < s1; u0 += UA) {
+    ka = max(ka, (s1 - s0 + UA - 1) / UA);
+    kt = max(kt, (s1 - s0 + UT - 1) / UT);
+  }
+  const size_t shift = a.rs_shift ? min((size_t)r * a.cs, a.count) : 0;
+  for (size_t k = 0; k < ka; k++) {
+    // ReduceScatter: step s adds the own contribution to chunk (r - s)
+    for (int s = 0; s < n; s++) {
+      size_t s0, s1;
+      chunk((r - s + n) % n, s0, s1);
+      const size_t u0 = s0 + k * UA;
+      if (u0 >= s1) continue;
       const size_t u1 = min(u0 + UA, s1);
       if (s > 0) L.recv_wait();
       L.send_wait();
@@ -537,13 +551,11 @@ __global__ void __launch_bounds__(512) ring_kernel(const __grid_constant__ CollA
       if (s > 0) L.recv_done();
       L.send_done();
     }
-  }
-  // own chunk r completed the circle: materialize 0 + P (cf/collectives.py:74-79)
-  {
+    // own chunk r completed the circle: materialize 0 + P (cf/collectives.py:74-79)
     size_t s0, s1;
     chunk(r, s0, s1);
-    const size_t shift = a.rs_shift ? min((size_t)r * a.cs, a.count) : 0;
-    for (size_t u0 = s0; u0 < s1; u0 += UA) {
+    const size_t u0 = s0 + k * UA;
+    if (u0 < s1) {
       const size_t u1 = min(u0 + UA, s1);
       L.recv_wait();
       const A* in_slot = reinterpret_cast<const A*>(L.recv_slot());
@@ -553,27 +565,27 @@ __global__ void __launch_bounds__(512) ring_kernel(const __grid_constant__ CollA
     }
   }
   if (a.push) {
-    // AllGather phase: forward finished chunks around the ring; send unit k of
-    // chunk (r - t) and receive unit k of chunk (r - 1 - t) interleaved
+    // AllGather: step t forwards unit k of chunk (r - t) and receives unit k
+    // of chunk (r - 1 - t), which step t + 1 forwards
     __syncthreads();
-    for (int t = 0; t < n - 1; t++) {
-      size_t a0, a1, b0, b1;
-      chunk((r - t + n) % n, a0, a1);
-      chunk((r - 1 - t + n) % n, b0, b1);
-      const size_t us = (a1 - a0 + UT - 1) / UT, ur = (b1 - b0 + UT - 1) / UT;
-      for (size_t k = 0; k < max(us, ur); k++) {
-        if (k < us) {
-          const size_t u0 = a0 + k * UT, u1 = min(u0 + UT, a1);
+    for (size_t k = 0; k < kt; k++) {
+      for (int t = 0; t < n - 1; t++) {
+        size_t a0, a1, b0, b1;
+        chunk((r - t + n) % n, a0, a1);
+        chunk((r - 1 - t + n) % n, b0, b1);
+        const size_t us0 = a0 + k * UT, ur0 = b0 + k * UT;
+        if (us0 < a1) {
+          const size_t u1 = min(us0 + UT, a1);
           L.send_wait();
           T* out_slot = reinterpret_cast<T*>(L.send_slot());
-          for (size_t i = u0 + threadIdx.x; i < u1; i += blockDim.x) out_slot[i - u0] = y[i];
+          for (size_t i = us0 + threadIdx.x; i < u1; i += blockDim.x) out_slot[i - us0] = y[i];
           L.send_done();
         }
-        if (k < ur) {
-          const size_t u0 = b0 + k * UT, u1 = min(u0 + UT, b1);
+        if (ur0 < b1) {
+          const size_t u1 = min(ur0 + UT, b1);
           L.recv_wait();
           const T* in_slot = reinterpret_cast<const T*>(L.recv_slot());
-          for (size_t i = u0 + threadIdx.x; i < u1; i += blockDim.x) y[i] = in_slot[i - u0];
+          for (size_t i = ur0 + threadIdx.x; i < u1; i += blockDim.x) y[i] = in_slot[i - ur0];
           L.recv_done();
         }
       }

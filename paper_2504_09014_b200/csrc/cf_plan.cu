@@ -526,11 +526,17 @@ cfStatus load(cfComm* c, const char* json, size_t len, int dtype_override, cfPla
     for (int r : prank) per_dev[c->local[r].dev]++;
     for (auto& kv : per_dev) {
       progs_per_dev_max = std::max(progs_per_dev_max, kv.second);
-      cap = std::min(cap, occupancy(c, kernel, kv.first, pl->threads) * c->sm_count[kv.first] / kv.second);
+      int nb = 0;
+      cudaSetDevice(kv.first);
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, pl->threads, kPlanWindow * sizeof(DevOp)) !=
+          cudaSuccess)
+        nb = 1;
+      cap = std::min(cap, std::max(nb, 1) * c->sm_count[kv.first] / kv.second);
     }
   }
   if (cap < 1) return fail(CF_E_CONFIG, "plan has more programs per device than co-resident CTAs");
-  const long long per_cta = (long long)pl->threads * 16 * 4;
+  // one 16-byte vector per thread per source and CTA: latency, not issue, bound
+  const long long per_cta = (long long)pl->threads * 16;
   pl->K = (int)std::max(1LL, std::min<long long>({(max_bytes + per_cta - 1) / per_cta, (long long)cap, 32LL}));
   const int K = pl->K;
 
@@ -883,7 +889,9 @@ extern "C" cfStatus cfPlanExecute(cfPlan_t pl, const void* const* inputs, void* 
     cfStatus s = join_streams(c, (int)gi, streams, false);
     if (s != CF_OK) { cudaSetDevice(prev); return s; }
     void* args[] = {&a};
-    cudaError_t e = cudaLaunchKernel(kernel, dim3(np * pl->K), dim3(pl->threads), args, 0, streams[c->groups[gi][0]]);
+    a.window = kPlanWindow;
+    cudaError_t e = cudaLaunchKernel(kernel, dim3(np * pl->K), dim3(pl->threads), args,
+                                     kPlanWindow * sizeof(DevOp), streams[c->groups[gi][0]]);
     if (e != cudaSuccess) {
       cudaSetDevice(prev);
       return fail(CF_E_CUDA, "plan kernel launch: %s", cudaGetErrorString(e));

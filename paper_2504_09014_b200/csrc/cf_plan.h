@@ -125,6 +125,7 @@ struct PlanArgs {
   int in_buf, out_buf;
   int input_private;           // 1: plan writes its input -> copy user input into the plan buffer
   int gpu_scope;               // every rank on this device: .gpu-scope release/acquire
+  int window;                  // ops staged into shared memory at a time
   int entry_barrier;           // rank barrier after the prologue (zeroing / private input)
   int exit_barrier;            // rank barrier at the end (not needed when one launch holds every rank)
   uint32_t flag_stride;
@@ -139,6 +140,8 @@ struct PlanArgs {
 };
 constexpr int kMaxBufs = 16;
 constexpr int kMaxZero = 16;
+constexpr int kPlanWindow = 32;   // DevOps staged in shared memory at a time
+static_assert(sizeof(DevOp) % 16 == 0, "DevOp is copied as 16-byte vectors");
 
 }  // namespace plan
 }  // namespace cf

@@ -280,9 +280,23 @@ __global__ void __launch_bounds__(512) plan_kernel(const __grid_constant__ PlanA
   // rank barriers are numbered consecutively across calls (monotonic counters)
   const uint64_t per_call = (uint64_t)(a.entry_barrier + a.exit_barrier);
   if (a.entry_barrier) rank_barrier(a, rank, (e - 1) * per_call + 1);
+  // Ops are staged into shared memory in windows of a.window ops: every field
+  // read of the interpreter then hits shared memory (the acquire loads of the
+  // waits invalidate L1, which would otherwise send each field load to L2).
+  extern __shared__ uint4 s_raw[];
+  DevOp* s_ops = reinterpret_cast<DevOp*>(s_raw);
   const int end = a.prog_end[pid];
-  for (int i = a.prog_begin[pid]; i < end; i++) {
-    const DevOp& op = a.ops[i];
+  for (int w0 = a.prog_begin[pid]; w0 < end; w0 += a.window) {
+    const int w1 = min(w0 + a.window, end);
+    __syncthreads();
+    {
+      const uint4* src = reinterpret_cast<const uint4*>(a.ops + w0);
+      const int nvec = (w1 - w0) * (int)(sizeof(DevOp) / 16);
+      for (int t = threadIdx.x; t < nvec; t += blockDim.x) s_raw[t] = src[t];
+    }
+    __syncthreads();
+  for (int i = w0; i < w1; i++) {
+    const DevOp& op = s_ops[i - w0];
     switch (op.code) {
       case D_SYNC_CTA:
         __syncthreads();
@@ -318,6 +332,7 @@ __global__ void __launch_bounds__(512) plan_kernel(const __grid_constant__ PlanA
       default:
         break;
     }
+  }
   }
   if (a.exit_barrier) rank_barrier(a, rank, e * per_call);
   __syncthreads();
