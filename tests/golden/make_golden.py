@@ -104,6 +104,11 @@ PLAN_CASES = [
     ("allpairs_ag", "", 8, 64, 1, "HB"), ("ring_ag", "", 4, 8, 1, "HB"),
     ("ring_rs", "", 4, 8, 1, "HB"), ("2pr", "", 4, 16, 1, "HB"),
     ("2pa", "memory", 8, 8192, 1, "HB"), ("1pa", "", 8, 8192, 1, "LL"),
+    ("ring_rs", "", 2, 8, 1, "HB"), ("2pr", "", 8, 32, 1, "HB"), ("2pr", "", 4, 32, 2, "HB"),
+    ("ring_ag", "", 8, 16, 1, "HB"), ("2pa", "ll", 8, 64, 1, "LL"), ("2pa", "ll", 4, 16, 2, "LL"),
+    ("2pa", "port", 8, 64, 1, "HB"), ("1pa", "", 2, 8, 1, "LL"), ("1pa", "", 4, 16, 2, "LL"),
+    ("switch_2pa", "", 4, 16, 2, "HB"), ("allpairs_ag", "", 4, 8, 2, "HB"),
+    ("ring_rs", "", 4, 32, 2, "HB"),
 ]
 
 
@@ -165,12 +170,19 @@ def make_ll():
 
 
 def copy_frontend():
+    from commforge.lowering import graph_from_plan
     fdir = os.path.join(HERE, "frontend")
     os.makedirs(fdir, exist_ok=True)
     src = "/root/reference/pkg/tests/golden"
     for name in sorted(os.listdir(src)):
         if name.endswith(".json"):
             shutil.copyfile(os.path.join(src, name), os.path.join(fdir, name))
+    # the reference's lowering of the TS-frontend documents (pre-lowering -> plan)
+    for name in ("frontend_1pa_n4e8", "frontend_ringrs_n4e8"):
+        with open(os.path.join(src, name + ".json"), "rb") as f:
+            plan = lower(graph_from_plan(parse_plan(f.read())))
+        with open(os.path.join(fdir, name + "_lowered.json"), "wb") as f:
+            f.write(serialize_plan(plan))
     print("frontend goldens copied")
 
 
