@@ -181,15 +181,52 @@ def run(kind: str, send, recv, count: int, dtype: str, algo: int, world) -> None
     _lib.check(fn(world.comm, sp, rp, int(count), CODES[dtype], int(algo), st))
 
 
+def _plan_runtime(world, kind, name, var, elems, dtype):
+    """Lowered DSL plan of a library algorithm on this world (cached per shape):
+    the MSCCL++ DSL path -- builder, native lowering, GPU interpreter (K10)."""
+    from .algorithms import build_algo
+    from .executor import Runtime
+    from .lowering import LoweringParams, lower
+    cache = world.__dict__.setdefault("_plan_cache", {})
+    key = (kind, name, var, elems, dtype)
+    if key not in cache:
+        proto = "LL" if name == "1pa" or var == "ll" else "HB"
+        params = LoweringParams(world.num_ranks, elems, dtype, proto)
+        cache[key] = Runtime(lower(build_algo(name, params, variant=var), params), world)
+    return cache[key]
+
+
+def _run_via_plan(kind, name, var, tensors, elems, dtype, world):
+    import torch
+    n = world.num_ranks
+    if kind == "allgather":
+        rt = _plan_runtime(world, kind, name, var, elems, dtype)
+        ins = tensors
+    else:
+        padded = _padded(elems, required_multiple(name, n))
+        rt = _plan_runtime(world, kind, name, var, padded, dtype)
+        ins = tensors if padded == elems else \
+            [torch.cat([t, t.new_zeros(padded - elems)]) for t in tensors]
+    outs = [t.new_empty(rt.out_elems) for t in ins]
+    rt.run_raw(ins, outs)
+    world.synchronize()
+    rt.check_device_error()
+    return [o[:elems] for o in outs] if kind == "allreduce" else outs
+
+
 def collective(kind: str, inputs, world, selector: Selector | None = None, dtype: str = "i32",
                algo: str | None = None, variant: str = "", mode: str = "round-robin",
-               seed: int | None = None, outputs=None):
+               seed: int | None = None, outputs=None, via_plan: bool = False):
     """Select, run on the GPUs, return per-rank outputs (cf/collectives.py:532-573).
 
     `mode` and `seed` drive the reference's simulated scheduler; real GPUs
     schedule themselves, so they are accepted and ignored.  `outputs`
     (extension): per-rank host torch tensors to receive the results when the
     inputs are host torch tensors (e.g. pinned buffers reused across calls).
+    `via_plan` (extension) runs the algorithm as a lowered DSL plan on the GPU
+    interpreter instead of its hand-written kernel; the 2pa "port" variant
+    always does (its puts are PortChannel requests served by the proxy's
+    copy-engine DMA).  Plan ops round 2-byte types once per op.
     """
     import torch
     if kind not in _COLL:
@@ -234,7 +271,10 @@ def collective(kind: str, inputs, world, selector: Selector | None = None, dtype
         shape = {"allreduce": 0, "allgather": 0, "reducescatter": 0}[kind]
         outs = [t.new_empty(shape) for t in tensors]
         return outs if on_gpu else [_to_host(o, dtype) for o in outs]
-    if kind == "allreduce":
+    if via_plan or (name == "2pa" and var == "port"):
+        outs = _run_via_plan(kind, name, var or ("memory" if name == "2pa" else ""), tensors, elems,
+                             dtype, world)
+    elif kind == "allreduce":
         recv = [torch.empty_like(t) for t in tensors]
         run(kind, tensors, recv, elems, dtype, aid, world)
         outs = recv

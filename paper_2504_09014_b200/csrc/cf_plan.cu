@@ -9,7 +9,9 @@
 //   reduce  memory chan   : own dst += chan.dst's src      switch: own dst = sum_r src@r
 //   copy    memory chan   : own dst  = chan.dst's src      switch: src -> dst@r for all r
 //   reduce_put            : chan.dst's dst = own src + own src2
-//   flush                 : no-op (puts are executed by the issuing CTAs themselves)
+//   port put / signal     : a request to the host proxy (copy-engine DMA, then the
+//                           signal in stream order); flush waits for its completion
+//   memory put / flush    : executed by the CTAs themselves; memory flush is a no-op
 // Fusions (same results, fewer passes over memory):
 //   reduce chains on one destination -> one n-source reduce, plan order kept
 //   copy feeding such a chain         -> first source of the chain
@@ -55,6 +57,7 @@ struct Group {
   int32_t* d_meta = nullptr;  // begin | end | rank
   char** d_bufptr = nullptr;
   int32_t* d_zero = nullptr;
+  uint64_t* d_done = nullptr;  // proxy completion counters [nprog * K]
   int nops = 0;
 };
 
@@ -78,6 +81,7 @@ struct cfPlan {
   std::vector<std::vector<int>> zero_bufs;  // per rank
   std::vector<cf::plan::Group> groups;
   int n_device_ops = 0;
+  bool uses_port = false;             // port-channel ops go through the proxy
 };
 
 namespace cf {
@@ -139,10 +143,19 @@ std::vector<HOp> lower_program(const Plan& P, int pi, int es) {
         need(op.has_src && op.has_dst, "src and dst");
         check_ref(P, op.src, ch->src, false, op.src.size, w);
         check_ref(P, op.dst, ch->dst, false, op.src.size, w);
-        h.code = D_COPY;
         h.size = op.src.size;
         h.src = {{op.src.buf, ch->src, op.src.off, false}};
         h.dst = {{op.dst.buf, ch->dst, op.dst.off, false}};
+        if (ch->type == C_PORT) {
+          // PortChannel: the proxy copies with the copy engine, then signals
+          h.code = D_PORT_PUT;
+          h.chan = op.chan;
+          h.peer = ch->dst;
+          if (op.kind == P_PUT_WITH_SIGNAL) h.flags |= F_SIGNAL;
+          out.push_back(h);
+          break;
+        }
+        h.code = D_COPY;
         if (h.size > 0) out.push_back(h);
         if (op.kind == P_PUT_WITH_SIGNAL) {
           HOp s;
@@ -156,7 +169,7 @@ std::vector<HOp> lower_program(const Plan& P, int pi, int es) {
       }
       case P_SIGNAL:
         need_chan(false);
-        h.code = D_SIGNAL;
+        h.code = ch->type == C_PORT ? D_PORT_SIGNAL : D_SIGNAL;
         h.chan = op.chan;
         h.peer = ch->dst;
         out.push_back(h);
@@ -167,8 +180,13 @@ std::vector<HOp> lower_program(const Plan& P, int pi, int es) {
         h.chan = op.chan;
         out.push_back(h);
         break;
-      case P_FLUSH:
+      case P_FLUSH:   // memory-channel flush is a no-op (cf/channels.py:239-240)
         need_chan(true);
+        if (ch->type == C_PORT) {
+          h.code = D_PORT_FLUSH;
+          h.chan = op.chan;
+          out.push_back(h);
+        }
         break;
       case P_PUT_PACKETS: {
         need_chan(false);
@@ -301,7 +319,12 @@ bool overlaps(const R& a, long long asz, const R& b, long long bsz, int es) {
 }
 
 bool is_data(const HOp& h) {
-  return h.code == D_MULTI || h.code == D_COPY || h.code == D_PUT_PACKETS || h.code == D_READ_PACKETS;
+  return h.code == D_MULTI || h.code == D_COPY || h.code == D_PUT_PACKETS || h.code == D_READ_PACKETS ||
+         h.code == D_PORT_PUT;
+}
+
+bool port_signals(const HOp& h) {
+  return h.code == D_PORT_SIGNAL || (h.code == D_PORT_PUT && (h.flags & F_SIGNAL));
 }
 
 bool touches(const HOp& h, const R& r, long long size, int es, bool writes_only) {
@@ -550,9 +573,18 @@ cfStatus load(cfComm* c, const char* json, size_t len, int dtype_override, cfPla
   std::vector<long long> sig(P.chans.size(), 0);
   std::vector<int> waiter(P.chans.size(), -1);
   long long max_flag = 1;
+  std::vector<int> port_signaler(P.chans.size(), -1);
   for (size_t p = 0; p < hops.size(); p++)
     for (auto& o : hops[p]) {
-      if (o.code == D_SIGNAL) sig[o.chan]++;
+      if (o.code == D_SIGNAL || port_signals(o)) sig[o.chan]++;
+      if (port_signals(o)) {   // the proxy writes absolute counts: one signaling block per channel
+        if (port_signaler[o.chan] >= 0 && port_signaler[o.chan] != (int)p)
+          return fail(CF_E_PROTOCOL, "port channel '%s' is signalled from more than one thread block",
+                      P.chans[o.chan].id.c_str());
+        port_signaler[o.chan] = (int)p;
+        pl->uses_port = true;
+      }
+      if (o.code == D_PORT_PUT || o.code == D_PORT_FLUSH) pl->uses_port = true;
       if (o.code == D_WAIT) {
         if (waiter[o.chan] >= 0 && waiter[o.chan] != (int)p)
           return fail(CF_E_PROTOCOL, "channel '%s' is waited on by more than one thread block",
@@ -643,7 +675,7 @@ cfStatus load(cfComm* c, const char* json, size_t len, int dtype_override, cfPla
   // encode device ops
   for (size_t p = 0; p < hops.size(); p++) {
     std::vector<DevOp> dv;
-    std::map<int, int> wm;
+    std::map<int, int> wm, pm;
     for (auto& o : hops[p]) {
       DevOp d;
       memset(&d, 0, sizeof(d));
@@ -669,6 +701,16 @@ cfStatus load(cfComm* c, const char* json, size_t len, int dtype_override, cfPla
       }
       DevOp* prev = dv.empty() ? nullptr : &dv.back();
       switch (o.code) {
+        case D_PORT_PUT:
+        case D_PORT_SIGNAL:
+          d.id = o.chan;
+          d.peer = o.peer;
+          d.flags |= (uint8_t)(o.flags & F_SIGNAL);
+          if (port_signals(o)) {
+            d.m = (uint64_t)(++pm[o.chan]);
+            d.per_call = (uint64_t)sig[o.chan];
+          }
+          break;
         case D_SIGNAL:   // consecutive signals batch into one op (one thread per signal)
           if (prev && prev->code == D_SIGNAL && prev->ndst < kMaxDst) {
             prev->dst[prev->ndst++] = {o.chan, o.peer, 0};
@@ -804,6 +846,8 @@ cfStatus load(cfComm* c, const char* json, size_t len, int dtype_override, cfPla
     if (ok) ok = cudaMemcpy(G.d_bufptr, bp.data(), bp.size() * sizeof(char*), cudaMemcpyHostToDevice) == cudaSuccess;
     if (ok) ok = cudaMemcpy(G.d_zero, zl.data(), zl.size() * sizeof(int32_t), cudaMemcpyHostToDevice) == cudaSuccess;
     G.nops = (int)all.size();
+    if (ok) ok = cudaMalloc((void**)&G.d_done, std::max<size_t>(1, G.progs.size() * K) * sizeof(uint64_t)) == cudaSuccess &&
+                 cudaMemset(G.d_done, 0, std::max<size_t>(1, G.progs.size() * K) * sizeof(uint64_t)) == cudaSuccess;
     pl->groups.push_back(G);
     if (!ok) {
       cudaSetDevice(prev_dev);
@@ -812,6 +856,10 @@ cfStatus load(cfComm* c, const char* json, size_t len, int dtype_override, cfPla
     }
   }
   cudaSetDevice(prev_dev);
+  if (pl->uses_port) {
+    cfStatus ps = proxy_start(c);
+    if (ps != CF_OK) { cfPlanDestroy(pl.release()); return ps; }
+  }
   *out = pl.release();
   return CF_OK;
 }
@@ -890,6 +938,11 @@ extern "C" cfStatus cfPlanExecute(cfPlan_t pl, const void* const* inputs, void* 
     if (s != CF_OK) { cudaSetDevice(prev); return s; }
     void* args[] = {&a};
     a.window = kPlanWindow;
+    if (pl->uses_port) {
+      if (!proxy_alive(c)) { cudaSetDevice(prev); return fail(CF_E_PROXY_DOWN, "port-channel proxy is not running"); }
+      for (int li : c->groups[gi]) a.port[c->local[li].rank] = proxy_queue(c, li);
+      a.port_done = G.d_done;
+    }
     cudaError_t e = cudaLaunchKernel(kernel, dim3(np * pl->K), dim3(pl->threads), args,
                                      kPlanWindow * sizeof(DevOp), streams[c->groups[gi][0]]);
     if (e != cudaSuccess) {
@@ -944,6 +997,7 @@ extern "C" cfStatus cfPlanDestroy(cfPlan_t pl) {
     cudaFree(G.d_meta);
     cudaFree(G.d_bufptr);
     cudaFree(G.d_zero);
+    cudaFree(G.d_done);
   }
   for (size_t r = 0; r < pl->heap.size(); r++)
     if (pl->heap[r]) {

@@ -7,6 +7,7 @@
 #include <cstdint>
 #include <string>
 #include <vector>
+#include "cf_proxy.h"
 #include "device/cf_device.cuh"
 
 namespace cf {
@@ -80,14 +81,18 @@ enum DevCode : uint8_t {
   D_COPY,          // dst[*] = src0                               put / copy / switch broadcast
   D_PUT_PACKETS,   // payload -> LL packets                       cf/channels.py:244-280
   D_READ_PACKETS,  // LL packets -> payload                       cf/channels.py:303-330
+  D_PORT_PUT,      // port put (+signal): request to the proxy    cf/channels.py:80-108
+  D_PORT_SIGNAL,   // port signal, ordered after earlier puts     cf/channels.py:98-103
+  D_PORT_FLUSH,    // wait until the proxy completed every request  cf/channels.py:110-114
 };
-enum DevFlags : uint8_t { F_ZERO = 1, F_ROUND_EACH = 2, F_VEC = 4, F_LL16 = 8 };
+enum DevFlags : uint8_t { F_ZERO = 1, F_ROUND_EACH = 2, F_VEC = 4, F_LL16 = 8, F_SIGNAL = 16 };
 
 struct DRef {
-  int32_t buf;
+  int32_t buf;         // plan buffer index, or kAbsolute: `off` is the device address
   int32_t rank;
   uint64_t off;        // bytes
 };
+constexpr int32_t kAbsolute = -1;
 
 struct DevOp {
   uint8_t code, nsrc, ndst, flags;
@@ -137,6 +142,8 @@ struct PlanArgs {
   uint64_t* bars[CF_MAX_RANKS];
   int rank_ctas[CF_MAX_RANKS];
   int rank_leader[CF_MAX_RANKS];
+  PortQueue port[CF_MAX_RANKS];  // proxy request rings (plans with port channels)
+  uint64_t* port_done;           // [nprog * K] completion counters of this launch's CTAs
 };
 constexpr int kMaxBufs = 16;
 constexpr int kMaxZero = 16;

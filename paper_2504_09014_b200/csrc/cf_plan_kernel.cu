@@ -27,6 +27,7 @@ __device__ __forceinline__ void red_add_release(uint64_t* p, uint64_t v, bool gp
 }
 
 __device__ __forceinline__ char* ref_ptr(const PlanArgs& a, const DRef& r) {
+  if (r.buf == kAbsolute) return reinterpret_cast<char*>(r.off);   // plan-owned, resolved at load
   char* base;
   if (r.buf == a.in_buf && !a.input_private) base = a.io_in[r.rank];
   else if (r.buf == a.out_buf) base = a.io_out[r.rank];
@@ -241,6 +242,34 @@ __device__ void packet_op(const PlanArgs& a, const DevOp& op, int j, uint64_t e,
   }
 }
 
+// Port channel ops: thread 0 posts one proxy request for this CTA's slice
+// (copy-engine DMA), the signal (if any) targeting this CTA's lane of the
+// receiver with the absolute count (call-1)*signals_per_call + m.  The CTA's
+// prior writes to the source are published before the post.
+template <typename T>
+__device__ void port_op(const PlanArgs& a, const DevOp& op, int rank, int pid, int j, uint64_t e, RankState* rs,
+                        uint64_t& last) {
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  uint64_t src = 0, dst = 0, bytes = 0;
+  if (op.code == D_PORT_PUT) {
+    constexpr int V = 16 / sizeof(T);
+    const uint64_t size = op.size;
+    const uint64_t per = ((size + a.K - 1) / a.K + V - 1) / V * V;
+    const uint64_t lo = min((uint64_t)j * per, size), hi = min(lo + per, size);
+    if (hi > lo) {
+      src = (uint64_t)(ref_ptr(a, op.src[0]) + lo * sizeof(T));
+      dst = (uint64_t)(ref_ptr(a, op.dst[0]) + lo * sizeof(T));
+      bytes = (hi - lo) * sizeof(T);
+    }
+  }
+  const bool sig = op.code == D_PORT_SIGNAL || (op.flags & F_SIGNAL);
+  if (!bytes && !sig) return;
+  const uint64_t sem = sig ? (uint64_t)(a.lanes[op.peer] + (size_t)op.id * a.K + j) : 0;
+  const uint64_t val = sig ? (e - 1) * op.per_call + op.m : 0;
+  last = port_post(a.port[rank], src, dst, bytes, sem, val, (uint64_t)(a.port_done + (size_t)pid * a.K + j), rs);
+}
+
 // Prologue of a call, split over the rank's CTAs: copy the user input into the
 // private input buffer (plans that write their input, e.g. ring RS) and zero
 // the buffers the plan reads before writing (cf/executor.py:153-154).
@@ -285,6 +314,7 @@ __global__ void __launch_bounds__(512) plan_kernel(const __grid_constant__ PlanA
   // waits invalidate L1, which would otherwise send each field load to L2).
   extern __shared__ uint4 s_raw[];
   DevOp* s_ops = reinterpret_cast<DevOp*>(s_raw);
+  uint64_t port_last = ~0ull;   // thread 0: this CTA's most recent proxy ticket
   const int end = a.prog_end[pid];
   for (int w0 = a.prog_begin[pid]; w0 < end; w0 += a.window) {
     const int w1 = min(w0 + a.window, end);
@@ -329,11 +359,22 @@ __global__ void __launch_bounds__(512) plan_kernel(const __grid_constant__ PlanA
       case D_READ_PACKETS:
         packet_op<T>(a, op, j, e, rs);
         break;
+      case D_PORT_PUT:
+      case D_PORT_SIGNAL:
+        port_op<T>(a, op, rank, pid, j, e, rs, port_last);
+        break;
+      case D_PORT_FLUSH:
+        if (threadIdx.x == 0 && port_last != ~0ull) port_flush(a.port_done + (size_t)pid * a.K + j, port_last, rs);
+        __syncthreads();
+        break;
       default:
         break;
     }
   }
   }
+  // requests still in flight complete before the call ends (their data and
+  // signals are part of this call)
+  if (threadIdx.x == 0 && port_last != ~0ull) port_flush(a.port_done + (size_t)pid * a.K + j, port_last, rs);
   if (a.exit_barrier) rank_barrier(a, rank, e * per_call);
   __syncthreads();
   if (threadIdx.x == 0) {

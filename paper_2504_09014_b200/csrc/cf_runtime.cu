@@ -349,6 +349,7 @@ extern "C" cfStatus cfCommDestroy(cfComm_t c) {
   if (!c->local.empty()) cudaSetDevice(c->local[0].dev);
   for (auto& r : c->regs) release_reg(c, r);
   for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
+  proxy_stop(c);
   nvls_teardown(c);
   for (auto& lr : c->local) {
     if (lr.dev >= 0) cudaSetDevice(lr.dev);

@@ -14,6 +14,7 @@
 
 namespace cf {
 
+struct Proxy;
 cfStatus fail(cfStatus s, const char* fmt, ...);
 
 #define CF_CUDA(call)                                                                \
@@ -107,6 +108,7 @@ struct cfComm {
   std::map<std::pair<const void*, int>, int> occ;  // (kernel, device) -> CTAs/SM
   bool multicast_supported = false;
   cf::Nvls nvls;
+  cf::Proxy* proxy = nullptr;          // PortChannel proxy thread (started on demand)
 
   cf::RankState* state(int li) const { return (cf::RankState*)(local[li].heap + lay.state_off); }
   uint64_t* sem(int li, int p) const { return (uint64_t*)(peer_heap[li][p] + lay.sem_off); }
@@ -135,4 +137,8 @@ cfStatus join_streams(cfComm* c, int group, const cudaStream_t* streams, bool af
 bool multicast_capable(int dev);
 cfStatus nvls_setup_inprocess(cfComm* c);
 void nvls_teardown(cfComm* c);
+// PortChannel proxy (cf_proxy.cu)
+cfStatus proxy_start(cfComm* c);
+void proxy_stop(cfComm* c);
+bool proxy_alive(const cfComm* c);
 }  // namespace cf
