@@ -30,7 +30,10 @@ CUmulticastObjectProp mc_prop(const cfComm* c, size_t size) {
   memset(&p, 0, sizeof(p));
   p.numDevices = (unsigned)c->nranks;
   p.size = size;
-  p.handleTypes = c->multiprocess ? CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR : CU_MEM_HANDLE_TYPE_NONE;
+  // the driver rejects multicast objects without a shareable handle type
+  // (CUDA_ERROR_INVALID_VALUE, measured on B200), even in one process
+  (void)c;
+  p.handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
   p.flags = 0;
   return p;
 }
@@ -72,7 +75,7 @@ cfStatus bind_rank(cfComm* c, int li) {
   mp.type = CU_MEM_ALLOCATION_TYPE_PINNED;
   mp.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
   mp.location.id = dev;
-  mp.requestedHandleTypes = c->multiprocess ? CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR : CU_MEM_HANDLE_TYPE_NONE;
+  mp.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
   NvlsRank& nr = c->nvls.ranks[li];
   CUmemGenericAllocationHandle mem;
   CF_TRY(drv_check(p_cuMemCreate(&mem, c->nvls.size, &mp, 0), "cuMemCreate"));

@@ -82,6 +82,7 @@ struct cfPlan {
   std::vector<cf::plan::Group> groups;
   int n_device_ops = 0;
   bool uses_port = false;             // port-channel ops go through the proxy
+  bool has_prologue = false;          // per-call zeroing / private input copy
 };
 
 namespace cf {
@@ -810,6 +811,24 @@ cfStatus load(cfComm* c, const char* json, size_t len, int dtype_override, cfPla
     st.base.timeout_ns = c->cfg.spin_timeout_ns;
     cudaMemcpy(pl->heap[r] + pl->state_off, &st, sizeof(st), cudaMemcpyHostToDevice);
   }
+  // plan-owned buffers live at fixed addresses: bake them into the data ops so
+  // the interpreter resolves them without a table load
+  for (auto& prog : pl->prog_ops)
+    for (auto& d : prog) {
+      if (d.code != D_MULTI && d.code != D_COPY && d.code != D_PUT_PACKETS && d.code != D_READ_PACKETS &&
+          d.code != D_PORT_PUT)
+        continue;
+      auto bake = [&](DRef& r) {
+        const bool io = r.buf == pl->out_buf || (r.buf == pl->in_buf && !pl->input_private);
+        if (io || r.buf == kAbsolute) return;
+        r.off = (uint64_t)(pl->heap[r.rank] + pl->buf_off[r.buf]) + r.off;
+        r.buf = kAbsolute;
+      };
+      for (int k = 0; k < d.nsrc; k++) bake(d.src[k]);
+      for (int k = 0; k < d.ndst; k++) bake(d.dst[k]);
+    }
+  pl->has_prologue = pl->input_private;
+  for (auto& z : pl->zero_bufs) pl->has_prologue |= !z.empty();
   // device tables per device group
   for (size_t gi = 0; gi < c->groups.size(); gi++) {
     Group G;
@@ -938,6 +957,7 @@ extern "C" cfStatus cfPlanExecute(cfPlan_t pl, const void* const* inputs, void* 
     if (s != CF_OK) { cudaSetDevice(prev); return s; }
     void* args[] = {&a};
     a.window = kPlanWindow;
+    a.has_prologue = pl->has_prologue ? 1 : 0;
     if (pl->uses_port) {
       if (!proxy_alive(c)) { cudaSetDevice(prev); return fail(CF_E_PROXY_DOWN, "port-channel proxy is not running"); }
       for (int li : c->groups[gi]) a.port[c->local[li].rank] = proxy_queue(c, li);

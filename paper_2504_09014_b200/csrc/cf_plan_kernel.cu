@@ -305,7 +305,7 @@ __global__ void __launch_bounds__(512) plan_kernel(const __grid_constant__ PlanA
   if (threadIdx.x == 0) s_e = *(volatile uint64_t*)&rs->epoch + 1;
   __syncthreads();
   const uint64_t e = s_e;
-  prologue(a, rank);
+  if (a.has_prologue) prologue(a, rank);
   // rank barriers are numbered consecutively across calls (monotonic counters)
   const uint64_t per_call = (uint64_t)(a.entry_barrier + a.exit_barrier);
   if (a.entry_barrier) rank_barrier(a, rank, (e - 1) * per_call + 1);

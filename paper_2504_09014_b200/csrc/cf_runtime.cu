@@ -148,9 +148,12 @@ static int select_algo(const cfComm* c, int coll, size_t nbytes, int dtype) {
   if (coll == 2) return CF_ALGO_RS_DIRECT;
   if (c->nranks == 1) return CF_ALGO_2PA;
   if (coresident) {
-    // ranks share one GPU's memory: LL doubles HBM traffic, so only tiny
-    // messages use it; the pull two-shot moves the minimum bytes.
-    if (nbytes <= 16 * 1024) return CF_ALGO_1PA;
+    // Ranks share one GPU (one launch, no handshakes).  Measured (bench sweep,
+    // bf16, 8 ranks, L2 flushed): the whole-vector pull (1pa_hb) has the
+    // lowest latency up to 64 KiB (3.9-4.7 us vs 5.0-5.8 us for 2pa, 5.5-12 us
+    // for LL, which doubles the bytes); the two-shot pull moves the minimum
+    // bytes and wins from 256 KiB on (5.9 vs 6.4 us) to 1 GiB.
+    if (nbytes <= 64 * 1024) return CF_ALGO_1PA_HB;
     return CF_ALGO_2PA;
   }
   if (nbytes < 256 * 1024 && nbytes <= c->cfg.ll_max_bytes) return CF_ALGO_1PA;
@@ -671,7 +674,12 @@ extern "C" cfStatus cfAllReduce(cfComm_t c, const void* const* send, void* const
   const int n = c->nranks;
   const size_t es = dtype_size(dtype), V = 16 / es;
   const size_t bytes = count * es;
-  if (algo == CF_ALGO_AUTO) algo = select_algo(c, 0, bytes, dtype);
+  if (algo == CF_ALGO_AUTO) {
+    algo = select_algo(c, 0, bytes, dtype);
+    if (algo == CF_ALGO_1PA_HB)
+      for (size_t li = 0; li < c->local.size(); li++)
+        if (send[li] == recv[li]) algo = CF_ALGO_2PA;   // 1pa_hb cannot run in place
+  }
   if (algo == CF_ALGO_SWITCH_2PA && c->nvls.enabled) return nvls_allreduce(c, send, recv, count, dtype, streams);
   Job j;
   j.count = count;
