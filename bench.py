@@ -434,6 +434,8 @@ def run_multi_gpu(args):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    if os.environ.get("CF_BENCH_ONE_GPU"):   # path check on a 1-GPU box: ranks share cuda:0
+        local = 0
     torch.cuda.set_device(local)
     dist.init_process_group("gloo", init_method="env://")
     comm = Communicator(device=local)
@@ -461,9 +463,24 @@ def run_multi_gpu(args):
         torch.cuda.synchronize(dev)
     comm.check_device_error()
     t_local = e0.elapsed_time(e1) / 1e3 / args.steps
+    # e2e: pinned host input -> device -> all_reduce -> pinned host output, per step
+    host_in = send.cpu().pin_memory()
+    host_out = torch.empty_like(host_in).pin_memory()
+    e2e_local = []
+    for it in range(4):
+        torch.cuda.synchronize(dev)
+        dist.barrier()
+        t0 = time.perf_counter()
+        send.copy_(host_in, non_blocking=True)
+        comm.all_reduce(send, recv, algo="2pa")
+        host_out.copy_(recv, non_blocking=True)
+        torch.cuda.synchronize(dev)
+        if it:
+            e2e_local.append(time.perf_counter() - t0)
     times = [None] * world
-    dist.all_gather_object(times, t_local)
-    t = max(times)
+    dist.all_gather_object(times, (t_local, float(np.mean(e2e_local))))
+    t = max(x[0] for x in times)
+    te = max(x[1] for x in times)
     if rank == 0:
         value = busbw(HEAD_BYTES, t, world)
         print(json.dumps({
@@ -477,7 +494,12 @@ def run_multi_gpu(args):
                        "l2": "inputs larger than L2"},
             "pct_of_900": round(100 * value / 900, 2),
             "roofline": {"bound": "nvlink", "achieved": round(value, 1), "peak": 900.0,
-                         "unit": "GB/s", "frac": round(value / 900, 4), "traffic": None},
+                         "unit": "GB/s", "frac": round(value / 900, 4), "traffic": None,
+                         "note": "busbw per GPU per direction vs nominal NVLink 5"},
+            "e2e": {"value": round(busbw(HEAD_BYTES, te, world), 3), "unit": "GB/s",
+                    "h2d_bytes_per_step": HEAD_BYTES, "d2h_bytes_per_step": HEAD_BYTES,
+                    "ms_per_step": round(te * 1e3, 3),
+                    "api": "Communicator.all_reduce with pinned host copies (per rank)"},
             "gpu_launches": args.steps, "clocks": clk.summary()}))
     comm.close()
     dist.destroy_process_group()
