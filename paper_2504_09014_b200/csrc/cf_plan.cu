@@ -570,6 +570,38 @@ cfStatus load(cfComm* c, const char* json, size_t len, int dtype_override, cfPla
     return fail(f.s, "%s", f.m.c_str());
   }
 
+  // One launch holding every rank: a wait after a program's last data op only
+  // guards data the call's end publishes anyway (the kernel boundary is a
+  // barrier over all ranks), so such tail waits -- and the signals of channels
+  // whose every wait is a tail wait -- are dropped.
+  if (c->groups.size() == 1 && (int)c->local.size() == n) {
+    std::vector<char> all_tail(P.chans.size(), 1);
+    std::vector<std::vector<char>> tail(hops.size());
+    for (size_t p = 0; p < hops.size(); p++) {
+      int last = -1;
+      for (int i = 0; i < (int)hops[p].size(); i++)
+        if (is_data(hops[p][i])) last = i;
+      tail[p].assign(hops[p].size(), 0);
+      for (int i = 0; i < (int)hops[p].size(); i++) {
+        if (hops[p][i].code != D_WAIT) continue;
+        tail[p][i] = i > last;
+        if (i < last) all_tail[hops[p][i].chan] = 0;
+      }
+    }
+    for (size_t p = 0; p < hops.size(); p++) {
+      std::vector<HOp> keep;
+      for (size_t i = 0; i < hops[p].size(); i++) {
+        HOp& o = hops[p][i];
+        const bool elide = o.chan >= 0 && all_tail[o.chan];
+        if (o.code == D_WAIT && tail[p][i] && elide) continue;
+        if ((o.code == D_SIGNAL || o.code == D_PORT_SIGNAL) && elide) continue;
+        if (o.code == D_PORT_PUT && elide) o.flags &= ~F_SIGNAL;
+        keep.push_back(o);
+      }
+      hops[p].swap(keep);
+    }
+  }
+
   // signals per call per channel; waits restricted to one program per channel
   std::vector<long long> sig(P.chans.size(), 0);
   std::vector<int> waiter(P.chans.size(), -1);
