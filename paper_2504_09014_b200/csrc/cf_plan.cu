@@ -577,6 +577,16 @@ cfStatus load(cfComm* c, const char* json, size_t len, int dtype_override, cfPla
   if (c->groups.size() == 1 && (int)c->local.size() == n) {
     std::vector<char> all_tail(P.chans.size(), 1);
     std::vector<std::vector<char>> tail(hops.size());
+    // a channel with fewer signals than waits deadlocks in the reference
+    // (cf/sched.py:93-99); keep its waits so the device reports E_DEADLOCK too
+    std::vector<long long> nsig(P.chans.size(), 0), nwait(P.chans.size(), 0);
+    for (auto& h : hops)
+      for (auto& o : h) {
+        if (o.code == D_SIGNAL || port_signals(o)) nsig[o.chan]++;
+        if (o.code == D_WAIT) nwait[o.chan]++;
+      }
+    for (size_t ch = 0; ch < P.chans.size(); ch++)
+      if (nsig[ch] < nwait[ch]) all_tail[ch] = 0;
     for (size_t p = 0; p < hops.size(); p++) {
       int last = -1;
       for (int i = 0; i < (int)hops[p].size(); i++)
