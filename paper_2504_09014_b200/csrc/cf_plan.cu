@@ -471,6 +471,92 @@ void add_interval(std::vector<Interval>& iv, long long lo, long long hi) {
   iv.swap(m);
 }
 
+// ------------------------------------------------------------------ read_packets -> reduce fusion
+
+bool data_code(int code) {
+  return code == D_MULTI || code == D_COPY || code == D_PUT_PACKETS || code == D_READ_PACKETS ||
+         code == D_PORT_PUT;
+}
+
+// byte span of a DRef touched by op d (payload or packet layout)
+void dref_span(const DevOp& d, const DRef& r, bool packet, int es, uint64_t& lo, uint64_t& hi) {
+  lo = r.off;
+  hi = r.off + d.size * es * (packet ? 2 : 1);
+}
+
+bool same_loc(const DRef& a, const DRef& b) { return a.buf == b.buf && a.rank == b.rank; }
+
+// Is byte range [lo, hi) of location `loc` touched by any data op other than
+// ops (pa, ia) and (pb, ib)?
+bool touched_elsewhere(const cfPlan* pl, const DRef& loc, uint64_t lo, uint64_t hi, size_t pa, size_t ia,
+                       size_t pb, size_t ib) {
+  for (size_t p = 0; p < pl->prog_ops.size(); p++)
+    for (size_t i = 0; i < pl->prog_ops[p].size(); i++) {
+      if ((p == pa && i == ia) || (p == pb && i == ib)) continue;
+      const DevOp& d = pl->prog_ops[p][i];
+      if (!data_code(d.code)) continue;
+      for (int k = 0; k < d.nsrc + d.ndst; k++) {
+        const bool is_src = k < d.nsrc;
+        const DRef& r = is_src ? d.src[k] : d.dst[k - d.nsrc];
+        if (!same_loc(r, loc)) continue;
+        const bool packet = (d.code == D_READ_PACKETS && is_src) || (d.code == D_PUT_PACKETS && !is_src) ||
+                            (d.code == D_MULTI && is_src && ((d.pkt_mask >> k) & 1u));
+        uint64_t a0, a1;
+        dref_span(d, r, packet, pl->es, a0, a1);
+        if (a0 < hi && lo < a1) return true;
+      }
+    }
+  return false;
+}
+
+// [read_packets P_k -> T_k]* ; tb_sync ; reduce(... T_k ...)  ==>  reduce(... P_k ...)
+// when T_k is scratch nobody else touches: the reduction reads the LL16
+// packets directly (one pass, no temporary), exactly the one-shot LL kernel.
+void fuse_packet_reads(cfPlan* pl) {
+  for (size_t p = 0; p < pl->prog_ops.size(); p++) {
+    auto& ops = pl->prog_ops[p];
+    for (size_t m = 0; m < ops.size(); m++) {
+      DevOp& M = ops[m];
+      if (M.code != D_MULTI || !(M.flags & F_VEC)) continue;
+      for (size_t r = m; r-- > 0;) {
+        DevOp& R = ops[r];
+        if (R.code == D_SYNC_CTA) continue;
+        if (R.code != D_READ_PACKETS) break;
+        if (!(R.flags & F_LL16) || R.size != M.size) break;
+        for (int k = 0; k < R.nsrc; k++) {
+          for (int s = 0; s < M.nsrc; s++) {
+            if ((M.pkt_mask >> s) & 1u) continue;
+            if (!same_loc(M.src[s], R.dst[k]) || M.src[s].off != R.dst[k].off) continue;
+            if (R.dst[k].buf != kAbsolute) continue;   // plan-owned scratch only, never user I/O
+            uint64_t lo, hi;
+            dref_span(R, R.dst[k], false, pl->es, lo, hi);
+            if (touched_elsewhere(pl, R.dst[k], lo, hi, p, r, p, m)) continue;
+            M.src[s] = R.src[k];
+            M.llflag_k[s] = R.llflag_k[k];
+            M.pkt_mask |= 1u << s;
+            for (int q = k; q + 1 < R.nsrc; q++) {   // drop pair k from the batch
+              R.src[q] = R.src[q + 1];
+              R.dst[q] = R.dst[q + 1];
+              R.llflag_k[q] = R.llflag_k[q + 1];
+            }
+            R.nsrc--;
+            R.ndst--;
+            k--;
+            break;
+          }
+        }
+        if (R.nsrc == 0) R.code = D_NOP;
+        break;
+      }
+    }
+    std::vector<DevOp> keep;
+    for (auto& d : ops)
+      if (d.code != D_NOP) keep.push_back(d);
+    pl->n_device_ops -= (int)(ops.size() - keep.size());
+    ops.swap(keep);
+  }
+}
+
 }  // namespace
 
 // ------------------------------------------------------------------ load
@@ -869,6 +955,7 @@ cfStatus load(cfComm* c, const char* json, size_t len, int dtype_override, cfPla
       for (int k = 0; k < d.nsrc; k++) bake(d.src[k]);
       for (int k = 0; k < d.ndst; k++) bake(d.dst[k]);
     }
+  fuse_packet_reads(pl.get());
   pl->has_prologue = pl->input_private;
   for (auto& z : pl->zero_bufs) pl->has_prologue |= !z.empty();
   // device tables per device group

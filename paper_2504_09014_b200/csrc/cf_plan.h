@@ -108,7 +108,9 @@ struct DevOp {
   //   D_WAIT    src[k] = {channel, signals per call, m}   (nsrc waits)
   DRef src[kMaxSrc];
   DRef dst[kMaxDst];
-  uint32_t llflag_k[kMaxDst];  // D_READ_PACKETS batch: plan flag of source k
+  uint32_t llflag_k[kMaxSrc];  // plan flag of packet source k (READ_PACKETS batch, MULTI pkt_mask)
+  uint32_t pkt_mask;           // D_MULTI: sources read straight from LL16 packet areas
+  uint32_t pad_[3];
 };
 
 // Per-rank execution state of one loaded plan (in the plan heap of the rank).

@@ -109,11 +109,39 @@ __device__ __forceinline__ void acc_vec(typename Vec<T>::Acc* acc, uint4 x, bool
   }
 }
 
-// D_MULTI / D_COPY on this CTA's slice [lo, hi) of the op's elements.
+// Issue the 16-byte payload load of source k at vector v: a plain vector, or
+// the two LL16 packets carrying it (flags checked later, see finish_src).
 template <typename T>
-__device__ void data_op(const PlanArgs& a, const DevOp& op, int j) {
+__device__ __forceinline__ void issue_src(const char* p, size_t v, int nval, bool pkt, uint4& r0, uint4& r1) {
+  if (!pkt) {
+    r0 = load_part<T>(p + v * 16, nval);
+    return;
+  }
+  r0 = ld16_volatile(p + v * 32);
+  r1 = nval * (int)sizeof(T) > 8 ? ld16_volatile(p + v * 32 + 16) : make_uint4(0, 0, 0, 0);
+}
+template <typename T>
+__device__ __forceinline__ uint4 finish_src(const char* p, size_t v, int nval, bool pkt, uint32_t flag, uint4 r0,
+                                            uint4 r1, RankState* rs) {
+  if (!pkt) return r0;
+  uint2 d0 = make_uint2(r0.x, r0.z), d1 = make_uint2(r1.x, r1.z);
+  if (r0.y != flag || r0.w != flag) d0 = ll16_get(p + v * 32, flag, rs);
+  if (nval * (int)sizeof(T) > 8) {
+    if (r1.y != flag || r1.w != flag) d1 = ll16_get(p + v * 32 + 16, flag, rs);
+  } else {
+    d1 = make_uint2(0, 0);
+  }
+  return make_uint4(d0.x, d0.y, d1.x, d1.y);
+}
+
+// D_MULTI / D_COPY on this CTA's slice [lo, hi) of the op's elements.  MULTI
+// sources flagged in pkt_mask are read straight from LL16 packet areas (a
+// read_packets fused into the reduce).
+template <typename T>
+__device__ void data_op(const PlanArgs& a, const DevOp& op, int j, uint64_t e, RankState* rs) {
   using A = typename Vec<T>::Acc;
   constexpr int V = Vec<T>::N;
+  constexpr int B = 8;   // sources in flight per round
   const uint64_t size = op.size;
   const uint64_t per = ((size + a.K - 1) / a.K + V - 1) / V * V;
   const uint64_t lo = min((uint64_t)j * per, size), hi = min(lo + per, size);
@@ -121,9 +149,14 @@ __device__ void data_op(const PlanArgs& a, const DevOp& op, int j) {
   const int nsrc = op.nsrc, ndst = op.ndst;
   const bool zero = op.flags & F_ZERO, round_each = op.flags & F_ROUND_EACH;
   const bool multi = op.code == D_MULTI;
+  const uint32_t pkt = op.pkt_mask;
   const char* src[kMaxSrc];
   char* dst[kMaxDst];
-  for (int k = 0; k < nsrc; k++) src[k] = ref_ptr(a, op.src[k]);
+  uint32_t flag[kMaxSrc];
+  for (int k = 0; k < nsrc; k++) {
+    src[k] = ref_ptr(a, op.src[k]);
+    flag[k] = (pkt >> k) & 1u ? runtime_flag(e, a.flag_stride, op.llflag_k[k]) : 0u;
+  }
   for (int k = 0; k < ndst; k++) dst[k] = ref_ptr(a, op.dst[k]);
   if (op.flags & F_VEC) {
     for (uint64_t v = lo / V + threadIdx.x; v * V < hi; v += blockDim.x) {
@@ -134,23 +167,24 @@ __device__ void data_op(const PlanArgs& a, const DevOp& op, int j) {
         res = load_part<T>(src[0] + boff, nval);
       } else {
         A acc[V];
-        int k = 0;
         if (zero) {
 #pragma unroll
           for (int i = 0; i < V; i++) acc[i] = A(0);
-        } else {
-          Vec<T>::load(load_part<T>(src[0] + boff, nval), acc);
-          k = 1;
         }
-        for (; k + 4 <= nsrc; k += 4) {   // four loads in flight per step
-          const uint4 x0 = load_part<T>(src[k] + boff, nval), x1 = load_part<T>(src[k + 1] + boff, nval);
-          const uint4 x2 = load_part<T>(src[k + 2] + boff, nval), x3 = load_part<T>(src[k + 3] + boff, nval);
-          acc_vec<T>(acc, x0, round_each);
-          acc_vec<T>(acc, x1, round_each);
-          acc_vec<T>(acc, x2, round_each);
-          acc_vec<T>(acc, x3, round_each);
+        for (int k0 = 0; k0 < nsrc; k0 += B) {   // B sources' loads in flight per round
+          uint4 r0[B], r1[B];
+#pragma unroll
+          for (int i = 0; i < B; i++)
+            if (k0 + i < nsrc) issue_src<T>(src[k0 + i], v, nval, (pkt >> (k0 + i)) & 1u, r0[i], r1[i]);
+#pragma unroll
+          for (int i = 0; i < B; i++) {
+            const int k = k0 + i;
+            if (k >= nsrc) break;
+            const uint4 x = finish_src<T>(src[k], v, nval, (pkt >> k) & 1u, flag[k], r0[i], r1[i], rs);
+            if (k == 0 && !zero) Vec<T>::load(x, acc);
+            else acc_vec<T>(acc, x, round_each);
+          }
         }
-        for (; k < nsrc; k++) acc_vec<T>(acc, load_part<T>(src[k] + boff, nval), round_each);
         res = Vec<T>::store(acc);
       }
       for (int d = 0; d < ndst; d++) store_part<T>(dst[d] + boff, res, nval);
@@ -353,7 +387,7 @@ __global__ void __launch_bounds__(512) plan_kernel(const __grid_constant__ PlanA
         break;
       case D_MULTI:
       case D_COPY:
-        data_op<T>(a, op, j);
+        data_op<T>(a, op, j, e, rs);
         break;
       case D_PUT_PACKETS:
       case D_READ_PACKETS:
