@@ -148,6 +148,19 @@ CF_API cfStatus cfNvlsCreate(cfComm_t comm, int* fd);
 CF_API cfStatus cfNvlsImport(cfComm_t comm, int fd);
 CF_API cfStatus cfNvlsBind(cfComm_t comm);
 
+/* Channels for user kernels (the Primitive API; reference
+ * MemoryChannel / PortChannel, cf/channels.py:54-330).  Fills `handle` with a
+ * device struct (cf::MemoryChannelDevice / cf::PortChannelDevice from
+ * csrc/device/cf_device.cuh and csrc/cf_proxy.h) that kernels of both
+ * endpoints take by value.  `tag` (< CF_MAX_CHANNEL_TAGS) names the channel's
+ * semaphore slot for the (src, dst) pair; one-process communicators. */
+#define CF_CHANNEL_HANDLE_BYTES 256
+#define CF_MAX_CHANNEL_TAGS 64
+CF_API cfStatus cfMemoryChannelCreate(cfComm_t comm, int src_rank, int dst_rank, int tag, void* src_buf,
+                                      void* dst_buf, void* handle, size_t* handle_bytes);
+CF_API cfStatus cfPortChannelCreate(cfComm_t comm, int src_rank, int dst_rank, int tag, void* src_buf,
+                                    void* dst_buf, void* handle, size_t* handle_bytes);
+
 CF_API cfStatus cfCommNumRanks(cfComm_t comm, int* nranks);
 CF_API cfStatus cfCommLocalRanks(cfComm_t comm, int* nlocal, int* ranks /* nullable, nlocal entries */);
 CF_API cfStatus cfCommMulticastSupported(cfComm_t comm, int* supported);

@@ -29,7 +29,8 @@ ALGO_NAMES = {v: k for k, v in ALGOS.items()}
 EXPORTS = (
     "cfStatusCode", "cfLastErrorMessage", "cfVersion", "cfCommInitAll", "cfCommCreateRank",
     "cfCommGetHandle", "cfCommConnect", "cfCommDestroy", "cfBufferExport", "cfBufferImport",
-    "cfBufferRelease", "cfDeviceMulticastSupported", "cfNvlsCreate", "cfNvlsImport", "cfNvlsBind", "cfCommNumRanks",
+    "cfBufferRelease", "cfMemoryChannelCreate", "cfPortChannelCreate",
+    "cfDeviceMulticastSupported", "cfNvlsCreate", "cfNvlsImport", "cfNvlsBind", "cfCommNumRanks",
     "cfCommLocalRanks",
     "cfCommMulticastSupported", "cfCommLastDeviceError", "cfCommClearDeviceError", "cfAllReduce",
     "cfAllGather", "cfReduceScatter", "cfSelectAlgorithm", "cfPlanLoad", "cfPlanExecute",
@@ -63,6 +64,8 @@ _PROTOS = {
     "cfBufferImport": ([vp, vp, vp, sz], i32),
     "cfBufferRelease": ([vp, vp], i32),
     "cfDeviceMulticastSupported": ([i32, P(i32)], i32),
+    "cfMemoryChannelCreate": ([vp, i32, i32, i32, vp, vp, vp, P(sz)], i32),
+    "cfPortChannelCreate": ([vp, i32, i32, i32, vp, vp, vp, P(sz)], i32),
     "cfNvlsCreate": ([vp, P(i32)], i32),
     "cfNvlsImport": ([vp, i32], i32),
     "cfNvlsBind": ([vp], i32),

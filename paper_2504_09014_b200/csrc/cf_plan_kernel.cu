@@ -158,7 +158,39 @@ __device__ void data_op(const PlanArgs& a, const DevOp& op, int j, uint64_t e, R
     flag[k] = (pkt >> k) & 1u ? runtime_flag(e, a.flag_stride, op.llflag_k[k]) : 0u;
   }
   for (int k = 0; k < ndst; k++) dst[k] = ref_ptr(a, op.dst[k]);
-  if (op.flags & F_VEC) {
+  if ((op.flags & F_VEC) && multi && nsrc <= B && !pkt) {
+    // common fused shape (n-source pull-reduce + push): pointers in
+    // registers, all sources in flight, statically indexed
+    const char* ps[B];
+    char* pd[kMaxDst];
+#pragma unroll
+    for (int i = 0; i < B; i++) ps[i] = i < nsrc ? src[i] : nullptr;
+#pragma unroll
+    for (int i = 0; i < kMaxDst; i++) pd[i] = i < ndst ? dst[i] : nullptr;
+    for (uint64_t v = lo / V + threadIdx.x; v * V < hi; v += blockDim.x) {
+      const int nval = (int)min((uint64_t)V, hi - v * V);
+      const size_t boff = (size_t)v * 16;
+      uint4 x[B];
+#pragma unroll
+      for (int i = 0; i < B; i++)
+        if (i < nsrc) x[i] = load_part<T>(ps[i] + boff, nval);
+      A acc[V];
+      if (zero) {
+#pragma unroll
+        for (int i = 0; i < V; i++) acc[i] = A(0);
+        acc_vec<T>(acc, x[0], round_each);
+      } else {
+        Vec<T>::load(x[0], acc);
+      }
+#pragma unroll
+      for (int i = 1; i < B; i++)
+        if (i < nsrc) acc_vec<T>(acc, x[i], round_each);
+      const uint4 res = Vec<T>::store(acc);
+#pragma unroll
+      for (int d = 0; d < kMaxDst; d++)
+        if (d < ndst) store_part<T>(pd[d] + boff, res, nval);
+    }
+  } else if (op.flags & F_VEC) {
     for (uint64_t v = lo / V + threadIdx.x; v * V < hi; v += blockDim.x) {
       const int nval = (int)min((uint64_t)V, hi - v * V);
       const size_t boff = (size_t)v * 16;

@@ -85,4 +85,44 @@ __device__ __forceinline__ void port_flush(const uint64_t* done, uint64_t t, Ran
 }
 #endif
 
+// PortChannel handle for user kernels (Primitive API, cf/channels.py:54-150):
+// put / signal / put_with_signal / flush on the source rank (one thread per
+// channel), wait on the destination rank.  Requests go to the source rank's
+// proxy, which copies with the copy engine and then writes the semaphore.
+struct PortChannelDevice {
+  PortQueue q;
+  char* src_buf;            // source rank's buffer
+  char* dst_buf;            // destination rank's buffer (UVA address for the DMA engine)
+  uint64_t* sem;            // destination semaphore slot
+  uint64_t* sent;           // source side: signals issued (absolute count)
+  uint64_t* done;           // source side: completion counter written by the proxy
+  uint64_t* last;           // source side: last ticket + 1 (0: nothing issued)
+  uint64_t* expected;       // destination side: waits issued
+  RankState* src_st;
+  RankState* dst_st;
+#ifdef __CUDACC__
+  __device__ void put(size_t dst_off, size_t src_off, size_t bytes) const {
+    *last = port_post(q, (uint64_t)(src_buf + src_off), (uint64_t)(dst_buf + dst_off), bytes, 0, 0,
+                      (uint64_t)done, src_st) + 1;
+  }
+  __device__ void signal() const {
+    const uint64_t v = ++*sent;
+    *last = port_post(q, 0, 0, 0, (uint64_t)sem, v, (uint64_t)done, src_st) + 1;
+  }
+  __device__ void put_with_signal(size_t dst_off, size_t src_off, size_t bytes) const {
+    const uint64_t v = ++*sent;
+    *last = port_post(q, (uint64_t)(src_buf + src_off), (uint64_t)(dst_buf + dst_off), bytes, (uint64_t)sem, v,
+                      (uint64_t)done, src_st) + 1;
+  }
+  // every request issued so far completed (the source may be reused)
+  __device__ void flush() const {
+    if (*last) port_flush(done, *last - 1, src_st);
+  }
+  __device__ bool wait() const {
+    const uint64_t target = ++*expected;
+    return wait_geq(sem, target, dst_st, false);
+  }
+#endif
+};
+
 }  // namespace cf

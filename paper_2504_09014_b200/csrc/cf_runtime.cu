@@ -33,7 +33,8 @@ void HeapLayout::compute(int nranks, size_t ll_max) {
   sem_off = 256;
   sem_bytes = (size_t)CF_MAX_RANKS * CF_MAX_BLOCKS * sizeof(uint64_t);
   ack_off = round_up(sem_off + sem_bytes, 256);
-  ring_off = round_up(ack_off + sem_bytes, 4096);
+  chan_off = round_up(ack_off + sem_bytes, 256);
+  ring_off = round_up(chan_off + 5 * (size_t)CF_MAX_RANKS * CF_MAX_CHANNEL_TAGS * sizeof(uint64_t), 4096);
   scr_off = round_up(ring_off + kRingBytes, 4096);
   // one LL16 packet (16 B) per 8 payload bytes: a slot holds 2*ll_max bytes
   slot = round_up(2 * ll_max + 64, 256);

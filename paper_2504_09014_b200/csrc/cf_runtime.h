@@ -41,6 +41,7 @@ struct HeapLayout {
   size_t sem_off = 256;
   size_t sem_bytes = (size_t)CF_MAX_RANKS * CF_MAX_BLOCKS * sizeof(uint64_t);
   size_t ack_off = 0;
+  size_t chan_off = 0;      // user channels: 5 arrays [CF_MAX_RANKS][CF_MAX_CHANNEL_TAGS] u64
   size_t ring_off = 0;
   size_t scr_off = 0, scr_bytes = 0;
   size_t slot = 0, half = 0;

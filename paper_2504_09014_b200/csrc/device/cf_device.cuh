@@ -288,4 +288,58 @@ __device__ __forceinline__ int order_src(int mode, int k, int lead, int n) {
   return k;
 }
 
+// ---------------------------------------------------------------- channels
+//
+// The Primitive API for user kernels.  A channel handle is
+// built on the host (cfMemoryChannelCreate / cfPortChannelCreate) and passed
+// by value to the kernels of BOTH endpoints: put / signal / put_packets /
+// flush run on the source rank, wait / read_packets on the destination rank
+// (cf/channels.py:54-330).  Semaphores count (signal = +1, wait = expected+1
+// then spin), so k signals satisfy k waits (reference test_channels.py:185-229).
+
+struct MemoryChannelDevice {
+  char* src_buf;            // source rank's buffer (source device)
+  char* dst_buf;            // destination rank's buffer as mapped on the source device
+  char* dst_local;          // destination rank's buffer on the destination device
+  uint64_t* sem;            // semaphore slot in the destination heap
+  uint64_t* expected;       // destination-side wait counter
+  RankState* src_st;
+  RankState* dst_st;
+  int gpu_scope;            // both endpoints on one device
+  int pad_;
+
+  // put (HB): cooperative 16-byte copy src_buf[src_off..] -> dst_buf[dst_off..]
+  // by threads tid of nthreads; visible to the peer after signal().
+  __device__ void put(size_t dst_off, size_t src_off, size_t bytes, int tid, int nthreads) const {
+    const size_t nv = bytes / 16;
+    for (size_t i = tid; i < nv; i += nthreads) st16(dst_buf + dst_off + i * 16, ld16(src_buf + src_off + i * 16));
+    for (size_t i = nv * 16 + tid; i < bytes; i += nthreads) dst_buf[dst_off + i] = src_buf[src_off + i];
+  }
+  // signal (one thread, after a block barrier covering the puts it publishes)
+  __device__ void signal() const {
+    fence_publish(gpu_scope);
+    if (gpu_scope) asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(sem) : "memory");
+    else asm volatile("red.release.sys.global.add.u64 [%0], 1;" ::"l"(sem) : "memory");
+  }
+  // wait (one thread on the destination rank): false on timeout (E_DEADLOCK)
+  __device__ bool wait() const {
+    const uint64_t target = ++*expected;
+    return wait_geq(sem, target, dst_st, gpu_scope);
+  }
+  __device__ void flush() const {}   // memory channel: the put completed in place
+  // put_packets (LL): `bytes` (multiple of 8) as LL16 packets at packet offset
+  // pkt_off of the destination buffer; no semaphore needed.
+  __device__ void put_packets(size_t pkt_off, size_t src_off, size_t bytes, uint32_t flag, int tid,
+                              int nthreads) const {
+    for (size_t u = tid; u < bytes / 8; u += nthreads)
+      ll16_put(dst_buf + pkt_off + u * 16, *reinterpret_cast<const uint2*>(src_buf + src_off + u * 8), flag);
+  }
+  // read_packets (destination rank): decode packets at pkt_off of the local
+  // destination buffer into out, spinning until every flag is stamped.
+  __device__ void read_packets(char* out, size_t pkt_off, size_t bytes, uint32_t flag, int tid, int nthreads) const {
+    for (size_t u = tid; u < bytes / 8; u += nthreads)
+      *reinterpret_cast<uint2*>(out + u * 8) = ll16_get(dst_local + pkt_off + u * 16, flag, dst_st);
+  }
+};
+
 }  // namespace cf

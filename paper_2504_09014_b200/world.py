@@ -130,6 +130,23 @@ class World:
             from .errors import raise_status
             raise_status(code.value, "device-side wait timed out (peer never signalled)")
 
+    def _channel(self, fn, src, dst, tag, src_buf, dst_buf) -> bytes:
+        buf = ctypes.create_string_buffer(256)
+        nbytes = ctypes.c_size_t(256)
+        _lib.check(fn(self.comm, int(src), int(dst), int(tag), src_buf.data_ptr(), dst_buf.data_ptr(),
+                      buf, ctypes.byref(nbytes)))
+        return buf.raw[:nbytes.value]
+
+    def memory_channel(self, src: int, dst: int, tag: int, src_buf, dst_buf) -> bytes:
+        """Device handle of a MemoryChannel src -> dst (cf/channels.py:153-300) over
+        two CUDA tensors, for user kernels (cf::MemoryChannelDevice)."""
+        return self._channel(_lib.lib().cfMemoryChannelCreate, src, dst, tag, src_buf, dst_buf)
+
+    def port_channel(self, src: int, dst: int, tag: int, src_buf, dst_buf) -> bytes:
+        """Device handle of a PortChannel src -> dst (cf/channels.py:54-150): puts
+        are copy-engine DMA issued by libcf's proxy (cf::PortChannelDevice)."""
+        return self._channel(_lib.lib().cfPortChannelCreate, src, dst, tag, src_buf, dst_buf)
+
     def multicast_supported(self) -> bool:
         v = ctypes.c_int()
         _lib.check(_lib.lib().cfCommMulticastSupported(self.comm, ctypes.byref(v)))

@@ -1,0 +1,86 @@
+// Test kernels for the device Primitive API (cf_device.cuh / cf_proxy.h):
+// a ring pass where rank r sends its buffer to rank r+1 through a user
+// channel.  All ranks are co-resident CTAs of one launch (blockIdx.y = rank).
+// Test infrastructure: built into tests/kernels/ by __graft_entry__.build().
+#include <cuda_runtime.h>
+#include "cf_proxy.h"
+#include "device/cf_device.cuh"
+
+using namespace cf;
+
+__global__ void mem_ring(const MemoryChannelDevice* tx, const MemoryChannelDevice* rx, size_t bytes, int ll,
+                         uint32_t flag, char* const* outs, int rounds) {
+  const int r = blockIdx.y, tid = threadIdx.x, nt = blockDim.x;
+  const MemoryChannelDevice& t = tx[r];
+  const MemoryChannelDevice& x = rx[r];
+  for (int k = 0; k < rounds; k++) {
+    if (!ll) {
+      t.put(0, 0, bytes, tid, nt);
+      __syncthreads();
+      if (tid == 0) t.signal();
+      if (tid == 0) x.wait();
+      __syncthreads();
+      for (size_t i = tid; i < bytes; i += nt) outs[r][i] = x.dst_local[i];
+      __syncthreads();
+    } else {
+      t.put_packets(2 * bytes * k, 0, bytes, flag + k, tid, nt);   // fresh packet area per round
+      x.read_packets(outs[r], 2 * bytes * k, bytes, flag + k, tid, nt);
+      __syncthreads();
+    }
+  }
+}
+
+__global__ void port_ring(const PortChannelDevice* tx, const PortChannelDevice* rx, size_t bytes,
+                          char* const* outs, int rounds) {
+  const int r = blockIdx.y, tid = threadIdx.x;
+  for (int k = 0; k < rounds; k++) {
+    if (tid == 0) {
+      if (k & 1) {
+        tx[r].put(0, 0, bytes);
+        tx[r].signal();
+      } else {
+        tx[r].put_with_signal(0, 0, bytes);
+      }
+      tx[r].flush();
+      rx[r].wait();
+    }
+    __syncthreads();
+    for (size_t i = tid; i < bytes; i += blockDim.x) outs[r][i] = rx[r].dst_buf[i];
+    __syncthreads();
+  }
+}
+
+template <typename H>
+static int upload(const void* host, int n, H** dev) {
+  if (cudaMalloc((void**)dev, sizeof(H) * n) != cudaSuccess) return 1;
+  return cudaMemcpy(*dev, host, sizeof(H) * n, cudaMemcpyHostToDevice) != cudaSuccess;
+}
+
+extern "C" int cftest_mem_ring(const void* tx, const void* rx, int n, size_t bytes, int ll, unsigned flag,
+                               void* const* outs, int rounds) {
+  MemoryChannelDevice *dtx, *drx;
+  char** douts;
+  if (upload(tx, n, &dtx) || upload(rx, n, &drx)) return 1;
+  if (cudaMalloc((void**)&douts, sizeof(char*) * n) != cudaSuccess) return 1;
+  cudaMemcpy(douts, outs, sizeof(char*) * n, cudaMemcpyHostToDevice);
+  mem_ring<<<dim3(1, n), 256>>>(dtx, drx, bytes, ll, flag, douts, rounds);
+  int rc = cudaDeviceSynchronize() != cudaSuccess;
+  cudaFree(dtx);
+  cudaFree(drx);
+  cudaFree(douts);
+  return rc;
+}
+
+extern "C" int cftest_port_ring(const void* tx, const void* rx, int n, size_t bytes, void* const* outs, int rounds) {
+  PortChannelDevice *dtx, *drx;
+  char** douts;
+  if (upload(tx, n, &dtx) || upload(rx, n, &drx)) return 1;
+  if (cudaMalloc((void**)&douts, sizeof(char*) * n) != cudaSuccess) return 1;
+  cudaMemcpy(douts, outs, sizeof(char*) * n, cudaMemcpyHostToDevice);
+  port_ring<<<dim3(1, n), 64>>>(dtx, drx, bytes, douts, rounds);
+  int rc = cudaDeviceSynchronize() != cudaSuccess;
+  cudaFree(dtx);
+  cudaFree(drx);
+  cudaFree(douts);
+  return rc;
+}
