@@ -52,7 +52,7 @@ __device__ __forceinline__ void counter_barrier(uint64_t* ctr, uint64_t target, 
 
 // All CTAs of `rank` meet; the rank's leader CTA exchanges `k` with every
 // other rank's leader, then releases its rank.
-__device__ void rank_barrier(const PlanArgs& a, int rank, uint64_t k) {
+__device__ __noinline__ void rank_barrier(const PlanArgs& a, int rank, uint64_t k) {
   PlanState* ps = a.st[rank];
   const bool gpu = a.gpu_scope;
   __syncthreads();
@@ -138,7 +138,65 @@ __device__ __forceinline__ uint4 finish_src(const char* p, size_t v, int nval, b
 // sources flagged in pkt_mask are read straight from LL16 packet areas (a
 // read_packets fused into the reduce).
 template <typename T>
-__device__ void data_op(const PlanArgs& a, const DevOp& op, int j, uint64_t e, RankState* rs) {
+__device__ __noinline__ void data_op_general(const PlanArgs& a, const DevOp& op, int j, uint64_t e,
+                                             RankState* rs);
+
+// The common fused shape -- an n-source (n <= 8) pull-reduce pushed to up to 8
+// destinations, plain (non-packet) 16-byte vectors -- with every pointer in a
+// register and all sources in flight; anything else goes to the general path
+// (kept out of line so its register pressure does not spill this loop).
+template <typename T>
+__device__ __noinline__ void multi_fast(const PlanArgs& a, const DevOp& op, int j);
+
+template <typename T>
+__device__ __forceinline__ void data_op(const PlanArgs& a, const DevOp& op, int j, uint64_t e, RankState* rs) {
+  if ((op.flags & F_VEC) && op.code == D_MULTI && op.nsrc <= 8 && !op.pkt_mask) multi_fast<T>(a, op, j);
+  else data_op_general<T>(a, op, j, e, rs);
+}
+
+// Out of line so the interpreter's live state does not share its registers.
+template <typename T>
+__device__ __noinline__ void multi_fast(const PlanArgs& a, const DevOp& op, int j) {
+  using A = typename Vec<T>::Acc;
+  constexpr int V = Vec<T>::N;
+  constexpr int B = 8;
+  const int nsrc = op.nsrc, ndst = op.ndst;
+  const uint64_t size = op.size;
+  const uint64_t per = ((size + a.K - 1) / a.K + V - 1) / V * V;
+  const uint64_t lo = min((uint64_t)j * per, size), hi = min(lo + per, size);
+  const bool zero = op.flags & F_ZERO, round_each = op.flags & F_ROUND_EACH;
+  {
+    // pointers are re-derived from the shared-memory op each iteration (a few
+    // LDS) instead of being held live: keeps the loop under the register cap
+    for (uint64_t v = lo / V + threadIdx.x; v * V < hi; v += blockDim.x) {
+      const int nval = (int)min((uint64_t)V, hi - v * V);
+      const size_t boff = (size_t)v * 16;
+      uint4 x[B];
+#pragma unroll
+      for (int i = 0; i < B; i++)
+        if (i < nsrc) x[i] = load_part<T>(ref_ptr(a, op.src[i]) + boff, nval);
+      A acc[V];
+      if (zero) {
+#pragma unroll
+        for (int i = 0; i < V; i++) acc[i] = A(0);
+        acc_vec<T>(acc, x[0], round_each);
+      } else {
+        Vec<T>::load(x[0], acc);
+      }
+#pragma unroll
+      for (int i = 1; i < B; i++)
+        if (i < nsrc) acc_vec<T>(acc, x[i], round_each);
+      const uint4 res = Vec<T>::store(acc);
+#pragma unroll
+      for (int d = 0; d < kMaxDst; d++)
+        if (d < ndst) store_part<T>(ref_ptr(a, op.dst[d]) + boff, res, nval);
+    }
+  }
+}
+
+template <typename T>
+__device__ __noinline__ void data_op_general(const PlanArgs& a, const DevOp& op, int j, uint64_t e,
+                                             RankState* rs) {
   using A = typename Vec<T>::Acc;
   constexpr int V = Vec<T>::N;
   constexpr int B = 8;   // sources in flight per round
@@ -158,39 +216,7 @@ __device__ void data_op(const PlanArgs& a, const DevOp& op, int j, uint64_t e, R
     flag[k] = (pkt >> k) & 1u ? runtime_flag(e, a.flag_stride, op.llflag_k[k]) : 0u;
   }
   for (int k = 0; k < ndst; k++) dst[k] = ref_ptr(a, op.dst[k]);
-  if ((op.flags & F_VEC) && multi && nsrc <= B && !pkt) {
-    // common fused shape (n-source pull-reduce + push): pointers in
-    // registers, all sources in flight, statically indexed
-    const char* ps[B];
-    char* pd[kMaxDst];
-#pragma unroll
-    for (int i = 0; i < B; i++) ps[i] = i < nsrc ? src[i] : nullptr;
-#pragma unroll
-    for (int i = 0; i < kMaxDst; i++) pd[i] = i < ndst ? dst[i] : nullptr;
-    for (uint64_t v = lo / V + threadIdx.x; v * V < hi; v += blockDim.x) {
-      const int nval = (int)min((uint64_t)V, hi - v * V);
-      const size_t boff = (size_t)v * 16;
-      uint4 x[B];
-#pragma unroll
-      for (int i = 0; i < B; i++)
-        if (i < nsrc) x[i] = load_part<T>(ps[i] + boff, nval);
-      A acc[V];
-      if (zero) {
-#pragma unroll
-        for (int i = 0; i < V; i++) acc[i] = A(0);
-        acc_vec<T>(acc, x[0], round_each);
-      } else {
-        Vec<T>::load(x[0], acc);
-      }
-#pragma unroll
-      for (int i = 1; i < B; i++)
-        if (i < nsrc) acc_vec<T>(acc, x[i], round_each);
-      const uint4 res = Vec<T>::store(acc);
-#pragma unroll
-      for (int d = 0; d < kMaxDst; d++)
-        if (d < ndst) store_part<T>(pd[d] + boff, res, nval);
-    }
-  } else if (op.flags & F_VEC) {
+  if (op.flags & F_VEC) {
     for (uint64_t v = lo / V + threadIdx.x; v * V < hi; v += blockDim.x) {
       const int nval = (int)min((uint64_t)V, hi - v * V);
       const size_t boff = (size_t)v * 16;
@@ -243,7 +269,7 @@ __device__ void data_op(const PlanArgs& a, const DevOp& op, int j, uint64_t e, R
 // LL packets (cf/channels.py:244-330).  LL16: 8 payload bytes per 16-byte
 // packet {d0, f, d1, f}; LL8: one reference packet {d, f} per 4 payload bytes.
 template <typename T>
-__device__ void packet_op(const PlanArgs& a, const DevOp& op, int j, uint64_t e, RankState* rs) {
+__device__ __noinline__ void packet_op(const PlanArgs& a, const DevOp& op, int j, uint64_t e, RankState* rs) {
   constexpr int V = 16 / sizeof(T);
   const uint64_t size = op.size;
   const uint64_t per = ((size + a.K - 1) / a.K + V - 1) / V * V;
@@ -313,7 +339,7 @@ __device__ void packet_op(const PlanArgs& a, const DevOp& op, int j, uint64_t e,
 // receiver with the absolute count (call-1)*signals_per_call + m.  The CTA's
 // prior writes to the source are published before the post.
 template <typename T>
-__device__ void port_op(const PlanArgs& a, const DevOp& op, int rank, int pid, int j, uint64_t e, RankState* rs,
+__device__ __noinline__ void port_op(const PlanArgs& a, const DevOp& op, int rank, int pid, int j, uint64_t e, RankState* rs,
                         uint64_t& last) {
   __syncthreads();
   if (threadIdx.x != 0) return;
@@ -339,7 +365,7 @@ __device__ void port_op(const PlanArgs& a, const DevOp& op, int rank, int pid, i
 // Prologue of a call, split over the rank's CTAs: copy the user input into the
 // private input buffer (plans that write their input, e.g. ring RS) and zero
 // the buffers the plan reads before writing (cf/executor.py:153-154).
-__device__ void prologue(const PlanArgs& a, int rank) {
+__device__ __noinline__ void prologue(const PlanArgs& a, int rank) {
   const int cta = (int)blockIdx.x - a.rank_leader[rank];
   const int nct = a.rank_ctas[rank];
   const size_t stride = (size_t)nct * blockDim.x;
