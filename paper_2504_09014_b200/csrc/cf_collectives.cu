@@ -71,13 +71,8 @@ __device__ __forceinline__ uint4 load_vec(const char* base, size_t v, size_t cou
   constexpr int V = 16 / sizeof(T);
   const size_t e0 = v * V;
   if (e0 + V <= count) return ld16(base + v * 16);
-  union { uint4 u; T t[V]; } r;
-  r.u = make_uint4(0, 0, 0, 0);
-  const T* src = reinterpret_cast<const T*>(base);
-#pragma unroll
-  for (int j = 0; j < V; j++)
-    if (e0 + j < count) r.t[j] = src[e0 + j];
-  return r.u;
+  const int nb = e0 < count ? (int)((count - e0) * sizeof(T)) : 0;
+  return ld_partial16<sizeof(T)>(base + v * 16, nb);
 }
 
 // Store the lanes of vector `v` whose element index lies in [lo, hi) at
@@ -92,14 +87,9 @@ __device__ __forceinline__ void store_vec(char* base, size_t v, uint4 val, size_
     st16(p, val);
     return;
   }
-  union { uint4 u; T t[V]; } x;
-  x.u = val;
-  T* dst = reinterpret_cast<T*>(base);
-#pragma unroll
-  for (int j = 0; j < V; j++) {
-    const size_t e = e0 + j;
-    if (e >= lo && e < hi) dst[e - shift] = x.t[j];
-  }
+  const int jlo = lo > e0 ? (int)min(lo - e0, (size_t)V) : 0;
+  const int jhi = hi > e0 ? (int)min(hi - e0, (size_t)V) : 0;
+  st_masked16<sizeof(T)>(p, val, jlo, jhi);
 }
 
 // Accumulate NR (runtime n <= NR) 16-byte vectors in order: x[0] first (or a

@@ -83,18 +83,13 @@ template <typename T>
 __device__ __forceinline__ uint4 load_part(const char* p, int nval) {
   constexpr int V = 16 / sizeof(T);
   if (nval >= V) return ld16(p);
-  union { uint4 u; T t[V]; } r;
-  r.u = make_uint4(0, 0, 0, 0);
-  for (int i = 0; i < nval; i++) r.t[i] = reinterpret_cast<const T*>(p)[i];
-  return r.u;
+  return ld_partial16<sizeof(T)>(p, nval * (int)sizeof(T));
 }
 template <typename T>
 __device__ __forceinline__ void store_part(char* p, uint4 v, int nval) {
   constexpr int V = 16 / sizeof(T);
   if (nval >= V) { st16(p, v); return; }
-  union { uint4 u; T t[V]; } x;
-  x.u = v;
-  for (int i = 0; i < nval; i++) reinterpret_cast<T*>(p)[i] = x.t[i];
+  st_masked16<sizeof(T)>(p, v, 0, nval);
 }
 
 template <typename T>

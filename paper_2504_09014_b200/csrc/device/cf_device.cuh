@@ -131,6 +131,36 @@ __device__ __forceinline__ void st8_volatile(void* p, uint2 v) {
   asm volatile("st.volatile.global.v2.u32 [%0], {%1,%2};" ::"l"(p), "r"(v.x), "r"(v.y) : "memory");
 }
 
+// Partial 16-byte vectors (ragged heads/tails) in registers only: the loops
+// unroll, so every word index is a compile-time constant (a union or array
+// with a runtime index would live in local memory).
+template <int ES>
+__device__ __forceinline__ uint4 ld_partial16(const char* p, int nbytes) {
+  uint32_t w[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+  for (int b = 0; b < 16; b += ES) {
+    if (b < nbytes) {
+      const uint32_t v = ES == 4 ? *reinterpret_cast<const uint32_t*>(p + b)
+                                 : (uint32_t)*reinterpret_cast<const uint16_t*>(p + b);
+      w[b / 4] |= v << ((b % 4) * 8);
+    }
+  }
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
+// Store elements [jlo, jhi) of a 16-byte vector at base + j*ES.
+template <int ES>
+__device__ __forceinline__ void st_masked16(char* base, uint4 v, int jlo, int jhi) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int b = 0; b < 16; b += ES) {
+    const int jj = b / ES;
+    if (jj >= jlo && jj < jhi) {
+      if (ES == 4) *reinterpret_cast<uint32_t*>(base + b) = w[b / 4];
+      else *reinterpret_cast<uint16_t*>(base + b) = (uint16_t)(w[b / 4] >> ((b % 4) * 8));
+    }
+  }
+}
+
 // ---------------------------------------------------------------- spin waits
 
 // Spin until *sem >= target (acquire).  Returns false on timeout or when the
