@@ -1008,6 +1008,20 @@ cfStatus load(cfComm* c, const char* json, size_t len, int dtype_override, cfPla
     cfStatus ps = proxy_start(c);
     if (ps != CF_OK) { cfPlanDestroy(pl.release()); return ps; }
   }
+  if (getenv("CF_PLAN_DUMP")) {   // "explain": the compiled device program of each (rank, tb)
+    static const char* names[] = {"nop", "sync_cta", "sync_group", "dev_barrier", "signal", "wait", "multi",
+                                  "copy", "put_packets", "read_packets", "port_put", "port_signal",
+                                  "port_flush"};
+    fprintf(stderr, "plan '%s': K=%d CTAs/program, entry=%d prologue=%d\n", pl->ir.name.c_str(), pl->K,
+            (int)pl->has_prologue, (int)pl->input_private);
+    for (size_t p = 0; p < pl->prog_ops.size(); p++) {
+      fprintf(stderr, "  r%d.tb%d:", pl->prog_rank[p], pl->prog_tb[p]);
+      for (auto& d : pl->prog_ops[p])
+        fprintf(stderr, " %s[n=%llu s%d d%d f%x p%x]", names[d.code], (unsigned long long)d.size, d.nsrc, d.ndst,
+                d.flags, d.pkt_mask);
+      fprintf(stderr, "\n");
+    }
+  }
   *out = pl.release();
   return CF_OK;
 }
