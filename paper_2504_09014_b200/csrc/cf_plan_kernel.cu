@@ -35,6 +35,15 @@ __device__ __forceinline__ char* ref_ptr(const PlanArgs& a, const DRef& r) {
   return base + r.off;
 }
 
+// Data-op references are resolved to absolute addresses when their window is
+// staged (see resolve_window), so the op bodies read one shared-memory word per
+// pointer instead of a chain of dependent parameter/table loads.
+__device__ __forceinline__ char* ptr(const DRef& r) { return reinterpret_cast<char*>(r.off); }
+
+__device__ __forceinline__ bool is_data_code(uint8_t c) {
+  return c == D_MULTI || c == D_COPY || c == D_PUT_PACKETS || c == D_READ_PACKETS || c == D_PORT_PUT;
+}
+
 __device__ __forceinline__ uint32_t runtime_flag(uint64_t e, uint32_t stride, uint32_t f) {
   return (uint32_t)(((e - 1) * (uint64_t)stride + f) % 0xffffffffull) + 1u;
 }
@@ -133,7 +142,7 @@ __device__ __forceinline__ uint4 finish_src(const char* p, size_t v, int nval, b
 // sources flagged in pkt_mask are read straight from LL16 packet areas (a
 // read_packets fused into the reduce).
 template <typename T>
-__device__ __noinline__ void data_op_general(const PlanArgs& a, const DevOp& op, int j, uint64_t e,
+__device__ __noinline__ void data_op_general(const DevOp& op, uint64_t lo, uint64_t hi, uint32_t fstride, uint64_t e,
                                              RankState* rs);
 
 // The common fused shape -- an n-source (n <= 8) pull-reduce pushed to up to 8
@@ -141,64 +150,71 @@ __device__ __noinline__ void data_op_general(const PlanArgs& a, const DevOp& op,
 // register and all sources in flight; anything else goes to the general path
 // (kept out of line so its register pressure does not spill this loop).
 template <typename T>
-__device__ __noinline__ void multi_fast(const PlanArgs& a, const DevOp& op, int j);
+__device__ __noinline__ void multi_fast(const DevOp& op, uint64_t lo, uint64_t hi);
+
+// This CTA's slice [lo, hi) of an op's elements: contiguous, whole vectors.
+template <typename T>
+__device__ __forceinline__ void slice(uint64_t size, int K, int j, uint64_t& lo, uint64_t& hi) {
+  constexpr int V = 16 / sizeof(T);
+  const uint64_t per = ((size + K - 1) / K + V - 1) / V * V;
+  lo = min((uint64_t)j * per, size);
+  hi = min(lo + per, size);
+}
 
 template <typename T>
 __device__ __forceinline__ void data_op(const PlanArgs& a, const DevOp& op, int j, uint64_t e, RankState* rs) {
-  if ((op.flags & F_VEC) && op.code == D_MULTI && op.nsrc <= 8 && !op.pkt_mask) multi_fast<T>(a, op, j);
-  else data_op_general<T>(a, op, j, e, rs);
+  uint64_t lo, hi;
+  slice<T>(op.size, a.K, j, lo, hi);
+  if (lo >= hi) return;
+  if ((op.flags & F_VEC) && op.code == D_MULTI && op.nsrc <= 8 && !op.pkt_mask) {
+    constexpr int V = 16 / sizeof(T);
+    const uint64_t full = lo + (hi - lo) / V * V;
+    if (full > lo) multi_fast<T>(op, lo, full);
+    if (full < hi) data_op_general<T>(op, full, hi, a.flag_stride, e, rs);   // ragged last vector
+  } else {
+    data_op_general<T>(op, lo, hi, a.flag_stride, e, rs);
+  }
 }
 
 // Out of line so the interpreter's live state does not share its registers.
 template <typename T>
-__device__ __noinline__ void multi_fast(const PlanArgs& a, const DevOp& op, int j) {
+__device__ __noinline__ void multi_fast(const DevOp& op, uint64_t lo, uint64_t hi) {
   using A = typename Vec<T>::Acc;
   constexpr int V = Vec<T>::N;
   constexpr int B = 8;
   const int nsrc = op.nsrc, ndst = op.ndst;
-  const uint64_t size = op.size;
-  const uint64_t per = ((size + a.K - 1) / a.K + V - 1) / V * V;
-  const uint64_t lo = min((uint64_t)j * per, size), hi = min(lo + per, size);
   const bool zero = op.flags & F_ZERO, round_each = op.flags & F_ROUND_EACH;
-  {
-    // pointers are re-derived from the shared-memory op each iteration (a few
-    // LDS) instead of being held live: keeps the loop under the register cap
-    for (uint64_t v = lo / V + threadIdx.x; v * V < hi; v += blockDim.x) {
-      const int nval = (int)min((uint64_t)V, hi - v * V);
-      const size_t boff = (size_t)v * 16;
-      uint4 x[B];
+  // whole vectors only (the caller hands the ragged tail to the general path),
+  // so every load is a plain 16-byte load and x[] stays in registers
+  for (uint64_t v = lo / V + threadIdx.x; v * V < hi; v += blockDim.x) {
+    const size_t boff = (size_t)v * 16;
+    uint4 x[B];
 #pragma unroll
-      for (int i = 0; i < B; i++)
-        if (i < nsrc) x[i] = load_part<T>(ref_ptr(a, op.src[i]) + boff, nval);
-      A acc[V];
-      if (zero) {
+    for (int i = 0; i < B; i++) x[i] = i < nsrc ? ld16(ptr(op.src[i]) + boff) : make_uint4(0, 0, 0, 0);
+    A acc[V];
+    if (zero) {
 #pragma unroll
-        for (int i = 0; i < V; i++) acc[i] = A(0);
-        acc_vec<T>(acc, x[0], round_each);
-      } else {
-        Vec<T>::load(x[0], acc);
-      }
-#pragma unroll
-      for (int i = 1; i < B; i++)
-        if (i < nsrc) acc_vec<T>(acc, x[i], round_each);
-      const uint4 res = Vec<T>::store(acc);
-#pragma unroll
-      for (int d = 0; d < kMaxDst; d++)
-        if (d < ndst) store_part<T>(ref_ptr(a, op.dst[d]) + boff, res, nval);
+      for (int i = 0; i < V; i++) acc[i] = A(0);
+      acc_vec<T>(acc, x[0], round_each);
+    } else {
+      Vec<T>::load(x[0], acc);
     }
+#pragma unroll
+    for (int i = 1; i < B; i++)
+      if (i < nsrc) acc_vec<T>(acc, x[i], round_each);
+    const uint4 res = Vec<T>::store(acc);
+#pragma unroll
+    for (int d = 0; d < kMaxDst; d++)
+      if (d < ndst) st16(ptr(op.dst[d]) + boff, res);
   }
 }
 
 template <typename T>
-__device__ __noinline__ void data_op_general(const PlanArgs& a, const DevOp& op, int j, uint64_t e,
+__device__ __noinline__ void data_op_general(const DevOp& op, uint64_t lo, uint64_t hi, uint32_t fstride, uint64_t e,
                                              RankState* rs) {
   using A = typename Vec<T>::Acc;
   constexpr int V = Vec<T>::N;
   constexpr int B = 8;   // sources in flight per round
-  const uint64_t size = op.size;
-  const uint64_t per = ((size + a.K - 1) / a.K + V - 1) / V * V;
-  const uint64_t lo = min((uint64_t)j * per, size), hi = min(lo + per, size);
-  if (lo >= hi) return;
   const int nsrc = op.nsrc, ndst = op.ndst;
   const bool zero = op.flags & F_ZERO, round_each = op.flags & F_ROUND_EACH;
   const bool multi = op.code == D_MULTI;
@@ -207,10 +223,10 @@ __device__ __noinline__ void data_op_general(const PlanArgs& a, const DevOp& op,
   char* dst[kMaxDst];
   uint32_t flag[kMaxSrc];
   for (int k = 0; k < nsrc; k++) {
-    src[k] = ref_ptr(a, op.src[k]);
-    flag[k] = (pkt >> k) & 1u ? runtime_flag(e, a.flag_stride, op.llflag_k[k]) : 0u;
+    src[k] = ptr(op.src[k]);
+    flag[k] = (pkt >> k) & 1u ? runtime_flag(e, fstride, op.llflag_k[k]) : 0u;
   }
-  for (int k = 0; k < ndst; k++) dst[k] = ref_ptr(a, op.dst[k]);
+  for (int k = 0; k < ndst; k++) dst[k] = ptr(op.dst[k]);
   if (op.flags & F_VEC) {
     for (uint64_t v = lo / V + threadIdx.x; v * V < hi; v += blockDim.x) {
       const int nval = (int)min((uint64_t)V, hi - v * V);
@@ -264,10 +280,10 @@ __device__ __noinline__ void data_op_general(const PlanArgs& a, const DevOp& op,
 // LL packets (cf/channels.py:244-330).  LL16: 8 payload bytes per 16-byte
 // packet {d0, f, d1, f}; LL8: one reference packet {d, f} per 4 payload bytes.
 template <typename T>
-__device__ __noinline__ void packet_op(const PlanArgs& a, const DevOp& op, int j, uint64_t e, RankState* rs) {
+__device__ __noinline__ void packet_op(const DevOp& op, int K, int j, uint32_t fstride, uint64_t e, RankState* rs) {
   constexpr int V = 16 / sizeof(T);
   const uint64_t size = op.size;
-  const uint64_t per = ((size + a.K - 1) / a.K + V - 1) / V * V;
+  const uint64_t per = ((size + K - 1) / K + V - 1) / V * V;
   const uint64_t lo = min((uint64_t)j * per, size), hi = min(lo + per, size);
   if (lo >= hi) return;
   const bool put = op.code == D_PUT_PACKETS;
@@ -277,25 +293,25 @@ __device__ __noinline__ void packet_op(const PlanArgs& a, const DevOp& op, int j
   if (op.flags & F_LL16) {
     const uint64_t u0 = lo * sizeof(T) / 8, u1 = (hi * sizeof(T) + 7) / 8;
     if (put) {
-      const uint32_t flag = runtime_flag(e, a.flag_stride, op.llflag);
-      const char* src = ref_ptr(a, op.src[0]);
+      const uint32_t flag = runtime_flag(e, fstride, op.llflag);
+      const char* src = ptr(op.src[0]);
       for (uint64_t u = u0 + threadIdx.x; u < u1; u += blockDim.x) {
         const uint2 d = *reinterpret_cast<const uint2*>(src + u * 8);
-        for (int k = 0; k < nb; k++) ll16_put(ref_ptr(a, op.dst[k]) + u * 16, d, flag);
+        for (int k = 0; k < nb; k++) ll16_put(ptr(op.dst[k]) + u * 16, d, flag);
       }
     } else {
       for (uint64_t u = u0 + threadIdx.x; u < u1; u += blockDim.x) {
         uint4 raw[kMaxDst];
 #pragma unroll
         for (int k = 0; k < kMaxDst; k++)   // all packets in flight first
-          if (k < nb) raw[k] = ld16_volatile(ref_ptr(a, op.src[k]) + u * 16);
+          if (k < nb) raw[k] = ld16_volatile(ptr(op.src[k]) + u * 16);
 #pragma unroll
         for (int k = 0; k < kMaxDst; k++) {
           if (k < nb) {
-            const uint32_t flag = runtime_flag(e, a.flag_stride, op.llflag_k[k]);
+            const uint32_t flag = runtime_flag(e, fstride, op.llflag_k[k]);
             uint2 d = make_uint2(raw[k].x, raw[k].z);
-            if (raw[k].y != flag || raw[k].w != flag) d = ll16_get(ref_ptr(a, op.src[k]) + u * 16, flag, rs);
-            *reinterpret_cast<uint2*>(ref_ptr(a, op.dst[k]) + u * 8) = d;
+            if (raw[k].y != flag || raw[k].w != flag) d = ll16_get(ptr(op.src[k]) + u * 16, flag, rs);
+            *reinterpret_cast<uint2*>(ptr(op.dst[k]) + u * 8) = d;
           }
         }
       }
@@ -303,9 +319,9 @@ __device__ __noinline__ void packet_op(const PlanArgs& a, const DevOp& op, int j
   } else {
     const uint64_t u0 = lo * sizeof(T) / 4, u1 = (hi * sizeof(T) + 3) / 4;
     for (int k = 0; k < nb; k++) {
-      const char* src = ref_ptr(a, op.src[put ? 0 : k]);
-      char* dst = ref_ptr(a, op.dst[k]);
-      const uint32_t flag = runtime_flag(e, a.flag_stride, put ? op.llflag : op.llflag_k[k]);
+      const char* src = ptr(op.src[put ? 0 : k]);
+      char* dst = ptr(op.dst[k]);
+      const uint32_t flag = runtime_flag(e, fstride, put ? op.llflag : op.llflag_k[k]);
       for (uint64_t u = u0 + threadIdx.x; u < u1; u += blockDim.x) {
         if (put) {
           const uint32_t d = *reinterpret_cast<const uint32_t*>(src + u * 4);
@@ -340,13 +356,14 @@ __device__ __noinline__ void port_op(const PlanArgs& a, const DevOp& op, int ran
   if (threadIdx.x != 0) return;
   uint64_t src = 0, dst = 0, bytes = 0;
   if (op.code == D_PORT_PUT) {
+    const int K = a.K;
     constexpr int V = 16 / sizeof(T);
     const uint64_t size = op.size;
-    const uint64_t per = ((size + a.K - 1) / a.K + V - 1) / V * V;
+    const uint64_t per = ((size + K - 1) / K + V - 1) / V * V;
     const uint64_t lo = min((uint64_t)j * per, size), hi = min(lo + per, size);
     if (hi > lo) {
-      src = (uint64_t)(ref_ptr(a, op.src[0]) + lo * sizeof(T));
-      dst = (uint64_t)(ref_ptr(a, op.dst[0]) + lo * sizeof(T));
+      src = (uint64_t)(ptr(op.src[0]) + lo * sizeof(T));
+      dst = (uint64_t)(ptr(op.dst[0]) + lo * sizeof(T));
       bytes = (hi - lo) * sizeof(T);
     }
   }
@@ -382,6 +399,22 @@ __device__ __noinline__ void prologue(const PlanArgs& a, int rank) {
   }
 }
 
+// Rewrite the staged window's data-op references as absolute addresses (the io
+// buffers change per call, so this cannot all be done at load time).
+__device__ __forceinline__ void resolve_window(const PlanArgs& a, DevOp* ops, int nops) {
+  constexpr int kSlots = kMaxSrc + kMaxDst;
+  for (int t = threadIdx.x; t < nops * kSlots; t += blockDim.x) {
+    DevOp& op = ops[t / kSlots];
+    if (!is_data_code(op.code)) continue;
+    const int k = t % kSlots;
+    if (k < kMaxSrc ? k >= op.nsrc : k - kMaxSrc >= op.ndst) continue;
+    DRef& r = k < kMaxSrc ? op.src[k] : op.dst[k - kMaxSrc];
+    if (r.buf == kAbsolute) continue;
+    r.off = reinterpret_cast<uint64_t>(ref_ptr(a, r));
+    r.buf = kAbsolute;
+  }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(512) plan_kernel(const __grid_constant__ PlanArgs a) {
   const int pid = blockIdx.x / a.K, j = blockIdx.x % a.K;
@@ -411,6 +444,8 @@ __global__ void __launch_bounds__(512) plan_kernel(const __grid_constant__ PlanA
       const int nvec = (w1 - w0) * (int)(sizeof(DevOp) / 16);
       for (int t = threadIdx.x; t < nvec; t += blockDim.x) s_raw[t] = src[t];
     }
+    __syncthreads();
+    resolve_window(a, s_ops, w1 - w0);
     __syncthreads();
   for (int i = w0; i < w1; i++) {
     const DevOp& op = s_ops[i - w0];
@@ -444,7 +479,7 @@ __global__ void __launch_bounds__(512) plan_kernel(const __grid_constant__ PlanA
         break;
       case D_PUT_PACKETS:
       case D_READ_PACKETS:
-        packet_op<T>(a, op, j, e, rs);
+        packet_op<T>(op, a.K, j, a.flag_stride, e, rs);
         break;
       case D_PORT_PUT:
       case D_PORT_SIGNAL:

@@ -11,7 +11,7 @@ sys.path.insert(0, ROOT)
 def main():
     import torch
     import bench
-    from paper_2504_09014_b200 import Runtime, make_world
+    from paper_2504_09014_b200 import Runtime, _lib, make_world
     from paper_2504_09014_b200.algorithms import build_2pa
     from paper_2504_09014_b200.lowering import LoweringParams, ProgramGraph, lower
     n = 8
@@ -45,6 +45,13 @@ def main():
         t_warm = bench.time_plan(rt, xs, ys, 50, 3, None)
         print(f"{name:10s} device_ops={rt.n_device_ops:3d}  {t_warm * 1e6:7.2f} us (L2 warm)")
         rt.close()
+    # the hand-written kernels on the same sizes, for comparison
+    for elems in (8192, 8192 * 64):
+        xs = [torch.randn(elems, device=dev).to(torch.bfloat16) for _ in range(n)]
+        ys = [torch.empty(elems, device=dev, dtype=torch.bfloat16) for _ in range(n)]
+        for algo in ("2pa", "1pa_hb"):
+            t = bench.time_coll(w, "allreduce", xs, ys, elems, "bf16", _lib.ALGOS[algo], 50, 3, None)
+            print(f"hand {algo:6s} {elems * 2:8d} B  {t * 1e6:7.2f} us (L2 warm)")
 
 
 if __name__ == "__main__":
