@@ -160,19 +160,18 @@ def run_reference_arm(args):
 
 # ----------------------------------------------------------------------------- GPU arm
 
-def time_coll(world, kind, send, recv, count, dtype, algo, iters, warmup, flush=None, reps=3):
-    """Device time per call: `iters` calls captured in one CUDA graph (no host
-    launch overhead), replayed `reps` times, CUDA events on the replay stream.
-    With `flush`, each call is preceded by an L2 flush (memset of a buffer
-    larger than L2) and the time of a flush-only graph is subtracted."""
+def time_graph(dev, fn, iters, warmup, flush=None, reps=3):
+    """Device time per call of `fn`: `iters` calls captured in one CUDA graph
+    (no host launch overhead), replayed `reps` times (best), CUDA events on the
+    replay stream.  With `flush`, each call is preceded by an L2 flush (memset
+    of a buffer larger than L2) and the time of a flush-only graph is
+    subtracted."""
     import torch
-    from paper_2504_09014_b200 import collectives as C
-    dev = world.device(0)
     for _ in range(warmup):
-        C.run(kind, send, recv, count, dtype, algo, world)
-    world.synchronize()
+        fn()
+    torch.cuda.synchronize(dev)
 
-    def capture(with_coll):
+    def capture(with_fn):
         g = torch.cuda.CUDAGraph()
         s = torch.cuda.Stream(dev)
         s.wait_stream(torch.cuda.current_stream(dev))
@@ -181,54 +180,8 @@ def time_coll(world, kind, send, recv, count, dtype, algo, iters, warmup, flush=
                 for _ in range(iters):
                     if flush is not None:
                         flush.zero_()
-                    if with_coll:
-                        C.run(kind, send, recv, count, dtype, algo, world)
-        torch.cuda.synchronize(dev)
-        return g
-
-    def replay(g):
-        g.replay()
-        torch.cuda.synchronize(dev)
-        best = None
-        for _ in range(reps):
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            st = torch.cuda.current_stream(dev)
-            e0.record(st)
-            g.replay()
-            e1.record(st)
-            e1.synchronize()
-            t = e0.elapsed_time(e1) / 1e3
-            best = t if best is None else min(best, t)
-        return best
-
-    g = capture(True)
-    t = replay(g)
-    if flush is not None:
-        t -= replay(capture(False))
-    world.check_device_error()
-    return max(t, 0.0) / iters
-
-
-def time_plan(rt, send, recv, iters, warmup, flush, reps=3):
-    """time_coll for a plan Runtime (CUDA graph of `iters` executions)."""
-    import torch
-    dev = rt.world.device(0)
-    for _ in range(warmup):
-        rt.run_raw(send, recv)
-    rt.world.synchronize()
-
-    def capture(with_plan):
-        g = torch.cuda.CUDAGraph()
-        s = torch.cuda.Stream(dev)
-        s.wait_stream(torch.cuda.current_stream(dev))
-        with torch.cuda.stream(s):
-            with torch.cuda.graph(g, stream=s):
-                for _ in range(iters):
-                    if flush is not None:
-                        flush.zero_()
-                    if with_plan:
-                        rt.run_raw(send, recv)
+                    if with_fn:
+                        fn()
         torch.cuda.synchronize(dev)
         return g
 
@@ -251,8 +204,58 @@ def time_plan(rt, send, recv, iters, warmup, flush, reps=3):
     t = replay(capture(True))
     if flush is not None:
         t -= replay(capture(False))
-    rt.check_device_error()
     return max(t, 0.0) / iters
+
+
+def time_coll(world, kind, send, recv, count, dtype, algo, iters, warmup, flush=None, reps=3):
+    """time_graph of one libcf collective call on every rank."""
+    from paper_2504_09014_b200 import collectives as C
+    t = time_graph(world.device(0), lambda: C.run(kind, send, recv, count, dtype, algo, world),
+                   iters, warmup, flush, reps)
+    world.check_device_error()
+    return t
+
+
+def time_plan(rt, send, recv, iters, warmup, flush, reps=3):
+    """time_graph of one plan execution (K10) on every rank."""
+    t = time_graph(rt.world.device(0), lambda: rt.run_raw(send, recv), iters, warmup, flush, reps)
+    rt.check_device_error()
+    return t
+
+
+def run_fused(w, flush):
+    """K13 vs the unfused composition (AllReduce, then one batched residual add
+    and one batched RMSNorm over all ranks' rows) at the C5 shapes."""
+    import torch
+    import torch.nn.functional as F
+    from paper_2504_09014_b200 import _lib, allreduce_add_rmsnorm
+    from paper_2504_09014_b200 import collectives as C
+    n, dev, hidden = w.num_ranks, w.device(0), 8192
+    rows = []
+    for b in (1, 4, 16, 64, 256):
+        X = torch.randn(n, b, hidden, device=dev).to(torch.bfloat16)
+        R = torch.randn(n, b, hidden, device=dev).to(torch.bfloat16)
+        H, RO, Y = torch.empty_like(X), torch.empty_like(X), torch.empty_like(X)
+        wt = torch.ones(hidden, device=dev, dtype=torch.bfloat16)
+        xs, rs, ros, ys = list(X), list(R), list(RO), list(Y)
+        hs = list(H)
+
+        def fused():
+            allreduce_add_rmsnorm(w, xs, rs, wt, eps=1e-6, resid_out=ros, norm_out=ys)
+
+        def unfused():
+            C.run("allreduce", xs, hs, b * hidden, "bf16", _lib.ALGOS["auto"], w)
+            torch.add(H, R, out=RO)
+            F.rms_norm(RO, (hidden,), wt, 1e-6)
+
+        tf = time_graph(dev, fused, 20, 3, flush)
+        tu = time_graph(dev, unfused, 20, 3, flush)
+        w.check_device_error()
+        rows.append({"batch": b, "bytes": b * hidden * 2, "fused_us": round(tf * 1e6, 2),
+                     "unfused_us": round(tu * 1e6, 2), "speedup": round(tu / tf, 2) if tf else None})
+    return {"config": "C5 consumer: AllReduce + residual add + RMSNorm [b, 8192] bf16, fused K13 vs "
+                      "libcf AllReduce + torch add + torch rms_norm (batched over ranks), 8 co-resident ranks",
+            "rows": rows}
 
 
 def run_gpu_arm(args):
@@ -416,6 +419,7 @@ def run_sweep(w, args):
             rt.close()
     out.append({"config": "C5 Llama-70B TP decode AllReduce via DSL plans (K10), bf16, "
                           "8 co-resident ranks", "rows": c5})
+    out.append(run_fused(w, flush))
     # C1: fp32 1 MiB one-shot LL (8 simulated ranks)
     c1 = [torch.randn(MiB // 4, device=dev) for _ in range(n)]
     c1o = [torch.empty_like(x) for x in c1]

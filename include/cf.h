@@ -187,6 +187,24 @@ CF_API cfStatus cfAllGather(cfComm_t comm, const void* const* send, void* const*
 CF_API cfStatus cfReduceScatter(cfComm_t comm, const void* const* send, void* const* recv, size_t recvcount,
                          cfDtype dtype, int algo, const cudaStream_t* streams);
 
+/* Fused AllReduce + residual add + RMSNorm (the reference
+ * composes it as `collective("allreduce", ...)` (cf/collectives.py:532-573)
+ * followed by host arithmetic).  Per local rank, on rows x hidden elements
+ * (f32/f16/bf16; hidden * elem_size a multiple of 16 bytes):
+ *   h         = send_0 + send_1 + ... + send_{n-1}  (f32 accumulate, rounded
+ *               to dtype once; identical bits on every rank)
+ *   resid_out = dtype(h + resid_in)
+ *   norm_out  = dtype(resid_out * rsqrt(mean_row(resid_out^2) + eps) * weight)
+ * weight holds `hidden` elements.  resid_out may alias resid_in.  algo:
+ * CF_ALGO_1PA_HB (one-shot: every rank reduces every row; not in place),
+ * CF_ALGO_2PA (two-shot: rank r owns rows [r*ceil(rows/n), ...) and stores
+ * both results into every rank; in the one-process-per-GPU mode norm_out and
+ * resid_out must be registered), or CF_ALGO_AUTO. */
+CF_API cfStatus cfAllReduceAddRMSNorm(cfComm_t comm, const void* const* send, const void* const* resid_in,
+                                      void* const* resid_out, void* const* norm_out, const void* const* weight,
+                                      size_t rows, size_t hidden, float eps, cfDtype dtype, int algo,
+                                      const cudaStream_t* streams);
+
 /* The algorithm the measured selector picks (cf/collectives.py:473-491).
  * collective: 0 = allreduce, 1 = allgather, 2 = reducescatter; nbytes as the
  * reference counts them (AG: output bytes). */

@@ -10,6 +10,7 @@ __version__ = "0.1.0"
 from .collectives import AlgoDescriptor, Selector, collective, required_multiple, select_algorithm
 from .errors import CommforgeError
 from .executor import RunResult, Runtime
+from .fused import allreduce_add_rmsnorm
 from .lowering import LoweringParams, ProgramGraph, lower
 from .plan import ExecutionPlan, parse_plan, serialize_plan, validate_plan
 from .world import Topology, World, make_world
@@ -17,7 +18,7 @@ from .world import Topology, World, make_world
 SimWorld = World  # the reference's name for the world type (cf/world.py:80)
 
 __all__ = [
-    "AlgoDescriptor", "CommforgeError", "ExecutionPlan", "LoweringParams", "ProgramGraph",
+    "AlgoDescriptor", "CommforgeError", "allreduce_add_rmsnorm", "ExecutionPlan", "LoweringParams", "ProgramGraph",
     "RunResult", "Runtime", "Selector", "SimWorld", "Topology", "World", "collective", "lower",
     "make_world", "parse_plan", "required_multiple", "select_algorithm", "serialize_plan",
     "validate_plan",

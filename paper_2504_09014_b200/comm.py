@@ -103,6 +103,28 @@ class Communicator:
         self._call(_lib.lib().cfReduceScatter, send, recv, recv.numel(), aid, stream)
         return recv
 
+    def all_reduce_add_rmsnorm(self, send, residual, weight, eps: float = 1e-6, algo: str = "auto",
+                               resid_out=None, norm_out=None, stream=None):
+        """K13 on this rank (see ``fused.allreduce_add_rmsnorm``): returns
+        ``(norm_out, resid_out)``; ``resid_out`` defaults to ``residual``
+        (updated in place).  The two-shot algorithm writes both outputs from
+        the peers, so register them (``register``) before the first call."""
+        import torch
+        if send.dim() != 2:
+            raise ShapeError("all_reduce_add_rmsnorm takes [rows, hidden] tensors")
+        resid_out = residual if resid_out is None else resid_out
+        norm_out = torch.empty_like(send) if norm_out is None else norm_out
+        aid = {"auto": -1, "1pa_hb": _lib.ALGOS["1pa_hb"], "2pa": _lib.ALGOS["2pa"]}.get(algo)
+        if aid is None:
+            raise ShapeError(f"fused allreduce+rmsnorm runs as 1pa_hb or 2pa, not {algo!r}")
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        P = _lib.ptr_array
+        _lib.check(_lib.lib().cfAllReduceAddRMSNorm(
+            self._comm, P([send.data_ptr()]), P([residual.data_ptr()]), P([resid_out.data_ptr()]),
+            P([norm_out.data_ptr()]), P([weight.data_ptr()]), send.shape[0], send.shape[1], float(eps),
+            CODES[from_torch(send.dtype)], aid, P([s.cuda_stream])))
+        return norm_out, resid_out
+
     def setup_nvls(self) -> bool:
         """Collective: build the NVLS multicast object (SwitchChannel).  Rank 0
         creates it and passes its POSIX fd to the other ranks over a Unix

@@ -618,6 +618,117 @@ __global__ void __launch_bounds__(512) ring_gather_kernel(const __grid_constant_
 
 // ---------------------------------------------------------------- launchers
 
+// ---------------------------------------------------------------- K13
+
+// AllReduce + residual add + RMSNorm (the epilogue of the C5
+// consumer fused into the collective; the reference composes it from a
+// `collective("allreduce")` and host-side arithmetic).  Per row of `hidden`
+// elements, with h = x_0 + x_1 + ... + x_{n-1} (f32 accumulate, rounded to T
+// once -- the same bits on every rank):
+//   resid_out = T(h + resid)                       (written to out2)
+//   norm_out  = T(resid_out * rsqrt(mean(resid_out^2) + eps) * weight)   (out)
+// One CTA per row.  `push` (two-shot): rank r owns rows [r*per, (r+1)*per)
+// and stores both results into every rank's buffers; otherwise (one-shot)
+// every rank computes every row for itself.  The first kCache vectors of a
+// thread's share of the row stay in registers between the two passes; the
+// rest are re-read from this rank's own resid_out (written by the same thread).
+template <typename T, int NR>
+__global__ void __launch_bounds__(512) ar_rmsnorm_kernel(const __grid_constant__ CollArgs a) {
+  const RankCtx& rk = a.rk[blockIdx.y];
+  using A = typename Vec<T>::Acc;
+  constexpr int V = Vec<T>::N;
+  constexpr int kCache = 4;
+  const int n = a.n, r = rk.rank;
+  const uint64_t e = begin_call(rk);
+  if (!a.single_launch) handshake(rk, n, e * kPhases + 1, false, a.gpu_scope);
+  size_t r0 = 0, r1 = a.rows;
+  if (a.push) {
+    const size_t per = (a.rows + n - 1) / n;
+    r0 = min((size_t)r * per, a.rows);
+    r1 = min(r0 + per, a.rows);
+  }
+  const size_t nv = a.hidden / V;
+  const size_t T0 = threadIdx.x, NT = blockDim.x;
+  __shared__ float s_red[32];
+  for (size_t row = r0 + blockIdx.x; row < r1; row += gridDim.x) {
+    const size_t off = row * a.hidden * sizeof(T);
+    float ss = 0.f;
+    uint4 cache[kCache];
+    auto pass1 = [&](size_t v) -> uint4 {
+      const size_t b = off + v * 16;
+      uint4 x[NR];
+#pragma unroll
+      for (int k = 0; k < NR; k++)
+        if (k < n) x[k] = ld16(rk.in[k] + b);
+      A hv[V], rv[V];
+      Vec<T>::load(reduce_vecs<T, NR>(x, n, false), hv);
+      Vec<T>::load(ld16(rk.resid + b), rv);
+#pragma unroll
+      for (int j = 0; j < V; j++) hv[j] = hv[j] + rv[j];
+      const uint4 ro = Vec<T>::store(hv);
+      A q[V];
+      Vec<T>::load(ro, q);
+#pragma unroll
+      for (int j = 0; j < V; j++) ss = fmaf(q[j], q[j], ss);
+      if (a.push) {
+#pragma unroll
+        for (int p = 0; p < NR; p++)
+          if (p < n) st16(rk.out2[p] + b, ro);
+      } else {
+        st16(rk.out2[r] + b, ro);
+      }
+      return ro;
+    };
+#pragma unroll
+    for (int i = 0; i < kCache; i++)
+      if (T0 + i * NT < nv) cache[i] = pass1(T0 + i * NT);
+    for (size_t v = T0 + kCache * NT; v < nv; v += NT) pass1(v);
+    // block sum of squares
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    if ((T0 & 31) == 0) s_red[T0 >> 5] = ss;
+    __syncthreads();
+    if (T0 < 32) {
+      float t = T0 < (NT + 31) / 32 ? s_red[T0] : 0.f;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+      if (T0 == 0) s_red[0] = t;
+    }
+    __syncthreads();
+    const float inv = rsqrtf(s_red[0] / (float)a.hidden + a.eps);
+    __syncthreads();   // s_red is reused by the next row
+    auto pass2 = [&](size_t v, uint4 ro) {
+      const size_t b = off + v * 16;
+      A q[V], w[V];
+      Vec<T>::load(ro, q);
+      Vec<T>::load(ld16(rk.weight + v * 16), w);
+#pragma unroll
+      for (int j = 0; j < V; j++) q[j] = q[j] * inv * w[j];
+      const uint4 y = Vec<T>::store(q);
+      if (a.push) {
+#pragma unroll
+        for (int p = 0; p < NR; p++)
+          if (p < n) st16(rk.out[p] + b, y);
+      } else {
+        st16(rk.out[r] + b, y);
+      }
+    };
+#pragma unroll
+    for (int i = 0; i < kCache; i++)
+      if (T0 + i * NT < nv) pass2(T0 + i * NT, cache[i]);
+    for (size_t v = T0 + kCache * NT; v < nv; v += NT) pass2(v, ld16(rk.out2[r] + off + v * 16));
+  }
+  if (!a.single_launch) handshake(rk, n, e * kPhases + 2, true, a.gpu_scope);
+  end_call(rk, e);
+}
+
+template <typename T>
+static const void* pick_norm(int nr) {
+  if (nr <= 2) return (const void*)ar_rmsnorm_kernel<T, 2>;
+  if (nr <= 4) return (const void*)ar_rmsnorm_kernel<T, 4>;
+  return (const void*)ar_rmsnorm_kernel<T, 8>;
+}
+
 template <template <typename, int> class K> struct KernelTable;
 
 template <typename T>
@@ -652,7 +763,8 @@ static const void* by_dtype(int dtype, int n) {
 }
 
 // Kernel entry point for (kind, dtype, n).  kind: 0 pull-reduce, 1 LL one-shot,
-// 2 LL two-shot, 3 push-gather.
+// 2 LL two-shot, 3 push-gather, 4 NVLS multimem, 5 ring RS(+AG), 6 ring AG,
+// 7 AllReduce + residual + RMSNorm.
 const void* collective_kernel(int kind, int dtype, int n) {
   switch (kind) {
     case 0: return by_dtype<pick_pull<float>, pick_pull<int32_t>, pick_pull<__half>,
@@ -683,6 +795,13 @@ const void* collective_kernel(int kind, int dtype, int n) {
         case 1: return (const void*)ring_kernel<float>;
         case 2: return (const void*)ring_kernel<__half>;
         case 3: return (const void*)ring_kernel<__nv_bfloat16>;
+      }
+      break;
+    case 7:   // K13 (floating point only)
+      switch (dtype) {
+        case 1: return pick_norm<float>(n);
+        case 2: return pick_norm<__half>(n);
+        case 3: return pick_norm<__nv_bfloat16>(n);
       }
       break;
     case 6:

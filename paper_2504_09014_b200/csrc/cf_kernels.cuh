@@ -17,6 +17,9 @@ struct RankCtx {
   uint64_t* sem[CF_MAX_RANKS];    // every rank's semaphore slab (data / handshake signals)
   uint64_t* ack[CF_MAX_RANKS];    // every rank's ack slab (ring credits, ring "ready")
   char* ring[CF_MAX_RANKS];       // every rank's ring slot region
+  char* out2[CF_MAX_RANKS];       // K13: every rank's residual-out buffer (push)
+  const char* resid;              // K13: this rank's residual input
+  const char* weight;             // K13: this rank's RMSNorm weight [hidden]
   RankState* st;                  // this rank's state
 };
 
@@ -46,6 +49,10 @@ struct CollArgs {
   size_t cs;        // reference chunk size in elements (cf/collectives.py:170-172)
   size_t slot;      // LL slot stride in bytes
   size_t half;      // LL parity-half stride in bytes
+  size_t rows;      // K13: rows of `hidden` elements (count = rows * hidden)
+  size_t hidden;
+  float eps;        // K13: RMSNorm epsilon
+  int pad2_;
   RankCtx rk[CF_MAX_RANKS];
 };
 

@@ -518,7 +518,7 @@ extern "C" cfStatus cfSelectAlgorithm(cfComm_t c, int coll, size_t nbytes, cfDty
 
 namespace {
 
-enum Kind { kPull = 0, kLL1 = 1, kLL2 = 2, kGather = 3, kNvls = 4, kRing = 5, kRingGather = 6 };
+enum Kind { kPull = 0, kLL1 = 1, kLL2 = 2, kGather = 3, kNvls = 4, kRing = 5, kRingGather = 6, kNorm = 7 };
 
 struct Job {
   int kind = kPull;
@@ -528,6 +528,16 @@ struct Job {
   size_t cs = 0;      // reference chunk (elements)
   size_t slot = 0;
   size_t work = 0;    // 16-byte vectors per rank (grid sizing)
+  size_t rows = 0, hidden = 0;   // K13
+  float eps = 0.f;
+  int blocks = 0;     // explicit CTAs per rank (K13: one per row), else from `work`
+};
+
+// K13's extra per-local-rank buffers.
+struct NormBufs {
+  const void* const* resid_in;
+  void* const* resid_out;
+  const void* const* weight;
 };
 
 cfStatus check_ptrs(cfComm* c, const void* const* send, void* const* recv, const cudaStream_t* streams) {
@@ -543,13 +553,18 @@ cfStatus check_ptrs(cfComm* c, const void* const* send, void* const* recv, const
 }
 
 cfStatus launch(cfComm* c, const Job& j, int dtype, const void* const* send, void* const* recv,
-                const cudaStream_t* streams) {
+                const cudaStream_t* streams, const NormBufs* nb = nullptr) {
   // one-process-per-GPU: peers' buffers come from the registration table
-  const bool need_in = j.kind == kPull;
-  const bool need_out = j.kind == kGather || j.kind == kRingGather || (j.kind == kPull && j.push);
+  const bool need_in = j.kind == kPull || j.kind == kNorm;
+  const bool need_out = j.kind == kGather || j.kind == kRingGather || ((j.kind == kPull || j.kind == kNorm) && j.push);
+  const bool need_out2 = j.kind == kNorm && j.push;
   const Registration* reg_in = nullptr;
   const Registration* reg_out = nullptr;
+  const Registration* reg_out2 = nullptr;
   if (c->multiprocess) {
+    if (need_out2 && !(reg_out2 = c->find_reg(nb->resid_out[0])))
+      return fail(CF_E_TOPOLOGY, "residual-out buffer %p is not registered (cfBufferExport/cfBufferImport); "
+                                 "the two-shot fused kernel writes it from the peers", nb->resid_out[0]);
     if (need_in && !(reg_in = c->find_reg(send[0])))
       return fail(CF_E_TOPOLOGY, "send buffer %p is not registered (cfBufferExport/cfBufferImport); "
                                  "HB algorithms read it from the peers", send[0]);
@@ -579,6 +594,9 @@ cfStatus launch(cfComm* c, const Job& j, int dtype, const void* const* send, voi
     a.cs = j.cs;
     a.slot = j.slot ? j.slot : c->lay.slot;
     a.half = c->lay.half;
+    a.rows = j.rows;
+    a.hidden = j.hidden;
+    a.eps = j.eps;
     for (size_t k = 0; k < g.size(); k++) {
       const int li = g[k];
       RankCtx& rk = a.rk[k];
@@ -592,19 +610,27 @@ cfStatus launch(cfComm* c, const Job& j, int dtype, const void* const* send, voi
         rk.sem[p] = c->sem(li, p);
         rk.ack[p] = c->ack(li, p);
         rk.ring[p] = c->ring(li, p);
+        if (nb) rk.out2[p] = c->multiprocess ? nullptr : (char*)nb->resid_out[p];
+      }
+      if (nb) {
+        rk.resid = (const char*)nb->resid_in[li];
+        rk.weight = (const char*)nb->weight[li];
       }
       if (c->multiprocess) {
         for (int p = 0; p < c->nranks; p++) {
           if (reg_in) rk.in[p] = reg_in->peer[p] + ((const char*)send[li] - reg_in->ptr);
           if (reg_out) rk.out[p] = reg_out->peer[p] + ((char*)recv[li] - reg_out->ptr);
+          if (reg_out2) rk.out2[p] = reg_out2->peer[p] + ((char*)nb->resid_out[li] - reg_out2->ptr);
         }
         rk.in[rk.rank] = (const char*)send[li];
         rk.out[rk.rank] = (char*)recv[li];
+        if (nb) rk.out2[rk.rank] = (char*)nb->resid_out[li];
       }
     }
     int mb = max_blocks_per_rank(c, kernel, (int)gi, threads);
     if (j.kind == kRing || j.kind == kRingGather) mb = std::min(mb, kRingCtas);   // ring slot region
     int blocks = (int)std::min<size_t>((size_t)mb, std::max<size_t>(1, ceil_div(j.work, (size_t)threads)));
+    if (j.blocks) blocks = std::min(mb, j.blocks);
     CF_TRY(join_streams(c, (int)gi, streams, false));
     void* args[] = {&a};
     CF_CUDA(cudaLaunchKernel(kernel, dim3(blocks, g.size()), dim3(threads), args, 0, streams[g[0]]));
@@ -765,4 +791,57 @@ extern "C" cfStatus cfReduceScatter(cfComm_t c, const void* const* send, void* c
   j.cs = recvcount;
   j.work = ceil_div(recvcount, 16 / es) + 1;
   return launch(c, j, dtype, send, recv, streams);
+}
+
+// K13: AllReduce + residual add + RMSNorm (see cf.h).
+extern "C" cfStatus cfAllReduceAddRMSNorm(cfComm_t c, const void* const* send, const void* const* resid_in,
+                                          void* const* resid_out, void* const* norm_out,
+                                          const void* const* weight, size_t rows, size_t hidden, float eps,
+                                          cfDtype dtype, int algo, const cudaStream_t* streams) {
+  CF_TRY(check_ptrs(c, send, norm_out, streams));
+  if (!resid_in || !resid_out || !weight) return fail(CF_E_CONFIG, "null buffer array");
+  if (dtype != CF_F32 && dtype != CF_F16 && dtype != CF_BF16)
+    return fail(CF_E_SHAPE, "RMSNorm needs a floating-point dtype (got %d)", (int)dtype);
+  if (rows == 0 || hidden == 0) return CF_OK;
+  const int n = c->nranks;
+  const size_t es = dtype_size(dtype);
+  if ((hidden * es) % 16)
+    return fail(CF_E_BAD_ALIGN, "hidden=%zu: rows must be whole 16-byte vectors (hidden * %zu %% 16 != 0)",
+                hidden, es);
+  if (!(eps >= 0.f)) return fail(CF_E_CONFIG, "eps must be >= 0");
+  for (size_t li = 0; li < c->local.size(); li++) {
+    if (!resid_in[li] || !resid_out[li] || !weight[li]) return fail(CF_E_OOB, "local rank %zu: null buffer", li);
+    if (((uintptr_t)resid_in[li] | (uintptr_t)resid_out[li] | (uintptr_t)weight[li]) & 15)
+      return fail(CF_E_BAD_ALIGN, "local rank %zu: buffers must be 16-byte aligned", li);
+  }
+  if (algo == CF_ALGO_AUTO) {
+    // two-shot once every rank owns at least one row and the rows are large
+    // enough for the (n-1)x smaller reads to beat the extra pushes
+    algo = (rows >= (size_t)n && rows * hidden * es >= ((size_t)256 << 10)) ? CF_ALGO_2PA : CF_ALGO_1PA_HB;
+    if (algo == CF_ALGO_1PA_HB)
+      for (size_t li = 0; li < c->local.size(); li++)
+        if (send[li] == norm_out[li]) algo = CF_ALGO_2PA;
+  }
+  Job j;
+  j.kind = kNorm;
+  j.order = kLead;
+  j.rows = rows;
+  j.hidden = hidden;
+  j.eps = eps;
+  j.count = rows * hidden;
+  switch (algo) {
+    case CF_ALGO_1PA_HB:
+      for (size_t li = 0; li < c->local.size(); li++)
+        if (send[li] == norm_out[li]) return fail(CF_E_SHAPE, "one-shot fused AllReduce cannot run in place");
+      j.blocks = (int)std::min<size_t>(rows, CF_MAX_BLOCKS);
+      break;
+    case CF_ALGO_2PA:
+      j.push = 1;
+      j.blocks = (int)std::min<size_t>(ceil_div(rows, (size_t)n), CF_MAX_BLOCKS);
+      break;
+    default:
+      return fail(CF_E_NO_ALGO, "algorithm %d: the fused AllReduce+RMSNorm runs as 1pa_hb or 2pa", algo);
+  }
+  NormBufs nb{resid_in, resid_out, weight};
+  return launch(c, j, dtype, send, norm_out, streams, &nb);
 }

@@ -37,8 +37,13 @@ def main():
     cases = [("sync", graph_sync(8192)), ("copy16k", graph_copy(8192)),
              ("2pa_b1", build_2pa(LoweringParams(n, 8192, "bf16"), "memory")),
              ("2pa_b64", build_2pa(LoweringParams(n, 8192 * 64, "bf16"), "memory"))]
+    from paper_2504_09014_b200 import parse_plan
+    from paper_2504_09014_b200.plan import scale_plan
+    with open(os.path.join(ROOT, "tests/golden/plans/1pa_n8_e64.json"), "rb") as f:
+        p1 = parse_plan(f.read())
+    cases += [("1pa_b1", scale_plan(p1, 128)), ("1pa_b64", scale_plan(p1, 8192))]
     for name, g in cases:
-        plan = lower(g, LoweringParams(n, g.params.elems, "bf16"))
+        plan = g if not isinstance(g, ProgramGraph) else lower(g, LoweringParams(n, g.params.elems, "bf16"))
         rt = Runtime(plan, w, dtype="bf16")
         xs = [torch.randn(rt.in_elems, device=dev).to(torch.bfloat16) for _ in range(n)]
         ys = [torch.empty(rt.out_elems, device=dev, dtype=torch.bfloat16) for _ in range(n)]

@@ -1,0 +1,125 @@
+"""GPU parity of K13, the fused AllReduce + residual add + RMSNorm
+(``cfAllReduceAddRMSNorm``), against a plain PyTorch fp32 restatement of the
+unfused composition (``collective("allreduce")`` then host arithmetic).
+
+Tolerances: the residual output is an integer-exact function of the inputs
+(sequential f32 adds x_0 + x_1 + ..., one rounding to dtype, one f32 add of the
+residual, one rounding) and must match bit for bit.  The normalised output
+depends on the row's sum of squares, which the kernel reduces as a tree: it
+may differ from the sequential fp32 reference by one rounding of the output
+dtype, so it is checked with rtol = 2^-7 (bf16), 2^-10 (f16), 1e-5 (f32).
+Every rank must hold identical bits (TP replicas must not diverge)."""
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+_WORLDS = {}
+RTOL = {torch.bfloat16: 2 ** -7, torch.float16: 2 ** -10, torch.float32: 1e-5}
+
+
+def world(n):
+    from paper_2504_09014_b200 import make_world
+    if n not in _WORLDS:
+        _WORLDS[n] = make_world(1, n, spin_timeout_ms=5000)
+    return _WORLDS[n]
+
+
+def reference(xs, res, w, eps):
+    """The unfused composition in plain PyTorch fp32."""
+    dt = xs[0].dtype
+    s = xs[0].float()
+    for x in xs[1:]:
+        s = s + x.float()
+    ro = (s.to(dt).float() + res.float()).to(dt)
+    var = ro.float().pow(2).mean(-1, keepdim=True)
+    y = (ro.float() * torch.rsqrt(var + eps) * w.float()).to(dt)
+    return y, ro
+
+
+def make(n, rows, hidden, dt, seed):
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    xs = [(torch.randn(rows, hidden, generator=g) * 0.5).to(dt).cuda() for _ in range(n)]
+    res = (torch.randn(rows, hidden, generator=g)).to(dt).cuda()
+    w = (1.0 + 0.1 * torch.randn(hidden, generator=g)).to(dt).cuda()
+    return xs, res, w
+
+
+def check(n, rows, hidden, dt, algo, seed=0, eps=1e-6, separate_out=False):
+    from paper_2504_09014_b200 import allreduce_add_rmsnorm
+    wd = world(n)
+    xs, res, w = make(n, rows, hidden, dt, seed)
+    y_ref, ro_ref = reference(xs, res, w, eps)
+    residuals = [res.clone() for _ in range(n)]
+    outs = [torch.empty_like(res) for _ in range(n)] if separate_out else None
+    y, ro = allreduce_add_rmsnorm(wd, xs, residuals, w, eps=eps, algo=algo, resid_out=outs)
+    wd.synchronize()
+    for r in range(n):
+        assert torch.equal(ro[r].view(torch.int16 if dt != torch.float32 else torch.int32),
+                           ro_ref.view(torch.int16 if dt != torch.float32 else torch.int32)), f"rank {r} resid"
+        torch.testing.assert_close(y[r].float(), y_ref.float(), rtol=RTOL[dt], atol=1e-6)
+        assert torch.equal(y[r], y[0])
+    if separate_out:
+        for r in range(n):
+            assert torch.equal(residuals[r], res)   # input untouched
+
+
+@pytest.mark.parametrize("algo", ["1pa_hb", "2pa", None])
+@pytest.mark.parametrize("rows,hidden", [(1, 8192), (3, 64), (8, 8192), (64, 8192), (17, 4096)])
+def test_fused_bf16_c5_shapes(algo, rows, hidden):
+    check(8, rows, hidden, torch.bfloat16, algo, seed=rows * 7 + hidden)
+
+
+@pytest.mark.parametrize("dt", [torch.float32, torch.float16])
+@pytest.mark.parametrize("algo", ["1pa_hb", "2pa"])
+def test_fused_dtypes(dt, algo):
+    check(8, 16, 2048, dt, algo, seed=3)
+
+
+@pytest.mark.parametrize("n", [2, 4])
+def test_fused_rank_counts(n):
+    check(n, 9, 1024, torch.bfloat16, "2pa", seed=n)
+    check(n, 9, 1024, torch.bfloat16, "1pa_hb", seed=n + 1)
+
+
+def test_fused_wide_rows_uncached_path():
+    # 20000 bf16 = 2500 vectors per row: more than kCache * threads, so part of
+    # each row is re-read from resid_out between the passes
+    check(8, 5, 20000, torch.bfloat16, "2pa", seed=11)
+    check(8, 2, 20000, torch.bfloat16, "1pa_hb", seed=12)
+
+
+def test_fused_separate_resid_out():
+    check(8, 8, 8192, torch.bfloat16, "2pa", seed=5, separate_out=True)
+
+
+def test_fused_repeated_calls_and_in_place_norm():
+    from paper_2504_09014_b200 import allreduce_add_rmsnorm
+    wd = world(8)
+    for it in range(4):
+        xs, res, w = make(8, 16, 8192, torch.bfloat16, 100 + it)
+        y_ref, ro_ref = reference(xs, res, w, 1e-5)
+        residuals = [res.clone() for _ in range(8)]
+        # two-shot may write its output over its input (each row is read
+        # before it is written, by the same CTA)
+        y, ro = allreduce_add_rmsnorm(wd, xs, residuals, w, eps=1e-5, algo="2pa", norm_out=xs)
+        wd.synchronize()
+        for r in range(8):
+            assert torch.equal(ro[r], ro_ref)
+            torch.testing.assert_close(y[r].float(), y_ref.float(), rtol=2 ** -7, atol=1e-6)
+
+
+def test_fused_errors():
+    from paper_2504_09014_b200 import allreduce_add_rmsnorm
+    from paper_2504_09014_b200.errors import BadAlignError, ShapeError
+    wd = world(8)
+    xs, res, w = make(8, 2, 64, torch.bfloat16, 0)
+    with pytest.raises(ShapeError):   # one-shot cannot run in place
+        allreduce_add_rmsnorm(wd, xs, [res.clone() for _ in range(8)], w, algo="1pa_hb", norm_out=xs)
+    xi = [torch.ones(2, 64, dtype=torch.int32, device="cuda") for _ in range(8)]
+    with pytest.raises(ShapeError):   # RMSNorm needs floating point
+        allreduce_add_rmsnorm(wd, xi, [x.clone() for x in xi], torch.ones(64, dtype=torch.int32, device="cuda"))
+    xo = [torch.ones(2, 3, dtype=torch.bfloat16, device="cuda") for _ in range(8)]
+    with pytest.raises(BadAlignError):   # rows must be whole 16-byte vectors
+        allreduce_add_rmsnorm(wd, xo, [x.clone() for x in xo], torch.ones(3, dtype=torch.bfloat16, device="cuda"))

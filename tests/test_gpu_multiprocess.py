@@ -57,6 +57,21 @@ def _worker(rank, world, port, q):
             out[("rs", elems)] = rs_out.cpu().numpy().copy()
             for t in (send, recv, ag, rs_in):
                 comm.deregister(t)
+        # K13 fused AllReduce + residual + RMSNorm, both algorithms
+        fx = gen_inputs(world, 6 * 1024, "f32", "uniform", 5)
+        x = torch.from_numpy(fx[rank]).cuda().view(6, 1024)
+        res = torch.from_numpy(gen_inputs(1, 6 * 1024, "f32", "uniform", 6)[0]).cuda().view(6, 1024)
+        wt = torch.linspace(0.5, 1.5, 1024, device="cuda")
+        for algo in ("1pa_hb", "2pa"):
+            ro = torch.empty_like(res)
+            y = torch.empty_like(x)
+            for t in (x, ro, y):
+                comm.register(t)
+            comm.all_reduce_add_rmsnorm(x, res, wt, eps=1e-6, algo=algo, resid_out=ro, norm_out=y)
+            torch.cuda.synchronize()
+            out[("norm", algo)] = (y.cpu().numpy().copy(), ro.cpu().numpy().copy())
+            for t in (x, ro, y):
+                comm.deregister(t)
         comm.check_device_error()
         comm.close()
         dist.barrier()
@@ -97,3 +112,15 @@ def test_two_processes_one_gpu_all_collectives():
         for r in range(world):
             assert np.array_equal(res[r][("ag", elems)], cat)
             assert np.array_equal(res[r][("rs", elems)].view(np.uint32), rs_want[r].view(np.uint32))
+    fx = gen_inputs(world, 6 * 1024, "f32", "uniform", 5)
+    h = fx[0].astype(np.float32)
+    for x in fx[1:]:
+        h = (h + x).astype(np.float32)
+    ro = (h + gen_inputs(1, 6 * 1024, "f32", "uniform", 6)[0]).astype(np.float32).reshape(6, 1024)
+    var = (ro.astype(np.float64) ** 2).mean(-1, keepdims=True)
+    y = ro / np.sqrt(var + 1e-6) * np.linspace(0.5, 1.5, 1024)
+    for algo in ("1pa_hb", "2pa"):
+        for r in range(world):
+            got_y, got_ro = res[r][("norm", algo)]
+            assert np.array_equal(got_ro.view(np.uint32), ro.view(np.uint32)), (algo, r)
+            np.testing.assert_allclose(got_y, y, rtol=1e-5, atol=1e-6)
