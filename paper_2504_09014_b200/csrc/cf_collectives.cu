@@ -233,6 +233,15 @@ __global__ void __launch_bounds__(512) ll_oneshot_kernel(const __grid_constant__
 
 // ---------------------------------------------------------------- K4
 
+// A 16-byte payload carried by two LL16 packets whose raw words were already
+// loaded (r0, r1): re-poll only a packet whose flags are not yet `flag`.
+__device__ __forceinline__ uint4 ll16x2_finish(const char* s, uint4 r0, uint4 r1, uint32_t flag, RankState* st) {
+  uint2 p0 = make_uint2(r0.x, r0.z), p1 = make_uint2(r1.x, r1.z);
+  if (r0.y != flag || r0.w != flag) p0 = ll16_get(s, flag, st);
+  if (r1.y != flag || r1.w != flag) p1 = ll16_get(s + 16, flag, st);
+  return make_uint4(p0.x, p0.y, p1.x, p1.y);
+}
+
 // Two-shot LL (cf/collectives.py:216-231): phase 1 sends chunk p of the send
 // buffer as packets into peer p's ph1 slot r; rank r reduces chunk r (owner
 // first, peers ascending), stores it, and sends the result as packets into
@@ -269,7 +278,8 @@ __global__ void __launch_bounds__(512) ll_twoshot_kernel(const __grid_constant__
   {
     const size_t b = vlo(r), nv = vhi(r) > b ? vhi(r) - b : 0;
     for (size_t i = t0; i < nv; i += stride) {
-      uint4 x[NR];
+      // every peer's two packets in flight first, then re-poll the unstamped ones
+      uint4 x[NR], raw1[NR];
 #pragma unroll
       for (int k = 0; k < NR; k++) {
         if (k < n) {
@@ -278,10 +288,16 @@ __global__ void __launch_bounds__(512) ll_twoshot_kernel(const __grid_constant__
             x[k] = load_vec<T>(rk.in[r], b + i, a.count);
           } else {
             const char* s = rk.scr[r] + ph1 + (size_t)q * a.slot + i * 32;
-            const uint2 p0 = ll16_get(s, flag, rk.st);
-            const uint2 p1 = ll16_get(s + 16, flag, rk.st);
-            x[k] = make_uint4(p0.x, p0.y, p1.x, p1.y);
+            x[k] = ld16_volatile(s);
+            raw1[k] = ld16_volatile(s + 16);
           }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < NR; k++) {
+        if (k < n) {
+          const int q = order_src(kLead, k, r, n);
+          if (q != r) x[k] = ll16x2_finish(rk.scr[r] + ph1 + (size_t)q * a.slot + i * 32, x[k], raw1[k], flag, rk.st);
         }
       }
       const uint4 res = reduce_vecs<T, NR>(x, n, false);
@@ -296,15 +312,25 @@ __global__ void __launch_bounds__(512) ll_twoshot_kernel(const __grid_constant__
       }
     }
   }
-  // phase 2: decode the peers' reduced chunks
-  for (int p = 0; p < n; p++) {
-    if (p == r) continue;
-    const size_t b = vlo(p), nv = vhi(p) > b ? vhi(p) - b : 0;
-    const char* src = rk.scr[r] + ph2 + (size_t)p * a.slot;
-    for (size_t i = t0; i < nv; i += stride) {
-      const uint2 p0 = ll16_get(src + i * 32, flag, rk.st);
-      const uint2 p1 = ll16_get(src + i * 32 + 16, flag, rk.st);
-      store_vec<T>(rk.out[r], b + i, make_uint4(p0.x, p0.y, p1.x, p1.y), clo(p), chi(p), 0);
+  // phase 2: decode the peers' reduced chunks (all peers' packets of vector i
+  // in flight at once)
+  const size_t nvmax = (a.cs + V - 1) / V + 1;
+  for (size_t i = t0; i < nvmax; i += stride) {
+    uint4 raw0[NR], raw1[NR];
+#pragma unroll
+    for (int p = 0; p < NR; p++) {
+      if (p < n && p != r && vlo(p) + i < vhi(p)) {
+        const char* s = rk.scr[r] + ph2 + (size_t)p * a.slot + i * 32;
+        raw0[p] = ld16_volatile(s);
+        raw1[p] = ld16_volatile(s + 16);
+      }
+    }
+#pragma unroll
+    for (int p = 0; p < NR; p++) {
+      if (p < n && p != r && vlo(p) + i < vhi(p)) {
+        const uint4 v = ll16x2_finish(rk.scr[r] + ph2 + (size_t)p * a.slot + i * 32, raw0[p], raw1[p], flag, rk.st);
+        store_vec<T>(rk.out[r], vlo(p) + i, v, clo(p), chi(p), 0);
+      }
     }
   }
   end_call(rk, e);
