@@ -187,6 +187,18 @@ CF_API cfStatus cfAllGather(cfComm_t comm, const void* const* send, void* const*
 CF_API cfStatus cfReduceScatter(cfComm_t comm, const void* const* send, void* const* recv, size_t recvcount,
                          cfDtype dtype, int algo, const cudaStream_t* streams);
 
+/* AllReduce of HOST buffers (the reference's calling convention: collective()
+ * takes host arrays and returns host arrays, cf/collectives.py:532-573 with
+ * the copies of cf/executor.py:160-175).  One-process worlds only
+ * (CF_E_TOPOLOGY otherwise).  The comm keeps device staging buffers (grown on
+ * demand); two-shot messages >= 32 MiB per rank run as a pipeline of windows
+ * per chunk so H2D copies, the kernel and D2H copies overlap -- results are
+ * bit-identical to cfAllReduce.  Pinned host memory makes the copies
+ * asynchronous; completion is ordered on streams[] (synchronize them before
+ * reading recv). */
+CF_API cfStatus cfAllReduceHost(cfComm_t comm, const void* const* host_send, void* const* host_recv, size_t count,
+                                cfDtype dtype, int algo, const cudaStream_t* streams);
+
 /* Fused AllReduce + residual add + RMSNorm (the reference
  * composes it as `collective("allreduce", ...)` (cf/collectives.py:532-573)
  * followed by host arithmetic).  Per local rank, on rows x hidden elements

@@ -33,7 +33,7 @@ EXPORTS = (
     "cfDeviceMulticastSupported", "cfNvlsCreate", "cfNvlsImport", "cfNvlsBind", "cfCommNumRanks",
     "cfCommLocalRanks",
     "cfCommMulticastSupported", "cfCommLastDeviceError", "cfCommClearDeviceError", "cfAllReduce",
-    "cfAllGather", "cfReduceScatter", "cfAllReduceAddRMSNorm", "cfSelectAlgorithm", "cfPlanLoad", "cfPlanExecute",
+    "cfAllGather", "cfReduceScatter", "cfAllReduceHost", "cfAllReduceAddRMSNorm", "cfSelectAlgorithm", "cfPlanLoad", "cfPlanExecute",
     "cfPlanInfo", "cfPlanLastDeviceError", "cfPlanDestroy",
 )
 
@@ -77,6 +77,7 @@ _PROTOS = {
     "cfAllReduce": ([vp, P(vp), P(vp), sz, i32, i32, P(vp)], i32),
     "cfAllGather": ([vp, P(vp), P(vp), sz, i32, i32, P(vp)], i32),
     "cfReduceScatter": ([vp, P(vp), P(vp), sz, i32, i32, P(vp)], i32),
+    "cfAllReduceHost": ([vp, P(vp), P(vp), sz, i32, i32, P(vp)], i32),
     "cfAllReduceAddRMSNorm": ([vp, P(vp), P(vp), P(vp), P(vp), P(vp), sz, sz, ctypes.c_float, i32, i32,
                                P(vp)], i32),
     "cfSelectAlgorithm": ([vp, i32, sz, i32, P(i32)], i32),

@@ -240,9 +240,10 @@ def collective(kind: str, inputs, world, selector: Selector | None = None, dtype
         dtype = from_torch(inputs[0].dtype)
         tensors = [a.contiguous().view(-1) for a in inputs]
     elif host_tensors:
-        # host torch tensors (pinned for async copies): H2D, run, D2H into host tensors
+        # host torch tensors (pinned for async copies): AllReduce goes through
+        # cfAllReduceHost below; the other collectives copy H2D, run, copy D2H
         dtype = from_torch(inputs[0].dtype)
-        tensors = [a.reshape(-1).to(world.device(r), non_blocking=True) for r, a in enumerate(inputs)]
+        tensors = [a.reshape(-1) for a in inputs]
         on_gpu = True
     else:
         tensors = None
@@ -265,8 +266,23 @@ def collective(kind: str, inputs, world, selector: Selector | None = None, dtype
     aid = _algo_id(kind, name, var)
     mult = required_multiple(_lib.ALGO_NAMES[aid] if _lib.ALGO_NAMES[aid] != "2pa_ll" else "2pa", n)
 
+    if host_tensors and kind == "allreduce" and elems and not (via_plan or (name == "2pa" and var == "port")):
+        # host in, host out through libcf's pipelined host path (copies overlap the kernel)
+        src = [a.contiguous().view(-1) for a in inputs]
+        pin = src[0].is_pinned()
+        host = outputs if outputs is not None else \
+            [torch.empty(a.shape, dtype=a.dtype, pin_memory=pin) for a in src]
+        _lib.check(_lib.lib().cfAllReduceHost(
+            world.comm, _lib.ptr_array([a.data_ptr() for a in src]),
+            _lib.ptr_array([h.data_ptr() for h in host]), elems, CODES[dtype], aid,
+            _lib.ptr_array(world.streams())))
+        world.synchronize()
+        world.check_device_error()
+        return host
     if not on_gpu:
         tensors = _to_device(arrays, world, dtype)
+    elif host_tensors:
+        tensors = [t.to(world.device(r), non_blocking=True) for r, t in enumerate(tensors)]
     if elems == 0:
         shape = {"allreduce": 0, "allgather": 0, "reducescatter": 0}[kind]
         outs = [t.new_empty(shape) for t in tensors]

@@ -135,8 +135,10 @@ __global__ void __launch_bounds__(512) pull_reduce_kernel(const __grid_constant_
 
   size_t lo = 0, hi = a.count;
   if (!a.whole) {
-    lo = min((size_t)r * a.cs, a.count);
-    hi = min(lo + a.cs, a.count);
+    const size_t c0 = (size_t)r * a.cs;
+    lo = min(c0 + a.win_lo, a.count);
+    hi = min(c0 + min(a.cs, a.win_hi), a.count);
+    lo = min(lo, hi);
   }
   const bool zero = a.order != kLead;
   const char* src[NR];

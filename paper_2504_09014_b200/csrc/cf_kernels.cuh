@@ -53,6 +53,8 @@ struct CollArgs {
   size_t hidden;
   float eps;        // K13: RMSNorm epsilon
   int pad2_;
+  size_t win_lo;    // pull-reduce (not whole): element window [win_lo, win_hi) inside each
+  size_t win_hi;    // rank's chunk (pipelined host calls); 0 / SIZE_MAX = the whole chunk
   RankCtx rk[CF_MAX_RANKS];
 };
 

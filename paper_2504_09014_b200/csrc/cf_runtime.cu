@@ -355,10 +355,24 @@ extern "C" cfStatus cfCommDestroy(cfComm_t c) {
   for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
   proxy_stop(c);
   nvls_teardown(c);
+  for (size_t gi = 0; gi < c->pipes.size(); gi++) {
+    auto& hp = c->pipes[gi];
+    cudaSetDevice(c->local[c->groups[gi][0]].dev);
+    for (cudaEvent_t e : {hp.fork, hp.done})
+      if (e) cudaEventDestroy(e);
+    for (int k = 0; k < kHostPieces; k++) {
+      if (hp.in[k]) cudaEventDestroy(hp.in[k]);
+      if (hp.ar[k]) cudaEventDestroy(hp.ar[k]);
+    }
+    if (hp.h2d) cudaStreamDestroy(hp.h2d);
+    if (hp.d2h) cudaStreamDestroy(hp.d2h);
+  }
   for (auto& lr : c->local) {
     if (lr.dev >= 0) cudaSetDevice(lr.dev);
     if (lr.heap) cudaFree(lr.heap);
     if (lr.ev) cudaEventDestroy(lr.ev);
+    if (lr.stage_in) cudaFree(lr.stage_in);
+    if (lr.stage_out) cudaFree(lr.stage_out);
   }
   delete c;
   return CF_OK;
@@ -531,6 +545,7 @@ struct Job {
   size_t rows = 0, hidden = 0;   // K13
   float eps = 0.f;
   int blocks = 0;     // explicit CTAs per rank (K13: one per row), else from `work`
+  size_t win_lo = 0, win_hi = ~(size_t)0;   // pull-reduce window inside each chunk
 };
 
 // K13's extra per-local-rank buffers.
@@ -596,6 +611,8 @@ cfStatus launch(cfComm* c, const Job& j, int dtype, const void* const* send, voi
     a.half = c->lay.half;
     a.rows = j.rows;
     a.hidden = j.hidden;
+    a.win_lo = j.win_lo;
+    a.win_hi = j.win_hi;
     a.eps = j.eps;
     for (size_t k = 0; k < g.size(); k++) {
       const int li = g[k];
@@ -844,4 +861,168 @@ extern "C" cfStatus cfAllReduceAddRMSNorm(cfComm_t c, const void* const* send, c
   }
   NormBufs nb{resid_in, resid_out, weight};
   return launch(c, j, dtype, send, norm_out, streams, &nb);
+}
+
+// ---------------------------------------------------------------- host-buffer AllReduce
+
+namespace {
+
+// Copy window [w0, w1) of every n-row chunk (row pitch cs elements) of a
+// count-element message between host and a device buffer of the same layout.
+cudaError_t copy_window(char* dst, const char* src, size_t count, size_t cs, int n, size_t w0, size_t w1,
+                        size_t es, cudaMemcpyKind kind, cudaStream_t st) {
+  // rows whose whole window lies inside the message: one 2-D copy
+  size_t full = 0;
+  while ((int)full < n && full * cs + w1 <= count) full++;
+  if (full)
+    if (cudaError_t e = cudaMemcpy2DAsync(dst + w0 * es, cs * es, src + w0 * es, cs * es, (w1 - w0) * es, full,
+                                          kind, st))
+      return e;
+  // at most one ragged row (the padded tail lies beyond `count`)
+  if ((int)full < n && full * cs + w0 < count) {
+    const size_t o = full * cs + w0;
+    return cudaMemcpyAsync(dst + o * es, src + o * es, (count - o) * es, kind, st);
+  }
+  return cudaSuccess;
+}
+
+}  // namespace
+
+// AllReduce of HOST buffers (the reference's own calling convention:
+// collective() takes host arrays, cf/collectives.py:532-573).  Large two-shot
+// messages run as a pipeline of up to kHostPieces windows per chunk: the
+// H2D copy of window p+1, the K3 kernel on window p and the D2H copy of
+// window p-1 overlap (copy engines in both directions + SMs).  Windowing
+// keeps each element's owner chunk, so results are bit-identical to
+// cfAllReduce.  Completion is ordered on streams[] like every other call.
+extern "C" cfStatus cfAllReduceHost(cfComm_t c, const void* const* hsend, void* const* hrecv, size_t count,
+                                    cfDtype dtype, int algo, const cudaStream_t* streams) {
+  CF_TRY(check_ptrs(c, hsend, hrecv, streams));
+  if (c->multiprocess)
+    return fail(CF_E_TOPOLOGY, "cfAllReduceHost serves one-process worlds; in the one-process-per-GPU mode "
+                               "copy into registered device buffers and call cfAllReduce");
+  if ((int)dtype < 0 || (int)dtype > 3) return fail(CF_E_SHAPE, "unknown dtype %d", (int)dtype);
+  if (count == 0) return CF_OK;
+  const int n = c->nranks;
+  const size_t es = dtype_size(dtype), V = 16 / es;
+  const size_t bytes = count * es;
+  if (algo == CF_ALGO_AUTO) algo = select_algo(c, 0, bytes, dtype);
+  const size_t padded = round_up(count, (size_t)n);
+  const size_t need = round_up(padded * es, 256);
+  DeviceGuard guard;
+  for (size_t li = 0; li < c->local.size(); li++) {
+    LocalRank& lr = c->local[li];
+    if (lr.stage_bytes >= need) continue;
+    CF_CUDA(cudaSetDevice(lr.dev));
+    CF_CUDA(cudaDeviceSynchronize());   // earlier calls may still read the old staging
+    if (lr.stage_in) cudaFree(lr.stage_in);
+    if (lr.stage_out) cudaFree(lr.stage_out);
+    lr.stage_in = lr.stage_out = nullptr;
+    lr.stage_bytes = 0;
+    CF_CUDA(cudaMalloc(&lr.stage_in, need));
+    CF_CUDA(cudaMalloc(&lr.stage_out, need));
+    lr.stage_bytes = need;
+  }
+  if (c->pipes.empty()) {
+    c->pipes.resize(c->groups.size());
+    for (size_t gi = 0; gi < c->groups.size(); gi++) {
+      auto& hp = c->pipes[gi];
+      CF_CUDA(cudaSetDevice(c->local[c->groups[gi][0]].dev));
+      CF_CUDA(cudaStreamCreateWithFlags(&hp.h2d, cudaStreamNonBlocking));
+      CF_CUDA(cudaStreamCreateWithFlags(&hp.d2h, cudaStreamNonBlocking));
+      CF_CUDA(cudaEventCreateWithFlags(&hp.fork, cudaEventDisableTiming));
+      CF_CUDA(cudaEventCreateWithFlags(&hp.done, cudaEventDisableTiming));
+      for (int k = 0; k < kHostPieces; k++) {
+        CF_CUDA(cudaEventCreateWithFlags(&hp.in[k], cudaEventDisableTiming));
+        CF_CUDA(cudaEventCreateWithFlags(&hp.ar[k], cudaEventDisableTiming));
+      }
+    }
+  }
+  std::vector<const void*> din(c->local.size());
+  std::vector<void*> dout(c->local.size());
+  for (size_t li = 0; li < c->local.size(); li++) {
+    din[li] = c->local[li].stage_in;
+    dout[li] = c->local[li].stage_out;
+  }
+  // pipeline only the two-shot HB kernel (windows keep each element's owner)
+  const bool pipelined = algo == CF_ALGO_2PA && bytes >= ((size_t)32 << 20);
+  const size_t cs = padded / n;
+  size_t pieces = 1, q = cs;
+  if (pipelined) {
+    pieces = std::min<size_t>(kHostPieces, bytes / ((size_t)8 << 20));
+    if (const char* env = getenv("CF_HOST_PIECES")) pieces = std::max<size_t>(1, std::min<size_t>(kHostPieces, atoi(env)));
+    q = round_up(ceil_div(cs, pieces), V);
+    pieces = ceil_div(cs, q);
+  }
+  const size_t G = c->groups.size();
+  auto s0 = [&](size_t gi) { return streams[c->groups[gi][0]]; };
+  // fork the copy streams off the callers' streams
+  for (size_t gi = 0; gi < G; gi++) {
+    auto& hp = c->pipes[gi];
+    CF_CUDA(cudaSetDevice(c->local[c->groups[gi][0]].dev));
+    CF_TRY(join_streams(c, (int)gi, streams, false));
+    CF_CUDA(cudaEventRecord(hp.fork, s0(gi)));
+    CF_CUDA(cudaStreamWaitEvent(hp.h2d, hp.fork, 0));
+    CF_CUDA(cudaStreamWaitEvent(hp.d2h, hp.fork, 0));
+  }
+  for (size_t p = 0; p < pieces; p++) {
+    const size_t w0 = p * q, w1 = std::min(cs, w0 + q);
+    for (size_t gi = 0; gi < G; gi++) {
+      auto& hp = c->pipes[gi];
+      CF_CUDA(cudaSetDevice(c->local[c->groups[gi][0]].dev));
+      for (int li : c->groups[gi]) {
+        if (pipelined)
+          CF_CUDA(copy_window(c->local[li].stage_in, (const char*)hsend[li], count, cs, n, w0, w1, es,
+                              cudaMemcpyHostToDevice, hp.h2d));
+        else
+          CF_CUDA(cudaMemcpyAsync(c->local[li].stage_in, hsend[li], bytes, cudaMemcpyHostToDevice, hp.h2d));
+      }
+      CF_CUDA(cudaEventRecord(hp.in[p], hp.h2d));
+    }
+    for (size_t gi = 0; gi < G; gi++) {   // every rank's window is read by every rank
+      CF_CUDA(cudaSetDevice(c->local[c->groups[gi][0]].dev));
+      for (size_t g2 = 0; g2 < G; g2++) CF_CUDA(cudaStreamWaitEvent(s0(gi), c->pipes[g2].in[p], 0));
+    }
+    if (pipelined) {
+      Job j;
+      j.kind = kPull;
+      j.push = 1;
+      j.order = kLead;
+      j.count = count;
+      j.cs = cs;
+      j.win_lo = w0;
+      j.win_hi = w1;
+      j.work = ceil_div(w1 - w0, V) + 1;
+      CF_TRY(launch(c, j, dtype, din.data(), dout.data(), streams));
+    } else {
+      CF_TRY(cfAllReduce(c, din.data(), dout.data(), count, dtype, algo, streams));
+    }
+    for (size_t gi = 0; gi < G; gi++) {
+      CF_CUDA(cudaSetDevice(c->local[c->groups[gi][0]].dev));
+      CF_CUDA(cudaEventRecord(c->pipes[gi].ar[p], s0(gi)));
+    }
+    for (size_t gi = 0; gi < G; gi++) {   // two-shot pushes: window p is final once every rank ran it
+      auto& hp = c->pipes[gi];
+      CF_CUDA(cudaSetDevice(c->local[c->groups[gi][0]].dev));
+      for (size_t g2 = 0; g2 < G; g2++) CF_CUDA(cudaStreamWaitEvent(hp.d2h, c->pipes[g2].ar[p], 0));
+      for (int li : c->groups[gi]) {
+        if (pipelined)
+          CF_CUDA(copy_window((char*)hrecv[li], c->local[li].stage_out, count, cs, n, w0, w1, es,
+                              cudaMemcpyDeviceToHost, hp.d2h));
+        else
+          CF_CUDA(cudaMemcpyAsync(hrecv[li], c->local[li].stage_out, bytes, cudaMemcpyDeviceToHost, hp.d2h));
+      }
+    }
+  }
+  // join: the callers' streams complete after the last D2H copy
+  for (size_t gi = 0; gi < G; gi++) {
+    auto& hp = c->pipes[gi];
+    CF_CUDA(cudaSetDevice(c->local[c->groups[gi][0]].dev));
+    CF_CUDA(cudaEventRecord(hp.done, hp.d2h));
+    CF_CUDA(cudaStreamWaitEvent(s0(gi), hp.done, 0));
+    CF_CUDA(cudaEventRecord(hp.fork, hp.h2d));   // h2d idle before the next call's fork
+    CF_CUDA(cudaStreamWaitEvent(s0(gi), hp.fork, 0));
+    CF_TRY(join_streams(c, (int)gi, streams, true));
+  }
+  return CF_OK;
 }

@@ -54,6 +54,17 @@ struct LocalRank {
   int dev = -1;
   char* heap = nullptr;
   cudaEvent_t ev = nullptr;   // stream joins for co-resident ranks
+  char* stage_in = nullptr;   // cfAllReduceHost device staging (grown on demand)
+  char* stage_out = nullptr;
+  size_t stage_bytes = 0;
+};
+
+// cfAllReduceHost: per-device copy streams and the events of one pipelined call.
+constexpr int kHostPieces = 32;
+struct HostPipe {
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  cudaEvent_t fork = nullptr, done = nullptr;
+  cudaEvent_t in[kHostPieces] = {}, ar[kHostPieces] = {};
 };
 
 // A registered buffer range (one-process-per-GPU mode) and the peers' mapped
@@ -110,6 +121,7 @@ struct cfComm {
   bool multicast_supported = false;
   cf::Nvls nvls;
   cf::Proxy* proxy = nullptr;          // PortChannel proxy thread (started on demand)
+  std::vector<cf::HostPipe> pipes;     // per group (cfAllReduceHost), created on first use
 
   cf::RankState* state(int li) const { return (cf::RankState*)(local[li].heap + lay.state_off); }
   uint64_t* sem(int li, int p) const { return (uint64_t*)(peer_heap[li][p] + lay.sem_off); }

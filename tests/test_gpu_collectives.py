@@ -180,3 +180,28 @@ def test_nvls_multicast_path_single_rank():
 
 def test_coresident_world_has_no_multicast():
     assert not world(8).multicast_supported()
+
+
+@pytest.mark.parametrize("dtype,elems", [("f32", (48 << 20) // 4 + 5), ("bf16", (64 << 20) // 2 + 24),
+                                         ("bf16", 1000), ("i32", 4096 + 3)])
+def test_host_buffer_allreduce_matches_device_path(dtype, elems):
+    """cfAllReduceHost (pinned host tensors through collective()): the
+    pipelined windows (>= 32 MiB per rank, ragged chunks) give the same bits
+    as the device-buffer kernel, and the small path equals it too."""
+    import torch
+    from paper_2504_09014_b200 import collective
+    from paper_2504_09014_b200.dtypes import torch_dtype
+    w = world(8)
+    g = torch.Generator().manual_seed(elems)
+    host = [(torch.randn(elems, generator=g) * 4).to(torch_dtype(dtype)) if dtype != "i32"
+            else torch.randint(-1000, 1000, (elems,), generator=g, dtype=torch.int32) for _ in range(8)]
+    host = [h.pin_memory() for h in host]
+    got = collective("allreduce", host, w, algo="2pa")
+    dev = collective("allreduce", [h.cuda() for h in host], w, algo="2pa")
+    for r in range(8):
+        assert not got[r].is_cuda
+        assert torch.equal(got[r].view(torch.int16 if dtype == "bf16" else got[r].dtype),
+                           dev[r].cpu().view(torch.int16 if dtype == "bf16" else dev[r].dtype)), r
+    # pageable host tensors take the same path (synchronous copies)
+    got2 = collective("allreduce", [h.clone() for h in host[:8]], w, algo="2pa")
+    assert all(torch.equal(a, b) for a, b in zip(got, got2))
