@@ -198,6 +198,12 @@ CF_API cfStatus cfReduceScatter(cfComm_t comm, const void* const* send, void* co
  * reading recv). */
 CF_API cfStatus cfAllReduceHost(cfComm_t comm, const void* const* host_send, void* const* host_recv, size_t count,
                                 cfDtype dtype, int algo, const cudaStream_t* streams);
+/* cfAllReduceHost with caller-provided device staging buffers (count elements
+ * each, send != recv) -- the form the one-process-per-GPU mode uses, with the
+ * staging buffers registered through cfBufferExport/cfBufferImport. */
+CF_API cfStatus cfAllReduceHostStaged(cfComm_t comm, const void* const* host_send, void* const* host_recv,
+                                      const void* const* dev_send, void* const* dev_recv, size_t count,
+                                      cfDtype dtype, int algo, const cudaStream_t* streams);
 
 /* Fused AllReduce + residual add + RMSNorm (the reference
  * composes it as `collective("allreduce", ...)` (cf/collectives.py:532-573)

@@ -33,7 +33,8 @@ EXPORTS = (
     "cfDeviceMulticastSupported", "cfNvlsCreate", "cfNvlsImport", "cfNvlsBind", "cfCommNumRanks",
     "cfCommLocalRanks",
     "cfCommMulticastSupported", "cfCommLastDeviceError", "cfCommClearDeviceError", "cfAllReduce",
-    "cfAllGather", "cfReduceScatter", "cfAllReduceHost", "cfAllReduceAddRMSNorm", "cfSelectAlgorithm", "cfPlanLoad", "cfPlanExecute",
+    "cfAllGather", "cfReduceScatter", "cfAllReduceHost", "cfAllReduceHostStaged",
+    "cfAllReduceAddRMSNorm", "cfSelectAlgorithm", "cfPlanLoad", "cfPlanExecute",
     "cfPlanInfo", "cfPlanLastDeviceError", "cfPlanDestroy",
 )
 
@@ -78,6 +79,7 @@ _PROTOS = {
     "cfAllGather": ([vp, P(vp), P(vp), sz, i32, i32, P(vp)], i32),
     "cfReduceScatter": ([vp, P(vp), P(vp), sz, i32, i32, P(vp)], i32),
     "cfAllReduceHost": ([vp, P(vp), P(vp), sz, i32, i32, P(vp)], i32),
+    "cfAllReduceHostStaged": ([vp, P(vp), P(vp), P(vp), P(vp), sz, i32, i32, P(vp)], i32),
     "cfAllReduceAddRMSNorm": ([vp, P(vp), P(vp), P(vp), P(vp), P(vp), sz, sz, ctypes.c_float, i32, i32,
                                P(vp)], i32),
     "cfSelectAlgorithm": ([vp, i32, sz, i32, P(i32)], i32),

@@ -103,6 +103,41 @@ class Communicator:
         self._call(_lib.lib().cfReduceScatter, send, recv, recv.numel(), aid, stream)
         return recv
 
+    def all_reduce_host(self, host_send, host_recv=None, algo: str = "auto", variant: str = "", stream=None,
+                        sync: bool = True):
+        """AllReduce of a HOST tensor (pinned for overlap): the pipelined
+        host path (``cfAllReduceHostStaged``) -- windowed H2D copy, K3 and D2H
+        copy overlap.  Collective: every rank calls it with the same size.
+        Device staging buffers are allocated and registered on first use per
+        (size, dtype) and reused.  With ``sync`` (default) the call returns
+        once ``host_recv`` holds the result; otherwise it is stream-ordered."""
+        import torch
+        src = host_send.contiguous().view(-1)
+        host_recv = torch.empty(src.shape, dtype=src.dtype, pin_memory=src.is_pinned()) \
+            if host_recv is None else host_recv
+        key = (src.numel(), src.dtype)
+        stage = self.__dict__.setdefault("_stage", {})
+        if key not in stage:
+            for old in list(stage.values()):   # one staging pair at a time
+                for t in old:
+                    self.deregister(t)
+            stage.clear()
+            pair = (torch.empty(src.numel(), dtype=src.dtype, device=self.device),
+                    torch.empty(src.numel(), dtype=src.dtype, device=self.device))
+            for t in pair:
+                self.register(t)
+            stage[key] = pair
+        ds, dr = stage[key]
+        aid = -1 if algo == "auto" else _algo_id("allreduce", algo, variant)
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        P = _lib.ptr_array
+        _lib.check(_lib.lib().cfAllReduceHostStaged(
+            self._comm, P([src.data_ptr()]), P([host_recv.data_ptr()]), P([ds.data_ptr()]), P([dr.data_ptr()]),
+            src.numel(), CODES[from_torch(src.dtype)], aid, P([s.cuda_stream])))
+        if sync:
+            s.synchronize()
+        return host_recv
+
     def all_reduce_add_rmsnorm(self, send, residual, weight, eps: float = 1e-6, algo: str = "auto",
                                resid_out=None, norm_out=None, stream=None):
         """K13 on this rank (see ``fused.allreduce_add_rmsnorm``): returns

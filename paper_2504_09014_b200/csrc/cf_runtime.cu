@@ -895,20 +895,20 @@ cudaError_t copy_window(char* dst, const char* src, size_t count, size_t cs, int
 // window p-1 overlap (copy engines in both directions + SMs).  Windowing
 // keeps each element's owner chunk, so results are bit-identical to
 // cfAllReduce.  Completion is ordered on streams[] like every other call.
+static cfStatus host_allreduce(cfComm* c, const void* const* hsend, void* const* hrecv, const void* const* dsend,
+                               void* const* drecv, size_t count, cfDtype dtype, int algo,
+                               const cudaStream_t* streams);
+
 extern "C" cfStatus cfAllReduceHost(cfComm_t c, const void* const* hsend, void* const* hrecv, size_t count,
                                     cfDtype dtype, int algo, const cudaStream_t* streams) {
   CF_TRY(check_ptrs(c, hsend, hrecv, streams));
   if (c->multiprocess)
     return fail(CF_E_TOPOLOGY, "cfAllReduceHost serves one-process worlds; in the one-process-per-GPU mode "
-                               "copy into registered device buffers and call cfAllReduce");
+                               "pass registered device staging buffers to cfAllReduceHostStaged");
   if ((int)dtype < 0 || (int)dtype > 3) return fail(CF_E_SHAPE, "unknown dtype %d", (int)dtype);
   if (count == 0) return CF_OK;
-  const int n = c->nranks;
-  const size_t es = dtype_size(dtype), V = 16 / es;
-  const size_t bytes = count * es;
-  if (algo == CF_ALGO_AUTO) algo = select_algo(c, 0, bytes, dtype);
-  const size_t padded = round_up(count, (size_t)n);
-  const size_t need = round_up(padded * es, 256);
+  const size_t padded = round_up(count, (size_t)c->nranks);
+  const size_t need = round_up(padded * dtype_size(dtype), 256);
   DeviceGuard guard;
   for (size_t li = 0; li < c->local.size(); li++) {
     LocalRank& lr = c->local[li];
@@ -923,6 +923,36 @@ extern "C" cfStatus cfAllReduceHost(cfComm_t c, const void* const* hsend, void* 
     CF_CUDA(cudaMalloc(&lr.stage_out, need));
     lr.stage_bytes = need;
   }
+  std::vector<const void*> din(c->local.size());
+  std::vector<void*> dout(c->local.size());
+  for (size_t li = 0; li < c->local.size(); li++) {
+    din[li] = c->local[li].stage_in;
+    dout[li] = c->local[li].stage_out;
+  }
+  return host_allreduce(c, hsend, hrecv, din.data(), dout.data(), count, dtype, algo, streams);
+}
+
+extern "C" cfStatus cfAllReduceHostStaged(cfComm_t c, const void* const* hsend, void* const* hrecv,
+                                          const void* const* dsend, void* const* drecv, size_t count,
+                                          cfDtype dtype, int algo, const cudaStream_t* streams) {
+  CF_TRY(check_ptrs(c, hsend, hrecv, streams));
+  CF_TRY(check_ptrs(c, dsend, drecv, streams));
+  if ((int)dtype < 0 || (int)dtype > 3) return fail(CF_E_SHAPE, "unknown dtype %d", (int)dtype);
+  if (count == 0) return CF_OK;
+  for (size_t li = 0; li < c->local.size(); li++)
+    if (dsend[li] == drecv[li]) return fail(CF_E_SHAPE, "staging send and recv must differ");
+  DeviceGuard guard;
+  return host_allreduce(c, hsend, hrecv, dsend, drecv, count, dtype, algo, streams);
+}
+
+static cfStatus host_allreduce(cfComm* c, const void* const* hsend, void* const* hrecv, const void* const* dsend,
+                               void* const* drecv, size_t count, cfDtype dtype, int algo,
+                               const cudaStream_t* streams) {
+  const int n = c->nranks;
+  const size_t es = dtype_size(dtype), V = 16 / es;
+  const size_t bytes = count * es;
+  if (algo == CF_ALGO_AUTO) algo = select_algo(c, 0, bytes, dtype);
+  const size_t padded = round_up(count, (size_t)n);
   if (c->pipes.empty()) {
     c->pipes.resize(c->groups.size());
     for (size_t gi = 0; gi < c->groups.size(); gi++) {
@@ -937,12 +967,6 @@ extern "C" cfStatus cfAllReduceHost(cfComm_t c, const void* const* hsend, void* 
         CF_CUDA(cudaEventCreateWithFlags(&hp.ar[k], cudaEventDisableTiming));
       }
     }
-  }
-  std::vector<const void*> din(c->local.size());
-  std::vector<void*> dout(c->local.size());
-  for (size_t li = 0; li < c->local.size(); li++) {
-    din[li] = c->local[li].stage_in;
-    dout[li] = c->local[li].stage_out;
   }
   // pipeline only the two-shot HB kernel (windows keep each element's owner)
   const bool pipelined = algo == CF_ALGO_2PA && bytes >= ((size_t)32 << 20);
@@ -972,10 +996,10 @@ extern "C" cfStatus cfAllReduceHost(cfComm_t c, const void* const* hsend, void* 
       CF_CUDA(cudaSetDevice(c->local[c->groups[gi][0]].dev));
       for (int li : c->groups[gi]) {
         if (pipelined)
-          CF_CUDA(copy_window(c->local[li].stage_in, (const char*)hsend[li], count, cs, n, w0, w1, es,
+          CF_CUDA(copy_window((char*)dsend[li], (const char*)hsend[li], count, cs, n, w0, w1, es,
                               cudaMemcpyHostToDevice, hp.h2d));
         else
-          CF_CUDA(cudaMemcpyAsync(c->local[li].stage_in, hsend[li], bytes, cudaMemcpyHostToDevice, hp.h2d));
+          CF_CUDA(cudaMemcpyAsync((void*)dsend[li], hsend[li], bytes, cudaMemcpyHostToDevice, hp.h2d));
       }
       CF_CUDA(cudaEventRecord(hp.in[p], hp.h2d));
     }
@@ -993,9 +1017,9 @@ extern "C" cfStatus cfAllReduceHost(cfComm_t c, const void* const* hsend, void* 
       j.win_lo = w0;
       j.win_hi = w1;
       j.work = ceil_div(w1 - w0, V) + 1;
-      CF_TRY(launch(c, j, dtype, din.data(), dout.data(), streams));
+      CF_TRY(launch(c, j, dtype, dsend, drecv, streams));
     } else {
-      CF_TRY(cfAllReduce(c, din.data(), dout.data(), count, dtype, algo, streams));
+      CF_TRY(cfAllReduce(c, dsend, drecv, count, dtype, algo, streams));
     }
     for (size_t gi = 0; gi < G; gi++) {
       CF_CUDA(cudaSetDevice(c->local[c->groups[gi][0]].dev));
@@ -1007,10 +1031,10 @@ extern "C" cfStatus cfAllReduceHost(cfComm_t c, const void* const* hsend, void* 
       for (size_t g2 = 0; g2 < G; g2++) CF_CUDA(cudaStreamWaitEvent(hp.d2h, c->pipes[g2].ar[p], 0));
       for (int li : c->groups[gi]) {
         if (pipelined)
-          CF_CUDA(copy_window((char*)hrecv[li], c->local[li].stage_out, count, cs, n, w0, w1, es,
+          CF_CUDA(copy_window((char*)hrecv[li], (const char*)drecv[li], count, cs, n, w0, w1, es,
                               cudaMemcpyDeviceToHost, hp.d2h));
         else
-          CF_CUDA(cudaMemcpyAsync(hrecv[li], c->local[li].stage_out, bytes, cudaMemcpyDeviceToHost, hp.d2h));
+          CF_CUDA(cudaMemcpyAsync(hrecv[li], drecv[li], bytes, cudaMemcpyDeviceToHost, hp.d2h));
       }
     }
   }

@@ -57,6 +57,11 @@ def _worker(rank, world, port, q):
             out[("rs", elems)] = rs_out.cpu().numpy().copy()
             for t in (send, recv, ag, rs_in):
                 comm.deregister(t)
+        # pipelined host-buffer AllReduce (windows: >= 32 MiB per rank, ragged)
+        he = (40 << 20) // 4 + 3
+        hx = torch.from_numpy(gen_inputs(world, he, "f32", "uniform", 9)[rank]).pin_memory()
+        out[("host",)] = comm.all_reduce_host(hx, algo="2pa").numpy().copy()
+        out[("host_small",)] = comm.all_reduce_host(hx[:1000].clone().pin_memory(), algo="2pa").numpy().copy()
         # K13 fused AllReduce + residual + RMSNorm, both algorithms
         fx = gen_inputs(world, 6 * 1024, "f32", "uniform", 5)
         x = torch.from_numpy(fx[rank]).cuda().view(6, 1024)
@@ -112,6 +117,12 @@ def test_two_processes_one_gpu_all_collectives():
         for r in range(world):
             assert np.array_equal(res[r][("ag", elems)], cat)
             assert np.array_equal(res[r][("rs", elems)].view(np.uint32), rs_want[r].view(np.uint32))
+    hins = gen_inputs(world, (40 << 20) // 4 + 3, "f32", "uniform", 9)
+    hwant = oracle.allreduce(hins, "2pa", "f32")
+    hsmall = oracle.allreduce([x[:1000] for x in hins], "2pa", "f32")
+    for r in range(world):
+        assert np.array_equal(res[r][("host",)].view(np.uint32), hwant[r].view(np.uint32))
+        assert np.array_equal(res[r][("host_small",)].view(np.uint32), hsmall[r].view(np.uint32))
     fx = gen_inputs(world, 6 * 1024, "f32", "uniform", 5)
     h = fx[0].astype(np.float32)
     for x in fx[1:]:
