@@ -219,21 +219,17 @@ __device__ __noinline__ void data_op_general(const DevOp& op, uint64_t lo, uint6
   const bool zero = op.flags & F_ZERO, round_each = op.flags & F_ROUND_EACH;
   const bool multi = op.code == D_MULTI;
   const uint32_t pkt = op.pkt_mask;
-  const char* src[kMaxSrc];
-  char* dst[kMaxDst];
-  uint32_t flag[kMaxSrc];
-  for (int k = 0; k < nsrc; k++) {
-    src[k] = ptr(op.src[k]);
-    flag[k] = (pkt >> k) & 1u ? runtime_flag(e, fstride, op.llflag_k[k]) : 0u;
-  }
-  for (int k = 0; k < ndst; k++) dst[k] = ptr(op.dst[k]);
+  // pointers and (runtime) packet flags are read from the staged op in shared
+  // memory at each use: no per-thread arrays (they would live in local memory)
+  auto src = [&](int k) -> const char* { return ptr(op.src[k]); };
+  auto dst = [&](int k) -> char* { return ptr(op.dst[k]); };
   if (op.flags & F_VEC) {
     for (uint64_t v = lo / V + threadIdx.x; v * V < hi; v += blockDim.x) {
       const int nval = (int)min((uint64_t)V, hi - v * V);
       const size_t boff = (size_t)v * 16;
       uint4 res;
       if (!multi) {
-        res = load_part<T>(src[0] + boff, nval);
+        res = load_part<T>(src(0) + boff, nval);
       } else {
         A acc[V];
         if (zero) {
@@ -244,35 +240,35 @@ __device__ __noinline__ void data_op_general(const DevOp& op, uint64_t lo, uint6
           uint4 r0[B], r1[B];
 #pragma unroll
           for (int i = 0; i < B; i++)
-            if (k0 + i < nsrc) issue_src<T>(src[k0 + i], v, nval, (pkt >> (k0 + i)) & 1u, r0[i], r1[i]);
+            if (k0 + i < nsrc) issue_src<T>(src(k0 + i), v, nval, (pkt >> (k0 + i)) & 1u, r0[i], r1[i]);
 #pragma unroll
           for (int i = 0; i < B; i++) {
             const int k = k0 + i;
             if (k >= nsrc) break;
-            const uint4 x = finish_src<T>(src[k], v, nval, (pkt >> k) & 1u, flag[k], r0[i], r1[i], rs);
+            const uint4 x = finish_src<T>(src(k), v, nval, (pkt >> k) & 1u, op.llflag_k[k], r0[i], r1[i], rs);
             if (k == 0 && !zero) Vec<T>::load(x, acc);
             else acc_vec<T>(acc, x, round_each);
           }
         }
         res = Vec<T>::store(acc);
       }
-      for (int d = 0; d < ndst; d++) store_part<T>(dst[d] + boff, res, nval);
+      for (int d = 0; d < ndst; d++) store_part<T>(dst(d) + boff, res, nval);
     }
   } else {
     for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
       const size_t boff = (size_t)i * sizeof(T);
       T res;
       if (!multi) {
-        res = *reinterpret_cast<const T*>(src[0] + boff);
+        res = *reinterpret_cast<const T*>(src(0) + boff);
       } else {
-        A acc = zero ? A(0) : to_acc<T>(*reinterpret_cast<const T*>(src[0] + boff));
+        A acc = zero ? A(0) : to_acc<T>(*reinterpret_cast<const T*>(src(0) + boff));
         for (int k = zero ? 0 : 1; k < nsrc; k++) {
-          acc = acc_add(acc, to_acc<T>(*reinterpret_cast<const T*>(src[k] + boff)));
+          acc = acc_add(acc, to_acc<T>(*reinterpret_cast<const T*>(src(k) + boff)));
           if (round_each) acc = Vec<T>::round(acc);
         }
         res = from_acc<T>(acc);
       }
-      for (int d = 0; d < ndst; d++) *reinterpret_cast<T*>(dst[d] + boff) = res;
+      for (int d = 0; d < ndst; d++) *reinterpret_cast<T*>(dst(d) + boff) = res;
     }
   }
 }
@@ -293,7 +289,7 @@ __device__ __noinline__ void packet_op(const DevOp& op, int K, int j, uint32_t f
   if (op.flags & F_LL16) {
     const uint64_t u0 = lo * sizeof(T) / 8, u1 = (hi * sizeof(T) + 7) / 8;
     if (put) {
-      const uint32_t flag = runtime_flag(e, fstride, op.llflag);
+      const uint32_t flag = op.llflag;
       const char* src = ptr(op.src[0]);
       for (uint64_t u = u0 + threadIdx.x; u < u1; u += blockDim.x) {
         const uint2 d = *reinterpret_cast<const uint2*>(src + u * 8);
@@ -308,7 +304,7 @@ __device__ __noinline__ void packet_op(const DevOp& op, int K, int j, uint32_t f
 #pragma unroll
         for (int k = 0; k < kMaxDst; k++) {
           if (k < nb) {
-            const uint32_t flag = runtime_flag(e, fstride, op.llflag_k[k]);
+            const uint32_t flag = op.llflag_k[k];
             uint2 d = make_uint2(raw[k].x, raw[k].z);
             if (raw[k].y != flag || raw[k].w != flag) d = ll16_get(ptr(op.src[k]) + u * 16, flag, rs);
             *reinterpret_cast<uint2*>(ptr(op.dst[k]) + u * 8) = d;
@@ -321,7 +317,7 @@ __device__ __noinline__ void packet_op(const DevOp& op, int K, int j, uint32_t f
     for (int k = 0; k < nb; k++) {
       const char* src = ptr(op.src[put ? 0 : k]);
       char* dst = ptr(op.dst[k]);
-      const uint32_t flag = runtime_flag(e, fstride, put ? op.llflag : op.llflag_k[k]);
+      const uint32_t flag = put ? op.llflag : op.llflag_k[k];
       for (uint64_t u = u0 + threadIdx.x; u < u1; u += blockDim.x) {
         if (put) {
           const uint32_t d = *reinterpret_cast<const uint32_t*>(src + u * 4);
@@ -401,12 +397,18 @@ __device__ __noinline__ void prologue(const PlanArgs& a, int rank) {
 
 // Rewrite the staged window's data-op references as absolute addresses (the io
 // buffers change per call, so this cannot all be done at load time).
-__device__ __forceinline__ void resolve_window(const PlanArgs& a, DevOp* ops, int nops) {
+__device__ __forceinline__ void resolve_window(const PlanArgs& a, DevOp* ops, int nops, uint64_t e) {
   constexpr int kSlots = kMaxSrc + kMaxDst;
   for (int t = threadIdx.x; t < nops * kSlots; t += blockDim.x) {
     DevOp& op = ops[t / kSlots];
     if (!is_data_code(op.code)) continue;
     const int k = t % kSlots;
+    // packet flags: plan flag -> this call's runtime flag (folds in the epoch)
+    const bool pkt_op = op.code == D_PUT_PACKETS || op.code == D_READ_PACKETS;
+    if (k == 0 && pkt_op) op.llflag = runtime_flag(e, a.flag_stride, op.llflag);
+    if (k < kMaxSrc && k < op.nsrc &&
+        ((op.code == D_READ_PACKETS) || (op.code == D_MULTI && ((op.pkt_mask >> k) & 1u))))
+      op.llflag_k[k] = runtime_flag(e, a.flag_stride, op.llflag_k[k]);
     if (k < kMaxSrc ? k >= op.nsrc : k - kMaxSrc >= op.ndst) continue;
     DRef& r = k < kMaxSrc ? op.src[k] : op.dst[k - kMaxSrc];
     if (r.buf == kAbsolute) continue;
@@ -445,7 +447,7 @@ __global__ void __launch_bounds__(512) plan_kernel(const __grid_constant__ PlanA
       for (int t = threadIdx.x; t < nvec; t += blockDim.x) s_raw[t] = src[t];
     }
     __syncthreads();
-    resolve_window(a, s_ops, w1 - w0);
+    resolve_window(a, s_ops, w1 - w0, e);
     __syncthreads();
   for (int i = w0; i < w1; i++) {
     const DevOp& op = s_ops[i - w0];
