@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(512) pull_reduce_kernel(const __grid_constant_
 // cf/collectives.py:156-161).  No semaphores, no fences: the flag travels in
 // the same 16-byte store as the data.
 template <typename T, int NR>
-__global__ void __launch_bounds__(512) ll_oneshot_kernel(const __grid_constant__ CollArgs a) {
+__global__ void __launch_bounds__(512, 2) ll_oneshot_kernel(const __grid_constant__ CollArgs a) {
   const RankCtx& rk = a.rk[blockIdx.y];
   constexpr int V = Vec<T>::N;
   const int n = a.n, r = rk.rank;
@@ -191,41 +191,48 @@ __global__ void __launch_bounds__(512) ll_oneshot_kernel(const __grid_constant__
     for (int p = 0; p < NR; p++) {
       if (p < n && p != r) {
         char* d = rk.scr[p] + par + (size_t)r * a.slot + v * 32;
-        ll16_put(d, make_uint2(x.x, x.y), flag);
-        ll16_put(d + 16, make_uint2(x.z, x.w), flag);
+        ll16_put_scoped(d, make_uint2(x.x, x.y), flag, a.gpu_scope);
+        ll16_put_scoped(d + 16, make_uint2(x.z, x.w), flag, a.gpu_scope);
       }
     }
   }
   (void)lead;
   using A = typename Vec<T>::Acc;
   for (size_t v = t0; v < nvec; v += stride) {
-    // issue every peer's two packets first (2(n-1) loads in flight), then
-    // accumulate in the 1pa order -- own input, then peers ascending -- and
-    // re-poll only the packets whose flags were not yet stamped
-    uint4 raw0[NR - 1], raw1[NR - 1];
-#pragma unroll
-    for (int i = 0; i < NR - 1; i++) {
-      if (i < n - 1) {
-        const int q = i + (i >= r ? 1 : 0);
-        const char* s = rk.scr[r] + par + (size_t)q * a.slot + v * 32;
-        raw0[i] = ld16_volatile(s);
-        raw1[i] = ld16_volatile(s + 16);
-      }
-    }
+    // peers in groups of G: issue the group's packets (2G loads in flight),
+    // then accumulate in the 1pa order -- own input, then peers ascending --
+    // re-polling only the packets whose flags were not yet stamped.  Groups
+    // keep the register footprint under the 2-CTAs/SM bound.
+    constexpr int G = 4;
     A acc[V];
     Vec<T>::load(load_vec<T>(rk.in[r], v, a.count), acc);
 #pragma unroll
-    for (int i = 0; i < NR - 1; i++) {
-      if (i < n - 1) {
-        const int q = i + (i >= r ? 1 : 0);
-        const char* s = rk.scr[r] + par + (size_t)q * a.slot + v * 32;
-        uint2 p0 = make_uint2(raw0[i].x, raw0[i].z), p1 = make_uint2(raw1[i].x, raw1[i].z);
-        if (raw0[i].y != flag || raw0[i].w != flag) p0 = ll16_get(s, flag, rk.st);
-        if (raw1[i].y != flag || raw1[i].w != flag) p1 = ll16_get(s + 16, flag, rk.st);
-        A t[V];
-        Vec<T>::load(make_uint4(p0.x, p0.y, p1.x, p1.y), t);
+    for (int g0 = 0; g0 < NR - 1; g0 += G) {
+      uint4 raw0[G], raw1[G];
 #pragma unroll
-        for (int j = 0; j < V; j++) acc[j] = acc_add(acc[j], t[j]);
+      for (int gi = 0; gi < G; gi++) {
+        const int i = g0 + gi;
+        if (i < NR - 1 && i < n - 1) {
+          const int q = i + (i >= r ? 1 : 0);
+          const char* s = rk.scr[r] + par + (size_t)q * a.slot + v * 32;
+          raw0[gi] = ld16_volatile(s);
+          raw1[gi] = ld16_volatile(s + 16);
+        }
+      }
+#pragma unroll
+      for (int gi = 0; gi < G; gi++) {
+        const int i = g0 + gi;
+        if (i < NR - 1 && i < n - 1) {
+          const int q = i + (i >= r ? 1 : 0);
+          const char* s = rk.scr[r] + par + (size_t)q * a.slot + v * 32;
+          uint2 p0 = make_uint2(raw0[gi].x, raw0[gi].z), p1 = make_uint2(raw1[gi].x, raw1[gi].z);
+          if (raw0[gi].y != flag || raw0[gi].w != flag) p0 = ll16_get(s, flag, rk.st);
+          if (raw1[gi].y != flag || raw1[gi].w != flag) p1 = ll16_get(s + 16, flag, rk.st);
+          A t[V];
+          Vec<T>::load(make_uint4(p0.x, p0.y, p1.x, p1.y), t);
+#pragma unroll
+          for (int j = 0; j < V; j++) acc[j] = acc_add(acc[j], t[j]);
+        }
       }
     }
     store_vec<T>(rk.out[r], v, Vec<T>::store(acc), 0, a.count, 0);
@@ -272,8 +279,8 @@ __global__ void __launch_bounds__(512) ll_twoshot_kernel(const __grid_constant__
     char* dst = rk.scr[p] + ph1 + (size_t)r * a.slot;
     for (size_t i = t0; i < nv; i += stride) {
       const uint4 x = load_vec<T>(rk.in[r], b + i, a.count);
-      ll16_put(dst + i * 32, make_uint2(x.x, x.y), flag);
-      ll16_put(dst + i * 32 + 16, make_uint2(x.z, x.w), flag);
+      ll16_put_scoped(dst + i * 32, make_uint2(x.x, x.y), flag, a.gpu_scope);
+      ll16_put_scoped(dst + i * 32 + 16, make_uint2(x.z, x.w), flag, a.gpu_scope);
     }
   }
   // reduce my chunk, store, broadcast as packets
@@ -308,8 +315,8 @@ __global__ void __launch_bounds__(512) ll_twoshot_kernel(const __grid_constant__
       for (int p = 0; p < NR; p++) {
         if (p < n && p != r) {
           char* d = rk.scr[p] + ph2 + (size_t)r * a.slot + i * 32;
-          ll16_put(d, make_uint2(res.x, res.y), flag);
-          ll16_put(d + 16, make_uint2(res.z, res.w), flag);
+          ll16_put_scoped(d, make_uint2(res.x, res.y), flag, a.gpu_scope);
+          ll16_put_scoped(d + 16, make_uint2(res.z, res.w), flag, a.gpu_scope);
         }
       }
     }

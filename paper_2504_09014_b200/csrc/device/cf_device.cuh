@@ -187,6 +187,13 @@ __device__ __forceinline__ bool wait_geq(const uint64_t* sem, uint64_t target, R
 __device__ __forceinline__ void ll16_put(void* dst, uint2 data, uint32_t flag) {
   st16_volatile(dst, make_uint4(data.x, flag, data.y, flag));
 }
+// LL16 put choosing the store by scope: ranks on one GPU meet in its L2, where
+// a plain 16-byte store is already one transaction; across GPUs the store is
+// volatile (not cached, not merged) like the reference's packet writes.
+__device__ __forceinline__ void ll16_put_scoped(void* dst, uint2 data, uint32_t flag, bool gpu) {
+  if (gpu) st16(dst, make_uint4(data.x, flag, data.y, flag));
+  else st16_volatile(dst, make_uint4(data.x, flag, data.y, flag));
+}
 // Poll one LL16 packet until both flag words equal `flag`.
 __device__ __forceinline__ uint2 ll16_get(const void* src, uint32_t flag, RankState* st) {
   uint4 v = ld16_volatile(src);
