@@ -223,6 +223,30 @@ def time_plan(rt, send, recv, iters, warmup, flush, reps=3):
     return t
 
 
+def run_ag_rs(w, flush, send, recv):
+    """C2-style AllGather (output bytes S_out) and ReduceScatter (input bytes S)
+    in bf16 on 8 co-resident ranks, every algorithm; busbw = algbw (n-1)/n."""
+    from paper_2504_09014_b200 import _lib
+    n = w.num_ranks
+    rows = []
+    for nb in (64 * KiB, MiB, 16 * MiB, 256 * MiB):
+        row = {"bytes": nb}
+        shard = nb // 2 // n
+        iters = 20 if nb <= 16 * MiB else 5
+        fl = flush if nb < 64 * MiB else None
+        for name in ("allpairs_ag", "ring_ag"):
+            t = time_coll(w, "allgather", [s[:shard] for s in send], [r[:shard * n] for r in recv], shard,
+                          "bf16", _lib.ALGOS[name], iters, 3, fl)
+            row["ag_" + name] = {"us": round(t * 1e6, 2), "busbw": round(nb / t / 1e9 * (n - 1) / n, 2)}
+        for name in ("rs_direct", "ring_rs"):
+            t = time_coll(w, "reducescatter", [s[:shard * n] for s in send], [r[:shard] for r in recv], shard,
+                          "bf16", _lib.ALGOS[name], iters, 3, fl)
+            row["rs_" + name] = {"us": round(t * 1e6, 2), "busbw": round(nb / t / 1e9 * (n - 1) / n, 2)}
+        rows.append(row)
+    return {"config": "C2/RS: AllGather (S = output bytes) and ReduceScatter (S = input bytes), bf16, "
+                      "8 co-resident ranks", "rows": rows}
+
+
 def run_fused(w, flush):
     """K13 vs the unfused composition (AllReduce, then one batched residual add
     and one batched RMSNorm over all ranks' rows) at the C5 shapes."""
@@ -420,6 +444,7 @@ def run_sweep(w, args):
     out.append({"config": "C5 Llama-70B TP decode AllReduce via DSL plans (K10), bf16, "
                           "8 co-resident ranks", "rows": c5})
     out.append(run_fused(w, flush))
+    out.append(run_ag_rs(w, flush, send, recv))
     # C1: fp32 1 MiB one-shot LL (8 simulated ranks)
     c1 = [torch.randn(MiB // 4, device=dev) for _ in range(n)]
     c1o = [torch.empty_like(x) for x in c1]
