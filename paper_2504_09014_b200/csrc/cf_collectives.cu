@@ -520,6 +520,37 @@ __device__ __forceinline__ RingLink make_link(const CollArgs& a, const RankCtx& 
   return L;
 }
 
+// V accumulator values (f32 / i32) <-> NQ 16-byte words of a ring slot.
+template <typename T>
+struct AccVec {
+  using A = typename Vec<T>::Acc;
+  static constexpr int V = Vec<T>::N;
+  static constexpr int NQ = V * (int)sizeof(A) / 16;
+  __device__ static void load(const void* p, A* a) {
+#pragma unroll
+    for (int q = 0; q < NQ; q++) {
+      const uint4 w = ld16(reinterpret_cast<const char*>(p) + q * 16);
+      const uint32_t u[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+      for (int k = 0; k < 4; k++) a[q * 4 + k] = bits_to<A>(u[k]);
+    }
+  }
+  __device__ static void store(void* p, const A* a) {
+#pragma unroll
+    for (int q = 0; q < NQ; q++)
+      st16(reinterpret_cast<char*>(p) + q * 16,
+           make_uint4(to_bits(a[q * 4]), to_bits(a[q * 4 + 1]), to_bits(a[q * 4 + 2]), to_bits(a[q * 4 + 3])));
+  }
+  template <typename X> __device__ static X bits_to(uint32_t u);
+  __device__ static uint32_t to_bits(float x) { return __float_as_uint(x); }
+  __device__ static uint32_t to_bits(int32_t x) { return (uint32_t)x; }
+};
+template <typename T> template <typename X>
+__device__ X AccVec<T>::bits_to(uint32_t u) {
+  if constexpr (sizeof(X) == 4 && X(0.5f) != X(0)) return __uint_as_float(u);
+  else return (X)u;
+}
+
 // Ring ReduceScatter (build_ring_rs, cf/collectives.py:30-79) and, with
 // `push`, the two-phase ring AllReduce (build_2pr, :107-136).  Step s sends
 // the partial of chunk (r - s) mod n to the next rank; the partial that
@@ -556,6 +587,9 @@ __global__ void __launch_bounds__(512) ring_kernel(const __grid_constant__ CollA
     kt = max(kt, (s1 - s0 + UT - 1) / UT);
   }
   const size_t shift = a.rs_shift ? min((size_t)r * a.cs, a.count) : 0;
+  // every chunk starts on the 16-byte grid: whole-vector loops (chunk ends,
+  // CTA slices and units are then multiples of V as well)
+  const bool vec = a.cs % V == 0 && a.count % V == 0 && (((uintptr_t)x | (uintptr_t)y) & 15) == 0;
   for (size_t k = 0; k < ka; k++) {
     // ReduceScatter: step s adds the own contribution to chunk (r - s)
     for (int s = 0; s < n; s++) {
@@ -568,10 +602,24 @@ __global__ void __launch_bounds__(512) ring_kernel(const __grid_constant__ CollA
       L.send_wait();
       const A* in_slot = reinterpret_cast<const A*>(L.recv_slot());
       A* out_slot = reinterpret_cast<A*>(L.send_slot());
-      for (size_t i = u0 + threadIdx.x; i < u1; i += blockDim.x) {
-        A v = to_acc<T>(x[i]);
-        if (s > 0) v = acc_add(in_slot[i - u0], v);
-        out_slot[i - u0] = v;
+      if (vec) {   // whole 16-byte vectors of T; the slots carry V accumulators per vector
+        for (size_t i = u0 + threadIdx.x * V; i < u1; i += (size_t)blockDim.x * V) {
+          A v[V];
+          Vec<T>::load(ld16(x + i), v);
+          if (s > 0) {
+            A p[V];
+            AccVec<T>::load(in_slot + (i - u0), p);
+#pragma unroll
+            for (int j = 0; j < (int)V; j++) v[j] = acc_add(p[j], v[j]);
+          }
+          AccVec<T>::store(out_slot + (i - u0), v);
+        }
+      } else {
+        for (size_t i = u0 + threadIdx.x; i < u1; i += blockDim.x) {
+          A v = to_acc<T>(x[i]);
+          if (s > 0) v = acc_add(in_slot[i - u0], v);
+          out_slot[i - u0] = v;
+        }
       }
       if (s > 0) L.recv_done();
       L.send_done();
@@ -584,8 +632,18 @@ __global__ void __launch_bounds__(512) ring_kernel(const __grid_constant__ CollA
       const size_t u1 = min(u0 + UA, s1);
       L.recv_wait();
       const A* in_slot = reinterpret_cast<const A*>(L.recv_slot());
-      for (size_t i = u0 + threadIdx.x; i < u1; i += blockDim.x)
-        y[i - shift] = from_acc<T>(acc_add(A(0), in_slot[i - u0]));
+      if (vec) {
+        for (size_t i = u0 + threadIdx.x * V; i < u1; i += (size_t)blockDim.x * V) {
+          A p[V];
+          AccVec<T>::load(in_slot + (i - u0), p);
+#pragma unroll
+          for (int j = 0; j < (int)V; j++) p[j] = acc_add(A(0), p[j]);
+          st16(y + (i - shift), Vec<T>::store(p));
+        }
+      } else {
+        for (size_t i = u0 + threadIdx.x; i < u1; i += blockDim.x)
+          y[i - shift] = from_acc<T>(acc_add(A(0), in_slot[i - u0]));
+      }
       L.recv_done();
     }
   }
@@ -603,14 +661,24 @@ __global__ void __launch_bounds__(512) ring_kernel(const __grid_constant__ CollA
           const size_t u1 = min(us0 + UT, a1);
           L.send_wait();
           T* out_slot = reinterpret_cast<T*>(L.send_slot());
-          for (size_t i = us0 + threadIdx.x; i < u1; i += blockDim.x) out_slot[i - us0] = y[i];
+          if (vec) {
+            for (size_t i = us0 + threadIdx.x * V; i < u1; i += (size_t)blockDim.x * V)
+              st16(out_slot + (i - us0), ld16(y + i));
+          } else {
+            for (size_t i = us0 + threadIdx.x; i < u1; i += blockDim.x) out_slot[i - us0] = y[i];
+          }
           L.send_done();
         }
         if (ur0 < b1) {
           const size_t u1 = min(ur0 + UT, b1);
           L.recv_wait();
           const T* in_slot = reinterpret_cast<const T*>(L.recv_slot());
-          for (size_t i = ur0 + threadIdx.x; i < u1; i += blockDim.x) y[i] = in_slot[i - ur0];
+          if (vec) {
+            for (size_t i = ur0 + threadIdx.x * V; i < u1; i += (size_t)blockDim.x * V)
+              st16(y + i, ld16(in_slot + (i - ur0)));
+          } else {
+            for (size_t i = ur0 + threadIdx.x; i < u1; i += blockDim.x) y[i] = in_slot[i - ur0];
+          }
           L.recv_done();
         }
       }
@@ -639,11 +707,19 @@ __global__ void __launch_bounds__(512) ring_gather_kernel(const __grid_constant_
   const size_t cnt = a.count;
   size_t s0, s1;
   cta_slice(0, cnt, b, B, V, s0, s1);
-  for (size_t i = s0 + threadIdx.x; i < s1; i += blockDim.x) y[(size_t)r * cnt + i] = x[i];
+  const bool vec = cnt % V == 0 && (((uintptr_t)x | (uintptr_t)y | (uintptr_t)yn) & 15) == 0;
+  auto copy = [&](T* d, const T* src) {   // this CTA's slice [s0, s1)
+    if (vec) {
+      for (size_t i = s0 + threadIdx.x * V; i < s1; i += (size_t)blockDim.x * V) st16(d + i, ld16(src + i));
+    } else {
+      for (size_t i = s0 + threadIdx.x; i < s1; i += blockDim.x) d[i] = src[i];
+    }
+  };
+  copy(y + (size_t)r * cnt, x);
   for (int t = 0; t < n - 1; t++) {
     const size_t off = (size_t)((r - t + n) % n) * cnt;
     __syncthreads();
-    for (size_t i = s0 + threadIdx.x; i < s1; i += blockDim.x) yn[off + i] = y[off + i];
+    copy(yn + off, y + off);
     L.send_done();
     L.recv_wait();   // shard (r - 1 - t) landed in my output
     L.qr++;
