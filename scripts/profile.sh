@@ -4,18 +4,23 @@ cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
 NCU=/usr/local/cuda/bin/ncu
 P="python scripts/profile_kernels.py"
-# launch list of the headline bench configuration (cold-cache, serialised)
-timeout 600 $NCU --metrics gpu__time_duration.sum --clock-control none --csv \
-  --log-file gpurun_out/launches_headline.csv $P --algo 2pa --bytes 268435456 --dtype bf16 --iters 5 > /dev/null 2>&1
+G=tests/golden/plans
+# launch list of the bench command itself (cold-cache, serialised; no sweep)
+timeout 900 $NCU --metrics gpu__time_duration.sum --clock-control none --csv -c 400 \
+  --log-file gpurun_out/launches_headline.csv python bench.py --steps 2 --warmup 3 --no-sweep > /dev/null 2>&1
 echo "launch list rc=$?"
-# full sets: headline two-shot, C1 one-shot LL, 1 MiB two-shot, C5 plan
-timeout 900 $NCU --set full --clock-control none --import-source on -k regex:pull_reduce -s 2 -c 1 \
-  -o gpurun_out/prof_2pa_256m -f $P --algo 2pa --bytes 268435456 --dtype bf16 --iters 3 > gpurun_out/ncu_2pa.log 2>&1
-echo "2pa rc=$?"
-timeout 900 $NCU --set full --clock-control none --import-source on -k regex:ll_oneshot -s 2 -c 1 \
-  -o gpurun_out/prof_1pa_c1 -f $P --algo 1pa --bytes 1048576 --dtype f32 --iters 3 > gpurun_out/ncu_1pa.log 2>&1
-echo "1pa rc=$?"
-timeout 900 $NCU --set full --clock-control none --import-source on -k regex:pull_reduce -s 2 -c 1 \
-  -o gpurun_out/prof_2pa_1m -f $P --algo 2pa --bytes 1048576 --dtype bf16 --iters 3 > gpurun_out/ncu_2pa1m.log 2>&1
-echo "2pa1m rc=$?"
-ls -la gpurun_out/
+full() {   # name kernel-regex args...
+  local name=$1 k=$2; shift 2
+  timeout 900 $NCU --set full --clock-control none --import-source on -k regex:$k -s 2 -c 1 \
+    -o gpurun_out/prof_$name -f "$@" > gpurun_out/ncu_$name.log 2>&1
+  echo "$name rc=$?"
+}
+full 2pa_256m pull_reduce $P --algo 2pa --bytes 268435456 --dtype bf16 --iters 3
+full 2pa_1m pull_reduce $P --algo 2pa --bytes 1048576 --dtype bf16 --iters 3
+full 1pa_c1 ll_oneshot $P --algo 1pa --bytes 1048576 --dtype f32 --iters 3
+full 2pr_64m ring_kernel $P --algo 2pr --bytes 67108864 --dtype bf16 --iters 3
+full ag_256m push_gather $P --kind allgather --algo allpairs_ag --bytes 268435456 --dtype bf16 --iters 3
+full fused_b256 ar_rmsnorm $P --kind fused --algo 2pa --bytes 4194304 --dtype bf16 --iters 3
+full plan2pa_b1 plan_kernel $P --plan $G/2pa_memory_n8_e64.json --scale 128 --dtype bf16
+full plan1pa_b64 plan_kernel $P --plan $G/1pa_n8_e64.json --scale 8192 --dtype bf16
+ls -la gpurun_out/*.ncu-rep

@@ -42,6 +42,18 @@ def main():
         recv = [torch.empty(rt.out_elems, device=dev, dtype=tdt) for _ in range(n)]
         for _ in range(args.iters):
             rt.run_raw(send, recv)
+    elif args.kind == "fused":
+        # K13: AllReduce + residual + RMSNorm on [rows, 8192]
+        from paper_2504_09014_b200 import allreduce_add_rmsnorm
+        hidden = 8192
+        rows = max(1, args.bytes // (hidden * ELEM_SIZE[args.dtype]))
+        xs = [torch.randn(rows, hidden, device=dev).to(tdt) for _ in range(n)]
+        rs = [torch.randn(rows, hidden, device=dev).to(tdt) for _ in range(n)]
+        ys = [torch.empty_like(x) for x in xs]
+        wt = torch.ones(hidden, device=dev, dtype=tdt)
+        algo = None if args.algo == "auto" else args.algo
+        for _ in range(args.iters):
+            allreduce_add_rmsnorm(w, xs, rs, wt, algo=algo, norm_out=ys)
     else:
         if args.kind == "allgather":
             send = [torch.randn(count // n, device=dev).to(tdt) for _ in range(n)]
