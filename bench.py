@@ -445,6 +445,19 @@ def run_sweep(w, args):
                           "8 co-resident ranks", "rows": c5})
     out.append(run_fused(w, flush))
     out.append(run_ag_rs(w, flush, send, recv))
+    # C3: fp16 small-message AllReduce, LL one-shot vs the selector's pick
+    c3 = []
+    for nb in (KiB, 4 * KiB, 16 * KiB, 64 * KiB, 256 * KiB, MiB):
+        cnt = nb // 2
+        xs = [s_[:cnt].view(torch.float16) for s_ in send]
+        ys = [r_[:cnt].view(torch.float16) for r_ in recv]
+        row = {"bytes": nb}
+        for name in ("1pa", "auto"):
+            t = time_coll(w, "allreduce", xs, ys, cnt, "f16", _lib.ALGOS[name], 20, 3, flush)
+            row[name] = {"us": round(t * 1e6, 2), "busbw": round(busbw(nb, t, n), 2)}
+        c3.append(row)
+    out.append({"config": "C3 AllReduce fp16 1 KiB-1 MiB, LL one-shot (1pa) and the selector's pick, "
+                          "8 co-resident ranks", "rows": c3})
     # C1: fp32 1 MiB one-shot LL (8 simulated ranks)
     c1 = [torch.randn(MiB // 4, device=dev) for _ in range(n)]
     c1o = [torch.empty_like(x) for x in c1]
@@ -452,6 +465,52 @@ def run_sweep(w, args):
     out.append({"config": "C1 AllReduce fp32 1 MiB one-shot LL, 8 co-resident ranks",
                 "us": round(t * 1e6, 2), "busbw": round(busbw(MiB, t, n), 2)})
     return out
+
+
+def multi_sweep(comm, dev, world, send, recv):
+    """N>1: AllReduce latency / busbw over sizes -- libcf (CUDA graph and
+    eager) next to NCCL (eager, through torch.distributed; the comparison
+    baseline of BASELINE.md, never part of the product path).  Per-rank times;
+    the caller takes the max over ranks."""
+    import torch
+    import torch.distributed as dist
+    nccl = None
+    try:
+        nccl = dist.new_group(backend="nccl")
+        probe = torch.ones(16, device=dev)
+        dist.all_reduce(probe, group=nccl)
+        torch.cuda.synchronize(dev)
+    except Exception as e:   # comparison only: report, never fail the bench
+        nccl = None
+        nccl_err = f"{type(e).__name__}: {e}"[:200]
+    rows = []
+    for nb in (KiB, 16 * KiB, 256 * KiB, MiB, 16 * MiB, 256 * MiB):
+        cnt = nb // 2
+        x, y = send[:cnt], recv[:cnt]
+        iters = 50 if nb <= MiB else 10
+        t_graph = time_graph(dev, lambda: comm.all_reduce(x, y, algo="auto"), iters, 3)
+        st = torch.cuda.current_stream(dev)
+
+        def eager(fn):
+            for _ in range(3):
+                fn()
+            torch.cuda.synchronize(dev)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            for _ in range(iters):
+                fn()
+            e1.record(st)
+            e1.synchronize()
+            return e0.elapsed_time(e1) / 1e3 / iters
+
+        t_eager = eager(lambda: comm.all_reduce(x, y, algo="auto"))
+        row = {"bytes": nb, "cf_graph_s": t_graph, "cf_eager_s": t_eager}
+        if nccl is not None:
+            z = y.clone()
+            row["nccl_eager_s"] = eager(lambda: dist.all_reduce(z, group=nccl))
+        rows.append(row)
+    comm.check_device_error()
+    return rows, (None if nccl is not None else nccl_err)
 
 
 def run_multi_gpu(args):
@@ -504,10 +563,20 @@ def run_multi_gpu(args):
         torch.cuda.synchronize(dev)
         if it:
             e2e_local.append(time.perf_counter() - t0)
+    rows_local, nccl_err = multi_sweep(comm, dev, world, send, recv)
     times = [None] * world
-    dist.all_gather_object(times, (t_local, float(np.mean(e2e_local))))
+    dist.all_gather_object(times, (t_local, float(np.mean(e2e_local)), rows_local))
     t = max(x[0] for x in times)
     te = max(x[1] for x in times)
+    sweep = []
+    for i, row in enumerate(rows_local):
+        nb = row["bytes"]
+        out = {"bytes": nb}
+        for key in ("cf_graph_s", "cf_eager_s", "nccl_eager_s"):
+            if key in row:
+                tk = max(x[2][i][key] for x in times)   # max over ranks
+                out[key[:-2]] = {"us": round(tk * 1e6, 2), "busbw": round(busbw(nb, tk, world), 2)}
+        sweep.append(out)
     if rank == 0:
         value = busbw(HEAD_BYTES, t, world)
         print(json.dumps({
@@ -527,7 +596,10 @@ def run_multi_gpu(args):
                     "h2d_bytes_per_step": HEAD_BYTES, "d2h_bytes_per_step": HEAD_BYTES,
                     "ms_per_step": round(te * 1e3, 3),
                     "api": "Communicator.all_reduce_host (cfAllReduceHostStaged), pinned host tensors"},
-            "gpu_launches": args.steps, "clocks": clk.summary()}))
+            "gpu_launches": args.steps, "clocks": clk.summary(),
+            "sweep": {"config": "AllReduce bf16, libcf (auto) in a CUDA graph and eager vs NCCL eager "
+                                "(torch.distributed, comparison only); latency = max over ranks",
+                      "nccl_error": nccl_err, "rows": sweep}}))
     comm.close()
     dist.destroy_process_group()
     return 0
