@@ -242,6 +242,15 @@ CF_API cfStatus cfPlanInfo(cfPlan_t plan, size_t* in_elems, size_t* out_elems, i
                            int* n_device_ops);
 /* Device spin-timeout word of the plan's ranks (0 or CF_E_DEADLOCK).  Synchronizes. */
 CF_API cfStatus cfPlanLastDeviceError(cfPlan_t plan, int* code);
+/* One process per GPU: every rank loads the same plan with cfPlanLoad, exports
+ * its plan heap (semaphore lanes, barrier counters, scratch buffers) with
+ * cfPlanGetHandle, all-gathers the handles through the caller's bootstrap and
+ * connects with all nranks handles (rank order); then cfPlanExecute runs this
+ * rank's programs (inputs/outputs: one entry; plans that touch the peers'
+ * input/output need those buffers registered, CF_E_TOPOLOGY otherwise). */
+#define CF_PLAN_HANDLE_BYTES 128
+CF_API cfStatus cfPlanGetHandle(cfPlan_t plan, void* handle, size_t* bytes);
+CF_API cfStatus cfPlanConnect(cfPlan_t plan, const void* handles, size_t bytes_per_handle);
 CF_API cfStatus cfPlanDestroy(cfPlan_t plan);
 
 #ifdef __cplusplus

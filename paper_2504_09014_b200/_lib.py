@@ -24,6 +24,7 @@ ALGOS = {
     "allpairs_ag": 6, "ring_ag": 7, "ring_rs": 8, "rs_direct": 9,
 }
 ALGO_NAMES = {v: k for k, v in ALGOS.items()}
+CF_PLAN_HANDLE_BYTES = 128
 
 # every symbol include/cf.h declares (tests check the .so exports all of them)
 EXPORTS = (
@@ -35,7 +36,7 @@ EXPORTS = (
     "cfCommMulticastSupported", "cfCommLastDeviceError", "cfCommClearDeviceError", "cfAllReduce",
     "cfAllGather", "cfReduceScatter", "cfAllReduceHost", "cfAllReduceHostStaged",
     "cfAllReduceAddRMSNorm", "cfSelectAlgorithm", "cfPlanLoad", "cfPlanExecute",
-    "cfPlanInfo", "cfPlanLastDeviceError", "cfPlanDestroy",
+    "cfPlanInfo", "cfPlanLastDeviceError", "cfPlanGetHandle", "cfPlanConnect", "cfPlanDestroy",
 )
 
 
@@ -87,6 +88,8 @@ _PROTOS = {
     "cfPlanExecute": ([vp, P(vp), P(vp), P(vp)], i32),
     "cfPlanLastDeviceError": ([vp, P(i32)], i32),
     "cfPlanInfo": ([vp, P(sz), P(sz), P(i32), P(i32), P(i32)], i32),
+    "cfPlanGetHandle": ([vp, vp, P(sz)], i32),
+    "cfPlanConnect": ([vp, vp, sz], i32),
     "cfPlanDestroy": ([vp], i32),
 }
 

@@ -160,6 +160,12 @@ class Communicator:
             CODES[from_torch(send.dtype)], aid, P([s.cuda_stream])))
         return norm_out, resid_out
 
+    def load_plan(self, plan, dtype: str | None = None) -> "RankRuntime":
+        """Collective: load an execution plan on this rank (K10, one process per
+        GPU) -- every rank loads the same plan, the plan heaps are exchanged
+        through the bootstrap.  See ``RankRuntime``."""
+        return RankRuntime(self, plan, dtype)
+
     def setup_nvls(self) -> bool:
         """Collective: build the NVLS multicast object (SwitchChannel).  Rank 0
         creates it and passes its POSIX fd to the other ranks over a Unix
@@ -222,6 +228,64 @@ class Communicator:
         if self._comm is not None:
             _lib.lib().cfCommDestroy(self._comm)
             self._comm = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class RankRuntime:
+    """This rank's share of a plan in the one-process-per-GPU mode (the
+    multi-process counterpart of ``executor.Runtime``, ``cf/executor.py:73-178``).
+    ``run(send, recv)`` enqueues one execution of this rank's programs on the
+    stream; every rank must call it in the same order.  Plans that read or
+    write the peers' input / output need those tensors registered
+    (``Communicator.register``) before the first run."""
+
+    def __init__(self, comm: Communicator, plan, dtype: str | None = None):
+        from .plan import ExecutionPlan, serialize_plan
+        self.comm = comm
+        doc = serialize_plan(plan) if isinstance(plan, ExecutionPlan) else \
+            (plan.encode() if isinstance(plan, str) else bytes(plan))
+        L = _lib.lib()
+        h = ctypes.c_void_p()
+        _lib.check(L.cfPlanLoad(comm.comm, doc, len(doc), CODES[dtype] if dtype else -1, ctypes.byref(h)))
+        self._plan = h
+        blob = ctypes.create_string_buffer(_lib.CF_PLAN_HANDLE_BYTES)
+        nbytes = ctypes.c_size_t(_lib.CF_PLAN_HANDLE_BYTES)
+        _lib.check(L.cfPlanGetHandle(h, blob, ctypes.byref(nbytes)))
+        allh = b"".join(all_gather_bytes(blob.raw, comm.group))
+        _lib.check(L.cfPlanConnect(h, allh, _lib.CF_PLAN_HANDLE_BYTES))
+        in_e, out_e = ctypes.c_size_t(), ctypes.c_size_t()
+        dt, nprog, nops = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        _lib.check(L.cfPlanInfo(h, ctypes.byref(in_e), ctypes.byref(out_e), ctypes.byref(dt),
+                                ctypes.byref(nprog), ctypes.byref(nops)))
+        self.in_elems, self.out_elems = in_e.value, out_e.value
+        self.n_device_ops = nops.value
+
+    def run(self, send, recv, stream=None):
+        import torch
+        if send.numel() != self.in_elems or recv.numel() != self.out_elems:
+            raise ShapeError(f"plan wants {self.in_elems} input / {self.out_elems} output elements")
+        s = stream if stream is not None else torch.cuda.current_stream(self.comm.device)
+        P = _lib.ptr_array
+        _lib.check(_lib.lib().cfPlanExecute(self._plan, P([send.data_ptr()]), P([recv.data_ptr()]),
+                                            P([s.cuda_stream])))
+        return recv
+
+    def check_device_error(self):
+        from .errors import DeadlockError
+        code = ctypes.c_int()
+        _lib.check(_lib.lib().cfPlanLastDeviceError(self._plan, ctypes.byref(code)))
+        if code.value:
+            raise DeadlockError(message="plan execution timed out on the device")
+
+    def close(self):
+        if getattr(self, "_plan", None) is not None:
+            _lib.lib().cfPlanDestroy(self._plan)
+            self._plan = None
 
     def __del__(self):
         try:

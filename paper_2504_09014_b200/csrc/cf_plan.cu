@@ -59,6 +59,7 @@ struct Group {
   int32_t* d_zero = nullptr;
   uint64_t* d_done = nullptr;  // proxy completion counters [nprog * K]
   int nops = 0;
+  std::vector<int32_t> beg, end;  // host copy of the op ranges (parameter-space table)
 };
 
 }  // namespace
@@ -83,6 +84,13 @@ struct cfPlan {
   int n_device_ops = 0;
   bool uses_port = false;             // port-channel ops go through the proxy
   bool has_prologue = false;          // per-call zeroing / private input copy
+  // one-process-per-GPU: this process runs rank `me`'s programs; the peers'
+  // plan heaps are IPC-mapped by cfPlanConnect, which finalizes the plan
+  bool mp = false;
+  int me = 0;
+  bool ready = false;
+  std::vector<bool> heap_mapped;      // heap[r] is an IPC mapping (close, not free)
+  bool peer_in = false, peer_out = false;  // data ops touch another rank's I/O buffer
 };
 
 namespace cf {
@@ -561,6 +569,8 @@ void fuse_packet_reads(cfPlan* pl) {
 
 // ------------------------------------------------------------------ load
 
+cfStatus finalize(cfPlan* pl);
+
 cfStatus load(cfComm* c, const char* json, size_t len, int dtype_override, cfPlan** out) {
   std::unique_ptr<cfPlan> pl(new cfPlan());
   pl->comm = c;
@@ -571,7 +581,6 @@ cfStatus load(cfComm* c, const char* json, size_t len, int dtype_override, cfPla
     if (P.nranks != c->nranks)
       bad(CF_E_RANK_MISMATCH, "plan wants " + std::to_string(P.nranks) + " ranks, world has " +
                                   std::to_string(c->nranks));
-    if (c->multiprocess) bad(CF_E_TOPOLOGY, "plan execution needs a one-process world in this build");
     if ((int)P.bufs.size() > kMaxBufs) bad(CF_E_SHAPE, "plans are limited to 16 buffers");
     for (size_t b = 0; b < P.bufs.size(); b++) {
       if (P.bufs[b].elems <= 0) bad(CF_E_BAD_SIZE, "buffer '" + P.bufs[b].id + "' has non-positive elems");
@@ -631,9 +640,20 @@ cfStatus load(cfComm* c, const char* json, size_t len, int dtype_override, cfPla
       if (is_data(o)) max_bytes = std::max(max_bytes, o.size * es);
   const void* kernel = plan_kernel_for(pl->dtype);
   int cap = INT32_MAX, progs_per_dev_max = 1;
+  pl->mp = c->multiprocess;
+  pl->me = c->local[0].rank;
   {
+    // programs co-resident per device; one process per GPU: every rank
+    // computes the same K from the busiest rank (lanes are indexed by K)
     std::map<int, int> per_dev;
-    for (int r : prank) per_dev[c->local[r].dev]++;
+    if (pl->mp) {
+      std::map<int, int> per_rank;
+      int busiest = 0;
+      for (int r : prank) busiest = std::max(busiest, ++per_rank[r]);
+      per_dev[c->local[0].dev] = busiest;
+    } else {
+      for (int r : prank) per_dev[c->local[r].dev]++;
+    }
     for (auto& kv : per_dev) {
       progs_per_dev_max = std::max(progs_per_dev_max, kv.second);
       int nb = 0;
@@ -927,8 +947,11 @@ cfStatus load(cfComm* c, const char* json, size_t len, int dtype_override, cfPla
   int prev_dev = -1;
   cudaGetDevice(&prev_dev);
   pl->heap.assign(n, nullptr);
+  pl->heap_mapped.assign(n, false);
   for (int r = 0; r < n; r++) {
-    if (cudaSetDevice(c->local[r].dev) != cudaSuccess || cudaMalloc((void**)&pl->heap[r], pl->heap_bytes) != cudaSuccess ||
+    if (pl->mp && r != pl->me) continue;   // peers' heaps arrive through cfPlanConnect
+    if (cudaSetDevice(c->local[pl->mp ? 0 : r].dev) != cudaSuccess ||
+        cudaMalloc((void**)&pl->heap[r], pl->heap_bytes) != cudaSuccess ||
         cudaMemset(pl->heap[r], 0, pl->heap_bytes) != cudaSuccess) {
       cudaSetDevice(prev_dev);
       cfPlanDestroy(pl.release());
@@ -939,15 +962,40 @@ cfStatus load(cfComm* c, const char* json, size_t len, int dtype_override, cfPla
     st.base.timeout_ns = c->cfg.spin_timeout_ns;
     cudaMemcpy(pl->heap[r] + pl->state_off, &st, sizeof(st), cudaMemcpyHostToDevice);
   }
+  pl->has_prologue = pl->input_private;
+  for (auto& z : pl->zero_bufs) pl->has_prologue |= !z.empty();
+  cudaSetDevice(prev_dev);
+  if (pl->mp) {   // finalized by cfPlanConnect once every heap is mapped
+    *out = pl.release();
+    return CF_OK;
+  }
+  const cfStatus fs = finalize(pl.get());
+  if (fs != CF_OK) {
+    cfPlanDestroy(pl.release());
+    return fs;
+  }
+  *out = pl.release();
+  return CF_OK;
+}
+
+// Bake plan-owned buffer addresses into the device ops, fuse packet reads,
+// upload the per-device tables, start the proxy (port channels).
+cfStatus finalize(cfPlan* pl) {
+  cfComm* c = pl->comm;
+  Plan& P = pl->ir;
+  const int n = P.nranks, K = pl->K;
+  int prev_dev = -1;
+  cudaGetDevice(&prev_dev);
   // plan-owned buffers live at fixed addresses: bake them into the data ops so
   // the interpreter resolves them without a table load
-  for (auto& prog : pl->prog_ops)
-    for (auto& d : prog) {
+  for (size_t p = 0; p < pl->prog_ops.size(); p++)
+    for (auto& d : pl->prog_ops[p]) {
       if (d.code != D_MULTI && d.code != D_COPY && d.code != D_PUT_PACKETS && d.code != D_READ_PACKETS &&
           d.code != D_PORT_PUT)
         continue;
       auto bake = [&](DRef& r) {
         const bool io = r.buf == pl->out_buf || (r.buf == pl->in_buf && !pl->input_private);
+        if (io && r.rank != pl->prog_rank[p]) (r.buf == pl->out_buf ? pl->peer_out : pl->peer_in) = true;
         if (io || r.buf == kAbsolute) return;
         r.off = (uint64_t)(pl->heap[r.rank] + pl->buf_off[r.buf]) + r.off;
         r.buf = kAbsolute;
@@ -955,15 +1003,14 @@ cfStatus load(cfComm* c, const char* json, size_t len, int dtype_override, cfPla
       for (int k = 0; k < d.nsrc; k++) bake(d.src[k]);
       for (int k = 0; k < d.ndst; k++) bake(d.dst[k]);
     }
-  fuse_packet_reads(pl.get());
-  pl->has_prologue = pl->input_private;
-  for (auto& z : pl->zero_bufs) pl->has_prologue |= !z.empty();
+  fuse_packet_reads(pl);
   // device tables per device group
   for (size_t gi = 0; gi < c->groups.size(); gi++) {
     Group G;
     G.dev = c->local[c->groups[gi][0]].dev;
     std::set<int> ranks;
     for (int li : c->groups[gi]) ranks.insert(c->local[li].rank);
+    const auto& prank = pl->prog_rank;
     std::vector<DevOp> all;
     std::vector<int32_t> meta;
     std::vector<int32_t> beg, end, rk;
@@ -975,6 +1022,8 @@ cfStatus load(cfComm* c, const char* json, size_t len, int dtype_override, cfPla
       end.push_back((int32_t)all.size());
       rk.push_back(prank[p]);
     }
+    G.beg = beg;
+    G.end = end;
     meta = beg;
     meta.insert(meta.end(), end.begin(), end.end());
     meta.insert(meta.end(), rk.begin(), rk.end());
@@ -999,15 +1048,11 @@ cfStatus load(cfComm* c, const char* json, size_t len, int dtype_override, cfPla
     pl->groups.push_back(G);
     if (!ok) {
       cudaSetDevice(prev_dev);
-      cfPlanDestroy(pl.release());
       return fail(CF_E_CUDA, "plan table upload failed");
     }
   }
   cudaSetDevice(prev_dev);
-  if (pl->uses_port) {
-    cfStatus ps = proxy_start(c);
-    if (ps != CF_OK) { cfPlanDestroy(pl.release()); return ps; }
-  }
+  if (pl->uses_port) CF_TRY(proxy_start(c));
   if (getenv("CF_PLAN_DUMP")) {   // "explain": the compiled device program of each (rank, tb)
     static const char* names[] = {"nop", "sync_cta", "sync_group", "dev_barrier", "signal", "wait", "multi",
                                   "copy", "put_packets", "read_packets", "port_put", "port_signal",
@@ -1022,7 +1067,7 @@ cfStatus load(cfComm* c, const char* json, size_t len, int dtype_override, cfPla
       fprintf(stderr, "\n");
     }
   }
-  *out = pl.release();
+  pl->ready = true;
   return CF_OK;
 }
 
@@ -1042,8 +1087,19 @@ extern "C" cfStatus cfPlanLoad(cfComm_t comm, const char* json, size_t len, int 
 extern "C" cfStatus cfPlanExecute(cfPlan_t pl, const void* const* inputs, void* const* outputs,
                                   const cudaStream_t* streams) {
   if (!pl || !inputs || !outputs || !streams) return fail(CF_E_CONFIG, "null argument");
+  if (!pl->ready) return fail(CF_E_CONFIG, "plan not connected (cfPlanGetHandle / cfPlanConnect)");
   cfComm* c = pl->comm;
   const int n = pl->ir.nranks;
+  // one process per GPU: peers' I/O buffers come from the registration table
+  const Registration* reg_in = nullptr;
+  const Registration* reg_out = nullptr;
+  if (pl->mp) {
+    if (pl->peer_in && !(reg_in = c->find_reg(inputs[0])))
+      return fail(CF_E_TOPOLOGY, "plan reads the peers' input: register input %p (cfBufferExport/Import)", inputs[0]);
+    if (pl->peer_out && !(reg_out = c->find_reg(outputs[0])))
+      return fail(CF_E_TOPOLOGY, "plan writes the peers' output: register output %p (cfBufferExport/Import)",
+                  outputs[0]);
+  }
   for (size_t li = 0; li < c->local.size(); li++) {
     if (!inputs[li] || !outputs[li]) return fail(CF_E_OOB, "local rank %zu: null buffer", li);
     if (((uintptr_t)inputs[li] | (uintptr_t)outputs[li]) & 15)
@@ -1070,11 +1126,11 @@ extern "C" cfStatus cfPlanExecute(cfPlan_t pl, const void* const* inputs, void* 
     a.in_buf = pl->in_buf;
     a.out_buf = pl->out_buf;
     a.input_private = pl->input_private ? 1 : 0;
-    a.gpu_scope = pl->groups.size() == 1 ? 1 : 0;
+    a.gpu_scope = (pl->groups.size() == 1 && !pl->mp) ? 1 : 0;
     // One launch holding every rank: the kernel boundary already separates
     // calls, so only a prologue that zeroes / copies buffers peers touch needs
     // the entry barrier, and no exit barrier is needed.
-    const bool single = pl->groups.size() == 1 && (int)c->local.size() == n;
+    const bool single = !pl->mp && pl->groups.size() == 1 && (int)c->local.size() == n;
     bool prologue = pl->input_private;
     for (auto& z : pl->zero_bufs) prologue |= !z.empty();
     a.entry_barrier = (!single || prologue) ? 1 : 0;
@@ -1082,8 +1138,15 @@ extern "C" cfStatus cfPlanExecute(cfPlan_t pl, const void* const* inputs, void* 
     a.flag_stride = pl->flag_stride;
     for (size_t b = 0; b < pl->ir.bufs.size(); b++) a.buf_bytes[b] = (uint64_t)pl->ir.bufs[b].elems * pl->es;
     for (int r = 0; r < n; r++) {
-      a.io_in[r] = (char*)inputs[r];     // one-process world: local index == rank
-      a.io_out[r] = (char*)outputs[r];
+      if (pl->mp) {
+        a.io_in[r] = r == pl->me ? (char*)inputs[0]
+                   : reg_in ? reg_in->peer[r] + ((const char*)inputs[0] - reg_in->ptr) : nullptr;
+        a.io_out[r] = r == pl->me ? (char*)outputs[0]
+                    : reg_out ? reg_out->peer[r] + ((char*)outputs[0] - reg_out->ptr) : nullptr;
+      } else {
+        a.io_in[r] = (char*)inputs[r];     // one-process world: local index == rank
+        a.io_out[r] = (char*)outputs[r];
+      }
       a.st[r] = (PlanState*)(pl->heap[r] + pl->state_off);
       a.lanes[r] = (uint64_t*)(pl->heap[r] + pl->lanes_off);
       a.bars[r] = (uint64_t*)(pl->heap[r] + pl->bars_off);
@@ -1098,6 +1161,12 @@ extern "C" cfStatus cfPlanExecute(cfPlan_t pl, const void* const* inputs, void* 
     cudaSetDevice(G.dev);
     cfStatus s = join_streams(c, (int)gi, streams, false);
     if (s != CF_OK) { cudaSetDevice(prev); return s; }
+    if (np <= kParamProgs) {
+      a.prog_in_param = 1;
+      for (int p = 0; p < np; p++) {
+        a.prog_tab[p] = make_int4(pl->prog_rank[G.progs[p]], G.beg[p], G.end[p], 0);
+      }
+    }
     void* args[] = {&a};
     a.window = kPlanWindow;
     a.has_prologue = pl->has_prologue ? 1 : 0;
@@ -1136,7 +1205,8 @@ extern "C" cfStatus cfPlanLastDeviceError(cfPlan_t pl, int* code) {
   cudaGetDevice(&prev);
   uint32_t worst = 0;
   for (size_t r = 0; r < pl->heap.size(); r++) {
-    cudaSetDevice(pl->comm->local[r].dev);
+    if (!pl->heap[r] || pl->heap_mapped[r]) continue;   // own heaps only
+    cudaSetDevice(pl->comm->local[pl->mp ? 0 : r].dev);
     cudaDeviceSynchronize();
     PlanState st;
     if (cudaMemcpy(&st, pl->heap[r] + pl->state_off, sizeof(st), cudaMemcpyDeviceToHost) != cudaSuccess) {
@@ -1164,10 +1234,78 @@ extern "C" cfStatus cfPlanDestroy(cfPlan_t pl) {
   }
   for (size_t r = 0; r < pl->heap.size(); r++)
     if (pl->heap[r]) {
-      cudaSetDevice(pl->comm->local[r].dev);
-      cudaFree(pl->heap[r]);
+      cudaSetDevice(pl->comm->local[pl->mp ? 0 : r].dev);
+      if (pl->heap_mapped[r]) cudaIpcCloseMemHandle(pl->heap[r]);
+      else cudaFree(pl->heap[r]);
     }
   cudaSetDevice(prev);
   delete pl;
   return CF_OK;
+}
+
+// ------------------------------------------------------------------ one process per GPU
+
+namespace {
+struct PlanBlob {
+  uint32_t magic;
+  int32_t rank;
+  uint64_t heap_bytes;
+  cudaIpcMemHandle_t ipc;
+};
+constexpr uint32_t kPlanMagic = 0x43465031;  // "CFP1"
+}  // namespace
+
+extern "C" cfStatus cfPlanGetHandle(cfPlan_t pl, void* handle, size_t* bytes) {
+  if (!pl || !bytes) return fail(CF_E_CONFIG, "null argument");
+  if (!pl->mp) return fail(CF_E_CONFIG, "cfPlanGetHandle is for one-process-per-GPU communicators");
+  if (*bytes < CF_PLAN_HANDLE_BYTES || !handle) {
+    *bytes = CF_PLAN_HANDLE_BYTES;
+    return fail(CF_E_CONFIG, "plan handle buffer needs %d bytes", CF_PLAN_HANDLE_BYTES);
+  }
+  static_assert(sizeof(PlanBlob) <= CF_PLAN_HANDLE_BYTES, "plan handle too large");
+  PlanBlob b;
+  memset(&b, 0, sizeof(b));
+  b.magic = kPlanMagic;
+  b.rank = pl->me;
+  b.heap_bytes = pl->heap_bytes;
+  int prev = -1;
+  cudaGetDevice(&prev);
+  cudaSetDevice(pl->comm->local[0].dev);
+  const cudaError_t e = cudaIpcGetMemHandle(&b.ipc, pl->heap[pl->me]);
+  cudaSetDevice(prev);
+  if (e != cudaSuccess) return fail(CF_E_CUDA, "cudaIpcGetMemHandle(plan heap): %s", cudaGetErrorString(e));
+  memset(handle, 0, CF_PLAN_HANDLE_BYTES);
+  memcpy(handle, &b, sizeof(b));
+  *bytes = CF_PLAN_HANDLE_BYTES;
+  return CF_OK;
+}
+
+extern "C" cfStatus cfPlanConnect(cfPlan_t pl, const void* handles, size_t bytes_per_handle) {
+  if (!pl || !handles) return fail(CF_E_CONFIG, "null argument");
+  if (!pl->mp) return fail(CF_E_CONFIG, "cfPlanConnect is for one-process-per-GPU communicators");
+  if (pl->ready) return CF_OK;
+  if (bytes_per_handle < sizeof(PlanBlob)) return fail(CF_E_CONFIG, "plan handle too small");
+  const int n = pl->ir.nranks;
+  int prev = -1;
+  cudaGetDevice(&prev);
+  cudaSetDevice(pl->comm->local[0].dev);
+  for (int r = 0; r < n; r++) {
+    PlanBlob b;
+    memcpy(&b, (const char*)handles + (size_t)r * bytes_per_handle, sizeof(b));
+    if (b.magic != kPlanMagic || b.rank != r || b.heap_bytes != pl->heap_bytes) {
+      cudaSetDevice(prev);
+      return fail(CF_E_RANK_MISMATCH, "plan handle %d is not rank %d's handle of this plan", r, r);
+    }
+    if (r == pl->me) continue;
+    void* p = nullptr;
+    const cudaError_t e = cudaIpcOpenMemHandle(&p, b.ipc, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+      cudaSetDevice(prev);
+      return fail(CF_E_CUDA, "cudaIpcOpenMemHandle(plan heap of rank %d): %s", r, cudaGetErrorString(e));
+    }
+    pl->heap[r] = (char*)p;
+    pl->heap_mapped[r] = true;
+  }
+  cudaSetDevice(prev);
+  return finalize(pl);
 }

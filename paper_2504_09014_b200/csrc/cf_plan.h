@@ -147,7 +147,13 @@ struct PlanArgs {
   int rank_leader[CF_MAX_RANKS];
   PortQueue port[CF_MAX_RANKS];  // proxy request rings (plans with port channels)
   uint64_t* port_done;           // [nprog * K] completion counters of this launch's CTAs
+  // Program table {rank, begin, end, -} in the parameter space when it fits,
+  // so a CTA knows its op range without a dependent global load.
+  int prog_in_param;
+  int4 prog_tab[256];
 };
+constexpr int kParamProgs = 256;
+static_assert(sizeof(PlanArgs) <= 32764, "kernel parameter space");
 constexpr int kMaxBufs = 16;
 constexpr int kMaxZero = 16;
 constexpr int kPlanWindow = 32;   // DevOps staged in shared memory at a time

@@ -420,33 +420,44 @@ __device__ __forceinline__ void resolve_window(const PlanArgs& a, DevOp* ops, in
 template <typename T>
 __global__ void __launch_bounds__(512) plan_kernel(const __grid_constant__ PlanArgs a) {
   const int pid = blockIdx.x / a.K, j = blockIdx.x % a.K;
-  const int rank = a.prog_rank[pid];
+  int rank, pb, pe;
+  if (a.prog_in_param) {
+    const int4 t = a.prog_tab[pid];
+    rank = t.x, pb = t.y, pe = t.z;
+  } else {
+    rank = a.prog_rank[pid], pb = a.prog_begin[pid], pe = a.prog_end[pid];
+  }
   PlanState* ps = a.st[rank];
   RankState* rs = &ps->base;
+  // Ops are staged into shared memory in windows of a.window ops: every field
+  // read of the interpreter then hits shared memory (the acquire loads of the
+  // waits invalidate L1, which would otherwise send each field load to L2).
+  // The first window's copy is in flight together with the epoch load.
+  extern __shared__ uint4 s_raw[];
+  DevOp* s_ops = reinterpret_cast<DevOp*>(s_raw);
+  auto stage = [&](int w0, int w1) {
+    const uint4* src = reinterpret_cast<const uint4*>(a.ops + w0);
+    const int nvec = (w1 - w0) * (int)(sizeof(DevOp) / 16);
+    for (int t = threadIdx.x; t < nvec; t += blockDim.x) s_raw[t] = src[t];
+  };
   __shared__ uint64_t s_e;
   if (threadIdx.x == 0) s_e = *(volatile uint64_t*)&rs->epoch + 1;
+  if (pb < pe) stage(pb, min(pb + a.window, pe));
   __syncthreads();
   const uint64_t e = s_e;
   if (a.has_prologue) prologue(a, rank);
   // rank barriers are numbered consecutively across calls (monotonic counters)
   const uint64_t per_call = (uint64_t)(a.entry_barrier + a.exit_barrier);
   if (a.entry_barrier) rank_barrier(a, rank, (e - 1) * per_call + 1);
-  // Ops are staged into shared memory in windows of a.window ops: every field
-  // read of the interpreter then hits shared memory (the acquire loads of the
-  // waits invalidate L1, which would otherwise send each field load to L2).
-  extern __shared__ uint4 s_raw[];
-  DevOp* s_ops = reinterpret_cast<DevOp*>(s_raw);
   uint64_t port_last = ~0ull;   // thread 0: this CTA's most recent proxy ticket
-  const int end = a.prog_end[pid];
-  for (int w0 = a.prog_begin[pid]; w0 < end; w0 += a.window) {
+  const int end = pe;
+  for (int w0 = pb; w0 < end; w0 += a.window) {
     const int w1 = min(w0 + a.window, end);
-    __syncthreads();
-    {
-      const uint4* src = reinterpret_cast<const uint4*>(a.ops + w0);
-      const int nvec = (w1 - w0) * (int)(sizeof(DevOp) / 16);
-      for (int t = threadIdx.x; t < nvec; t += blockDim.x) s_raw[t] = src[t];
+    if (w0 != pb) {
+      __syncthreads();
+      stage(w0, w1);
+      __syncthreads();
     }
-    __syncthreads();
     resolve_window(a, s_ops, w1 - w0, e);
     __syncthreads();
   for (int i = w0; i < w1; i++) {

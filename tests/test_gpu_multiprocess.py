@@ -135,3 +135,90 @@ def test_two_processes_one_gpu_all_collectives():
             got_y, got_ro = res[r][("norm", algo)]
             assert np.array_equal(got_ro.view(np.uint32), ro.view(np.uint32)), (algo, r)
             np.testing.assert_allclose(got_y, y, rtol=1e-5, atol=1e-6)
+
+
+PLAN_CASES = [("2pa", "memory", 2048, "f32"), ("2pa", "ll", 1024, "f32"), ("1pa", "", 512, "bf16"),
+              ("ring_rs", "", 4096, "f32"), ("allpairs_ag", "", 1000, "f32"), ("2pr", "", 4096, "bf16"),
+              ("2pa", "port", 4096, "f32")]
+
+
+def _plan_doc(name, var, elems, dtype, n):
+    from paper_2504_09014_b200.algorithms import build_algo
+    from paper_2504_09014_b200.lowering import LoweringParams, lower
+    from paper_2504_09014_b200.plan import serialize_plan
+    proto = "LL" if name == "1pa" or var == "ll" else "HB"
+    params = LoweringParams(n, elems, dtype, proto)
+    return serialize_plan(lower(build_algo(name, params, variant=var), params))
+
+
+def _plan_worker(rank, world, port, q):
+    try:
+        import sys
+        root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+        sys.path[:0] = [root, os.path.join(root, "tests", "golden")]
+        import torch
+        import torch.distributed as dist
+        from inputs import gen_inputs
+        from paper_2504_09014_b200.comm import Communicator
+        from paper_2504_09014_b200.dtypes import torch_dtype
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                                world_size=world)
+        comm = Communicator(spin_timeout_ms=60000)
+        out = {}
+        for name, var, elems, dtype in PLAN_CASES:
+            rt = comm.load_plan(_plan_doc(name, var, elems, dtype, world), dtype=dtype)
+            ins = gen_inputs(world, rt.in_elems, dtype, "normal", 31 + elems)
+            x = ins[rank]
+            send = (torch.from_numpy(x.view(np.int16)).view(torch.bfloat16) if dtype == "bf16"
+                    else torch.from_numpy(x)).cuda()
+            recv = torch.empty(rt.out_elems, dtype=torch_dtype(dtype), device="cuda")
+            comm.register(send)
+            comm.register(recv)
+            for _ in range(3):   # repeated executions reuse lanes / flags / barriers
+                rt.run(send, recv)
+            torch.cuda.synchronize()
+            rt.check_device_error()
+            got = recv.cpu()
+            out[(name, var)] = (got.view(torch.int16).numpy().view(np.uint16) if dtype == "bf16"
+                                else got.numpy()).copy()
+            comm.deregister(send)
+            comm.deregister(recv)
+            rt.close()
+        comm.close()
+        dist.barrier()
+        dist.destroy_process_group()
+        q.put((rank, out, None))
+    except Exception:
+        import traceback
+        q.put((rank, None, traceback.format_exc()))
+
+
+def test_two_processes_one_gpu_plans():
+    """K10 in the one-process-per-GPU mode: plan heaps exchanged over the
+    bootstrap, peers' I/O through registered buffers, port channels through
+    each process's proxy; outputs equal the sequential plan interpreter's."""
+    from oracle import oracle
+    from inputs import gen_inputs
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_plan_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        r, out, err = q.get(timeout=600)
+        assert err is None, err
+        res[r] = out
+    for p in procs:
+        p.join(timeout=60)
+    for name, var, elems, dtype in PLAN_CASES:
+        doc = _plan_doc(name, var, elems, dtype, world)
+        import json
+        in_elems = next(b["elems"] for b in json.loads(doc)["buffers"] if b["kind"] == "input")
+        ins = gen_inputs(world, in_elems, dtype, "normal", 31 + elems)
+        want = oracle.run_plan(doc, ins, dtype=dtype)
+        for r in range(world):
+            assert np.array_equal(res[r][(name, var)].view(np.uint8), want[r].view(np.uint8)), (name, var, r)
