@@ -509,6 +509,20 @@ def multi_sweep(comm, dev, world, send, recv):
             z = y.clone()
             row["nccl_eager_s"] = eager(lambda: dist.all_reduce(z, group=nccl))
         rows.append(row)
+    # C5: Llama-70B TP decode AllReduce [b, 8192] bf16 through DSL plans (K10)
+    from paper_2504_09014_b200.algorithms import build_algo
+    from paper_2504_09014_b200.lowering import LoweringParams, lower
+    for name, var in (("2pa", "memory"), ("1pa", "")):
+        for b in (1, 16, 256):
+            elems = 8192 * b
+            params = LoweringParams(world, elems, "bf16", "LL" if name == "1pa" else "HB")
+            rt = comm.load_plan(lower(build_algo(name, params, variant=var), params), dtype="bf16")
+            px, py = send[:rt.in_elems], recv[:rt.out_elems]
+            t = time_graph(dev, lambda: rt.run(px, py), 20, 3)
+            rt.check_device_error()
+            rows.append({"bytes": elems * 2, "plan": f"{name}{'_' + var if var else ''}", "batch": b,
+                         "cf_plan_graph_s": t})
+            rt.close()
     comm.check_device_error()
     return rows, (None if nccl is not None else nccl_err)
 
@@ -572,7 +586,10 @@ def run_multi_gpu(args):
     for i, row in enumerate(rows_local):
         nb = row["bytes"]
         out = {"bytes": nb}
-        for key in ("cf_graph_s", "cf_eager_s", "nccl_eager_s"):
+        for k2 in ("plan", "batch"):
+            if k2 in row:
+                out[k2] = row[k2]
+        for key in ("cf_graph_s", "cf_eager_s", "nccl_eager_s", "cf_plan_graph_s"):
             if key in row:
                 tk = max(x[2][i][key] for x in times)   # max over ranks
                 out[key[:-2]] = {"us": round(tk * 1e6, 2), "busbw": round(busbw(nb, tk, world), 2)}
