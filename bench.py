@@ -484,9 +484,17 @@ def multi_sweep(comm, dev, world, send, recv):
         nccl = None
         nccl_err = f"{type(e).__name__}: {e}"[:200]
     rows = []
-    for nb in (KiB, 16 * KiB, 256 * KiB, MiB, 16 * MiB, 256 * MiB):
+    # 1 KiB .. 1 GiB (x4); buffers of the largest size, registered once
+    big = GiB if not os.environ.get("CF_BENCH_ONE_GPU") else 256 * MiB
+    bs = torch.randn(big // 2, device=dev).to(torch.bfloat16)
+    br = torch.empty_like(bs)
+    comm.register(bs)
+    comm.register(br)
+    for nb in [KiB << (2 * i) for i in range(11)]:
+        if nb > big:
+            break
         cnt = nb // 2
-        x, y = send[:cnt], recv[:cnt]
+        x, y = bs[:cnt], br[:cnt]
         iters = 50 if nb <= MiB else 10
         t_graph = time_graph(dev, lambda: comm.all_reduce(x, y, algo="auto"), iters, 3)
         st = torch.cuda.current_stream(dev)
@@ -509,6 +517,9 @@ def multi_sweep(comm, dev, world, send, recv):
             z = y.clone()
             row["nccl_eager_s"] = eager(lambda: dist.all_reduce(z, group=nccl))
         rows.append(row)
+    comm.deregister(bs)
+    comm.deregister(br)
+    del bs, br
     # C5: Llama-70B TP decode AllReduce [b, 8192] bf16 through DSL plans (K10)
     from paper_2504_09014_b200.algorithms import build_algo
     from paper_2504_09014_b200.lowering import LoweringParams, lower
