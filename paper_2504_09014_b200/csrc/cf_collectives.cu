@@ -34,15 +34,17 @@ __device__ __forceinline__ uint64_t begin_call(const RankCtx& rk) {
   return s_e;
 }
 
+// No fences: every CTA of this launch read the epoch before its arrival was
+// counted (the last arriver sees all of them), and the next launch on the
+// stream sees these stores through the kernel boundary.  Data visibility to
+// peers is the handshakes' / LL flags' business, not the epoch's.
 __device__ __forceinline__ void end_call(const RankCtx& rk, uint64_t e) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
     const uint32_t prev = atomicAdd(&rk.st->arrive, 1u);
     if (prev == gridDim.x - 1) {
       *(volatile uint32_t*)&rk.st->arrive = 0;
       *(volatile uint64_t*)&rk.st->epoch = e;
-      __threadfence();
     }
   }
 }

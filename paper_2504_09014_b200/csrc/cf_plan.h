@@ -150,9 +150,9 @@ struct PlanArgs {
   // Program table {rank, begin, end, -} in the parameter space when it fits,
   // so a CTA knows its op range without a dependent global load.
   int prog_in_param;
-  int4 prog_tab[256];
+  int4 prog_tab[128];
 };
-constexpr int kParamProgs = 256;
+constexpr int kParamProgs = 128;
 static_assert(sizeof(PlanArgs) <= 32764, "kernel parameter space");
 constexpr int kMaxBufs = 16;
 constexpr int kMaxZero = 16;

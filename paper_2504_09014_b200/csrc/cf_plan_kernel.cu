@@ -514,10 +514,9 @@ __global__ void __launch_bounds__(512) plan_kernel(const __grid_constant__ PlanA
   __syncthreads();
   if (threadIdx.x == 0) {
     const uint32_t prev = atomicAdd(&rs->arrive, 1u);
-    if (prev == (uint32_t)a.rank_ctas[rank] - 1) {
+    if (prev == (uint32_t)a.rank_ctas[rank] - 1) {   // no fence needed: see end_call
       *(volatile uint32_t*)&rs->arrive = 0;
       *(volatile uint64_t*)&rs->epoch = e;
-      __threadfence();
     }
   }
 }
