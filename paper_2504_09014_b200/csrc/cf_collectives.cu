@@ -38,6 +38,13 @@ __device__ __forceinline__ uint64_t begin_call(const RankCtx& rk) {
 // counted (the last arriver sees all of them), and the next launch on the
 // stream sees these stores through the kernel boundary.  Data visibility to
 // peers is the handshakes' / LL flags' business, not the epoch's.
+// Single-launch HB kernels need the epoch only in thread 0 at the very end:
+// load it without the block barrier so the data loads start right away.
+__device__ __forceinline__ uint64_t begin_call_lazy(const RankCtx& rk, bool single) {
+  if (!single) return begin_call(rk);
+  return threadIdx.x == 0 ? *(volatile uint64_t*)&rk.st->epoch + 1 : 0;
+}
+
 __device__ __forceinline__ void end_call(const RankCtx& rk, uint64_t e) {
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -132,7 +139,7 @@ __global__ void __launch_bounds__(512) pull_reduce_kernel(const __grid_constant_
   const RankCtx& rk = a.rk[blockIdx.y];
   constexpr int V = Vec<T>::N;
   const int n = a.n, r = rk.rank;
-  const uint64_t e = begin_call(rk);
+  const uint64_t e = begin_call_lazy(rk, a.single_launch);
   if (!a.single_launch) handshake(rk, n, e * kPhases + 1, false, a.gpu_scope);
 
   size_t lo = 0, hi = a.count;
@@ -357,7 +364,7 @@ __global__ void __launch_bounds__(512) push_gather_kernel(const __grid_constant_
   const RankCtx& rk = a.rk[blockIdx.y];
   constexpr int V = 16 / sizeof(T);
   const int n = a.n, r = rk.rank;
-  const uint64_t e = begin_call(rk);
+  const uint64_t e = begin_call_lazy(rk, a.single_launch);
   if (!a.single_launch) handshake(rk, n, e * kPhases + 1, false, a.gpu_scope);
   const size_t stride = (size_t)gridDim.x * blockDim.x;
   const size_t t0 = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -752,7 +759,7 @@ __global__ void __launch_bounds__(512) ar_rmsnorm_kernel(const __grid_constant__
   constexpr int V = Vec<T>::N;
   constexpr int kCache = 4;
   const int n = a.n, r = rk.rank;
-  const uint64_t e = begin_call(rk);
+  const uint64_t e = begin_call_lazy(rk, a.single_launch);
   if (!a.single_launch) handshake(rk, n, e * kPhases + 1, false, a.gpu_scope);
   size_t r0 = 0, r1 = a.rows;
   if (a.push) {
