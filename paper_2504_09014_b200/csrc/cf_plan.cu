@@ -82,6 +82,7 @@ struct cfPlan {
   std::vector<std::vector<int>> zero_bufs;  // per rank
   std::vector<cf::plan::Group> groups;
   int n_device_ops = 0;
+  int window = 1;                     // ops staged per shared-memory window (<= kPlanWindow)
   bool uses_port = false;             // port-channel ops go through the proxy
   bool has_prologue = false;          // per-call zeroing / private input copy
   // one-process-per-GPU: this process runs rank `me`'s programs; the peers'
@@ -931,6 +932,8 @@ cfStatus load(cfComm* c, const char* json, size_t len, int dtype_override, cfPla
   }
   pl->prog_rank = prank;
   pl->prog_tb = ptb;
+  // shared-memory window: the longest program, up to kPlanWindow ops
+  for (auto& prog : pl->prog_ops) pl->window = std::max(pl->window, (int)std::min<size_t>(prog.size(), kPlanWindow));
 
   // per-rank plan heap: [PlanState | lanes | bars | buffers]
   pl->state_off = 0;
@@ -1168,7 +1171,7 @@ extern "C" cfStatus cfPlanExecute(cfPlan_t pl, const void* const* inputs, void* 
       }
     }
     void* args[] = {&a};
-    a.window = kPlanWindow;
+    a.window = pl->window;
     a.has_prologue = pl->has_prologue ? 1 : 0;
     if (pl->uses_port) {
       if (!proxy_alive(c)) { cudaSetDevice(prev); return fail(CF_E_PROXY_DOWN, "port-channel proxy is not running"); }
@@ -1176,7 +1179,7 @@ extern "C" cfStatus cfPlanExecute(cfPlan_t pl, const void* const* inputs, void* 
       a.port_done = G.d_done;
     }
     cudaError_t e = cudaLaunchKernel(kernel, dim3(np * pl->K), dim3(pl->threads), args,
-                                     kPlanWindow * sizeof(DevOp), streams[c->groups[gi][0]]);
+                                     pl->window * sizeof(DevOp), streams[c->groups[gi][0]]);
     if (e != cudaSuccess) {
       cudaSetDevice(prev);
       return fail(CF_E_CUDA, "plan kernel launch: %s", cudaGetErrorString(e));

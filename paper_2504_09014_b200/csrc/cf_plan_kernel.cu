@@ -26,14 +26,6 @@ __device__ __forceinline__ void red_add_release(uint64_t* p, uint64_t v, bool gp
   else asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-__device__ __forceinline__ char* ref_ptr(const PlanArgs& a, const DRef& r) {
-  if (r.buf == kAbsolute) return reinterpret_cast<char*>(r.off);   // plan-owned, resolved at load
-  char* base;
-  if (r.buf == a.in_buf && !a.input_private) base = a.io_in[r.rank];
-  else if (r.buf == a.out_buf) base = a.io_out[r.rank];
-  else base = a.bufptr[r.buf * a.n + r.rank];
-  return base + r.off;
-}
 
 // Data-op references are resolved to absolute addresses when their window is
 // staged (see resolve_window), so the op bodies read one shared-memory word per
@@ -397,7 +389,8 @@ __device__ __noinline__ void prologue(const PlanArgs& a, int rank) {
 
 // Rewrite the staged window's data-op references as absolute addresses (the io
 // buffers change per call, so this cannot all be done at load time).
-__device__ __forceinline__ void resolve_window(const PlanArgs& a, DevOp* ops, int nops, uint64_t e) {
+__device__ __forceinline__ void resolve_window(const PlanArgs& a, DevOp* ops, int nops, uint64_t e,
+                                               char* const* io) {
   constexpr int kSlots = kMaxSrc + kMaxDst;
   for (int t = threadIdx.x; t < nops * kSlots; t += blockDim.x) {
     DevOp& op = ops[t / kSlots];
@@ -412,7 +405,11 @@ __device__ __forceinline__ void resolve_window(const PlanArgs& a, DevOp* ops, in
     if (k < kMaxSrc ? k >= op.nsrc : k - kMaxSrc >= op.ndst) continue;
     DRef& r = k < kMaxSrc ? op.src[k] : op.dst[k - kMaxSrc];
     if (r.buf == kAbsolute) continue;
-    r.off = reinterpret_cast<uint64_t>(ref_ptr(a, r));
+    char* base;
+    if (r.buf == a.in_buf && !a.input_private) base = io[r.rank];
+    else if (r.buf == a.out_buf) base = io[CF_MAX_RANKS + r.rank];
+    else base = a.bufptr[r.buf * a.n + r.rank];
+    r.off = reinterpret_cast<uint64_t>(base + r.off);
     r.buf = kAbsolute;
   }
 }
@@ -440,6 +437,16 @@ __global__ void __launch_bounds__(512) plan_kernel(const __grid_constant__ PlanA
     const int nvec = (w1 - w0) * (int)(sizeof(DevOp) / 16);
     for (int t = threadIdx.x; t < nvec; t += blockDim.x) s_raw[t] = src[t];
   };
+  // the ranks' I/O bases in shared memory: the resolve pass indexes them per
+  // thread, which on the parameter space would serialize the warp
+  __shared__ char* s_io[2 * CF_MAX_RANKS];
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int r = 0; r < CF_MAX_RANKS; r++) {
+      s_io[r] = a.io_in[r];
+      s_io[CF_MAX_RANKS + r] = a.io_out[r];
+    }
+  }
   __shared__ uint64_t s_e;
   if (threadIdx.x == 0) s_e = *(volatile uint64_t*)&rs->epoch + 1;
   if (pb < pe) stage(pb, min(pb + a.window, pe));
@@ -458,7 +465,7 @@ __global__ void __launch_bounds__(512) plan_kernel(const __grid_constant__ PlanA
       stage(w0, w1);
       __syncthreads();
     }
-    resolve_window(a, s_ops, w1 - w0, e);
+    resolve_window(a, s_ops, w1 - w0, e, s_io);
     __syncthreads();
   for (int i = w0; i < w1; i++) {
     const DevOp& op = s_ops[i - w0];
