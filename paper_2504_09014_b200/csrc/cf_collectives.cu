@@ -18,6 +18,16 @@
 
 namespace cf {
 
+#ifdef CF_TS
+#define TS_DECL uint64_t ts_[8]; int tsn_ = 0;
+#define TS_MARK() do { if (threadIdx.x == 0 && blockIdx.x == 0) ts_[tsn_] = globaltimer(); tsn_++; } while (0)
+#define TS_DUMP(nm) do { if (threadIdx.x == 0 && blockIdx.x == 0) { printf("TS %s rank %d t0 %llu", nm, rk.rank, (unsigned long long)ts_[0]); for (int q_ = 1; q_ < tsn_; q_++) printf(" +%llu", (unsigned long long)(ts_[q_] - ts_[0])); printf("\n"); } } while (0)
+#else
+#define TS_DECL
+#define TS_MARK()
+#define TS_DUMP(nm)
+#endif
+
 // ---------------------------------------------------------------- call bracket
 
 // Semaphore values are epoch * kPhases + phase (phase in [1, kPhases)) for every
@@ -73,6 +83,19 @@ __device__ __forceinline__ void handshake(const RankCtx& rk, int n, uint64_t v, 
 
 // ---------------------------------------------------------------- vector helpers
 
+// Ragged-edge paths stay out of line: the small-message kernels execute each
+// instruction about once per launch on a cold instruction cache, so code size
+// on the latency path is latency (one copy of the edge code, not one per
+// unrolled peer).
+template <int ES>
+__device__ __noinline__ uint4 ld_partial16_ool(const char* p, int nbytes) {
+  return ld_partial16<ES>(p, nbytes);
+}
+template <int ES>
+__device__ __noinline__ void st_masked16_ool(char* p, uint4 v, int jlo, int jhi) {
+  st_masked16<ES>(p, v, jlo, jhi);
+}
+
 // Load 16-byte vector `v` of a T array of `count` elements; lanes past the end
 // read as zero.
 template <typename T>
@@ -81,7 +104,7 @@ __device__ __forceinline__ uint4 load_vec(const char* base, size_t v, size_t cou
   const size_t e0 = v * V;
   if (e0 + V <= count) return ld16(base + v * 16);
   const int nb = e0 < count ? (int)((count - e0) * sizeof(T)) : 0;
-  return ld_partial16<sizeof(T)>(base + v * 16, nb);
+  return ld_partial16_ool<sizeof(T)>(base + v * 16, nb);
 }
 
 // Store the lanes of vector `v` whose element index lies in [lo, hi) at
@@ -98,7 +121,7 @@ __device__ __forceinline__ void store_vec(char* base, size_t v, uint4 val, size_
   }
   const int jlo = lo > e0 ? (int)min(lo - e0, (size_t)V) : 0;
   const int jhi = hi > e0 ? (int)min(hi - e0, (size_t)V) : 0;
-  st_masked16<sizeof(T)>(p, val, jlo, jhi);
+  st_masked16_ool<sizeof(T)>(p, val, jlo, jhi);
 }
 
 // Accumulate NR (runtime n <= NR) 16-byte vectors in order: x[0] first (or a
@@ -180,22 +203,29 @@ __global__ void __launch_bounds__(512) pull_reduce_kernel(const __grid_constant_
 // slot r of each peer's scratch (parity half e&1), then polls its own n-1
 // slots and reduces in the 1pa order (own input first, peers ascending,
 // cf/collectives.py:156-161).  No semaphores, no fences: the flag travels in
-// the same 16-byte store as the data.
+// the same 16-byte store as the data.  Latency structure: the first input
+// load is issued before the epoch read; the read phase keeps every peer's
+// packets in flight and re-polls all unstamped ones per round
+// (ll16x2_poll), so waiting for n-1 peers costs one round trip per round.
 template <typename T, int NR>
-__global__ void __launch_bounds__(512, 2) ll_oneshot_kernel(const __grid_constant__ CollArgs a) {
+__global__ void __launch_bounds__(512, 1) ll_oneshot_kernel(const __grid_constant__ CollArgs a) {
   const RankCtx& rk = a.rk[blockIdx.y];
-  constexpr int V = Vec<T>::N;
+  constexpr int P = NR - 1;
   const int n = a.n, r = rk.rank;
-  const uint64_t e = begin_call(rk);
-  const uint32_t flag = ll_flag(e);
-  const size_t par = (e & 1) * a.half;
+  TS_DECL
+  TS_MARK();
+  constexpr int V = Vec<T>::N;
   const size_t nvec = (a.count + V - 1) / V;
   const size_t stride = (size_t)gridDim.x * blockDim.x;
   const size_t t0 = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int lead = a.order == kLead ? r : 0;
+  const uint4 first = t0 < nvec ? load_vec<T>(rk.in[r], t0, a.count) : make_uint4(0, 0, 0, 0);
+  const uint64_t e = begin_call(rk);
+  TS_MARK();
+  const uint32_t flag = ll_flag(e);
+  const size_t par = (e & 1) * a.half;
 
   for (size_t v = t0; v < nvec; v += stride) {
-    const uint4 x = load_vec<T>(rk.in[r], v, a.count);
+    const uint4 x = v == t0 ? first : load_vec<T>(rk.in[r], v, a.count);
 #pragma unroll
     for (int p = 0; p < NR; p++) {
       if (p < n && p != r) {
@@ -205,60 +235,42 @@ __global__ void __launch_bounds__(512, 2) ll_oneshot_kernel(const __grid_constan
       }
     }
   }
-  (void)lead;
+  TS_MARK();
   using A = typename Vec<T>::Acc;
+  const uint32_t all = (1u << (n - 1)) - 1u;
   for (size_t v = t0; v < nvec; v += stride) {
-    // peers in groups of G: issue the group's packets (2G loads in flight),
-    // then accumulate in the 1pa order -- own input, then peers ascending --
-    // re-polling only the packets whose flags were not yet stamped.  Groups
-    // keep the register footprint under the 2-CTAs/SM bound.
-    constexpr int G = 4;
-    A acc[V];
-    Vec<T>::load(load_vec<T>(rk.in[r], v, a.count), acc);
+    const uint4 own = v == t0 ? first : load_vec<T>(rk.in[r], v, a.count);
+    const char* base = rk.scr[r] + par + v * 32;
+    uint4 r0[P], r1[P];
 #pragma unroll
-    for (int g0 = 0; g0 < NR - 1; g0 += G) {
-      uint4 raw0[G], raw1[G];
-#pragma unroll
-      for (int gi = 0; gi < G; gi++) {
-        const int i = g0 + gi;
-        if (i < NR - 1 && i < n - 1) {
-          const int q = i + (i >= r ? 1 : 0);
-          const char* s = rk.scr[r] + par + (size_t)q * a.slot + v * 32;
-          raw0[gi] = ld16_volatile(s);
-          raw1[gi] = ld16_volatile(s + 16);
-        }
+    for (int i = 0; i < P; i++) {
+      if (i < n - 1) {
+        const char* u = ll_unit(base, a.slot, r, i);
+        r0[i] = ld16_volatile(u);
+        r1[i] = ld16_volatile(u + 16);
       }
+    }
+    ll16x2_poll<P>(base, a.slot, r, r0, r1, all, flag, rk.st);
+    A acc[V];
+    Vec<T>::load(own, acc);
 #pragma unroll
-      for (int gi = 0; gi < G; gi++) {
-        const int i = g0 + gi;
-        if (i < NR - 1 && i < n - 1) {
-          const int q = i + (i >= r ? 1 : 0);
-          const char* s = rk.scr[r] + par + (size_t)q * a.slot + v * 32;
-          uint2 p0 = make_uint2(raw0[gi].x, raw0[gi].z), p1 = make_uint2(raw1[gi].x, raw1[gi].z);
-          if (raw0[gi].y != flag || raw0[gi].w != flag) p0 = ll16_get(s, flag, rk.st);
-          if (raw1[gi].y != flag || raw1[gi].w != flag) p1 = ll16_get(s + 16, flag, rk.st);
-          A t[V];
-          Vec<T>::load(make_uint4(p0.x, p0.y, p1.x, p1.y), t);
+    for (int i = 0; i < P; i++) {
+      if (i < n - 1) {
+        A t[V];
+        Vec<T>::load(ll16x2_payload(r0[i], r1[i]), t);
 #pragma unroll
-          for (int j = 0; j < V; j++) acc[j] = acc_add(acc[j], t[j]);
-        }
+        for (int j = 0; j < V; j++) acc[j] = acc_add(acc[j], t[j]);
       }
     }
     store_vec<T>(rk.out[r], v, Vec<T>::store(acc), 0, a.count, 0);
   }
+  TS_MARK();
   end_call(rk, e);
+  TS_MARK();
+  TS_DUMP("1pa");
 }
 
 // ---------------------------------------------------------------- K4
-
-// A 16-byte payload carried by two LL16 packets whose raw words were already
-// loaded (r0, r1): re-poll only a packet whose flags are not yet `flag`.
-__device__ __forceinline__ uint4 ll16x2_finish(const char* s, uint4 r0, uint4 r1, uint32_t flag, RankState* st) {
-  uint2 p0 = make_uint2(r0.x, r0.z), p1 = make_uint2(r1.x, r1.z);
-  if (r0.y != flag || r0.w != flag) p0 = ll16_get(s, flag, st);
-  if (r1.y != flag || r1.w != flag) p1 = ll16_get(s + 16, flag, st);
-  return make_uint4(p0.x, p0.y, p1.x, p1.y);
-}
 
 // Two-shot LL (cf/collectives.py:216-231): phase 1 sends chunk p of the send
 // buffer as packets into peer p's ph1 slot r; rank r reduces chunk r (owner
@@ -266,12 +278,18 @@ __device__ __forceinline__ uint4 ll16x2_finish(const char* s, uint4 r0, uint4 r1
 // every peer's ph2 slot r; phase 2 decodes the peers' chunks into recv.
 // Chunks follow the reference chunking (cs elements); packets carry the
 // 16-byte vectors covering a chunk, and stores are masked to the chunk.
+// Each phase issues all of its loads (inputs, every peer's packets) before
+// the first store / poll check, so a phase costs one round trip, not n-1.
 template <typename T, int NR>
 __global__ void __launch_bounds__(512) ll_twoshot_kernel(const __grid_constant__ CollArgs a) {
   const RankCtx& rk = a.rk[blockIdx.y];
   constexpr int V = Vec<T>::N;
+  constexpr int P = NR - 1;
   const int n = a.n, r = rk.rank;
+  TS_DECL
+  TS_MARK();
   const uint64_t e = begin_call(rk);
+  TS_MARK();
   const uint32_t flag = ll_flag(e);
   const size_t ph1 = (e & 1) * a.half, ph2 = ph1 + (size_t)n * a.slot;
   const size_t stride = (size_t)gridDim.x * blockDim.x;
@@ -280,44 +298,63 @@ __global__ void __launch_bounds__(512) ll_twoshot_kernel(const __grid_constant__
   auto chi = [&](int c) { return min((size_t)c * a.cs + a.cs, a.count); };
   auto vlo = [&](int c) { return clo(c) / V; };
   auto vhi = [&](int c) { return (chi(c) + V - 1) / V; };
+  const size_t nvmax = (a.cs + V - 1) / V + 1;   // vectors covering any chunk
+  // Chunk bounds min(c * cs, count) on the 16-byte grid (cs and count
+  // multiples of V, the common case): every vector belongs to exactly one
+  // chunk, so phases 1 and 2 run one vector per thread over the whole buffer
+  // (peer = v / cv) -- all threads busy, one short code path.  Otherwise the
+  // per-chunk loops below handle vectors that straddle two chunks.
+  const bool grid = a.cs % V == 0 && a.count % V == 0;
+  const uint32_t cv = (uint32_t)(a.cs / V);
+  const size_t nvec = (a.count + V - 1) / V;
 
   // phase 1: scatter my chunks as packets
-  for (int p = 0; p < n; p++) {
-    if (p == r) continue;
-    const size_t b = vlo(p), nv = vhi(p) > b ? vhi(p) - b : 0;
-    char* dst = rk.scr[p] + ph1 + (size_t)r * a.slot;
-    for (size_t i = t0; i < nv; i += stride) {
-      const uint4 x = load_vec<T>(rk.in[r], b + i, a.count);
-      ll16_put_scoped(dst + i * 32, make_uint2(x.x, x.y), flag, a.gpu_scope);
-      ll16_put_scoped(dst + i * 32 + 16, make_uint2(x.z, x.w), flag, a.gpu_scope);
+  if (grid) {
+    for (size_t v = t0; v < nvec; v += stride) {
+      const uint32_t p = (uint32_t)v / cv, i = (uint32_t)v - p * cv;
+      if ((int)p == r) continue;
+      const uint4 x = load_vec<T>(rk.in[r], v, a.count);
+      char* d = rk.scr[p] + ph1 + (size_t)r * a.slot + (size_t)i * 32;
+      ll16_put_scoped(d, make_uint2(x.x, x.y), flag, a.gpu_scope);
+      ll16_put_scoped(d + 16, make_uint2(x.z, x.w), flag, a.gpu_scope);
+    }
+  } else for (size_t i = t0; i < nvmax; i += stride) {   // every peer's input vector loaded first
+    uint4 x[NR];
+#pragma unroll
+    for (int p = 0; p < NR; p++)
+      if (p < n && p != r && vlo(p) + i < vhi(p)) x[p] = load_vec<T>(rk.in[r], vlo(p) + i, a.count);
+#pragma unroll
+    for (int p = 0; p < NR; p++) {
+      if (p < n && p != r && vlo(p) + i < vhi(p)) {
+        char* d = rk.scr[p] + ph1 + (size_t)r * a.slot + i * 32;
+        ll16_put_scoped(d, make_uint2(x[p].x, x[p].y), flag, a.gpu_scope);
+        ll16_put_scoped(d + 16, make_uint2(x[p].z, x[p].w), flag, a.gpu_scope);
+      }
     }
   }
-  // reduce my chunk, store, broadcast as packets
+  TS_MARK();
+  // reduce my chunk (owner first, peers ascending), store, broadcast as packets
   {
     const size_t b = vlo(r), nv = vhi(r) > b ? vhi(r) - b : 0;
+    const uint32_t all = (1u << (n - 1)) - 1u;
     for (size_t i = t0; i < nv; i += stride) {
-      // every peer's two packets in flight first, then re-poll the unstamped ones
-      uint4 x[NR], raw1[NR];
+      const uint4 own = load_vec<T>(rk.in[r], b + i, a.count);
+      const char* base = rk.scr[r] + ph1 + i * 32;
+      uint4 r0[P], r1[P];
 #pragma unroll
-      for (int k = 0; k < NR; k++) {
-        if (k < n) {
-          const int q = order_src(kLead, k, r, n);
-          if (q == r) {
-            x[k] = load_vec<T>(rk.in[r], b + i, a.count);
-          } else {
-            const char* s = rk.scr[r] + ph1 + (size_t)q * a.slot + i * 32;
-            x[k] = ld16_volatile(s);
-            raw1[k] = ld16_volatile(s + 16);
-          }
+      for (int k = 0; k < P; k++) {
+        if (k < n - 1) {
+          const char* u = ll_unit(base, a.slot, r, k);
+          r0[k] = ld16_volatile(u);
+          r1[k] = ld16_volatile(u + 16);
         }
       }
+      ll16x2_poll<P>(base, a.slot, r, r0, r1, all, flag, rk.st);
+      uint4 x[NR];
+      x[0] = own;
 #pragma unroll
-      for (int k = 0; k < NR; k++) {
-        if (k < n) {
-          const int q = order_src(kLead, k, r, n);
-          if (q != r) x[k] = ll16x2_finish(rk.scr[r] + ph1 + (size_t)q * a.slot + i * 32, x[k], raw1[k], flag, rk.st);
-        }
-      }
+      for (int k = 0; k < P; k++)
+        if (k < n - 1) x[k + 1] = ll16x2_payload(r0[k], r1[k]);
       const uint4 res = reduce_vecs<T, NR>(x, n, false);
       store_vec<T>(rk.out[r], b + i, res, clo(r), chi(r), 0);
 #pragma unroll
@@ -330,28 +367,39 @@ __global__ void __launch_bounds__(512) ll_twoshot_kernel(const __grid_constant__
       }
     }
   }
-  // phase 2: decode the peers' reduced chunks (all peers' packets of vector i
-  // in flight at once)
-  const size_t nvmax = (a.cs + V - 1) / V + 1;
-  for (size_t i = t0; i < nvmax; i += stride) {
-    uint4 raw0[NR], raw1[NR];
+  TS_MARK();
+  // phase 2: decode the peers' reduced chunks
+  if (grid) {
+    for (size_t v = t0; v < nvec; v += stride) {
+      const uint32_t p = (uint32_t)v / cv, i = (uint32_t)v - p * cv;
+      if ((int)p == r) continue;
+      const char* u = rk.scr[r] + ph2 + (size_t)p * a.slot + (size_t)i * 32;
+      uint4 r0[1] = {ld16_volatile(u)}, r1[1] = {ld16_volatile(u + 16)};
+      ll16x2_poll<1>(u, 0, 1, r0, r1, 1u, flag, rk.st);
+      store_vec<T>(rk.out[r], v, ll16x2_payload(r0[0], r1[0]), 0, a.count, 0);
+    }
+  } else for (size_t i = t0; i < nvmax; i += stride) {   // all peers' packets of vector i in flight
+    const char* base = rk.scr[r] + ph2 + i * 32;
+    uint4 r0[NR], r1[NR];
+    uint32_t pend = 0;
 #pragma unroll
     for (int p = 0; p < NR; p++) {
       if (p < n && p != r && vlo(p) + i < vhi(p)) {
-        const char* s = rk.scr[r] + ph2 + (size_t)p * a.slot + i * 32;
-        raw0[p] = ld16_volatile(s);
-        raw1[p] = ld16_volatile(s + 16);
+        const char* u = base + (size_t)p * a.slot;
+        r0[p] = ld16_volatile(u);
+        r1[p] = ld16_volatile(u + 16);
+        pend |= 1u << p;
       }
     }
+    ll16x2_poll<NR>(base, a.slot, NR, r0, r1, pend, flag, rk.st);
 #pragma unroll
-    for (int p = 0; p < NR; p++) {
-      if (p < n && p != r && vlo(p) + i < vhi(p)) {
-        const uint4 v = ll16x2_finish(rk.scr[r] + ph2 + (size_t)p * a.slot + i * 32, raw0[p], raw1[p], flag, rk.st);
-        store_vec<T>(rk.out[r], vlo(p) + i, v, clo(p), chi(p), 0);
-      }
-    }
+    for (int p = 0; p < NR; p++)
+      if ((pend >> p) & 1u) store_vec<T>(rk.out[r], vlo(p) + i, ll16x2_payload(r0[p], r1[p]), clo(p), chi(p), 0);
   }
+  TS_MARK();
   end_call(rk, e);
+  TS_MARK();
+  TS_DUMP("2pa_ll");
 }
 
 // ---------------------------------------------------------------- K6

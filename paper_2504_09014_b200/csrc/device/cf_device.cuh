@@ -213,6 +213,55 @@ __device__ __forceinline__ uint2 ll16_get(const void* src, uint32_t flag, RankSt
   return make_uint2(v.x, v.z);
 }
 
+// Address of 32-byte LL16 unit i of a batch: slot i of `base` (slots
+// `stride` bytes apart), skipping slot `skip` (the reader's own rank).
+__device__ __forceinline__ const char* ll_unit(const char* base, size_t stride, int skip, int i) {
+  return base + (size_t)(i + (i >= skip ? 1 : 0)) * stride;
+}
+
+// Batched poll of K 32-byte LL16 units (two packets each, at ll_unit(i) and
+// ll_unit(i) + 16) whose first loads r0/r1 the caller already issued.  Every
+// round re-issues the loads of ALL units still unstamped before checking any
+// of them, so waiting for K peers costs one local round trip per round, not
+// one per peer.  `pend` selects the participating units.
+template <int K>
+__device__ __forceinline__ void ll16x2_poll(const char* base, size_t stride, int skip, uint4 (&r0)[K],
+                                            uint4 (&r1)[K], uint32_t pend, uint32_t flag, RankState* st) {
+  auto stamped = [&](int i) {
+    return r0[i].y == flag && r0[i].w == flag && r1[i].y == flag && r1[i].w == flag;
+  };
+#pragma unroll
+  for (int i = 0; i < K; i++)
+    if (((pend >> i) & 1u) && stamped(i)) pend &= ~(1u << i);
+  if (!pend) return;
+  const uint64_t t0 = globaltimer();
+  for (uint32_t it = 1; pend; ++it) {
+#pragma unroll
+    for (int i = 0; i < K; i++) {
+      if ((pend >> i) & 1u) {
+        const char* u = ll_unit(base, stride, skip, i);
+        r0[i] = ld16_volatile(u);
+        r1[i] = ld16_volatile(u + 16);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < K; i++)
+      if (((pend >> i) & 1u) && stamped(i)) pend &= ~(1u << i);
+    if ((it & 255u) == 0 && pend) {
+      if (*(volatile uint32_t*)&st->error != kDevOk) return;
+      if (globaltimer() - t0 > st->timeout_ns) {
+        atomicExch(&st->error, (uint32_t)kDevTimeout);
+        return;
+      }
+    }
+  }
+}
+
+// Payload of a stamped LL16 unit.
+__device__ __forceinline__ uint4 ll16x2_payload(uint4 r0, uint4 r1) {
+  return make_uint4(r0.x, r0.z, r1.x, r1.z);
+}
+
 // ---------------------------------------------------------------- element math
 
 template <typename T> struct Vec;  // 16-byte vector of T <-> f32/i32 accumulators
