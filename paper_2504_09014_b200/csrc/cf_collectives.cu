@@ -124,6 +124,29 @@ __device__ __forceinline__ void store_vec(char* base, size_t v, uint4 val, size_
   st_masked16_ool<sizeof(T)>(p, val, jlo, jhi);
 }
 
+// 8-byte payload units (one LL16 packet each): unit u of a T array of
+// `count` elements; ragged last unit out of line.
+template <typename T>
+__device__ __forceinline__ uint2 load_unit(const char* base, size_t u, size_t count) {
+  constexpr int H = 8 / sizeof(T);
+  const size_t e0 = u * H;
+  if (e0 + H <= count) return ld8(base + u * 8);
+  const int nb = e0 < count ? (int)((count - e0) * sizeof(T)) : 0;
+  const uint4 w = ld_partial16_ool<sizeof(T)>(base + u * 8, nb);
+  return make_uint2(w.x, w.y);
+}
+template <typename T>
+__device__ __forceinline__ void store_unit(char* base, size_t u, uint2 val, size_t count) {
+  constexpr int H = 8 / sizeof(T);
+  const size_t e0 = u * H;
+  if (e0 + H <= count) {
+    st8(base + u * 8, val);
+    return;
+  }
+  const int jhi = e0 < count ? (int)(count - e0) : 0;
+  st_masked16_ool<sizeof(T)>(base + u * 8, make_uint4(val.x, val.y, 0u, 0u), 0, jhi);
+}
+
 // Accumulate NR (runtime n <= NR) 16-byte vectors in order: x[0] first (or a
 // zero accumulator when `zero`), then x[1], x[2], ...  f16/bf16 accumulate in
 // f32 and round once; i32 wraps; f32 is one RNE add per source.
@@ -148,6 +171,17 @@ __device__ __forceinline__ uint4 reduce_vecs(const uint4 (&x)[NR], int n, bool z
     }
   }
   return Vec<T>::store(acc);
+}
+
+// reduce_vecs on 8-byte units (the upper half of each vector is zero and its
+// lanes are dead code).
+template <typename T, int NR>
+__device__ __forceinline__ uint2 reduce_units(const uint2 (&x)[NR], int n) {
+  uint4 w[NR];
+#pragma unroll
+  for (int k = 0; k < NR; k++) w[k] = make_uint4(x[k].x, x[k].y, 0u, 0u);
+  const uint4 res = reduce_vecs<T, NR>(w, n, false);
+  return make_uint2(res.x, res.y);
 }
 
 // ---------------------------------------------------------------- K2 / K3 / K8
@@ -203,66 +237,50 @@ __global__ void __launch_bounds__(512) pull_reduce_kernel(const __grid_constant_
 // slot r of each peer's scratch (parity half e&1), then polls its own n-1
 // slots and reduces in the 1pa order (own input first, peers ascending,
 // cf/collectives.py:156-161).  No semaphores, no fences: the flag travels in
-// the same 16-byte store as the data.  Latency structure: the first input
-// load is issued before the epoch read; the read phase keeps every peer's
-// packets in flight and re-polls all unstamped ones per round
-// (ll16x2_poll), so waiting for n-1 peers costs one round trip per round.
+// the same 16-byte store as the data.  One thread per 8-byte payload unit
+// (= one packet), so a warp's packet stores to a peer cover 512 contiguous
+// bytes.  Latency structure: the first input load is issued before the epoch
+// read; the read phase keeps every peer's packet in flight and re-polls all
+// unstamped ones per round (ll16_poll): waiting for n-1 peers costs one round
+// trip per round, not one per peer.
 template <typename T, int NR>
-__global__ void __launch_bounds__(512, 1) ll_oneshot_kernel(const __grid_constant__ CollArgs a) {
+__global__ void __launch_bounds__(512, 2) ll_oneshot_kernel(const __grid_constant__ CollArgs a) {
   const RankCtx& rk = a.rk[blockIdx.y];
   constexpr int P = NR - 1;
+  constexpr int H = 8 / sizeof(T);
   const int n = a.n, r = rk.rank;
   TS_DECL
   TS_MARK();
-  constexpr int V = Vec<T>::N;
-  const size_t nvec = (a.count + V - 1) / V;
+  const size_t nunit = (a.count + H - 1) / H;
   const size_t stride = (size_t)gridDim.x * blockDim.x;
   const size_t t0 = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const uint4 first = t0 < nvec ? load_vec<T>(rk.in[r], t0, a.count) : make_uint4(0, 0, 0, 0);
+  const uint2 first = t0 < nunit ? load_unit<T>(rk.in[r], t0, a.count) : make_uint2(0u, 0u);
   const uint64_t e = begin_call(rk);
   TS_MARK();
   const uint32_t flag = ll_flag(e);
   const size_t par = (e & 1) * a.half;
 
-  for (size_t v = t0; v < nvec; v += stride) {
-    const uint4 x = v == t0 ? first : load_vec<T>(rk.in[r], v, a.count);
+  for (size_t u = t0; u < nunit; u += stride) {
+    const uint2 x = u == t0 ? first : load_unit<T>(rk.in[r], u, a.count);
 #pragma unroll
-    for (int p = 0; p < NR; p++) {
-      if (p < n && p != r) {
-        char* d = rk.scr[p] + par + (size_t)r * a.slot + v * 32;
-        ll16_put_scoped(d, make_uint2(x.x, x.y), flag, a.gpu_scope);
-        ll16_put_scoped(d + 16, make_uint2(x.z, x.w), flag, a.gpu_scope);
-      }
-    }
+    for (int p = 0; p < NR; p++)
+      if (p < n && p != r) ll16_put_scoped(rk.scr[p] + par + (size_t)r * a.slot + u * 16, x, flag, a.gpu_scope);
   }
   TS_MARK();
-  using A = typename Vec<T>::Acc;
   const uint32_t all = (1u << (n - 1)) - 1u;
-  for (size_t v = t0; v < nvec; v += stride) {
-    const uint4 own = v == t0 ? first : load_vec<T>(rk.in[r], v, a.count);
-    const char* base = rk.scr[r] + par + v * 32;
-    uint4 r0[P], r1[P];
+  for (size_t u = t0; u < nunit; u += stride) {
+    const uint2 own = u == t0 ? first : load_unit<T>(rk.in[r], u, a.count);
+    const char* base = rk.scr[r] + par + u * 16;
+    uint4 pk[P];
 #pragma unroll
-    for (int i = 0; i < P; i++) {
-      if (i < n - 1) {
-        const char* u = ll_unit(base, a.slot, r, i);
-        r0[i] = ld16_volatile(u);
-        r1[i] = ld16_volatile(u + 16);
-      }
-    }
-    ll16x2_poll<P>(base, a.slot, r, r0, r1, all, flag, rk.st);
-    A acc[V];
-    Vec<T>::load(own, acc);
+    for (int i = 0; i < P; i++)
+      if (i < n - 1) pk[i] = ld16_volatile(ll_unit(base, a.slot, r, i));
+    ll16_poll<P>(base, a.slot, r, pk, all, flag, rk.st);
+    uint2 x[NR];
+    x[0] = own;
 #pragma unroll
-    for (int i = 0; i < P; i++) {
-      if (i < n - 1) {
-        A t[V];
-        Vec<T>::load(ll16x2_payload(r0[i], r1[i]), t);
-#pragma unroll
-        for (int j = 0; j < V; j++) acc[j] = acc_add(acc[j], t[j]);
-      }
-    }
-    store_vec<T>(rk.out[r], v, Vec<T>::store(acc), 0, a.count, 0);
+    for (int i = 0; i < P; i++) x[i + 1] = make_uint2(pk[i].x, pk[i].z);
+    store_unit<T>(rk.out[r], u, reduce_units<T, NR>(x, n), a.count);
   }
   TS_MARK();
   end_call(rk, e);
@@ -299,24 +317,24 @@ __global__ void __launch_bounds__(512) ll_twoshot_kernel(const __grid_constant__
   auto vlo = [&](int c) { return clo(c) / V; };
   auto vhi = [&](int c) { return (chi(c) + V - 1) / V; };
   const size_t nvmax = (a.cs + V - 1) / V + 1;   // vectors covering any chunk
-  // Chunk bounds min(c * cs, count) on the 16-byte grid (cs and count
-  // multiples of V, the common case): every vector belongs to exactly one
-  // chunk, so phases 1 and 2 run one vector per thread over the whole buffer
-  // (peer = v / cv) -- all threads busy, one short code path.  Otherwise the
-  // per-chunk loops below handle vectors that straddle two chunks.
-  const bool grid = a.cs % V == 0 && a.count % V == 0;
-  const uint32_t cv = (uint32_t)(a.cs / V);
-  const size_t nvec = (a.count + V - 1) / V;
+  // Chunk bounds min(c * cs, count) on the 8-byte unit grid (cs and count
+  // multiples of H, the common case): every unit belongs to exactly one
+  // chunk, so each phase runs one 8-byte unit (= one packet) per thread over
+  // the whole buffer (peer = u / cu) -- all threads busy, contiguous packet
+  // stores, one short code path.  Otherwise the per-chunk vector loops below
+  // handle 16-byte vectors that straddle two chunks.
+  constexpr int H = 8 / sizeof(T);
+  const bool grid = a.cs % H == 0 && a.count % H == 0;
+  const uint32_t cu = (uint32_t)(a.cs / H);
+  const size_t nunit = a.count / H;
 
   // phase 1: scatter my chunks as packets
   if (grid) {
-    for (size_t v = t0; v < nvec; v += stride) {
-      const uint32_t p = (uint32_t)v / cv, i = (uint32_t)v - p * cv;
+    for (size_t u = t0; u < nunit; u += stride) {
+      const uint32_t p = (uint32_t)u / cu, i = (uint32_t)u - p * cu;
       if ((int)p == r) continue;
-      const uint4 x = load_vec<T>(rk.in[r], v, a.count);
-      char* d = rk.scr[p] + ph1 + (size_t)r * a.slot + (size_t)i * 32;
-      ll16_put_scoped(d, make_uint2(x.x, x.y), flag, a.gpu_scope);
-      ll16_put_scoped(d + 16, make_uint2(x.z, x.w), flag, a.gpu_scope);
+      ll16_put_scoped(rk.scr[p] + ph1 + (size_t)r * a.slot + (size_t)i * 16, ld8(rk.in[r] + u * 8), flag,
+                      a.gpu_scope);
     }
   } else for (size_t i = t0; i < nvmax; i += stride) {   // every peer's input vector loaded first
     uint4 x[NR];
@@ -334,9 +352,29 @@ __global__ void __launch_bounds__(512) ll_twoshot_kernel(const __grid_constant__
   }
   TS_MARK();
   // reduce my chunk (owner first, peers ascending), store, broadcast as packets
-  {
+  const uint32_t all = (1u << (n - 1)) - 1u;
+  if (grid) {
+    const size_t u0 = min((size_t)r * cu, nunit), nu = min(u0 + cu, nunit) - u0;
+    for (size_t i = t0; i < nu; i += stride) {
+      const uint2 own = ld8(rk.in[r] + (u0 + i) * 8);
+      const char* base = rk.scr[r] + ph1 + i * 16;
+      uint4 pk[P];
+#pragma unroll
+      for (int k = 0; k < P; k++)
+        if (k < n - 1) pk[k] = ld16_volatile(ll_unit(base, a.slot, r, k));
+      ll16_poll<P>(base, a.slot, r, pk, all, flag, rk.st);
+      uint2 x[NR];
+      x[0] = own;
+#pragma unroll
+      for (int k = 0; k < P; k++) x[k + 1] = make_uint2(pk[k].x, pk[k].z);
+      const uint2 res = reduce_units<T, NR>(x, n);
+      st8(rk.out[r] + (u0 + i) * 8, res);
+#pragma unroll
+      for (int p = 0; p < NR; p++)
+        if (p < n && p != r) ll16_put_scoped(rk.scr[p] + ph2 + (size_t)r * a.slot + i * 16, res, flag, a.gpu_scope);
+    }
+  } else {
     const size_t b = vlo(r), nv = vhi(r) > b ? vhi(r) - b : 0;
-    const uint32_t all = (1u << (n - 1)) - 1u;
     for (size_t i = t0; i < nv; i += stride) {
       const uint4 own = load_vec<T>(rk.in[r], b + i, a.count);
       const char* base = rk.scr[r] + ph1 + i * 32;
@@ -370,13 +408,13 @@ __global__ void __launch_bounds__(512) ll_twoshot_kernel(const __grid_constant__
   TS_MARK();
   // phase 2: decode the peers' reduced chunks
   if (grid) {
-    for (size_t v = t0; v < nvec; v += stride) {
-      const uint32_t p = (uint32_t)v / cv, i = (uint32_t)v - p * cv;
+    for (size_t u = t0; u < nunit; u += stride) {
+      const uint32_t p = (uint32_t)u / cu, i = (uint32_t)u - p * cu;
       if ((int)p == r) continue;
-      const char* u = rk.scr[r] + ph2 + (size_t)p * a.slot + (size_t)i * 32;
-      uint4 r0[1] = {ld16_volatile(u)}, r1[1] = {ld16_volatile(u + 16)};
-      ll16x2_poll<1>(u, 0, 1, r0, r1, 1u, flag, rk.st);
-      store_vec<T>(rk.out[r], v, ll16x2_payload(r0[0], r1[0]), 0, a.count, 0);
+      const char* src = rk.scr[r] + ph2 + (size_t)p * a.slot + (size_t)i * 16;
+      uint4 pk[1] = {ld16_volatile(src)};
+      ll16_poll<1>(src, 0, 1, pk, 1u, flag, rk.st);
+      st8(rk.out[r] + u * 8, make_uint2(pk[0].x, pk[0].z));
     }
   } else for (size_t i = t0; i < nvmax; i += stride) {   // all peers' packets of vector i in flight
     const char* base = rk.scr[r] + ph2 + i * 32;

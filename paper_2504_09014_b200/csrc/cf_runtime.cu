@@ -733,7 +733,7 @@ extern "C" cfStatus cfAllReduce(cfComm_t c, const void* const* send, void* const
         return fail(CF_E_BAD_SIZE, "1pa: %zu bytes exceed the LL capacity %zu", bytes, c->cfg.ll_max_bytes);
       j.kind = kLL1;
       j.order = kLead;
-      j.work = ceil_div(count, V);
+      j.work = ceil_div(bytes, (size_t)8);   // one thread per 8-byte packet unit
       break;
     case CF_ALGO_1PA_HB:
       for (size_t li = 0; li < c->local.size(); li++)
@@ -766,7 +766,7 @@ extern "C" cfStatus cfAllReduce(cfComm_t c, const void* const* send, void* const
       j.slot = c->lay.half / (2 * n) / 256 * 256;
       if (32 * (ceil_div(j.cs, V) + 1) > j.slot)
         return fail(CF_E_BAD_SIZE, "2pa_ll: %zu bytes exceed the LL capacity", bytes);
-      j.work = ceil_div(j.cs, V) + 1;
+      j.work = ceil_div(bytes, (size_t)8);    // phases 1 / 2: one thread per 8-byte packet unit
       break;
     }
     default:

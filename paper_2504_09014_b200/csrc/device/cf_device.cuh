@@ -122,6 +122,14 @@ __device__ __forceinline__ void st16_volatile(void* p, uint4 v) {
   asm volatile("st.volatile.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y),
                "r"(v.z), "r"(v.w) : "memory");
 }
+__device__ __forceinline__ uint2 ld8(const void* p) {
+  uint2 v;
+  asm volatile("ld.global.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void st8(void* p, uint2 v) {
+  asm volatile("st.global.v2.u32 [%0], {%1,%2};" ::"l"(p), "r"(v.x), "r"(v.y) : "memory");
+}
 __device__ __forceinline__ uint2 ld8_volatile(const void* p) {
   uint2 v;
   asm volatile("ld.volatile.global.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p) : "memory");
@@ -247,6 +255,33 @@ __device__ __forceinline__ void ll16x2_poll(const char* base, size_t stride, int
 #pragma unroll
     for (int i = 0; i < K; i++)
       if (((pend >> i) & 1u) && stamped(i)) pend &= ~(1u << i);
+    if ((it & 255u) == 0 && pend) {
+      if (*(volatile uint32_t*)&st->error != kDevOk) return;
+      if (globaltimer() - t0 > st->timeout_ns) {
+        atomicExch(&st->error, (uint32_t)kDevTimeout);
+        return;
+      }
+    }
+  }
+}
+
+// Batched poll of K single LL16 packets (8 payload bytes each) at
+// ll_unit(base, stride, skip, i); same round structure as ll16x2_poll.
+template <int K>
+__device__ __forceinline__ void ll16_poll(const char* base, size_t stride, int skip, uint4 (&pk)[K],
+                                          uint32_t pend, uint32_t flag, RankState* st) {
+#pragma unroll
+  for (int i = 0; i < K; i++)
+    if (((pend >> i) & 1u) && pk[i].y == flag && pk[i].w == flag) pend &= ~(1u << i);
+  if (!pend) return;
+  const uint64_t t0 = globaltimer();
+  for (uint32_t it = 1; pend; ++it) {
+#pragma unroll
+    for (int i = 0; i < K; i++)
+      if ((pend >> i) & 1u) pk[i] = ld16_volatile(ll_unit(base, stride, skip, i));
+#pragma unroll
+    for (int i = 0; i < K; i++)
+      if (((pend >> i) & 1u) && pk[i].y == flag && pk[i].w == flag) pend &= ~(1u << i);
     if ((it & 255u) == 0 && pend) {
       if (*(volatile uint32_t*)&st->error != kDevOk) return;
       if (globaltimer() - t0 > st->timeout_ns) {
