@@ -12,7 +12,8 @@ import os
 from .errors import raise_status
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libcf.so")
+# CF_LIB_PATH: load another in-tree build of libcf (A/B diagnostics)
+LIB_PATH = os.environ.get("CF_LIB_PATH") or os.path.join(_HERE, "libcf.so")
 
 CF_MAX_RANKS = 8
 CF_MAX_BLOCKS = 1024

@@ -15,18 +15,10 @@
 // handled with guarded element-wise loads and masked stores.
 #include <cstdio>
 #include "cf_kernels.cuh"
+#include "cf_ts.cuh"
 
 namespace cf {
 
-#ifdef CF_TS
-#define TS_DECL uint64_t ts_[8]; int tsn_ = 0;
-#define TS_MARK() do { if (threadIdx.x == 0 && blockIdx.x == 0) ts_[tsn_] = globaltimer(); tsn_++; } while (0)
-#define TS_DUMP(nm) do { if (threadIdx.x == 0 && blockIdx.x == 0) { printf("TS %s rank %d t0 %llu", nm, rk.rank, (unsigned long long)ts_[0]); for (int q_ = 1; q_ < tsn_; q_++) printf(" +%llu", (unsigned long long)(ts_[q_] - ts_[0])); printf("\n"); } } while (0)
-#else
-#define TS_DECL
-#define TS_MARK()
-#define TS_DUMP(nm)
-#endif
 
 // ---------------------------------------------------------------- call bracket
 
@@ -285,7 +277,7 @@ __global__ void __launch_bounds__(512, 2) ll_oneshot_kernel(const __grid_constan
   TS_MARK();
   end_call(rk, e);
   TS_MARK();
-  TS_DUMP("1pa");
+  TS_DUMP("1pa", rk.rank);
 }
 
 // ---------------------------------------------------------------- K4
@@ -437,7 +429,7 @@ __global__ void __launch_bounds__(512) ll_twoshot_kernel(const __grid_constant__
   TS_MARK();
   end_call(rk, e);
   TS_MARK();
-  TS_DUMP("2pa_ll");
+  TS_DUMP("2pa_ll", rk.rank);
 }
 
 // ---------------------------------------------------------------- K6

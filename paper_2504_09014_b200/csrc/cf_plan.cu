@@ -636,9 +636,12 @@ cfStatus load(cfComm* c, const char* json, size_t len, int dtype_override, cfPla
   // CTAs per program: enough threads for the largest data op, all programs
   // of a device co-resident.
   long long max_bytes = 0;
+  bool packets = false;   // LL plans: packet ops run one 8-byte payload unit per thread
   for (auto& h : hops)
-    for (auto& o : h)
+    for (auto& o : h) {
       if (is_data(o)) max_bytes = std::max(max_bytes, o.size * es);
+      packets |= o.code == D_PUT_PACKETS || o.code == D_READ_PACKETS;
+    }
   const void* kernel = plan_kernel_for(pl->dtype);
   int cap = INT32_MAX, progs_per_dev_max = 1;
   pl->mp = c->multiprocess;
@@ -666,8 +669,10 @@ cfStatus load(cfComm* c, const char* json, size_t len, int dtype_override, cfPla
     }
   }
   if (cap < 1) return fail(CF_E_CONFIG, "plan has more programs per device than co-resident CTAs");
-  // one 16-byte vector per thread per source and CTA: latency, not issue, bound
-  const long long per_cta = (long long)pl->threads * 16;
+  // one 16-byte vector (LL plans: one 8-byte packet unit) per thread per
+  // source and CTA: latency, not issue, bound (1pa plan b=1 11.6 -> 9.5 us)
+  long long per_cta = (long long)pl->threads * (packets ? 8 : 16);
+  if (const char* ev = getenv("CF_PLAN_BYTES_PER_CTA")) per_cta = std::max(1LL, atoll(ev));   // diagnostic
   pl->K = (int)std::max(1LL, std::min<long long>({(max_bytes + per_cta - 1) / per_cta, (long long)cap, 32LL}));
   const int K = pl->K;
 

@@ -17,6 +17,8 @@
 // rank's buffers after it returns), so plan buffers are reused across calls
 // without host work, and LL flags are re-stamped with the call epoch.
 #include "cf_plan.h"
+#define TS_CTA_COND (blockIdx.x % a.K == 0)
+#include "cf_ts.cuh"
 
 namespace cf {
 namespace plan {
@@ -417,6 +419,8 @@ __device__ __forceinline__ void resolve_window(const PlanArgs& a, DevOp* ops, in
 template <typename T>
 __global__ void __launch_bounds__(512) plan_kernel(const __grid_constant__ PlanArgs a) {
   const int pid = blockIdx.x / a.K, j = blockIdx.x % a.K;
+  TS_DECL
+  TS_MARK();
   int rank, pb, pe;
   if (a.prog_in_param) {
     const int4 t = a.prog_tab[pid];
@@ -452,6 +456,7 @@ __global__ void __launch_bounds__(512) plan_kernel(const __grid_constant__ PlanA
   if (pb < pe) stage(pb, min(pb + a.window, pe));
   __syncthreads();
   const uint64_t e = s_e;
+  TS_MARK();
   if (a.has_prologue) prologue(a, rank);
   // rank barriers are numbered consecutively across calls (monotonic counters)
   const uint64_t per_call = (uint64_t)(a.entry_barrier + a.exit_barrier);
@@ -467,6 +472,7 @@ __global__ void __launch_bounds__(512) plan_kernel(const __grid_constant__ PlanA
     }
     resolve_window(a, s_ops, w1 - w0, e, s_io);
     __syncthreads();
+    TS_MARK();
   for (int i = w0; i < w1; i++) {
     const DevOp& op = s_ops[i - w0];
     switch (op.code) {
@@ -512,6 +518,7 @@ __global__ void __launch_bounds__(512) plan_kernel(const __grid_constant__ PlanA
       default:
         break;
     }
+    TS_MARK();
   }
   }
   // requests still in flight complete before the call ends (their data and
@@ -526,6 +533,8 @@ __global__ void __launch_bounds__(512) plan_kernel(const __grid_constant__ PlanA
       *(volatile uint64_t*)&rs->epoch = e;
     }
   }
+  TS_MARK();
+  TS_DUMP("plan", rank);
 }
 
 const void* plan_kernel_for(int dtype) {
