@@ -551,6 +551,15 @@ __device__ __forceinline__ void cta_slice(size_t lo, size_t hi, int b, int B, si
 // Values are epoch * kPhases + sequence; the value epoch * kPhases itself is
 // the receiver's "entered this call" ready mark, so slots are never
 // overwritten while the previous call still reads them.
+// Before a ring link's data release: the CTA's slot stores are ordered before
+// thread 0's st.release by the preceding __syncthreads (bar.sync is a
+// CTA-scope synchronization and release is cumulative), which is enough at
+// .gpu scope; across GPUs the full system fence is kept.  (Dropping the
+// .gpu fence: ring RS 256 MiB 2.30 -> 2.14 ms.)
+__device__ __forceinline__ void ring_publish(bool gpu) {
+  if (!gpu) __threadfence_system();
+}
+
 struct RingLink {
   char* my_slots;         // slots I receive into (from prev)
   char* nx_slots;         // slots I send into (next's)
@@ -581,10 +590,31 @@ struct RingLink {
   __device__ void send_done() {
     __syncthreads();
     if (threadIdx.x == 0) {
-      fence_publish(gpu);
+      ring_publish(gpu);
       st_release(data_out, base + qs + 1, gpu);
     }
     qs++;
+  }
+  // One barrier for both waits of a step: thread 0 polls the incoming data,
+  // thread 32 (another warp) the send credit, concurrently.
+  __device__ void wait_both(bool rcv, bool snd) {
+    if (rcv && threadIdx.x == 0) wait_geq(data_in, base + qr + 1, st, gpu);
+    if (snd && threadIdx.x == 32) wait_geq(ack_in, base + (qs >= kRingSlots ? qs - kRingSlots + 1 : 0), st, gpu);
+    __syncthreads();
+  }
+  // One barrier for both completions of a step: free the received slot, then
+  // publish the sent one.
+  __device__ void done_both(bool rcv, bool snd) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      if (rcv) st_release(ack_out, base + qr + 1, gpu);
+      if (snd) {
+        ring_publish(gpu);
+        st_release(data_out, base + qs + 1, gpu);
+      }
+    }
+    if (rcv) qr++;
+    if (snd) qs++;
   }
 };
 
@@ -638,6 +668,11 @@ __device__ X AccVec<T>::bits_to(uint32_t u) {
   else return (X)u;
 }
 
+// 16-byte vectors of T per thread per ring unit prefetched into registers
+// (a 32 KiB unit of f32 partials covers 8192 elements: 4 bf16 / 8 f32 vectors
+// per thread at 256 threads).
+constexpr int kRingPre = 8;
+
 // Ring ReduceScatter (build_ring_rs, cf/collectives.py:30-79) and, with
 // `push`, the two-phase ring AllReduce (build_2pr, :107-136).  Step s sends
 // the partial of chunk (r - s) mod n to the next rank; the partial that
@@ -656,7 +691,6 @@ __global__ void __launch_bounds__(512) ring_kernel(const __grid_constant__ CollA
   const T* x = reinterpret_cast<const T*>(rk.in[r]);
   T* y = reinterpret_cast<T*>(rk.out[r]);
   constexpr size_t UA = kRingSlot / sizeof(A);   // elements per unit, RS phase
-  constexpr size_t UT = kRingSlot / sizeof(T);   // elements per unit, AG phase
   auto chunk = [&](int c, size_t& s0, size_t& s1) {
     const size_t lo = min((size_t)c * a.cs, a.count), hi = min(lo + a.cs, a.count);
     cta_slice(lo, hi, b, B, V, s0, s1);
@@ -666,17 +700,18 @@ __global__ void __launch_bounds__(512) ring_kernel(const __grid_constant__ CollA
   // so with kRingSlots credits the ring never stalls on a full slot ring.
   // Sender and receiver skip the same (chunk, unit) pairs, so the per-link
   // sequence numbers stay aligned.
-  size_t ka = 0, kt = 0;
+  size_t ka = 0;
   for (int c = 0; c < n; c++) {
     size_t s0, s1;
     chunk(c, s0, s1);
     ka = max(ka, (s1 - s0 + UA - 1) / UA);
-    kt = max(kt, (s1 - s0 + UT - 1) / UT);
   }
   const size_t shift = a.rs_shift ? min((size_t)r * a.cs, a.count) : 0;
   // every chunk starts on the 16-byte grid: whole-vector loops (chunk ends,
   // CTA slices and units are then multiples of V as well)
   const bool vec = a.cs % V == 0 && a.count % V == 0 && (((uintptr_t)x | (uintptr_t)y) & 15) == 0;
+  TS_DECL
+  TS_MARK();
   for (size_t k = 0; k < ka; k++) {
     // ReduceScatter: step s adds the own contribution to chunk (r - s)
     for (int s = 0; s < n; s++) {
@@ -685,6 +720,42 @@ __global__ void __launch_bounds__(512) ring_kernel(const __grid_constant__ CollA
       const size_t u0 = s0 + k * UA;
       if (u0 >= s1) continue;
       const size_t u1 = min(u0 + UA, s1);
+      if (vec && blockDim.x * V * kRingPre >= UA) {
+        // whole 16-byte vectors of T, the own contribution prefetched into
+        // registers before the waits (its HBM latency overlaps the flag
+        // round trip); the slots carry V accumulators per vector
+        uint4 xv[kRingPre];
+#pragma unroll
+        for (int m = 0; m < kRingPre; m++) {
+          const size_t i = u0 + ((size_t)m * blockDim.x + threadIdx.x) * V;
+          if (i < u1) xv[m] = ld16(x + i);
+        }
+        const bool tsk = k == 10 && (s == 3 || s == 4);
+        if (tsk) TS_MARK();
+        L.wait_both(s > 0, true);
+        if (tsk) TS_MARK();
+        const A* in_slot = reinterpret_cast<const A*>(L.recv_slot());
+        A* out_slot = reinterpret_cast<A*>(L.send_slot());
+#pragma unroll
+        for (int m = 0; m < kRingPre; m++) {
+          const size_t i = u0 + ((size_t)m * blockDim.x + threadIdx.x) * V;
+          if (i < u1) {
+            A v[V];
+            Vec<T>::load(xv[m], v);
+            if (s > 0) {
+              A p[V];
+              AccVec<T>::load(in_slot + (i - u0), p);
+#pragma unroll
+              for (int j = 0; j < (int)V; j++) v[j] = acc_add(p[j], v[j]);
+            }
+            AccVec<T>::store(out_slot + (i - u0), v);
+          }
+        }
+        if (tsk) TS_MARK();
+        L.done_both(s > 0, true);
+        if (tsk) TS_MARK();
+        continue;
+      }
       if (s > 0) L.recv_wait();
       L.send_wait();
       const A* in_slot = reinterpret_cast<const A*>(L.recv_slot());
@@ -735,42 +806,42 @@ __global__ void __launch_bounds__(512) ring_kernel(const __grid_constant__ CollA
     }
   }
   if (a.push) {
-    // AllGather: step t forwards unit k of chunk (r - t) and receives unit k
-    // of chunk (r - 1 - t), which step t + 1 forwards
-    __syncthreads();
-    for (size_t k = 0; k < kt; k++) {
-      for (int t = 0; t < n - 1; t++) {
-        size_t a0, a1, b0, b1;
-        chunk((r - t + n) % n, a0, a1);
-        chunk((r - 1 - t + n) % n, b0, b1);
-        const size_t us0 = a0 + k * UT, ur0 = b0 + k * UT;
-        if (us0 < a1) {
-          const size_t u1 = min(us0 + UT, a1);
-          L.send_wait();
-          T* out_slot = reinterpret_cast<T*>(L.send_slot());
-          if (vec) {
-            for (size_t i = us0 + threadIdx.x * V; i < u1; i += (size_t)blockDim.x * V)
-              st16(out_slot + (i - us0), ld16(y + i));
-          } else {
-            for (size_t i = us0 + threadIdx.x; i < u1; i += blockDim.x) out_slot[i - us0] = y[i];
-          }
-          L.send_done();
+    // AllGather (build_ring_ag's forwarding, cf/collectives.py:82-104): step t
+    // stores this CTA's slice of chunk (r - t) straight into the next rank's
+    // output and signals; chunk (r - 1 - t) lands in mine from the previous
+    // rank.  Each output range is written once per call, so no slots or
+    // credits -- but the next rank must have consumed every ReduceScatter
+    // unit I sent it: then it no longer reads its input, which its output may
+    // alias (in place), and it entered this call.
+    const int next = (r + 1) % n;
+    T* yn = reinterpret_cast<T*>(rk.out[next]);
+    if (threadIdx.x == 0) wait_geq(L.ack_in, L.base + L.qs, rk.st, L.gpu);
+    for (int t = 0; t < n - 1; t++) {
+      size_t s0, s1;
+      chunk((r - t + n) % n, s0, s1);
+      __syncthreads();
+      if (vec) {   // 4 vectors in flight per thread
+        const size_t step = (size_t)blockDim.x * V;
+        size_t i = s0 + threadIdx.x * V;
+        for (; i + 3 * step < s1; i += 4 * step) {
+          const uint4 w0 = ld16(y + i), w1 = ld16(y + i + step), w2 = ld16(y + i + 2 * step),
+                      w3 = ld16(y + i + 3 * step);
+          st16(yn + i, w0);
+          st16(yn + i + step, w1);
+          st16(yn + i + 2 * step, w2);
+          st16(yn + i + 3 * step, w3);
         }
-        if (ur0 < b1) {
-          const size_t u1 = min(ur0 + UT, b1);
-          L.recv_wait();
-          const T* in_slot = reinterpret_cast<const T*>(L.recv_slot());
-          if (vec) {
-            for (size_t i = ur0 + threadIdx.x * V; i < u1; i += (size_t)blockDim.x * V)
-              st16(y + i, ld16(in_slot + (i - ur0)));
-          } else {
-            for (size_t i = ur0 + threadIdx.x; i < u1; i += blockDim.x) y[i] = in_slot[i - ur0];
-          }
-          L.recv_done();
-        }
+        for (; i < s1; i += step) st16(yn + i, ld16(y + i));
+      } else {
+        for (size_t i = s0 + threadIdx.x; i < s1; i += blockDim.x) yn[i] = y[i];
       }
+      L.send_done();
+      L.recv_wait();   // chunk (r - 1 - t) landed in my output
+      L.qr++;
     }
   }
+  TS_MARK();
+  TS_DUMP("ring", rk.rank);
   end_call(rk, e);
 }
 

@@ -571,7 +571,8 @@ cfStatus launch(cfComm* c, const Job& j, int dtype, const void* const* send, voi
                 const cudaStream_t* streams, const NormBufs* nb = nullptr) {
   // one-process-per-GPU: peers' buffers come from the registration table
   const bool need_in = j.kind == kPull || j.kind == kNorm;
-  const bool need_out = j.kind == kGather || j.kind == kRingGather || ((j.kind == kPull || j.kind == kNorm) && j.push);
+  const bool need_out = j.kind == kGather || j.kind == kRingGather ||
+                        ((j.kind == kPull || j.kind == kNorm || j.kind == kRing) && j.push);
   const bool need_out2 = j.kind == kNorm && j.push;
   const Registration* reg_in = nullptr;
   const Registration* reg_out = nullptr;
@@ -590,7 +591,13 @@ cfStatus launch(cfComm* c, const Job& j, int dtype, const void* const* send, voi
   DeviceGuard guard;
   const void* kernel = collective_kernel(j.kind, dtype, c->nranks);
   if (!kernel) return fail(CF_E_INTERNAL, "no kernel for kind %d dtype %d", j.kind, dtype);
-  const int threads = c->cfg.threads;
+  // Ring links are latency chains (every step waits for the previous rank's
+  // step): smaller CTAs give each rank up to kRingCtas independent links.
+  const bool ring = j.kind == kRing || j.kind == kRingGather;
+#ifndef CF_RING_THREADS
+#define CF_RING_THREADS 256
+#endif
+  const int threads = j.kind == kRing ? std::min(c->cfg.threads, CF_RING_THREADS) : c->cfg.threads;
   for (size_t gi = 0; gi < c->groups.size(); gi++) {
     const auto& g = c->groups[gi];
     const int dev = c->local[g[0]].dev;
@@ -645,7 +652,7 @@ cfStatus launch(cfComm* c, const Job& j, int dtype, const void* const* send, voi
       }
     }
     int mb = max_blocks_per_rank(c, kernel, (int)gi, threads);
-    if (j.kind == kRing || j.kind == kRingGather) mb = std::min(mb, kRingCtas);   // ring slot region
+    if (ring) mb = std::min(mb, kRingCtas);   // ring slot region
     int blocks = (int)std::min<size_t>((size_t)mb, std::max<size_t>(1, ceil_div(j.work, (size_t)threads)));
     if (j.blocks) blocks = std::min(mb, j.blocks);
     CF_TRY(join_streams(c, (int)gi, streams, false));

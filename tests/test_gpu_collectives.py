@@ -119,6 +119,32 @@ def test_repeated_calls_reuse_scratch_and_semaphores():
     w.check_device_error()
 
 
+@pytest.mark.parametrize("elems", [4096, 300000, 1 << 20])
+def test_allreduce_in_place_vs_oracle(elems):
+    """send == recv: every in-place-capable AllReduce kernel (the 2PR AllGather
+    phase stores straight into the next rank's buffer, which is also its
+    input) returns the oracle's bits."""
+    import torch
+    from paper_2504_09014_b200 import collectives as C
+    from paper_2504_09014_b200 import _lib
+    n = 8
+    w = world(n)
+    ins = gen_inputs(n, elems, "bf16", "normal", 900 + elems % 89)
+    for algo in ("2pa", "2pr", "1pa", "2pa_ll"):
+        if algo in ("1pa", "2pa_ll") and elems > (1 << 18):
+            continue
+        want = oracle.allreduce(ins, "2pa" if algo == "2pa_ll" else algo, "bf16")
+        for rep in range(2):   # twice: the second call reuses slots / flags
+            bufs = [torch.from_numpy(x.view(np.int16)).to(w.device(r)).view(torch.bfloat16)
+                    for r, x in enumerate(ins)]
+            C.run("allreduce", bufs, bufs, elems, "bf16", _lib.ALGOS[algo], w)
+            w.synchronize()
+            for r in range(n):
+                got = bufs[r].view(torch.int16).cpu().numpy().view(np.uint16)
+                assert np.array_equal(got, want[r]), (algo, rep, r)
+    w.check_device_error()
+
+
 def test_large_allreduce_property():
     """Size-independent check at a large size: integer-valued bf16 sums are exact."""
     import torch
