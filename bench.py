@@ -490,6 +490,21 @@ def multi_sweep(comm, dev, world, send, recv):
     br = torch.empty_like(bs)
     comm.register(bs)
     comm.register(br)
+    st = torch.cuda.current_stream(dev)
+    iters = 10
+
+    def eager(fn):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(iters):
+            fn()
+        e1.record(st)
+        e1.synchronize()
+        return e0.elapsed_time(e1) / 1e3 / iters
+
     for nb in [KiB << (2 * i) for i in range(11)]:
         if nb > big:
             break
@@ -497,26 +512,49 @@ def multi_sweep(comm, dev, world, send, recv):
         x, y = bs[:cnt], br[:cnt]
         iters = 50 if nb <= MiB else 10
         t_graph = time_graph(dev, lambda: comm.all_reduce(x, y, algo="auto"), iters, 3)
-        st = torch.cuda.current_stream(dev)
-
-        def eager(fn):
-            for _ in range(3):
-                fn()
-            torch.cuda.synchronize(dev)
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(st)
-            for _ in range(iters):
-                fn()
-            e1.record(st)
-            e1.synchronize()
-            return e0.elapsed_time(e1) / 1e3 / iters
-
         t_eager = eager(lambda: comm.all_reduce(x, y, algo="auto"))
         row = {"bytes": nb, "cf_graph_s": t_graph, "cf_eager_s": t_eager}
         if nccl is not None:
             z = y.clone()
             row["nccl_eager_s"] = eager(lambda: dist.all_reduce(z, group=nccl))
         rows.append(row)
+    # C2 / RS: AllGather (S = output bytes) and ReduceScatter (S = input bytes)
+    # over the same registered buffers, libcf (auto) graph vs NCCL eager
+    for nb in [KiB << (2 * i) for i in range(11)]:
+        if nb > big or nb // 2 < world:
+            continue
+        cnt = nb // 2 // world * world
+        shard = cnt // world
+        iters = 50 if nb <= MiB else 10
+        for kind in ("allgather", "reducescatter"):
+            if kind == "allgather":
+                x, y = bs[:shard], br[:cnt]
+                fn = lambda: comm.all_gather(x, y, algo="auto")  # noqa: E731
+            else:
+                x, y = bs[:cnt], br[:shard]
+                fn = lambda: comm.reduce_scatter(x, y, algo="auto")  # noqa: E731
+            row = {"bytes": cnt * 2, "kind": kind, "cf_graph_s": time_graph(dev, fn, iters, 3)}
+            if nccl is not None:
+                zx, zy = x.clone(), y.clone()
+                if kind == "allgather":
+                    row["nccl_eager_s"] = eager(lambda: dist.all_gather_into_tensor(zy, zx, group=nccl))
+                else:
+                    row["nccl_eager_s"] = eager(lambda: dist.reduce_scatter_tensor(zy, zx, group=nccl))
+            rows.append(row)
+    # NVLS (switch_2pa, multimem ld_reduce / st) when the box builds a multicast object
+    nvls = False
+    try:
+        nvls = comm.setup_nvls()
+    except Exception as e:   # report, never fail the bench
+        rows.append({"bytes": 0, "kind": "nvls", "error": f"{type(e).__name__}: {e}"[:200]})
+    if nvls:
+        for nb in [MiB << (2 * i) for i in range(6)]:
+            if nb > big:
+                break
+            cnt = nb // 2
+            x, y = bs[:cnt], br[:cnt]
+            rows.append({"bytes": nb, "kind": "nvls", "cf_graph_s": time_graph(
+                dev, lambda: comm.all_reduce(x, y, algo="switch_2pa"), 10, 3)})
     comm.deregister(bs)
     comm.deregister(br)
     del bs, br
@@ -536,6 +574,34 @@ def multi_sweep(comm, dev, world, send, recv):
             rt.close()
     comm.check_device_error()
     return rows, (None if nccl is not None else nccl_err)
+
+
+def gather_max_over_ranks(t_local, e2e_local, rows_local, world, group=None):
+    """All ranks: gather every rank's step time, e2e time and sweep rows
+    (torch.distributed object all-gather over the bootstrap group) and reduce
+    each time to its max over ranks; busbw per row uses the collective's bus
+    factor (AllReduce 2(n-1)/n, AllGather / ReduceScatter (n-1)/n)."""
+    import torch.distributed as dist
+    times = [None] * world
+    dist.all_gather_object(times, (t_local, e2e_local, rows_local), group=group)
+    t = max(x[0] for x in times)
+    te = max(x[1] for x in times)
+    sweep = []
+    for i, row in enumerate(rows_local):
+        nb = row["bytes"]
+        kind = row.get("kind", "allreduce")
+        out = {"bytes": nb}
+        for k2 in ("plan", "batch", "kind", "error"):
+            if k2 in row:
+                out[k2] = row[k2]
+        for key in ("cf_graph_s", "cf_eager_s", "nccl_eager_s", "cf_plan_graph_s"):
+            if key in row:
+                tk = max(x[2][i][key] for x in times)   # max over ranks
+                bw = busbw(nb, tk, world) if kind in ("allreduce", "nvls") else \
+                    (nb / tk / 1e9 * (world - 1) / world if tk > 0 else 0.0)
+                out[key[:-2]] = {"us": round(tk * 1e6, 2), "busbw": round(bw, 2)}
+        sweep.append(out)
+    return t, te, sweep
 
 
 def run_multi_gpu(args):
@@ -589,22 +655,7 @@ def run_multi_gpu(args):
         if it:
             e2e_local.append(time.perf_counter() - t0)
     rows_local, nccl_err = multi_sweep(comm, dev, world, send, recv)
-    times = [None] * world
-    dist.all_gather_object(times, (t_local, float(np.mean(e2e_local)), rows_local))
-    t = max(x[0] for x in times)
-    te = max(x[1] for x in times)
-    sweep = []
-    for i, row in enumerate(rows_local):
-        nb = row["bytes"]
-        out = {"bytes": nb}
-        for k2 in ("plan", "batch"):
-            if k2 in row:
-                out[k2] = row[k2]
-        for key in ("cf_graph_s", "cf_eager_s", "nccl_eager_s", "cf_plan_graph_s"):
-            if key in row:
-                tk = max(x[2][i][key] for x in times)   # max over ranks
-                out[key[:-2]] = {"us": round(tk * 1e6, 2), "busbw": round(busbw(nb, tk, world), 2)}
-        sweep.append(out)
+    t, te, sweep = gather_max_over_ranks(t_local, float(np.mean(e2e_local)), rows_local, world)
     if rank == 0:
         value = busbw(HEAD_BYTES, t, world)
         print(json.dumps({
@@ -625,8 +676,9 @@ def run_multi_gpu(args):
                     "ms_per_step": round(te * 1e3, 3),
                     "api": "Communicator.all_reduce_host (cfAllReduceHostStaged), pinned host tensors"},
             "gpu_launches": args.steps, "clocks": clk.summary(),
-            "sweep": {"config": "AllReduce bf16, libcf (auto) in a CUDA graph and eager vs NCCL eager "
-                                "(torch.distributed, comparison only); latency = max over ranks",
+            "sweep": {"config": "bf16 AllReduce (+ C5 DSL plans, AllGather, ReduceScatter, NVLS when the "
+                                "box builds a multicast object), libcf (auto) in a CUDA graph and eager vs "
+                                "NCCL eager (torch.distributed, comparison only); latency = max over ranks",
                       "nccl_error": nccl_err, "rows": sweep}}))
     comm.close()
     dist.destroy_process_group()

@@ -31,6 +31,41 @@ def all_gather_bytes(blob: bytes, group=None) -> list:
     return [bytes(o.cpu().numpy().tobytes()) for o in out]
 
 
+def share_fd(fd, rank: int, nranks: int, group=None) -> int:
+    """Collective: rank 0 passes its file descriptor `fd` to every other rank
+    of the group (same host) over a Unix-domain socket with SCM_RIGHTS; the
+    socket path travels through the bootstrap group.  Returns the fd valid in
+    this process (rank 0: its own; others: a new descriptor to close)."""
+    import os
+    import socket
+    import tempfile
+    import torch.distributed as dist
+    path, srv = None, None
+    if rank == 0:
+        path = os.path.join(tempfile.mkdtemp(prefix="cf_fd_"), "sock")
+        srv = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+        srv.bind(path)
+        srv.listen(max(1, nranks))
+    box = [path]
+    dist.broadcast_object_list(box, src=0, group=group)
+    if rank == 0:
+        for _ in range(nranks - 1):
+            conn, _ = srv.accept()
+            socket.send_fds(conn, [b"f"], [fd])
+            conn.close()
+        srv.close()
+        dist.barrier(group=group)
+        os.unlink(path)
+        os.rmdir(os.path.dirname(path))
+        return fd
+    cli = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+    cli.connect(box[0])
+    _, fds, _, _ = socket.recv_fds(cli, 1, 1)
+    cli.close()
+    dist.barrier(group=group)
+    return fds[0]
+
+
 class Communicator:
     """This process's rank of an ``nranks``-GPU communicator."""
 
@@ -169,49 +204,40 @@ class Communicator:
     def setup_nvls(self) -> bool:
         """Collective: build the NVLS multicast object (SwitchChannel).  Rank 0
         creates it and passes its POSIX fd to the other ranks over a Unix
-        socket (SCM_RIGHTS); every rank then binds and maps its memory.  All
-        ranks must share one host.  Returns False (on every rank) when any
-        GPU lacks multicast support."""
+        socket (SCM_RIGHTS, ``share_fd``); every rank then binds and maps its
+        memory.  All ranks must share one host.  Returns False on every rank
+        when any GPU lacks multicast support or any step fails on any rank
+        (every step's outcome is agreed on before the next, so a failure
+        never leaves a rank waiting in a collective)."""
         import os
-        import socket
-        import tempfile
         import torch.distributed as dist
         L = _lib.lib()
-        ok = self._multicast_capable()
-        flags = [None] * self.nranks
-        dist.all_gather_object(flags, ok, group=self.group)
-        if not all(flags):
+
+        def agree(ok: bool) -> bool:
+            flags = [None] * self.nranks
+            dist.all_gather_object(flags, bool(ok), group=self.group)
+            return all(flags)
+
+        if not agree(self._multicast_capable()):
             return False
-        path = None
+        fd = ctypes.c_int(-1)
         if self.rank == 0:
-            fd = ctypes.c_int(-1)
-            _lib.check(L.cfNvlsCreate(self._comm, ctypes.byref(fd)))
-            path = os.path.join(tempfile.mkdtemp(prefix="cf_nvls_"), "sock")
-            srv = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
-            srv.bind(path)
-            srv.listen(self.nranks)
-        box = [path]
-        dist.broadcast_object_list(box, src=0, group=self.group)
-        if self.rank == 0:
-            for _ in range(self.nranks - 1):
-                conn, _ = srv.accept()
-                socket.send_fds(conn, [b"f"], [fd.value])
-                conn.close()
-            srv.close()
+            created = L.cfNvlsCreate(self._comm, ctypes.byref(fd)) == 0
         else:
-            cli = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
-            cli.connect(box[0])
-            _, fds, _, _ = socket.recv_fds(cli, 1, 1)
-            cli.close()
-            _lib.check(L.cfNvlsImport(self._comm, fds[0]))
-            os.close(fds[0])
-        dist.barrier(group=self.group)          # every device added before any bind
-        _lib.check(L.cfNvlsBind(self._comm))
-        dist.barrier(group=self.group)
+            created = True
+        if not agree(created):
+            return False
+        got = share_fd(fd.value if self.rank == 0 else None, self.rank, self.nranks, self.group)
+        imported = True
+        if self.rank != 0:
+            imported = L.cfNvlsImport(self._comm, got) == 0
+            os.close(got)
+        ok = agree(imported)          # every device added before any bind
+        if ok:
+            ok = agree(L.cfNvlsBind(self._comm) == 0)
         if self.rank == 0:
             os.close(fd.value)
-            os.unlink(path)
-        return True
+        return ok
 
     def _multicast_capable(self) -> bool:
         from .world import device_multicast_capable
