@@ -101,7 +101,9 @@ typedef struct {
   int max_blocks;           /* CTA cap per rank (0 = derived from occupancy and co-residency) */
   int threads;              /* threads per CTA (0 = 512) */
   uint64_t spin_timeout_ns; /* device spin-wait timeout -> CF_E_DEADLOCK (0 = 10 s) */
-  int use_multicast;        /* 1 = build NVLS multicast objects when supported */
+  int use_multicast;        /* 1 = build NVLS multicast objects when supported; 2 = emulated switch:
+                               switch_2pa runs the NVLS kernel (K5) on unicast staging with per-rank
+                               loads / stores in place of multimem (in-process communicators; tests) */
   size_t nvls_bytes;        /* per-rank NVLS staging region (input and output halves each; 0 = 64 MiB) */
 } cfConfig;
 

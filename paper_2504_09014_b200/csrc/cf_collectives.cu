@@ -470,13 +470,9 @@ __global__ void __launch_bounds__(512) push_gather_kernel(const __grid_constant_
 
 // ---------------------------------------------------------------- K5
 
-// NVLS AllReduce (build_switch_2pa, cf/collectives.py:235-250): the send
-// buffers were copied into each rank's multicast-bound input half; after the
-// entry handshake rank r's CTAs multimem.ld_reduce their slice of chunk r (the
-// NVSwitch sums the same address over every member, f16/bf16 accumulating in
-// f32) and multimem.st the result into every member's output half; the exit
-// handshake publishes it.  rk.in[rank] / rk.out[rank] hold the multicast
-// addresses of the two halves.
+// NVLS switch primitives: multimem.ld_reduce sums the same address over every
+// member of the multicast object inside the NVSwitch (f16/bf16 accumulating in
+// f32), multimem.st broadcasts a store to every member.
 template <typename T>
 __device__ __forceinline__ uint4 multimem_ld_reduce(const void* p);
 template <>
@@ -515,22 +511,67 @@ __device__ __forceinline__ void multimem_st16(void* p, uint4 v) {
                "r"(v.z), "r"(v.w) : "memory");
 }
 
+// K5 NVLS AllReduce (build_switch_2pa, cf/collectives.py:235-250; switch_reduce /
+// switch_broadcast, cf/channels.py:367-409), one launch per call.  The message
+// runs in pieces of the staging half; per piece:
+//   A  copy the send buffer into the own multicast-bound input half,
+//   B  (after the entry handshake) multimem.ld_reduce the slice of chunk r and
+//      multimem.st it into every member's output half,
+//   C  (after the exit handshake) copy the own output half into recv.
+// Vector v of a piece belongs to chunk v / cv and, within it, to CTA
+// (v mod cv) / per on EVERY rank in all three phases, so the CTA-pair
+// handshakes (CTA b of each rank) order exactly the accesses that meet.
+// `emul` replaces the two multimem instructions by per-rank loads / stores
+// (0 + x_0 + x_1 + ..., the reference switch order) on unicast staging, so the
+// co-resident world exercises this control path on one GPU.
 template <typename T>
-__global__ void __launch_bounds__(512) nvls_allreduce_kernel(const __grid_constant__ CollArgs a) {
+__global__ void __launch_bounds__(512) nvls_kernel(const __grid_constant__ CollArgs a) {
   const RankCtx& rk = a.rk[blockIdx.y];
   constexpr int V = 16 / sizeof(T);
-  const int n = a.n, r = rk.rank;
+  const int n = a.n, r = rk.rank, b = blockIdx.x, B = gridDim.x;
   const uint64_t e = begin_call(rk);
-  handshake(rk, n, e * kPhases + 1, false, a.gpu_scope);
-  const size_t nvec = (a.count + V - 1) / V;       // staging halves are padded: whole vectors
-  const size_t cv = (nvec + n - 1) / n;
-  const size_t v0 = min((size_t)r * cv, nvec), v1 = min(v0 + cv, nvec);
-  const char* in = rk.in[r];
-  char* out = rk.out[r];
-  for (size_t v = v0 + (size_t)blockIdx.x * blockDim.x + threadIdx.x; v < v1;
-       v += (size_t)gridDim.x * blockDim.x)
-    multimem_st16(out + v * 16, multimem_ld_reduce<T>(in + v * 16));
-  handshake(rk, n, e * kPhases + 2, true, a.gpu_scope);
+  const size_t total = (a.count + V - 1) / V;      // 16-byte vectors of the message
+  const size_t piece = a.half / 16;                // vectors per staging half
+  char* my_in = rk.nv[r];
+  char* my_out = rk.nv[r] + a.half;
+  int ph = 1;
+  for (size_t p0 = 0; p0 < total; p0 += piece, ph += 2) {
+    const size_t pv = min(piece, total - p0);
+    const size_t cv = (pv + n - 1) / n;
+    const size_t per = (cv + B - 1) / B;
+    const size_t w0 = min((size_t)b * per, cv), w1 = min(w0 + per, cv);
+    // A: this CTA's share of every chunk, send buffer -> own input half
+    for (int o = 0; o < n; o++)
+      for (size_t w = w0 + threadIdx.x; w < w1; w += blockDim.x) {
+        const size_t v = (size_t)o * cv + w;
+        if (v < pv) st16(my_in + v * 16, load_vec<T>(rk.in[r], p0 + v, a.count));
+      }
+    handshake(rk, n, e * kPhases + ph, true, a.gpu_scope);
+    // B: reduce chunk r across the members, broadcast the result
+    for (size_t w = w0 + threadIdx.x; w < w1; w += blockDim.x) {
+      const size_t v = (size_t)r * cv + w;
+      if (v >= pv) break;
+      if (!a.emul) {
+        multimem_st16(rk.nv_mc + a.half + v * 16, multimem_ld_reduce<T>(rk.nv_mc + v * 16));
+      } else {
+        uint4 x[CF_MAX_RANKS];
+#pragma unroll
+        for (int q = 0; q < CF_MAX_RANKS; q++)
+          if (q < n) x[q] = ld16(rk.nv[q] + v * 16);
+        const uint4 res = reduce_vecs<T, CF_MAX_RANKS>(x, n, true);
+#pragma unroll
+        for (int q = 0; q < CF_MAX_RANKS; q++)
+          if (q < n) st16(rk.nv[q] + a.half + v * 16, res);
+      }
+    }
+    handshake(rk, n, e * kPhases + ph + 1, true, a.gpu_scope);
+    // C: this CTA's share of every chunk, own output half -> recv
+    for (int o = 0; o < n; o++)
+      for (size_t w = w0 + threadIdx.x; w < w1; w += blockDim.x) {
+        const size_t v = (size_t)o * cv + w;
+        if (v < pv) store_vec<T>(rk.out[r], p0 + v, ld16(my_out + v * 16), 0, a.count, 0);
+      }
+  }
   end_call(rk, e);
 }
 
@@ -1052,10 +1093,10 @@ const void* collective_kernel(int kind, int dtype, int n) {
       break;
     case 4:
       switch (dtype) {
-        case 0: return (const void*)nvls_allreduce_kernel<int32_t>;
-        case 1: return (const void*)nvls_allreduce_kernel<float>;
-        case 2: return (const void*)nvls_allreduce_kernel<__half>;
-        case 3: return (const void*)nvls_allreduce_kernel<__nv_bfloat16>;
+        case 0: return (const void*)nvls_kernel<int32_t>;
+        case 1: return (const void*)nvls_kernel<float>;
+        case 2: return (const void*)nvls_kernel<__half>;
+        case 3: return (const void*)nvls_kernel<__nv_bfloat16>;
       }
       break;
     case 5:

@@ -18,6 +18,9 @@ struct RankCtx {
   uint64_t* ack[CF_MAX_RANKS];    // every rank's ack slab (ring credits, ring "ready")
   char* ring[CF_MAX_RANKS];       // every rank's ring slot region
   char* out2[CF_MAX_RANKS];       // K13: every rank's residual-out buffer (push)
+  char* nv[CF_MAX_RANKS];         // K5: NVLS staging [input half | output half], unicast: own rank's
+                                  // (emulated switch: every rank's)
+  char* nv_mc;                    // K5: own staging's multicast mapping (null when emulated)
   const char* resid;              // K13: this rank's residual input
   const char* weight;             // K13: this rank's RMSNorm weight [hidden]
   RankState* st;                  // this rank's state
@@ -62,7 +65,7 @@ struct CollArgs {
   size_t rows;      // K13: rows of `hidden` elements (count = rows * hidden)
   size_t hidden;
   float eps;        // K13: RMSNorm epsilon
-  int pad2_;
+  int emul;         // K5: emulated switch (per-rank loads/stores in place of multimem)
   size_t win_lo;    // pull-reduce (not whole): element window [win_lo, win_hi) inside each
   size_t win_hi;    // rank's chunk (pipelined host calls); 0 / SIZE_MAX = the whole chunk
   RankCtx rk[CF_MAX_RANKS];

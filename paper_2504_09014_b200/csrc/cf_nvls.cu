@@ -131,7 +131,33 @@ cfStatus nvls_setup_inprocess(cfComm* c) {
   return CF_OK;
 }
 
+// Emulated switch (cfConfig.use_multicast = 2): plain per-rank staging, the
+// kernel replaces multimem by per-rank loads / stores (in-process worlds).
+cfStatus nvls_setup_emulated(cfComm* c) {
+  if (c->multiprocess) return fail(CF_E_CONFIG, "the emulated switch needs every rank in this process");
+  c->nvls.half = round_up(c->cfg.nvls_bytes ? c->cfg.nvls_bytes : (size_t)64 << 20, (size_t)4096);
+  c->nvls.size = 2 * c->nvls.half;
+  c->nvls.ranks.assign(c->local.size(), NvlsRank());
+  for (size_t li = 0; li < c->local.size(); li++) {
+    CF_CUDA(cudaSetDevice(c->local[li].dev));
+    CF_CUDA(cudaMalloc((void**)&c->nvls.ranks[li].uc, c->nvls.size));
+    CF_CUDA(cudaMemset(c->nvls.ranks[li].uc, 0, c->nvls.size));
+  }
+  c->nvls.emul = true;
+  c->nvls.enabled = true;
+  return CF_OK;
+}
+
 void nvls_teardown(cfComm* c) {
+  if (c->nvls.emul) {
+    for (size_t li = 0; li < c->nvls.ranks.size(); li++) {
+      cudaSetDevice(c->local[li].dev);
+      cudaDeviceSynchronize();
+      cudaFree(c->nvls.ranks[li].uc);
+    }
+    c->nvls = Nvls();
+    return;
+  }
   if (!c->nvls.mc && c->nvls.ranks.empty()) return;
   CF_DRV(cuMemUnmap);
   CF_DRV(cuMemAddressFree);

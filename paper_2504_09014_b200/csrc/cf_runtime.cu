@@ -244,7 +244,11 @@ extern "C" cfStatus cfCommInitAll(cfComm_t* out, int nranks, const int* devs, co
   // NVLS needs one device per rank, each multicast-capable
   bool mc_ok = c->groups.size() == (size_t)nranks;
   for (int r = 0; r < nranks && mc_ok; r++) mc_ok = multicast_capable(devs[r]);
-  if (c->cfg.use_multicast && mc_ok) {
+  if (c->cfg.use_multicast == 2) {
+    // emulated switch: the K5 control path on unicast staging (tests, one GPU)
+    s = nvls_setup_emulated(c);
+    if (s != CF_OK) { cfCommDestroy(c); return s; }
+  } else if (c->cfg.use_multicast && mc_ok) {
     // a box that advertises multicast but cannot build the object (e.g. no
     // fabric manager) keeps working: switch_2pa then runs the all-pairs kernel
     if (nvls_setup_inprocess(c) != CF_OK) {
@@ -253,7 +257,7 @@ extern "C" cfStatus cfCommInitAll(cfComm_t* out, int nranks, const int* devs, co
       nvls_teardown(c);
     }
   }
-  c->multicast_supported = c->nvls.enabled;
+  c->multicast_supported = c->nvls.enabled && !c->nvls.emul;
   c->connected = true;
   *out = c;
   return CF_OK;
@@ -663,54 +667,48 @@ cfStatus launch(cfComm* c, const Job& j, int dtype, const void* const* send, voi
   return CF_OK;
 }
 
-// K5: copy into the multicast-bound input half, multimem reduce/broadcast,
-// copy the output half out; messages larger than the staging half run in
-// pieces (AllReduce is element-wise).
+// K5: one nvls_kernel launch per device group (copy-in, multimem reduce /
+// broadcast and copy-out fused, the message in pieces of the staging half).
 cfStatus nvls_allreduce(cfComm* c, const void* const* send, void* const* recv, size_t count, int dtype,
                         const cudaStream_t* streams) {
   DeviceGuard guard;
   const size_t es = dtype_size(dtype);
-  const size_t piece = c->nvls.half / es;
   const void* kernel = collective_kernel(4, dtype, c->nranks);
   const int threads = c->cfg.threads;
-  for (size_t off = 0; off < count; off += piece) {
-    const size_t cnt = std::min(piece, count - off);
-    for (size_t li = 0; li < c->local.size(); li++) {
-      CF_CUDA(cudaSetDevice(c->local[li].dev));
-      CF_CUDA(cudaMemcpyAsync(c->nvls.ranks[li].uc, (const char*)send[li] + off * es, cnt * es,
-                              cudaMemcpyDeviceToDevice, streams[li]));
-    }
-    for (size_t gi = 0; gi < c->groups.size(); gi++) {
-      const auto& g = c->groups[gi];
-      CF_CUDA(cudaSetDevice(c->local[g[0]].dev));
-      CollArgs a;
-      memset(&a, 0, sizeof(a));
-      a.n = c->nranks;
-      a.nlocal = (int)g.size();
-      a.count = cnt;
-      a.gpu_scope = 0;
-      for (size_t k = 0; k < g.size(); k++) {
-        const int li = g[k];
-        RankCtx& rk = a.rk[k];
-        rk.rank = c->local[li].rank;
-        rk.st = c->state(li);
-        for (int p = 0; p < c->nranks; p++) rk.sem[p] = c->sem(li, p);
-        rk.in[rk.rank] = c->nvls.ranks[li].mc;
-        rk.out[rk.rank] = c->nvls.ranks[li].mc + c->nvls.half;
+  const size_t total = ceil_div(count * es, (size_t)16), piece = c->nvls.half / 16;
+  const size_t work = ceil_div(std::min(total, piece), (size_t)c->nranks);   // vectors per chunk
+  for (size_t gi = 0; gi < c->groups.size(); gi++) {
+    const auto& g = c->groups[gi];
+    CF_CUDA(cudaSetDevice(c->local[g[0]].dev));
+    CollArgs a;
+    memset(&a, 0, sizeof(a));
+    a.n = c->nranks;
+    a.nlocal = (int)g.size();
+    a.count = count;
+    a.half = c->nvls.half;
+    a.emul = c->nvls.emul ? 1 : 0;
+    a.gpu_scope = (c->groups.size() == 1 && !c->multiprocess) ? 1 : 0;
+    for (size_t k = 0; k < g.size(); k++) {
+      const int li = g[k];
+      RankCtx& rk = a.rk[k];
+      rk.rank = c->local[li].rank;
+      rk.st = c->state(li);
+      for (int p = 0; p < c->nranks; p++) rk.sem[p] = c->sem(li, p);
+      rk.in[rk.rank] = (const char*)send[li];
+      rk.out[rk.rank] = (char*)recv[li];
+      if (c->nvls.emul) {   // every rank's unicast staging (in-process only)
+        for (size_t q = 0; q < c->local.size(); q++) rk.nv[c->local[q].rank] = c->nvls.ranks[q].uc;
+      } else {
+        rk.nv[rk.rank] = c->nvls.ranks[li].uc;
       }
-      const size_t work = ceil_div(ceil_div(cnt * es, 16), (size_t)c->nranks);
-      const int mb = max_blocks_per_rank(c, kernel, (int)gi, threads);
-      const int blocks = (int)std::min<size_t>((size_t)mb, std::max<size_t>(1, ceil_div(work, (size_t)threads)));
-      CF_TRY(join_streams(c, (int)gi, streams, false));
-      void* args[] = {&a};
-      CF_CUDA(cudaLaunchKernel(kernel, dim3(blocks, g.size()), dim3(threads), args, 0, streams[g[0]]));
-      CF_TRY(join_streams(c, (int)gi, streams, true));
+      rk.nv_mc = c->nvls.ranks[li].mc;
     }
-    for (size_t li = 0; li < c->local.size(); li++) {
-      CF_CUDA(cudaSetDevice(c->local[li].dev));
-      CF_CUDA(cudaMemcpyAsync((char*)recv[li] + off * es, c->nvls.ranks[li].uc + c->nvls.half, cnt * es,
-                              cudaMemcpyDeviceToDevice, streams[li]));
-    }
+    const int mb = max_blocks_per_rank(c, kernel, (int)gi, threads);
+    const int blocks = (int)std::min<size_t>((size_t)mb, std::max<size_t>(1, ceil_div(work, (size_t)threads)));
+    CF_TRY(join_streams(c, (int)gi, streams, false));
+    void* args[] = {&a};
+    CF_CUDA(cudaLaunchKernel(kernel, dim3(blocks, g.size()), dim3(threads), args, 0, streams[g[0]]));
+    CF_TRY(join_streams(c, (int)gi, streams, true));
   }
   return CF_OK;
 }

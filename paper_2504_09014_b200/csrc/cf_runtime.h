@@ -92,6 +92,7 @@ struct NvlsRank {
 
 struct Nvls {
   bool enabled = false;
+  bool emul = false;            // emulated switch: cudaMalloc'd unicast staging, no multicast object
   size_t half = 0;              // bytes of each half (input, output)
   size_t size = 0;              // 2*half rounded to the multicast granularity
   size_t gran = 0;
@@ -149,6 +150,7 @@ cfStatus join_streams(cfComm* c, int group, const cudaStream_t* streams, bool af
 // NVLS: probe support; set up for a one-process world; tear down.
 bool multicast_capable(int dev);
 cfStatus nvls_setup_inprocess(cfComm* c);
+cfStatus nvls_setup_emulated(cfComm* c);
 void nvls_teardown(cfComm* c);
 // PortChannel proxy (cf_proxy.cu)
 cfStatus proxy_start(cfComm* c);

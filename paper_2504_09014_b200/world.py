@@ -58,7 +58,7 @@ class World:
     def __init__(self, num_nodes: int = 1, gpus_per_node: int = 1,
                  intra_kind: str = "switch-attached", seed: int = 0, devices=None,
                  ll_max_bytes: int = 0, max_blocks: int = 0, threads: int = 0,
-                 spin_timeout_ms: int = 0, use_multicast: bool = True, nvls_bytes: int = 0):
+                 spin_timeout_ms: int = 0, use_multicast=True, nvls_bytes: int = 0):
         if num_nodes * gpus_per_node < 1:
             raise BadSizeError("world needs at least one rank")
         if num_nodes != 1:
@@ -83,9 +83,11 @@ class World:
         if len(devices) != n:
             raise OutOfBoundsError(f"need {n} device ids, got {len(devices)}")
         self.devices = devices
-        # NVLS is set up when every rank has its own multicast-capable GPU
-        cfg = _lib.cfConfig(ll_max_bytes, max_blocks, threads,
-                            int(spin_timeout_ms) * 1_000_000, int(bool(use_multicast)), nvls_bytes)
+        # NVLS is set up when every rank has its own multicast-capable GPU;
+        # use_multicast="emulate" runs switch_2pa's NVLS kernel on unicast
+        # staging with per-rank loads / stores in place of multimem (tests)
+        mc = 2 if use_multicast == "emulate" else int(bool(use_multicast))
+        cfg = _lib.cfConfig(ll_max_bytes, max_blocks, threads, int(spin_timeout_ms) * 1_000_000, mc, nvls_bytes)
         handle = ctypes.c_void_p()
         devs = (ctypes.c_int * n)(*devices)
         _lib.check(_lib.lib().cfCommInitAll(ctypes.byref(handle), n, devs, ctypes.byref(cfg)))

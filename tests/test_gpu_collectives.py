@@ -204,6 +204,32 @@ def test_nvls_multicast_path_single_rank():
         w.close()
 
 
+@pytest.mark.parametrize("n", [2, 4, 8])
+@pytest.mark.parametrize("dtype", ["f32", "bf16", "f16", "i32"])
+def test_nvls_kernel_control_path_emulated(n, dtype):
+    """K5's fused kernel (copy-in, switch reduce / broadcast, copy-out, in
+    pieces of the staging half, CTA-pair handshakes) with the two multimem
+    instructions emulated by per-rank loads / stores: bit-exact to the
+    reference switch order 0 + x_0 + ... + x_{n-1}, including messages of
+    several pieces, ragged counts and repeated calls."""
+    from paper_2504_09014_b200 import collective, make_world
+    w = make_world(1, n, devices=[0] * n, use_multicast="emulate", nvls_bytes=64 << 10,
+                   spin_timeout_ms=5000)
+    try:
+        assert not w.multicast_supported()
+        dist = {"f32": "wide", "i32": "int"}.get(dtype, "normal")
+        for elems in (1, 7, 4096, 16384 + 3, 200001):
+            ins = gen_inputs(n, elems, dtype, dist, 31 * n + elems % 17)
+            want = oracle.allreduce(ins, "switch_2pa", dtype)
+            for _ in range(2):
+                got = collective("allreduce", ins, w, dtype=dtype, algo="switch_2pa")
+                for r in range(n):
+                    assert np.array_equal(got[r].view(np.uint8), want[r].view(np.uint8)), (elems, r)
+        w.check_device_error()
+    finally:
+        w.close()
+
+
 def test_coresident_world_has_no_multicast():
     assert not world(8).multicast_supported()
 
