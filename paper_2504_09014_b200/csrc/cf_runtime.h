@@ -143,7 +143,7 @@ int occupancy(cfComm* c, const void* kernel, int dev, int threads);
 // Driver API function by name (nullptr if unavailable).
 void* driver_fn(const char* name);
 // Co-residency cap: CTAs per rank such that every rank of the group fits at once.
-int max_blocks_per_rank(cfComm* c, const void* kernel, int group, int threads);
+int max_blocks_per_rank(cfComm* c, const void* kernel, int group, int threads, int per_sm = 0);
 // Make streams[first] of the group wait for the others; after the launch, the
 // others wait for it.  `after` selects the phase.
 cfStatus join_streams(cfComm* c, int group, const cudaStream_t* streams, bool after);

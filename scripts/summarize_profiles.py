@@ -53,7 +53,9 @@ def to_bytes(s):
 def main():
     tag = sys.argv[1] if len(sys.argv) > 1 else "round1"
     src = os.path.join(ROOT, "gpurun_out")
-    dst = os.path.join(ROOT, "profiles", tag)
+    # optional 2nd argument: output directory (on the GPU box: under gpurun_out/
+    # so the summary travels back while the large .ncu-rep files are dropped)
+    dst = sys.argv[2] if len(sys.argv) > 2 else os.path.join(ROOT, "profiles", tag)
     os.makedirs(dst, exist_ok=True)
     md = [f"# ncu summaries ({tag})", "",
           "Captured with `scripts/profile.sh` (ncu --set full --clock-control none, 1 GPU, "
@@ -77,7 +79,7 @@ def main():
             if f.startswith("prof_2pa_256m") and info:
                 d = info[0]
                 traffic = to_bytes(d["dram__bytes_read.sum"]) + to_bytes(d["dram__bytes_write.sum"])
-                with open(os.path.join(ROOT, "profiles", "headline_traffic.json"), "w") as fh:
+                with open(os.path.join(dst, "headline_traffic.json"), "w") as fh:
                     json.dump({"kernel": d["kernel"], "dram_bytes_per_launch": traffic,
                                "source": f"profiles/{tag}/summary.md ({f})"}, fh, indent=1)
         elif f.startswith("launches") and f.endswith(".csv"):
