@@ -709,10 +709,12 @@ __device__ X AccVec<T>::bits_to(uint32_t u) {
   else return (X)u;
 }
 
-// 16-byte vectors of T per thread per ring unit prefetched into registers
-// (a 32 KiB unit of f32 partials covers 8192 elements: 4 bf16 / 8 f32 vectors
-// per thread at 256 threads).
-constexpr int kRingPre = 8;
+// Passes (16-byte vectors of T per thread) of a ring unit's own contribution
+// prefetched into registers before a step's waits.
+#ifndef CF_RING_PRE
+#define CF_RING_PRE 4
+#endif
+constexpr int kRingPre = CF_RING_PRE;
 
 // Ring ReduceScatter (build_ring_rs, cf/collectives.py:30-79) and, with
 // `push`, the two-phase ring AllReduce (build_2pr, :107-136).  Step s sends
@@ -721,8 +723,14 @@ constexpr int kRingPre = 8;
 // accumulator type, f32 for f16/bf16, so rounding happens once), and after n
 // steps chunk r holds 0 + x_r + x_{r+1} + ... + x_{r-1}: the reference's
 // ring order.  The AllGather phase then forwards the finished chunks.
+// 256-thread ring CTAs, 3 resident per SM (<= 85 registers): 55 independent
+// links per rank at 8 co-resident ranks (256 MiB ring RS: 2/SM 1.69 ms,
+// 3/SM 1.48 ms, 4/SM 1.52 ms).
+#ifndef CF_RING_MINB
+#define CF_RING_MINB 3
+#endif
 template <typename T>
-__global__ void __launch_bounds__(512) ring_kernel(const __grid_constant__ CollArgs a) {
+__global__ void __launch_bounds__(256, CF_RING_MINB) ring_kernel(const __grid_constant__ CollArgs a) {
   using A = typename Vec<T>::Acc;
   const RankCtx& rk = a.rk[blockIdx.y];
   const int n = a.n, r = rk.rank, b = blockIdx.x, B = gridDim.x;
@@ -761,40 +769,39 @@ __global__ void __launch_bounds__(512) ring_kernel(const __grid_constant__ CollA
       const size_t u0 = s0 + k * UA;
       if (u0 >= s1) continue;
       const size_t u1 = min(u0 + UA, s1);
-      if (vec && blockDim.x * V * kRingPre >= UA) {
-        // whole 16-byte vectors of T, the own contribution prefetched into
-        // registers before the waits (its HBM latency overlaps the flag
-        // round trip); the slots carry V accumulators per vector
+      if (vec) {
+        // whole 16-byte vectors of T; the first kRingPre passes of the own
+        // contribution are prefetched into registers before the waits (their
+        // HBM latency overlaps the flag round trip), later passes load after;
+        // the slots carry V accumulators per vector
+        const size_t pass = (size_t)blockDim.x * V;
         uint4 xv[kRingPre];
 #pragma unroll
         for (int m = 0; m < kRingPre; m++) {
-          const size_t i = u0 + ((size_t)m * blockDim.x + threadIdx.x) * V;
+          const size_t i = u0 + m * pass + threadIdx.x * V;
           if (i < u1) xv[m] = ld16(x + i);
         }
-        const bool tsk = k == 10 && (s == 3 || s == 4);
-        if (tsk) TS_MARK();
         L.wait_both(s > 0, true);
-        if (tsk) TS_MARK();
         const A* in_slot = reinterpret_cast<const A*>(L.recv_slot());
         A* out_slot = reinterpret_cast<A*>(L.send_slot());
+        auto step = [&](size_t i, uint4 xi) {
+          A v[V];
+          Vec<T>::load(xi, v);
+          if (s > 0) {
+            A p[V];
+            AccVec<T>::load(in_slot + (i - u0), p);
+#pragma unroll
+            for (int j = 0; j < (int)V; j++) v[j] = acc_add(p[j], v[j]);
+          }
+          AccVec<T>::store(out_slot + (i - u0), v);
+        };
 #pragma unroll
         for (int m = 0; m < kRingPre; m++) {
-          const size_t i = u0 + ((size_t)m * blockDim.x + threadIdx.x) * V;
-          if (i < u1) {
-            A v[V];
-            Vec<T>::load(xv[m], v);
-            if (s > 0) {
-              A p[V];
-              AccVec<T>::load(in_slot + (i - u0), p);
-#pragma unroll
-              for (int j = 0; j < (int)V; j++) v[j] = acc_add(p[j], v[j]);
-            }
-            AccVec<T>::store(out_slot + (i - u0), v);
-          }
+          const size_t i = u0 + m * pass + threadIdx.x * V;
+          if (i < u1) step(i, xv[m]);
         }
-        if (tsk) TS_MARK();
+        for (size_t i = u0 + kRingPre * pass + threadIdx.x * V; i < u1; i += pass) step(i, ld16(x + i));
         L.done_both(s > 0, true);
-        if (tsk) TS_MARK();
         continue;
       }
       if (s > 0) L.recv_wait();

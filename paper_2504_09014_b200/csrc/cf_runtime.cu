@@ -602,10 +602,7 @@ cfStatus launch(cfComm* c, const Job& j, int dtype, const void* const* send, voi
   // Ring links are latency chains (every step waits for the previous rank's
   // step): smaller CTAs give each rank up to kRingCtas independent links.
   const bool ring = j.kind == kRing || j.kind == kRingGather;
-#ifndef CF_RING_THREADS
-#define CF_RING_THREADS 256
-#endif
-  const int threads = j.kind == kRing ? std::min(c->cfg.threads, CF_RING_THREADS) : c->cfg.threads;
+  const int threads = j.kind == kRing ? std::min(c->cfg.threads, 256) : c->cfg.threads;   // ring_kernel's bound
   for (size_t gi = 0; gi < c->groups.size(); gi++) {
     const auto& g = c->groups[gi];
     const int dev = c->local[g[0]].dev;

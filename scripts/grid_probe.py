@@ -20,7 +20,10 @@ def main():
             send = [torch.randn(cnt, device=dev).to(torch.bfloat16) for _ in range(n)]
             recv = [torch.empty_like(s) for s in send]
             t = time_coll(w, "allreduce", send, recv, cnt, "bf16", _lib.ALGOS["2pa"], 10, 3, None)
-            row.append(f"{nb >> 20} MiB {t * 1e6:8.1f} us")
+            row.append(f"2pa {nb >> 20} MiB {t * 1e6:8.1f} us")
+            t = time_coll(w, "allgather", [s[:cnt // n] for s in send], recv, cnt // n, "bf16",
+                          _lib.ALGOS["allpairs_ag"], 10, 3, None)
+            row.append(f"ag {nb >> 20} MiB {t * 1e6:8.1f} us")
             del send, recv
         print(f"max_blocks={mb:3d}: " + " | ".join(row), flush=True)
         w.close()
