@@ -557,7 +557,7 @@ __global__ void __launch_bounds__(512) nvls_kernel(const __grid_constant__ CollA
         uint4 x[CF_MAX_RANKS];
 #pragma unroll
         for (int q = 0; q < CF_MAX_RANKS; q++)
-          if (q < n) x[q] = ld16(rk.nv[q] + v * 16);
+          if (q < n) x[q] = ld16_cg(rk.nv[q] + v * 16);
         const uint4 res = reduce_vecs<T, CF_MAX_RANKS>(x, n, true);
 #pragma unroll
         for (int q = 0; q < CF_MAX_RANKS; q++)
@@ -569,7 +569,7 @@ __global__ void __launch_bounds__(512) nvls_kernel(const __grid_constant__ CollA
     for (int o = 0; o < n; o++)
       for (size_t w = w0 + threadIdx.x; w < w1; w += blockDim.x) {
         const size_t v = (size_t)o * cv + w;
-        if (v < pv) store_vec<T>(rk.out[r], p0 + v, ld16(my_out + v * 16), 0, a.count, 0);
+        if (v < pv) store_vec<T>(rk.out[r], p0 + v, ld16_cg(my_out + v * 16), 0, a.count, 0);
       }
   }
   end_call(rk, e);

@@ -221,10 +221,13 @@ def test_nvls_kernel_control_path_emulated(n, dtype):
         for elems in (1, 7, 4096, 16384 + 3, 200001):
             ins = gen_inputs(n, elems, dtype, dist, 31 * n + elems % 17)
             want = oracle.allreduce(ins, "switch_2pa", dtype)
-            for _ in range(2):
+            for rep in range(2):
                 got = collective("allreduce", ins, w, dtype=dtype, algo="switch_2pa")
                 for r in range(n):
-                    assert np.array_equal(got[r].view(np.uint8), want[r].view(np.uint8)), (elems, r)
+                    g = got[r].view(np.uint8).reshape(elems, -1)
+                    bad = np.nonzero(np.any(g != want[r].view(np.uint8).reshape(elems, -1), axis=1))[0]
+                    assert not len(bad), (elems, rep, r, len(bad), bad[:4], bad[-2:], got[r][bad[:3]],
+                                          want[r][bad[:3]], [x[bad[:3]] for x in ins])
         w.check_device_error()
     finally:
         w.close()
