@@ -65,6 +65,33 @@ def test_allreduce_vs_oracle(n, dtype, elems):
             assert np.array_equal(got[r].view(np.uint8), want[r].view(np.uint8)), (algo, var, r)
 
 
+@pytest.mark.parametrize("n", [3, 5, 6, 7])
+@pytest.mark.parametrize("dtype", ["f32", "bf16", "i32"])
+def test_odd_rank_counts_vs_oracle(n, dtype):
+    """Rank counts that are not powers of two (kernels templated on 2/4/8
+    slots run n < slots; chunking pads to n or 2n): every AllReduce algorithm,
+    both ReduceScatters and both AllGathers, bit-exact to the oracle."""
+    from paper_2504_09014_b200 import collective
+    dist = {"f32": "wide", "i32": "int"}.get(dtype, "normal")
+    for elems in (1, 37, 4096 + 5, 70001):
+        ins = gen_inputs(n, elems, dtype, dist, 1000 + 10 * n + elems % 7)
+        for algo, var in ALGOS:
+            got = collective("allreduce", ins, world(n), dtype=dtype, algo=algo, variant=var)
+            want = oracle.allreduce(ins, _ORACLE_NAME.get(algo, algo), dtype)
+            for r in range(n):
+                assert np.array_equal(got[r].view(np.uint8), want[r].view(np.uint8)), (elems, algo, var, r)
+        for algo in ("ring_rs", "rs_direct"):
+            got = collective("reducescatter", ins, world(n), dtype=dtype, algo=algo)
+            want = oracle.reducescatter(ins, "ring_rs" if algo == "ring_rs" else "direct", dtype)
+            for r in range(n):
+                assert np.array_equal(got[r].view(np.uint8), want[r].view(np.uint8)), (elems, algo, r)
+        for algo in ("allpairs_ag", "ring_ag"):
+            got = collective("allgather", ins, world(n), dtype=dtype, algo=algo)
+            for g, wnt in zip(got, oracle.allgather(ins)):
+                assert np.array_equal(g.view(np.uint8), wnt.view(np.uint8)), (elems, algo)
+    world(n).check_device_error()
+
+
 @pytest.mark.parametrize("n", [2, 8])
 @pytest.mark.parametrize("dtype", ["bf16", "f32"])
 @pytest.mark.parametrize("elems", [5, 4096, 100003])
@@ -204,7 +231,7 @@ def test_nvls_multicast_path_single_rank():
         w.close()
 
 
-@pytest.mark.parametrize("n", [2, 4, 8])
+@pytest.mark.parametrize("n", [2, 3, 4, 6, 8])
 @pytest.mark.parametrize("dtype", ["f32", "bf16", "f16", "i32"])
 def test_nvls_kernel_control_path_emulated(n, dtype):
     """K5's fused kernel (copy-in, switch reduce / broadcast, copy-out, in
