@@ -17,7 +17,7 @@ KERNELS = [   # (file tag, substring of the demangled name)
     ("k1_ll_oneshot_f32_8", "ll_oneshot_kernel<float, 8>"),
     ("k4_ll_twoshot_bf16_8", "ll_twoshot_kernel<__nv_bfloat16, 8>"),
     ("k6_push_gather_bf16", "push_gather_kernel<__nv_bfloat16>"),
-    ("k5_nvls_bf16", "nvls_allreduce_kernel<__nv_bfloat16>"),
+    ("k5_nvls_bf16", "nvls_kernel<__nv_bfloat16>"),
     ("k9_ring_bf16", "ring_kernel<__nv_bfloat16>"),
     ("k7_ring_gather_bf16", "ring_gather_kernel<__nv_bfloat16>"),
     ("k13_ar_rmsnorm_bf16_8", "ar_rmsnorm_kernel<__nv_bfloat16, 8>"),
