@@ -287,3 +287,72 @@ def test_host_buffer_allreduce_matches_device_path(dtype, elems):
     # pageable host tensors take the same path (synchronous copies)
     got2 = collective("allreduce", [h.clone() for h in host[:8]], w, algo="2pa")
     assert all(torch.equal(a, b) for a, b in zip(got, got2))
+
+
+def test_cuda_graph_replay_advances_epochs():
+    """Every kernel family captured ONCE in a CUDA graph and replayed: inputs
+    change on every replay (produced inside the graph from a device step
+    counter), so a kernel that failed to advance its device epoch would pair
+    new LL flags / semaphores with stale ones and return an older replay's
+    sums.  f32 integer values: every reduction order is exact."""
+    import torch
+    from paper_2504_09014_b200 import Runtime, _lib, parse_plan
+    from paper_2504_09014_b200 import collectives as C
+    from paper_2504_09014_b200.plan import scale_plan
+    n, cnt = 8, 40960 + 24
+    w = world(n)
+    dev = w.device(0)
+    g = torch.Generator(device=dev).manual_seed(77)
+    base = [torch.randint(-1000, 1001, (cnt,), device=dev, generator=g).float() for _ in range(n)]
+    step = torch.zeros((), device=dev)
+    xs = [torch.empty(cnt, device=dev) for _ in range(n)]
+    algos = ["1pa", "2pa_ll", "2pa", "1pa_hb", "2pr"]
+    outs = {a: [torch.empty(cnt, device=dev) for _ in range(n)] for a in algos}
+    rs_out = [torch.empty(cnt // n, device=dev) for _ in range(n)]
+    ag_out = [torch.empty(cnt, device=dev) for _ in range(n)]
+    plans = {}
+    for name in ("2pa_memory_n8_e64", "1pa_n8_e64"):
+        with open(os.path.join(GOLD, "plans", name + ".json"), "rb") as f:
+            rt = Runtime(scale_plan(parse_plan(f.read()), 640), w, dtype="f32")
+        plans[name] = (rt, [torch.empty(rt.out_elems, device=dev) for _ in range(n)])
+
+    def body():
+        step.add_(1)
+        for r in range(n):
+            torch.add(base[r], step * (r + 1), out=xs[r])
+        for a in algos:
+            C.run("allreduce", xs, outs[a], cnt, "f32", _lib.ALGOS[a], w)
+        C.run("reducescatter", xs, rs_out, cnt // n, "f32", _lib.ALGOS["rs_direct"], w)
+        C.run("allgather", [x[:cnt // n] for x in xs], ag_out, cnt // n, "f32", _lib.ALGOS["allpairs_ag"], w)
+        for rt, ys in plans.values():
+            rt.run_raw([x[:rt.in_elems] for x in xs], ys)
+
+    s = torch.cuda.Stream(dev)
+    s.wait_stream(torch.cuda.current_stream(dev))
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        body()   # warm-up outside the graph (epoch 1 of every kernel)
+        torch.cuda.synchronize(dev)
+        with torch.cuda.graph(graph, stream=s):
+            body()
+    torch.cuda.synchronize(dev)
+    total_base = torch.stack(base).sum(0)
+    for rep in range(6):
+        graph.replay()
+        torch.cuda.synchronize(dev)
+        k = float(step.item())
+        assert k == rep + 2
+        want = total_base + k * sum(r + 1 for r in range(n))
+        for a in algos:
+            for r in range(n):
+                assert torch.equal(outs[a][r], want), (rep, a, r)
+        for r in range(n):
+            assert torch.equal(rs_out[r], want[r * (cnt // n):(r + 1) * (cnt // n)]), (rep, "rs", r)
+            assert torch.equal(ag_out[r], torch.cat([xs[q][:cnt // n] for q in range(n)])), (rep, "ag", r)
+        for name, (rt, ys) in plans.items():
+            for r in range(n):
+                assert torch.equal(ys[r], want[:rt.out_elems]), (rep, name, r)
+    w.check_device_error()
+    for rt, _ in plans.values():
+        rt.check_device_error()
+        rt.close()
