@@ -62,11 +62,17 @@ __device__ __forceinline__ void end_call(const RankCtx& rk, uint64_t e) {
 // then wait until each peer's CTA b signalled >= v.  `publish` makes this
 // CTA's prior global writes visible system-wide first (fence before signal,
 // cf/channels.py:227-232).
+// `publish`: EVERY thread fences its own prior writes before the barrier --
+// one thread's fence after bar.sync is not relied on to cover the other
+// warps' stores still in flight (a rare stale read of the emulated NVLS
+// kernel pointed at exactly that).
 __device__ __forceinline__ void handshake(const RankCtx& rk, int n, uint64_t v, bool publish, bool gpu) {
   const int t = threadIdx.x, r = rk.rank, b = blockIdx.x;
-  if (publish) __syncthreads();
+  if (publish) {
+    fence_publish(gpu);
+    __syncthreads();
+  }
   if (t < n && t != r) {
-    if (publish) fence_publish(gpu);
     st_release(rk.sem[t] + sem_index(r, b), v, gpu);
     wait_geq(rk.sem[r] + sem_index(t, b), v, rk.st, gpu);
   }
@@ -519,8 +525,9 @@ __device__ __forceinline__ void multimem_st16(void* p, uint4 v) {
 //      multimem.st it into every member's output half,
 //   C  (after the exit handshake) copy the own output half into recv.
 // Vector v of a piece belongs to chunk v / cv and, within it, to CTA
-// (v mod cv) / per on EVERY rank in all three phases, so the CTA-pair
-// handshakes (CTA b of each rank) order exactly the accesses that meet.
+// (v mod cv) / per on EVERY rank, in all three phases and in every piece, so
+// the CTA-pair handshakes (CTA b of each rank) order exactly the accesses
+// that meet.
 // `emul` replaces the two multimem instructions by per-rank loads / stores
 // (0 + x_0 + x_1 + ..., the reference switch order) on unicast staging, so the
 // co-resident world exercises this control path on one GPU.
@@ -534,12 +541,17 @@ __global__ void __launch_bounds__(512) nvls_kernel(const __grid_constant__ CollA
   const size_t piece = a.half / 16;                // vectors per staging half
   char* my_in = rk.nv[r];
   char* my_out = rk.nv[r] + a.half;
+  // The chunk / CTA owning staging vector v must be the same in EVERY piece:
+  // the handshakes order CTA b with the CTAs b of the other ranks only, so a
+  // CTA that moves on to the next piece must never touch an offset another
+  // CTA of its rank may still read.  cv / per therefore come from the first
+  // (largest) piece; a shorter last piece just ends early (v < pv).
+  const size_t cv = (min(piece, total) + n - 1) / n;
+  const size_t per = (cv + B - 1) / B;
+  const size_t w0 = min((size_t)b * per, cv), w1 = min(w0 + per, cv);
   int ph = 1;
   for (size_t p0 = 0; p0 < total; p0 += piece, ph += 2) {
     const size_t pv = min(piece, total - p0);
-    const size_t cv = (pv + n - 1) / n;
-    const size_t per = (cv + B - 1) / B;
-    const size_t w0 = min((size_t)b * per, cv), w1 = min(w0 + per, cv);
     // A: this CTA's share of every chunk, send buffer -> own input half
     for (int o = 0; o < n; o++)
       for (size_t w = w0 + threadIdx.x; w < w1; w += blockDim.x) {
@@ -592,14 +604,18 @@ __device__ __forceinline__ void cta_slice(size_t lo, size_t hi, int b, int B, si
 // Values are epoch * kPhases + sequence; the value epoch * kPhases itself is
 // the receiver's "entered this call" ready mark, so slots are never
 // overwritten while the previous call still reads them.
-// Before a ring link's data release: the CTA's slot stores are ordered before
-// thread 0's st.release by the preceding __syncthreads (bar.sync is a
-// CTA-scope synchronization and release is cumulative), which is enough at
-// .gpu scope; across GPUs the full system fence is kept.  (Dropping the
-// .gpu fence: ring RS 256 MiB 2.30 -> 2.14 ms.)
+// Thread 0's fence before a ring link's data release: across GPUs the full
+// system fence; at .gpu scope the per-thread fences below already ordered the
+// slot stores.
 __device__ __forceinline__ void ring_publish(bool gpu) {
   if (!gpu) __threadfence_system();
 }
+// Every thread fences its own slot stores before the barrier that precedes
+// thread 0's release (not relying on bar.sync making one thread's fence
+// cumulative over the other warps' in-flight stores; costs ~5% of ring RS).
+#ifndef CF_RING_THREAD_FENCE
+#define CF_RING_THREAD_FENCE 1
+#endif
 
 struct RingLink {
   char* my_slots;         // slots I receive into (from prev)
@@ -629,6 +645,7 @@ struct RingLink {
     __syncthreads();
   }
   __device__ void send_done() {
+    if (CF_RING_THREAD_FENCE) fence_publish(gpu);
     __syncthreads();
     if (threadIdx.x == 0) {
       ring_publish(gpu);
@@ -646,6 +663,7 @@ struct RingLink {
   // One barrier for both completions of a step: free the received slot, then
   // publish the sent one.
   __device__ void done_both(bool rcv, bool snd) {
+    if (CF_RING_THREAD_FENCE && snd) fence_publish(gpu);
     __syncthreads();
     if (threadIdx.x == 0) {
       if (rcv) st_release(ack_out, base + qr + 1, gpu);

@@ -43,10 +43,12 @@ __device__ __forceinline__ uint32_t runtime_flag(uint64_t e, uint32_t stride, ui
 }
 
 // counter barrier: every participant adds 1, then waits for the call's total
+// (every thread fences its own writes before the block barrier: one thread's
+// fence after bar.sync is not relied on to cover the other warps' stores)
 __device__ __forceinline__ void counter_barrier(uint64_t* ctr, uint64_t target, RankState* rs) {
+  __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
     atomicAdd((unsigned long long*)ctr, 1ull);
     wait_geq(ctr, target, rs, true);
   }
@@ -58,11 +60,9 @@ __device__ __forceinline__ void counter_barrier(uint64_t* ctr, uint64_t target, 
 __device__ __noinline__ void rank_barrier(const PlanArgs& a, int rank, uint64_t k) {
   PlanState* ps = a.st[rank];
   const bool gpu = a.gpu_scope;
+  fence_publish(gpu);
   __syncthreads();
-  if (threadIdx.x == 0) {
-    fence_publish(gpu);
-    atomicAdd((unsigned long long*)&ps->bar_arrive, 1ull);
-  }
+  if (threadIdx.x == 0) atomicAdd((unsigned long long*)&ps->bar_arrive, 1ull);
   if ((int)blockIdx.x == a.rank_leader[rank]) {
     if (threadIdx.x == 0) wait_geq(&ps->bar_arrive, k * (uint64_t)a.rank_ctas[rank], &ps->base, true);
     __syncthreads();
@@ -342,6 +342,7 @@ __device__ __noinline__ void packet_op(const DevOp& op, int K, int j, uint32_t f
 template <typename T>
 __device__ __noinline__ void port_op(const PlanArgs& a, const DevOp& op, int rank, int pid, int j, uint64_t e, RankState* rs,
                         uint64_t& last) {
+  __threadfence_system();   // every thread's writes to the source, before the copy engine reads it
   __syncthreads();
   if (threadIdx.x != 0) return;
   uint64_t src = 0, dst = 0, bytes = 0;
@@ -483,11 +484,11 @@ __global__ void __launch_bounds__(512) plan_kernel(const __grid_constant__ PlanA
       case D_DEV_BARRIER:
         counter_barrier(a.bars[rank] + op.id, ((e - 1) * op.per_call + op.m) * op.members, rs);
         break;
-      case D_SIGNAL:   // ndst consecutive signals, one thread each
+      case D_SIGNAL:   // ndst consecutive signals, one thread each, after every thread's fence
+        fence_publish(a.gpu_scope);
         __syncthreads();
         if ((int)threadIdx.x < op.ndst) {
           const DRef& s = op.dst[threadIdx.x];
-          fence_publish(a.gpu_scope);
           red_add_release(a.lanes[s.rank] + (size_t)s.buf * a.K + j, 1, a.gpu_scope);
         }
         break;
