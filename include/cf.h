@@ -149,6 +149,14 @@ CF_API cfStatus cfDeviceMulticastSupported(int cuda_dev, int* supported);
 CF_API cfStatus cfNvlsCreate(cfComm_t comm, int* fd);
 CF_API cfStatus cfNvlsImport(cfComm_t comm, int fd);
 CF_API cfStatus cfNvlsBind(cfComm_t comm);
+/* Emulated switch for one-process-per-GPU communicators (tests, boxes without
+ * multicast): `staging` (>= 32 B, 16-byte aligned, registered with
+ * cfBufferExport/cfBufferImport on every rank) is split into the input and
+ * output halves; switch_2pa then runs the NVLS kernel with per-rank loads /
+ * stores over the mapped peers' staging in place of multimem (the in-process
+ * twin is cfConfig.use_multicast = 2).  Replaces SwitchChannel
+ * (cf/channels.py:333-409) in emulation only. */
+CF_API cfStatus cfNvlsEmulate(cfComm_t comm, void* staging, size_t bytes);
 
 /* Channels for user kernels (the Primitive API; reference
  * MemoryChannel / PortChannel, cf/channels.py:54-330).  Fills `handle` with a

@@ -32,7 +32,8 @@ EXPORTS = (
     "cfStatusCode", "cfLastErrorMessage", "cfVersion", "cfCommInitAll", "cfCommCreateRank",
     "cfCommGetHandle", "cfCommConnect", "cfCommDestroy", "cfBufferExport", "cfBufferImport",
     "cfBufferRelease", "cfMemoryChannelCreate", "cfPortChannelCreate",
-    "cfDeviceMulticastSupported", "cfNvlsCreate", "cfNvlsImport", "cfNvlsBind", "cfCommNumRanks",
+    "cfDeviceMulticastSupported", "cfNvlsCreate", "cfNvlsImport", "cfNvlsBind", "cfNvlsEmulate",
+    "cfCommNumRanks",
     "cfCommLocalRanks",
     "cfCommMulticastSupported", "cfCommLastDeviceError", "cfCommClearDeviceError", "cfAllReduce",
     "cfAllGather", "cfReduceScatter", "cfAllReduceHost", "cfAllReduceHostStaged",
@@ -72,6 +73,7 @@ _PROTOS = {
     "cfNvlsCreate": ([vp, P(i32)], i32),
     "cfNvlsImport": ([vp, i32], i32),
     "cfNvlsBind": ([vp], i32),
+    "cfNvlsEmulate": ([vp, vp, sz], i32),
     "cfCommNumRanks": ([vp, P(i32)], i32),
     "cfCommLocalRanks": ([vp, P(i32), P(i32)], i32),
     "cfCommMulticastSupported": ([vp, P(i32)], i32),

@@ -239,6 +239,18 @@ class Communicator:
             os.close(fd.value)
         return ok
 
+    def setup_nvls_emulated(self, staging_bytes: int = 64 << 20) -> None:
+        """Collective: the emulated switch (no multicast object): every rank
+        registers a staging buffer (input + output halves) and switch_2pa runs
+        the NVLS kernel with per-rank loads / stores over the mapped peers'
+        staging in place of multimem.  Tests the one-process-per-GPU NVLS
+        control path on boxes without multicast."""
+        import torch
+        staging = torch.zeros(staging_bytes, dtype=torch.uint8, device=self.device)
+        self.register(staging)
+        _lib.check(_lib.lib().cfNvlsEmulate(self._comm, staging.data_ptr(), staging_bytes))
+        self._nvls_staging = staging
+
     def _multicast_capable(self) -> bool:
         from .world import device_multicast_capable
         return device_multicast_capable(self.device.index)

@@ -149,6 +149,10 @@ cfStatus nvls_setup_emulated(cfComm* c) {
 }
 
 void nvls_teardown(cfComm* c) {
+  if (c->nvls.emul && c->multiprocess) {   // staging is the caller's registered buffer
+    c->nvls = Nvls();
+    return;
+  }
   if (c->nvls.emul) {
     for (size_t li = 0; li < c->nvls.ranks.size(); li++) {
       cudaSetDevice(c->local[li].dev);
@@ -243,5 +247,29 @@ extern "C" cfStatus cfNvlsBind(cfComm_t c) {
   CF_TRY(bind_rank(c, 0));
   c->nvls.enabled = true;
   c->multicast_supported = true;
+  return CF_OK;
+}
+
+extern "C" cfStatus cfNvlsEmulate(cfComm_t c, void* staging, size_t bytes) {
+  if (!c || !staging) return fail(CF_E_CONFIG, "null argument");
+  if (!c->multiprocess) return fail(CF_E_CONFIG, "cfNvlsEmulate is for cfCommCreateRank communicators "
+                                                 "(in-process worlds: cfConfig.use_multicast = 2)");
+  if (c->nvls.enabled && !c->nvls.emul) return fail(CF_E_CONFIG, "a real multicast object is already bound");
+  const Registration* reg = c->find_reg(staging);
+  if (!reg) return fail(CF_E_TOPOLOGY, "staging %p is not registered (cfBufferExport/cfBufferImport)", staging);
+  const size_t off = (const char*)staging - reg->ptr;
+  if (off + bytes > reg->bytes) return fail(CF_E_OOB, "staging range exceeds its registration");
+  const size_t half = bytes / 2 / 16 * 16;
+  if (half == 0 || ((uintptr_t)staging & 15)) return fail(CF_E_BAD_ALIGN, "staging must be 16-byte aligned, >= 32 B");
+  c->nvls = Nvls();
+  c->nvls.half = half;
+  c->nvls.size = 2 * half;
+  c->nvls.ranks.assign(1, NvlsRank());
+  c->nvls.ranks[0].uc = (char*)staging;
+  c->nvls.peer_uc.assign(c->nranks, nullptr);
+  for (int q = 0; q < c->nranks; q++) c->nvls.peer_uc[q] = reg->peer[q] + off;
+  c->nvls.peer_uc[c->local[0].rank] = (char*)staging;
+  c->nvls.emul = true;
+  c->nvls.enabled = true;
   return CF_OK;
 }

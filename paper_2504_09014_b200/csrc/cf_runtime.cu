@@ -699,7 +699,9 @@ cfStatus nvls_allreduce(cfComm* c, const void* const* send, void* const* recv, s
       for (int p = 0; p < c->nranks; p++) rk.sem[p] = c->sem(li, p);
       rk.in[rk.rank] = (const char*)send[li];
       rk.out[rk.rank] = (char*)recv[li];
-      if (c->nvls.emul) {   // every rank's unicast staging (in-process only)
+      if (c->nvls.emul && c->multiprocess) {   // every rank's registered staging, mapped
+        for (int q = 0; q < c->nranks; q++) rk.nv[q] = c->nvls.peer_uc[q];
+      } else if (c->nvls.emul) {   // every rank's unicast staging (in-process)
         for (size_t q = 0; q < c->local.size(); q++) rk.nv[c->local[q].rank] = c->nvls.ranks[q].uc;
       } else {
         rk.nv[rk.rank] = c->nvls.ranks[li].uc;

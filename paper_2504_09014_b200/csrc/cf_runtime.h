@@ -92,7 +92,8 @@ struct NvlsRank {
 
 struct Nvls {
   bool enabled = false;
-  bool emul = false;            // emulated switch: cudaMalloc'd unicast staging, no multicast object
+  bool emul = false;            // emulated switch: unicast staging, no multicast object
+  std::vector<char*> peer_uc;   // emulated switch, one process per rank: every rank's staging (mapped)
   size_t half = 0;              // bytes of each half (input, output)
   size_t size = 0;              // 2*half rounded to the multicast granularity
   size_t gran = 0;

@@ -77,6 +77,17 @@ def _worker(rank, world, port, q):
             out[("norm", algo)] = (y.cpu().numpy().copy(), ro.cpu().numpy().copy())
             for t in (x, ro, y):
                 comm.deregister(t)
+        # NVLS kernel (K5) over the emulated switch: several pieces of a small
+        # staging half, ragged count, .sys handshakes across the processes
+        comm.setup_nvls_emulated(64 << 10)
+        ne = 50001
+        nx = gen_inputs(world, ne, "f32", "wide", 33)
+        ns = torch.from_numpy(nx[rank]).cuda()
+        nr = torch.empty_like(ns)
+        for _ in range(2):
+            comm.all_reduce(ns, nr, algo="switch_2pa")
+            torch.cuda.synchronize()
+        out[("nvls",)] = nr.cpu().numpy().copy()
         comm.check_device_error()
         comm.close()
         dist.barrier()
@@ -123,6 +134,9 @@ def test_two_processes_one_gpu_all_collectives():
     for r in range(world):
         assert np.array_equal(res[r][("host",)].view(np.uint32), hwant[r].view(np.uint32))
         assert np.array_equal(res[r][("host_small",)].view(np.uint32), hsmall[r].view(np.uint32))
+    nwant = oracle.allreduce(gen_inputs(world, 50001, "f32", "wide", 33), "switch_2pa", "f32")
+    for r in range(world):
+        assert np.array_equal(res[r][("nvls",)].view(np.uint32), nwant[r].view(np.uint32)), ("nvls", r)
     fx = gen_inputs(world, 6 * 1024, "f32", "uniform", 5)
     h = fx[0].astype(np.float32)
     for x in fx[1:]:
