@@ -39,22 +39,25 @@ def _worker(rank, world, port, q):
             recv = torch.empty_like(send)
             comm.register(send)
             comm.register(recv)
-            for algo in ("1pa", "2pa", "2pa_ll", "1pa_hb"):
+            for algo in ("1pa", "2pa", "2pa_ll", "1pa_hb", "2pr"):
                 name, var = (algo, "") if algo != "2pa_ll" else ("2pa", "ll")
                 comm.all_reduce(send, recv, algo=name, variant=var)
                 torch.cuda.synchronize()
                 out[("ar", algo, elems)] = recv.cpu().numpy().copy()
             ag = torch.empty(world * elems, device="cuda", dtype=torch.float32)
             comm.register(ag)
-            comm.all_gather(send, ag, algo="allpairs_ag")
-            torch.cuda.synchronize()
-            out[("ag", elems)] = ag.cpu().numpy().copy()
+            for algo in ("allpairs_ag", "ring_ag"):
+                ag.zero_()
+                comm.all_gather(send, ag, algo=algo)
+                torch.cuda.synchronize()
+                out[("ag", algo, elems)] = ag.cpu().numpy().copy()
             rs_in = torch.from_numpy(np.concatenate([ins[rank]] * world)).cuda()
             rs_out = torch.empty(elems, device="cuda", dtype=torch.float32)
             comm.register(rs_in)
-            comm.reduce_scatter(rs_in, rs_out, algo="rs_direct")
-            torch.cuda.synchronize()
-            out[("rs", elems)] = rs_out.cpu().numpy().copy()
+            for algo in ("rs_direct", "ring_rs"):
+                comm.reduce_scatter(rs_in, rs_out, algo=algo)
+                torch.cuda.synchronize()
+                out[("rs", algo, elems)] = rs_out.cpu().numpy().copy()
             for t in (send, recv, ag, rs_in):
                 comm.deregister(t)
         # pipelined host-buffer AllReduce (windows: >= 32 MiB per rank, ragged)
@@ -117,7 +120,7 @@ def test_two_processes_one_gpu_all_collectives():
         p.join(timeout=60)
     for elems in (1000, 65536 + 8):
         ins = gen_inputs(world, elems, "f32", "wide", 77 + elems)
-        for algo in ("1pa", "2pa", "2pa_ll", "1pa_hb"):
+        for algo in ("1pa", "2pa", "2pa_ll", "1pa_hb", "2pr"):
             want = oracle.allreduce(ins, {"2pa_ll": "2pa", "1pa_hb": "1pa"}.get(algo, algo), "f32")
             for r in range(world):
                 assert np.array_equal(res[r][("ar", algo, elems)].view(np.uint32),
@@ -125,9 +128,12 @@ def test_two_processes_one_gpu_all_collectives():
         cat = np.concatenate(ins)
         rs_ins = [np.concatenate([x] * world) for x in ins]
         rs_want = oracle.reducescatter(rs_ins, "direct", "f32")
+        rs_ring = oracle.reducescatter(rs_ins, "ring_rs", "f32")
         for r in range(world):
-            assert np.array_equal(res[r][("ag", elems)], cat)
-            assert np.array_equal(res[r][("rs", elems)].view(np.uint32), rs_want[r].view(np.uint32))
+            for algo in ("allpairs_ag", "ring_ag"):
+                assert np.array_equal(res[r][("ag", algo, elems)], cat), (algo, r)
+            assert np.array_equal(res[r][("rs", "rs_direct", elems)].view(np.uint32), rs_want[r].view(np.uint32))
+            assert np.array_equal(res[r][("rs", "ring_rs", elems)].view(np.uint32), rs_ring[r].view(np.uint32))
     hins = gen_inputs(world, (40 << 20) // 4 + 3, "f32", "uniform", 9)
     hwant = oracle.allreduce(hins, "2pa", "f32")
     hsmall = oracle.allreduce([x[:1000] for x in hins], "2pa", "f32")
