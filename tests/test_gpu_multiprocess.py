@@ -242,3 +242,77 @@ def test_two_processes_one_gpu_plans():
         want = oracle.run_plan(doc, ins, dtype=dtype)
         for r in range(world):
             assert np.array_equal(res[r][(name, var)].view(np.uint8), want[r].view(np.uint8)), (name, var, r)
+
+
+def _worker4(rank, world, port, q):
+    try:
+        import sys
+        root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+        sys.path[:0] = [root, os.path.join(root, "tests", "golden")]
+        import torch
+        import torch.distributed as dist
+        from inputs import gen_inputs
+        from paper_2504_09014_b200.comm import Communicator
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                                world_size=world)
+        comm = Communicator(spin_timeout_ms=120000)
+        out = {}
+        elems = 4096 + 8
+        ins = gen_inputs(world, elems, "bf16", "normal", 41)
+        send = torch.from_numpy(ins[rank].view(np.int16)).cuda().view(torch.bfloat16)
+        recv = torch.empty_like(send)
+        ag = torch.empty(world * elems, device="cuda", dtype=torch.bfloat16)
+        for t in (send, recv, ag):
+            comm.register(t)
+        for algo in ("1pa", "2pa", "2pa_ll", "2pr"):
+            name, var = (algo, "") if algo != "2pa_ll" else ("2pa", "ll")
+            comm.all_reduce(send, recv, algo=name, variant=var)
+            torch.cuda.synchronize()
+            out[("ar", algo)] = recv.view(torch.int16).cpu().numpy().view(np.uint16).copy()
+        comm.all_gather(send, ag, algo="allpairs_ag")
+        torch.cuda.synchronize()
+        out[("ag",)] = ag.view(torch.int16).cpu().numpy().view(np.uint16).copy()
+        comm.setup_nvls_emulated(16 << 10)
+        comm.all_reduce(send, recv, algo="switch_2pa")
+        torch.cuda.synchronize()
+        out[("nvls",)] = recv.view(torch.int16).cpu().numpy().view(np.uint16).copy()
+        comm.check_device_error()
+        comm.close()
+        dist.destroy_process_group()
+        q.put((rank, out, None))
+    except Exception as e:   # report to the parent instead of hanging it
+        import traceback
+        q.put((rank, None, traceback.format_exc()))
+
+
+def test_four_processes_one_gpu():
+    """Four ranks, one process each, sharing cuda:0 (time-sliced contexts):
+    the n > 2 peer tables of the multi-process path (registration, handshakes,
+    LL slots, ring links, emulated NVLS staging) vs the oracle, bf16."""
+    from oracle import oracle
+    from inputs import gen_inputs
+    world = 4
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker4, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        r, out, err = q.get(timeout=900)
+        assert err is None, err
+        res[r] = out
+    for p in procs:
+        p.join(timeout=60)
+    ins = gen_inputs(world, 4096 + 8, "bf16", "normal", 41)
+    for algo in ("1pa", "2pa", "2pa_ll", "2pr"):
+        want = oracle.allreduce(ins, "2pa" if algo == "2pa_ll" else algo, "bf16")
+        for r in range(world):
+            assert np.array_equal(res[r][("ar", algo)], want[r]), (algo, r)
+    cat = np.concatenate(ins)
+    nwant = oracle.allreduce(ins, "switch_2pa", "bf16")
+    for r in range(world):
+        assert np.array_equal(res[r][("ag",)], cat)
+        assert np.array_equal(res[r][("nvls",)], nwant[r])
