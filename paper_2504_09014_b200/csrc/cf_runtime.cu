@@ -61,7 +61,11 @@ int max_blocks_per_rank(cfComm* c, const void* kernel, int group, int threads, i
   int occ = occupancy(c, kernel, dev, threads);
   if (per_sm > 0) occ = std::min(occ, per_sm);
   const int cap = occ * c->sm_count[dev];
-  int mb = std::max(1, cap / (int)g.size());
+  // every rank on this device shares its SMs (one launch per device, or one
+  // per rank with CF_SPLIT_GROUPS): all CTAs of a call must be co-resident
+  int on_dev = 0;
+  for (const auto& lr : c->local) on_dev += lr.dev == dev;
+  int mb = std::max(1, cap / std::max(on_dev, (int)g.size()));
   mb = std::min(mb, CF_MAX_BLOCKS);
   if (c->cfg.max_blocks > 0) mb = std::min(mb, c->cfg.max_blocks);
   return mb;
@@ -128,6 +132,13 @@ static void apply_defaults(cfConfig* cfg) {
 
 static void build_groups(cfComm* c) {
   c->groups.clear();
+  // CF_SPLIT_GROUPS=1 (tests): one launch per rank even when ranks share a
+  // device -- the multi-GPU in-process path (per-device launches, .sys
+  // handshakes) exercised on one GPU; the caller supplies one stream per rank
+  if (getenv("CF_SPLIT_GROUPS") && *getenv("CF_SPLIT_GROUPS") == '1' && !c->multiprocess) {
+    for (int li = 0; li < (int)c->local.size(); li++) c->groups.push_back({li});
+    return;
+  }
   std::map<int, int> by_dev;
   for (int li = 0; li < (int)c->local.size(); li++) {
     const int d = c->local[li].dev;

@@ -116,6 +116,15 @@ class World:
 
     def streams(self):
         import torch
+        if os.environ.get("CF_SPLIT_GROUPS") == "1" and len(set(self.devices)) < self.num_ranks:
+            # one launch per rank on a shared device (test mode of libcf's
+            # per-device launch path): each rank needs its own stream, ordered
+            # after the caller's current stream
+            if getattr(self, "_rank_streams", None) is None:
+                self._rank_streams = [torch.cuda.Stream(self.device(r)) for r in range(self.num_ranks)]
+            for r, st in enumerate(self._rank_streams):
+                st.wait_stream(torch.cuda.current_stream(self.device(r)))
+            return [st.cuda_stream for st in self._rank_streams]
         return [torch.cuda.current_stream(self.device(r)).cuda_stream for r in range(self.num_ranks)]
 
     def synchronize(self):

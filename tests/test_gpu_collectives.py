@@ -356,3 +356,62 @@ def test_cuda_graph_replay_advances_epochs():
     for rt, _ in plans.values():
         rt.check_device_error()
         rt.close()
+
+
+def test_one_launch_per_rank_path(monkeypatch):
+    """CF_SPLIT_GROUPS=1: ranks that share cuda:0 are launched one kernel per
+    rank on their own streams -- the in-process multi-GPU path (per-device
+    launches, .sys handshakes, no single-launch shortcuts) of
+    make_world(1, 8) on an 8-GPU box, exercised on one GPU.  Every hand
+    kernel, K13 and two DSL plans vs the oracle."""
+    import torch
+    from paper_2504_09014_b200 import Runtime, allreduce_add_rmsnorm, collective, make_world, parse_plan
+    from paper_2504_09014_b200.plan import scale_plan
+    monkeypatch.setenv("CF_SPLIT_GROUPS", "1")
+    n = 4
+    w = make_world(1, n, devices=[0] * n, spin_timeout_ms=10000)
+    try:
+        for elems, dtype in ((5000, "f32"), (70001, "bf16")):
+            dist = "wide" if dtype == "f32" else "normal"
+            ins = gen_inputs(n, elems, dtype, dist, 500 + elems % 11)
+            for algo, var in ALGOS:
+                got = collective("allreduce", ins, w, dtype=dtype, algo=algo, variant=var)
+                want = oracle.allreduce(ins, _ORACLE_NAME.get(algo, algo), dtype)
+                for r in range(n):
+                    assert np.array_equal(got[r].view(np.uint8), want[r].view(np.uint8)), (algo, var, r)
+            assert len(w._rank_streams) == n   # the per-rank launch path is the one that ran
+            for algo in ("ring_rs", "rs_direct"):
+                got = collective("reducescatter", ins, w, dtype=dtype, algo=algo)
+                want = oracle.reducescatter(ins, "ring_rs" if algo == "ring_rs" else "direct", dtype)
+                for r in range(n):
+                    assert np.array_equal(got[r].view(np.uint8), want[r].view(np.uint8)), (algo, r)
+            for algo in ("allpairs_ag", "ring_ag"):
+                got = collective("allgather", ins, w, dtype=dtype, algo=algo)
+                for g, wnt in zip(got, oracle.allgather(ins)):
+                    assert np.array_equal(g.view(np.uint8), wnt.view(np.uint8)), algo
+        # K13, both algorithms (residual output is the oracle sum + residual, bit for bit)
+        xs = gen_inputs(n, 8 * 512, "f32", "uniform", 61)
+        res = gen_inputs(1, 8 * 512, "f32", "uniform", 62)[0]
+        h = oracle.allreduce(xs, "oracle", "f32")[0]
+        for algo in ("1pa_hb", "2pa"):
+            xt = [torch.from_numpy(x).cuda().view(8, 512) for x in xs]
+            rt = [torch.from_numpy(res).cuda().view(8, 512) for _ in range(n)]
+            allreduce_add_rmsnorm(w, xt, rt, torch.ones(512, device="cuda"), eps=1e-6, algo=algo)
+            w.synchronize()
+            for r in range(n):
+                assert np.array_equal(rt[r].cpu().numpy().reshape(-1).view(np.uint32),
+                                      (h + res).astype(np.float32).view(np.uint32)), (algo, r)
+        # DSL plans (HB and LL) through K10
+        for name in ("2pa_memory_n4_e8", "1pa_n4_e8"):
+            with open(os.path.join(GOLD, "plans", name + ".json"), "rb") as f:
+                plan = scale_plan(parse_plan(f.read()), 512)
+            rt_ = Runtime(plan, w, dtype="f32")
+            pins = gen_inputs(n, rt_.in_elems, "f32", "int", 63)
+            outs = rt_.execute(pins).outputs
+            want = oracle.allreduce(pins, "oracle", "f32")
+            for r in range(n):
+                assert np.array_equal(outs[r][:len(want[r])], want[r]), (name, r)
+            rt_.close()
+        w.check_device_error()
+    finally:
+        w.close()
