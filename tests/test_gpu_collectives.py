@@ -369,8 +369,16 @@ def test_one_launch_per_rank_path(monkeypatch):
     from paper_2504_09014_b200.plan import scale_plan
     monkeypatch.setenv("CF_SPLIT_GROUPS", "1")
     n = 4
-    w = make_world(1, n, devices=[0] * n, spin_timeout_ms=10000)
+    w = make_world(1, n, devices=[0] * n, spin_timeout_ms=10000, use_multicast="emulate",
+                   nvls_bytes=64 << 10)
     try:
+        # host tensors: the pipelined H2D / kernel / D2H path (windows of >= 32 MiB per rank)
+        hins = gen_inputs(n, (36 << 20) // 4 + 5, "f32", "uniform", 64)
+        got = collective("allreduce", [torch.from_numpy(x).pin_memory() for x in hins], w, dtype="f32",
+                         algo="2pa")
+        want = oracle.allreduce(hins, "2pa", "f32")
+        for r in range(n):
+            assert np.array_equal(got[r].numpy().view(np.uint32), want[r].view(np.uint32)), ("host", r)
         for elems, dtype in ((5000, "f32"), (70001, "bf16")):
             dist = "wide" if dtype == "f32" else "normal"
             ins = gen_inputs(n, elems, dtype, dist, 500 + elems % 11)
