@@ -474,6 +474,7 @@ def multi_sweep(comm, dev, world, send, recv):
     the caller takes the max over ranks."""
     import torch
     import torch.distributed as dist
+    from paper_2504_09014_b200 import _lib
     nccl = None
     try:
         nccl = dist.new_group(backend="nccl")
@@ -543,17 +544,44 @@ def multi_sweep(comm, dev, world, send, recv):
             rows.append(row)
     # NVLS (switch_2pa, multimem ld_reduce / st) when the box builds a multicast object
     nvls = False
+    nvls_kind = "nvls"
     try:
         nvls = comm.setup_nvls()
+        if not nvls and os.environ.get("CF_BENCH_ONE_GPU"):
+            # path check on a 1-GPU box: the emulated switch runs the same
+            # kernel and bench code (rows labelled as such, not an NVLS number)
+            comm.setup_nvls_emulated(64 << 20)
+            nvls, nvls_kind = True, "nvls_emulated"
     except Exception as e:   # report, never fail the bench
         rows.append({"bytes": 0, "kind": "nvls", "error": f"{type(e).__name__}: {e}"[:200]})
+    if nvls:
+        # first real multimem execution on this box: check it against the
+        # two-shot result (switch order is unspecified: tolerance) before
+        # timing; any failure drops the NVLS rows, never the bench line
+        try:
+            cnt = MiB // 2
+            x, y = bs[:cnt], br[:cnt]   # registered buffers (the HB check writes peers' recv)
+            comm.all_reduce(x, y, algo="2pa")
+            y2 = y.clone()
+            comm.all_reduce(x, y, algo="switch_2pa")
+            torch.cuda.synchronize(dev)
+            comm.check_device_error()
+            ok = bool(torch.allclose(y.float(), y2.float(), rtol=2 ** -7, atol=1e-2))
+            flags = [None] * world
+            dist.all_gather_object(flags, ok)
+            if not all(flags):
+                raise RuntimeError("switch_2pa result differs from 2pa")
+        except Exception as e:
+            nvls = False
+            _lib.lib().cfCommClearDeviceError(comm.comm)
+            rows.append({"bytes": 0, "kind": "nvls", "error": f"{type(e).__name__}: {e}"[:200]})
     if nvls:
         for nb in [MiB << (2 * i) for i in range(6)]:
             if nb > big:
                 break
             cnt = nb // 2
             x, y = bs[:cnt], br[:cnt]
-            rows.append({"bytes": nb, "kind": "nvls", "cf_graph_s": time_graph(
+            rows.append({"bytes": nb, "kind": nvls_kind, "cf_graph_s": time_graph(
                 dev, lambda: comm.all_reduce(x, y, algo="switch_2pa"), 10, 3)})
     comm.deregister(bs)
     comm.deregister(br)
@@ -597,7 +625,7 @@ def gather_max_over_ranks(t_local, e2e_local, rows_local, world, group=None):
         for key in ("cf_graph_s", "cf_eager_s", "nccl_eager_s", "cf_plan_graph_s"):
             if key in row:
                 tk = max(x[2][i][key] for x in times)   # max over ranks
-                bw = busbw(nb, tk, world) if kind in ("allreduce", "nvls") else \
+                bw = busbw(nb, tk, world) if kind in ("allreduce", "nvls", "nvls_emulated") else \
                     (nb / tk / 1e9 * (world - 1) / world if tk > 0 else 0.0)
                 out[key[:-2]] = {"us": round(tk * 1e6, 2), "busbw": round(bw, 2)}
         sweep.append(out)
