@@ -165,11 +165,12 @@ static int select_algo(const cfComm* c, int coll, size_t nbytes, int dtype) {
   if (c->nranks == 1) return CF_ALGO_2PA;
   if (coresident) {
     // Ranks share one GPU (one launch, no handshakes).  Measured (bench sweep,
-    // bf16, 8 ranks, L2 flushed): the whole-vector pull (1pa_hb) has the
-    // lowest latency up to 64 KiB (3.9-4.7 us vs 5.0-5.8 us for 2pa, 5.5-12 us
-    // for LL, which doubles the bytes); the two-shot pull moves the minimum
-    // bytes and wins from 256 KiB on (5.9 vs 6.4 us) to 1 GiB.
-    if (nbytes <= 64 * 1024) return CF_ALGO_1PA_HB;
+    // bf16, 8 ranks, L2 flushed, profiles/round1/bench_line.json): the
+    // whole-vector pull (1pa_hb) has the lowest latency up to 256 KiB
+    // (3.3-4.4 us vs 4.3-4.8 us for 2pa, 3.4-13 us for LL, which doubles the
+    // bytes); the two-shot pull moves the minimum bytes and wins from 1 MiB
+    // on (5.9 vs 10.1 us) to 1 GiB.
+    if (nbytes <= 256 * 1024) return CF_ALGO_1PA_HB;
     return CF_ALGO_2PA;
   }
   if (nbytes < 256 * 1024 && nbytes <= c->cfg.ll_max_bytes) return CF_ALGO_1PA;
