@@ -787,6 +787,8 @@ extern "C" cfStatus cfAllReduce(cfComm_t c, const void* const* send, void* const
       j.work = ceil_div(j.cs, V) + 1;
       break;
     case CF_ALGO_2PA_LL: {
+      if (bytes > c->cfg.ll_max_bytes)   // cfConfig.ll_max_bytes bounds every LL algorithm
+        return fail(CF_E_BAD_SIZE, "2pa_ll: %zu bytes exceed the LL capacity %zu", bytes, c->cfg.ll_max_bytes);
       j.kind = kLL2;
       j.cs = round_up(count, n) / n;
       j.slot = c->lay.half / (2 * n) / 256 * 256;

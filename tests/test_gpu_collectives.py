@@ -192,6 +192,56 @@ def test_large_allreduce_property():
     w.check_device_error()
 
 
+def test_maximum_size_allreduce_and_allgather():
+    """BASELINE's largest sweep point, 1 GiB per rank x 8 co-resident ranks
+    (16 GiB resident): integer-valued bf16 two-shot sums are exact and equal
+    on every rank; the 8 GiB AllGather output is bit-exact (sampled)."""
+    import torch
+    from paper_2504_09014_b200 import collectives as C
+    from paper_2504_09014_b200 import _lib
+    n = 8
+    w = world(n)
+    elems = 512 << 20   # 1 GiB of bf16 per rank
+    send = [torch.randint(-8, 8, (elems,), device=w.device(r), dtype=torch.int8).to(torch.bfloat16)
+            for r in range(n)]
+    recv = [torch.empty_like(s) for s in send]
+    C.run("allreduce", send, recv, elems, "bf16", _lib.ALGOS["2pa"], w)
+    w.synchronize()
+    want = torch.zeros(elems, device=w.device(0))
+    for s_ in send:
+        want += s_.float()
+    for o in recv:
+        assert torch.equal(o.float(), want)
+    del recv, want
+    shard = elems // n
+    out = [torch.empty(elems, device=w.device(r), dtype=torch.bfloat16) for r in range(n)]
+    C.run("allgather", [s_[:shard] for s_ in send], out, shard, "bf16", _lib.ALGOS["allpairs_ag"], w)
+    w.synchronize()
+    idx = torch.randint(0, elems, (1 << 20,), device=w.device(0))
+    cat = torch.cat([s_[:shard] for s_ in send])
+    for o in out:
+        assert torch.equal(o[idx].view(torch.int16), cat[idx].view(torch.int16))
+    w.check_device_error()
+
+
+def test_ll_capacity_boundary():
+    """LL algorithms accept exactly ll_max_bytes per rank and reject one
+    element more with E_BAD_SIZE (the scratch is sized for it)."""
+    from paper_2504_09014_b200 import collective
+    from paper_2504_09014_b200.errors import BadSizeError
+    n, cap = 4, 1 << 16
+    w = world(n, ll_max_bytes=cap)
+    ins = gen_inputs(n, cap // 4, "f32", "int", 71)
+    for algo, var in (("1pa", ""), ("2pa", "ll")):
+        got = collective("allreduce", ins, w, dtype="f32", algo=algo, variant=var)
+        want = oracle.allreduce(ins, "1pa" if algo == "1pa" else "2pa", "f32")
+        for r in range(n):
+            assert np.array_equal(got[r], want[r]), (algo, r)
+        with pytest.raises(BadSizeError):
+            collective("allreduce", gen_inputs(n, cap // 4 + 1, "f32", "int", 72), w, dtype="f32",
+                       algo=algo, variant=var)
+
+
 def test_errors_map_to_reference_codes():
     import torch
     from paper_2504_09014_b200 import collective, collectives as C, _lib
