@@ -41,3 +41,10 @@ def gen_inputs(n: int, elems: int, dtype: str, dist: str, seed: int, scale: floa
             a = a.astype(np.int32)
         out.append(a)
     return out
+
+
+def ag_bf16_shards(n: int, cnt: int, seed: int):
+    """bf16 AllGather inputs of ag_bf16.json: random 16-bit patterns (NaNs
+    included) as uint16, one array per rank."""
+    rng = np.random.default_rng(seed)
+    return [rng.integers(0, 1 << 16, cnt, dtype=np.uint32).astype(np.uint16) for _ in range(n)]

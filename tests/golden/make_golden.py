@@ -20,6 +20,13 @@ Fixtures
   ll_packets.json    reference MemoryChannel.put_ll byte layout  cf/channels.py:244-280
   frontend/*.json    the reference's TS-frontend golden documents (data), used
                      as pre-lowering inputs       pkg/tests/golden/frontend_*.json
+  ag_bf16.json       bf16 AllGather through the reference: each rank's bf16
+                     shard (random 16-bit patterns, NaNs included) viewed as
+                     i32 words -- odd counts padded by one uint16 per shard,
+                     stripped afterwards -- and gathered by collective("allgather",
+                     algo=allpairs_ag | ring_ag)      cf/collectives.py:253-270, 82-104
+                     (`python tests/golden/make_golden.py --ag-bf16` regenerates
+                     only this file)
 """
 
 from __future__ import annotations
@@ -39,7 +46,7 @@ sys.path.insert(0, HERE)
 os.environ.setdefault("PYTHONDONTWRITEBYTECODE", "1")
 sys.dont_write_bytecode = True
 
-from inputs import gen_inputs  # noqa: E402
+from inputs import ag_bf16_shards, gen_inputs  # noqa: E402
 
 from commforge import collective, make_world  # noqa: E402
 from commforge.channels import LL, MemoryChannel  # noqa: E402
@@ -186,7 +193,35 @@ def copy_frontend():
     print("frontend goldens copied")
 
 
+def make_ag_bf16():
+    cases = []
+    for n in (2, 4, 8):
+        for cnt in (2, 7, 64, 4097):
+            seed = 500 * n + cnt
+            shards = ag_bf16_shards(n, cnt, seed)
+            pad = cnt % 2
+            words = [np.concatenate([s_, np.zeros(pad, np.uint16)]).view(np.int32) for s_ in shards]
+            for algo in ("allpairs_ag", "ring_ag"):
+                world = make_world(1, n, "switch-attached", 0)
+                outs = collective("allgather", words, world, dtype="i32", algo=algo)
+                got = []
+                for o in outs:
+                    half = np.asarray(o).view(np.uint16).reshape(n, cnt + pad)[:, :cnt]
+                    got.append(half.reshape(-1))
+                cat = np.concatenate(shards)
+                assert all(np.array_equal(g, cat) for g in got), (n, cnt, algo)
+                cases.append({"n": n, "count": cnt, "seed": seed, "algo": algo,
+                              "digests": [digest(g) for g in got]})
+    with open(os.path.join(HERE, "ag_bf16.json"), "w") as f:
+        json.dump(cases, f, indent=0)
+    print(f"ag_bf16: {len(cases)} cases")
+
+
 if __name__ == "__main__":
+    if "--ag-bf16" in sys.argv:
+        make_ag_bf16()
+        sys.exit(0)
+    make_ag_bf16()
     make_ll()
     make_plans()
     make_collectives()

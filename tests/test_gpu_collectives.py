@@ -473,3 +473,16 @@ def test_one_launch_per_rank_path(monkeypatch):
         w.check_device_error()
     finally:
         w.close()
+
+
+def test_bf16_allgather_matches_reference_digests():
+    """libcf's bf16 AllGather (both algorithms) returns the bytes the reference
+    itself produced for the same shards (tests/golden/ag_bf16.json)."""
+    from inputs import ag_bf16_shards
+    from paper_2504_09014_b200 import collective
+    with open(os.path.join(GOLD, "ag_bf16.json")) as f:
+        cases = json.load(f)
+    for c in cases:
+        shards = ag_bf16_shards(c["n"], c["count"], c["seed"])
+        got = collective("allgather", shards, world(c["n"]), dtype="bf16", algo=c["algo"])
+        assert [_digest(g) for g in got] == c["digests"], (c["n"], c["count"], c["algo"])

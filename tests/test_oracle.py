@@ -128,3 +128,18 @@ def test_threaded_reduce_matches_single_thread():
     a = oracle.reduce_ordered("f32", ins, list(range(8)), nthreads=1)
     b = oracle.reduce_ordered("f32", ins, list(range(8)), nthreads=0)
     assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+
+
+def test_oracle_bf16_allgather_matches_reference():
+    """bf16 AllGather digests produced by the reference itself (i32 view of
+    the 16-bit shards, tests/golden/make_golden.py --ag-bf16) pin the oracle."""
+    import hashlib
+    from inputs import ag_bf16_shards
+    with open(os.path.join(GOLD, "ag_bf16.json")) as f:
+        cases = json.load(f)
+    assert len(cases) == 24
+    for c in cases:
+        shards = ag_bf16_shards(c["n"], c["count"], c["seed"])
+        for r, o in enumerate(oracle.allgather(shards)):
+            assert hashlib.sha256(np.ascontiguousarray(o).view(np.uint8).tobytes()).hexdigest() == \
+                c["digests"][r], (c["n"], c["count"], c["algo"], r)
