@@ -27,6 +27,12 @@ Fixtures
                      algo=allpairs_ag | ring_ag)      cf/collectives.py:253-270, 82-104
                      (`python tests/golden/make_golden.py --ag-bf16` regenerates
                      only this file)
+  lowp.json          f16 / bf16 AllReduce anchored on the reference: the
+                     reference has 4-byte types only (cf/dtypes.py:7-8), so each
+                     case runs the reference's f32 path on the exactly-upcast
+                     inputs (its order, f32 adds) and rounds the result once to
+                     the 2-byte type (RNE) -- the semantics the kernels
+                     implement (`--lowp` regenerates only this file)
 """
 
 from __future__ import annotations
@@ -217,11 +223,49 @@ def make_ag_bf16():
     print(f"ag_bf16: {len(cases)} cases")
 
 
+def _round16(x: np.ndarray, dtype: str) -> np.ndarray:
+    """f32 -> f16 / bf16 bit patterns, round to nearest even (finite inputs)."""
+    x = np.ascontiguousarray(x, np.float32)
+    if dtype == "f16":
+        return x.astype(np.float16).view(np.uint16)
+    u = x.view(np.uint32).astype(np.uint64)
+    return ((u + 0x7FFF + ((u >> 16) & 1)) >> 16).astype(np.uint16)
+
+
+def _up32(a: np.ndarray, dtype: str) -> np.ndarray:
+    if dtype == "f16":
+        return np.asarray(a, np.float16).astype(np.float32)
+    return (np.asarray(a, np.uint16).astype(np.uint32) << 16).view(np.float32)
+
+
+def make_lowp():
+    cases = []
+    for n in (2, 4, 8):
+        for elems in (7, 64, 3 * n + 1, 512):
+            for dtype in ("f16", "bf16"):
+                seed = 700 * n + elems + (1 if dtype == "bf16" else 0)
+                ins = gen_inputs(n, elems, dtype, "normal", seed)
+                up = [_up32(a, dtype) for a in ins]
+                for algo, var in AR:
+                    world = make_world(1, n, "switch-attached", 0)
+                    outs = collective("allreduce", up, world, dtype="f32", algo=algo, variant=var)
+                    cases.append({"n": n, "elems": elems, "dtype": dtype, "seed": seed, "algo": algo,
+                                  "variant": var,
+                                  "digests": [digest(_round16(np.asarray(o), dtype)) for o in outs]})
+    with open(os.path.join(HERE, "lowp.json"), "w") as f:
+        json.dump(cases, f, indent=0)
+    print(f"lowp: {len(cases)} cases")
+
+
 if __name__ == "__main__":
+    if "--lowp" in sys.argv:
+        make_lowp()
+        sys.exit(0)
     if "--ag-bf16" in sys.argv:
         make_ag_bf16()
         sys.exit(0)
     make_ag_bf16()
+    make_lowp()
     make_ll()
     make_plans()
     make_collectives()

@@ -486,3 +486,20 @@ def test_bf16_allgather_matches_reference_digests():
         shards = ag_bf16_shards(c["n"], c["count"], c["seed"])
         got = collective("allgather", shards, world(c["n"]), dtype="bf16", algo=c["algo"])
         assert [_digest(g) for g in got] == c["digests"], (c["n"], c["count"], c["algo"])
+
+
+def test_lowp_allreduce_matches_reference_f32_path():
+    """f16 / bf16 AllReduce on the GPU (every hand-kernel algorithm) returns
+    the bytes of the reference's f32 path on the upcast inputs rounded once to
+    the 2-byte type (tests/golden/lowp.json).  The 2pa *port* variant runs as
+    a DSL plan whose intermediate buffers have the 2-byte type, so it rounds
+    per plan op (checked against the oracle's plan interpreter in
+    test_gpu_plans) and is not part of this round-once table."""
+    from paper_2504_09014_b200 import collective
+    with open(os.path.join(GOLD, "lowp.json")) as f:
+        cases = [c for c in json.load(f) if c["variant"] != "port"]
+    assert len(cases) == 120
+    for c in cases:
+        ins = gen_inputs(c["n"], c["elems"], c["dtype"], "normal", c["seed"])
+        got = collective("allreduce", ins, world(c["n"]), dtype=c["dtype"], algo=c["algo"], variant=c["variant"])
+        assert [_digest(g) for g in got] == c["digests"], (c["n"], c["elems"], c["dtype"], c["algo"], c["variant"])

@@ -160,3 +160,24 @@ def test_runtime_rejects_bad_plans():
     rt = Runtime(plan, world(4))
     with pytest.raises(ShapeError):
         rt.execute([np.zeros(7, np.int32)] * 4)
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f16"])
+@pytest.mark.parametrize("algo,var", [("2pa", "port"), ("2pa", "memory"), ("2pa", "ll"), ("1pa", ""),
+                                      ("2pr", ""), ("switch_2pa", "")])
+def test_dsl_path_low_precision_vs_plan_oracle(algo, var, dtype):
+    """2-byte types through the DSL path: the plan's buffers have the 2-byte
+    type, so every reduce op rounds; the GPU interpreter's bytes equal the
+    oracle's sequential plan interpreter on the same lowered plan."""
+    from paper_2504_09014_b200 import collective, serialize_plan
+    from paper_2504_09014_b200.algorithms import build_algo
+    from paper_2504_09014_b200.lowering import LoweringParams, lower
+    n, elems = 8, 8 * 96
+    ins = gen_inputs(n, elems, dtype, "normal", 91)
+    got = collective("allreduce", ins, world(n), dtype=dtype, algo=algo, variant=var, via_plan=True)
+    proto = "LL" if algo == "1pa" or var == "ll" else "HB"
+    params = LoweringParams(n, elems, dtype, proto)
+    doc = serialize_plan(lower(build_algo(algo, params, variant=var), params))
+    want = oracle.run_plan(doc, ins, dtype=dtype)
+    for r in range(n):
+        assert np.array_equal(got[r].view(np.uint8), want[r][:elems].view(np.uint8)), r

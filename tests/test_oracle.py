@@ -143,3 +143,23 @@ def test_oracle_bf16_allgather_matches_reference():
         for r, o in enumerate(oracle.allgather(shards)):
             assert hashlib.sha256(np.ascontiguousarray(o).view(np.uint8).tobytes()).hexdigest() == \
                 c["digests"][r], (c["n"], c["count"], c["algo"], r)
+
+
+def _lowp_cases():
+    with open(os.path.join(GOLD, "lowp.json")) as f:
+        return json.load(f)
+
+
+def test_oracle_lowp_allreduce_matches_reference_f32_path():
+    """f16 / bf16 AllReduce: the oracle equals the reference's own f32 path on
+    the exactly-upcast inputs, rounded once (tests/golden/make_golden.py --lowp)
+    -- the 2-byte semantics anchored on reference outputs, every algorithm."""
+    import hashlib
+    cases = _lowp_cases()
+    assert len(cases) == 144
+    for c in cases:
+        ins = gen_inputs(c["n"], c["elems"], c["dtype"], "normal", c["seed"])
+        name = {"2pa": "2pa"}.get(c["algo"], c["algo"])
+        outs = oracle.allreduce(ins, name, c["dtype"])
+        got = [hashlib.sha256(np.ascontiguousarray(o).view(np.uint8).tobytes()).hexdigest() for o in outs]
+        assert got == c["digests"], (c["n"], c["elems"], c["dtype"], c["algo"], c["variant"])
