@@ -241,6 +241,9 @@ __global__ void __launch_bounds__(512) pull_reduce_kernel(const __grid_constant_
 // read; the read phase keeps every peer's packet in flight and re-polls all
 // unstamped ones per round (ll16_poll): waiting for n-1 peers costs one round
 // trip per round, not one per peer.
+#ifndef CF_LL1_STREAM
+#define CF_LL1_STREAM 1
+#endif
 template <typename T, int NR>
 __global__ void __launch_bounds__(512, 2) ll_oneshot_kernel(const __grid_constant__ CollArgs a) {
   const RankCtx& rk = a.rk[blockIdx.y];
@@ -258,16 +261,13 @@ __global__ void __launch_bounds__(512, 2) ll_oneshot_kernel(const __grid_constan
   const uint32_t flag = ll_flag(e);
   const size_t par = (e & 1) * a.half;
 
-  for (size_t u = t0; u < nunit; u += stride) {
-    const uint2 x = u == t0 ? first : load_unit<T>(rk.in[r], u, a.count);
+  const uint32_t all = (1u << (n - 1)) - 1u;
+  auto put = [&](size_t u, uint2 x) {
 #pragma unroll
     for (int p = 0; p < NR; p++)
       if (p < n && p != r) ll16_put_scoped(rk.scr[p] + par + (size_t)r * a.slot + u * 16, x, flag, a.gpu_scope);
-  }
-  TS_MARK();
-  const uint32_t all = (1u << (n - 1)) - 1u;
-  for (size_t u = t0; u < nunit; u += stride) {
-    const uint2 own = u == t0 ? first : load_unit<T>(rk.in[r], u, a.count);
+  };
+  auto read = [&](size_t u, uint2 own) {
     const char* base = rk.scr[r] + par + u * 16;
     uint4 pk[P];
 #pragma unroll
@@ -279,7 +279,25 @@ __global__ void __launch_bounds__(512, 2) ll_oneshot_kernel(const __grid_constan
 #pragma unroll
     for (int i = 0; i < P; i++) x[i + 1] = make_uint2(pk[i].x, pk[i].z);
     store_unit<T>(rk.out[r], u, reduce_units<T, NR>(x, n), a.count);
+  };
+#if CF_LL1_STREAM
+  // Streamed: every thread reads unit u one iteration after putting it (the
+  // peers' threads with the same index put it at about the same time), so
+  // packets are consumed while they are still in L2 instead of after the
+  // whole message was scattered (lag 1 hides the flag round trip).
+  uint2 prev = first;
+  for (size_t u = t0; u < nunit; u += stride) {
+    const uint2 x = u == t0 ? first : load_unit<T>(rk.in[r], u, a.count);
+    put(u, x);
+    if (u != t0) read(u - stride, prev);
+    prev = x;
   }
+  if (t0 < nunit) read(t0 + (nunit - 1 - t0) / stride * stride, prev);
+#else
+  for (size_t u = t0; u < nunit; u += stride) put(u, u == t0 ? first : load_unit<T>(rk.in[r], u, a.count));
+  TS_MARK();
+  for (size_t u = t0; u < nunit; u += stride) read(u, u == t0 ? first : load_unit<T>(rk.in[r], u, a.count));
+#endif
   TS_MARK();
   end_call(rk, e);
   TS_MARK();
