@@ -284,7 +284,10 @@ __global__ void __launch_bounds__(512, 2) ll_oneshot_kernel(const __grid_constan
   // Streamed: every thread reads unit u one iteration after putting it (the
   // peers' threads with the same index put it at about the same time), so
   // packets are consumed while they are still in L2 instead of after the
-  // whole message was scattered (lag 1 hides the flag round trip).
+  // whole message was scattered (lag 1 hides the flag round trip).  Every rank
+  // launches the same grid (same count, same occupancy on a homogeneous box),
+  // so the unit a thread waits for was put, one iteration earlier, by a
+  // thread that is itself never waiting on a later unit.
   uint2 prev = first;
   for (size_t u = t0; u < nunit; u += stride) {
     const uint2 x = u == t0 ? first : load_unit<T>(rk.in[r], u, a.count);

@@ -15,7 +15,7 @@ def main():
         w = make_world(1, n, devices=[0] * n, max_blocks=mb)
         dev = w.device(0)
         row = []
-        for nb in (16 << 20, 256 << 20):
+        for nb in [int(x) << 20 for x in os.environ.get("MIB", "16,256").split(",")]:
             cnt = nb // 2
             send = [torch.randn(cnt, device=dev).to(torch.bfloat16) for _ in range(n)]
             recv = [torch.empty_like(s) for s in send]
