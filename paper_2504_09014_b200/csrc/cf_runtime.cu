@@ -672,9 +672,12 @@ cfStatus launch(cfComm* c, const Job& j, int dtype, const void* const* send, voi
         if (nb) rk.out2[rk.rank] = (char*)nb->resid_out[li];
       }
     }
-    // two-shot push (K3): one CTA per SM; the pull-only variants (K2, K8) gain
-    // from full residency (K8 256 MiB 394 -> 354 us, K2 1 MiB 13.4 -> 10.1 us)
-    int mb = max_blocks_per_rank(c, kernel, (int)gi, threads, (j.kind == kPull && j.push) ? 1 : 0);
+    // two-shot push (K3) above 8 MiB per rank: one CTA per SM (64 MiB: 182 ->
+    // 171 us); below, full residency hides more latency (4 MiB: 15.8 -> 14.4
+    // us); the pull-only variants (K2, K8) gain from full residency at every
+    // size (K8 256 MiB 394 -> 354 us, K2 1 MiB 13.4 -> 10.1 us)
+    const bool k3_big = j.kind == kPull && j.push && j.count * dtype_size(dtype) > ((size_t)8 << 20);
+    int mb = max_blocks_per_rank(c, kernel, (int)gi, threads, k3_big ? 1 : 0);
     if (ring) mb = std::min(mb, kRingCtas);   // ring slot region
     int blocks = (int)std::min<size_t>((size_t)mb, std::max<size_t>(1, ceil_div(j.work, (size_t)threads)));
     if (j.blocks) blocks = std::min(mb, j.blocks);
