@@ -244,7 +244,9 @@ CF_API cfStatus cfSelectAlgorithm(cfComm_t comm, int collective, size_t nbytes, 
  * allocates the plan's buffers per rank.  cfPlanExecute runs every (rank, tb)
  * program on the GPU with the caller's per-local-rank input/output buffers
  * bound zero-copy as the plan's input/output buffers (sizes: the declared
- * elems).  One-process communicators only in this version. */
+ * elems).  One-process communicators run every rank's programs; one process
+ * per GPU runs this rank's programs after cfPlanGetHandle / cfPlanConnect
+ * (below). */
 CF_API cfStatus cfPlanLoad(cfComm_t comm, const char* json, size_t len, int dtype_override, cfPlan_t* plan);
 CF_API cfStatus cfPlanExecute(cfPlan_t plan, const void* const* inputs, void* const* outputs,
                               const cudaStream_t* streams);

@@ -13,7 +13,7 @@ def main():
     from paper_2504_09014_b200 import Runtime, make_world, parse_plan
     from paper_2504_09014_b200.plan import scale_plan
     n = 8
-    w = make_world(1, n, devices=[0] * n)
+    w = make_world(1, n, devices=[0] * n, threads=int(os.environ.get("THREADS", "0")))
     dev = w.device(0)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     for pname in os.environ.get("PLANS", "2pa_memory_n8_e64,1pa_n8_e64").split(","):
