@@ -229,9 +229,11 @@ def run_ag_rs(w, flush, send, recv):
     from paper_2504_09014_b200 import _lib
     n = w.num_ranks
     rows = []
-    for nb in (64 * KiB, MiB, 16 * MiB, 256 * MiB):
+    for nb in [KiB << (2 * i) for i in range(11)]:   # 1 KiB .. 1 GiB (C2's sweep), x4
         row = {"bytes": nb}
         shard = nb // 2 // n
+        if shard == 0:
+            continue
         iters = 20 if nb <= 16 * MiB else 5
         fl = flush if nb < 64 * MiB else None
         for name in ("allpairs_ag", "ring_ag"):
