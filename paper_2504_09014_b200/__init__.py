@@ -13,13 +13,14 @@ from .executor import RunResult, Runtime
 from .fused import allreduce_add_rmsnorm
 from .lowering import LoweringParams, ProgramGraph, lower
 from .plan import ExecutionPlan, parse_plan, serialize_plan, validate_plan
+from .timing import BenchRow, CostParams, algobw, busbw, rows_to_csv, run_benchmark
 from .world import Topology, World, make_world
 
 SimWorld = World  # the reference's name for the world type (cf/world.py:80)
 
 __all__ = [
-    "AlgoDescriptor", "CommforgeError", "allreduce_add_rmsnorm", "ExecutionPlan", "LoweringParams", "ProgramGraph",
-    "RunResult", "Runtime", "Selector", "SimWorld", "Topology", "World", "collective", "lower",
-    "make_world", "parse_plan", "required_multiple", "select_algorithm", "serialize_plan",
-    "validate_plan",
+    "AlgoDescriptor", "BenchRow", "CommforgeError", "CostParams", "allreduce_add_rmsnorm", "algobw", "busbw",
+    "ExecutionPlan", "LoweringParams", "ProgramGraph", "RunResult", "Runtime", "Selector", "SimWorld",
+    "Topology", "World", "collective", "lower", "make_world", "parse_plan", "required_multiple",
+    "rows_to_csv", "run_benchmark", "select_algorithm", "serialize_plan", "validate_plan",
 ]

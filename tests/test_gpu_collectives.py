@@ -503,3 +503,22 @@ def test_lowp_allreduce_matches_reference_f32_path():
         ins = gen_inputs(c["n"], c["elems"], c["dtype"], "normal", c["seed"])
         got = collective("allreduce", ins, world(c["n"]), dtype=c["dtype"], algo=c["algo"], variant=c["variant"])
         assert [_digest(g) for g in got] == c["digests"], (c["n"], c["elems"], c["dtype"], c["algo"], c["variant"])
+
+
+def test_run_benchmark_measured_rows():
+    """run_benchmark (cf/timing.py:331-349) on real GPUs: one measured row per
+    (variant, size), LL variants skipped above their capacity, exactly one
+    row per size marked as the selector's pick."""
+    from paper_2504_09014_b200 import rows_to_csv, run_benchmark
+    w = world(4, ll_max_bytes=1 << 16)
+    sizes = [4096, 1 << 20]
+    rows = run_benchmark("allreduce", sizes, w, iters=5)
+    algos = {(r.algo, r.nbytes) for r in rows}
+    assert ("1pa", 4096) in algos and ("1pa", 1 << 20) not in algos   # LL capacity
+    assert ("2pa_port", 1 << 20) in algos and ("2pr", 1 << 20) in algos
+    for nb in sizes:
+        assert sum(r.selected for r in rows if r.nbytes == nb) == 1, nb
+    assert all(r.latency_us > 0 and r.algobw_gbps > 0 for r in rows)
+    ag = run_benchmark("allgather", [1 << 16], w, iters=5)
+    assert [r.algo for r in ag] == ["allpairs_ag", "ring_ag"] and sum(r.selected for r in ag) == 1
+    assert rows_to_csv(rows).count("\n") == len(rows) + 1

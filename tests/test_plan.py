@@ -107,3 +107,18 @@ def test_flag_reuse_detected():
                           PlanOp("put_packets", chan="m0", src=("in", 0, 4), dst=("scr", 0, 4), flag=1),
                           PlanOp("put_packets", chan="m0", src=("in", 0, 4), dst=("scr", 2, 4), flag=1)))])
     assert ("error", "flag-reuse") in _codes(p)
+
+
+def test_timing_api_matches_reference_definitions():
+    """algobw / rows_to_csv keep cf/timing.py:54-58, 352-358 (same values,
+    same CSV columns, same error code on a non-positive latency)."""
+    import paper_2504_09014_b200 as cf
+    from paper_2504_09014_b200.errors import BadTimeError
+    assert cf.algobw(1 << 20, 1e-3) == (1 << 20) / 1e-3
+    assert cf.busbw(1 << 20, 1e-3, 8) == cf.algobw(1 << 20, 1e-3) * 2 * 7 / 8
+    assert cf.busbw(1 << 20, 1e-3, 8, "allgather") == cf.algobw(1 << 20, 1e-3) * 7 / 8
+    with pytest.raises(BadTimeError):
+        cf.algobw(10, 0.0)
+    csv = cf.rows_to_csv([cf.BenchRow("2pa_memory", "allreduce", 4096, 3.25, 1.26, True)])
+    assert csv == "algo,collective,bytes,latency_us,algobw_gbps,selected\n" \
+                  "2pa_memory,allreduce,4096,3.250000,1.260000,1\n"
