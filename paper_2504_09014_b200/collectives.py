@@ -317,3 +317,9 @@ def collective(kind: str, inputs, world, selector: Selector | None = None, dtype
     world.synchronize()
     world.check_device_error()
     return outs if on_gpu else [_to_host(o, dtype) for o in outs]
+
+
+# The reference defines the algorithm builders in this module
+# (cf/collectives.py:30-270); they live in algorithms.py here.
+from .algorithms import (build_1pa, build_2pa, build_2pr, build_algo, build_allpairs_ag,  # noqa: E402,F401
+                         build_ring_ag, build_ring_rs, build_switch_2pa)

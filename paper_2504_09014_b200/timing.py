@@ -86,10 +86,11 @@ def _measure(world, fn, iters: int, reps: int) -> float:
     return best
 
 
-def timed_latency(collective: str, name: str, variant: str, nbytes: int, world, dtype: str = "bf16",
-                  iters: int = 20, reps: int = 3) -> float:
-    """Measured seconds per call of one algorithm (cf/timing.py:318-328 measures
-    the same quantity on its model)."""
+def timed_latency(name: str, variant: str, nbytes: int, world, p: CostParams | None = None,
+                  collective: str = "allreduce", dtype: str = "bf16", iters: int = 20, reps: int = 3) -> float:
+    """Measured seconds per call of one algorithm -- the reference's signature
+    (cf/timing.py:318-328, which computes the same quantity on its model);
+    ``p`` is ignored."""
     import torch
     from . import collectives as C
     from .dtypes import ELEM_SIZE, torch_dtype
@@ -136,7 +137,7 @@ def run_benchmark(collective: str, sizes: list[int], world, p: CostParams | None
     for name, variant in variants:
         for nbytes in sorted(sizes):
             try:
-                latency = timed_latency(collective, name, variant, nbytes, world, dtype, iters)
+                latency = timed_latency(name, variant, nbytes, world, p, collective, dtype, iters)
             except BadSizeError:   # beyond an LL algorithm's capacity: no row, as no plan
                 continue
             pick = sel.select(collective, nbytes, world.topology, world=world, dtype=dtype)
