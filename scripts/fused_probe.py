@@ -15,12 +15,13 @@ def main():
     dev = w.device(0)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     row = []
-    for b in (1, 16, 64, 256):
+    for b in (1, 4, 8, 16, 32, 64, 256):
         xs = [torch.randn(b, hidden, device=dev).to(torch.bfloat16) for _ in range(n)]
         rs = [torch.randn(b, hidden, device=dev).to(torch.bfloat16) for _ in range(n)]
         ys = [torch.empty_like(x) for x in xs]
         wt = torch.ones(hidden, device=dev, dtype=torch.bfloat16)
-        t = time_graph(dev, lambda: allreduce_add_rmsnorm(w, xs, rs, wt, norm_out=ys), 20, 3, flush)
+        algo = os.environ.get("ALGO") or None
+        t = time_graph(dev, lambda: allreduce_add_rmsnorm(w, xs, rs, wt, norm_out=ys, algo=algo), 20, 3, flush)
         row.append(f"b={b}: {t * 1e6:6.2f} us")
     print("K13 " + " | ".join(row), flush=True)
     w.close()
