@@ -986,6 +986,33 @@ cfStatus load(cfComm* c, const char* json, size_t len, int dtype_override, cfPla
   return CF_OK;
 }
 
+// CTA-local syncs that another barrier already provides: first / last op of a
+// program (the staging barrier / the end-of-call barrier), next to an op that
+// starts with a block barrier (signal, port ops, group / device barriers,
+// another sync) or after one that ends with one (wait, port flush, group /
+// device barriers).  Fusion leaves such syncs behind (the hoisted copy's).
+void drop_redundant_syncs(cfPlan* pl) {
+  auto starts_bar = [](uint8_t c) {
+    return c == D_SIGNAL || c == D_SYNC_GROUP || c == D_DEV_BARRIER || c == D_PORT_PUT || c == D_PORT_SIGNAL ||
+           c == D_SYNC_CTA || c == D_WAIT;
+  };
+  auto ends_bar = [](uint8_t c) {
+    return c == D_WAIT || c == D_SYNC_GROUP || c == D_DEV_BARRIER || c == D_PORT_FLUSH || c == D_SYNC_CTA;
+  };
+  for (auto& ops : pl->prog_ops) {
+    std::vector<DevOp> keep;
+    for (size_t i = 0; i < ops.size(); i++) {
+      if (ops[i].code == D_SYNC_CTA) {
+        const bool first = keep.empty(), last = i + 1 == ops.size();
+        if (first || last || ends_bar(keep.back().code) || starts_bar(ops[i + 1].code)) continue;
+      }
+      keep.push_back(ops[i]);
+    }
+    pl->n_device_ops -= (int)(ops.size() - keep.size());
+    ops.swap(keep);
+  }
+}
+
 // Bake plan-owned buffer addresses into the device ops, fuse packet reads,
 // upload the per-device tables, start the proxy (port channels).
 cfStatus finalize(cfPlan* pl) {
@@ -1012,6 +1039,7 @@ cfStatus finalize(cfPlan* pl) {
       for (int k = 0; k < d.ndst; k++) bake(d.dst[k]);
     }
   fuse_packet_reads(pl);
+  drop_redundant_syncs(pl);
   // device tables per device group
   for (size_t gi = 0; gi < c->groups.size(); gi++) {
     Group G;
