@@ -1011,6 +1011,47 @@ void drop_redundant_syncs(cfPlan* pl) {
     pl->n_device_ops -= (int)(ops.size() - keep.size());
     ops.swap(keep);
   }
+  // A CTA-local sync whose two sides (the data ops back to the previous and
+  // on to the next non-data op) share no location with a write on either
+  // side orders nothing (e.g. the 1pa plan's packet scatter vs its fused
+  // read-reduce: packets written by peers are ordered by their flags).
+  const int es = pl->es;
+  auto refs_conflict = [&](const DevOp& x, const DevOp& y) {
+    for (int i = 0; i < x.nsrc + x.ndst; i++)
+      for (int k = 0; k < y.nsrc + y.ndst; k++) {
+        const bool xw = i >= x.nsrc, yw = k >= y.nsrc;
+        if (!xw && !yw) continue;
+        const DRef& rx = xw ? x.dst[i - x.nsrc] : x.src[i];
+        const DRef& ry = yw ? y.dst[k - y.nsrc] : y.src[k];
+        if (!same_loc(rx, ry)) continue;
+        auto pkt = [](const DevOp& d, int j, bool w) {
+          return (d.code == D_READ_PACKETS && !w) || (d.code == D_PUT_PACKETS && w) ||
+                 (d.code == D_MULTI && !w && ((d.pkt_mask >> j) & 1u));
+        };
+        uint64_t a0, a1, b0, b1;
+        dref_span(x, rx, pkt(x, i, xw), es, a0, a1);
+        dref_span(y, ry, pkt(y, k, yw), es, b0, b1);
+        if (a0 < b1 && b0 < a1) return true;
+      }
+    return false;
+  };
+  auto is_data = [](uint8_t c) { return c == D_MULTI || c == D_COPY || c == D_PUT_PACKETS || c == D_READ_PACKETS; };
+  for (auto& ops : pl->prog_ops) {
+    for (size_t i = 0; i < ops.size(); i++) {
+      if (ops[i].code != D_SYNC_CTA) continue;
+      size_t a = i, b = i + 1;
+      while (a > 0 && is_data(ops[a - 1].code)) a--;
+      while (b < ops.size() && is_data(ops[b].code)) b++;
+      bool hazard = a == i || b == i + 1;   // a non-data neighbour: keep
+      for (size_t x = a; x < i && !hazard; x++)
+        for (size_t y = i + 1; y < b && !hazard; y++) hazard = refs_conflict(ops[x], ops[y]);
+      if (!hazard) {
+        ops.erase(ops.begin() + i);
+        pl->n_device_ops--;
+        i--;
+      }
+    }
+  }
 }
 
 // Bake plan-owned buffer addresses into the device ops, fuse packet reads,
