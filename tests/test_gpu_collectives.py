@@ -522,3 +522,23 @@ def test_run_benchmark_measured_rows():
     ag = run_benchmark("allgather", [1 << 16], w, iters=5)
     assert [r.algo for r in ag] == ["allpairs_ag", "ring_ag"] and sum(r.selected for r in ag) == 1
     assert rows_to_csv(rows).count("\n") == len(rows) + 1
+
+
+def test_host_buffer_allreduce_every_algorithm():
+    """Host tensors through collective() for every AllReduce algorithm and the
+    selector's pick: same bits as the device-buffer call (the host path copies
+    around the same kernels; only 2pa pipelines windows)."""
+    import torch
+    from paper_2504_09014_b200 import collective
+    w = world(8)
+    for elems in (5000, (3 << 20) + 7):
+        g = torch.Generator().manual_seed(elems)
+        host = [(torch.randn(elems, generator=g) * 4).to(torch.bfloat16).pin_memory() for _ in range(8)]
+        for algo, var in ALGOS + [(None, "")]:
+            if (algo == "1pa" or var == "ll") and elems * 2 > (4 << 20):   # LL capacity
+                continue
+            got = collective("allreduce", host, w, dtype="bf16", algo=algo, variant=var)
+            dev = collective("allreduce", [h.cuda() for h in host], w, dtype="bf16", algo=algo, variant=var)
+            for r in range(8):
+                assert not got[r].is_cuda
+                assert torch.equal(got[r].view(torch.int16), dev[r].cpu().view(torch.int16)), (elems, algo, var, r)
