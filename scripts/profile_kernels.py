@@ -22,13 +22,15 @@ def main():
     ap.add_argument("--iters", type=int, default=3)
     ap.add_argument("--plan", default="")
     ap.add_argument("--scale", type=int, default=1)
+    ap.add_argument("--emulate-nvls", action="store_true",
+                    help="world with the emulated switch (switch_2pa runs the K5 NVLS kernel)")
     args = ap.parse_args()
     import torch
     from paper_2504_09014_b200 import _lib, make_world
     from paper_2504_09014_b200 import collectives as C
     from paper_2504_09014_b200.dtypes import ELEM_SIZE, torch_dtype
     n = args.ranks
-    w = make_world(1, n, devices=[0] * n)
+    w = make_world(1, n, devices=[0] * n, use_multicast="emulate" if args.emulate_nvls else True)
     dev = w.device(0)
     count = args.bytes // ELEM_SIZE[args.dtype]
     tdt = torch_dtype(args.dtype)

@@ -19,4 +19,6 @@ full 1pa_1k ll_oneshot $P --algo 1pa --bytes 1024 --dtype bf16 --iters 3
 full rs_256m pull_reduce $P --kind reducescatter --algo rs_direct --bytes 268435456 --dtype bf16 --iters 3
 full ringrs_256m ring_kernel $P --kind reducescatter --algo ring_rs --bytes 268435456 --dtype bf16 --iters 3
 full ringag_256m ring_gather $P --kind allgather --algo ring_ag --bytes 268435456 --dtype bf16 --iters 3
+# K5 control path through the emulated switch (per-rank loads / stores in place of multimem)
+full nvlsemul_64m nvls_kernel $P --algo switch_2pa --emulate-nvls --bytes 67108864 --dtype bf16 --iters 3
 ls -la gpurun_out/*.ncu-rep
