@@ -884,15 +884,36 @@ cfStatus load(cfComm* c, const char* json, size_t len, int dtype_override, cfPla
           d.src[0] = w;
           break;
         }
-        case D_PUT_PACKETS:   // same payload to several peers: one load, ndst packet stores
-          if (prev && prev->code == D_PUT_PACKETS && prev->size == d.size && prev->llflag == d.llflag &&
-              prev->ndst < kMaxDst && (prev->flags & F_LL16) == (d.flags & F_LL16) &&
-              prev->src[0].buf == d.src[0].buf && prev->src[0].rank == d.src[0].rank &&
-              prev->src[0].off == d.src[0].off) {
+        case D_PUT_PACKETS: {  // batched: one payload to several peers (one load, ndst packet stores),
+                               // or several (payload -> peer) pairs with all loads in flight
+          const bool like = prev && prev->code == D_PUT_PACKETS && prev->size == d.size &&
+                            prev->llflag == d.llflag && prev->ndst < kMaxDst &&
+                            (prev->flags & F_LL16) == (d.flags & F_LL16);
+          const bool same_src = like && !(prev->flags & F_PAIRED) && prev->src[0].buf == d.src[0].buf &&
+                                prev->src[0].rank == d.src[0].rank && prev->src[0].off == d.src[0].off;
+          if (same_src) {
             prev->dst[prev->ndst++] = d.dst[0];
             continue;
           }
+          if (like && (prev->flags & F_PAIRED || prev->ndst == 1)) {
+            // no packet range of the batch may overlap a payload range of it
+            const long long len_pkt = 2 * d.size * es, len_pay = d.size * es;
+            auto ovl = [](const DRef& x, long long lx, const DRef& y, long long ly) {
+              return x.buf == y.buf && x.rank == y.rank && (long long)x.off < (long long)y.off + ly &&
+                     (long long)y.off < (long long)x.off + lx;
+            };
+            bool ok = true;
+            for (int k = 0; k < prev->ndst && ok; k++)
+              ok = !ovl(prev->dst[k], len_pkt, d.src[0], len_pay) && !ovl(d.dst[0], len_pkt, prev->src[k], len_pay);
+            if (ok) {
+              prev->flags |= F_PAIRED;
+              prev->src[prev->nsrc++] = d.src[0];
+              prev->dst[prev->ndst++] = d.dst[0];
+              continue;
+            }
+          }
           break;
+        }
         case D_READ_PACKETS: {  // several packet ranges drained together, loads in flight
           d.llflag_k[0] = d.llflag;
           bool ok = prev && prev->code == D_READ_PACKETS && prev->size == d.size && prev->nsrc < kMaxDst &&

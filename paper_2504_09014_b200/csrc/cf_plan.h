@@ -85,7 +85,8 @@ enum DevCode : uint8_t {
   D_PORT_SIGNAL,   // port signal, ordered after earlier puts     cf/channels.py:98-103
   D_PORT_FLUSH,    // wait until the proxy completed every request  cf/channels.py:110-114
 };
-enum DevFlags : uint8_t { F_ZERO = 1, F_ROUND_EACH = 2, F_VEC = 4, F_LL16 = 8, F_SIGNAL = 16 };
+enum DevFlags : uint8_t { F_ZERO = 1, F_ROUND_EACH = 2, F_VEC = 4, F_LL16 = 8, F_SIGNAL = 16,
+                          F_PAIRED = 32 /* D_PUT_PACKETS batch: src[k] -> dst[k] */ };
 
 struct DRef {
   int32_t buf;         // plan buffer index, or kAbsolute: `off` is the device address

@@ -282,7 +282,18 @@ __device__ __noinline__ void packet_op(const DevOp& op, int K, int j, uint32_t f
   const int nb = put ? op.ndst : op.nsrc;
   if (op.flags & F_LL16) {
     const uint64_t u0 = lo * sizeof(T) / 8, u1 = (hi * sizeof(T) + 7) / 8;
-    if (put) {
+    if (put && (op.flags & F_PAIRED)) {   // src[k] -> dst[k]: every payload load in flight first
+      const uint32_t flag = op.llflag;
+      for (uint64_t u = u0 + threadIdx.x; u < u1; u += blockDim.x) {
+        uint2 d[kMaxDst];
+#pragma unroll
+        for (int k = 0; k < kMaxDst; k++)
+          if (k < nb) d[k] = *reinterpret_cast<const uint2*>(ptr(op.src[k]) + u * 8);
+#pragma unroll
+        for (int k = 0; k < kMaxDst; k++)
+          if (k < nb) ll16_put(ptr(op.dst[k]) + u * 16, d[k], flag);
+      }
+    } else if (put) {
       const uint32_t flag = op.llflag;
       const char* src = ptr(op.src[0]);
       for (uint64_t u = u0 + threadIdx.x; u < u1; u += blockDim.x) {
@@ -309,7 +320,7 @@ __device__ __noinline__ void packet_op(const DevOp& op, int K, int j, uint32_t f
   } else {
     const uint64_t u0 = lo * sizeof(T) / 4, u1 = (hi * sizeof(T) + 3) / 4;
     for (int k = 0; k < nb; k++) {
-      const char* src = ptr(op.src[put ? 0 : k]);
+      const char* src = ptr(op.src[put && !(op.flags & F_PAIRED) ? 0 : k]);
       char* dst = ptr(op.dst[k]);
       const uint32_t flag = put ? op.llflag : op.llflag_k[k];
       for (uint64_t u = u0 + threadIdx.x; u < u1; u += blockDim.x) {
