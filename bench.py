@@ -429,7 +429,7 @@ def run_sweep(w, args):
     from paper_2504_09014_b200 import Runtime, parse_plan
     from paper_2504_09014_b200.plan import scale_plan
     c5 = []
-    for pname in ("2pa_memory_n8_e64", "1pa_n8_e64"):
+    for pname in ("2pa_memory_n8_e64", "2pa_ll_n8_e64", "1pa_n8_e64"):
         with open(os.path.join(ROOT, "tests", "golden", "plans", pname + ".json"), "rb") as f:
             base = parse_plan(f.read())
         for b in (1, 4, 16, 64, 256):

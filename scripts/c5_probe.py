@@ -16,7 +16,7 @@ def main():
     w = make_world(1, n, devices=[0] * n, threads=int(os.environ.get("THREADS", "0")))
     dev = w.device(0)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-    for pname in os.environ.get("PLANS", "2pa_memory_n8_e64,1pa_n8_e64").split(","):
+    for pname in os.environ.get("PLANS", "2pa_memory_n8_e64,2pa_ll_n8_e64,1pa_n8_e64").split(","):
         with open(os.path.join(ROOT, "tests", "golden", "plans", pname + ".json"), "rb") as f:
             base = parse_plan(f.read())
         row = []
