@@ -241,6 +241,12 @@ __global__ void __launch_bounds__(512) pull_reduce_kernel(const __grid_constant_
 // read; the read phase keeps every peer's packet in flight and re-polls all
 // unstamped ones per round (ll16_poll): waiting for n-1 peers costs one round
 // trip per round, not one per peer.
+// Packet units per thread per round in K4's scatter / gather phases.
+#ifndef CF_LL2U
+#define CF_LL2U 4
+#endif
+constexpr int kLL2U = CF_LL2U;
+
 #ifndef CF_LL1_STREAM
 #define CF_LL1_STREAM 1
 #endif
@@ -348,12 +354,22 @@ __global__ void __launch_bounds__(512) ll_twoshot_kernel(const __grid_constant__
   const size_t nunit = a.count / H;
 
   // phase 1: scatter my chunks as packets
-  if (grid) {
-    for (size_t u = t0; u < nunit; u += stride) {
-      const uint32_t p = (uint32_t)u / cu, i = (uint32_t)u - p * cu;
-      if ((int)p == r) continue;
-      ll16_put_scoped(rk.scr[p] + ph1 + (size_t)r * a.slot + (size_t)i * 16, ld8(rk.in[r] + u * 8), flag,
-                      a.gpu_scope);
+  if (grid) {   // kLL2U units per thread per round: their loads in flight together
+    for (size_t ub = t0; ub < nunit; ub += (size_t)kLL2U * stride) {
+      uint2 x[kLL2U];
+#pragma unroll
+      for (int j = 0; j < kLL2U; j++) {
+        const size_t u = ub + (size_t)j * stride;
+        if (u < nunit && (int)((uint32_t)u / cu) != r) x[j] = ld8(rk.in[r] + u * 8);
+      }
+#pragma unroll
+      for (int j = 0; j < kLL2U; j++) {
+        const size_t u = ub + (size_t)j * stride;
+        if (u >= nunit) break;
+        const uint32_t p = (uint32_t)u / cu, i = (uint32_t)u - p * cu;
+        if ((int)p != r)
+          ll16_put_scoped(rk.scr[p] + ph1 + (size_t)r * a.slot + (size_t)i * 16, x[j], flag, a.gpu_scope);
+      }
     }
   } else for (size_t i = t0; i < nvmax; i += stride) {   // every peer's input vector loaded first
     uint4 x[NR];
@@ -426,14 +442,43 @@ __global__ void __launch_bounds__(512) ll_twoshot_kernel(const __grid_constant__
   }
   TS_MARK();
   // phase 2: decode the peers' reduced chunks
-  if (grid) {
-    for (size_t u = t0; u < nunit; u += stride) {
-      const uint32_t p = (uint32_t)u / cu, i = (uint32_t)u - p * cu;
-      if ((int)p == r) continue;
-      const char* src = rk.scr[r] + ph2 + (size_t)p * a.slot + (size_t)i * 16;
-      uint4 pk[1] = {ld16_volatile(src)};
-      ll16_poll<1>(src, 0, 1, pk, 1u, flag, rk.st);
-      st8(rk.out[r] + u * 8, make_uint2(pk[0].x, pk[0].z));
+  if (grid) {   // kLL2U packets per thread in flight, unstamped ones re-polled together
+    for (size_t ub = t0; ub < nunit; ub += (size_t)kLL2U * stride) {
+      const char* src[kLL2U];
+      uint4 pk[kLL2U];
+      uint32_t pend = 0;
+#pragma unroll
+      for (int j = 0; j < kLL2U; j++) {
+        const size_t u = ub + (size_t)j * stride;
+        if (u >= nunit) break;
+        const uint32_t p = (uint32_t)u / cu, i = (uint32_t)u - p * cu;
+        if ((int)p == r) continue;
+        src[j] = rk.scr[r] + ph2 + (size_t)p * a.slot + (size_t)i * 16;
+        pk[j] = ld16_volatile(src[j]);
+        pend |= 1u << j;
+      }
+      const uint32_t todo = pend;
+#pragma unroll
+      for (int j = 0; j < kLL2U; j++)
+        if (((pend >> j) & 1u) && pk[j].y == flag && pk[j].w == flag) pend &= ~(1u << j);
+      if (pend) {
+        const uint64_t tw = globaltimer();
+        for (uint32_t it = 1; pend; ++it) {
+#pragma unroll
+          for (int j = 0; j < kLL2U; j++)
+            if ((pend >> j) & 1u) pk[j] = ld16_volatile(src[j]);
+#pragma unroll
+          for (int j = 0; j < kLL2U; j++)
+            if (((pend >> j) & 1u) && pk[j].y == flag && pk[j].w == flag) pend &= ~(1u << j);
+          if ((it & 255u) == 0 && pend) {
+            if (*(volatile uint32_t*)&rk.st->error != kDevOk) break;
+            if (globaltimer() - tw > rk.st->timeout_ns) { atomicExch(&rk.st->error, (uint32_t)kDevTimeout); break; }
+          }
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < kLL2U; j++)
+        if ((todo >> j) & 1u) st8(rk.out[r] + (ub + (size_t)j * stride) * 8, make_uint2(pk[j].x, pk[j].z));
     }
   } else for (size_t i = t0; i < nvmax; i += stride) {   // all peers' packets of vector i in flight
     const char* base = rk.scr[r] + ph2 + i * 32;
