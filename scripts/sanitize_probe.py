@@ -18,7 +18,7 @@ def main():
     n = 4
     w = make_world(1, n, devices=[0] * n, use_multicast="emulate", nvls_bytes=16 << 10, spin_timeout_ms=60000)
     bad = 0
-    for elems in (5, 1001, 4099):
+    for elems in (5, 1001, 4099, 4096, 6000):
         for dtype in ("f32", "bf16"):
             ins = gen_inputs(n, elems, dtype, "normal", elems)
             for algo, var in (("1pa", ""), ("1pa_hb", ""), ("2pa", "memory"), ("2pa", "ll"), ("2pa", "port"),
