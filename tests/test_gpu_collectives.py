@@ -65,6 +65,21 @@ def test_allreduce_vs_oracle(n, dtype, elems):
             assert np.array_equal(got[r].view(np.uint8), want[r].view(np.uint8)), (algo, var, r)
 
 
+@pytest.mark.parametrize("n,dtype,elems", [(8, "bf16", 32 * 1000), (8, "bf16", 1 << 20), (8, "bf16", (1 << 21) - 32),
+                                          (8, "f32", (1 << 20) - 16), (4, "bf16", 3 << 18), (2, "f32", 1 << 19)])
+def test_ll_twoshot_multi_round(n, dtype, elems):
+    """K4's grid path (chunk bounds on the 8-byte grid) at sizes where every
+    thread runs several rounds of kLL2U units, the last one partial: same bits
+    as the oracle's two-shot order, twice (parity halves alternate)."""
+    from paper_2504_09014_b200 import collective
+    ins = gen_inputs(n, elems, dtype, "normal", 77 + elems % 101)
+    want = oracle.allreduce(ins, "2pa", dtype)
+    for rep in range(2):
+        got = collective("allreduce", ins, world(n), dtype=dtype, algo="2pa", variant="ll")
+        for r in range(n):
+            assert np.array_equal(got[r].view(np.uint8), want[r].view(np.uint8)), (rep, r)
+
+
 @pytest.mark.parametrize("n", [3, 5, 6, 7])
 @pytest.mark.parametrize("dtype", ["f32", "bf16", "i32"])
 def test_odd_rank_counts_vs_oracle(n, dtype):
