@@ -304,7 +304,8 @@ def run_gpu_arm(args):
         gen.manual_seed(20250409 + 4000 + r)
         send.append(torch.randn(count, device=dev, dtype=torch.float32, generator=gen).to(tdt))
     recv = [torch.empty_like(s) for s in send]
-    algo_name = C.select_algorithm("allreduce", HEAD_BYTES, w.topology, world=w, dtype=HEAD_DTYPE)
+    algo_name = C.select_algorithm("allreduce", HEAD_BYTES, w.topology, selector=C.Selector(measured=True),
+                                   world=w, dtype=HEAD_DTYPE)
     algo = _lib.ALGOS["2pa_ll" if algo_name.variant == "ll" else algo_name.name]
     # parity spot check of the headline config (vs the size-independent property:
     # every rank holds identical bits, and a sampled slice equals the oracle)

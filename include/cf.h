@@ -99,7 +99,7 @@ typedef struct cfPlan* cfPlan_t;
 typedef struct {
   size_t ll_max_bytes;      /* largest per-rank message the LL algorithms accept (0 = default 4 MiB) */
   int max_blocks;           /* CTA cap per rank (0 = derived from occupancy and co-residency) */
-  int threads;              /* threads per CTA (0 = 512) */
+  int threads;              /* threads per CTA (0 = 512; multiple of 32 in [64, 512]) */
   uint64_t spin_timeout_ns; /* device spin-wait timeout -> CF_E_DEADLOCK (0 = 10 s) */
   int use_multicast;        /* 1 = build NVLS multicast objects when supported; 2 = emulated switch:
                                switch_2pa runs the NVLS kernel (K5) on unicast staging with per-rank
@@ -225,9 +225,12 @@ CF_API cfStatus cfAllReduceHostStaged(cfComm_t comm, const void* const* host_sen
  *   norm_out  = dtype(resid_out * rsqrt(mean_row(resid_out^2) + eps) * weight)
  * weight holds `hidden` elements.  resid_out may alias resid_in.  algo:
  * CF_ALGO_1PA_HB (one-shot: every rank reduces every row; not in place),
- * CF_ALGO_2PA (two-shot: rank r owns rows [r*ceil(rows/n), ...) and stores
- * both results into every rank; in the one-process-per-GPU mode norm_out and
- * resid_out must be registered), or CF_ALGO_AUTO. */
+ * CF_ALGO_2PA (two-shot: rank r owns rows [r*ceil(rows/n), ...), reduces them
+ * and stores h into every rank's norm_out; every rank then finishes all rows
+ * with its own resid_in and weight; in the one-process-per-GPU mode send and
+ * norm_out must be registered), or CF_ALGO_AUTO (picked from rows, hidden,
+ * dtype and n only; in place it needs CF_ALGO_2PA, which it takes itself in
+ * one-process communicators and reports as CF_E_SHAPE one process per GPU). */
 CF_API cfStatus cfAllReduceAddRMSNorm(cfComm_t comm, const void* const* send, const void* const* resid_in,
                                       void* const* resid_out, void* const* norm_out, const void* const* weight,
                                       size_t rows, size_t hidden, float eps, cfDtype dtype, int algo,
@@ -254,6 +257,12 @@ CF_API cfStatus cfPlanInfo(cfPlan_t plan, size_t* in_elems, size_t* out_elems, i
                            int* n_device_ops);
 /* Device spin-timeout word of the plan's ranks (0 or CF_E_DEADLOCK).  Synchronizes. */
 CF_API cfStatus cfPlanLastDeviceError(cfPlan_t plan, int* code);
+/* After a reported timeout: return every plan heap this process owns to its
+ * load-time state (error word, semaphore lanes, barriers, LL scratch), so the
+ * plan runs again (the reference Runtime rebuilds its channels per execute,
+ * cf/executor.py:159).  One process per GPU: every rank calls it while no
+ * execution of the plan is in flight.  Synchronizes. */
+CF_API cfStatus cfPlanClearDeviceError(cfPlan_t plan);
 /* One process per GPU: every rank loads the same plan with cfPlanLoad, exports
  * its plan heap (semaphore lanes, barrier counters, scratch buffers) with
  * cfPlanGetHandle, all-gathers the handles through the caller's bootstrap and

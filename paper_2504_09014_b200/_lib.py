@@ -38,7 +38,7 @@ EXPORTS = (
     "cfCommMulticastSupported", "cfCommLastDeviceError", "cfCommClearDeviceError", "cfAllReduce",
     "cfAllGather", "cfReduceScatter", "cfAllReduceHost", "cfAllReduceHostStaged",
     "cfAllReduceAddRMSNorm", "cfSelectAlgorithm", "cfPlanLoad", "cfPlanExecute",
-    "cfPlanInfo", "cfPlanLastDeviceError", "cfPlanGetHandle", "cfPlanConnect", "cfPlanDestroy",
+    "cfPlanInfo", "cfPlanLastDeviceError", "cfPlanClearDeviceError", "cfPlanGetHandle", "cfPlanConnect", "cfPlanDestroy",
 )
 
 
@@ -90,6 +90,7 @@ _PROTOS = {
     "cfPlanLoad": ([vp, ctypes.c_char_p, sz, i32, P(vp)], i32),
     "cfPlanExecute": ([vp, P(vp), P(vp), P(vp)], i32),
     "cfPlanLastDeviceError": ([vp, P(i32)], i32),
+    "cfPlanClearDeviceError": ([vp], i32),
     "cfPlanInfo": ([vp, P(sz), P(sz), P(i32), P(i32), P(i32)], i32),
     "cfPlanGetHandle": ([vp, vp, P(sz)], i32),
     "cfPlanConnect": ([vp, vp, sz], i32),

@@ -80,12 +80,17 @@ _DESC = {
 
 @dataclass
 class Selector:
-    """cf/collectives.py:464-486.  With no thresholds and no override it uses
-    libcf's measured crossover table for the world it is asked about."""
+    """cf/collectives.py:464-486.  By default it is the reference's threshold
+    table, so ``collective()`` picks the reference's algorithm -- the same
+    output shapes (e.g. ring_rs pads ReduceScatter to 2n) and the same
+    accumulation order, hence the reference's bits.  ``measured=True`` asks
+    libcf's measured crossover table for the world instead (the fastest
+    kernel per size; its order may differ from the reference's pick)."""
 
     thresholds: dict = field(default_factory=dict)
     override: str | None = None
     override_variant: str = ""
+    measured: bool = False
 
     def table(self, collective: str) -> list[AlgoDescriptor]:
         return default_table(collective, self.thresholds)
@@ -101,7 +106,7 @@ class Selector:
                     return d
             return AlgoDescriptor(self.override, "HB", "port", 0, None, "single-node",
                                   variant=self.override_variant)
-        if world is not None and not self.thresholds:
+        if self.measured and world is not None:
             algo = ctypes.c_int()
             _lib.check(_lib.lib().cfSelectAlgorithm(world.comm, _COLL[collective], int(nbytes),
                                                     CODES[dtype], ctypes.byref(algo)))

@@ -318,6 +318,7 @@ class RankRuntime:
         code = ctypes.c_int()
         _lib.check(_lib.lib().cfPlanLastDeviceError(self._plan, ctypes.byref(code)))
         if code.value:
+            _lib.lib().cfPlanClearDeviceError(self._plan)   # the plan runs again after a reset
             raise DeadlockError(message="plan execution timed out on the device")
 
     def close(self):

@@ -1026,13 +1026,20 @@ __global__ void __launch_bounds__(512) ring_gather_kernel(const __grid_constant_
 // `collective("allreduce")` and host-side arithmetic).  Per row of `hidden`
 // elements, with h = x_0 + x_1 + ... + x_{n-1} (f32 accumulate, rounded to T
 // once -- the same bits on every rank):
-//   resid_out = T(h + resid)                       (written to out2)
-//   norm_out  = T(resid_out * rsqrt(mean(resid_out^2) + eps) * weight)   (out)
-// One CTA per row.  `push` (two-shot): rank r owns rows [r*per, (r+1)*per)
-// and stores both results into every rank's buffers; otherwise (one-shot)
-// every rank computes every row for itself.  The first kCache vectors of a
-// thread's share of the row stay in registers between the two passes; the
-// rest are re-read from this rank's own resid_out (written by the same thread).
+//   resid_out = T(h + resid[r])                       (written to out2)
+//   norm_out  = T(resid_out * rsqrt(mean(resid_out^2) + eps) * weight[r])   (out)
+// One CTA per row.  One-shot: every rank reduces every row itself.  Two-shot
+// (`push`): rank r owns rows [r*per, (r+1)*per); phase 1 reduces the owned
+// rows and stores h into every rank's norm_out (rows are disjoint per owner,
+// so this is safe in place); after a CTA-pair handshake every rank finishes
+// ALL rows with its OWN residual and weight (phase 2 touches only local
+// buffers), so per-rank residuals / weights are honoured.  CTA b of rank q
+// finishes exactly the rows CTA b of each owner pushed, so the pair handshake
+// orders every access that meets, and no exit handshake is needed: after the
+// mid handshake no peer reads or writes this rank's buffers.  The first
+// kCache vectors of a thread's share of the row stay in registers between
+// the two passes; the rest are re-read from this rank's own resid_out
+// (written by the same thread).
 template <typename T, int NR>
 __global__ void __launch_bounds__(512) ar_rmsnorm_kernel(const __grid_constant__ CollArgs a) {
   const RankCtx& rk = a.rk[blockIdx.y];
@@ -1040,29 +1047,52 @@ __global__ void __launch_bounds__(512) ar_rmsnorm_kernel(const __grid_constant__
   constexpr int V = Vec<T>::N;
   constexpr int kCache = 4;
   const int n = a.n, r = rk.rank;
-  const uint64_t e = begin_call_lazy(rk, a.single_launch);
+  const bool push = a.push;
+  const uint64_t e = push ? begin_call(rk) : begin_call_lazy(rk, a.single_launch);
   if (!a.single_launch) handshake(rk, n, e * kPhases + 1, false, a.gpu_scope);
-  size_t r0 = 0, r1 = a.rows;
-  if (a.push) {
-    const size_t per = (a.rows + n - 1) / n;
-    r0 = min((size_t)r * per, a.rows);
-    r1 = min(r0 + per, a.rows);
-  }
   const size_t nv = a.hidden / V;
   const size_t T0 = threadIdx.x, NT = blockDim.x;
+  const size_t per = push ? (a.rows + n - 1) / n : a.rows;
   __shared__ float s_red[32];
-  for (size_t row = r0 + blockIdx.x; row < r1; row += gridDim.x) {
+  if (push) {
+    // phase 1: owned rows, h pushed into every rank's norm_out
+    const size_t r0 = min((size_t)r * per, a.rows), r1 = min(r0 + per, a.rows);
+    for (size_t row = r0 + blockIdx.x; row < r1; row += gridDim.x) {
+      const size_t off = row * a.hidden * sizeof(T);
+      for (size_t v = T0; v < nv; v += NT) {
+        const size_t b = off + v * 16;
+        uint4 x[NR];
+#pragma unroll
+        for (int k = 0; k < NR; k++)
+          if (k < n) x[k] = ld16(rk.in[k] + b);
+        const uint4 h = reduce_vecs<T, NR>(x, n, false);
+#pragma unroll
+        for (int p = 0; p < NR; p++)
+          if (p < n) st16(rk.out[p] + b, h);
+      }
+    }
+    handshake(rk, n, e * kPhases + 2, true, a.gpu_scope);
+  }
+  // finish a row on this rank: h (reduced here, or pushed by its owner) +
+  // own residual, sum of squares, then the normalised row with own weight
+  auto finish_row = [&](size_t row) {
     const size_t off = row * a.hidden * sizeof(T);
     float ss = 0.f;
     uint4 cache[kCache];
     auto pass1 = [&](size_t v) -> uint4 {
       const size_t b = off + v * 16;
-      uint4 x[NR];
+      uint4 hv4;
+      if (push) {
+        hv4 = ld16(rk.out[r] + b);
+      } else {
+        uint4 x[NR];
 #pragma unroll
-      for (int k = 0; k < NR; k++)
-        if (k < n) x[k] = ld16(rk.in[k] + b);
+        for (int k = 0; k < NR; k++)
+          if (k < n) x[k] = ld16(rk.in[k] + b);
+        hv4 = reduce_vecs<T, NR>(x, n, false);
+      }
       A hv[V], rv[V];
-      Vec<T>::load(reduce_vecs<T, NR>(x, n, false), hv);
+      Vec<T>::load(hv4, hv);
       Vec<T>::load(ld16(rk.resid + b), rv);
 #pragma unroll
       for (int j = 0; j < V; j++) hv[j] = hv[j] + rv[j];
@@ -1071,13 +1101,7 @@ __global__ void __launch_bounds__(512) ar_rmsnorm_kernel(const __grid_constant__
       Vec<T>::load(ro, q);
 #pragma unroll
       for (int j = 0; j < V; j++) ss = fmaf(q[j], q[j], ss);
-      if (a.push) {
-#pragma unroll
-        for (int p = 0; p < NR; p++)
-          if (p < n) st16(rk.out2[p] + b, ro);
-      } else {
-        st16(rk.out2[r] + b, ro);
-      }
+      st16(rk.out2[r] + b, ro);
       return ro;
     };
 #pragma unroll
@@ -1105,21 +1129,22 @@ __global__ void __launch_bounds__(512) ar_rmsnorm_kernel(const __grid_constant__
       Vec<T>::load(ld16(rk.weight + v * 16), w);
 #pragma unroll
       for (int j = 0; j < V; j++) q[j] = q[j] * inv * w[j];
-      const uint4 y = Vec<T>::store(q);
-      if (a.push) {
-#pragma unroll
-        for (int p = 0; p < NR; p++)
-          if (p < n) st16(rk.out[p] + b, y);
-      } else {
-        st16(rk.out[r] + b, y);
-      }
+      st16(rk.out[r] + b, Vec<T>::store(q));
     };
 #pragma unroll
     for (int i = 0; i < kCache; i++)
       if (T0 + i * NT < nv) pass2(T0 + i * NT, cache[i]);
     for (size_t v = T0 + kCache * NT; v < nv; v += NT) pass2(v, ld16(rk.out2[r] + off + v * 16));
+  };
+  if (push) {
+    for (int o = 0; o < n; o++) {
+      const size_t r0 = min((size_t)o * per, a.rows), r1 = min(r0 + per, a.rows);
+      for (size_t row = r0 + blockIdx.x; row < r1; row += gridDim.x) finish_row(row);
+    }
+  } else {
+    for (size_t row = blockIdx.x; row < a.rows; row += gridDim.x) finish_row(row);
+    if (!a.single_launch) handshake(rk, n, e * kPhases + 2, true, a.gpu_scope);
   }
-  if (!a.single_launch) handshake(rk, n, e * kPhases + 2, true, a.gpu_scope);
   end_call(rk, e);
 }
 

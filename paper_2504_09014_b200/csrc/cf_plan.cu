@@ -1297,6 +1297,31 @@ extern "C" cfStatus cfPlanInfo(cfPlan_t pl, size_t* in_elems, size_t* out_elems,
   return CF_OK;
 }
 
+// Reset after a reported device timeout: a timed-out execution leaves
+// semaphore lanes, barrier counters and LL scratch in a state later calls
+// cannot reason about, so every heap this process owns returns to its load-
+// time state (zeroed, fresh PlanState).  One process per GPU: every rank calls
+// it at a quiescent point (no execution of the plan in flight anywhere).
+extern "C" cfStatus cfPlanClearDeviceError(cfPlan_t pl) {
+  if (!pl) return fail(CF_E_CONFIG, "null plan");
+  int prev = -1;
+  cudaGetDevice(&prev);
+  for (size_t r = 0; r < pl->heap.size(); r++) {
+    if (!pl->heap[r] || pl->heap_mapped[r]) continue;   // own heaps only
+    cudaSetDevice(pl->comm->local[pl->mp ? 0 : r].dev);
+    PlanState st;
+    memset(&st, 0, sizeof(st));
+    st.base.timeout_ns = pl->comm->cfg.spin_timeout_ns;
+    if (cudaDeviceSynchronize() != cudaSuccess || cudaMemset(pl->heap[r], 0, pl->heap_bytes) != cudaSuccess ||
+        cudaMemcpy(pl->heap[r] + pl->state_off, &st, sizeof(st), cudaMemcpyHostToDevice) != cudaSuccess) {
+      cudaSetDevice(prev);
+      return fail(CF_E_CUDA, "plan state reset failed");
+    }
+  }
+  cudaSetDevice(prev);
+  return CF_OK;
+}
+
 extern "C" cfStatus cfPlanLastDeviceError(cfPlan_t pl, int* code) {
   if (!pl || !code) return fail(CF_E_CONFIG, "null argument");
   int prev = -1;

@@ -205,8 +205,9 @@ static cfStatus comm_common_init(cfComm* c, int nranks, const cfConfig* cfg) {
   c->nranks = nranks;
   if (cfg) c->cfg = *cfg;
   apply_defaults(&c->cfg);
-  if (c->cfg.threads % 32 || c->cfg.threads < 64 || c->cfg.threads > 1024)
-    return fail(CF_E_CONFIG, "threads must be a multiple of 32 in [64, 1024]");
+  // every collective kernel is compiled with __launch_bounds__(512)
+  if (c->cfg.threads % 32 || c->cfg.threads < 64 || c->cfg.threads > 512)
+    return fail(CF_E_CONFIG, "threads must be a multiple of 32 in [64, 512]");
   c->lay.compute(nranks, c->cfg.ll_max_bytes);
   return CF_OK;
 }
@@ -593,7 +594,7 @@ cfStatus launch(cfComm* c, const Job& j, int dtype, const void* const* send, voi
   const bool need_in = j.kind == kPull || j.kind == kNorm;
   const bool need_out = j.kind == kGather || j.kind == kRingGather ||
                         ((j.kind == kPull || j.kind == kNorm || j.kind == kRing) && j.push);
-  const bool need_out2 = j.kind == kNorm && j.push;
+  const bool need_out2 = false;   // K13 writes only its own resid_out (both modes)
   const Registration* reg_in = nullptr;
   const Registration* reg_out = nullptr;
   const Registration* reg_out2 = nullptr;
@@ -867,10 +868,20 @@ extern "C" cfStatus cfAllReduceAddRMSNorm(cfComm_t c, const void* const* send, c
     // enough for the (n-1)x smaller reads to beat the extra pushes (measured,
     // [b, 8192] bf16, 8 ranks: one-shot 7.0 vs 9.4 us at 256 KiB, 9.7 vs 9.9
     // at 512 KiB, 16.6 vs 10.6 at 1 MiB)
+    // The pick depends only on rank-uniform arguments (rows, hidden, dtype,
+    // n), so every rank of a one-process-per-GPU communicator launches the
+    // same kernel.  In place (send == norm_out) needs two-shot: in one
+    // process every rank is local, so the in-place test is uniform too; one
+    // process per GPU cannot see the peers' pointers and reports it instead.
     algo = (rows >= (size_t)n && rows * hidden * es > ((size_t)512 << 10)) ? CF_ALGO_2PA : CF_ALGO_1PA_HB;
     if (algo == CF_ALGO_1PA_HB)
       for (size_t li = 0; li < c->local.size(); li++)
-        if (send[li] == norm_out[li]) algo = CF_ALGO_2PA;
+        if (send[li] == norm_out[li]) {
+          if (c->multiprocess)
+            return fail(CF_E_SHAPE, "in-place fused AllReduce with algo=auto: pass CF_ALGO_2PA explicitly in "
+                                    "the one-process-per-GPU mode (AUTO must pick the same kernel on every rank)");
+          algo = CF_ALGO_2PA;
+        }
   }
   Job j;
   j.kind = kNorm;

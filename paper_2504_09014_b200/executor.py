@@ -86,6 +86,7 @@ class Runtime:
         code = ctypes.c_int()
         _lib.check(_lib.lib().cfPlanLastDeviceError(self._plan, ctypes.byref(code)))
         if code.value:
+            _lib.lib().cfPlanClearDeviceError(self._plan)   # the plan runs again after a reset
             raise DeadlockError(message="plan execution timed out on the device: a wait, packet "
                                         "read or barrier was never satisfied")
         trace = self._static_trace() if collect_trace else None
@@ -110,6 +111,7 @@ class Runtime:
         code = ctypes.c_int()
         _lib.check(_lib.lib().cfPlanLastDeviceError(self._plan, ctypes.byref(code)))
         if code.value:
+            _lib.lib().cfPlanClearDeviceError(self._plan)   # the plan runs again after a reset
             raise DeadlockError(message="plan execution timed out on the device")
 
     def _static_trace(self):

@@ -87,6 +87,28 @@ def collectives_cases():
     # the facade's automatic selection at a few sizes (cf/collectives.py:550-556)
     for n, elems in ((8, 16), (8, 8192), (4, 4096)):
         cases.append(("allreduce", "", "", n, elems, "i32", "int", 77 + elems))
+    # default selection with f32 (order-sensitive) on both sides of the 32 KiB
+    # crossover, default ReduceScatter (ring_rs: 2n padding, ring order) and
+    # default AllGather on both sides of the 1 MiB crossover
+    for n, elems in ((8, 16), (8, 8193), (4, 8192), (4, 8191)):
+        cases.append(("allreduce", "", "", n, elems, "f32", "uniform", 91 + elems))
+    for n, elems in ((4, 12), (8, 24), (8, 100), (2, 7), (4, 1026)):
+        cases.append(("reducescatter", "", "", n, elems, "f32", "uniform", 93 + elems))
+        cases.append(("reducescatter", "", "", n, elems, "i32", "int", 95 + elems))
+    for n, elems in ((8, 5), (4, 65536), (2, 131072)):
+        cases.append(("allgather", "", "", n, elems, "i32", "bits", 97 + elems))
+    return cases
+
+
+# default selection under explicit thresholds: the reference's Selector with a
+# small `large` so 2pr (ring order) is picked at test sizes (cf/collectives.py:464-486)
+SEL_THRESHOLDS = {"small": 64, "large": 1024}
+
+
+def selector_cases():
+    cases = []
+    for n, elems in ((4, 8), (4, 100), (8, 512), (8, 1000)):
+        cases.append(("allreduce", "", "", n, elems, "f32", "uniform", 101 + elems))
     return cases
 
 
@@ -103,6 +125,14 @@ def make_collectives():
         if elems <= 16:
             case["outputs"] = [np.asarray(o).view(np.uint32).tolist() for o in res]
         out.append(case)
+    from commforge.collectives import Selector
+    for kind, algo, var, n, elems, dtype, dist, seed in selector_cases():
+        ins = gen_inputs(n, elems, dtype, dist, seed)
+        w = make_world(1, n, seed=7)
+        res = collective(kind, ins, w, dtype=dtype, selector=Selector(thresholds=dict(SEL_THRESHOLDS)))
+        out.append({"kind": kind, "algo": "", "variant": "", "n": n, "elems": elems, "dtype": dtype,
+                    "dist": dist, "seed": seed, "thresholds": SEL_THRESHOLDS,
+                    "out_len": [int(len(o)) for o in res], "digests": [digest(o) for o in res]})
     with open(os.path.join(HERE, "collectives.json"), "w") as f:
         json.dump(out, f, indent=0, sort_keys=True)
     print(f"collectives.json: {len(out)} cases")
@@ -260,6 +290,9 @@ def make_lowp():
 if __name__ == "__main__":
     if "--lowp" in sys.argv:
         make_lowp()
+        sys.exit(0)
+    if "--collectives" in sys.argv:
+        make_collectives()
         sys.exit(0)
     if "--ag-bf16" in sys.argv:
         make_ag_bf16()

@@ -57,3 +57,16 @@ def test_kernels_are_sm100a_cubins():
                          capture_output=True, text=True).stdout
     assert "sm_100a" in out
     assert all("sm_100a" in line for line in out.splitlines() if line.strip())
+
+
+def test_config_rejects_threads_beyond_launch_bounds():
+    """Every collective kernel is compiled with __launch_bounds__(512): larger
+    CTAs are rejected at init (E_CONFIG), before any device is touched."""
+    from paper_2504_09014_b200 import _lib, errors
+    lib = _lib.lib()
+    for threads in (1024, 544, 48, 100):
+        cfg = _lib.cfConfig(threads=threads)
+        comm = ctypes.c_void_p()
+        devs = (ctypes.c_int * 2)(0, 0)
+        st = lib.cfCommInitAll(ctypes.byref(comm), 2, devs, ctypes.byref(cfg))
+        assert errors.STATUS_CODES[st] == "E_CONFIG", threads

@@ -31,17 +31,20 @@ def _digest(a):
 
 def _cases():
     with open(os.path.join(GOLD, "collectives.json")) as f:
-        return [c for c in json.load(f) if c["algo"]]
+        return json.load(f)
 
 
-@pytest.mark.parametrize("case", _cases(), ids=lambda c: f"{c['kind']}-{c['algo']}{c['variant']}"
-                         f"-n{c['n']}-e{c['elems']}-{c['dtype']}-{c['dist']}")
+@pytest.mark.parametrize("case", _cases(), ids=lambda c: f"{c['kind']}-{c['algo'] or 'default'}{c['variant']}"
+                         f"-n{c['n']}-e{c['elems']}-{c['dtype']}-{c['dist']}{'-sel' if 'thresholds' in c else ''}")
 def test_gpu_matches_reference_bits(case):
-    """Every reference algorithm on the GPU returns the reference's exact bits."""
-    from paper_2504_09014_b200 import collective
+    """Every reference algorithm on the GPU returns the reference's exact bits;
+    so does the facade's default selection (algo=None: the reference's
+    threshold table, also with explicit Selector thresholds)."""
+    from paper_2504_09014_b200 import Selector, collective
     ins = gen_inputs(case["n"], case["elems"], case["dtype"], case["dist"], case["seed"])
-    outs = collective(case["kind"], ins, world(case["n"]), dtype=case["dtype"],
-                      algo=case["algo"], variant=case["variant"])
+    sel = Selector(thresholds=dict(case["thresholds"])) if "thresholds" in case else None
+    outs = collective(case["kind"], ins, world(case["n"]), dtype=case["dtype"], selector=sel,
+                      algo=case["algo"] or None, variant=case["variant"])
     assert [len(o) for o in outs] == case["out_len"]
     assert [_digest(o) for o in outs] == case["digests"]
 

@@ -123,3 +123,25 @@ def test_fused_errors():
     xo = [torch.ones(2, 3, dtype=torch.bfloat16, device="cuda") for _ in range(8)]
     with pytest.raises(BadAlignError):   # rows must be whole 16-byte vectors
         allreduce_add_rmsnorm(wd, xo, [x.clone() for x in xo], torch.ones(3, dtype=torch.bfloat16, device="cuda"))
+
+
+@pytest.mark.parametrize("algo", ["1pa_hb", "2pa", None])
+@pytest.mark.parametrize("rows,hidden", [(8, 8192), (64, 8192), (17, 1024)])
+def test_fused_per_rank_residual_and_weight(algo, rows, hidden):
+    """Distinct residuals and weights per rank: rank r's outputs use ITS
+    residual and weight (cf.h contract), also on the two-shot path where
+    another rank reduced the row."""
+    from paper_2504_09014_b200 import allreduce_add_rmsnorm
+    n, dt, eps = 8, torch.bfloat16, 1e-6
+    wd = world(n)
+    g = torch.Generator(device="cpu").manual_seed(rows + hidden)
+    xs = [(torch.randn(rows, hidden, generator=g) * 0.5).to(dt).cuda() for _ in range(n)]
+    res = [torch.randn(rows, hidden, generator=g).to(dt).cuda() for _ in range(n)]
+    ws = [(1.0 + 0.1 * torch.randn(hidden, generator=g)).to(dt).cuda() for _ in range(n)]
+    want = [reference(xs, res[r], ws[r], eps) for r in range(n)]
+    y, ro = allreduce_add_rmsnorm(wd, xs, [t.clone() for t in res], ws, eps=eps, algo=algo)
+    wd.synchronize()
+    for r in range(n):
+        y_ref, ro_ref = want[r]
+        assert torch.equal(ro[r].view(torch.int16), ro_ref.view(torch.int16)), f"rank {r} resid"
+        torch.testing.assert_close(y[r].float(), y_ref.float(), rtol=RTOL[dt], atol=1e-6)

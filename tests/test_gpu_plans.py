@@ -4,6 +4,7 @@ and vs the oracle's sequential plan interpreter.  Needs a B200."""
 import hashlib
 import json
 import os
+import time
 
 import numpy as np
 import pytest
@@ -143,6 +144,14 @@ def test_wait_without_signal_raises_deadlock():
     rt = Runtime(plan, w)
     with pytest.raises(DeadlockError):
         rt.execute([np.zeros(4, np.int32)] * 2)
+    # the report resets the plan (cfPlanClearDeviceError): the error word is
+    # clear, and the next execution really spins for its timeout again
+    # instead of short-circuiting on a stale error word
+    rt.check_device_error()
+    t0 = time.perf_counter()
+    with pytest.raises(DeadlockError):
+        rt.execute([np.zeros(4, np.int32)] * 2)
+    assert time.perf_counter() - t0 >= 0.25
     rt.close()
     w.close()
 

@@ -23,11 +23,12 @@ def _cases():
         return json.load(f)
 
 
-def _auto_algo(kind, n, elems):
+def _auto_algo(kind, n, elems, thresholds=None):
     # cf/collectives.py:418-461 single-node defaults, bytes = elems*4*(n if AG)
+    t = {"small": 32 * 1024, "large": 64 << 20, **(thresholds or {})}
     nbytes = elems * 4 * (n if kind == "allgather" else 1)
     if kind == "allreduce":
-        return "1pa" if nbytes < 32 * 1024 else ("2pa" if nbytes < 64 << 20 else "2pr")
+        return "1pa" if nbytes < t["small"] else ("2pa" if nbytes < t["large"] else "2pr")
     if kind == "allgather":
         return "allpairs_ag" if nbytes < 1 << 20 else "ring_ag"
     return "ring_rs"
@@ -37,7 +38,7 @@ def _auto_algo(kind, n, elems):
                          f"{c['variant']}-n{c['n']}-e{c['elems']}-{c['dtype']}-{c['dist']}")
 def test_oracle_matches_reference_collective(case):
     ins = gen_inputs(case["n"], case["elems"], case["dtype"], case["dist"], case["seed"])
-    algo = case["algo"] or _auto_algo(case["kind"], case["n"], case["elems"])
+    algo = case["algo"] or _auto_algo(case["kind"], case["n"], case["elems"], case.get("thresholds"))
     if case["kind"] == "allreduce":
         outs = oracle.allreduce(ins, algo, case["dtype"])
     elif case["kind"] == "reducescatter":
