@@ -100,31 +100,48 @@ class ClockSampler:
 
 # ----------------------------------------------------------------------------- CPU arms
 
-def cpu_reference_step(n, elems, dtype, algo, seed=0):
-    """One step of the reference algorithm on the host: the oracle port
-    (C + pthreads over every core) applied to `elems` per rank."""
+def bench_inputs(n, elems, seed):
+    """Per-rank bf16 inputs of the headline workload as uint16 patterns: finite
+    values of both signs with magnitudes in [2^-31, 2^32) (fast to generate at
+    256 MiB per rank; the CPU step's cost does not depend on the values)."""
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(n):
+        b = rng.integers(0, 1 << 16, elems, dtype=np.uint16)
+        out.append((b & np.uint16(0x80FF)) | np.uint16(0x3000) | ((b >> np.uint16(1)) & np.uint16(0x0F00)))
+    return out
+
+
+def cpu_reference_steps(ins, dtype, algo, steps, budget_s=None):
+    """Time `steps` full steps of the reference algorithm on the host: the
+    oracle port (oracle/, C + pthreads over every host core) over every
+    rank's whole message -- the reference computes every rank's output of the
+    AllReduce (cf/executor.py:135-178), so one step is the whole job."""
     from oracle import oracle
-    from inputs import gen_inputs
-    ins = gen_inputs(n, elems, dtype, "normal", seed)
-    t0 = time.perf_counter()
-    oracle.allreduce(ins, algo, dtype, nthreads=0)
-    return time.perf_counter() - t0
+    ts = []
+    t_end = None if budget_s is None else time.perf_counter() + budget_s
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        oracle.allreduce(ins, algo, dtype, nthreads=0)
+        ts.append(time.perf_counter() - t0)
+        if t_end is not None and time.perf_counter() > t_end:
+            break
+    return ts
 
 
 def cpu_baseline(n, full_elems, dtype, algo, budget_s=15.0):
-    """Bounded sample (~budget_s of CPU work) of the same workload."""
+    """The reference's CPU path on the SAME workload (n ranks x full_elems),
+    a bounded number of steps (about budget_s of CPU work)."""
     from oracle import oracle
     es = 2 if dtype in ("bf16", "f16") else 4
-    elems = min(full_elems, 4 * MiB // es)
-    times = []
-    t_end = time.perf_counter() + budget_s
-    while time.perf_counter() < t_end and len(times) < 20:
-        times.append(cpu_reference_step(n, elems, dtype, algo, seed=len(times)))
+    ins = bench_inputs(n, full_elems, 77)
+    cpu_reference_steps(ins, dtype, algo, 1)            # warm-up (page faults)
+    times = cpu_reference_steps(ins, dtype, algo, 20, budget_s)
     t = float(np.median(times))
-    return {"value": round(busbw(elems * es, t, n), 4), "unit": "GB/s",
+    return {"value": round(busbw(full_elems * es, t, n), 4), "unit": "GB/s",
             "cores": oracle.max_threads(), "kind": "port",
-            "sample": f"{len(times)} steps of {n}-rank {dtype} AllReduce ({algo} order) on "
-                      f"{elems * es // KiB} KiB per rank (full workload {full_elems * es // MiB} MiB); "
+            "sample": f"{len(times)} full steps of the {n}-rank {dtype} AllReduce ({algo} order), "
+                      f"{full_elems * es // MiB} MiB per rank (the bench workload itself); "
                       f"median {t * 1e3:.1f} ms/step"}
 
 
@@ -135,23 +152,22 @@ def run_reference_arm(args):
     from oracle import oracle
     es = 2
     full = HEAD_BYTES // es
-    elems = min(full, 4 * MiB // es)
-    for _ in range(args.warmup):
-        cpu_reference_step(N_SIM, elems, HEAD_DTYPE, "2pa")
-    ts = [cpu_reference_step(N_SIM, elems, HEAD_DTYPE, "2pa", seed=i) for i in range(args.steps)]
+    ins = bench_inputs(N_SIM, full, 78)
+    cpu_reference_steps(ins, HEAD_DTYPE, "2pa", max(1, args.warmup))
+    ts = cpu_reference_steps(ins, HEAD_DTYPE, "2pa", args.steps)
     t = float(np.mean(ts))
-    v = busbw(elems * es, t, N_SIM)
+    v = busbw(HEAD_BYTES, t, N_SIM)
     line = {"impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": "GB/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(t * 1e3, 3), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": HEAD_DTYPE, "data": "synthetic",
             "config": {"workload": f"AllReduce {HEAD_DTYPE} {N_SIM} ranks, {HEAD_BYTES // MiB} MiB "
                                    "per rank (C4 shape), two-shot (2pa) order",
-                       "sample_bytes_per_rank": elems * es},
+                       "sample_bytes_per_rank": HEAD_BYTES, "same_config": True},
             "cpu_baseline": {"value": round(v, 4), "unit": "GB/s", "cores": oracle.max_threads(),
                              "kind": "port",
-                             "sample": f"{elems * es // KiB} KiB per rank of the {HEAD_BYTES // MiB} MiB "
-                                       "workload per step (oracle/ C port, pthreads)"},
+                             "sample": f"the full workload every step: {N_SIM} x {HEAD_BYTES // MiB} MiB "
+                                       "(oracle/ C port of the reference arithmetic, pthreads)"},
             "e2e": {"value": round(v, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
@@ -290,7 +306,9 @@ def run_gpu_arm(args):
     from paper_2504_09014_b200 import collectives as C
     from paper_2504_09014_b200.dtypes import torch_dtype
 
-    if args.gpus > 1:
+    if args.gpus > 1 or os.environ.get("CF_BENCH_MULTI"):
+        # CF_BENCH_MULTI=1 with --gpus 1: the one-process-per-GPU code path
+        # (and its NCCL arms) as a single rank -- a path check on 1-GPU boxes
         return run_multi_gpu(args)
     n = N_SIM
     w = make_world(1, n, devices=[0] * n)
@@ -386,7 +404,6 @@ def run_gpu_arm(args):
                        "algo": _lib.ALGO_NAMES[algo], "parallelism": "8 ranks / 1 GPU",
                        "l2": "inputs larger than L2 (8 x 256 MiB)"},
             "latency_us": round(t * 1e6, 2), "algbw_gbs": round(HEAD_BYTES / t / 1e9, 2),
-            "pct_of_900": round(100 * value / 900, 2),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": args.steps, "clocks": clk.summary(),
             "wall_s_timed": round(wall, 4), "sweep": sweep}
@@ -470,34 +487,147 @@ def run_sweep(w, args):
     return out
 
 
-def multi_sweep(comm, dev, world, send, recv):
-    """N>1: AllReduce latency / busbw over sizes -- libcf (CUDA graph and
-    eager) next to NCCL (eager, through torch.distributed; the comparison
-    baseline of BASELINE.md, never part of the product path).  Per-rank times;
-    the caller takes the max over ranks."""
+def nccl_setup(dev, rank, world):
+    """NCCL 2.28 through ctypes (scripts/nccl_ctypes.py): the comparison
+    baseline only.  Returns (Nccl, None) or (None, reason).  Ranks sharing
+    one GPU (CF_BENCH_ONE_GPU) cannot run NCCL (duplicate GPU)."""
+    import torch.distributed as dist
+    if os.environ.get("CF_BENCH_ONE_GPU"):
+        return None, "ranks share cuda:0 (CF_BENCH_ONE_GPU): NCCL needs one GPU per rank"
+    try:
+        sys.path.insert(0, os.path.join(ROOT, "scripts"))
+        from nccl_ctypes import Nccl
+        uid = [Nccl.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        nc = Nccl(world, rank, uid[0])
+        return nc, None
+    except Exception as e:   # comparison only: report, never fail the bench
+        return None, f"{type(e).__name__}: {e}"[:200]
+
+
+def multi_parity(comm, dev, rank, world, nvls):
+    """Before timing: libcf's NVLink results against the CPU oracle, bit for
+    bit (bf16, ragged size, seeded inputs regenerated on every rank): 1pa,
+    2pa_ll, 2pa, direct and ring AllGather, both ReduceScatters, and NVLS
+    (switch order is unspecified: SURVEY §8(c) tolerance).  Returns
+    {check: ok} agreed over ranks (all ranks must pass)."""
     import torch
     import torch.distributed as dist
+    from oracle import oracle
+    from inputs import gen_inputs
+    from paper_2504_09014_b200.dtypes import torch_dtype
+
+    def dev_t(a):
+        return torch.from_numpy(a.view(np.int16)).to(dev).view(torch_dtype("bf16"))
+
+    def host(t):
+        return t.view(torch.int16).cpu().numpy().view(np.uint16)
+
+    res = {}
+    elems = 8 * 4099 + 3     # ragged: chunk bounds off the vector grid
+    ins = gen_inputs(world, elems, "bf16", "normal", 20250409 + 7)
+    x = dev_t(ins[rank])
+    y = torch.empty_like(x)
+    comm.register(x)
+    comm.register(y)
+    algos = [("1pa", "1pa"), ("2pa_ll", "2pa"), ("2pa", "2pa")]
+    for name, oname in algos:
+        try:
+            y.zero_()
+            if name == "2pa_ll":
+                comm.all_reduce(x, y, algo="2pa", variant="ll")
+            else:
+                comm.all_reduce(x, y, algo=name)
+            torch.cuda.synchronize(dev)
+            comm.check_device_error()
+            res["allreduce_" + name] = bool(np.array_equal(host(y), oracle.allreduce(ins, oname, "bf16")[rank]))
+        except Exception as e:
+            res["allreduce_" + name] = f"{type(e).__name__}: {e}"[:160]
+    if nvls:
+        try:
+            comm.all_reduce(x, y, algo="switch_2pa")
+            torch.cuda.synchronize(dev)
+            comm.check_device_error()
+            want = oracle.allreduce(ins, "switch_2pa", "bf16")[rank]
+            w32 = (want.astype(np.uint32) << 16).view(np.float32)
+            g32 = (host(y).astype(np.uint32) << 16).view(np.float32)
+            sabs = np.sum([np.abs((a.astype(np.uint32) << 16).view(np.float32)) for a in ins], axis=0)
+            tol = 2.0 ** -8 * np.abs(w32) + (world - 1) * 2.0 ** -24 * sabs
+            res["allreduce_switch_2pa"] = bool(np.all(np.abs(g32 - w32) <= tol))
+        except Exception as e:
+            res["allreduce_switch_2pa"] = f"{type(e).__name__}: {e}"[:160]
+    comm.deregister(x)
+    comm.deregister(y)
+    # AllGather (bit-exact data movement, random 16-bit patterns incl. NaNs)
+    shard = 4099
+    sh = [a[:shard] for a in gen_inputs(world, shard, "bf16", "normal", 20250409 + 8)]
+    xs = dev_t(sh[rank])
+    ys = torch.empty(shard * world, device=dev, dtype=xs.dtype)
+    comm.register(xs)
+    comm.register(ys)
+    for name in ("allpairs_ag", "ring_ag"):
+        try:
+            ys.zero_()
+            comm.all_gather(xs, ys, algo=name)
+            torch.cuda.synchronize(dev)
+            res["allgather_" + name] = bool(np.array_equal(host(ys), oracle.allgather(sh)[rank]))
+        except Exception as e:
+            res["allgather_" + name] = f"{type(e).__name__}: {e}"[:160]
+    comm.deregister(xs)
+    comm.deregister(ys)
+    # ReduceScatter (reference orders: rs_direct = owner first, ring_rs = ring order)
+    shard = 4100   # n * shard divides 2n: ring_rs needs no padding
+    rin = gen_inputs(world, shard * world, "bf16", "normal", 20250409 + 9)
+    xr = dev_t(rin[rank])
+    yr = torch.empty(shard, device=dev, dtype=xr.dtype)
+    comm.register(xr)
+    comm.register(yr)
+    for name in ("rs_direct", "ring_rs"):
+        try:
+            comm.reduce_scatter(xr, yr, algo=name)
+            torch.cuda.synchronize(dev)
+            want = oracle.reducescatter(rin, "2pa" if name == "rs_direct" else "ring_rs", "bf16")[rank]
+            res["reducescatter_" + name] = bool(np.array_equal(host(yr), want[:shard]))
+        except Exception as e:
+            res["reducescatter_" + name] = f"{type(e).__name__}: {e}"[:160]
+    comm.deregister(xr)
+    comm.deregister(yr)
+    allres = [None] * world
+    dist.all_gather_object(allres, res)
+    return {k: all(r.get(k) is True for r in allres) if all(isinstance(r.get(k), bool) for r in allres)
+            else next(r[k] for r in allres if r.get(k) is not True) for k in res}
+
+
+def multi_sweep(comm, dev, rank, world, send, recv, nvls, nvls_kind, nccl):
+    """N>1: latency / busbw over sizes -- libcf (CUDA graph and eager) next to
+    NCCL 2.28 (comparison baseline only, never part of the product path) in a
+    CUDA graph on default buffers AND on symmetric windows (ncclMemAlloc +
+    ncclCommWindowRegister(NCCL_WIN_COLL_SYMMETRIC)); the better NCCL mode is
+    the bar.  L2 flushed between timed iterations below 64 MiB (both arms).
+    Per-rank times; the caller takes the max over ranks."""
+    import torch
     from paper_2504_09014_b200 import _lib
-    nccl = None
-    try:
-        nccl = dist.new_group(backend="nccl")
-        probe = torch.ones(16, device=dev)
-        dist.all_reduce(probe, group=nccl)
-        torch.cuda.synchronize(dev)
-    except Exception as e:   # comparison only: report, never fail the bench
-        nccl = None
-        nccl_err = f"{type(e).__name__}: {e}"[:200]
     rows = []
     # 1 KiB .. 1 GiB (x4); buffers of the largest size, registered once
-    big = GiB if not os.environ.get("CF_BENCH_ONE_GPU") else 256 * MiB
+    big = GiB if not os.environ.get("CF_BENCH_ONE_GPU") else 64 * MiB
     bs = torch.randn(big // 2, device=dev).to(torch.bfloat16)
     br = torch.empty_like(bs)
     comm.register(bs)
     comm.register(br)
+    flush = torch.empty(256 * MiB, dtype=torch.uint8, device=dev)
     st = torch.cuda.current_stream(dev)
-    iters = 10
+    sym = None
+    if nccl is not None:
+        try:   # symmetric windows, same size on every rank (collective calls)
+            sp, rp = nccl.mem_alloc(big), nccl.mem_alloc(big)
+            nccl.register_symmetric(sp, big)
+            nccl.register_symmetric(rp, big)
+            sym = (sp, rp)
+        except Exception as e:
+            rows.append({"bytes": 0, "kind": "nccl_symmetric", "error": f"{type(e).__name__}: {e}"[:200]})
+        nz_s, nz_r = bs.clone(), torch.empty_like(br)   # NCCL's default (plain) buffers
 
-    def eager(fn):
+    def eager(fn, iters):
         for _ in range(3):
             fn()
         torch.cuda.synchronize(dev)
@@ -509,27 +639,41 @@ def multi_sweep(comm, dev, world, send, recv):
         e1.synchronize()
         return e0.elapsed_time(e1) / 1e3 / iters
 
+    def cur():
+        return torch.cuda.current_stream(dev).cuda_stream
+
+    def nccl_times(kind, nbytes_in, nbytes_out, iters, fl):
+        """NCCL graph time on plain and on symmetric buffers (elements: 2 B)."""
+        out = {}
+        fn = {"allreduce": lambda s, r: nccl.all_reduce(s, r, nbytes_in // 2, "bf16", cur()),
+              "allgather": lambda s, r: nccl.all_gather(s, r, nbytes_in // 2, "bf16", cur()),
+              "reducescatter": lambda s, r: nccl.reduce_scatter(s, r, nbytes_out // 2, "bf16", cur())}[kind]
+        out["nccl_graph_s"] = time_graph(dev, lambda: fn(nz_s.data_ptr(), nz_r.data_ptr()), iters, 3, fl)
+        if sym is not None:
+            out["nccl_sym_graph_s"] = time_graph(dev, lambda: fn(sym[0], sym[1]), iters, 3, fl)
+        return out
+
     for nb in [KiB << (2 * i) for i in range(11)]:
         if nb > big:
             break
         cnt = nb // 2
         x, y = bs[:cnt], br[:cnt]
         iters = 50 if nb <= MiB else 10
-        t_graph = time_graph(dev, lambda: comm.all_reduce(x, y, algo="auto"), iters, 3)
-        t_eager = eager(lambda: comm.all_reduce(x, y, algo="auto"))
-        row = {"bytes": nb, "cf_graph_s": t_graph, "cf_eager_s": t_eager}
+        fl = flush if nb < 64 * MiB else None
+        row = {"bytes": nb, "kind": "allreduce",
+               "cf_graph_s": time_graph(dev, lambda: comm.all_reduce(x, y, algo="auto"), iters, 3, fl),
+               "cf_eager_s": eager(lambda: comm.all_reduce(x, y, algo="auto"), iters)}
         if nccl is not None:
-            z = y.clone()
-            row["nccl_eager_s"] = eager(lambda: dist.all_reduce(z, group=nccl))
+            row.update(nccl_times("allreduce", nb, nb, iters, fl))
         rows.append(row)
     # C2 / RS: AllGather (S = output bytes) and ReduceScatter (S = input bytes)
-    # over the same registered buffers, libcf (auto) graph vs NCCL eager
     for nb in [KiB << (2 * i) for i in range(11)]:
         if nb > big or nb // 2 < world:
             continue
         cnt = nb // 2 // world * world
         shard = cnt // world
         iters = 50 if nb <= MiB else 10
+        fl = flush if nb < 64 * MiB else None
         for kind in ("allgather", "reducescatter"):
             if kind == "allgather":
                 x, y = bs[:shard], br[:cnt]
@@ -537,47 +681,11 @@ def multi_sweep(comm, dev, world, send, recv):
             else:
                 x, y = bs[:cnt], br[:shard]
                 fn = lambda: comm.reduce_scatter(x, y, algo="auto")  # noqa: E731
-            row = {"bytes": cnt * 2, "kind": kind, "cf_graph_s": time_graph(dev, fn, iters, 3)}
+            row = {"bytes": cnt * 2, "kind": kind, "cf_graph_s": time_graph(dev, fn, iters, 3, fl)}
             if nccl is not None:
-                zx, zy = x.clone(), y.clone()
-                if kind == "allgather":
-                    row["nccl_eager_s"] = eager(lambda: dist.all_gather_into_tensor(zy, zx, group=nccl))
-                else:
-                    row["nccl_eager_s"] = eager(lambda: dist.reduce_scatter_tensor(zy, zx, group=nccl))
+                row.update(nccl_times(kind, (shard if kind == "allgather" else cnt) * 2,
+                                      (cnt if kind == "allgather" else shard) * 2, iters, fl))
             rows.append(row)
-    # NVLS (switch_2pa, multimem ld_reduce / st) when the box builds a multicast object
-    nvls = False
-    nvls_kind = "nvls"
-    try:
-        nvls = comm.setup_nvls()
-        if not nvls and os.environ.get("CF_BENCH_ONE_GPU"):
-            # path check on a 1-GPU box: the emulated switch runs the same
-            # kernel and bench code (rows labelled as such, not an NVLS number)
-            comm.setup_nvls_emulated(64 << 20)
-            nvls, nvls_kind = True, "nvls_emulated"
-    except Exception as e:   # report, never fail the bench
-        rows.append({"bytes": 0, "kind": "nvls", "error": f"{type(e).__name__}: {e}"[:200]})
-    if nvls:
-        # first real multimem execution on this box: check it against the
-        # two-shot result (switch order is unspecified: tolerance) before
-        # timing; any failure drops the NVLS rows, never the bench line
-        try:
-            cnt = MiB // 2
-            x, y = bs[:cnt], br[:cnt]   # registered buffers (the HB check writes peers' recv)
-            comm.all_reduce(x, y, algo="2pa")
-            y2 = y.clone()
-            comm.all_reduce(x, y, algo="switch_2pa")
-            torch.cuda.synchronize(dev)
-            comm.check_device_error()
-            ok = bool(torch.allclose(y.float(), y2.float(), rtol=2 ** -7, atol=1e-2))
-            flags = [None] * world
-            dist.all_gather_object(flags, ok)
-            if not all(flags):
-                raise RuntimeError("switch_2pa result differs from 2pa")
-        except Exception as e:
-            nvls = False
-            _lib.lib().cfCommClearDeviceError(comm.comm)
-            rows.append({"bytes": 0, "kind": "nvls", "error": f"{type(e).__name__}: {e}"[:200]})
     if nvls:
         for nb in [MiB << (2 * i) for i in range(6)]:
             if nb > big:
@@ -585,7 +693,7 @@ def multi_sweep(comm, dev, world, send, recv):
             cnt = nb // 2
             x, y = bs[:cnt], br[:cnt]
             rows.append({"bytes": nb, "kind": nvls_kind, "cf_graph_s": time_graph(
-                dev, lambda: comm.all_reduce(x, y, algo="switch_2pa"), 10, 3)})
+                dev, lambda: comm.all_reduce(x, y, algo="switch_2pa"), 10, 3, flush if nb < 64 * MiB else None)})
     comm.deregister(bs)
     comm.deregister(br)
     del bs, br
@@ -598,25 +706,32 @@ def multi_sweep(comm, dev, world, send, recv):
             params = LoweringParams(world, elems, "bf16", "LL" if name == "1pa" else "HB")
             rt = comm.load_plan(lower(build_algo(name, params, variant=var), params), dtype="bf16")
             px, py = send[:rt.in_elems], recv[:rt.out_elems]
-            t = time_graph(dev, lambda: rt.run(px, py), 20, 3)
+            t = time_graph(dev, lambda: rt.run(px, py), 20, 3, flush)
             rt.check_device_error()
-            rows.append({"bytes": elems * 2, "plan": f"{name}{'_' + var if var else ''}", "batch": b,
-                         "cf_plan_graph_s": t})
+            row = {"bytes": elems * 2, "kind": "allreduce", "plan": f"{name}{'_' + var if var else ''}",
+                   "batch": b, "cf_plan_graph_s": t,
+                   "cf_graph_s": time_graph(dev, lambda: comm.all_reduce(px[:elems], py[:elems], algo="auto"),
+                                            20, 3, flush)}
+            if nccl is not None and name == "2pa":
+                row.update(nccl_times("allreduce", elems * 2, elems * 2, 20, flush))
+            rows.append(row)
             rt.close()
     comm.check_device_error()
-    return rows, (None if nccl is not None else nccl_err)
+    return rows
 
 
 def gather_max_over_ranks(t_local, e2e_local, rows_local, world, group=None):
     """All ranks: gather every rank's step time, e2e time and sweep rows
     (torch.distributed object all-gather over the bootstrap group) and reduce
     each time to its max over ranks; busbw per row uses the collective's bus
-    factor (AllReduce 2(n-1)/n, AllGather / ReduceScatter (n-1)/n)."""
+    factor (AllReduce 2(n-1)/n, AllGather / ReduceScatter (n-1)/n) and is
+    also given as a percentage of 900 GB/s per direction (NVLink 5)."""
     import torch.distributed as dist
     times = [None] * world
     dist.all_gather_object(times, (t_local, e2e_local, rows_local), group=group)
     t = max(x[0] for x in times)
     te = max(x[1] for x in times)
+    one_gpu = bool(os.environ.get("CF_BENCH_ONE_GPU"))
     sweep = []
     for i, row in enumerate(rows_local):
         nb = row["bytes"]
@@ -625,18 +740,27 @@ def gather_max_over_ranks(t_local, e2e_local, rows_local, world, group=None):
         for k2 in ("plan", "batch", "kind", "error"):
             if k2 in row:
                 out[k2] = row[k2]
-        for key in ("cf_graph_s", "cf_eager_s", "nccl_eager_s", "cf_plan_graph_s"):
+        for key in ("cf_graph_s", "cf_eager_s", "nccl_graph_s", "nccl_sym_graph_s", "cf_plan_graph_s"):
             if key in row:
                 tk = max(x[2][i][key] for x in times)   # max over ranks
                 bw = busbw(nb, tk, world) if kind in ("allreduce", "nvls", "nvls_emulated") else \
                     (nb / tk / 1e9 * (world - 1) / world if tk > 0 else 0.0)
                 out[key[:-2]] = {"us": round(tk * 1e6, 2), "busbw": round(bw, 2)}
+                if not one_gpu:
+                    out[key[:-2]]["pct_of_900"] = round(100 * bw / 900, 2)
+        nc = [out[k]["us"] for k in ("nccl_graph", "nccl_sym_graph") if k in out]
+        if nc and "cf_graph" in out:
+            out["nccl_best_us"] = min(nc)
+            out["cf_vs_nccl_best"] = round(min(nc) / out["cf_graph"]["us"], 3) if out["cf_graph"]["us"] else None
         sweep.append(out)
     return t, te, sweep
 
 
 def run_multi_gpu(args):
-    """N GPUs, one rank per process (torchrun): the same AllReduce over NVLink."""
+    """N GPUs, one rank per process (torchrun, or self-launched by main()):
+    the AllReduce over NVLink.  CF_BENCH_ONE_GPU=1 runs the same code with
+    every rank on cuda:0 (a path check on a 1-GPU lease: time-sliced
+    contexts, labelled as such, no NVLink figure)."""
     import torch
     import torch.distributed as dist
     from paper_2504_09014_b200.comm import Communicator
@@ -644,12 +768,28 @@ def run_multi_gpu(args):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     local = int(os.environ.get("LOCAL_RANK", str(rank)))
-    if os.environ.get("CF_BENCH_ONE_GPU"):   # path check on a 1-GPU box: ranks share cuda:0
+    one_gpu = bool(os.environ.get("CF_BENCH_ONE_GPU"))
+    if one_gpu:
         local = 0
     torch.cuda.set_device(local)
     dist.init_process_group("gloo", init_method="env://")
     comm = Communicator(device=local)
     dev = torch.device("cuda", local)
+    nccl, nccl_err = nccl_setup(dev, rank, world)
+    # NVLS (switch_2pa, multimem ld_reduce / st) when the box builds a multicast object
+    nvls, nvls_kind, nvls_err = False, "nvls", None
+    try:
+        nvls = comm.setup_nvls()
+        if not nvls and one_gpu:
+            # path check on a 1-GPU box: the emulated switch runs the same
+            # kernel and bench code (rows labelled as such, not an NVLS number)
+            comm.setup_nvls_emulated(64 << 20)
+            nvls, nvls_kind = True, "nvls_emulated"
+    except Exception as e:   # report, never fail the bench
+        nvls_err = f"{type(e).__name__}: {e}"[:200]
+    parity = multi_parity(comm, dev, rank, world, nvls)
+    if nvls and parity.get("allreduce_switch_2pa") is not True:
+        nvls = False    # a failed first multimem execution drops the NVLS rows, never the line
     count = HEAD_BYTES // 2
     gen = torch.Generator(device=dev)
     gen.manual_seed(20250409 + 4000 + rank)
@@ -658,8 +798,9 @@ def run_multi_gpu(args):
     comm.register(send)
     comm.register(recv)
     stream = torch.cuda.current_stream(dev)
+    head_algo = "2pa"
     for _ in range(args.warmup):
-        comm.all_reduce(send, recv, algo="2pa")
+        comm.all_reduce(send, recv, algo=head_algo)
     torch.cuda.synchronize(dev)
     dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -668,52 +809,96 @@ def run_multi_gpu(args):
         dist.barrier()
         e0.record(stream)
         for _ in range(args.steps):
-            comm.all_reduce(send, recv, algo="2pa")
+            comm.all_reduce(send, recv, algo=head_algo)
         e1.record(stream)
         torch.cuda.synchronize(dev)
+    dist.barrier()
     comm.check_device_error()
     t_local = e0.elapsed_time(e1) / 1e3 / args.steps
     # e2e: pinned host input -> device -> all_reduce -> pinned host output, per step
     host_in = send.cpu().pin_memory()
     host_out = torch.empty_like(host_in).pin_memory()
     e2e_local = []
-    for it in range(5):
+    for it in range(4):
         torch.cuda.synchronize(dev)
         dist.barrier()
         t0 = time.perf_counter()
-        comm.all_reduce_host(host_in, host_out, algo="2pa")   # pipelined H2D / K3 / D2H
+        comm.all_reduce_host(host_in, host_out, algo=head_algo)   # pipelined H2D / K3 / D2H
         torch.cuda.synchronize(dev)
         if it:
             e2e_local.append(time.perf_counter() - t0)
-    rows_local, nccl_err = multi_sweep(comm, dev, world, send, recv)
+    rows_local = [] if args.no_sweep else multi_sweep(comm, dev, rank, world, send, recv, nvls, nvls_kind, nccl)
     t, te, sweep = gather_max_over_ranks(t_local, float(np.mean(e2e_local)), rows_local, world)
+    ok = all(v is True for v in parity.values())
     if rank == 0:
         value = busbw(HEAD_BYTES, t, world)
-        print(json.dumps({
+        where = (f"{world} ranks sharing cuda:0 (time-sliced path check; not an NVLink measurement)"
+                 if one_gpu else f"{world} ranks, one per GPU, peer loads/stores over NVLink 5 / NVSwitch")
+        line = {
             "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t * 1e3, 4),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": HEAD_DTYPE,
             "data": "synthetic",
-            "config": {"workload": f"AllReduce {HEAD_DTYPE}, {world} ranks (one per GPU, NVLink), "
-                                   f"{HEAD_BYTES // MiB} MiB per rank", "ranks": world,
-                       "algo": "2pa", "parallelism": f"{world} GPUs",
-                       "l2": "inputs larger than L2"},
-            "pct_of_900": round(100 * value / 900, 2),
-            "roofline": {"bound": "nvlink", "achieved": round(value, 1), "peak": 900.0,
-                         "unit": "GB/s", "frac": round(value / 900, 4), "traffic": None,
-                         "note": "busbw per GPU per direction vs nominal NVLink 5"},
+            "config": {"workload": f"AllReduce {HEAD_DTYPE}, {where}, {HEAD_BYTES // MiB} MiB per rank "
+                                   "(C4 shape)", "ranks": world, "algo": head_algo,
+                       "parallelism": f"{world} GPUs" if not one_gpu else f"{world} processes / 1 GPU",
+                       "l2": "inputs larger than L2 (headline); sweep rows < 64 MiB flush L2 between "
+                             "timed iterations (both arms)"},
+            "parity": parity,
             "e2e": {"value": round(busbw(HEAD_BYTES, te, world), 3), "unit": "GB/s",
                     "h2d_bytes_per_step": HEAD_BYTES, "d2h_bytes_per_step": HEAD_BYTES,
                     "ms_per_step": round(te * 1e3, 3),
                     "api": "Communicator.all_reduce_host (cfAllReduceHostStaged), pinned host tensors"},
             "gpu_launches": args.steps, "clocks": clk.summary(),
             "sweep": {"config": "bf16 AllReduce (+ C5 DSL plans, AllGather, ReduceScatter, NVLS when the "
-                                "box builds a multicast object), libcf (auto) in a CUDA graph and eager vs "
-                                "NCCL eager (torch.distributed, comparison only); latency = max over ranks",
-                      "nccl_error": nccl_err, "rows": sweep}}))
+                                "box builds a multicast object): libcf (selector's pick) in a CUDA graph and "
+                                "eager vs NCCL 2.28 in a CUDA graph on default buffers (nccl_graph) and on "
+                                "symmetric windows (nccl_sym_graph); latency = max over ranks",
+                      "nccl_version": Nccl_version(nccl), "nccl_error": nccl_err, "nvls": nvls_kind if nvls
+                      else None, "nvls_error": nvls_err, "rows": sweep}}
+        if one_gpu:
+            line["roofline"] = None
+        else:
+            line["pct_of_900"] = round(100 * value / 900, 2)
+            line["roofline"] = {"bound": "nvlink", "achieved": round(value, 1), "peak": 900.0,
+                                "unit": "GB/s", "frac": round(value / 900, 4), "traffic": None,
+                                "note": "busbw per GPU per direction vs nominal NVLink 5 (no measured "
+                                        "NVLink peak in MEASURED_PEAKS.json)"}
+        print(json.dumps(line))
+    if nccl is not None:
+        nccl.close()
     comm.close()
     dist.destroy_process_group()
-    return 0
+    return 0 if ok else 1
+
+
+def Nccl_version(nccl):
+    if nccl is None:
+        return None
+    try:
+        return nccl.version()
+    except Exception:
+        return None
+
+
+def self_launch(args):
+    """`bench.py --gpus N` without torchrun: spawn N ranks of this script on
+    127.0.0.1 (RANK / LOCAL_RANK / WORLD_SIZE / MASTER_* as torchrun sets
+    them); rank 0 prints the line.  Returns the worst exit code."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    procs = []
+    for r in range(args.gpus):
+        env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(args.gpus),
+                   LOCAL_WORLD_SIZE=str(args.gpus), MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        procs.append(subprocess.Popen([sys.executable, os.path.abspath(__file__)] + sys.argv[1:], env=env,
+                                      stdout=None if r == 0 else subprocess.DEVNULL))
+    rc = 0
+    for p in procs:
+        rc = max(rc, p.wait())
+    return rc
 
 
 def main():
@@ -726,6 +911,11 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)
+    if args.gpus > 1 and "RANK" not in os.environ:
+        return self_launch(args)
+    if os.environ.get("CF_BENCH_MULTI") and "RANK" not in os.environ:
+        os.environ.update(RANK="0", LOCAL_RANK="0", WORLD_SIZE="1", MASTER_ADDR="127.0.0.1",
+                          MASTER_PORT=str(29500 + os.getpid() % 1000))
     return run_gpu_arm(args)
 
 
