@@ -274,6 +274,26 @@ CF_API cfStatus cfPlanGetHandle(cfPlan_t plan, void* handle, size_t* bytes);
 CF_API cfStatus cfPlanConnect(cfPlan_t plan, const void* handles, size_t bytes_per_handle);
 CF_API cfStatus cfPlanDestroy(cfPlan_t plan);
 
+/* Native DSL (replaces the reference's Python builder library
+ * cf/collectives.py:30-270 and pass pipeline cf/lowering.py:295-648).
+ * Programs travel as the recorded-program JSON documented in csrc/cf_dsl.cpp
+ * (buffers, channels, instructions in emission order).  Output goes to
+ * `out` (capacity `cap`); `*out_len` receives the length, and a too-small
+ * buffer returns CF_E_BAD_SIZE with `*out_len` set so the caller can retry.
+ *   cfDslBuild: a library algorithm ("1pa", "2pa" + variant memory|ll|port,
+ *     "switch_2pa", "allpairs_ag", "ring_ag", "ring_rs", "2pr") recorded for
+ *     nranks x elems (cf/collectives.py:510-525 build_algo).
+ *   cfDslLower: replicate `instances` -> dependence analysis -> sync insertion
+ *     + redundant-sync elimination (CF_DSL_PASS_SYNC) -> fusion
+ *     (CF_DSL_PASS_FUSE) -> LL flag assignment -> canonical plan JSON, the
+ *     bytes cf/plan.py:146-162 serializes for the reference's lower(). */
+#define CF_DSL_PASS_SYNC 1
+#define CF_DSL_PASS_FUSE 2
+CF_API cfStatus cfDslBuild(const char* algo, const char* variant, int nranks, size_t elems, const char* dtype,
+                           const char* protocol, char* out, size_t cap, size_t* out_len);
+CF_API cfStatus cfDslLower(const char* program, size_t len, int instances, int passes, char* out, size_t cap,
+                           size_t* out_len);
+
 #ifdef __cplusplus
 }
 #endif

@@ -39,6 +39,7 @@ EXPORTS = (
     "cfAllGather", "cfReduceScatter", "cfAllReduceHost", "cfAllReduceHostStaged",
     "cfAllReduceAddRMSNorm", "cfSelectAlgorithm", "cfPlanLoad", "cfPlanExecute",
     "cfPlanInfo", "cfPlanLastDeviceError", "cfPlanClearDeviceError", "cfPlanGetHandle", "cfPlanConnect", "cfPlanDestroy",
+    "cfDslBuild", "cfDslLower",
 )
 
 
@@ -91,6 +92,8 @@ _PROTOS = {
     "cfPlanExecute": ([vp, P(vp), P(vp), P(vp)], i32),
     "cfPlanLastDeviceError": ([vp, P(i32)], i32),
     "cfPlanClearDeviceError": ([vp], i32),
+    "cfDslBuild": ([ctypes.c_char_p, ctypes.c_char_p, i32, sz, ctypes.c_char_p, ctypes.c_char_p, vp, sz, P(sz)], i32),
+    "cfDslLower": ([ctypes.c_char_p, sz, i32, i32, vp, sz, P(sz)], i32),
     "cfPlanInfo": ([vp, P(sz), P(sz), P(i32), P(i32), P(i32)], i32),
     "cfPlanGetHandle": ([vp, vp, P(sz)], i32),
     "cfPlanConnect": ([vp, vp, sz], i32),

@@ -43,6 +43,11 @@ class NcclError(RuntimeError):
     pass
 
 
+class UniqueId(ctypes.Structure):
+    """ncclUniqueId (nccl.h:38-39): a 128-byte struct passed BY VALUE."""
+    _fields_ = [("internal", ctypes.c_char * 128)]
+
+
 class Nccl:
     """One NCCL communicator (one rank per process)."""
 
@@ -54,7 +59,7 @@ class Nccl:
             L = _load()
             vp, sz, i32 = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int
             L.ncclGetUniqueId.argtypes = [ctypes.c_char_p]
-            L.ncclCommInitRank.argtypes = [ctypes.POINTER(vp), i32, ctypes.c_char * 128, i32]
+            L.ncclCommInitRank.argtypes = [ctypes.POINTER(vp), i32, UniqueId, i32]
             L.ncclCommDestroy.argtypes = [vp]
             L.ncclMemAlloc.argtypes = [ctypes.POINTER(vp), sz]
             L.ncclMemFree.argtypes = [vp]
@@ -87,8 +92,8 @@ class Nccl:
 
     def __init__(self, nranks: int, rank: int, uid: bytes):
         self.comm = ctypes.c_void_p()
-        arr = (ctypes.c_char * 128).from_buffer_copy(uid)
-        self._check(self.lib().ncclCommInitRank(ctypes.byref(self.comm), nranks, arr, rank))
+        u = UniqueId.from_buffer_copy(uid)
+        self._check(self.lib().ncclCommInitRank(ctypes.byref(self.comm), nranks, u, rank))
         self.nranks, self.rank = nranks, rank
         self._wins = []
         self._mem = []

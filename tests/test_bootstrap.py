@@ -78,7 +78,8 @@ def _max_worker(rank, world, port, q):
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     from bench import gather_max_over_ranks
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
-    rows = [{"bytes": 1 << 20, "cf_graph_s": 1e-5 * (rank + 1), "nccl_eager_s": 3e-5 / (rank + 1)},
+    rows = [{"bytes": 1 << 20, "cf_graph_s": 1e-5 * (rank + 1), "nccl_graph_s": 3e-5 / (rank + 1),
+             "nccl_sym_graph_s": 2.5e-5 + 1e-6 * rank},
             {"bytes": 1 << 20, "kind": "allgather", "cf_graph_s": 2e-5 * (world - rank)},
             {"bytes": 16384, "plan": "2pa_memory", "batch": 1, "cf_plan_graph_s": 5e-6 + 1e-6 * rank}]
     q.put((rank, gather_max_over_ranks(1.0 + rank, 10.0 - rank, rows, world)))
@@ -102,7 +103,10 @@ def test_bench_times_are_max_over_ranks():
     assert res[0] == res[1]
     t, te, sweep = res[0]
     assert (t, te) == (2.0, 10.0)
-    assert sweep[0]["cf_graph"]["us"] == 20.0 and sweep[0]["nccl_eager"]["us"] == 30.0
+    assert sweep[0]["cf_graph"]["us"] == 20.0 and sweep[0]["nccl_graph"]["us"] == 30.0
+    # the better NCCL buffer mode is the bar (max over ranks first)
+    assert sweep[0]["nccl_sym_graph"]["us"] == 26.0 and sweep[0]["nccl_best_us"] == 26.0
+    assert sweep[0]["cf_vs_nccl_best"] == 1.3
     # AllReduce: 2 (n-1)/n; AllGather: (n-1)/n
     assert sweep[0]["cf_graph"]["busbw"] == round((1 << 20) / 2e-5 * 1.0 / 1e9, 2)
     assert sweep[1]["kind"] == "allgather" and sweep[1]["cf_graph"]["us"] == 40.0
