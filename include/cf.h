@@ -158,6 +158,34 @@ CF_API cfStatus cfNvlsBind(cfComm_t comm);
  * (cf/channels.py:333-409) in emulation only. */
 CF_API cfStatus cfNvlsEmulate(cfComm_t comm, void* staging, size_t bytes);
 
+/* Symmetric heap and allocator (SURVEY §8(b) cfMemAlloc; the reference's
+ * per-rank regions, cf/world.py:113-138, and SwitchChannel, cf/channels.py:
+ * 333-409).  One cuMem allocation per rank, mapped into every rank; mode 1
+ * binds the heaps to an NVLS multicast object, mode 2 emulates the switch
+ * with unicast loads / stores (boxes without multicast), mode 0 is a plain
+ * symmetric heap.  Buffers from cfMemAlloc sit at the same offset of every
+ * rank's heap, so collectives on them need no registration and switch_2pa
+ * runs IN PLACE on them (multimem.ld_reduce from send, multimem.st into recv:
+ * no staging copies); AUTO picks it for symmetric buffers >= 1 MiB per rank
+ * when the heap is multicast-bound.
+ *   cfCommInitAll communicators: cfSymHeapCreate does everything (fd unused).
+ *   cfCommCreateRank communicators, phases separated by bootstrap barriers:
+ *     cfSymHeapCreate -> *fd of this rank's heap; send it to every peer
+ *     (Unix socket SCM_RIGHTS); cfSymHeapMapPeer for every peer; mode 1 then
+ *     cfSymHeapMulticast phase 0 (rank 0: *fd out), 1 (others: *fd in), 2 (all).
+ * cfMemAlloc is collective (same sizes, same order on every rank); ptrs gets
+ * one pointer per local rank.  cfMemFree takes any local rank's pointer. */
+CF_API cfStatus cfSymHeapCreate(cfComm_t comm, size_t bytes, int mode, int* fd);
+CF_API cfStatus cfSymHeapMapPeer(cfComm_t comm, int peer, int fd);
+CF_API cfStatus cfSymHeapMulticast(cfComm_t comm, int phase, int* fd);
+CF_API cfStatus cfSymHeapInfo(cfComm_t comm, int local_rank, void** bases, size_t* bytes, int* mode);
+CF_API cfStatus cfMemAlloc(cfComm_t comm, size_t bytes, void** ptrs);
+CF_API cfStatus cfMemFree(cfComm_t comm, const void* ptr);
+/* SwitchChannel handle for local rank `local_rank`'s kernels: a
+ * cf::SwitchChannelDevice (csrc/device/cf_device.cuh) with reduce /
+ * broadcast / reduce_broadcast over heap offsets. */
+CF_API cfStatus cfSwitchChannelCreate(cfComm_t comm, int local_rank, void* handle, size_t* handle_bytes);
+
 /* Channels for user kernels (the Primitive API; reference
  * MemoryChannel / PortChannel, cf/channels.py:54-330).  Fills `handle` with a
  * device struct (cf::MemoryChannelDevice / cf::PortChannelDevice from

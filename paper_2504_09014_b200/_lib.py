@@ -39,7 +39,8 @@ EXPORTS = (
     "cfAllGather", "cfReduceScatter", "cfAllReduceHost", "cfAllReduceHostStaged",
     "cfAllReduceAddRMSNorm", "cfSelectAlgorithm", "cfPlanLoad", "cfPlanExecute",
     "cfPlanInfo", "cfPlanLastDeviceError", "cfPlanClearDeviceError", "cfPlanGetHandle", "cfPlanConnect", "cfPlanDestroy",
-    "cfDslBuild", "cfDslLower",
+    "cfDslBuild", "cfDslLower", "cfSymHeapCreate", "cfSymHeapMapPeer", "cfSymHeapMulticast",
+    "cfSymHeapInfo", "cfMemAlloc", "cfMemFree", "cfSwitchChannelCreate",
 )
 
 
@@ -92,6 +93,13 @@ _PROTOS = {
     "cfPlanExecute": ([vp, P(vp), P(vp), P(vp)], i32),
     "cfPlanLastDeviceError": ([vp, P(i32)], i32),
     "cfPlanClearDeviceError": ([vp], i32),
+    "cfSymHeapCreate": ([vp, sz, i32, P(i32)], i32),
+    "cfSymHeapMapPeer": ([vp, i32, i32], i32),
+    "cfSymHeapMulticast": ([vp, i32, P(i32)], i32),
+    "cfSymHeapInfo": ([vp, i32, P(vp), P(sz), P(i32)], i32),
+    "cfMemAlloc": ([vp, sz, P(vp)], i32),
+    "cfMemFree": ([vp, vp], i32),
+    "cfSwitchChannelCreate": ([vp, i32, vp, P(sz)], i32),
     "cfDslBuild": ([ctypes.c_char_p, ctypes.c_char_p, i32, sz, ctypes.c_char_p, ctypes.c_char_p, vp, sz, P(sz)], i32),
     "cfDslLower": ([ctypes.c_char_p, sz, i32, i32, vp, sz, P(sz)], i32),
     "cfPlanInfo": ([vp, P(sz), P(sz), P(i32), P(i32), P(i32)], i32),
@@ -127,3 +135,20 @@ def check(status: int) -> None:
 def ptr_array(values):
     arr = (vp * len(values))(*[int(v) if v is not None else None for v in values])
     return arr
+
+
+class _DevMem:
+    """__cuda_array_interface__ view of raw device bytes (no ownership)."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (int(ptr), False),
+                                         "version": 3, "strides": None}
+
+
+def tensor_at(ptr: int, numel: int, dtype, device):
+    """A torch tensor over libcf-owned device memory (e.g. a cfMemAlloc
+    buffer).  The memory stays libcf's: free it through libcf, not torch."""
+    import torch
+    es = torch.empty(0, dtype=dtype).element_size()
+    raw = torch.as_tensor(_DevMem(ptr, numel * es), device=device)
+    return raw.view(dtype)

@@ -31,24 +31,25 @@ def all_gather_bytes(blob: bytes, group=None) -> list:
     return [bytes(o.cpu().numpy().tobytes()) for o in out]
 
 
-def share_fd(fd, rank: int, nranks: int, group=None) -> int:
-    """Collective: rank 0 passes its file descriptor `fd` to every other rank
-    of the group (same host) over a Unix-domain socket with SCM_RIGHTS; the
-    socket path travels through the bootstrap group.  Returns the fd valid in
-    this process (rank 0: its own; others: a new descriptor to close)."""
+def share_fd(fd, rank: int, nranks: int, group=None, src: int = 0) -> int:
+    """Collective: rank `src` passes its file descriptor `fd` to every other
+    rank of the group (same host) over a Unix-domain socket with SCM_RIGHTS;
+    the socket path travels through the bootstrap group.  Returns the fd valid
+    in this process (`src`: its own; others: a new descriptor to close)."""
     import os
     import socket
     import tempfile
     import torch.distributed as dist
     path, srv = None, None
-    if rank == 0:
+    if rank == src:
         path = os.path.join(tempfile.mkdtemp(prefix="cf_fd_"), "sock")
         srv = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
         srv.bind(path)
         srv.listen(max(1, nranks))
     box = [path]
-    dist.broadcast_object_list(box, src=0, group=group)
-    if rank == 0:
+    dist.broadcast_object_list(box, src=dist.get_global_rank(group, src) if group is not None else src,
+                              group=group)
+    if rank == src:
         for _ in range(nranks - 1):
             conn, _ = srv.accept()
             socket.send_fds(conn, [b"f"], [fd])
@@ -250,6 +251,68 @@ class Communicator:
         self.register(staging)
         _lib.check(_lib.lib().cfNvlsEmulate(self._comm, staging.data_ptr(), staging_bytes))
         self._nvls_staging = staging
+
+    def setup_symmetric(self, nbytes: int, mode: str = "auto") -> int:
+        """Collective: this rank's symmetric heap (include/cf.h cfSymHeapCreate),
+        its POSIX fd sent to every peer (SCM_RIGHTS over Unix sockets) and the
+        peers' heaps mapped here; with multicast, the heaps are bound to one
+        NVLS object (rank 0 creates it).  mode: "auto" (multicast when every
+        GPU supports it and the object builds, else plain), "emulate" (the
+        switch as unicast loads / stores: boxes without multicast), "none".
+        Returns the mode in use (1 multicast, 2 emulated, 0 plain); every
+        rank agrees on it."""
+        import os
+        import torch.distributed as dist
+        L = _lib.lib()
+
+        def agree(ok: bool) -> bool:
+            flags = [None] * self.nranks
+            dist.all_gather_object(flags, bool(ok), group=self.group)
+            return all(flags)
+
+        want = {"emulate": 2, "none": 0}.get(mode, 1)
+        if want == 1 and not agree(self._multicast_capable()):
+            want = 0
+        fd = ctypes.c_int(-1)
+        _lib.check(L.cfSymHeapCreate(self._comm, int(nbytes), want, ctypes.byref(fd)))
+        for src in range(self.nranks):
+            got = share_fd(fd.value if src == self.rank else None, self.rank, self.nranks, self.group, src=src)
+            if src != self.rank:
+                _lib.check(L.cfSymHeapMapPeer(self._comm, src, got))
+                os.close(got)
+        os.close(fd.value)
+        self._sym_mode = want
+        if want == 1:
+            mfd = ctypes.c_int(-1)
+            ok = agree(L.cfSymHeapMulticast(self._comm, 0, ctypes.byref(mfd)) == 0) if self.rank == 0 else \
+                agree(True)
+            if ok:
+                got = share_fd(mfd.value if self.rank == 0 else None, self.rank, self.nranks, self.group)
+                if self.rank != 0:
+                    g = ctypes.c_int(got)
+                    ok = L.cfSymHeapMulticast(self._comm, 1, ctypes.byref(g)) == 0
+                    os.close(got)
+                ok = agree(ok)          # every device added before any bind
+            if ok:
+                ok = agree(L.cfSymHeapMulticast(self._comm, 2, ctypes.byref(mfd)) == 0)
+            if self.rank == 0 and mfd.value >= 0:
+                os.close(mfd.value)
+            if not ok:
+                self._sym_mode = 0      # heap stays usable (HB algorithms), switch_2pa falls back
+        return self._sym_mode
+
+    def alloc_symmetric(self, numel: int, dtype):
+        """Collective: a tensor at the same offset of every rank's symmetric
+        heap (cfMemAlloc) -- collectives on it need no registration, and
+        switch_2pa runs in place on it."""
+        import torch
+        es = torch.empty(0, dtype=dtype).element_size()
+        ptr = (ctypes.c_void_p * 1)()
+        _lib.check(_lib.lib().cfMemAlloc(self._comm, int(numel) * es, ptr))
+        return _lib.tensor_at(ptr[0], numel, dtype, self.device)
+
+    def free_symmetric(self, tensor) -> None:
+        _lib.check(_lib.lib().cfMemFree(self._comm, tensor.data_ptr()))
 
     def _multicast_capable(self) -> bool:
         from .world import device_multicast_capable

@@ -542,46 +542,8 @@ __global__ void __launch_bounds__(512) push_gather_kernel(const __grid_constant_
 
 // ---------------------------------------------------------------- K5
 
-// NVLS switch primitives: multimem.ld_reduce sums the same address over every
-// member of the multicast object inside the NVSwitch (f16/bf16 accumulating in
-// f32), multimem.st broadcasts a store to every member.
-template <typename T>
-__device__ __forceinline__ uint4 multimem_ld_reduce(const void* p);
-template <>
-__device__ __forceinline__ uint4 multimem_ld_reduce<float>(const void* p) {
-  uint4 v;
-  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p) : "memory");
-  return v;
-}
-template <>
-__device__ __forceinline__ uint4 multimem_ld_reduce<__nv_bfloat16>(const void* p) {
-  uint4 v;
-  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.bf16x2 {%0,%1,%2,%3}, [%4];"
-               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p) : "memory");
-  return v;
-}
-template <>
-__device__ __forceinline__ uint4 multimem_ld_reduce<__half>(const void* p) {
-  uint4 v;
-  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.f16x2 {%0,%1,%2,%3}, [%4];"
-               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p) : "memory");
-  return v;
-}
-template <>
-__device__ __forceinline__ uint4 multimem_ld_reduce<int32_t>(const void* p) {
-  uint4 v;
-  const char* c = (const char*)p;
-  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.u32 %0, [%1];" : "=r"(v.x) : "l"(c) : "memory");
-  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.u32 %0, [%1];" : "=r"(v.y) : "l"(c + 4) : "memory");
-  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.u32 %0, [%1];" : "=r"(v.z) : "l"(c + 8) : "memory");
-  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.u32 %0, [%1];" : "=r"(v.w) : "l"(c + 12) : "memory");
-  return v;
-}
-__device__ __forceinline__ void multimem_st16(void* p, uint4 v) {
-  asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y),
-               "r"(v.z), "r"(v.w) : "memory");
-}
+// NVLS switch primitives (multimem_ld_reduce / multimem_st16) live in
+// device/cf_device.cuh with the SwitchChannelDevice they back.
 
 // K5 NVLS AllReduce (build_switch_2pa, cf/collectives.py:235-250; switch_reduce /
 // switch_broadcast, cf/channels.py:367-409), one launch per call.  The message
@@ -650,6 +612,53 @@ __global__ void __launch_bounds__(512) nvls_kernel(const __grid_constant__ CollA
         if (v < pv) store_vec<T>(rk.out[r], p0 + v, ld16_cg(my_out + v * 16), 0, a.count, 0);
       }
   }
+  end_call(rk, e);
+}
+
+// K5 direct: NVLS AllReduce in place on SYMMETRIC buffers (cfMemAlloc), the
+// copy-free form of build_switch_2pa (cf/collectives.py:235-250): rank r's
+// CTAs multimem.ld_reduce chunk r of the send buffer across every member and
+// multimem.st the sums into every member's recv buffer -- S of NVLink traffic
+// per rank per direction and no staging copies.  `emul` (boxes without
+// multicast) runs the same schedule with per-member unicast loads / stores in
+// the reference switch order (0 + x_0 + x_1 + ...).  A ragged last vector
+// (count * sizeof(T) not a multiple of 16) is reduced through the unicast
+// mappings by one thread of the last rank.  Entry handshake: every member's
+// send buffer is produced; exit handshake: every member stored its chunk
+// into this rank's recv buffer.  A single co-resident launch (emulated) needs
+// neither.
+template <typename T>
+__global__ void __launch_bounds__(512) nvls_direct_kernel(const __grid_constant__ CollArgs a) {
+  const RankCtx& rk = a.rk[blockIdx.y];
+  constexpr int V = 16 / sizeof(T);
+  const int n = a.n, r = rk.rank;
+  const uint64_t e = begin_call_lazy(rk, a.single_launch);
+  if (!a.single_launch) handshake(rk, n, e * kPhases + 1, false, a.gpu_scope);
+  const size_t full = a.count / V;
+  const size_t cv = (full + n - 1) / n;
+  const size_t v0 = min((size_t)r * cv, full), v1 = min(v0 + cv, full);
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  if (!a.emul) {
+    for (size_t v = v0 + (size_t)blockIdx.x * blockDim.x + threadIdx.x; v < v1; v += stride)
+      multimem_st16(rk.mc_out + v * 16, multimem_ld_reduce<T>(rk.mc_in + v * 16));
+  } else {
+    for (size_t v = v0 + (size_t)blockIdx.x * blockDim.x + threadIdx.x; v < v1; v += stride) {
+      const uint4 s = switch_sum_unicast<T>((char* const*)rk.in, n, v * 16);
+#pragma unroll
+      for (int q = 0; q < CF_MAX_RANKS; q++)
+        if (q < n) st16(rk.out[q] + v * 16, s);
+    }
+  }
+  if (full * V < a.count && r == n - 1 && blockIdx.x == 0 && threadIdx.x == 0) {
+    const int nb = (int)((a.count - full * V) * sizeof(T));
+    uint4 x[CF_MAX_RANKS];
+#pragma unroll
+    for (int q = 0; q < CF_MAX_RANKS; q++)
+      if (q < n) x[q] = ld_partial16_ool<sizeof(T)>(rk.in[q] + full * 16, nb);
+    const uint4 s = reduce_vecs<T, CF_MAX_RANKS>(x, n, true);
+    for (int q = 0; q < n; q++) st_masked16_ool<sizeof(T)>(rk.out[q] + full * 16, s, 0, nb / (int)sizeof(T));
+  }
+  if (!a.single_launch) handshake(rk, n, e * kPhases + 2, true, a.gpu_scope);
   end_call(rk, e);
 }
 
@@ -1190,7 +1199,7 @@ static const void* by_dtype(int dtype, int n) {
 
 // Kernel entry point for (kind, dtype, n).  kind: 0 pull-reduce, 1 LL one-shot,
 // 2 LL two-shot, 3 push-gather, 4 NVLS multimem, 5 ring RS(+AG), 6 ring AG,
-// 7 AllReduce + residual + RMSNorm.
+// 7 AllReduce + residual + RMSNorm, 8 NVLS in place on symmetric buffers.
 const void* collective_kernel(int kind, int dtype, int n) {
   switch (kind) {
     case 0: return by_dtype<pick_pull<float>, pick_pull<int32_t>, pick_pull<__half>,
@@ -1228,6 +1237,14 @@ const void* collective_kernel(int kind, int dtype, int n) {
         case 1: return pick_norm<float>(n);
         case 2: return pick_norm<__half>(n);
         case 3: return pick_norm<__nv_bfloat16>(n);
+      }
+      break;
+    case 8:   // K5 direct (symmetric buffers)
+      switch (dtype) {
+        case 0: return (const void*)nvls_direct_kernel<int32_t>;
+        case 1: return (const void*)nvls_direct_kernel<float>;
+        case 2: return (const void*)nvls_direct_kernel<__half>;
+        case 3: return (const void*)nvls_direct_kernel<__nv_bfloat16>;
       }
       break;
     case 6:

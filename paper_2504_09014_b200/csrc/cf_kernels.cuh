@@ -21,6 +21,8 @@ struct RankCtx {
   char* nv[CF_MAX_RANKS];         // K5: NVLS staging [input half | output half], unicast: own rank's
                                   // (emulated switch: every rank's)
   char* nv_mc;                    // K5: own staging's multicast mapping (null when emulated)
+  const char* mc_in;              // K5 direct: multicast mapping of the (symmetric) send buffer
+  char* mc_out;                   // K5 direct: multicast mapping of the (symmetric) recv buffer
   const char* resid;              // K13: this rank's residual input
   const char* weight;             // K13: this rank's RMSNorm weight [hidden]
   RankState* st;                  // this rank's state

@@ -99,13 +99,6 @@ void* driver_fn(const char* name) {
   return fn;
 }
 
-// Restores the caller's current device on scope exit.
-struct DeviceGuard {
-  int prev = -1;
-  DeviceGuard() { cudaGetDevice(&prev); }
-  ~DeviceGuard() { if (prev >= 0) cudaSetDevice(prev); }
-};
-
 static cfStatus alloc_heap(cfComm* c, LocalRank& lr) {
   CF_CUDA(cudaSetDevice(lr.dev));
   CF_CUDA(cudaMalloc((void**)&lr.heap, c->lay.total));
@@ -157,6 +150,10 @@ static void build_groups(cfComm* c) {
 // Measured crossover table: replaces DEFAULT_THRESHOLDS
 // (cf/collectives.py:418).  Thresholds are per-rank message bytes.  Values
 // come from bench.py sweeps; see DESIGN.md "selector".
+// AUTO picks the in-place NVLS kernel for symmetric buffers from this size up
+// (per rank; provisional until measured on a multicast-capable box)
+constexpr size_t kNvlsAutoBytes = (size_t)1 << 20;
+
 static int select_algo(const cfComm* c, int coll, size_t nbytes, int dtype) {
   (void)dtype;
   const bool coresident = c->groups.size() == 1 && c->local.size() > 1;
@@ -376,6 +373,7 @@ extern "C" cfStatus cfCommDestroy(cfComm_t c) {
   for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
   proxy_stop(c);
   nvls_teardown(c);
+  sym_teardown(c);
   for (size_t gi = 0; gi < c->pipes.size(); gi++) {
     auto& hp = c->pipes[gi];
     cudaSetDevice(c->local[c->groups[gi][0]].dev);
@@ -576,6 +574,32 @@ struct NormBufs {
   const void* const* weight;
 };
 
+// every rank's symmetric heap is mapped here (multi-process: after cfSymHeapMapPeer)
+bool sym_mapped(const cfComm* c) {
+  if (!c->sym.on()) return false;
+  for (size_t li = 0; li < c->local.size(); li++)
+    for (int p = 0; p < c->nranks; p++)
+      if (!c->sym.peer[li][p]) return false;
+  return true;
+}
+
+// send / recv of every local rank are symmetric (same heap offsets on every
+// local rank, `bytes` inside the heap) and the switch is usable (multicast
+// bound, or emulated): the in-place NVLS kernel applies
+bool sym_switch_ok(const cfComm* c, const void* const* send, void* const* recv, size_t bytes, long long* oi,
+                   long long* oo) {
+  if (c->sym.mode == 0 || !sym_mapped(c)) return false;
+  *oi = c->sym.offset(0, send[0]);
+  *oo = c->sym.offset(0, recv[0]);
+  if (*oi < 0 || *oo < 0 || (size_t)*oi + bytes > c->sym.bytes || (size_t)*oo + bytes > c->sym.bytes) return false;
+  if ((*oi & 15) || (*oo & 15)) return false;
+  for (size_t li = 0; li < c->local.size(); li++) {
+    if (c->sym.offset((int)li, send[li]) != *oi || c->sym.offset((int)li, recv[li]) != *oo) return false;
+    if (c->sym.mode == 1 && !c->sym.ranks[li].mc) return false;
+  }
+  return true;
+}
+
 cfStatus check_ptrs(cfComm* c, const void* const* send, void* const* recv, const cudaStream_t* streams) {
   if (!c) return fail(CF_E_CONFIG, "null communicator");
   if (!c->connected) return fail(CF_E_CONFIG, "communicator not connected (call cfCommConnect)");
@@ -598,16 +622,19 @@ cfStatus launch(cfComm* c, const Job& j, int dtype, const void* const* send, voi
   const Registration* reg_in = nullptr;
   const Registration* reg_out = nullptr;
   const Registration* reg_out2 = nullptr;
+  // symmetric-heap buffers (cfMemAlloc) need no registration: peers at base[p] + offset
+  const long long sym_in = c->multiprocess && sym_mapped(c) ? c->sym.offset(0, send[0]) : -1;
+  const long long sym_out = c->multiprocess && sym_mapped(c) ? c->sym.offset(0, recv[0]) : -1;
   if (c->multiprocess) {
     if (need_out2 && !(reg_out2 = c->find_reg(nb->resid_out[0])))
       return fail(CF_E_TOPOLOGY, "residual-out buffer %p is not registered (cfBufferExport/cfBufferImport); "
                                  "the two-shot fused kernel writes it from the peers", nb->resid_out[0]);
-    if (need_in && !(reg_in = c->find_reg(send[0])))
-      return fail(CF_E_TOPOLOGY, "send buffer %p is not registered (cfBufferExport/cfBufferImport); "
-                                 "HB algorithms read it from the peers", send[0]);
-    if (need_out && !(reg_out = c->find_reg(recv[0])))
-      return fail(CF_E_TOPOLOGY, "recv buffer %p is not registered (cfBufferExport/cfBufferImport); "
-                                 "HB algorithms write it from the peers", recv[0]);
+    if (need_in && sym_in < 0 && !(reg_in = c->find_reg(send[0])))
+      return fail(CF_E_TOPOLOGY, "send buffer %p is neither registered (cfBufferExport/cfBufferImport) nor "
+                                 "symmetric (cfMemAlloc); HB algorithms read it from the peers", send[0]);
+    if (need_out && sym_out < 0 && !(reg_out = c->find_reg(recv[0])))
+      return fail(CF_E_TOPOLOGY, "recv buffer %p is neither registered (cfBufferExport/cfBufferImport) nor "
+                                 "symmetric (cfMemAlloc); HB algorithms write it from the peers", recv[0]);
   }
   DeviceGuard guard;
   const void* kernel = collective_kernel(j.kind, dtype, c->nranks);
@@ -666,6 +693,8 @@ cfStatus launch(cfComm* c, const Job& j, int dtype, const void* const* send, voi
         for (int p = 0; p < c->nranks; p++) {
           if (reg_in) rk.in[p] = reg_in->peer[p] + ((const char*)send[li] - reg_in->ptr);
           if (reg_out) rk.out[p] = reg_out->peer[p] + ((char*)recv[li] - reg_out->ptr);
+          if (need_in && sym_in >= 0) rk.in[p] = c->sym.peer[0][p] + sym_in;
+          if (need_out && sym_out >= 0) rk.out[p] = c->sym.peer[0][p] + sym_out;
           if (reg_out2) rk.out2[p] = reg_out2->peer[p] + ((char*)nb->resid_out[li] - reg_out2->ptr);
         }
         rk.in[rk.rank] = (const char*)send[li];
@@ -738,6 +767,50 @@ cfStatus nvls_allreduce(cfComm* c, const void* const* send, void* const* recv, s
   return CF_OK;
 }
 
+// K5 direct: the in-place NVLS kernel on symmetric buffers (heap offsets
+// oi / oo on every rank), one launch per device group.
+cfStatus nvls_direct(cfComm* c, size_t count, int dtype, long long oi, long long oo, const cudaStream_t* streams) {
+  DeviceGuard guard;
+  const size_t es = dtype_size(dtype);
+  const void* kernel = collective_kernel(8, dtype, c->nranks);
+  const int threads = c->cfg.threads;
+  const size_t work = ceil_div(ceil_div(count * es, (size_t)16), (size_t)c->nranks);
+  for (size_t gi = 0; gi < c->groups.size(); gi++) {
+    const auto& g = c->groups[gi];
+    CF_CUDA(cudaSetDevice(c->local[g[0]].dev));
+    CollArgs a;
+    memset(&a, 0, sizeof(a));
+    a.n = c->nranks;
+    a.nlocal = (int)g.size();
+    a.count = count;
+    a.emul = c->sym.mode == 2 ? 1 : 0;
+    a.gpu_scope = (c->groups.size() == 1 && !c->multiprocess) ? 1 : 0;
+    a.single_launch = (c->groups.size() == 1 && !c->multiprocess && (int)g.size() == c->nranks) ? 1 : 0;
+    for (size_t k = 0; k < g.size(); k++) {
+      const int li = g[k];
+      RankCtx& rk = a.rk[k];
+      rk.rank = c->local[li].rank;
+      rk.st = c->state(li);
+      for (int p = 0; p < c->nranks; p++) {
+        rk.sem[p] = c->sem(li, p);
+        rk.in[p] = c->sym.peer[li][p] + oi;
+        rk.out[p] = c->sym.peer[li][p] + oo;
+      }
+      if (c->sym.mode == 1) {
+        rk.mc_in = c->sym.ranks[li].mc + oi;
+        rk.mc_out = c->sym.ranks[li].mc + oo;
+      }
+    }
+    const int mb = max_blocks_per_rank(c, kernel, (int)gi, threads);
+    const int blocks = (int)std::min<size_t>((size_t)mb, std::max<size_t>(1, ceil_div(work, (size_t)threads)));
+    CF_TRY(join_streams(c, (int)gi, streams, false));
+    void* args[] = {&a};
+    CF_CUDA(cudaLaunchKernel(kernel, dim3(blocks, g.size()), dim3(threads), args, 0, streams[g[0]]));
+    CF_TRY(join_streams(c, (int)gi, streams, true));
+  }
+  return CF_OK;
+}
+
 }  // namespace
 
 extern "C" cfStatus cfAllReduce(cfComm_t c, const void* const* send, void* const* recv, size_t count,
@@ -748,12 +821,19 @@ extern "C" cfStatus cfAllReduce(cfComm_t c, const void* const* send, void* const
   const int n = c->nranks;
   const size_t es = dtype_size(dtype), V = 16 / es;
   const size_t bytes = count * es;
+  long long oi = -1, oo = -1;
+  const bool sym_switch = sym_switch_ok(c, send, recv, bytes, &oi, &oo);
   if (algo == CF_ALGO_AUTO) {
     algo = select_algo(c, 0, bytes, dtype);
     if (algo == CF_ALGO_1PA_HB)
       for (size_t li = 0; li < c->local.size(); li++)
         if (send[li] == recv[li]) algo = CF_ALGO_2PA;   // 1pa_hb cannot run in place
+    // symmetric buffers on a real multicast heap: the in-place NVLS kernel
+    // moves S per rank per direction on NVLink instead of 2(n-1)/n S
+    // (provisional crossover until an NVLink sweep measures it)
+    if (sym_switch && c->sym.mode == 1 && bytes >= kNvlsAutoBytes) algo = CF_ALGO_SWITCH_2PA;
   }
+  if (algo == CF_ALGO_SWITCH_2PA && sym_switch) return nvls_direct(c, count, dtype, oi, oo, streams);
   if (algo == CF_ALGO_SWITCH_2PA && c->nvls.enabled) return nvls_allreduce(c, send, recv, count, dtype, streams);
   Job j;
   j.count = count;

@@ -30,6 +30,13 @@ cfStatus fail(cfStatus s, const char* fmt, ...);
     if (s_ != CF_OK) return s_;          \
   } while (0)
 
+// Restores the caller's current device on scope exit.
+struct DeviceGuard {
+  int prev = -1;
+  DeviceGuard() { cudaGetDevice(&prev); }
+  ~DeviceGuard() { if (prev >= 0) cudaSetDevice(prev); }
+};
+
 inline size_t round_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 inline size_t ceil_div(size_t x, size_t a) { return (x + a - 1) / a; }
 inline int dtype_size(int dt) { return dt <= 1 ? 4 : 2; }
@@ -102,6 +109,36 @@ struct Nvls {
   std::vector<NvlsRank> ranks;  // per local rank
 };
 
+// Symmetric heap (cfSymHeapCreate / cfMemAlloc): per rank one cuMem
+// allocation of `bytes`, mapped unicast on every local device and -- one
+// process per GPU -- imported into every peer by POSIX fd; with a multicast
+// object the heap is also bound and mapped multicast.  cfMemAlloc carves
+// the same offset out of every rank's heap, so a buffer's peers are
+// base[p] + offset: no per-buffer registration.
+struct SymRank {
+  unsigned long long mem = 0;   // CUmemGenericAllocationHandle (own allocation)
+  char* uc = nullptr;           // own heap, unicast
+  char* mc = nullptr;           // own heap, multicast mapping (mode 1)
+};
+
+struct SymHeap {
+  int mode = 0;                 // 0 none, 1 multicast (NVLS), 2 emulated switch (unicast)
+  size_t bytes = 0, gran = 0;
+  unsigned long long mc = 0;    // multicast object (mode 1)
+  bool mc_added = false;
+  std::vector<SymRank> ranks;   // per local rank
+  std::vector<std::array<char*, CF_MAX_RANKS>> peer;   // [li][p]: rank p's heap as seen from li
+  std::vector<std::pair<unsigned long long, char*>> imported;   // (handle, va) of mapped peers
+  std::map<size_t, size_t> used;  // allocations: offset -> bytes
+  bool on() const { return bytes != 0; }
+  // offset of p inside local rank li's heap, or -1
+  long long offset(int li, const void* p) const {
+    if (!bytes || li >= (int)ranks.size() || !ranks[li].uc) return -1;
+    const char* q = (const char*)p;
+    return (q >= ranks[li].uc && q < ranks[li].uc + bytes) ? (long long)(q - ranks[li].uc) : -1;
+  }
+};
+
 }  // namespace cf
 
 struct cfComm {
@@ -122,6 +159,7 @@ struct cfComm {
   std::map<std::pair<const void*, int>, int> occ;  // (kernel, device) -> CTAs/SM
   bool multicast_supported = false;
   cf::Nvls nvls;
+  cf::SymHeap sym;
   cf::Proxy* proxy = nullptr;          // PortChannel proxy thread (started on demand)
   std::vector<cf::HostPipe> pipes;     // per group (cfAllReduceHost), created on first use
 
@@ -153,6 +191,7 @@ bool multicast_capable(int dev);
 cfStatus nvls_setup_inprocess(cfComm* c);
 cfStatus nvls_setup_emulated(cfComm* c);
 void nvls_teardown(cfComm* c);
+void sym_teardown(cfComm* c);
 // PortChannel proxy (cf_proxy.cu)
 cfStatus proxy_start(cfComm* c);
 void proxy_stop(cfComm* c);

@@ -471,4 +471,117 @@ struct MemoryChannelDevice {
   }
 };
 
+
+// ---------------------------------------------------------------- NVLS switch
+//
+// multimem.ld_reduce sums the same address over every member of a multicast
+// object inside the NVSwitch (f16/bf16 accumulate in f32); multimem.st
+// broadcasts one store to every member.  Both need a multicast mapping
+// (cuMulticastCreate + cuMulticastBindMem + cuMemMap of the multicast handle).
+template <typename T>
+__device__ __forceinline__ uint4 multimem_ld_reduce(const void* p);
+template <>
+__device__ __forceinline__ uint4 multimem_ld_reduce<float>(const void* p) {
+  uint4 v;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p) : "memory");
+  return v;
+}
+template <>
+__device__ __forceinline__ uint4 multimem_ld_reduce<__nv_bfloat16>(const void* p) {
+  uint4 v;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.bf16x2 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p) : "memory");
+  return v;
+}
+template <>
+__device__ __forceinline__ uint4 multimem_ld_reduce<__half>(const void* p) {
+  uint4 v;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.f16x2 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p) : "memory");
+  return v;
+}
+template <>
+__device__ __forceinline__ uint4 multimem_ld_reduce<int32_t>(const void* p) {
+  uint4 v;
+  const char* c = (const char*)p;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.u32 %0, [%1];" : "=r"(v.x) : "l"(c) : "memory");
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.u32 %0, [%1];" : "=r"(v.y) : "l"(c + 4) : "memory");
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.u32 %0, [%1];" : "=r"(v.z) : "l"(c + 8) : "memory");
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.u32 %0, [%1];" : "=r"(v.w) : "l"(c + 12) : "memory");
+  return v;
+}
+__device__ __forceinline__ void multimem_st16(void* p, uint4 v) {
+  asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y),
+               "r"(v.z), "r"(v.w) : "memory");
+}
+
+// 0 + x_0 + x_1 + ... + x_{n-1} of one 16-byte vector read from every
+// member's unicast mapping (the reference switch order, cf/channels.py:380-388)
+template <typename T>
+__device__ __forceinline__ uint4 switch_sum_unicast(char* const* uc, int n, size_t off) {
+  using A = typename Vec<T>::Acc;
+  constexpr int V = Vec<T>::N;
+  A acc[V], t[V];
+#pragma unroll
+  for (int j = 0; j < V; j++) acc[j] = A(0);
+#pragma unroll
+  for (int q = 0; q < CF_MAX_RANKS; q++)
+    if (q < n) {
+      Vec<T>::load(ld16_cg(uc[q] + off), t);
+#pragma unroll
+      for (int j = 0; j < V; j++) acc[j] = acc_add(acc[j], t[j]);
+    }
+  return Vec<T>::store(acc);
+}
+
+// SwitchChannel (cf/channels.py:333-409) for user kernels: the members'
+// symmetric heaps bound to one multicast object.  Offsets are heap offsets
+// (cfMemAlloc returns the same offset on every rank).  `mc` is null on boxes
+// without multicast when the communicator emulates the switch
+// (cfConfig.use_multicast = 2): the same calls then run as per-member
+// unicast loads / stores through `uc`.  Built by cfSwitchChannelCreate.
+struct SwitchChannelDevice {
+  char* mc;                  // multicast mapping of the heap (null: emulated)
+  char* uc[CF_MAX_RANKS];    // every member's heap, as mapped on this rank's device
+  char* local;               // this rank's heap
+  int n;                     // members
+  int rank;
+
+  // switch_reduce (cf/channels.py:367-389): local dst[v] = sum over members of
+  // their heap at src_off, for the 16-byte vectors v = tid, tid+nthreads, ...
+  // of `bytes` (multiple of 16).
+  template <typename T>
+  __device__ void reduce(char* dst, size_t src_off, size_t bytes, int tid, int nthreads) const {
+    for (size_t v = tid; v < bytes / 16; v += nthreads)
+      st16(dst + v * 16, mc ? multimem_ld_reduce<T>(mc + src_off + v * 16)
+                            : switch_sum_unicast<T>(uc, n, src_off + v * 16));
+  }
+  // switch_broadcast (cf/channels.py:392-409): every member's heap at dst_off
+  // receives src[v].
+  __device__ void broadcast(size_t dst_off, const char* src, size_t bytes, int tid, int nthreads) const {
+    for (size_t v = tid; v < bytes / 16; v += nthreads) {
+      const uint4 x = ld16(src + v * 16);
+      if (mc) {
+        multimem_st16(mc + dst_off + v * 16, x);
+      } else {
+        for (int q = 0; q < n; q++) st16(uc[q] + dst_off + v * 16, x);
+      }
+    }
+  }
+  // fused reduce + broadcast of heap range [off, off + bytes) from src_off
+  // (one pass, the NVLS AllReduce of one chunk)
+  template <typename T>
+  __device__ void reduce_broadcast(size_t dst_off, size_t src_off, size_t bytes, int tid, int nthreads) const {
+    for (size_t v = tid; v < bytes / 16; v += nthreads) {
+      if (mc) {
+        multimem_st16(mc + dst_off + v * 16, multimem_ld_reduce<T>(mc + src_off + v * 16));
+      } else {
+        const uint4 x = switch_sum_unicast<T>(uc, n, src_off + v * 16);
+        for (int q = 0; q < n; q++) st16(uc[q] + dst_off + v * 16, x);
+      }
+    }
+  }
+};
+
 }  // namespace cf

@@ -158,6 +158,40 @@ class World:
         are copy-engine DMA issued by libcf's proxy (cf::PortChannelDevice)."""
         return self._channel(_lib.lib().cfPortChannelCreate, src, dst, tag, src_buf, dst_buf)
 
+    # -- symmetric heap (cfSymHeapCreate / cfMemAlloc) ----------------------
+
+    def symmetric_heap(self, nbytes: int, mode=None) -> int:
+        """Create every rank's symmetric heap of `nbytes` (include/cf.h).
+        mode: 1 NVLS multicast, 2 emulated switch, 0 plain; default: the
+        world's use_multicast ("emulate" -> 2; multicast built -> 1; else 0).
+        Returns the mode in use."""
+        if mode is None:
+            mode = 2 if self.config.use_multicast == 2 else (1 if self.multicast_supported() else 0)
+        _lib.check(_lib.lib().cfSymHeapCreate(self.comm, int(nbytes), int(mode), None))
+        self._sym_mode = int(mode)
+        return self._sym_mode
+
+    def alloc_symmetric(self, numel: int, dtype) -> list:
+        """Collective allocation from the symmetric heap: one tensor per rank,
+        all at the same heap offset.  switch_2pa runs in place on them
+        (multimem, no staging) and no registration is ever needed."""
+        import torch
+        es = torch.empty(0, dtype=dtype).element_size()
+        ptrs = (ctypes.c_void_p * self.num_ranks)()
+        _lib.check(_lib.lib().cfMemAlloc(self.comm, int(numel) * es, ptrs))
+        return [_lib.tensor_at(ptrs[r], numel, dtype, self.device(r)) for r in range(self.num_ranks)]
+
+    def free_symmetric(self, tensors) -> None:
+        _lib.check(_lib.lib().cfMemFree(self.comm, tensors[0].data_ptr()))
+
+    def switch_channel(self, rank: int) -> bytes:
+        """Device handle of the SwitchChannel over the symmetric heaps for
+        `rank`'s kernels (cf::SwitchChannelDevice; cf/channels.py:333-409)."""
+        buf = ctypes.create_string_buffer(256)
+        nbytes = ctypes.c_size_t(256)
+        _lib.check(_lib.lib().cfSwitchChannelCreate(self.comm, int(rank), buf, ctypes.byref(nbytes)))
+        return buf.raw[:nbytes.value]
+
     def multicast_supported(self) -> bool:
         v = ctypes.c_int()
         _lib.check(_lib.lib().cfCommMulticastSupported(self.comm, ctypes.byref(v)))

@@ -84,3 +84,24 @@ extern "C" int cftest_port_ring(const void* tx, const void* rx, int n, size_t by
   cudaFree(douts);
   return rc;
 }
+
+// NVLS AllReduce written against the SwitchChannel primitive: rank r (blockIdx.y)
+// reduces chunk r of every member's heap range [off_in, off_in + bytes) and
+// broadcasts the sums to [off_out, ...) of every member.  One co-resident
+// launch: inputs are complete before it, each output chunk has one writer.
+__global__ void switch_allreduce(const SwitchChannelDevice* sw, size_t off_in, size_t off_out, size_t bytes) {
+  const int r = blockIdx.y;
+  const SwitchChannelDevice& s = sw[r];
+  const size_t chunk = bytes / s.n;
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
+  s.reduce_broadcast<float>(off_out + r * chunk, off_in + r * chunk, chunk, tid, nt);
+}
+
+extern "C" int cftest_switch_allreduce(const void* handles, int n, size_t off_in, size_t off_out, size_t bytes) {
+  SwitchChannelDevice* d;
+  if (upload(handles, n, &d)) return 1;
+  switch_allreduce<<<dim3(8, n), 256>>>(d, off_in, off_out, bytes);
+  int rc = cudaDeviceSynchronize() != cudaSuccess;
+  cudaFree(d);
+  return rc;
+}

@@ -112,3 +112,41 @@ def test_bench_times_are_max_over_ranks():
     assert sweep[1]["kind"] == "allgather" and sweep[1]["cf_graph"]["us"] == 40.0
     assert sweep[1]["cf_graph"]["busbw"] == round((1 << 20) / 4e-5 * 0.5 / 1e9, 2)
     assert sweep[2]["plan"] == "2pa_memory" and sweep[2]["cf_plan_graph"]["us"] == 6.0
+
+
+def _fd_all_worker(rank, world, port, q, base):
+    import os
+    import torch.distributed as dist
+    from paper_2504_09014_b200.comm import share_fd
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    mine = os.open(f"{base}.{rank}", os.O_RDONLY)
+    seen = {}
+    for src in range(world):   # the symmetric-heap exchange: every rank's fd to every rank
+        got = share_fd(mine if src == rank else None, rank, world, src=src)
+        seen[src] = os.pread(got, 64, 0)
+        if src != rank:
+            os.close(got)
+    os.close(mine)
+    q.put((rank, seen))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_share_fd_all_to_all(world, tmp_path):
+    """Communicator.setup_symmetric's heap exchange: every rank's descriptor
+    reaches every other rank (share_fd with src = each rank in turn)."""
+    base = tmp_path / "heap"
+    for r in range(world):
+        (tmp_path / f"heap.{r}").write_bytes(f"heap of rank {r}".encode())
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_fd_all_worker, args=(r, world, port, q, str(base))) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in range(world):
+        assert res[r] == {s: f"heap of rank {s}".encode() for s in range(world)}
