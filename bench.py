@@ -494,6 +494,8 @@ def nccl_setup(dev, rank, world):
     import torch.distributed as dist
     if os.environ.get("CF_BENCH_ONE_GPU"):
         return None, "ranks share cuda:0 (CF_BENCH_ONE_GPU): NCCL needs one GPU per rank"
+    if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
+        os.environ["NCCL_DEBUG"] = "WARN"   # no version banner on stdout: one JSON line only
     try:
         sys.path.insert(0, os.path.join(ROOT, "scripts"))
         from nccl_ctypes import Nccl
@@ -505,7 +507,7 @@ def nccl_setup(dev, rank, world):
         return None, f"{type(e).__name__}: {e}"[:200]
 
 
-def multi_parity(comm, dev, rank, world, nvls):
+def multi_parity(comm, dev, rank, world, nvls, sym_mode=-1):
     """Before timing: libcf's NVLink results against the CPU oracle, bit for
     bit (bf16, ragged size, seeded inputs regenerated on every rank): 1pa,
     2pa_ll, 2pa, direct and ring AllGather, both ReduceScatters, and NVLS
@@ -543,21 +545,35 @@ def multi_parity(comm, dev, rank, world, nvls):
             res["allreduce_" + name] = bool(np.array_equal(host(y), oracle.allreduce(ins, oname, "bf16")[rank]))
         except Exception as e:
             res["allreduce_" + name] = f"{type(e).__name__}: {e}"[:160]
-    if nvls:
-        try:
-            comm.all_reduce(x, y, algo="switch_2pa")
-            torch.cuda.synchronize(dev)
-            comm.check_device_error()
-            want = oracle.allreduce(ins, "switch_2pa", "bf16")[rank]
-            w32 = (want.astype(np.uint32) << 16).view(np.float32)
-            g32 = (host(y).astype(np.uint32) << 16).view(np.float32)
-            sabs = np.sum([np.abs((a.astype(np.uint32) << 16).view(np.float32)) for a in ins], axis=0)
-            tol = 2.0 ** -8 * np.abs(w32) + (world - 1) * 2.0 ** -24 * sabs
-            res["allreduce_switch_2pa"] = bool(np.all(np.abs(g32 - w32) <= tol))
-        except Exception as e:
-            res["allreduce_switch_2pa"] = f"{type(e).__name__}: {e}"[:160]
     comm.deregister(x)
     comm.deregister(y)
+    if sym_mode >= 0:
+        # symmetric buffers (no registration): two-shot, and switch_2pa in
+        # place -- exact in the reference switch order when emulated, SURVEY
+        # §8(c) tolerance with a real multicast object (order unspecified)
+        xs = comm.alloc_symmetric(elems, torch_dtype("bf16"))
+        ys = comm.alloc_symmetric(elems, torch_dtype("bf16"))
+        xs.copy_(x)
+        for name in ("2pa",) + (("switch_2pa",) if nvls else ()):
+            key = f"allreduce_{name}_symmetric"
+            try:
+                ys.zero_()
+                comm.all_reduce(xs, ys, algo=name)
+                torch.cuda.synchronize(dev)
+                comm.check_device_error()
+                want = oracle.allreduce(ins, name, "bf16")[rank]
+                if name == "2pa" or sym_mode == 2:
+                    res[key] = bool(np.array_equal(host(ys), want))
+                else:
+                    w32 = (want.astype(np.uint32) << 16).view(np.float32)
+                    g32 = (host(ys).astype(np.uint32) << 16).view(np.float32)
+                    sabs = np.sum([np.abs((a.astype(np.uint32) << 16).view(np.float32)) for a in ins], axis=0)
+                    tol = 2.0 ** -8 * np.abs(w32) + (world - 1) * 2.0 ** -24 * sabs
+                    res[key] = bool(np.all(np.abs(g32 - w32) <= tol))
+            except Exception as e:
+                res[key] = f"{type(e).__name__}: {e}"[:160]
+        comm.free_symmetric(xs)
+        comm.free_symmetric(ys)
     # AllGather (bit-exact data movement, random 16-bit patterns incl. NaNs)
     shard = 4099
     sh = [a[:shard] for a in gen_inputs(world, shard, "bf16", "normal", 20250409 + 8)]
@@ -598,7 +614,7 @@ def multi_parity(comm, dev, rank, world, nvls):
             else next(r[k] for r in allres if r.get(k) is not True) for k in res}
 
 
-def multi_sweep(comm, dev, rank, world, send, recv, nvls, nvls_kind, nccl):
+def multi_sweep(comm, dev, rank, world, send, recv, nvls, nvls_kind, nccl, big=GiB, sym_mode=-1):
     """N>1: latency / busbw over sizes -- libcf (CUDA graph and eager) next to
     NCCL 2.28 (comparison baseline only, never part of the product path) in a
     CUDA graph on default buffers AND on symmetric windows (ncclMemAlloc +
@@ -608,12 +624,17 @@ def multi_sweep(comm, dev, rank, world, send, recv, nvls, nvls_kind, nccl):
     import torch
     from paper_2504_09014_b200 import _lib
     rows = []
-    # 1 KiB .. 1 GiB (x4); buffers of the largest size, registered once
-    big = GiB if not os.environ.get("CF_BENCH_ONE_GPU") else 64 * MiB
-    bs = torch.randn(big // 2, device=dev).to(torch.bfloat16)
-    br = torch.empty_like(bs)
-    comm.register(bs)
-    comm.register(br)
+    # 1 KiB .. 1 GiB (x4); buffers of the largest size from the symmetric heap
+    # (or registered once when there is none)
+    if sym_mode >= 0:
+        bs = comm.alloc_symmetric(big // 2, torch.bfloat16)
+        br = comm.alloc_symmetric(big // 2, torch.bfloat16)
+        bs.copy_(torch.randn(big // 2, device=dev).to(torch.bfloat16))
+    else:
+        bs = torch.randn(big // 2, device=dev).to(torch.bfloat16)
+        br = torch.empty_like(bs)
+        comm.register(bs)
+        comm.register(br)
     flush = torch.empty(256 * MiB, dtype=torch.uint8, device=dev)
     st = torch.cuda.current_stream(dev)
     sym = None
@@ -663,6 +684,13 @@ def multi_sweep(comm, dev, rank, world, send, recv, nvls, nvls_kind, nccl):
         row = {"bytes": nb, "kind": "allreduce",
                "cf_graph_s": time_graph(dev, lambda: comm.all_reduce(x, y, algo="auto"), iters, 3, fl),
                "cf_eager_s": eager(lambda: comm.all_reduce(x, y, algo="auto"), iters)}
+        # every algorithm on its own (the NVLink crossover table of the selector)
+        for name, var, cap in (("1pa", "", 2 * MiB), ("2pa", "ll", 2 * MiB), ("2pa", "", None),
+                               ("switch_2pa", "", None)):
+            if (cap is not None and nb > cap) or (name == "switch_2pa" and not nvls):
+                continue
+            key = f"cf_{name}{'_' + var if var else ''}_graph_s"
+            row[key] = time_graph(dev, lambda: comm.all_reduce(x, y, algo=name, variant=var), iters, 3, fl)
         if nccl is not None:
             row.update(nccl_times("allreduce", nb, nb, iters, fl))
         rows.append(row)
@@ -694,8 +722,12 @@ def multi_sweep(comm, dev, rank, world, send, recv, nvls, nvls_kind, nccl):
             x, y = bs[:cnt], br[:cnt]
             rows.append({"bytes": nb, "kind": nvls_kind, "cf_graph_s": time_graph(
                 dev, lambda: comm.all_reduce(x, y, algo="switch_2pa"), 10, 3, flush if nb < 64 * MiB else None)})
-    comm.deregister(bs)
-    comm.deregister(br)
+    if sym_mode >= 0:
+        comm.free_symmetric(bs)
+        comm.free_symmetric(br)
+    else:
+        comm.deregister(bs)
+        comm.deregister(br)
     del bs, br
     # C5: Llama-70B TP decode AllReduce [b, 8192] bf16 through DSL plans (K10)
     from paper_2504_09014_b200.algorithms import build_algo
@@ -740,14 +772,13 @@ def gather_max_over_ranks(t_local, e2e_local, rows_local, world, group=None):
         for k2 in ("plan", "batch", "kind", "error"):
             if k2 in row:
                 out[k2] = row[k2]
-        for key in ("cf_graph_s", "cf_eager_s", "nccl_graph_s", "nccl_sym_graph_s", "cf_plan_graph_s"):
-            if key in row:
-                tk = max(x[2][i][key] for x in times)   # max over ranks
-                bw = busbw(nb, tk, world) if kind in ("allreduce", "nvls", "nvls_emulated") else \
-                    (nb / tk / 1e9 * (world - 1) / world if tk > 0 else 0.0)
-                out[key[:-2]] = {"us": round(tk * 1e6, 2), "busbw": round(bw, 2)}
-                if not one_gpu:
-                    out[key[:-2]]["pct_of_900"] = round(100 * bw / 900, 2)
+        for key in [k for k in row if k.endswith("_s")]:
+            tk = max(x[2][i][key] for x in times)   # max over ranks
+            bw = busbw(nb, tk, world) if kind in ("allreduce", "nvls", "nvls_emulated") else \
+                (nb / tk / 1e9 * (world - 1) / world if tk > 0 else 0.0)
+            out[key[:-2]] = {"us": round(tk * 1e6, 2), "busbw": round(bw, 2)}
+            if not one_gpu:
+                out[key[:-2]]["pct_of_900"] = round(100 * bw / 900, 2)
         nc = [out[k]["us"] for k in ("nccl_graph", "nccl_sym_graph") if k in out]
         if nc and "cf_graph" in out:
             out["nccl_best_us"] = min(nc)
@@ -776,29 +807,34 @@ def run_multi_gpu(args):
     comm = Communicator(device=local)
     dev = torch.device("cuda", local)
     nccl, nccl_err = nccl_setup(dev, rank, world)
-    # NVLS (switch_2pa, multimem ld_reduce / st) when the box builds a multicast object
-    nvls, nvls_kind, nvls_err = False, "nvls", None
+    # symmetric heap (cfMemAlloc): every bench buffer lives there, so no
+    # registration; with a multicast object (mode 1) switch_2pa runs in place
+    # (multimem); on a 1-GPU path check the switch is emulated (mode 2)
+    big = GiB if not one_gpu else 64 * MiB
+    nvls_err = None
     try:
-        nvls = comm.setup_nvls()
-        if not nvls and one_gpu:
-            # path check on a 1-GPU box: the emulated switch runs the same
-            # kernel and bench code (rows labelled as such, not an NVLS number)
-            comm.setup_nvls_emulated(64 << 20)
-            nvls, nvls_kind = True, "nvls_emulated"
-    except Exception as e:   # report, never fail the bench
-        nvls_err = f"{type(e).__name__}: {e}"[:200]
-    parity = multi_parity(comm, dev, rank, world, nvls)
-    if nvls and parity.get("allreduce_switch_2pa") is not True:
+        sym_mode = comm.setup_symmetric(2 * big + 2 * HEAD_BYTES + 64 * MiB, mode="emulate" if one_gpu else "auto")
+    except Exception as e:
+        sym_mode, nvls_err = -1, f"{type(e).__name__}: {e}"[:200]
+    nvls = sym_mode in (1, 2)
+    nvls_kind = "nvls" if sym_mode == 1 else "nvls_emulated"
+    parity = multi_parity(comm, dev, rank, world, nvls, sym_mode)
+    if nvls and parity.get("allreduce_switch_2pa_symmetric") is not True:
         nvls = False    # a failed first multimem execution drops the NVLS rows, never the line
     count = HEAD_BYTES // 2
     gen = torch.Generator(device=dev)
     gen.manual_seed(20250409 + 4000 + rank)
-    send = torch.randn(count, device=dev, generator=gen).to(torch_dtype(HEAD_DTYPE))
-    recv = torch.empty_like(send)
-    comm.register(send)
-    comm.register(recv)
+    alloc = (lambda numel: comm.alloc_symmetric(numel, torch_dtype(HEAD_DTYPE))) if sym_mode >= 0 else \
+        (lambda numel: torch.empty(numel, device=dev, dtype=torch_dtype(HEAD_DTYPE)))
+    send, recv = alloc(count), alloc(count)
+    send.copy_(torch.randn(count, device=dev, generator=gen).to(torch_dtype(HEAD_DTYPE)))
+    if sym_mode < 0:
+        comm.register(send)
+        comm.register(recv)
     stream = torch.cuda.current_stream(dev)
-    head_algo = "2pa"
+    # the selector's pick for the headline (AUTO: in-place NVLS on a multicast
+    # heap, else the two-shot HB kernel)
+    head_algo = "switch_2pa" if (nvls and sym_mode == 1) else "2pa"
     for _ in range(args.warmup):
         comm.all_reduce(send, recv, algo=head_algo)
     torch.cuda.synchronize(dev)
@@ -823,11 +859,12 @@ def run_multi_gpu(args):
         torch.cuda.synchronize(dev)
         dist.barrier()
         t0 = time.perf_counter()
-        comm.all_reduce_host(host_in, host_out, algo=head_algo)   # pipelined H2D / K3 / D2H
+        comm.all_reduce_host(host_in, host_out, algo="2pa")   # pipelined H2D / K3 / D2H
         torch.cuda.synchronize(dev)
         if it:
             e2e_local.append(time.perf_counter() - t0)
-    rows_local = [] if args.no_sweep else multi_sweep(comm, dev, rank, world, send, recv, nvls, nvls_kind, nccl)
+    rows_local = [] if args.no_sweep else multi_sweep(comm, dev, rank, world, send, recv, nvls, nvls_kind, nccl,
+                                                       big, sym_mode)
     t, te, sweep = gather_max_over_ranks(t_local, float(np.mean(e2e_local)), rows_local, world)
     ok = all(v is True for v in parity.values())
     if rank == 0:
@@ -840,7 +877,9 @@ def run_multi_gpu(args):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": HEAD_DTYPE,
             "data": "synthetic",
             "config": {"workload": f"AllReduce {HEAD_DTYPE}, {where}, {HEAD_BYTES // MiB} MiB per rank "
-                                   "(C4 shape)", "ranks": world, "algo": head_algo,
+                                   "(C4 shape)", "ranks": world,
+                       "algo": head_algo + (" (in place, symmetric buffers)" if head_algo == "switch_2pa" else ""),
+                       "buffers": "symmetric heap (cfMemAlloc)" if sym_mode >= 0 else "registered torch tensors",
                        "parallelism": f"{world} GPUs" if not one_gpu else f"{world} processes / 1 GPU",
                        "l2": "inputs larger than L2 (headline); sweep rows < 64 MiB flush L2 between "
                              "timed iterations (both arms)"},
@@ -855,7 +894,7 @@ def run_multi_gpu(args):
                                 "eager vs NCCL 2.28 in a CUDA graph on default buffers (nccl_graph) and on "
                                 "symmetric windows (nccl_sym_graph); latency = max over ranks",
                       "nccl_version": Nccl_version(nccl), "nccl_error": nccl_err, "nvls": nvls_kind if nvls
-                      else None, "nvls_error": nvls_err, "rows": sweep}}
+                      else None, "nvls_error": nvls_err, "symmetric_heap_mode": sym_mode, "rows": sweep}}
         if one_gpu:
             line["roofline"] = None
         else:

@@ -1188,15 +1188,24 @@ extern "C" cfStatus cfPlanExecute(cfPlan_t pl, const void* const* inputs, void* 
   if (!pl->ready) return fail(CF_E_CONFIG, "plan not connected (cfPlanGetHandle / cfPlanConnect)");
   cfComm* c = pl->comm;
   const int n = pl->ir.nranks;
-  // one process per GPU: peers' I/O buffers come from the registration table
+  // one process per GPU: peers' I/O buffers come from the registration table,
+  // or from the symmetric heap (cfMemAlloc buffers: base[p] + offset)
   const Registration* reg_in = nullptr;
   const Registration* reg_out = nullptr;
+  long long sym_in = -1, sym_out = -1;
   if (pl->mp) {
-    if (pl->peer_in && !(reg_in = c->find_reg(inputs[0])))
-      return fail(CF_E_TOPOLOGY, "plan reads the peers' input: register input %p (cfBufferExport/Import)", inputs[0]);
-    if (pl->peer_out && !(reg_out = c->find_reg(outputs[0])))
-      return fail(CF_E_TOPOLOGY, "plan writes the peers' output: register output %p (cfBufferExport/Import)",
-                  outputs[0]);
+    bool mapped = c->sym.on();
+    for (int p = 0; mapped && p < c->nranks; p++) mapped = c->sym.peer[0][p] != nullptr;
+    if (mapped) {
+      sym_in = c->sym.offset(0, inputs[0]);
+      sym_out = c->sym.offset(0, outputs[0]);
+    }
+    if (pl->peer_in && sym_in < 0 && !(reg_in = c->find_reg(inputs[0])))
+      return fail(CF_E_TOPOLOGY, "plan reads the peers' input: register input %p (cfBufferExport/Import) or "
+                                 "allocate it with cfMemAlloc", inputs[0]);
+    if (pl->peer_out && sym_out < 0 && !(reg_out = c->find_reg(outputs[0])))
+      return fail(CF_E_TOPOLOGY, "plan writes the peers' output: register output %p (cfBufferExport/Import) or "
+                                 "allocate it with cfMemAlloc", outputs[0]);
   }
   for (size_t li = 0; li < c->local.size(); li++) {
     if (!inputs[li] || !outputs[li]) return fail(CF_E_OOB, "local rank %zu: null buffer", li);
@@ -1238,8 +1247,10 @@ extern "C" cfStatus cfPlanExecute(cfPlan_t pl, const void* const* inputs, void* 
     for (int r = 0; r < n; r++) {
       if (pl->mp) {
         a.io_in[r] = r == pl->me ? (char*)inputs[0]
+                   : sym_in >= 0 ? c->sym.peer[0][r] + sym_in
                    : reg_in ? reg_in->peer[r] + ((const char*)inputs[0] - reg_in->ptr) : nullptr;
         a.io_out[r] = r == pl->me ? (char*)outputs[0]
+                    : sym_out >= 0 ? c->sym.peer[0][r] + sym_out
                     : reg_out ? reg_out->peer[r] + ((char*)outputs[0] - reg_out->ptr) : nullptr;
       } else {
         a.io_in[r] = (char*)inputs[r];     // one-process world: local index == rank
