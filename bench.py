@@ -714,6 +714,18 @@ def multi_sweep(comm, dev, rank, world, send, recv, nvls, nvls_kind, nccl, big=G
                 row.update(nccl_times(kind, (shard if kind == "allgather" else cnt) * 2,
                                       (cnt if kind == "allgather" else shard) * 2, iters, fl))
             rows.append(row)
+    # CTA budget sweep of the two-shot kernel at large sizes (default budget
+    # one rank per GPU: 64 CTAs; the driver's 8-GPU run measures the choice)
+    for nb in (64 * MiB, 256 * MiB):
+        if nb > big:
+            continue
+        x, y = bs[:nb // 2], br[:nb // 2]
+        row = {"bytes": nb, "kind": "allreduce", "budget_sweep": True}
+        for ctas in (16, 32, 64, 128):
+            comm.set_cta_budget(ctas, "2pa")
+            row[f"cf_2pa_ctas{ctas}_graph_s"] = time_graph(dev, lambda: comm.all_reduce(x, y, algo="2pa"), 10, 3)
+        comm.set_cta_budget(0, "2pa")
+        rows.append(row)
     if nvls:
         for nb in [MiB << (2 * i) for i in range(6)]:
             if nb > big:
@@ -769,7 +781,7 @@ def gather_max_over_ranks(t_local, e2e_local, rows_local, world, group=None):
         nb = row["bytes"]
         kind = row.get("kind", "allreduce")
         out = {"bytes": nb}
-        for k2 in ("plan", "batch", "kind", "error"):
+        for k2 in ("plan", "batch", "kind", "error", "budget_sweep"):
             if k2 in row:
                 out[k2] = row[k2]
         for key in [k for k in row if k.endswith("_s")]:

@@ -204,7 +204,11 @@ CF_API cfStatus cfCommLocalRanks(cfComm_t comm, int* nlocal, int* ranks /* nulla
 CF_API cfStatus cfCommMulticastSupported(cfComm_t comm, int* supported);
 
 /* Device-side spin timeout word (SURVEY.md §5 failure detection): 0 if clean,
- * CF_E_DEADLOCK if any wait of any local rank timed out.  Synchronizes. */
+ * CF_E_DEADLOCK if any wait of any local rank timed out.  Reads the word
+ * with a synchronous legacy-stream copy: it waits for work on blocking
+ * streams, not for the whole device (a compute kernel on a non-blocking
+ * stream beside the collectives is not waited for) -- synchronize the
+ * streams the collectives ran on first. */
 CF_API cfStatus cfCommLastDeviceError(cfComm_t comm, int* code);
 CF_API cfStatus cfCommClearDeviceError(cfComm_t comm);
 
@@ -264,6 +268,16 @@ CF_API cfStatus cfAllReduceAddRMSNorm(cfComm_t comm, const void* const* send, co
                                       size_t rows, size_t hidden, float eps, cfDtype dtype, int algo,
                                       const cudaStream_t* streams);
 
+/* CTA budget per rank for `algo` (CF_ALGO_COUNT = the fused K13 kernel; -1 =
+ * every algorithm without its own budget; ctas = 0 restores the default).
+ * Default: no cap beyond co-residency when ranks share a GPU (the HBM-proxy
+ * world needs every SM); 64 CTAs per rank when every rank has its own GPU --
+ * NVLink-bound collectives saturate the link with far fewer than 148 CTAs,
+ * and a grid under half the SMs stays fully resident next to a compute
+ * kernel holding the other half, so the CTA-pair handshakes cannot wait on
+ * a partner that is not scheduled. */
+CF_API cfStatus cfCommSetCtaBudget(cfComm_t comm, int algo, int ctas);
+
 /* The algorithm the measured selector picks (cf/collectives.py:473-491).
  * collective: 0 = allreduce, 1 = allgather, 2 = reducescatter; nbytes as the
  * reference counts them (AG: output bytes). */
@@ -283,7 +297,8 @@ CF_API cfStatus cfPlanExecute(cfPlan_t plan, const void* const* inputs, void* co
                               const cudaStream_t* streams);
 CF_API cfStatus cfPlanInfo(cfPlan_t plan, size_t* in_elems, size_t* out_elems, int* dtype, int* n_programs,
                            int* n_device_ops);
-/* Device spin-timeout word of the plan's ranks (0 or CF_E_DEADLOCK).  Synchronizes. */
+/* Device spin-timeout word of the plan's ranks (0 or CF_E_DEADLOCK); read like
+ * cfCommLastDeviceError (synchronize the plan's streams first). */
 CF_API cfStatus cfPlanLastDeviceError(cfPlan_t plan, int* code);
 /* After a reported timeout: return every plan heap this process owns to its
  * load-time state (error word, semaphore lanes, barriers, LL scratch), so the

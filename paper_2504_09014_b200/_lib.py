@@ -25,6 +25,7 @@ ALGOS = {
     "allpairs_ag": 6, "ring_ag": 7, "ring_rs": 8, "rs_direct": 9,
 }
 ALGO_NAMES = {v: k for k, v in ALGOS.items()}
+CF_ALGO_COUNT = 10   # cfAlgo count; also the CTA-budget slot of the fused K13 kernel
 CF_PLAN_HANDLE_BYTES = 128
 
 # every symbol include/cf.h declares (tests check the .so exports all of them)
@@ -40,7 +41,7 @@ EXPORTS = (
     "cfAllReduceAddRMSNorm", "cfSelectAlgorithm", "cfPlanLoad", "cfPlanExecute",
     "cfPlanInfo", "cfPlanLastDeviceError", "cfPlanClearDeviceError", "cfPlanGetHandle", "cfPlanConnect", "cfPlanDestroy",
     "cfDslBuild", "cfDslLower", "cfSymHeapCreate", "cfSymHeapMapPeer", "cfSymHeapMulticast",
-    "cfSymHeapInfo", "cfMemAlloc", "cfMemFree", "cfSwitchChannelCreate",
+    "cfSymHeapInfo", "cfMemAlloc", "cfMemFree", "cfSwitchChannelCreate", "cfCommSetCtaBudget",
 )
 
 
@@ -93,6 +94,7 @@ _PROTOS = {
     "cfPlanExecute": ([vp, P(vp), P(vp), P(vp)], i32),
     "cfPlanLastDeviceError": ([vp, P(i32)], i32),
     "cfPlanClearDeviceError": ([vp], i32),
+    "cfCommSetCtaBudget": ([vp, i32, i32], i32),
     "cfSymHeapCreate": ([vp, sz, i32, P(i32)], i32),
     "cfSymHeapMapPeer": ([vp, i32, i32], i32),
     "cfSymHeapMulticast": ([vp, i32, P(i32)], i32),

@@ -252,6 +252,12 @@ class Communicator:
         _lib.check(_lib.lib().cfNvlsEmulate(self._comm, staging.data_ptr(), staging_bytes))
         self._nvls_staging = staging
 
+    def set_cta_budget(self, ctas: int, algo: str | None = None) -> None:
+        """CTAs per rank for `algo` (None: every algorithm; "fused": K13; 0:
+        the default, 64 one rank per GPU) -- include/cf.h cfCommSetCtaBudget."""
+        aid = -1 if algo is None else (_lib.CF_ALGO_COUNT if algo == "fused" else _lib.ALGOS[algo])
+        _lib.check(_lib.lib().cfCommSetCtaBudget(self._comm, aid, int(ctas)))
+
     def setup_symmetric(self, nbytes: int, mode: str = "auto") -> int:
         """Collective: this rank's symmetric heap (include/cf.h cfSymHeapCreate),
         its POSIX fd sent to every peer (SCM_RIGHTS over Unix sockets) and the
@@ -319,6 +325,8 @@ class Communicator:
         return device_multicast_capable(self.device.index)
 
     def check_device_error(self):
+        import torch
+        torch.cuda.current_stream(self.device).synchronize()
         code = ctypes.c_int()
         _lib.check(_lib.lib().cfCommLastDeviceError(self._comm, ctypes.byref(code)))
         if code.value:
@@ -377,7 +385,9 @@ class RankRuntime:
         return recv
 
     def check_device_error(self):
+        import torch
         from .errors import DeadlockError
+        torch.cuda.current_stream(self.comm.device).synchronize()
         code = ctypes.c_int()
         _lib.check(_lib.lib().cfPlanLastDeviceError(self._plan, ctypes.byref(code)))
         if code.value:

@@ -1341,7 +1341,8 @@ extern "C" cfStatus cfPlanLastDeviceError(cfPlan_t pl, int* code) {
   for (size_t r = 0; r < pl->heap.size(); r++) {
     if (!pl->heap[r] || pl->heap_mapped[r]) continue;   // own heaps only
     cudaSetDevice(pl->comm->local[pl->mp ? 0 : r].dev);
-    cudaDeviceSynchronize();
+    // synchronous legacy-stream copy: waits for the caller's (blocking)
+    // streams, not for unrelated non-blocking ones
     PlanState st;
     if (cudaMemcpy(&st, pl->heap[r] + pl->state_off, sizeof(st), cudaMemcpyDeviceToHost) != cudaSuccess) {
       cudaSetDevice(prev);

@@ -55,7 +55,17 @@ int occupancy(cfComm* c, const void* kernel, int dev, int threads) {
 
 // `per_sm` > 0 caps the residency used at that many CTAs per SM (K3 two-shot
 // at 256 MiB: 2 CTAs/SM 731 us, 1 CTA/SM 663 us).
-int max_blocks_per_rank(cfComm* c, const void* kernel, int group, int threads, int per_sm) {
+static int cta_budget(const cfComm* c, int algo) {
+  if (algo >= 0 && algo <= CF_ALGO_COUNT && c->budget[algo] > 0) return c->budget[algo];
+  if (c->budget_all > 0) return c->budget_all;
+  std::map<int, int> per_dev;
+  for (const auto& lr : c->local) per_dev[lr.dev]++;
+  for (const auto& d : per_dev)
+    if (d.second > 1) return 0;   // co-resident ranks (HBM proxy, tests): full residency
+  return kNvlinkCtaBudget;
+}
+
+int max_blocks_per_rank(cfComm* c, const void* kernel, int group, int threads, int per_sm, int algo) {
   const auto& g = c->groups[group];
   const int dev = c->local[g[0]].dev;
   int occ = occupancy(c, kernel, dev, threads);
@@ -68,6 +78,8 @@ int max_blocks_per_rank(cfComm* c, const void* kernel, int group, int threads, i
   int mb = std::max(1, cap / std::max(on_dev, (int)g.size()));
   mb = std::min(mb, CF_MAX_BLOCKS);
   if (c->cfg.max_blocks > 0) mb = std::min(mb, c->cfg.max_blocks);
+  const int budget = cta_budget(c, algo);
+  if (budget > 0) mb = std::min(mb, budget);
   return mb;
 }
 
@@ -520,7 +532,9 @@ extern "C" cfStatus cfCommLastDeviceError(cfComm_t c, int* code) {
   uint32_t worst = 0;
   for (size_t li = 0; li < c->local.size(); li++) {
     CF_CUDA(cudaSetDevice(c->local[li].dev));
-    CF_CUDA(cudaDeviceSynchronize());
+    // a synchronous copy on the legacy stream waits for every blocking stream
+    // (the caller's collectives) but not for unrelated non-blocking streams
+    // (a compute kernel running beside the collectives)
     RankState st;
     CF_CUDA(cudaMemcpy(&st, c->state((int)li), sizeof(st), cudaMemcpyDeviceToHost));
     worst = std::max(worst, st.error);
@@ -534,9 +548,21 @@ extern "C" cfStatus cfCommClearDeviceError(cfComm_t c) {
   DeviceGuard guard;
   for (size_t li = 0; li < c->local.size(); li++) {
     CF_CUDA(cudaSetDevice(c->local[li].dev));
-    CF_CUDA(cudaDeviceSynchronize());
     CF_CUDA(cudaMemset((char*)c->state((int)li) + offsetof(RankState, error), 0, sizeof(uint32_t)));
+    CF_CUDA(cudaStreamSynchronize(0));
   }
+  return CF_OK;
+}
+
+extern "C" cfStatus cfCommSetCtaBudget(cfComm_t c, int algo, int ctas) {
+  if (!c) return fail(CF_E_CONFIG, "null communicator");
+  if (ctas < 0 || ctas > CF_MAX_BLOCKS) return fail(CF_E_CONFIG, "ctas must be in [0, %d]", CF_MAX_BLOCKS);
+  if (algo == -1) {
+    c->budget_all = ctas;
+    return CF_OK;
+  }
+  if (algo < 0 || algo > CF_ALGO_COUNT) return fail(CF_E_NO_ALGO, "unknown algorithm %d", algo);
+  c->budget[algo] = ctas;
   return CF_OK;
 }
 
@@ -554,6 +580,7 @@ namespace {
 enum Kind { kPull = 0, kLL1 = 1, kLL2 = 2, kGather = 3, kNvls = 4, kRing = 5, kRingGather = 6, kNorm = 7 };
 
 struct Job {
+  int algo = -1;      // cfAlgo (CF_ALGO_COUNT: K13) -- selects the CTA budget
   int kind = kPull;
   int order = kLead;
   int push = 0, whole = 0, rs_shift = 0;
@@ -643,7 +670,7 @@ cfStatus launch(cfComm* c, const Job& j, int dtype, const void* const* send, voi
   // step): smaller CTAs give each rank up to kRingCtas independent links.
   const bool ring = j.kind == kRing || j.kind == kRingGather;
   int threads = j.kind == kRing ? std::min(c->cfg.threads, 256) : c->cfg.threads;   // ring_kernel's bound
-  if (j.kind == kNorm && j.blocks > max_blocks_per_rank(c, kernel, 0, threads))
+  if (j.kind == kNorm && j.blocks > max_blocks_per_rank(c, kernel, 0, threads, 0, j.algo))
     // K13 rows per rank beyond one resident round: 256-thread CTAs (2 per SM)
     // finish them in one round (b=256: 22.3 -> 20.3 us; fewer rows keep 512)
     threads = std::min(threads, 256);
@@ -707,7 +734,7 @@ cfStatus launch(cfComm* c, const Job& j, int dtype, const void* const* send, voi
     // us); the pull-only variants (K2, K8) gain from full residency at every
     // size (K8 256 MiB 394 -> 354 us, K2 1 MiB 13.4 -> 10.1 us)
     const bool k3_big = j.kind == kPull && j.push && j.count * dtype_size(dtype) > ((size_t)8 << 20);
-    int mb = max_blocks_per_rank(c, kernel, (int)gi, threads, k3_big ? 1 : 0);
+    int mb = max_blocks_per_rank(c, kernel, (int)gi, threads, k3_big ? 1 : 0, j.algo);
     if (ring) mb = std::min(mb, kRingCtas);   // ring slot region
     int blocks = (int)std::min<size_t>((size_t)mb, std::max<size_t>(1, ceil_div(j.work, (size_t)threads)));
     if (j.blocks) blocks = std::min(mb, j.blocks);
@@ -757,7 +784,7 @@ cfStatus nvls_allreduce(cfComm* c, const void* const* send, void* const* recv, s
       }
       rk.nv_mc = c->nvls.ranks[li].mc;
     }
-    const int mb = max_blocks_per_rank(c, kernel, (int)gi, threads);
+    const int mb = max_blocks_per_rank(c, kernel, (int)gi, threads, 0, CF_ALGO_SWITCH_2PA);
     const int blocks = (int)std::min<size_t>((size_t)mb, std::max<size_t>(1, ceil_div(work, (size_t)threads)));
     CF_TRY(join_streams(c, (int)gi, streams, false));
     void* args[] = {&a};
@@ -801,7 +828,7 @@ cfStatus nvls_direct(cfComm* c, size_t count, int dtype, long long oi, long long
         rk.mc_out = c->sym.ranks[li].mc + oo;
       }
     }
-    const int mb = max_blocks_per_rank(c, kernel, (int)gi, threads);
+    const int mb = max_blocks_per_rank(c, kernel, (int)gi, threads, 0, CF_ALGO_SWITCH_2PA);
     const int blocks = (int)std::min<size_t>((size_t)mb, std::max<size_t>(1, ceil_div(work, (size_t)threads)));
     CF_TRY(join_streams(c, (int)gi, streams, false));
     void* args[] = {&a};
@@ -836,6 +863,7 @@ extern "C" cfStatus cfAllReduce(cfComm_t c, const void* const* send, void* const
   if (algo == CF_ALGO_SWITCH_2PA && sym_switch) return nvls_direct(c, count, dtype, oi, oo, streams);
   if (algo == CF_ALGO_SWITCH_2PA && c->nvls.enabled) return nvls_allreduce(c, send, recv, count, dtype, streams);
   Job j;
+  j.algo = algo;
   j.count = count;
   switch (algo) {
     case CF_ALGO_1PA:
@@ -896,6 +924,7 @@ extern "C" cfStatus cfAllGather(cfComm_t c, const void* const* send, void* const
   if (algo != CF_ALGO_ALLPAIRS_AG && algo != CF_ALGO_RING_AG)
     return fail(CF_E_NO_ALGO, "algorithm %d is not an AllGather algorithm", algo);
   Job j;
+  j.algo = algo;
   j.kind = algo == CF_ALGO_RING_AG ? kRingGather : kGather;
   j.count = sendcount;
   j.work = ceil_div(sendcount * dtype_size(dtype), 16);
@@ -913,6 +942,7 @@ extern "C" cfStatus cfReduceScatter(cfComm_t c, const void* const* send, void* c
   if (algo != CF_ALGO_RS_DIRECT && algo != CF_ALGO_RING_RS)
     return fail(CF_E_NO_ALGO, "algorithm %d is not a ReduceScatter algorithm", algo);
   Job j;
+  j.algo = algo;
   j.kind = algo == CF_ALGO_RING_RS ? kRing : kPull;
   j.rs_shift = 1;
   j.order = kLead;
@@ -964,6 +994,7 @@ extern "C" cfStatus cfAllReduceAddRMSNorm(cfComm_t c, const void* const* send, c
         }
   }
   Job j;
+  j.algo = CF_ALGO_COUNT;
   j.kind = kNorm;
   j.order = kLead;
   j.rows = rows;
@@ -1133,6 +1164,7 @@ static cfStatus host_allreduce(cfComm* c, const void* const* hsend, void* const*
     }
     if (pipelined) {
       Job j;
+      j.algo = CF_ALGO_2PA;
       j.kind = kPull;
       j.push = 1;
       j.order = kLead;

@@ -158,6 +158,10 @@ struct cfComm {
   std::map<int, int> sm_count;         // device -> SMs
   std::map<std::pair<const void*, int>, int> occ;  // (kernel, device) -> CTAs/SM
   bool multicast_supported = false;
+  // CTA budget per rank and algorithm (cfCommSetCtaBudget; index CF_ALGO_COUNT =
+  // the fused K13 kernel; budget_all applies to every algorithm without its own)
+  int budget[CF_ALGO_COUNT + 1] = {};
+  int budget_all = 0;
   cf::Nvls nvls;
   cf::SymHeap sym;
   cf::Proxy* proxy = nullptr;          // PortChannel proxy thread (started on demand)
@@ -181,8 +185,14 @@ namespace cf {
 int occupancy(cfComm* c, const void* kernel, int dev, int threads);
 // Driver API function by name (nullptr if unavailable).
 void* driver_fn(const char* name);
-// Co-residency cap: CTAs per rank such that every rank of the group fits at once.
-int max_blocks_per_rank(cfComm* c, const void* kernel, int group, int threads, int per_sm = 0);
+// Co-residency cap: CTAs per rank such that every rank of the group fits at
+// once, further capped by the algorithm's CTA budget (cfCommSetCtaBudget;
+// algo -1 = none, CF_ALGO_COUNT = the fused K13 kernel).
+int max_blocks_per_rank(cfComm* c, const void* kernel, int group, int threads, int per_sm = 0, int algo = -1);
+// Default CTA budget per rank when every rank has its own GPU (NVLink-bound
+// collectives): well under half the SMs, so a concurrent compute kernel
+// holding half of them cannot leave a collective partially resident.
+constexpr int kNvlinkCtaBudget = 64;
 // Make streams[first] of the group wait for the others; after the launch, the
 // others wait for it.  `after` selects the phase.
 cfStatus join_streams(cfComm* c, int group, const cudaStream_t* streams, bool after);

@@ -108,6 +108,7 @@ class Runtime:
 
     def check_device_error(self):
         """Synchronize and raise DeadlockError if a device wait of this plan timed out."""
+        self.world.synchronize()
         code = ctypes.c_int()
         _lib.check(_lib.lib().cfPlanLastDeviceError(self._plan, ctypes.byref(code)))
         if code.value:

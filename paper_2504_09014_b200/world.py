@@ -128,12 +128,18 @@ class World:
         return [torch.cuda.current_stream(self.device(r)).cuda_stream for r in range(self.num_ranks)]
 
     def synchronize(self):
+        """Wait for the streams the world's collectives were issued on (not
+        the whole device: unrelated streams, e.g. a compute kernel running
+        beside the collectives, are not waited for)."""
         import torch
         for d in sorted(set(self.devices)):
-            torch.cuda.synchronize(d)
+            torch.cuda.current_stream(d).synchronize()
+        for st in getattr(self, "_rank_streams", None) or ():
+            st.synchronize()
 
     def check_device_error(self):
         """Raise DeadlockError if any device wait of this world timed out."""
+        self.synchronize()
         code = ctypes.c_int()
         _lib.check(_lib.lib().cfCommLastDeviceError(self.comm, ctypes.byref(code)))
         if code.value:
@@ -157,6 +163,12 @@ class World:
         """Device handle of a PortChannel src -> dst (cf/channels.py:54-150): puts
         are copy-engine DMA issued by libcf's proxy (cf::PortChannelDevice)."""
         return self._channel(_lib.lib().cfPortChannelCreate, src, dst, tag, src_buf, dst_buf)
+
+    def set_cta_budget(self, ctas: int, algo: str | None = None) -> None:
+        """CTAs per rank for `algo` (None: every algorithm; "fused": the K13
+        kernel; 0 restores the default) -- include/cf.h cfCommSetCtaBudget."""
+        aid = -1 if algo is None else (_lib.CF_ALGO_COUNT if algo == "fused" else _lib.ALGOS[algo])
+        _lib.check(_lib.lib().cfCommSetCtaBudget(self.comm, aid, int(ctas)))
 
     # -- symmetric heap (cfSymHeapCreate / cfMemAlloc) ----------------------
 

@@ -105,3 +105,48 @@ extern "C" int cftest_switch_allreduce(const void* handles, int n, size_t off_in
   cudaFree(d);
   return rc;
 }
+
+// A compute stand-in that holds `nctas` SMs (one CTA per SM through its
+// shared-memory request) until the host raises a flag, or a 30 s safety
+// timeout: the collectives of the partial-residency test run beside it.
+__global__ void spin_hold(volatile int* flag, unsigned long long timeout_ns, int* timed_out) {
+  extern __shared__ char smem[];
+  if (threadIdx.x == 0) {
+    smem[0] = 1;
+    unsigned long long t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (;;) {
+      if (*flag) break;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > timeout_ns) { atomicExch(timed_out, 1); break; }
+      __nanosleep(2000);
+    }
+  }
+  __syncthreads();
+}
+
+static int* g_flag = nullptr;
+static int* g_timed_out = nullptr;
+static cudaStream_t g_spin = nullptr;
+
+extern "C" int cftest_spin_start(int nctas, int smem_bytes) {
+  if (!g_flag && cudaHostAlloc((void**)&g_flag, 2 * sizeof(int), cudaHostAllocMapped) != cudaSuccess) return 1;
+  g_timed_out = g_flag + 1;
+  g_flag[0] = 0;
+  g_flag[1] = 0;
+  if (!g_spin && cudaStreamCreateWithFlags(&g_spin, cudaStreamNonBlocking) != cudaSuccess) return 2;
+  if (cudaFuncSetAttribute(spin_hold, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes) != cudaSuccess)
+    return 3;
+  int *dflag, *dto;
+  cudaHostGetDevicePointer((void**)&dflag, g_flag, 0);
+  cudaHostGetDevicePointer((void**)&dto, g_timed_out, 0);
+  spin_hold<<<nctas, 32, smem_bytes, g_spin>>>(dflag, 30ull * 1000000000ull, dto);
+  return cudaGetLastError() != cudaSuccess ? 4 : 0;
+}
+
+// 0: released by the flag; 1: the hold hit its timeout; >1: CUDA error
+extern "C" int cftest_spin_stop(void) {
+  *(volatile int*)g_flag = 1;
+  if (cudaStreamSynchronize(g_spin) != cudaSuccess) return 2;
+  return g_flag[1] ? 1 : 0;
+}
