@@ -69,12 +69,22 @@ __device__ __forceinline__ void end_call(const RankCtx& rk, uint64_t e) {
 __device__ __forceinline__ void handshake(const RankCtx& rk, int n, uint64_t v, bool publish, bool gpu) {
   const int t = threadIdx.x, r = rk.rank, b = blockIdx.x;
   if (publish) {
+#if CF_DROP_FENCE != 1
     fence_publish(gpu);
+#endif
     __syncthreads();
   }
   if (t < n && t != r) {
+    CF_STRESS_AT(10);
+#if CF_DROP_FENCE == 1
+    st_relaxed(rk.sem[t] + sem_index(r, b), v, gpu);
+#else
     st_release(rk.sem[t] + sem_index(r, b), v, gpu);
-    wait_geq(rk.sem[r] + sem_index(t, b), v, rk.st, gpu);
+#endif
+#if CF_DROP_FENCE == 5
+    if (!publish)
+#endif
+      wait_geq(rk.sem[r] + sem_index(t, b), v, rk.st, gpu);
   }
   __syncthreads();
 }
@@ -715,37 +725,48 @@ struct RingLink {
     if (threadIdx.x == 0) st_release(ack_out, base + qr + 1, gpu);
     qr++;
   }
+  __device__ void credit_wait() {
+#if CF_DROP_FENCE != 6
+    wait_geq(ack_in, base + (qs >= kRingSlots ? qs - kRingSlots + 1 : 0), st, gpu);
+#endif
+  }
+  __device__ void publish_data() {
+    CF_STRESS_AT(20);
+#if CF_DROP_FENCE == 3
+    st_relaxed(data_out, base + qs + 1, gpu);
+#else
+    ring_publish(gpu);
+    st_release(data_out, base + qs + 1, gpu);
+#endif
+  }
   __device__ void send_wait() {
-    if (threadIdx.x == 0) wait_geq(ack_in, base + (qs >= kRingSlots ? qs - kRingSlots + 1 : 0), st, gpu);
+    if (threadIdx.x == 0) credit_wait();
     __syncthreads();
   }
   __device__ void send_done() {
-    if (CF_RING_THREAD_FENCE) fence_publish(gpu);
+    if (CF_RING_THREAD_FENCE && CF_DROP_FENCE != 3) fence_publish(gpu);
     __syncthreads();
-    if (threadIdx.x == 0) {
-      ring_publish(gpu);
-      st_release(data_out, base + qs + 1, gpu);
-    }
+    if (threadIdx.x == 0) publish_data();
     qs++;
   }
   // One barrier for both waits of a step: thread 0 polls the incoming data,
   // thread 32 (another warp) the send credit, concurrently.
   __device__ void wait_both(bool rcv, bool snd) {
     if (rcv && threadIdx.x == 0) wait_geq(data_in, base + qr + 1, st, gpu);
-    if (snd && threadIdx.x == 32) wait_geq(ack_in, base + (qs >= kRingSlots ? qs - kRingSlots + 1 : 0), st, gpu);
+    if (snd && threadIdx.x == 32) credit_wait();
     __syncthreads();
   }
   // One barrier for both completions of a step: free the received slot, then
   // publish the sent one.
   __device__ void done_both(bool rcv, bool snd) {
-    if (CF_RING_THREAD_FENCE && snd) fence_publish(gpu);
+    if (CF_RING_THREAD_FENCE && CF_DROP_FENCE != 3 && snd) fence_publish(gpu);
     __syncthreads();
     if (threadIdx.x == 0) {
-      if (rcv) st_release(ack_out, base + qr + 1, gpu);
-      if (snd) {
-        ring_publish(gpu);
-        st_release(data_out, base + qs + 1, gpu);
+      if (rcv) {
+        CF_STRESS_AT(21);
+        st_release(ack_out, base + qr + 1, gpu);
       }
+      if (snd) publish_data();
     }
     if (rcv) qr++;
     if (snd) qs++;

@@ -177,6 +177,59 @@ __device__ __forceinline__ void st_masked16(char* base, uint4 v, int jlo, int jh
   }
 }
 
+// ---------------------------------------------------------------- robustness builds
+//
+// -DCF_STRESS=<ns>: a pseudo-random __nanosleep of up to <ns> at one in four
+// visits of every synchronization site (before LL packet stores and before
+// handshake / ring releases, after acquires), widening every race window --
+// the GPU counterpart of the reference's adversarial schedules
+// (pkg/tests/test_acceptance.py:115-202).
+// -DCF_DROP_FENCE=<site>: mutation builds, each removing one ordering
+// guarantee; tests/test_gpu_stress.py requires the stress run to fail on them:
+//   1  handshake release: no publishing fence, relaxed signal store
+//   2  every semaphore wait: relaxed instead of acquire load
+//   3  ring data release: no publishing fence, relaxed store
+//   4  LL packets: flags stored before (and apart from) the payload words
+//   5  exit / phase handshakes: signal without waiting for the peers
+//   6  ring credits: the sender does not wait for the receiver's ack
+#ifndef CF_DROP_FENCE
+#define CF_DROP_FENCE 0
+#endif
+#ifdef CF_STRESS
+__device__ __forceinline__ void cf_stress(uint32_t site) {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  uint32_t h = (uint32_t)t ^ (threadIdx.x * 0x9E3779B9u) ^ (blockIdx.x * 0x85EBCA6Bu) ^
+               (blockIdx.y * 0xC2B2AE35u) ^ (site * 0x27D4EB2Fu);
+  h ^= h >> 15;
+  h *= 0x2C1B3C6Du;
+  h ^= h >> 12;
+  if ((h & 3u) == 0) __nanosleep(h % (uint32_t)(CF_STRESS));
+}
+#define CF_STRESS_AT(site) ::cf::cf_stress(site)
+#else
+#define CF_STRESS_AT(site) ((void)0)
+#endif
+
+__device__ __forceinline__ void st_relaxed(uint64_t* p, uint64_t v, bool gpu) {
+  if (gpu) asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+  else asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_relaxed(const uint64_t* p, bool gpu) {
+  uint64_t v;
+  if (gpu) asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  else asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+// the load of a semaphore wait (mutation 2 drops its acquire)
+__device__ __forceinline__ uint64_t ld_wait(const uint64_t* p, bool gpu) {
+#if CF_DROP_FENCE == 2
+  return ld_relaxed(p, gpu);
+#else
+  return ld_acquire(p, gpu);
+#endif
+}
+
 // ---------------------------------------------------------------- spin waits
 
 // Spin until *sem >= target (acquire).  Returns false on timeout or when the
@@ -184,11 +237,17 @@ __device__ __forceinline__ void st_masked16(char* base, uint4 v, int jlo, int jh
 // full-timeout per wait).
 __device__ __forceinline__ bool wait_geq(const uint64_t* sem, uint64_t target, RankState* st,
                                          bool gpu = false) {
-  if (ld_acquire(sem, gpu) >= target) return true;
+  if (ld_wait(sem, gpu) >= target) {
+    CF_STRESS_AT(1);
+    return true;
+  }
   const uint64_t t0 = globaltimer();
   const uint64_t limit = st->timeout_ns;
   for (uint32_t it = 1;; ++it) {
-    if (ld_acquire(sem, gpu) >= target) return true;
+    if (ld_wait(sem, gpu) >= target) {
+      CF_STRESS_AT(2);
+      return true;
+    }
     if ((it & 255u) == 0) {
       if (*(volatile uint32_t*)&st->error != kDevOk) return false;
       if (globaltimer() - t0 > limit) {
@@ -199,16 +258,37 @@ __device__ __forceinline__ bool wait_geq(const uint64_t* sem, uint64_t target, R
   }
 }
 
+#if CF_DROP_FENCE == 4
+// mutation 4: a torn packet -- both flags land first, the payload later
+__device__ __forceinline__ void ll16_torn(void* dst, uint2 data, uint32_t flag) {
+  volatile uint32_t* w = reinterpret_cast<volatile uint32_t*>(dst);
+  w[1] = flag;
+  w[3] = flag;
+  CF_STRESS_AT(4);
+  w[0] = data.x;
+  w[2] = data.y;
+}
+#endif
 // LL16: two reference packets {d0, flag, d1, flag} in one 16-byte store.
 __device__ __forceinline__ void ll16_put(void* dst, uint2 data, uint32_t flag) {
+  CF_STRESS_AT(3);
+#if CF_DROP_FENCE == 4
+  ll16_torn(dst, data, flag);
+#else
   st16_volatile(dst, make_uint4(data.x, flag, data.y, flag));
+#endif
 }
 // LL16 put choosing the store by scope: ranks on one GPU meet in its L2, where
 // a plain 16-byte store is already one transaction; across GPUs the store is
 // volatile (not cached, not merged) like the reference's packet writes.
 __device__ __forceinline__ void ll16_put_scoped(void* dst, uint2 data, uint32_t flag, bool gpu) {
+  CF_STRESS_AT(3);
+#if CF_DROP_FENCE == 4
+  ll16_torn(dst, data, flag);
+#else
   if (gpu) st16(dst, make_uint4(data.x, flag, data.y, flag));
   else st16_volatile(dst, make_uint4(data.x, flag, data.y, flag));
+#endif
 }
 // Poll one LL16 packet until both flag words equal `flag`.
 __device__ __forceinline__ uint2 ll16_get(const void* src, uint32_t flag, RankState* st) {

@@ -150,3 +150,63 @@ extern "C" int cftest_spin_stop(void) {
   if (cudaStreamSynchronize(g_spin) != cudaSuccess) return 2;
   return g_flag[1] ? 1 : 0;
 }
+
+// Message-passing litmus test (MP): a producer CTA writes a 64 KiB payload
+// stamped with round i, then publishes flag = i; a consumer CTA on another SM
+// waits for the flag, reads the payload and counts words older than i.
+// `ordered` = 1: every producer thread fences before the barrier and the
+// flag is a release store, the consumer's flag load is an acquire (the
+// handshake of the collective kernels); 0: relaxed stores / loads only (the
+// CF_DROP_FENCE=1/2/3 mutations).  Returns the stale words seen.
+__global__ void mp_litmus(uint32_t* data, uint64_t* flag, uint64_t* ack, int rounds, int ordered, int consumer,
+                          unsigned long long* stale) {
+  const int words = 16384;
+  if (blockIdx.x != 0 && blockIdx.x != consumer) return;
+  unsigned long long bad = 0;
+  for (int i = 1; i <= rounds; i++) {
+    if (blockIdx.x == 0) {   // producer
+      if (threadIdx.x == 0)
+        while (ld_acquire_gpu(ack) < (uint64_t)(i - 1)) {}
+      __syncthreads();
+      for (int k = threadIdx.x; k < words; k += blockDim.x) data[k] = (uint32_t)i;
+      if (ordered) __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        if (ordered) st_release_gpu(flag, (uint64_t)i);
+        else st_relaxed(flag, (uint64_t)i, true);
+      }
+    } else {                 // consumer
+      if (threadIdx.x == 0)
+        while ((ordered ? ld_acquire_gpu(flag) : ld_relaxed(flag, true)) < (uint64_t)i) {}
+      __syncthreads();
+      for (int k = threadIdx.x; k < words; k += blockDim.x) {
+        uint32_t v;
+        asm volatile("ld.global.u32 %0, [%1];" : "=r"(v) : "l"(data + k));
+        bad += v < (uint32_t)i;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) st_release_gpu(ack, (uint64_t)i);
+    }
+  }
+  if (blockIdx.x == consumer && bad) atomicAdd(stale, bad);
+}
+
+extern "C" long long cftest_mp_litmus(int rounds, int ordered, int consumer) {
+  uint32_t* data;
+  uint64_t* sync;
+  unsigned long long* stale;
+  if (cudaMalloc((void**)&data, 16384 * 4) || cudaMalloc((void**)&sync, 256) || cudaMalloc((void**)&stale, 8))
+    return -1;
+  cudaMemset(data, 0, 16384 * 4);
+  cudaMemset(sync, 0, 256);
+  cudaMemset(stale, 0, 8);
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  mp_litmus<<<sms, 512>>>(data, sync, sync + 8, rounds, ordered, consumer, stale);
+  unsigned long long h = 0;
+  if (cudaMemcpy(&h, stale, 8, cudaMemcpyDeviceToHost) != cudaSuccess) return -2;
+  cudaFree(data);
+  cudaFree(sync);
+  cudaFree(stale);
+  return (long long)h;
+}
