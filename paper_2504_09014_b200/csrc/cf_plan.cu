@@ -29,7 +29,7 @@ namespace cf {
 namespace plan {
 cfStatus parse(const char* text, size_t len, int dtype_override, Plan& P);
 const char* op_name(int k);
-const void* plan_kernel_for(int dtype);
+const void* plan_kernel_for(int dtype, int cls);
 
 namespace {
 
@@ -69,7 +69,7 @@ struct Group {
 struct cfPlan {
   cfComm* comm = nullptr;
   cf::plan::Plan ir;
-  int dtype = 0, es = 4, K = 1, threads = 512;
+  int dtype = 0, es = 4, K = 1, threads = CF_PLAN_THREADS;
   int in_buf = -1, out_buf = -1;
   bool input_private = false;
   uint32_t flag_stride = 2;
@@ -84,6 +84,7 @@ struct cfPlan {
   int n_device_ops = 0;
   int window = 1;                     // ops staged per shared-memory window (<= kPlanWindow)
   bool uses_port = false;             // port-channel ops go through the proxy
+  int cls = 3;                        // interpreter class: bit 0 LL packet ops, bit 1 port ops
   bool has_prologue = false;          // per-call zeroing / private input copy
   // one-process-per-GPU: this process runs rank `me`'s programs; the peers'
   // plan heaps are IPC-mapped by cfPlanConnect, which finalizes the plan
@@ -637,12 +638,18 @@ cfStatus load(cfComm* c, const char* json, size_t len, int dtype_override, cfPla
   // of a device co-resident.
   long long max_bytes = 0;
   bool packets = false;   // LL plans: packet ops run one 8-byte payload unit per thread
+  bool port = false;
   for (auto& h : hops)
     for (auto& o : h) {
       if (is_data(o)) max_bytes = std::max(max_bytes, o.size * es);
       packets |= o.code == D_PUT_PACKETS || o.code == D_READ_PACKETS;
+      port |= o.code == D_PORT_PUT || o.code == D_PORT_SIGNAL || o.code == D_PORT_FLUSH;
     }
-  const void* kernel = plan_kernel_for(pl->dtype);
+  // the smallest interpreter class covering every op of the plan (MULTI ops
+  // take packet sources only where the plan has packet ops to fuse)
+  pl->cls = (packets ? 1 : 0) | (port ? 2 : 0);
+  if (const char* ev = getenv("CF_PLAN_CLASS")) pl->cls = atoi(ev);   // diagnostic: force a class
+  const void* kernel = plan_kernel_for(pl->dtype, pl->cls);
   int cap = INT32_MAX, progs_per_dev_max = 1;
   pl->mp = c->multiprocess;
   pl->me = c->local[0].rank;
@@ -1214,7 +1221,7 @@ extern "C" cfStatus cfPlanExecute(cfPlan_t pl, const void* const* inputs, void* 
   }
   int prev = -1;
   cudaGetDevice(&prev);
-  const void* kernel = plan_kernel_for(pl->dtype);
+  const void* kernel = plan_kernel_for(pl->dtype, pl->cls);
   for (size_t gi = 0; gi < pl->groups.size(); gi++) {
     Group& G = pl->groups[gi];
     PlanArgs a;

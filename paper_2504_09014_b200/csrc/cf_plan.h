@@ -10,6 +10,11 @@
 #include "cf_proxy.h"
 #include "device/cf_device.cuh"
 
+// threads per CTA of the plan interpreter (one launch-bounds for the kernel)
+#ifndef CF_PLAN_THREADS
+#define CF_PLAN_THREADS 512
+#endif
+
 namespace cf {
 namespace plan {
 

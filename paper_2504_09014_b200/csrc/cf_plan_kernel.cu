@@ -38,8 +38,14 @@ __device__ __forceinline__ bool is_data_code(uint8_t c) {
   return c == D_MULTI || c == D_COPY || c == D_PUT_PACKETS || c == D_READ_PACKETS || c == D_PORT_PUT;
 }
 
+// ((e - 1) * stride + f) mod (2^32 - 1) + 1 without a 64-bit division
+// (2^32 = 1 mod 2^32 - 1: fold the high word into the low word twice)
 __device__ __forceinline__ uint32_t runtime_flag(uint64_t e, uint32_t stride, uint32_t f) {
-  return (uint32_t)(((e - 1) * (uint64_t)stride + f) % 0xffffffffull) + 1u;
+  const uint64_t x = (e - 1) * (uint64_t)stride + f;
+  uint64_t y = (x >> 32) + (x & 0xffffffffull);
+  y = (y >> 32) + (y & 0xffffffffull);
+  if (y >= 0xffffffffull) y -= 0xffffffffull;
+  return (uint32_t)y + 1u;
 }
 
 // counter barrier: every participant adds 1, then waits for the call's total
@@ -428,8 +434,16 @@ __device__ __forceinline__ void resolve_window(const PlanArgs& a, DevOp* ops, in
   }
 }
 
-template <typename T>
-__global__ void __launch_bounds__(512) plan_kernel(const __grid_constant__ PlanArgs a) {
+// Op classes: one interpreter per class, so a plan runs the smallest body
+// that covers its ops (less register pressure and a smaller instruction
+// footprint on the latency path than one switch over every op kind).
+//   kClsHB   sync ops, MULTI / COPY on plain vectors (memory-channel plans)
+//   kClsLL   + LL packet ops and packet sources of MULTI
+//   kClsAll  + port-channel requests through the proxy
+enum PlanClass { kClsHB = 0, kClsLL = 1, kClsAll = 3 };
+
+template <typename T, int CLS>
+__global__ void __launch_bounds__(CF_PLAN_THREADS) plan_kernel(const __grid_constant__ PlanArgs a) {
   const int pid = blockIdx.x / a.K, j = blockIdx.x % a.K;
   TS_DECL
   TS_MARK();
@@ -473,7 +487,7 @@ __global__ void __launch_bounds__(512) plan_kernel(const __grid_constant__ PlanA
   // rank barriers are numbered consecutively across calls (monotonic counters)
   const uint64_t per_call = (uint64_t)(a.entry_barrier + a.exit_barrier);
   if (a.entry_barrier) rank_barrier(a, rank, (e - 1) * per_call + 1);
-  uint64_t port_last = ~0ull;   // thread 0: this CTA's most recent proxy ticket
+  [[maybe_unused]] uint64_t port_last = ~0ull;   // thread 0: this CTA's most recent proxy ticket
   const int end = pe;
   for (int w0 = pb; w0 < end; w0 += a.window) {
     const int w1 = min(w0 + a.window, end);
@@ -513,19 +527,36 @@ __global__ void __launch_bounds__(512) plan_kernel(const __grid_constant__ PlanA
         break;
       case D_MULTI:
       case D_COPY:
-        data_op<T>(a, op, j, e, rs);
+        if constexpr (CLS == kClsHB) {
+          // plain vectors only in this class: no packet sources
+          uint64_t lo, hi;
+          slice<T>(op.size, a.K, j, lo, hi);
+          constexpr int V = 16 / sizeof(T);
+          const uint64_t full = lo + (hi > lo ? (hi - lo) / V * V : 0);
+          if ((op.flags & F_VEC) && op.code == D_MULTI && op.nsrc <= 8) {
+            if (full > lo) multi_fast<T>(op, lo, full);
+            if (full < hi) data_op_general<T>(op, full, hi, a.flag_stride, e, rs);
+          } else if (lo < hi) {
+            data_op_general<T>(op, lo, hi, a.flag_stride, e, rs);
+          }
+        } else {
+          data_op<T>(a, op, j, e, rs);
+        }
         break;
       case D_PUT_PACKETS:
       case D_READ_PACKETS:
-        packet_op<T>(op, a.K, j, a.flag_stride, e, rs);
+        if constexpr ((CLS & kClsLL) != 0) packet_op<T>(op, a.K, j, a.flag_stride, e, rs);
         break;
       case D_PORT_PUT:
       case D_PORT_SIGNAL:
-        port_op<T>(a, op, rank, pid, j, e, rs, port_last);
+        if constexpr (CLS == kClsAll) port_op<T>(a, op, rank, pid, j, e, rs, port_last);
         break;
       case D_PORT_FLUSH:
-        if (threadIdx.x == 0 && port_last != ~0ull) port_flush(a.port_done + (size_t)pid * a.K + j, port_last, rs);
-        __syncthreads();
+        if constexpr (CLS == kClsAll) {
+          if (threadIdx.x == 0 && port_last != ~0ull)
+            port_flush(a.port_done + (size_t)pid * a.K + j, port_last, rs);
+          __syncthreads();
+        }
         break;
       default:
         break;
@@ -535,7 +566,8 @@ __global__ void __launch_bounds__(512) plan_kernel(const __grid_constant__ PlanA
   }
   // requests still in flight complete before the call ends (their data and
   // signals are part of this call)
-  if (threadIdx.x == 0 && port_last != ~0ull) port_flush(a.port_done + (size_t)pid * a.K + j, port_last, rs);
+  if constexpr (CLS == kClsAll)
+    if (threadIdx.x == 0 && port_last != ~0ull) port_flush(a.port_done + (size_t)pid * a.K + j, port_last, rs);
   if (a.exit_barrier) rank_barrier(a, rank, e * per_call);
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -549,14 +581,22 @@ __global__ void __launch_bounds__(512) plan_kernel(const __grid_constant__ PlanA
   TS_DUMP("plan", rank);
 }
 
-const void* plan_kernel_for(int dtype) {
+template <int CLS>
+static const void* by_dtype(int dtype) {
   switch (dtype) {
-    case 0: return (const void*)plan_kernel<int32_t>;
-    case 1: return (const void*)plan_kernel<float>;
-    case 2: return (const void*)plan_kernel<__half>;
-    case 3: return (const void*)plan_kernel<__nv_bfloat16>;
+    case 0: return (const void*)plan_kernel<int32_t, CLS>;
+    case 1: return (const void*)plan_kernel<float, CLS>;
+    case 2: return (const void*)plan_kernel<__half, CLS>;
+    case 3: return (const void*)plan_kernel<__nv_bfloat16, CLS>;
   }
   return nullptr;
+}
+
+// cls: bit 0 = the plan has LL packet ops, bit 1 = port-channel ops
+const void* plan_kernel_for(int dtype, int cls) {
+  if (cls & 2) return by_dtype<kClsAll>(dtype);
+  if (cls & 1) return by_dtype<kClsLL>(dtype);
+  return by_dtype<kClsHB>(dtype);
 }
 
 }  // namespace plan
