@@ -550,6 +550,85 @@ __global__ void __launch_bounds__(512) push_gather_kernel(const __grid_constant_
   end_call(rk, e);
 }
 
+// K6 bulk: the same direct AllGather on the TMA bulk-copy engine.  One warp
+// per CTA; lane 0 streams the shard through two 32 KiB shared-memory stages
+// -- cp.async.bulk global -> shared (mbarrier complete_tx), then one
+// cp.async.bulk shared -> global store per rank from the same stage -- so a
+// tile is read from HBM once and written n times by the copy engine, with
+// no register staging and one instruction per 32 KiB per destination.
+// Needs a 16-byte-multiple shard and 16-byte-aligned buffers.
+#ifndef CF_BULK_TILE_KB
+#define CF_BULK_TILE_KB 32
+#endif
+constexpr int kBulkTile = CF_BULK_TILE_KB * 1024;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* m, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(m)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* m, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(m)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* m, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(m)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst_smem, const void* src, uint32_t bytes, uint64_t* m) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst_smem)), "l"(src), "r"(bytes), "r"(smem_u32(m)) : "memory");
+}
+__device__ __forceinline__ void bulk_store(void* dst, const void* src_smem, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+               ::"l"(dst), "r"(smem_u32(src_smem)), "r"(bytes) : "memory");
+}
+
+template <typename T>
+__global__ void __launch_bounds__(32) push_gather_bulk_kernel(const __grid_constant__ CollArgs a) {
+  const RankCtx& rk = a.rk[blockIdx.y];
+  const int n = a.n, r = rk.rank;
+  extern __shared__ __align__(128) char sbuf[];   // 2 stages of kBulkTile
+  __shared__ __align__(8) uint64_t mbar[2];
+  const uint64_t e = begin_call(rk);
+  if (!a.single_launch) handshake(rk, n, e * kPhases + 1, false, a.gpu_scope);
+  const size_t sb = a.count * sizeof(T);
+  const size_t ntiles = (sb + kBulkTile - 1) / kBulkTile;
+  if (threadIdx.x == 0) {
+    mbar_init(&mbar[0], 1);
+    mbar_init(&mbar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    const char* src = rk.in[r];
+    auto tile_bytes = [&](size_t t) { return (uint32_t)min((size_t)kBulkTile, sb - t * kBulkTile); };
+    size_t t = blockIdx.x;
+    if (t < ntiles) {
+      mbar_expect_tx(&mbar[0], tile_bytes(t));
+      bulk_load(sbuf, src + t * kBulkTile, tile_bytes(t), &mbar[0]);
+    }
+    for (uint32_t k = 0; t < ntiles; k++, t += gridDim.x) {
+      const int st = k & 1;
+      const size_t tn = t + gridDim.x;
+      if (tn < ntiles) {
+        // the other stage still feeds the stores of tile k-1: wait until they read it
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        mbar_expect_tx(&mbar[st ^ 1], tile_bytes(tn));
+        bulk_load(sbuf + (st ^ 1) * kBulkTile, src + tn * kBulkTile, tile_bytes(tn), &mbar[st ^ 1]);
+      }
+      mbar_wait(&mbar[st], (k >> 1) & 1);
+      for (int p = 0; p < n; p++)
+        bulk_store(rk.out[p] + (size_t)r * sb + t * kBulkTile, sbuf + st * kBulkTile, tile_bytes(t));
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");   // every store performed
+    asm volatile("fence.proxy.async.global;" ::: "memory");      // ... and ordered before generic accesses
+  }
+  __syncwarp();
+  if (!a.single_launch) handshake(rk, n, e * kPhases + 2, true, a.gpu_scope);
+  end_call(rk, e);
+}
+
 // ---------------------------------------------------------------- K5
 
 // NVLS switch primitives (multimem_ld_reduce / multimem_st16) live in
@@ -1290,6 +1369,14 @@ const void* collective_kernel(int kind, int dtype, int n) {
         case 1: return pick_norm<float>(n);
         case 2: return pick_norm<__half>(n);
         case 3: return pick_norm<__nv_bfloat16>(n);
+      }
+      break;
+    case 9:   // K6 bulk (TMA bulk copies)
+      switch (dtype) {
+        case 0: return (const void*)push_gather_bulk_kernel<int32_t>;
+        case 1: return (const void*)push_gather_bulk_kernel<float>;
+        case 2: return (const void*)push_gather_bulk_kernel<__half>;
+        case 3: return (const void*)push_gather_bulk_kernel<__nv_bfloat16>;
       }
       break;
     case 8:   // K5 direct (symmetric buffers)

@@ -43,12 +43,13 @@ void HeapLayout::compute(int nranks, size_t ll_max) {
   total = round_up(scr_off + scr_bytes, 1 << 21);
 }
 
-int occupancy(cfComm* c, const void* kernel, int dev, int threads) {
+int occupancy(cfComm* c, const void* kernel, int dev, int threads, size_t smem) {
   auto key = std::make_pair(kernel, dev * 2048 + threads);   // residency depends on the block size
   auto it = c->occ.find(key);
   if (it != c->occ.end()) return it->second;
   int nb = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, threads, 0) != cudaSuccess) nb = 1;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, threads, smem) != cudaSuccess) nb = 1;
   c->occ[key] = std::max(nb, 1);
   return c->occ[key];
 }
@@ -65,10 +66,10 @@ static int cta_budget(const cfComm* c, int algo) {
   return kNvlinkCtaBudget;
 }
 
-int max_blocks_per_rank(cfComm* c, const void* kernel, int group, int threads, int per_sm, int algo) {
+int max_blocks_per_rank(cfComm* c, const void* kernel, int group, int threads, int per_sm, int algo, size_t smem) {
   const auto& g = c->groups[group];
   const int dev = c->local[g[0]].dev;
-  int occ = occupancy(c, kernel, dev, threads);
+  int occ = occupancy(c, kernel, dev, threads, smem);
   if (per_sm > 0) occ = std::min(occ, per_sm);
   const int cap = occ * c->sm_count[dev];
   // every rank on this device shares its SMs (one launch per device, or one
@@ -162,6 +163,21 @@ static void build_groups(cfComm* c) {
 // Measured crossover table: replaces DEFAULT_THRESHOLDS
 // (cf/collectives.py:418).  Thresholds are per-rank message bytes.  Values
 // come from bench.py sweeps; see DESIGN.md "selector".
+// K6 bulk (TMA bulk copies): tile size of push_gather_bulk_kernel, smallest
+// shard it takes (smaller shards: the register kernel's lower latency)
+#ifndef CF_BULK_TILE_KB
+#define CF_BULK_TILE_KB 32
+#endif
+constexpr size_t kBulkTileBytes = (size_t)CF_BULK_TILE_KB * 1024;
+constexpr size_t kAgBulkMin = (size_t)4 << 20;
+static bool ag_bulk_enabled() {
+  static const bool on = [] {
+    const char* v = getenv("CF_AG_BULK");
+    return !v || atoi(v) != 0;
+  }();
+  return on;
+}
+
 // AUTO picks the in-place NVLS kernel for symmetric buffers from this size up
 // (per rank; provisional until measured on a multicast-capable box)
 constexpr size_t kNvlsAutoBytes = (size_t)1 << 20;
@@ -577,7 +593,8 @@ extern "C" cfStatus cfSelectAlgorithm(cfComm_t c, int coll, size_t nbytes, cfDty
 
 namespace {
 
-enum Kind { kPull = 0, kLL1 = 1, kLL2 = 2, kGather = 3, kNvls = 4, kRing = 5, kRingGather = 6, kNorm = 7 };
+enum Kind { kPull = 0, kLL1 = 1, kLL2 = 2, kGather = 3, kNvls = 4, kRing = 5, kRingGather = 6, kNorm = 7,
+            kGatherBulk = 9 };
 
 struct Job {
   int algo = -1;      // cfAlgo (CF_ALGO_COUNT: K13) -- selects the CTA budget
@@ -591,6 +608,8 @@ struct Job {
   size_t rows = 0, hidden = 0;   // K13
   float eps = 0.f;
   int blocks = 0;     // explicit CTAs per rank (K13: one per row), else from `work`
+  int threads = 0;    // CTA size (0: the configured threads)
+  size_t smem = 0;    // dynamic shared memory per CTA
   size_t win_lo = 0, win_hi = ~(size_t)0;   // pull-reduce window inside each chunk
 };
 
@@ -643,7 +662,7 @@ cfStatus launch(cfComm* c, const Job& j, int dtype, const void* const* send, voi
                 const cudaStream_t* streams, const NormBufs* nb = nullptr) {
   // one-process-per-GPU: peers' buffers come from the registration table
   const bool need_in = j.kind == kPull || j.kind == kNorm;
-  const bool need_out = j.kind == kGather || j.kind == kRingGather ||
+  const bool need_out = j.kind == kGather || j.kind == kGatherBulk || j.kind == kRingGather ||
                         ((j.kind == kPull || j.kind == kNorm || j.kind == kRing) && j.push);
   const bool need_out2 = false;   // K13 writes only its own resid_out (both modes)
   const Registration* reg_in = nullptr;
@@ -670,6 +689,7 @@ cfStatus launch(cfComm* c, const Job& j, int dtype, const void* const* send, voi
   // step): smaller CTAs give each rank up to kRingCtas independent links.
   const bool ring = j.kind == kRing || j.kind == kRingGather;
   int threads = j.kind == kRing ? std::min(c->cfg.threads, 256) : c->cfg.threads;   // ring_kernel's bound
+  if (j.threads) threads = j.threads;
   if (j.kind == kNorm && j.blocks > max_blocks_per_rank(c, kernel, 0, threads, 0, j.algo))
     // K13 rows per rank beyond one resident round: 256-thread CTAs (2 per SM)
     // finish them in one round (b=256: 22.3 -> 20.3 us; fewer rows keep 512)
@@ -734,13 +754,13 @@ cfStatus launch(cfComm* c, const Job& j, int dtype, const void* const* send, voi
     // us); the pull-only variants (K2, K8) gain from full residency at every
     // size (K8 256 MiB 394 -> 354 us, K2 1 MiB 13.4 -> 10.1 us)
     const bool k3_big = j.kind == kPull && j.push && j.count * dtype_size(dtype) > ((size_t)8 << 20);
-    int mb = max_blocks_per_rank(c, kernel, (int)gi, threads, k3_big ? 1 : 0, j.algo);
+    int mb = max_blocks_per_rank(c, kernel, (int)gi, threads, k3_big ? 1 : 0, j.algo, j.smem);
     if (ring) mb = std::min(mb, kRingCtas);   // ring slot region
     int blocks = (int)std::min<size_t>((size_t)mb, std::max<size_t>(1, ceil_div(j.work, (size_t)threads)));
     if (j.blocks) blocks = std::min(mb, j.blocks);
     CF_TRY(join_streams(c, (int)gi, streams, false));
     void* args[] = {&a};
-    CF_CUDA(cudaLaunchKernel(kernel, dim3(blocks, g.size()), dim3(threads), args, 0, streams[g[0]]));
+    CF_CUDA(cudaLaunchKernel(kernel, dim3(blocks, g.size()), dim3(threads), args, j.smem, streams[g[0]]));
     CF_TRY(join_streams(c, (int)gi, streams, true));
   }
   return CF_OK;
@@ -928,6 +948,14 @@ extern "C" cfStatus cfAllGather(cfComm_t c, const void* const* send, void* const
   j.kind = algo == CF_ALGO_RING_AG ? kRingGather : kGather;
   j.count = sendcount;
   j.work = ceil_div(sendcount * dtype_size(dtype), 16);
+  const size_t sb = sendcount * dtype_size(dtype);
+  if (j.kind == kGather && sb % 16 == 0 && sb >= kAgBulkMin && ag_bulk_enabled()) {
+    // whole 16-byte shard of at least kAgBulkMin: the TMA bulk-copy kernel
+    j.kind = kGatherBulk;
+    j.threads = 32;
+    j.smem = 2 * kBulkTileBytes;
+    j.work = ceil_div(sb, kBulkTileBytes) * 32;   // one tile per CTA (32 threads)
+  }
   return launch(c, j, dtype, send, recv, streams);
 }
 

@@ -182,13 +182,14 @@ struct cfComm {
 
 namespace cf {
 // CTAs of `kernel` (launched with `threads`) that may run per SM on `dev`.
-int occupancy(cfComm* c, const void* kernel, int dev, int threads);
+int occupancy(cfComm* c, const void* kernel, int dev, int threads, size_t smem = 0);
 // Driver API function by name (nullptr if unavailable).
 void* driver_fn(const char* name);
 // Co-residency cap: CTAs per rank such that every rank of the group fits at
 // once, further capped by the algorithm's CTA budget (cfCommSetCtaBudget;
 // algo -1 = none, CF_ALGO_COUNT = the fused K13 kernel).
-int max_blocks_per_rank(cfComm* c, const void* kernel, int group, int threads, int per_sm = 0, int algo = -1);
+int max_blocks_per_rank(cfComm* c, const void* kernel, int group, int threads, int per_sm = 0, int algo = -1,
+                        size_t smem = 0);
 // Default CTA budget per rank when every rank has its own GPU (NVLink-bound
 // collectives): well under half the SMs, so a concurrent compute kernel
 // holding half of them cannot leave a collective partially resident.
