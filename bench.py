@@ -232,6 +232,13 @@ def time_coll(world, kind, send, recv, count, dtype, algo, iters, warmup, flush=
     return t
 
 
+
+def algo_id(name):
+    """libcf algorithm id; "<ring algo>+ring" = the literal ring transport (cf.h CF_ALGO_RING_LINKS)."""
+    from paper_2504_09014_b200 import _lib
+    base, _, links = name.partition("+")
+    return _lib.ALGOS[base] | (_lib.CF_ALGO_RING_LINKS if links else 0)
+
 def time_plan(rt, send, recv, iters, warmup, flush, reps=3):
     """time_graph of one plan execution (K10) on every rank."""
     t = time_graph(rt.world.device(0), lambda: rt.run_raw(send, recv), iters, warmup, flush, reps)
@@ -252,17 +259,19 @@ def run_ag_rs(w, flush, send, recv):
             continue
         iters = 20 if nb <= 16 * MiB else 5
         fl = flush if nb < 64 * MiB else None
-        for name in ("allpairs_ag", "ring_ag"):
+        for name in ("allpairs_ag", "ring_ag", "ring_ag+ring"):
             t = time_coll(w, "allgather", [s[:shard] for s in send], [r[:shard * n] for r in recv], shard,
-                          "bf16", _lib.ALGOS[name], iters, 3, fl)
+                          "bf16", algo_id(name), iters, 3, fl)
             row["ag_" + name] = {"us": round(t * 1e6, 2), "busbw": round(nb / t / 1e9 * (n - 1) / n, 2)}
-        for name in ("rs_direct", "ring_rs"):
+        for name in ("rs_direct", "ring_rs", "ring_rs+ring"):
             t = time_coll(w, "reducescatter", [s[:shard * n] for s in send], [r[:shard] for r in recv], shard,
-                          "bf16", _lib.ALGOS[name], iters, 3, fl)
+                          "bf16", algo_id(name), iters, 3, fl)
             row["rs_" + name] = {"us": round(t * 1e6, 2), "busbw": round(nb / t / 1e9 * (n - 1) / n, 2)}
         rows.append(row)
     return {"config": "C2/RS: AllGather (S = output bytes) and ReduceScatter (S = input bytes), bf16, "
-                      "8 co-resident ranks", "rows": rows}
+                      "8 co-resident ranks; ring_ag / ring_rs = the reference's ring algorithms (same bytes / "
+                      "ring accumulation order) on the all-pairs transport, '+ring' = the literal ring kernels",
+            "rows": rows}
 
 
 def run_fused(w, flush):
@@ -431,12 +440,12 @@ def run_sweep(w, args):
     for nb in sizes:
         count = nb // 2
         row = {"bytes": nb}
-        for name in ("auto", "1pa", "2pa_ll", "2pa", "1pa_hb"):
+        for name in ("auto", "1pa", "2pa_ll", "2pa", "1pa_hb", "2pr", "2pr+ring"):
             if name in ("1pa", "2pa_ll") and nb > ll_max:
                 continue
             if name == "1pa_hb" and nb > 64 * MiB:
                 continue
-            aid = _lib.ALGOS[name]
+            aid = algo_id(name)
             iters = 20 if nb <= 16 * MiB else 5
             t = time_coll(w, "allreduce", [s[:count] for s in send], [r[:count] for r in recv],
                           count, "bf16", aid, iters, 3, flush if nb < 64 * MiB else None)
@@ -532,7 +541,7 @@ def multi_parity(comm, dev, rank, world, nvls, sym_mode=-1):
     y = torch.empty_like(x)
     comm.register(x)
     comm.register(y)
-    algos = [("1pa", "1pa"), ("2pa_ll", "2pa"), ("2pa", "2pa")]
+    algos = [("1pa", "1pa"), ("2pa_ll", "2pa"), ("2pa", "2pa"), ("2pr", "2pr")]
     for name, oname in algos:
         try:
             y.zero_()
@@ -581,10 +590,10 @@ def multi_parity(comm, dev, rank, world, nvls, sym_mode=-1):
     ys = torch.empty(shard * world, device=dev, dtype=xs.dtype)
     comm.register(xs)
     comm.register(ys)
-    for name in ("allpairs_ag", "ring_ag"):
+    for name in ("allpairs_ag", "ring_ag", "ring_ag+ring"):
         try:
             ys.zero_()
-            comm.all_gather(xs, ys, algo=name)
+            comm.all_gather(xs, ys, algo=name.split("+")[0], variant="ring" if "+" in name else "")
             torch.cuda.synchronize(dev)
             res["allgather_" + name] = bool(np.array_equal(host(ys), oracle.allgather(sh)[rank]))
         except Exception as e:
@@ -598,9 +607,9 @@ def multi_parity(comm, dev, rank, world, nvls, sym_mode=-1):
     yr = torch.empty(shard, device=dev, dtype=xr.dtype)
     comm.register(xr)
     comm.register(yr)
-    for name in ("rs_direct", "ring_rs"):
+    for name in ("rs_direct", "ring_rs", "ring_rs+ring"):
         try:
-            comm.reduce_scatter(xr, yr, algo=name)
+            comm.reduce_scatter(xr, yr, algo=name.split("+")[0], variant="ring" if "+" in name else "")
             torch.cuda.synchronize(dev)
             want = oracle.reducescatter(rin, "2pa" if name == "rs_direct" else "ring_rs", "bf16")[rank]
             res["reducescatter_" + name] = bool(np.array_equal(host(yr), want[:shard]))

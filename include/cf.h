@@ -93,6 +93,21 @@ typedef enum {
   CF_ALGO_COUNT = 10
 } cfAlgo;
 
+/*
+ * Transport of the ring algorithms (CF_ALGO_2PR, CF_ALGO_RING_RS,
+ * CF_ALGO_RING_AG).  The reference moves their data around a ring of
+ * PortChannels (cf/collectives.py:30-136).  What a caller observes is the
+ * padding (2n for ring_rs / 2pr, cf/collectives.py:497-504) and the
+ * accumulation order (0 + x[c] + x[c+1] + ... for chunk c); on one NVSwitch
+ * domain every GPU reaches every peer at full bandwidth, so by default these
+ * algorithms run all-pairs -- rank r pulls chunk r from every peer and adds it
+ * in ring order (K3/K8 with the ring order), AllGather stores direct (K6) --
+ * with bit-identical results and no per-step ring chain.  OR this flag into
+ * the algorithm to run the literal ring over point-to-point links instead
+ * (K9 / K12 ring_kernel, K7 ring_gather_kernel).
+ */
+#define CF_ALGO_RING_LINKS 0x100
+
 typedef struct cfComm* cfComm_t;
 typedef struct cfPlan* cfPlan_t;
 

@@ -25,6 +25,7 @@ ALGOS = {
     "allpairs_ag": 6, "ring_ag": 7, "ring_rs": 8, "rs_direct": 9,
 }
 ALGO_NAMES = {v: k for k, v in ALGOS.items()}
+CF_ALGO_RING_LINKS = 0x100   # cf.h: OR into 2pr / ring_rs / ring_ag for the literal ring transport
 CF_ALGO_COUNT = 10   # cfAlgo count; also the CTA-budget slot of the fused K13 kernel
 CF_PLAN_HANDLE_BYTES = 128
 

@@ -143,12 +143,20 @@ def _algo_id(kind: str, name: str, variant: str) -> int:
         key = name
     if key not in _lib.ALGOS or key == "auto":
         raise NoAlgoError(f"unknown algorithm {name!r}")
+    links = 0
+    if key in ("2pr", "ring_rs", "ring_ag"):
+        # variant "ring" (extension): the literal ring over point-to-point
+        # links; "" runs the same order and padding all-pairs (cf.h
+        # CF_ALGO_RING_LINKS) -- identical results
+        if variant not in ("", "ring"):
+            raise NoAlgoError(f"unknown {key} variant {variant!r}")
+        links = _lib.CF_ALGO_RING_LINKS if variant == "ring" else 0
     ok = {"allreduce": {"1pa", "1pa_hb", "2pa", "2pa_ll", "switch_2pa", "2pr"},
           "allgather": {"allpairs_ag", "ring_ag"},
           "reducescatter": {"ring_rs", "rs_direct"}}[kind]
     if key not in ok:
         raise NoAlgoError(f"{name!r} is not a {kind} algorithm")
-    return _lib.ALGOS[key]
+    return _lib.ALGOS[key] | links
 
 
 def _padded(elems: int, multiple: int) -> int:
@@ -269,7 +277,8 @@ def collective(kind: str, inputs, world, selector: Selector | None = None, dtype
         d = sel.select(kind, nbytes, world.topology, world=world, dtype=dtype)
         name, var = d.name, d.variant
     aid = _algo_id(kind, name, var)
-    mult = required_multiple(_lib.ALGO_NAMES[aid] if _lib.ALGO_NAMES[aid] != "2pa_ll" else "2pa", n)
+    base = _lib.ALGO_NAMES[aid & ~_lib.CF_ALGO_RING_LINKS]
+    mult = required_multiple(base if base != "2pa_ll" else "2pa", n)
 
     if host_tensors and kind == "allreduce" and elems and not (via_plan or (name == "2pa" and var == "port")):
         # host in, host out through libcf's pipelined host path (copies overlap the kernel)

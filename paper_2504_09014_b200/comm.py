@@ -124,18 +124,17 @@ class Communicator:
         self._call(_lib.lib().cfAllReduce, send, recv, send.numel(), aid, stream)
         return recv
 
-    def all_gather(self, send, recv=None, algo: str = "auto", stream=None):
-        import torch
+    def all_gather(self, send, recv=None, algo: str = "auto", stream=None, variant: str = ""):
         recv = send.new_empty(send.numel() * self.nranks) if recv is None else recv
-        aid = -1 if algo == "auto" else _algo_id("allgather", algo, "")
+        aid = -1 if algo == "auto" else _algo_id("allgather", algo, variant)
         self._call(_lib.lib().cfAllGather, send, recv, send.numel(), aid, stream)
         return recv
 
-    def reduce_scatter(self, send, recv=None, algo: str = "auto", stream=None):
+    def reduce_scatter(self, send, recv=None, algo: str = "auto", stream=None, variant: str = ""):
         if send.numel() % self.nranks:
             raise ShapeError("reduce_scatter input must hold nranks equal shards")
         recv = send.new_empty(send.numel() // self.nranks) if recv is None else recv
-        aid = -1 if algo == "auto" else _algo_id("reducescatter", algo, "")
+        aid = -1 if algo == "auto" else _algo_id("reducescatter", algo, variant)
         self._call(_lib.lib().cfReduceScatter, send, recv, recv.numel(), aid, stream)
         return recv
 

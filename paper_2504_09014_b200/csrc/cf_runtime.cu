@@ -858,6 +858,18 @@ cfStatus nvls_direct(cfComm* c, size_t count, int dtype, long long oi, long long
   return CF_OK;
 }
 
+// Strip CF_ALGO_RING_LINKS off `algo`: true when the caller asked for the
+// literal ring transport (only meaningful for the three ring algorithms).
+cfStatus split_links(int& algo, bool& links) {
+  links = algo != CF_ALGO_AUTO && (algo & CF_ALGO_RING_LINKS);
+  if (links) {
+    algo &= ~CF_ALGO_RING_LINKS;
+    if (algo != CF_ALGO_2PR && algo != CF_ALGO_RING_RS && algo != CF_ALGO_RING_AG)
+      return fail(CF_E_NO_ALGO, "CF_ALGO_RING_LINKS applies to 2pr / ring_rs / ring_ag only (algo %d)", algo);
+  }
+  return CF_OK;
+}
+
 }  // namespace
 
 extern "C" cfStatus cfAllReduce(cfComm_t c, const void* const* send, void* const* recv, size_t count,
@@ -868,6 +880,8 @@ extern "C" cfStatus cfAllReduce(cfComm_t c, const void* const* send, void* const
   const int n = c->nranks;
   const size_t es = dtype_size(dtype), V = 16 / es;
   const size_t bytes = count * es;
+  bool links = false;
+  CF_TRY(split_links(algo, links));
   long long oi = -1, oo = -1;
   const bool sym_switch = sym_switch_ok(c, send, recv, bytes, &oi, &oo);
   if (algo == CF_ALGO_AUTO) {
@@ -913,7 +927,10 @@ extern "C" cfStatus cfAllReduce(cfComm_t c, const void* const* send, void* const
       break;
     }
     case CF_ALGO_2PR:
-      j.kind = kRing;
+      // ring order (0 + x_c + x_{c+1} + ...) on the reference's 2n-padded
+      // chunks; all-pairs by default (see CF_ALGO_RING_LINKS)
+      j.kind = links ? kRing : kPull;
+      j.order = kRingZero;
       j.push = 1;
       j.cs = round_up(count, 2 * n) / n;
       j.work = ceil_div(j.cs, V) + 1;
@@ -940,12 +957,16 @@ extern "C" cfStatus cfAllGather(cfComm_t c, const void* const* send, void* const
   CF_TRY(check_ptrs(c, send, recv, streams));
   if ((int)dtype < 0 || (int)dtype > 3) return fail(CF_E_SHAPE, "unknown dtype %d", (int)dtype);
   if (sendcount == 0) return CF_OK;
+  bool links = false;
+  CF_TRY(split_links(algo, links));
   if (algo == CF_ALGO_AUTO) algo = select_algo(c, 1, sendcount * dtype_size(dtype) * c->nranks, dtype);
   if (algo != CF_ALGO_ALLPAIRS_AG && algo != CF_ALGO_RING_AG)
     return fail(CF_E_NO_ALGO, "algorithm %d is not an AllGather algorithm", algo);
   Job j;
   j.algo = algo;
-  j.kind = algo == CF_ALGO_RING_AG ? kRingGather : kGather;
+  // ring_ag: the same bytes land in the same places either way; direct
+  // stores by default (see CF_ALGO_RING_LINKS)
+  j.kind = links ? kRingGather : kGather;
   j.count = sendcount;
   j.work = ceil_div(sendcount * dtype_size(dtype), 16);
   const size_t sb = sendcount * dtype_size(dtype);
@@ -966,14 +987,18 @@ extern "C" cfStatus cfReduceScatter(cfComm_t c, const void* const* send, void* c
   if (recvcount == 0) return CF_OK;
   const int n = c->nranks;
   const size_t es = dtype_size(dtype);
+  bool links = false;
+  CF_TRY(split_links(algo, links));
   if (algo == CF_ALGO_AUTO) algo = select_algo(c, 2, recvcount * es * n, dtype);
   if (algo != CF_ALGO_RS_DIRECT && algo != CF_ALGO_RING_RS)
     return fail(CF_E_NO_ALGO, "algorithm %d is not a ReduceScatter algorithm", algo);
   Job j;
   j.algo = algo;
-  j.kind = algo == CF_ALGO_RING_RS ? kRing : kPull;
+  // ring_rs: rank r pulls chunk r from every peer in ring order (0 + x_r +
+  // x_{r+1} + ...) unless the literal ring was asked for
+  j.kind = links ? kRing : kPull;
   j.rs_shift = 1;
-  j.order = kLead;
+  j.order = algo == CF_ALGO_RING_RS ? kRingZero : kLead;
   j.count = recvcount * n;
   j.cs = recvcount;
   j.work = ceil_div(recvcount, 16 / es) + 1;
@@ -1135,7 +1160,10 @@ static cfStatus host_allreduce(cfComm* c, const void* const* hsend, void* const*
   const size_t es = dtype_size(dtype), V = 16 / es;
   const size_t bytes = count * es;
   if (algo == CF_ALGO_AUTO) algo = select_algo(c, 0, bytes, dtype);
-  const size_t padded = round_up(count, (size_t)n);
+  // the two-shot pulls (2pa, all-pairs 2pr) pipeline: windows keep each
+  // element's owner and accumulation order
+  const bool pull2 = algo == CF_ALGO_2PA || algo == CF_ALGO_2PR;
+  const size_t padded = round_up(count, (size_t)(algo == CF_ALGO_2PR ? 2 * n : n));
   if (c->pipes.empty()) {
     c->pipes.resize(c->groups.size());
     for (size_t gi = 0; gi < c->groups.size(); gi++) {
@@ -1152,7 +1180,7 @@ static cfStatus host_allreduce(cfComm* c, const void* const* hsend, void* const*
     }
   }
   // pipeline only the two-shot HB kernel (windows keep each element's owner)
-  const bool pipelined = algo == CF_ALGO_2PA && bytes >= ((size_t)32 << 20);
+  const bool pipelined = pull2 && bytes >= ((size_t)32 << 20);
   const size_t cs = padded / n;
   size_t pieces = 1, q = cs;
   if (pipelined) {
@@ -1192,10 +1220,10 @@ static cfStatus host_allreduce(cfComm* c, const void* const* hsend, void* const*
     }
     if (pipelined) {
       Job j;
-      j.algo = CF_ALGO_2PA;
+      j.algo = algo;
       j.kind = kPull;
       j.push = 1;
-      j.order = kLead;
+      j.order = algo == CF_ALGO_2PA ? kLead : kRingZero;
       j.count = count;
       j.cs = cs;
       j.win_lo = w0;

@@ -25,7 +25,7 @@ from inputs import gen_inputs  # noqa: E402
 from oracle import oracle  # noqa: E402
 
 AR = [("1pa", "", "1pa"), ("2pa", "ll", "2pa"), ("2pa", "", "2pa"), ("1pa_hb", "", "1pa"),
-      ("switch_2pa", "", "switch_2pa"), ("2pr", "", "2pr")]
+      ("switch_2pa", "", "switch_2pa"), ("2pr", "ring", "2pr")]   # "ring": the literal ring kernel
 SIZES = (4099, 65536 + 24, 8 * 32768)
 
 
@@ -104,7 +104,8 @@ def _inproc_loop(w, n, iters, out):
             sh = gen_inputs(n, elems // n + 1, "i32", "bits", 7 * it + elems)
             for algo in ("allpairs_ag", "ring_ag"):
                 try:
-                    got = collective("allgather", sh, w, dtype="i32", algo=algo)
+                    got = collective("allgather", sh, w, dtype="i32", algo=algo,
+                                     variant="ring" if algo == "ring_ag" else "")
                     _record(out, f"{algo}:{elems}:{it}",
                             all(np.array_equal(g, x) for g, x in zip(got, oracle.allgather(sh))))
                 except DeadlockError:
@@ -112,7 +113,8 @@ def _inproc_loop(w, n, iters, out):
             rs = gen_inputs(n, 2 * n * (elems // (2 * n) + 1), "i32", "int", 11 * it + elems)
             for algo, oname in (("rs_direct", "2pa"), ("ring_rs", "ring_rs")):
                 try:
-                    got = collective("reducescatter", rs, w, dtype="i32", algo=algo)
+                    got = collective("reducescatter", rs, w, dtype="i32", algo=algo,
+                                     variant="ring" if algo == "ring_rs" else "")
                     want = oracle.reducescatter(rs, oname, "i32")
                     _record(out, f"{algo}:{elems}:{it}", all(np.array_equal(g, x) for g, x in zip(got, want)))
                 except DeadlockError:
@@ -161,7 +163,7 @@ def _mp_loop(comm, rank, world, iters, out):
             ag = comm.alloc_symmetric(world * elems, torch.int32)
             for algo in ("allpairs_ag", "ring_ag"):
                 try:
-                    comm.all_gather(x, ag, algo=algo)
+                    comm.all_gather(x, ag, algo=algo, variant="ring" if algo == "ring_ag" else "")
                     comm.check_device_error()
                     _record(out, f"{algo}:{elems}:{it}", np.array_equal(ag.cpu().numpy(),
                                                                         oracle.allgather(ins)[rank]))

@@ -5,6 +5,8 @@ import ctypes
 import os
 import re
 
+import pytest
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
@@ -70,3 +72,27 @@ def test_config_rejects_threads_beyond_launch_bounds():
         devs = (ctypes.c_int * 2)(0, 0)
         st = lib.cfCommInitAll(ctypes.byref(comm), 2, devs, ctypes.byref(cfg))
         assert errors.STATUS_CODES[st] == "E_CONFIG", threads
+
+
+def test_algo_ids_and_ring_transport_flag_match_header():
+    """cfAlgo values and CF_ALGO_RING_LINKS in include/cf.h equal the Python
+    table; variant "ring" of the three ring algorithms sets the flag, ""
+    leaves it clear (all-pairs transport, same order and padding), any other
+    variant is rejected like the reference rejects unknown variants."""
+    import re
+    from paper_2504_09014_b200 import _lib
+    from paper_2504_09014_b200.collectives import _algo_id
+    from paper_2504_09014_b200.errors import NoAlgoError
+    hdr = open(os.path.join(ROOT, "include", "cf.h")).read()
+    vals = {m.group(1).lower(): int(m.group(2)) for m in re.finditer(r"CF_ALGO_(\w+) = (-?\d+)", hdr)}
+    for name, v in _lib.ALGOS.items():
+        assert vals[name] == v, name
+    flag = int(re.search(r"#define CF_ALGO_RING_LINKS (0x[0-9a-f]+)", hdr).group(1), 16)
+    assert flag == _lib.CF_ALGO_RING_LINKS
+    for kind, name in (("allreduce", "2pr"), ("reducescatter", "ring_rs"), ("allgather", "ring_ag")):
+        assert _algo_id(kind, name, "") == _lib.ALGOS[name]
+        assert _algo_id(kind, name, "ring") == _lib.ALGOS[name] | flag
+        with pytest.raises(NoAlgoError):
+            _algo_id(kind, name, "port")
+    with pytest.raises(NoAlgoError):
+        _algo_id("allreduce", "2pa", "ring")

@@ -49,8 +49,15 @@ def test_gpu_matches_reference_bits(case):
     assert [_digest(o) for o in outs] == case["digests"]
 
 
+def _aid(name):
+    """libcf algorithm id; "+ring" = the literal ring transport (CF_ALGO_RING_LINKS)."""
+    from paper_2504_09014_b200 import _lib
+    base, _, links = name.partition("+")
+    return _lib.ALGOS[base] | (_lib.CF_ALGO_RING_LINKS if links else 0)
+
+
 ALGOS = [("1pa", ""), ("1pa_hb", ""), ("2pa", "memory"), ("2pa", "ll"), ("switch_2pa", ""),
-         ("2pr", "")]
+         ("2pr", ""), ("2pr", "ring")]
 _ORACLE_NAME = {"1pa_hb": "1pa"}
 
 
@@ -98,13 +105,13 @@ def test_odd_rank_counts_vs_oracle(n, dtype):
             want = oracle.allreduce(ins, _ORACLE_NAME.get(algo, algo), dtype)
             for r in range(n):
                 assert np.array_equal(got[r].view(np.uint8), want[r].view(np.uint8)), (elems, algo, var, r)
-        for algo in ("ring_rs", "rs_direct"):
-            got = collective("reducescatter", ins, world(n), dtype=dtype, algo=algo)
+        for algo, var in (("ring_rs", ""), ("ring_rs", "ring"), ("rs_direct", "")):
+            got = collective("reducescatter", ins, world(n), dtype=dtype, algo=algo, variant=var)
             want = oracle.reducescatter(ins, "ring_rs" if algo == "ring_rs" else "direct", dtype)
             for r in range(n):
                 assert np.array_equal(got[r].view(np.uint8), want[r].view(np.uint8)), (elems, algo, r)
-        for algo in ("allpairs_ag", "ring_ag"):
-            got = collective("allgather", ins, world(n), dtype=dtype, algo=algo)
+        for algo, var in (("allpairs_ag", ""), ("ring_ag", ""), ("ring_ag", "ring")):
+            got = collective("allgather", ins, world(n), dtype=dtype, algo=algo, variant=var)
             for g, wnt in zip(got, oracle.allgather(ins)):
                 assert np.array_equal(g.view(np.uint8), wnt.view(np.uint8)), (elems, algo)
     world(n).check_device_error()
@@ -117,13 +124,13 @@ def test_reducescatter_allgather_vs_oracle(n, dtype, elems):
     from paper_2504_09014_b200 import collective
     dist = "wide" if dtype == "f32" else "normal"
     ins = gen_inputs(n, elems, dtype, dist, 7 * n + elems % 13)
-    for algo in ("ring_rs", "rs_direct"):
-        got = collective("reducescatter", ins, world(n), dtype=dtype, algo=algo)
+    for algo, var in (("ring_rs", ""), ("ring_rs", "ring"), ("rs_direct", "")):
+        got = collective("reducescatter", ins, world(n), dtype=dtype, algo=algo, variant=var)
         want = oracle.reducescatter(ins, "ring_rs" if algo == "ring_rs" else "direct", dtype)
         for r in range(n):
             assert np.array_equal(got[r].view(np.uint8), want[r].view(np.uint8)), (algo, r)
-    for algo in ("allpairs_ag", "ring_ag"):
-        got = collective("allgather", ins, world(n), dtype=dtype, algo=algo)
+    for algo, var in (("allpairs_ag", ""), ("ring_ag", ""), ("ring_ag", "ring")):
+        got = collective("allgather", ins, world(n), dtype=dtype, algo=algo, variant=var)
         for g, wnt in zip(got, oracle.allgather(ins)):
             assert np.array_equal(g.view(np.uint8), wnt.view(np.uint8)), algo
 
@@ -153,10 +160,10 @@ def test_repeated_calls_reuse_scratch_and_semaphores():
     rng = np.random.default_rng(3)
     for it in range(60):
         elems = int(rng.choice([1, 33, 1024, 8192, 70000]))
-        algo = ["1pa", "2pa", "2pa_ll", "1pa_hb", "2pr"][it % 5]
+        algo = ["1pa", "2pa", "2pa_ll", "1pa_hb", "2pr", "2pr+ring"][it % 6]
         vals = [torch.full((elems,), float(r + it), device=w.device(r)) for r in range(n)]
         outs = [torch.empty_like(v) for v in vals]
-        C.run("allreduce", vals, outs, elems, "f32", _lib.ALGOS[algo], w)
+        C.run("allreduce", vals, outs, elems, "f32", _aid(algo), w)
         w.synchronize()
         want = float(sum(r + it for r in range(n)))
         for o in outs:
@@ -175,14 +182,14 @@ def test_allreduce_in_place_vs_oracle(elems):
     n = 8
     w = world(n)
     ins = gen_inputs(n, elems, "bf16", "normal", 900 + elems % 89)
-    for algo in ("2pa", "2pr", "1pa", "2pa_ll"):
+    for algo in ("2pa", "2pr", "2pr+ring", "1pa", "2pa_ll"):
         if algo in ("1pa", "2pa_ll") and elems > (1 << 18):
             continue
-        want = oracle.allreduce(ins, "2pa" if algo == "2pa_ll" else algo, "bf16")
+        want = oracle.allreduce(ins, {"2pa_ll": "2pa", "2pr+ring": "2pr"}.get(algo, algo), "bf16")
         for rep in range(2):   # twice: the second call reuses slots / flags
             bufs = [torch.from_numpy(x.view(np.int16)).to(w.device(r)).view(torch.bfloat16)
                     for r, x in enumerate(ins)]
-            C.run("allreduce", bufs, bufs, elems, "bf16", _lib.ALGOS[algo], w)
+            C.run("allreduce", bufs, bufs, elems, "bf16", _aid(algo), w)
             w.synchronize()
             for r in range(n):
                 got = bufs[r].view(torch.int16).cpu().numpy().view(np.uint16)
@@ -201,9 +208,9 @@ def test_large_allreduce_property():
     send = [torch.randint(-8, 8, (elems,), device=w.device(r), dtype=torch.int32)
             .to(torch.bfloat16) for r in range(n)]
     want = sum(s.float() for s in send)
-    for algo in ("2pa", "switch_2pa", "2pr"):
+    for algo in ("2pa", "switch_2pa", "2pr", "2pr+ring"):
         recv = [torch.empty_like(s) for s in send]
-        C.run("allreduce", send, recv, elems, "bf16", _lib.ALGOS[algo], w)
+        C.run("allreduce", send, recv, elems, "bf16", _aid(algo), w)
         w.synchronize()
         for o in recv:
             assert torch.equal(o.float(), want), algo
@@ -456,13 +463,13 @@ def test_one_launch_per_rank_path(monkeypatch):
                 for r in range(n):
                     assert np.array_equal(got[r].view(np.uint8), want[r].view(np.uint8)), (algo, var, r)
             assert len(w._rank_streams) == n   # the per-rank launch path is the one that ran
-            for algo in ("ring_rs", "rs_direct"):
-                got = collective("reducescatter", ins, w, dtype=dtype, algo=algo)
+            for algo, var in (("ring_rs", ""), ("ring_rs", "ring"), ("rs_direct", "")):
+                got = collective("reducescatter", ins, w, dtype=dtype, algo=algo, variant=var)
                 want = oracle.reducescatter(ins, "ring_rs" if algo == "ring_rs" else "direct", dtype)
                 for r in range(n):
                     assert np.array_equal(got[r].view(np.uint8), want[r].view(np.uint8)), (algo, r)
-            for algo in ("allpairs_ag", "ring_ag"):
-                got = collective("allgather", ins, w, dtype=dtype, algo=algo)
+            for algo, var in (("allpairs_ag", ""), ("ring_ag", ""), ("ring_ag", "ring")):
+                got = collective("allgather", ins, w, dtype=dtype, algo=algo, variant=var)
                 for g, wnt in zip(got, oracle.allgather(ins)):
                     assert np.array_equal(g.view(np.uint8), wnt.view(np.uint8)), algo
         # K13, both algorithms (residual output is the oracle sum + residual, bit for bit)

@@ -13,6 +13,14 @@ import torch.multiprocessing as mp
 pytestmark = pytest.mark.gpu
 
 
+
+def _nv(algo):
+    """(name, variant): "2pa_ll" = two-shot LL; "<ring algo>+ring" = the literal ring transport."""
+    if algo == "2pa_ll":
+        return "2pa", "ll"
+    name, _, links = algo.partition("+")
+    return name, links
+
 def _free_port():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
@@ -39,23 +47,23 @@ def _worker(rank, world, port, q):
             recv = torch.empty_like(send)
             comm.register(send)
             comm.register(recv)
-            for algo in ("1pa", "2pa", "2pa_ll", "1pa_hb", "2pr"):
-                name, var = (algo, "") if algo != "2pa_ll" else ("2pa", "ll")
+            for algo in ("1pa", "2pa", "2pa_ll", "1pa_hb", "2pr", "2pr+ring"):
+                name, var = _nv(algo)
                 comm.all_reduce(send, recv, algo=name, variant=var)
                 torch.cuda.synchronize()
                 out[("ar", algo, elems)] = recv.cpu().numpy().copy()
             ag = torch.empty(world * elems, device="cuda", dtype=torch.float32)
             comm.register(ag)
-            for algo in ("allpairs_ag", "ring_ag"):
+            for algo in ("allpairs_ag", "ring_ag", "ring_ag+ring"):
                 ag.zero_()
-                comm.all_gather(send, ag, algo=algo)
+                comm.all_gather(send, ag, algo=_nv(algo)[0], variant=_nv(algo)[1])
                 torch.cuda.synchronize()
                 out[("ag", algo, elems)] = ag.cpu().numpy().copy()
             rs_in = torch.from_numpy(np.concatenate([ins[rank]] * world)).cuda()
             rs_out = torch.empty(elems, device="cuda", dtype=torch.float32)
             comm.register(rs_in)
-            for algo in ("rs_direct", "ring_rs"):
-                comm.reduce_scatter(rs_in, rs_out, algo=algo)
+            for algo in ("rs_direct", "ring_rs", "ring_rs+ring"):
+                comm.reduce_scatter(rs_in, rs_out, algo=_nv(algo)[0], variant=_nv(algo)[1])
                 torch.cuda.synchronize()
                 out[("rs", algo, elems)] = rs_out.cpu().numpy().copy()
             for t in (send, recv, ag, rs_in):
@@ -120,8 +128,8 @@ def test_two_processes_one_gpu_all_collectives():
         p.join(timeout=60)
     for elems in (1000, 65536 + 8):
         ins = gen_inputs(world, elems, "f32", "wide", 77 + elems)
-        for algo in ("1pa", "2pa", "2pa_ll", "1pa_hb", "2pr"):
-            want = oracle.allreduce(ins, {"2pa_ll": "2pa", "1pa_hb": "1pa"}.get(algo, algo), "f32")
+        for algo in ("1pa", "2pa", "2pa_ll", "1pa_hb", "2pr", "2pr+ring"):
+            want = oracle.allreduce(ins, {"2pa_ll": "2pa", "1pa_hb": "1pa", "2pr+ring": "2pr"}.get(algo, algo), "f32")
             for r in range(world):
                 assert np.array_equal(res[r][("ar", algo, elems)].view(np.uint32),
                                       want[r].view(np.uint32)), (algo, r, elems)
@@ -130,10 +138,11 @@ def test_two_processes_one_gpu_all_collectives():
         rs_want = oracle.reducescatter(rs_ins, "direct", "f32")
         rs_ring = oracle.reducescatter(rs_ins, "ring_rs", "f32")
         for r in range(world):
-            for algo in ("allpairs_ag", "ring_ag"):
+            for algo in ("allpairs_ag", "ring_ag", "ring_ag+ring"):
                 assert np.array_equal(res[r][("ag", algo, elems)], cat), (algo, r)
             assert np.array_equal(res[r][("rs", "rs_direct", elems)].view(np.uint32), rs_want[r].view(np.uint32))
-            assert np.array_equal(res[r][("rs", "ring_rs", elems)].view(np.uint32), rs_ring[r].view(np.uint32))
+            for algo in ("ring_rs", "ring_rs+ring"):
+                assert np.array_equal(res[r][("rs", algo, elems)].view(np.uint32), rs_ring[r].view(np.uint32))
     hins = gen_inputs(world, (40 << 20) // 4 + 3, "f32", "uniform", 9)
     hwant = oracle.allreduce(hins, "2pa", "f32")
     hsmall = oracle.allreduce([x[:1000] for x in hins], "2pa", "f32")
@@ -265,8 +274,8 @@ def _worker4(rank, world, port, q):
         ag = torch.empty(world * elems, device="cuda", dtype=torch.bfloat16)
         for t in (send, recv, ag):
             comm.register(t)
-        for algo in ("1pa", "2pa", "2pa_ll", "2pr"):
-            name, var = (algo, "") if algo != "2pa_ll" else ("2pa", "ll")
+        for algo in ("1pa", "2pa", "2pa_ll", "2pr", "2pr+ring"):
+            name, var = _nv(algo)
             comm.all_reduce(send, recv, algo=name, variant=var)
             torch.cuda.synchronize()
             out[("ar", algo)] = recv.view(torch.int16).cpu().numpy().view(np.uint16).copy()
@@ -307,8 +316,8 @@ def test_four_processes_one_gpu():
     for p in procs:
         p.join(timeout=60)
     ins = gen_inputs(world, 4096 + 8, "bf16", "normal", 41)
-    for algo in ("1pa", "2pa", "2pa_ll", "2pr"):
-        want = oracle.allreduce(ins, "2pa" if algo == "2pa_ll" else algo, "bf16")
+    for algo in ("1pa", "2pa", "2pa_ll", "2pr", "2pr+ring"):
+        want = oracle.allreduce(ins, {"2pa_ll": "2pa", "2pr+ring": "2pr"}.get(algo, algo), "bf16")
         for r in range(world):
             assert np.array_equal(res[r][("ar", algo)], want[r]), (algo, r)
     cat = np.concatenate(ins)
