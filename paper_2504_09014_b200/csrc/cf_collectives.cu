@@ -1169,86 +1169,135 @@ __global__ void __launch_bounds__(512) ring_gather_kernel(const __grid_constant_
 // once -- the same bits on every rank):
 //   resid_out = T(h + resid[r])                       (written to out2)
 //   norm_out  = T(resid_out * rsqrt(mean(resid_out^2) + eps) * weight[r])   (out)
-// One CTA per row.  One-shot: every rank reduces every row itself.  Two-shot
-// (`push`): rank r owns rows [r*per, (r+1)*per); phase 1 reduces the owned
-// rows and stores h into every rank's norm_out (rows are disjoint per owner,
-// so this is safe in place); after a CTA-pair handshake every rank finishes
-// ALL rows with its OWN residual and weight (phase 2 touches only local
-// buffers), so per-rank residuals / weights are honoured.  CTA b of rank q
-// finishes exactly the rows CTA b of each owner pushed, so the pair handshake
-// orders every access that meets, and no exit handshake is needed: after the
-// mid handshake no peer reads or writes this rank's buffers.  The first
+// One CTA per row (G CTAs per rank, row R on CTA R mod G).  One-shot: every
+// rank reduces every row itself.  Two-shot (`push`): rank r owns rows
+// [r*per, (r+1)*per); phase 1 reduces the owned rows and stores h into every
+// rank's norm_out (rows are disjoint per owner, so this is safe in place);
+// after a CTA-pair handshake every rank finishes ALL rows with its OWN
+// residual and weight (phase 2 touches only local buffers), so per-rank
+// residuals / weights are honoured.  CTA b of rank q finishes exactly the rows
+// CTA b of each owner pushed, so the pair handshake orders every access that
+// meets, and no exit handshake is needed: after the mid handshake no peer
+// reads or writes this rank's buffers.  G counts rows, not owned rows: phase 2
+// (every row on every rank) is the longer phase, and one row per CTA keeps it
+// one row deep.  The first
 // kCache vectors of a thread's share of the row stay in registers between
 // the two passes; the rest are re-read from this rank's own resid_out
 // (written by the same thread).
 template <typename T, int NR>
 __global__ void __launch_bounds__(512) ar_rmsnorm_kernel(const __grid_constant__ CollArgs a) {
   const RankCtx& rk = a.rk[blockIdx.y];
+  TS_DECL
+  TS_MARK();
   using A = typename Vec<T>::Acc;
   constexpr int V = Vec<T>::N;
-  constexpr int kCache = 4;
+  constexpr int kCache = NR >= 8 ? 2 : 4;   // vectors of a thread's share held in registers between the passes
   const int n = a.n, r = rk.rank;
   const bool push = a.push;
-  const uint64_t e = push ? begin_call(rk) : begin_call_lazy(rk, a.single_launch);
+  // The epoch is needed only by the handshaking threads (t < n) and thread 0
+  // at the end: those threads load it themselves, nobody waits for it.
+  uint64_t e;
+  if (!a.single_launch) e = begin_call(rk);
+  else if (push) e = (int)threadIdx.x < n ? *(volatile uint64_t*)&rk.st->epoch + 1 : 0;
+  else e = begin_call_lazy(rk, true);
   if (!a.single_launch) handshake(rk, n, e * kPhases + 1, false, a.gpu_scope);
   const size_t nv = a.hidden / V;
   const size_t T0 = threadIdx.x, NT = blockDim.x;
   const size_t per = push ? (a.rows + n - 1) / n : a.rows;
   __shared__ float s_red[32];
   if (push) {
-    // phase 1: owned rows, h pushed into every rank's norm_out
+    // phase 1: owned rows, h pushed into every rank's norm_out.  Row R belongs
+    // to CTA R mod G on every rank (owner's push, every rank's finish), so the
+    // CTA-pair handshake orders exactly the accesses that meet.  Two vectors
+    // per thread per round: both vectors' n loads are in flight together.
+    const size_t G = gridDim.x;
     const size_t r0 = min((size_t)r * per, a.rows), r1 = min(r0 + per, a.rows);
-    for (size_t row = r0 + blockIdx.x; row < r1; row += gridDim.x) {
+    for (size_t row = r0 + (blockIdx.x + G - r0 % G) % G; row < r1; row += G) {
       const size_t off = row * a.hidden * sizeof(T);
-      for (size_t v = T0; v < nv; v += NT) {
-        const size_t b = off + v * 16;
-        uint4 x[NR];
+      for (size_t v = T0; v < nv; v += 2 * NT) {
+        const bool two = v + NT < nv;
+        uint4 x0[NR], x1[NR];
 #pragma unroll
         for (int k = 0; k < NR; k++)
-          if (k < n) x[k] = ld16(rk.in[k] + b);
-        const uint4 h = reduce_vecs<T, NR>(x, n, false);
+          if (k < n) {
+            x0[k] = ld16(rk.in[k] + off + v * 16);
+            if (two) x1[k] = ld16(rk.in[k] + off + (v + NT) * 16);
+          }
+        const uint4 h0 = reduce_vecs<T, NR>(x0, n, false);
 #pragma unroll
         for (int p = 0; p < NR; p++)
-          if (p < n) st16(rk.out[p] + b, h);
+          if (p < n) st16(rk.out[p] + off + v * 16, h0);
+        if (two) {
+          const uint4 h1 = reduce_vecs<T, NR>(x1, n, false);
+#pragma unroll
+          for (int p = 0; p < NR; p++)
+            if (p < n) st16(rk.out[p] + off + (v + NT) * 16, h1);
+        }
       }
     }
+    TS_MARK();
     handshake(rk, n, e * kPhases + 2, true, a.gpu_scope);
+    TS_MARK();
   }
   // finish a row on this rank: h (reduced here, or pushed by its owner) +
-  // own residual, sum of squares, then the normalised row with own weight
+  // own residual, sum of squares, then the normalised row with own weight.
+  // The first kCache vectors of the thread's share: every load (h or the n
+  // sources, residual, weight) is issued before the first store, and ro stays
+  // in registers for the second pass; the rest re-read resid_out.
+  auto h_of = [&](size_t b) -> uint4 {
+    if (push) return ld16(rk.out[r] + b);
+    uint4 x[NR];
+#pragma unroll
+    for (int k = 0; k < NR; k++)
+      if (k < n) x[k] = ld16(rk.in[k] + b);
+    return reduce_vecs<T, NR>(x, n, false);
+  };
+  auto resid_add = [&](uint4 hv4, uint4 rv4, float& ss) -> uint4 {
+    A hv[V], rv[V];
+    Vec<T>::load(hv4, hv);
+    Vec<T>::load(rv4, rv);
+#pragma unroll
+    for (int j = 0; j < V; j++) hv[j] = hv[j] + rv[j];
+    const uint4 ro = Vec<T>::store(hv);
+    A q[V];
+    Vec<T>::load(ro, q);
+#pragma unroll
+    for (int j = 0; j < V; j++) ss = fmaf(q[j], q[j], ss);
+    return ro;
+  };
+  auto normed = [&](uint4 ro, uint4 w4, float inv) -> uint4 {
+    A q[V], w[V];
+    Vec<T>::load(ro, q);
+    Vec<T>::load(w4, w);
+#pragma unroll
+    for (int j = 0; j < V; j++) q[j] = q[j] * inv * w[j];
+    return Vec<T>::store(q);
+  };
   auto finish_row = [&](size_t row) {
     const size_t off = row * a.hidden * sizeof(T);
     float ss = 0.f;
-    uint4 cache[kCache];
-    auto pass1 = [&](size_t v) -> uint4 {
-      const size_t b = off + v * 16;
-      uint4 hv4;
-      if (push) {
-        hv4 = ld16(rk.out[r] + b);
-      } else {
-        uint4 x[NR];
-#pragma unroll
-        for (int k = 0; k < NR; k++)
-          if (k < n) x[k] = ld16(rk.in[k] + b);
-        hv4 = reduce_vecs<T, NR>(x, n, false);
-      }
-      A hv[V], rv[V];
-      Vec<T>::load(hv4, hv);
-      Vec<T>::load(ld16(rk.resid + b), rv);
-#pragma unroll
-      for (int j = 0; j < V; j++) hv[j] = hv[j] + rv[j];
-      const uint4 ro = Vec<T>::store(hv);
-      A q[V];
-      Vec<T>::load(ro, q);
-#pragma unroll
-      for (int j = 0; j < V; j++) ss = fmaf(q[j], q[j], ss);
-      st16(rk.out2[r] + b, ro);
-      return ro;
-    };
+    uint4 hc[kCache], rc[kCache], wc[kCache];
 #pragma unroll
     for (int i = 0; i < kCache; i++)
-      if (T0 + i * NT < nv) cache[i] = pass1(T0 + i * NT);
-    for (size_t v = T0 + kCache * NT; v < nv; v += NT) pass1(v);
+      if (T0 + i * NT < nv) {
+        const size_t v = T0 + i * NT;
+        if (push) hc[i] = ld16(rk.out[r] + off + v * 16);
+        rc[i] = ld16(rk.resid + off + v * 16);
+        wc[i] = ld16(rk.weight + v * 16);
+      }
+#pragma unroll
+    for (int i = 0; i < kCache; i++)
+      if (T0 + i * NT < nv) {
+        // one-shot: the n sources of one vector in flight at a time (all
+        // kCache x n would not fit the registers)
+        if (!push) hc[i] = h_of(off + (T0 + i * NT) * 16);
+        hc[i] = resid_add(hc[i], rc[i], ss);   // hc[i] now holds ro
+        st16(rk.out2[r] + off + (T0 + i * NT) * 16, hc[i]);
+      }
+    for (size_t v = T0 + kCache * NT; v < nv; v += NT) {
+      const uint4 ro = resid_add(h_of(off + v * 16), ld16(rk.resid + off + v * 16), ss);
+      st16(rk.out2[r] + off + v * 16, ro);
+    }
     // block sum of squares
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
@@ -1263,30 +1312,20 @@ __global__ void __launch_bounds__(512) ar_rmsnorm_kernel(const __grid_constant__
     __syncthreads();
     const float inv = rsqrtf(s_red[0] / (float)a.hidden + a.eps);
     __syncthreads();   // s_red is reused by the next row
-    auto pass2 = [&](size_t v, uint4 ro) {
-      const size_t b = off + v * 16;
-      A q[V], w[V];
-      Vec<T>::load(ro, q);
-      Vec<T>::load(ld16(rk.weight + v * 16), w);
-#pragma unroll
-      for (int j = 0; j < V; j++) q[j] = q[j] * inv * w[j];
-      st16(rk.out[r] + b, Vec<T>::store(q));
-    };
 #pragma unroll
     for (int i = 0; i < kCache; i++)
-      if (T0 + i * NT < nv) pass2(T0 + i * NT, cache[i]);
-    for (size_t v = T0 + kCache * NT; v < nv; v += NT) pass2(v, ld16(rk.out2[r] + off + v * 16));
+      if (T0 + i * NT < nv) st16(rk.out[r] + off + (T0 + i * NT) * 16, normed(hc[i], wc[i], inv));
+    for (size_t v = T0 + kCache * NT; v < nv; v += NT)
+      st16(rk.out[r] + off + v * 16, normed(ld16(rk.out2[r] + off + v * 16), ld16(rk.weight + v * 16), inv));
   };
-  if (push) {
-    for (int o = 0; o < n; o++) {
-      const size_t r0 = min((size_t)o * per, a.rows), r1 = min(r0 + per, a.rows);
-      for (size_t row = r0 + blockIdx.x; row < r1; row += gridDim.x) finish_row(row);
-    }
-  } else {
-    for (size_t row = blockIdx.x; row < a.rows; row += gridDim.x) finish_row(row);
-    if (!a.single_launch) handshake(rk, n, e * kPhases + 2, true, a.gpu_scope);
+  for (size_t row = blockIdx.x; row < a.rows; row += gridDim.x) {
+    finish_row(row);
+    TS_MARK();
   }
+  if (!push && !a.single_launch) handshake(rk, n, e * kPhases + 2, true, a.gpu_scope);
   end_call(rk, e);
+  TS_MARK();
+  TS_DUMP("k13", rk.rank);
 }
 
 template <typename T>

@@ -694,6 +694,8 @@ cfStatus launch(cfComm* c, const Job& j, int dtype, const void* const* send, voi
     // K13 rows per rank beyond one resident round: 256-thread CTAs (2 per SM)
     // finish them in one round (b=256: 22.3 -> 20.3 us; fewer rows keep 512)
     threads = std::min(threads, 256);
+  if (j.kind == kNorm)
+    if (const char* env = getenv("CF_K13_THREADS")) threads = atoi(env);   // diagnostics
   for (size_t gi = 0; gi < c->groups.size(); gi++) {
     const auto& g = c->groups[gi];
     const int dev = c->local[g[0]].dev;
@@ -1062,7 +1064,7 @@ extern "C" cfStatus cfAllReduceAddRMSNorm(cfComm_t c, const void* const* send, c
       break;
     case CF_ALGO_2PA:
       j.push = 1;
-      j.blocks = (int)std::min<size_t>(ceil_div(rows, (size_t)n), CF_MAX_BLOCKS);
+      j.blocks = (int)std::min<size_t>(rows, CF_MAX_BLOCKS);   // phase 2 finishes every row
       break;
     default:
       return fail(CF_E_NO_ALGO, "algorithm %d: the fused AllReduce+RMSNorm runs as 1pa_hb or 2pa", algo);
