@@ -60,7 +60,19 @@ struct Group {
   uint64_t* d_done = nullptr;  // proxy completion counters [nprog * K]
   int nops = 0;
   std::vector<int32_t> beg, end;  // host copy of the op ranges (parameter-space table)
+  // Op arrays resolved on the host for one I/O binding (the n input and n
+  // output addresses of a call), uploaded once and reused while the caller
+  // keeps its buffers (decode loops, CUDA graphs): the interpreter then skips
+  // its per-call resolve pass.  Bounded; further bindings resolve on device.
+  std::vector<DevOp> h_ops;       // host copy, plan-owned buffers baked
+  struct Bound {
+    std::vector<char*> io;        // io_in[0..n) | io_out[0..n)
+    DevOp* d_ops = nullptr;
+    DevOp* h_pin = nullptr;       // pinned source of the upload (kept: the copy is stream-ordered)
+  };
+  std::vector<Bound> bound;
 };
+constexpr size_t kMaxBound = 32;
 
 }  // namespace
 }  // namespace plan
@@ -1129,6 +1141,7 @@ cfStatus finalize(cfPlan* pl) {
     }
     G.beg = beg;
     G.end = end;
+    G.h_ops = all;
     meta = beg;
     meta.insert(meta.end(), end.begin(), end.end());
     meta.insert(meta.end(), rk.begin(), rk.end());
@@ -1188,6 +1201,60 @@ extern "C" cfStatus cfPlanLoad(cfComm_t comm, const char* json, size_t len, int 
   if (dtype_override < -1 || dtype_override > 3) return fail(CF_E_SHAPE, "unknown dtype %d", dtype_override);
   return cf::plan::load(comm, json, len, dtype_override, plan);
 }
+
+namespace cf {
+namespace plan {
+namespace {
+// The group's op array with every I/O reference of this call's binding
+// resolved (see Group::bound), or nullptr: binding table full, or a stream
+// capture is in progress (the first upload of a binding happens outside
+// capture; a captured launch then reuses it).
+DevOp* bound_ops(const cfPlan* pl, Group& G, const PlanArgs& a, cudaStream_t st) {
+  const int n = pl->ir.nranks;
+  std::vector<char*> key(a.io_in, a.io_in + n);
+  key.insert(key.end(), a.io_out, a.io_out + n);
+  for (auto& b : G.bound)
+    if (b.io == key) return b.d_ops;
+  if (G.bound.size() >= kMaxBound || G.h_ops.empty()) return nullptr;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return nullptr;
+  Group::Bound b;
+  b.io = key;
+  const size_t bytes = G.h_ops.size() * sizeof(DevOp);
+  if (cudaMalloc((void**)&b.d_ops, bytes) != cudaSuccess) return nullptr;
+  if (cudaMallocHost((void**)&b.h_pin, bytes) != cudaSuccess) {
+    cudaFree(b.d_ops);
+    return nullptr;
+  }
+  memcpy(b.h_pin, G.h_ops.data(), bytes);
+  for (size_t i = 0; i < G.h_ops.size(); i++) {
+    DevOp& d = b.h_pin[i];
+    if (d.code != D_MULTI && d.code != D_COPY && d.code != D_PUT_PACKETS && d.code != D_READ_PACKETS &&
+        d.code != D_PORT_PUT)
+      continue;
+    auto fix = [&](DRef& r) {   // the device resolve pass, done once on the host
+      if (r.buf == kAbsolute) return;
+      char* base;
+      if (r.buf == pl->in_buf && !pl->input_private) base = a.io_in[r.rank];
+      else if (r.buf == pl->out_buf) base = a.io_out[r.rank];
+      else base = pl->heap[r.rank] + pl->buf_off[r.buf];
+      r.off = reinterpret_cast<uint64_t>(base + r.off);
+      r.buf = kAbsolute;
+    };
+    for (int k = 0; k < d.nsrc; k++) fix(d.src[k]);
+    for (int k = 0; k < d.ndst; k++) fix(d.dst[k]);
+  }
+  if (cudaMemcpyAsync(b.d_ops, b.h_pin, bytes, cudaMemcpyHostToDevice, st) != cudaSuccess) {
+    cudaFree(b.d_ops);
+    cudaFreeHost(b.h_pin);
+    return nullptr;
+  }
+  G.bound.push_back(std::move(b));
+  return G.bound.back().d_ops;
+}
+}  // namespace
+}  // namespace plan
+}  // namespace cf
 
 extern "C" cfStatus cfPlanExecute(cfPlan_t pl, const void* const* inputs, void* const* outputs,
                                   const cudaStream_t* streams) {
@@ -1283,6 +1350,10 @@ extern "C" cfStatus cfPlanExecute(cfPlan_t pl, const void* const* inputs, void* 
         a.prog_tab[p] = make_int4(pl->prog_rank[G.progs[p]], G.beg[p], G.end[p], 0);
       }
     }
+    if (DevOp* rops = bound_ops(pl, G, a, streams[c->groups[gi][0]])) {
+      a.ops = rops;
+      a.resolved = 1;
+    }
     void* args[] = {&a};
     a.window = pl->window;
     a.has_prologue = pl->has_prologue ? 1 : 0;
@@ -1369,6 +1440,10 @@ extern "C" cfStatus cfPlanDestroy(cfPlan_t pl) {
   for (auto& G : pl->groups) {
     cudaSetDevice(G.dev);
     cudaFree(G.d_ops);
+    for (auto& b : G.bound) {
+      cudaFree(b.d_ops);
+      cudaFreeHost(b.h_pin);
+    }
     cudaFree(G.d_meta);
     cudaFree(G.d_bufptr);
     cudaFree(G.d_zero);

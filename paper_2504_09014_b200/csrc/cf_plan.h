@@ -139,6 +139,7 @@ struct PlanArgs {
   int input_private;           // 1: plan writes its input -> copy user input into the plan buffer
   int gpu_scope;               // every rank on this device: .gpu-scope release/acquire
   int window;                  // ops staged into shared memory at a time
+  int resolved;                // 1: `ops` already holds this call's I/O addresses (host-resolved)
   int has_prologue;            // any zeroing / private-input copy this call
   int entry_barrier;           // rank barrier after the prologue (zeroing / private input)
   int exit_barrier;            // rank barrier at the end (not needed when one launch holds every rank)

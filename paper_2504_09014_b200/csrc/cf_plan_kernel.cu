@@ -245,7 +245,8 @@ __device__ __noinline__ void data_op_general(const DevOp& op, uint64_t lo, uint6
           for (int i = 0; i < B; i++) {
             const int k = k0 + i;
             if (k >= nsrc) break;
-            const uint4 x = finish_src<T>(src(k), v, nval, (pkt >> k) & 1u, op.llflag_k[k], r0[i], r1[i], rs);
+            const uint32_t fl = ((pkt >> k) & 1u) ? runtime_flag(e, fstride, op.llflag_k[k]) : 0u;
+            const uint4 x = finish_src<T>(src(k), v, nval, (pkt >> k) & 1u, fl, r0[i], r1[i], rs);
             if (k == 0 && !zero) Vec<T>::load(x, acc);
             else acc_vec<T>(acc, x, round_each);
           }
@@ -286,10 +287,12 @@ __device__ __noinline__ void packet_op(const DevOp& op, int K, int j, uint32_t f
   // batched ops: a put sends one payload to ndst packet ranges (one plan op
   // each); a read drains nsrc packet ranges into nsrc payload ranges
   const int nb = put ? op.ndst : op.nsrc;
+  // plan flags -> this call's runtime flags (fold in the epoch)
+  const uint32_t pflag = put ? runtime_flag(e, fstride, op.llflag) : 0;
   if (op.flags & F_LL16) {
     const uint64_t u0 = lo * sizeof(T) / 8, u1 = (hi * sizeof(T) + 7) / 8;
     if (put && (op.flags & F_PAIRED)) {   // src[k] -> dst[k]: every payload load in flight first
-      const uint32_t flag = op.llflag;
+      const uint32_t flag = pflag;
       for (uint64_t u = u0 + threadIdx.x; u < u1; u += blockDim.x) {
         uint2 d[kMaxDst];
 #pragma unroll
@@ -300,7 +303,7 @@ __device__ __noinline__ void packet_op(const DevOp& op, int K, int j, uint32_t f
           if (k < nb) ll16_put(ptr(op.dst[k]) + u * 16, d[k], flag);
       }
     } else if (put) {
-      const uint32_t flag = op.llflag;
+      const uint32_t flag = pflag;
       const char* src = ptr(op.src[0]);
       for (uint64_t u = u0 + threadIdx.x; u < u1; u += blockDim.x) {
         const uint2 d = *reinterpret_cast<const uint2*>(src + u * 8);
@@ -315,7 +318,7 @@ __device__ __noinline__ void packet_op(const DevOp& op, int K, int j, uint32_t f
 #pragma unroll
         for (int k = 0; k < kMaxDst; k++) {
           if (k < nb) {
-            const uint32_t flag = op.llflag_k[k];
+            const uint32_t flag = runtime_flag(e, fstride, op.llflag_k[k]);
             uint2 d = make_uint2(raw[k].x, raw[k].z);
             if (raw[k].y != flag || raw[k].w != flag) d = ll16_get(ptr(op.src[k]) + u * 16, flag, rs);
             *reinterpret_cast<uint2*>(ptr(op.dst[k]) + u * 8) = d;
@@ -328,7 +331,7 @@ __device__ __noinline__ void packet_op(const DevOp& op, int K, int j, uint32_t f
     for (int k = 0; k < nb; k++) {
       const char* src = ptr(op.src[put && !(op.flags & F_PAIRED) ? 0 : k]);
       char* dst = ptr(op.dst[k]);
-      const uint32_t flag = put ? op.llflag : op.llflag_k[k];
+      const uint32_t flag = put ? pflag : runtime_flag(e, fstride, op.llflag_k[k]);
       for (uint64_t u = u0 + threadIdx.x; u < u1; u += blockDim.x) {
         if (put) {
           const uint32_t d = *reinterpret_cast<const uint32_t*>(src + u * 4);
@@ -407,21 +410,15 @@ __device__ __noinline__ void prologue(const PlanArgs& a, int rank) {
   }
 }
 
-// Rewrite the staged window's data-op references as absolute addresses (the io
-// buffers change per call, so this cannot all be done at load time).
-__device__ __forceinline__ void resolve_window(const PlanArgs& a, DevOp* ops, int nops, uint64_t e,
-                                               char* const* io) {
+// Rewrite the staged window's I/O references as absolute addresses (the io
+// buffers change per call).  Only when the host did not hand over an op array
+// already resolved for this call's I/O binding (PlanArgs.resolved).
+__device__ __forceinline__ void resolve_window(const PlanArgs& a, DevOp* ops, int nops, char* const* io) {
   constexpr int kSlots = kMaxSrc + kMaxDst;
   for (int t = threadIdx.x; t < nops * kSlots; t += blockDim.x) {
     DevOp& op = ops[t / kSlots];
     if (!is_data_code(op.code)) continue;
     const int k = t % kSlots;
-    // packet flags: plan flag -> this call's runtime flag (folds in the epoch)
-    const bool pkt_op = op.code == D_PUT_PACKETS || op.code == D_READ_PACKETS;
-    if (k == 0 && pkt_op) op.llflag = runtime_flag(e, a.flag_stride, op.llflag);
-    if (k < kMaxSrc && k < op.nsrc &&
-        ((op.code == D_READ_PACKETS) || (op.code == D_MULTI && ((op.pkt_mask >> k) & 1u))))
-      op.llflag_k[k] = runtime_flag(e, a.flag_stride, op.llflag_k[k]);
     if (k < kMaxSrc ? k >= op.nsrc : k - kMaxSrc >= op.ndst) continue;
     DRef& r = k < kMaxSrc ? op.src[k] : op.dst[k - kMaxSrc];
     if (r.buf == kAbsolute) continue;
@@ -470,7 +467,7 @@ __global__ void __launch_bounds__(CF_PLAN_THREADS) plan_kernel(const __grid_cons
   // the ranks' I/O bases in shared memory: the resolve pass indexes them per
   // thread, which on the parameter space would serialize the warp
   __shared__ char* s_io[2 * CF_MAX_RANKS];
-  if (threadIdx.x == 0) {
+  if (!a.resolved && threadIdx.x == 0) {
 #pragma unroll
     for (int r = 0; r < CF_MAX_RANKS; r++) {
       s_io[r] = a.io_in[r];
@@ -496,8 +493,10 @@ __global__ void __launch_bounds__(CF_PLAN_THREADS) plan_kernel(const __grid_cons
       stage(w0, w1);
       __syncthreads();
     }
-    resolve_window(a, s_ops, w1 - w0, e, s_io);
-    __syncthreads();
+    if (!a.resolved) {
+      resolve_window(a, s_ops, w1 - w0, s_io);
+      __syncthreads();
+    }
     TS_MARK();
   for (int i = w0; i < w1; i++) {
     const DevOp& op = s_ops[i - w0];
