@@ -89,6 +89,19 @@ __device__ __forceinline__ void handshake(const RankCtx& rk, int n, uint64_t v, 
   __syncthreads();
 }
 
+// Barrier over every CTA of every rank: CTA b of rank r publishes its writes
+// and marks slot (r, b) on every rank (its own included), then waits until
+// all n x G slots of its own rank carry `v`.  The whole grid of every rank
+// must be resident (the CTA budget / co-residency cap guarantees it).
+__device__ __forceinline__ void all_cta_barrier(const RankCtx& rk, int n, uint64_t v, bool gpu) {
+  const int t = threadIdx.x, r = rk.rank, b = blockIdx.x, G = gridDim.x;
+  fence_publish(gpu);
+  __syncthreads();
+  if (t < n) st_release(rk.sem[t] + sem_index(r, b), v, gpu);
+  for (int i = t; i < n * G; i += blockDim.x) wait_geq(rk.sem[r] + sem_index(i / G, i % G), v, rk.st, gpu);
+  __syncthreads();
+}
+
 // ---------------------------------------------------------------- vector helpers
 
 // Ragged-edge paths stay out of line: the small-message kernels execute each
@@ -1171,16 +1184,13 @@ __global__ void __launch_bounds__(512) ring_gather_kernel(const __grid_constant_
 //   norm_out  = T(resid_out * rsqrt(mean(resid_out^2) + eps) * weight[r])   (out)
 // One CTA per row (G CTAs per rank, row R on CTA R mod G).  One-shot: every
 // rank reduces every row itself.  Two-shot (`push`): rank r owns rows
-// [r*per, (r+1)*per); phase 1 reduces the owned rows and stores h into every
-// rank's norm_out (rows are disjoint per owner, so this is safe in place);
-// after a CTA-pair handshake every rank finishes ALL rows with its OWN
-// residual and weight (phase 2 touches only local buffers), so per-rank
-// residuals / weights are honoured.  CTA b of rank q finishes exactly the rows
-// CTA b of each owner pushed, so the pair handshake orders every access that
-// meets, and no exit handshake is needed: after the mid handshake no peer
-// reads or writes this rank's buffers.  G counts rows, not owned rows: phase 2
-// (every row on every rank) is the longer phase, and one row per CTA keeps it
-// one row deep.  The first
+// [r*per, (r+1)*per); phase 1 reduces the owned rows -- spread over all G
+// CTAs of the rank by vector -- and stores h into every rank's norm_out (rows
+// are disjoint per owner, so this is safe in place); after a barrier over
+// every CTA of every rank, every rank finishes ALL rows with its OWN residual
+// and weight (phase 2 touches only local buffers), so per-rank residuals /
+// weights are honoured.  No exit handshake is needed: after the barrier no
+// peer reads or writes this rank's buffers.  The first
 // kCache vectors of a thread's share of the row stay in registers between
 // the two passes; the rest are re-read from this rank's own resid_out
 // (written by the same thread).
@@ -1206,37 +1216,35 @@ __global__ void __launch_bounds__(512) ar_rmsnorm_kernel(const __grid_constant__
   const size_t per = push ? (a.rows + n - 1) / n : a.rows;
   __shared__ float s_red[32];
   if (push) {
-    // phase 1: owned rows, h pushed into every rank's norm_out.  Row R belongs
-    // to CTA R mod G on every rank (owner's push, every rank's finish), so the
-    // CTA-pair handshake orders exactly the accesses that meet.  Two vectors
-    // per thread per round: both vectors' n loads are in flight together.
-    const size_t G = gridDim.x;
+    // phase 1: the owned rows as one contiguous range of vectors spread over
+    // every CTA of the rank, h pushed into every rank's norm_out; two vectors
+    // per thread per round (both vectors' n loads in flight together).
+    const size_t G = gridDim.x, stride = G * NT;
     const size_t r0 = min((size_t)r * per, a.rows), r1 = min(r0 + per, a.rows);
-    for (size_t row = r0 + (blockIdx.x + G - r0 % G) % G; row < r1; row += G) {
-      const size_t off = row * a.hidden * sizeof(T);
-      for (size_t v = T0; v < nv; v += 2 * NT) {
-        const bool two = v + NT < nv;
-        uint4 x0[NR], x1[NR];
+    const size_t v1 = r1 * nv;
+    for (size_t v = r0 * nv + blockIdx.x * NT + T0; v < v1; v += 2 * stride) {
+      const bool two = v + stride < v1;
+      uint4 x0[NR], x1[NR];
 #pragma unroll
-        for (int k = 0; k < NR; k++)
-          if (k < n) {
-            x0[k] = ld16(rk.in[k] + off + v * 16);
-            if (two) x1[k] = ld16(rk.in[k] + off + (v + NT) * 16);
-          }
-        const uint4 h0 = reduce_vecs<T, NR>(x0, n, false);
+      for (int k = 0; k < NR; k++)
+        if (k < n) {
+          x0[k] = ld16(rk.in[k] + v * 16);
+          if (two) x1[k] = ld16(rk.in[k] + (v + stride) * 16);
+        }
+      const uint4 h0 = reduce_vecs<T, NR>(x0, n, false);
+#pragma unroll
+      for (int p = 0; p < NR; p++)
+        if (p < n) st16(rk.out[p] + v * 16, h0);
+      if (two) {
+        const uint4 h1 = reduce_vecs<T, NR>(x1, n, false);
 #pragma unroll
         for (int p = 0; p < NR; p++)
-          if (p < n) st16(rk.out[p] + off + v * 16, h0);
-        if (two) {
-          const uint4 h1 = reduce_vecs<T, NR>(x1, n, false);
-#pragma unroll
-          for (int p = 0; p < NR; p++)
-            if (p < n) st16(rk.out[p] + off + (v + NT) * 16, h1);
-        }
+          if (p < n) st16(rk.out[p] + (v + stride) * 16, h1);
       }
     }
     TS_MARK();
-    handshake(rk, n, e * kPhases + 2, true, a.gpu_scope);
+    // every CTA of every rank pushed: any row may now be finished anywhere
+    all_cta_barrier(rk, n, e * kPhases + 2, a.gpu_scope);
     TS_MARK();
   }
   // finish a row on this rank: h (reduced here, or pushed by its owner) +
