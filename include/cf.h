@@ -187,7 +187,8 @@ CF_API cfStatus cfNvlsEmulate(cfComm_t comm, void* staging, size_t bytes);
  *   cfCommCreateRank communicators, phases separated by bootstrap barriers:
  *     cfSymHeapCreate -> *fd of this rank's heap; send it to every peer
  *     (Unix socket SCM_RIGHTS); cfSymHeapMapPeer for every peer; mode 1 then
- *     cfSymHeapMulticast phase 0 (rank 0: *fd out), 1 (others: *fd in), 2 (all).
+ *     cfSymHeapMulticast phase 0 (rank 0: *fd out), 1 (others: *fd in), 2 (all);
+ *     phase 3 on every rank when any rank failed a phase (switch off, heap kept).
  * cfMemAlloc is collective (same sizes, same order on every rank); ptrs gets
  * one pointer per local rank.  cfMemFree takes any local rank's pointer. */
 CF_API cfStatus cfSymHeapCreate(cfComm_t comm, size_t bytes, int mode, int* fd);

@@ -303,7 +303,10 @@ class Communicator:
             if self.rank == 0 and mfd.value >= 0:
                 os.close(mfd.value)
             if not ok:
-                self._sym_mode = 0      # heap stays usable (HB algorithms), switch_2pa falls back
+                # heap stays usable (HB algorithms); libcf stops using the
+                # switch on every rank, so AUTO picks the same kernel everywhere
+                _lib.check(L.cfSymHeapMulticast(self._comm, 3, ctypes.byref(mfd)))
+                self._sym_mode = 0
         return self._sym_mode
 
     def alloc_symmetric(self, numel: int, dtype):

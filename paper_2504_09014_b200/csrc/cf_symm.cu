@@ -247,7 +247,8 @@ extern "C" cfStatus cfSymHeapMapPeer(cfComm_t c, int peer, int fd) {
 // One process per GPU, mode 1, in phases the caller separates with bootstrap
 // barriers: phase 0 on rank 0 creates the multicast object and returns its fd
 // (send it to every rank); phase 1 on the others imports it (*fd in); phase 2
-// on every rank binds and maps its heap.
+// on every rank binds and maps its heap; phase 3 (every rank, when any rank
+// failed a phase) turns the switch off for this heap.
 extern "C" cfStatus cfSymHeapMulticast(cfComm_t c, int phase, int* fd) {
   if (!c || !fd) return fail(CF_E_CONFIG, "null argument");
   if (!c->multiprocess) return fail(CF_E_CONFIG, "in-process communicators bind in cfSymHeapCreate");
@@ -279,7 +280,14 @@ extern "C" cfStatus cfSymHeapMulticast(cfComm_t c, int phase, int* fd) {
     if (!c->sym.mc_added) return fail(CF_E_CONFIG, "multicast phase 0 / 1 first");
     return mc_bind(c, 0);
   }
-  return fail(CF_E_CONFIG, "phase must be 0, 1 or 2");
+  if (phase == 3) {
+    // some rank failed a phase: every rank stops using the switch (the heap
+    // stays usable for the HB algorithms), so no rank's AUTO picks NVLS
+    // while a peer picks another kernel
+    c->sym.mode = 0;
+    return CF_OK;
+  }
+  return fail(CF_E_CONFIG, "phase must be 0, 1, 2 or 3");
 }
 
 // Collective: every rank asks for the same sizes in the same order, so the
