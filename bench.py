@@ -842,6 +842,8 @@ def run_multi_gpu(args):
     parity = multi_parity(comm, dev, rank, world, nvls, sym_mode)
     if nvls and parity.get("allreduce_switch_2pa_symmetric") is not True:
         nvls = False    # a failed first multimem execution drops the NVLS rows, never the line
+        if sym_mode == 1:
+            comm.disable_switch()   # and AUTO stops picking it on every rank
     count = HEAD_BYTES // 2
     gen = torch.Generator(device=dev)
     gen.manual_seed(20250409 + 4000 + rank)

@@ -309,6 +309,14 @@ class Communicator:
                 self._sym_mode = 0
         return self._sym_mode
 
+    def disable_switch(self) -> None:
+        """Collective: stop using the NVLS switch on this heap (every rank calls
+        it, e.g. after a failed first multimem execution); the heap stays
+        usable for the other algorithms."""
+        mfd = ctypes.c_int(-1)
+        _lib.check(_lib.lib().cfSymHeapMulticast(self._comm, 3, ctypes.byref(mfd)))
+        self._sym_mode = 0
+
     def alloc_symmetric(self, numel: int, dtype):
         """Collective: a tensor at the same offset of every rank's symmetric
         heap (cfMemAlloc) -- collectives on it need no registration, and
