@@ -581,6 +581,7 @@ def multi_parity(comm, dev, rank, world, nvls, sym_mode=-1):
                     res[key] = bool(np.all(np.abs(g32 - w32) <= tol))
             except Exception as e:
                 res[key] = f"{type(e).__name__}: {e}"[:160]
+                comm.clear_device_error()
         comm.free_symmetric(xs)
         comm.free_symmetric(ys)
     # AllGather (bit-exact data movement, random 16-bit patterns incl. NaNs)

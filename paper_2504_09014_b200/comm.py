@@ -343,6 +343,12 @@ class Communicator:
             from .errors import raise_status
             raise_status(code.value, "device-side wait timed out")
 
+    def clear_device_error(self):
+        """Reset this rank's device error word after a reported timeout
+        (cfCommClearDeviceError); epochs and semaphores only grow, so later
+        calls start clean once every rank cleared it."""
+        _lib.check(_lib.lib().cfCommClearDeviceError(self._comm))
+
     def close(self):
         if self._comm is not None:
             _lib.lib().cfCommDestroy(self._comm)
