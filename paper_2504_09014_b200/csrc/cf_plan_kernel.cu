@@ -500,6 +500,7 @@ __global__ void __launch_bounds__(CF_PLAN_THREADS) plan_kernel(const __grid_cons
     TS_MARK();
   for (int i = w0; i < w1; i++) {
     const DevOp& op = s_ops[i - w0];
+    TS_MARK();
     switch (op.code) {
       case D_SYNC_CTA:
         __syncthreads();
