@@ -651,12 +651,24 @@ cfStatus load(cfComm* c, const char* json, size_t len, int dtype_override, cfPla
   long long max_bytes = 0;
   bool packets = false;   // LL plans: packet ops run one 8-byte payload unit per thread
   bool port = false;
-  for (auto& h : hops)
-    for (auto& o : h) {
-      if (is_data(o)) max_bytes = std::max(max_bytes, o.size * es);
-      packets |= o.code == D_PUT_PACKETS || o.code == D_READ_PACKETS;
+  for (auto& h : hops) {
+    int run = 0;   // consecutive packet ops of one kind and size: they batch into one device op
+    for (size_t i = 0; i < h.size(); i++) {
+      const HOp& o = h[i];
+      const bool pkt = o.code == D_PUT_PACKETS || o.code == D_READ_PACKETS;
+      // (paired puts -- different payload ranges -- and packet reads; a
+      // payload broadcast to several ranges stays one unit per thread)
+      const bool batch = pkt && i && h[i - 1].code == o.code && h[i - 1].size == o.size &&
+                         (o.code == D_READ_PACKETS || !(h[i - 1].src.size() && o.src.size() &&
+                                                        h[i - 1].src[0].buf == o.src[0].buf && h[i - 1].src[0].rank == o.src[0].rank &&
+                                                        h[i - 1].src[0].off == o.src[0].off));
+      run = batch ? std::min(run + 1, kMaxDst) : 1;
+      // a batched packet op spreads its ranges over the threads (one unit each)
+      if (is_data(o)) max_bytes = std::max(max_bytes, o.size * es * (pkt ? run : 1));
+      packets |= pkt;
       port |= o.code == D_PORT_PUT || o.code == D_PORT_SIGNAL || o.code == D_PORT_FLUSH;
     }
+  }
   // the smallest interpreter class covering every op of the plan (MULTI ops
   // take packet sources only where the plan has packet ops to fuse)
   pl->cls = (packets ? 1 : 0) | (port ? 2 : 0);

@@ -274,6 +274,51 @@ __device__ __noinline__ void data_op_general(const DevOp& op, uint64_t lo, uint6
   }
 }
 
+// One 8-byte unit per thread, every range of the batch: payload / packet
+// loads of all nb ranges in flight first (the large-slice path).
+template <typename T>
+__device__ __noinline__ void packet_units(const DevOp& op, uint64_t u0, uint64_t u1, bool put, bool paired, int nb,
+                                             uint32_t pflag, uint32_t fstride, uint64_t e, RankState* rs) {
+  if (put && paired) {   // src[k] -> dst[k]
+    for (uint64_t u = u0 + threadIdx.x; u < u1; u += blockDim.x) {
+      uint2 d[kMaxDst];
+#pragma unroll
+      for (int k = 0; k < kMaxDst; k++)
+        if (k < nb) d[k] = *reinterpret_cast<const uint2*>(ptr(op.src[k]) + u * 8);
+#pragma unroll
+      for (int k = 0; k < kMaxDst; k++)
+        if (k < nb) ll16_put(ptr(op.dst[k]) + u * 16, d[k], pflag);
+    }
+  } else if (put) {      // one payload -> nb ranges
+    const char* src = ptr(op.src[0]);
+    for (uint64_t u = u0 + threadIdx.x; u < u1; u += blockDim.x) {
+      const uint2 d = *reinterpret_cast<const uint2*>(src + u * 8);
+      for (int k = 0; k < nb; k++) ll16_put(ptr(op.dst[k]) + u * 16, d, pflag);
+    }
+  } else {
+    for (uint64_t u = u0 + threadIdx.x; u < u1; u += blockDim.x) {
+      uint4 raw[kMaxDst];
+#pragma unroll
+      for (int k = 0; k < kMaxDst; k++)   // all packets in flight first
+        if (k < nb) raw[k] = ld16_volatile(ptr(op.src[k]) + u * 16);
+#pragma unroll
+      for (int k = 0; k < kMaxDst; k++) {
+        if (k < nb) {
+          const uint32_t flag = runtime_flag(e, fstride, op.llflag_k[k]);
+          uint2 d = make_uint2(raw[k].x, raw[k].z);
+          if (raw[k].y != flag || raw[k].w != flag) d = ll16_get(ptr(op.src[k]) + u * 16, flag, rs);
+          *reinterpret_cast<uint2*>(ptr(op.dst[k]) + u * 8) = d;
+        }
+      }
+    }
+  }
+}
+
+#ifndef CF_PLAN_PKT_U
+#define CF_PLAN_PKT_U 2
+#endif
+constexpr int kPktU = CF_PLAN_PKT_U;
+
 // LL packets (cf/channels.py:244-330).  LL16: 8 payload bytes per 16-byte
 // packet {d0, f, d1, f}; LL8: one reference packet {d, f} per 4 payload bytes.
 template <typename T>
@@ -290,40 +335,51 @@ __device__ __noinline__ void packet_op(const DevOp& op, int K, int j, uint32_t f
   // plan flags -> this call's runtime flags (fold in the epoch)
   const uint32_t pflag = put ? runtime_flag(e, fstride, op.llflag) : 0;
   if (op.flags & F_LL16) {
+    // (range k, unit u) items flattened over the CTA's threads -- consecutive
+    // threads take consecutive units of one range -- so a batch of nb ranges
+    // spreads over nb times the threads instead of looping in each one;
+    // kPktU items per thread per round, their loads in flight together
     const uint64_t u0 = lo * sizeof(T) / 8, u1 = (hi * sizeof(T) + 7) / 8;
-    if (put && (op.flags & F_PAIRED)) {   // src[k] -> dst[k]: every payload load in flight first
-      const uint32_t flag = pflag;
-      for (uint64_t u = u0 + threadIdx.x; u < u1; u += blockDim.x) {
-        uint2 d[kMaxDst];
+    const uint32_t nu = (uint32_t)(u1 - u0), items = nu * (uint32_t)nb;
+    const bool paired = op.flags & F_PAIRED;
+    constexpr int U = kPktU;
+    if (nu >= 4 * blockDim.x || (put && !paired)) {
+      // enough units to keep every thread busy (or one payload to many
+      // ranges): one unit per thread, all nb ranges' accesses in flight
+      packet_units<T>(op, u0, u1, put, paired, nb, pflag, fstride, e, rs);
+      return;
+    }
+    for (uint32_t w0 = threadIdx.x; w0 < items; w0 += U * blockDim.x) {
+      uint32_t kk[U];
+      uint64_t uu[U];
 #pragma unroll
-        for (int k = 0; k < kMaxDst; k++)
-          if (k < nb) d[k] = *reinterpret_cast<const uint2*>(ptr(op.src[k]) + u * 8);
-#pragma unroll
-        for (int k = 0; k < kMaxDst; k++)
-          if (k < nb) ll16_put(ptr(op.dst[k]) + u * 16, d[k], flag);
+      for (int i = 0; i < U; i++) {
+        const uint32_t w = w0 + (uint32_t)i * blockDim.x;
+        kk[i] = w < items ? w / nu : (uint32_t)kMaxDst;
+        uu[i] = u0 + (w - kk[i] * nu);
       }
-    } else if (put) {
-      const uint32_t flag = pflag;
-      const char* src = ptr(op.src[0]);
-      for (uint64_t u = u0 + threadIdx.x; u < u1; u += blockDim.x) {
-        const uint2 d = *reinterpret_cast<const uint2*>(src + u * 8);
-        for (int k = 0; k < nb; k++) ll16_put(ptr(op.dst[k]) + u * 16, d, flag);
-      }
-    } else {
-      for (uint64_t u = u0 + threadIdx.x; u < u1; u += blockDim.x) {
-        uint4 raw[kMaxDst];
+      if (put) {
+        uint2 d[U];
 #pragma unroll
-        for (int k = 0; k < kMaxDst; k++)   // all packets in flight first
-          if (k < nb) raw[k] = ld16_volatile(ptr(op.src[k]) + u * 16);
+        for (int i = 0; i < U; i++)
+          if (kk[i] < (uint32_t)nb)
+            d[i] = *reinterpret_cast<const uint2*>(ptr(op.src[paired ? kk[i] : 0]) + uu[i] * 8);
 #pragma unroll
-        for (int k = 0; k < kMaxDst; k++) {
-          if (k < nb) {
-            const uint32_t flag = runtime_flag(e, fstride, op.llflag_k[k]);
-            uint2 d = make_uint2(raw[k].x, raw[k].z);
-            if (raw[k].y != flag || raw[k].w != flag) d = ll16_get(ptr(op.src[k]) + u * 16, flag, rs);
-            *reinterpret_cast<uint2*>(ptr(op.dst[k]) + u * 8) = d;
+        for (int i = 0; i < U; i++)
+          if (kk[i] < (uint32_t)nb) ll16_put(ptr(op.dst[kk[i]]) + uu[i] * 16, d[i], pflag);
+      } else {
+        uint4 raw[U];
+#pragma unroll
+        for (int i = 0; i < U; i++)   // all packets in flight first
+          if (kk[i] < (uint32_t)nb) raw[i] = ld16_volatile(ptr(op.src[kk[i]]) + uu[i] * 16);
+#pragma unroll
+        for (int i = 0; i < U; i++)
+          if (kk[i] < (uint32_t)nb) {
+            const uint32_t flag = runtime_flag(e, fstride, op.llflag_k[kk[i]]);
+            uint2 d = make_uint2(raw[i].x, raw[i].z);
+            if (raw[i].y != flag || raw[i].w != flag) d = ll16_get(ptr(op.src[kk[i]]) + uu[i] * 16, flag, rs);
+            *reinterpret_cast<uint2*>(ptr(op.dst[kk[i]]) + uu[i] * 8) = d;
           }
-        }
       }
     }
   } else {

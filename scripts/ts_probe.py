@@ -27,7 +27,7 @@ for nb in [int(x) for x in os.environ.get("SIZES", "1024,16384").split(",")]:
             torch.cuda.synchronize(dev)
 for pname in [p for p in os.environ.get("PLANS", "").split(",") if p]:
     base = parse_plan(open(os.path.join(ROOT, "tests", "golden", "plans", pname + ".json"), "rb").read())
-    for b in (1, 64):
+    for b in [int(x) for x in os.environ.get("BATCH", "1,64").split(",")]:
         rt = Runtime(scale_plan(base, 128 * b), w, dtype="bf16")
         xs = [torch.randn(rt.in_elems, device=dev).to(torch.bfloat16) for _ in range(n)]
         ys = [torch.empty(rt.out_elems, device=dev, dtype=torch.bfloat16) for _ in range(n)]
