@@ -535,6 +535,15 @@ bool touched_elsewhere(const cfPlan* pl, const DRef& loc, uint64_t lo, uint64_t 
 // when T_k is scratch nobody else touches: the reduction reads the LL16
 // packets directly (one pass, no temporary), exactly the one-shot LL kernel.
 void fuse_packet_reads(cfPlan* pl) {
+  // Below ~8 KiB of payload per range the separate batched read (its items
+  // spread over every thread) and a plain-source reduce beat the fused
+  // reduce, whose threads each chase 2 packets per source (2pa_ll plan b=1:
+  // 12.1 -> 11.4 us); from there on fusing wins (b=16: 16.2 -> 15.1 us,
+  // b=256: 101 -> 80 us; one box, A/B).
+  long long min_bytes = 8 << 10;
+  if (const char* ev = getenv("CF_PLAN_FUSE_READS_MIN")) min_bytes = atoll(ev);   // diagnostic
+  if (const char* ev = getenv("CF_PLAN_FUSE_READS"))   // diagnostic: 0 keeps read_packets separate
+    if (atoi(ev) == 0) return;
   for (size_t p = 0; p < pl->prog_ops.size(); p++) {
     auto& ops = pl->prog_ops[p];
     for (size_t m = 0; m < ops.size(); m++) {
@@ -545,6 +554,7 @@ void fuse_packet_reads(cfPlan* pl) {
         if (R.code == D_SYNC_CTA) continue;
         if (R.code != D_READ_PACKETS) break;
         if (!(R.flags & F_LL16) || R.size != M.size) break;
+        if ((long long)R.size * pl->es < min_bytes) break;
         for (int k = 0; k < R.nsrc; k++) {
           for (int s = 0; s < M.nsrc; s++) {
             if ((M.pkt_mask >> s) & 1u) continue;
