@@ -22,7 +22,7 @@ def main():
     for pname in ("2pa_memory", "2pa_ll", "1pa"):
         with open(os.path.join(ROOT, "tests", "golden", "plans", pname + "_n8_e64.json"), "rb") as f:
             base = parse_plan(f.read())
-        for b in (1, 16, 64, 256):
+        for b in [int(x) for x in os.environ.get("BATCH", "1,16,64,256").split(",")]:
             plan = scale_plan(base, 128 * b)
             rt = Runtime(plan, w, dtype="bf16")
             xs = [torch.randn(rt.in_elems, device=dev).to(torch.bfloat16) for _ in range(n)]
