@@ -158,8 +158,18 @@ struct PlanArgs {
   // so a CTA knows its op range without a dependent global load.
   int prog_in_param;
   int4 prog_tab[128];
+  // L2 prefetch hints (host-resolved bindings only): the source ranges of
+  // each program's first data op, so their HBM reads overlap the dependent
+  // load that stages the op window (npf = 0: none)
+  int npf;
+  struct Prefetch {
+    const char* src[8];
+    uint64_t size;       // the op's elements (sliced over the K CTAs like the op)
+    uint32_t nsrc, es;   // sources; bytes per element of the ranges (packet ranges: 2 x)
+  } pf[32];
 };
 constexpr int kParamProgs = 128;
+constexpr int kPfProgs = 32;
 static_assert(sizeof(PlanArgs) <= 32764, "kernel parameter space");
 constexpr int kMaxBufs = 16;
 constexpr int kMaxZero = 16;

@@ -533,6 +533,14 @@ __global__ void __launch_bounds__(CF_PLAN_THREADS) plan_kernel(const __grid_cons
   __shared__ uint64_t s_e;
   if (threadIdx.x == 0) s_e = *(volatile uint64_t*)&rs->epoch + 1;
   if (pb < pe) stage(pb, min(pb + a.window, pe));
+  if (pid < a.npf) {   // the first data op's source lines, requested while its op is staged
+    const PlanArgs::Prefetch& h = a.pf[pid];
+    uint64_t lo, hi;
+    slice<T>(h.size, a.K, j, lo, hi);
+    for (uint32_t k = 0; k < h.nsrc; k++)
+      for (uint64_t b = lo * h.es + threadIdx.x * 128ull; b < hi * h.es; b += blockDim.x * 128ull)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(h.src[k] + b));
+  }
   __syncthreads();
   const uint64_t e = s_e;
   TS_MARK();

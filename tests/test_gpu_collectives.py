@@ -49,6 +49,23 @@ def test_gpu_matches_reference_bits(case):
     assert [_digest(o) for o in outs] == case["digests"]
 
 
+_RING = [c for c in _cases() if c["algo"] in ("2pr", "ring_rs", "ring_ag")]
+
+
+@pytest.mark.parametrize("case", _RING, ids=lambda c: f"{c['kind']}-{c['algo']}-ring-n{c['n']}-e{c['elems']}-"
+                         f"{c['dtype']}-{c['dist']}")
+def test_literal_ring_matches_reference_bits(case):
+    """The reference's ring algorithms on the literal ring transport
+    (variant "ring": K9 / K12 / K7) return the reference's digests too --
+    the default all-pairs transport is pinned by
+    test_gpu_matches_reference_bits."""
+    from paper_2504_09014_b200 import collective
+    ins = gen_inputs(case["n"], case["elems"], case["dtype"], case["dist"], case["seed"])
+    outs = collective(case["kind"], ins, world(case["n"]), dtype=case["dtype"], algo=case["algo"], variant="ring")
+    assert [len(o) for o in outs] == case["out_len"]
+    assert [_digest(o) for o in outs] == case["digests"]
+
+
 def _aid(name):
     """libcf algorithm id; "+ring" = the literal ring transport (CF_ALGO_RING_LINKS)."""
     from paper_2504_09014_b200 import _lib
