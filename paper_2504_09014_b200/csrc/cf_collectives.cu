@@ -95,9 +95,18 @@ __device__ __forceinline__ void handshake(const RankCtx& rk, int n, uint64_t v, 
 // must be resident (the CTA budget / co-residency cap guarantees it).
 __device__ __forceinline__ void all_cta_barrier(const RankCtx& rk, int n, uint64_t v, bool gpu) {
   const int t = threadIdx.x, r = rk.rank, b = blockIdx.x, G = gridDim.x;
+#if CF_DROP_FENCE != 1
   fence_publish(gpu);
+#endif
   __syncthreads();
-  if (t < n) st_release(rk.sem[t] + sem_index(r, b), v, gpu);
+  if (t < n) {
+    CF_STRESS_AT(10);
+#if CF_DROP_FENCE == 1
+    st_relaxed(rk.sem[t] + sem_index(r, b), v, gpu);
+#else
+    st_release(rk.sem[t] + sem_index(r, b), v, gpu);
+#endif
+  }
   for (int i = t; i < n * G; i += blockDim.x) wait_geq(rk.sem[r] + sem_index(i / G, i % G), v, rk.st, gpu);
   __syncthreads();
 }

@@ -119,6 +119,20 @@ def _inproc_loop(w, n, iters, out):
                     _record(out, f"{algo}:{elems}:{it}", all(np.array_equal(g, x) for g, x in zip(got, want)))
                 except DeadlockError:
                     _deadlock(out)
+        # K13 two-shot (phase 1 over every CTA, all-CTA barrier): integer-valued
+        # f32 rows, so the residual output is exact
+        from paper_2504_09014_b200 import allreduce_add_rmsnorm
+        rows, hidden = 2 * n + 3, 512
+        g = torch.Generator().manual_seed(it)
+        xs = [torch.randint(-64, 64, (rows, hidden), generator=g).float().cuda() for _ in range(n)]
+        res = [torch.randint(-64, 64, (rows, hidden), generator=g).float().cuda() for _ in range(n)]
+        try:
+            _, ro = allreduce_add_rmsnorm(w, xs, res, torch.ones(hidden, device="cuda"), algo="2pa")
+            w.check_device_error()
+            h = sum(x for x in xs)
+            _record(out, f"k13:{it}", all(torch.equal(ro[r], h + res[r]) for r in range(n)))
+        except DeadlockError:
+            _deadlock(out)
 
 
 def _mp_worker(rank, world, port, iters, q):
