@@ -127,7 +127,8 @@ def _inproc_loop(w, n, iters, out):
         xs = [torch.randint(-64, 64, (rows, hidden), generator=g).float().cuda() for _ in range(n)]
         res = [torch.randint(-64, 64, (rows, hidden), generator=g).float().cuda() for _ in range(n)]
         try:
-            _, ro = allreduce_add_rmsnorm(w, xs, res, torch.ones(hidden, device="cuda"), algo="2pa")
+            _, ro = allreduce_add_rmsnorm(w, xs, [x.clone() for x in res], torch.ones(hidden, device="cuda"),
+                                          algo="2pa")   # resid_out defaults to the residuals, in place
             w.check_device_error()
             h = sum(x for x in xs)
             _record(out, f"k13:{it}", all(torch.equal(ro[r], h + res[r]) for r in range(n)))
