@@ -1210,7 +1210,7 @@ __global__ void __launch_bounds__(512) ar_rmsnorm_kernel(const __grid_constant__
   TS_MARK();
   using A = typename Vec<T>::Acc;
   constexpr int V = Vec<T>::N;
-  constexpr int kCache = NR >= 8 ? 2 : 4;   // vectors of a thread's share held in registers between the passes
+  constexpr int kCache = (NR >= 8 || sizeof(T) >= 4) ? 2 : 4;   // vectors of a thread's share held in registers between the passes
   const int n = a.n, r = rk.rank;
   const bool push = a.push;
   // The epoch is needed only by the handshaking threads (t < n) and thread 0
@@ -1335,9 +1335,66 @@ __global__ void __launch_bounds__(512) ar_rmsnorm_kernel(const __grid_constant__
     for (size_t v = T0 + kCache * NT; v < nv; v += NT)
       st16(rk.out[r] + off + v * 16, normed(ld16(rk.out2[r] + off + v * 16), ld16(rk.weight + v * 16), inv));
   };
-  for (size_t row = blockIdx.x; row < a.rows; row += gridDim.x) {
-    finish_row(row);
-    TS_MARK();
+  if (!push) {
+    for (size_t row = blockIdx.x; row < a.rows; row += gridDim.x) {
+      finish_row(row);
+      TS_MARK();
+    }
+  } else {
+    // two-shot phase 2 touches local buffers only: software-pipelined over
+    // the CTA's rows -- the next row's h and residual loads are in flight
+    // while this row is reduced and stored; the weight is loaded once
+    uint4 hn[kCache], rn[kCache], wc[kCache];
+    auto issue = [&](size_t row) {
+      const size_t off = row * a.hidden * sizeof(T);
+#pragma unroll
+      for (int i = 0; i < kCache; i++)
+        if (T0 + i * NT < nv) {
+          hn[i] = ld16(rk.out[r] + off + (T0 + i * NT) * 16);
+          rn[i] = ld16(rk.resid + off + (T0 + i * NT) * 16);
+        }
+    };
+#pragma unroll
+    for (int i = 0; i < kCache; i++)
+      if (T0 + i * NT < nv) wc[i] = ld16(rk.weight + (T0 + i * NT) * 16);
+    if (blockIdx.x < a.rows) issue(blockIdx.x);
+    for (size_t row = blockIdx.x; row < a.rows; row += gridDim.x) {
+      const size_t off = row * a.hidden * sizeof(T);
+      uint4 hc[kCache], rc[kCache];
+#pragma unroll
+      for (int i = 0; i < kCache; i++) hc[i] = hn[i], rc[i] = rn[i];
+      if (row + gridDim.x < a.rows) issue(row + gridDim.x);
+      float ss = 0.f;
+#pragma unroll
+      for (int i = 0; i < kCache; i++)
+        if (T0 + i * NT < nv) {
+          hc[i] = resid_add(hc[i], rc[i], ss);   // hc[i] now holds ro
+          st16(rk.out2[r] + off + (T0 + i * NT) * 16, hc[i]);
+        }
+      for (size_t v = T0 + kCache * NT; v < nv; v += NT) {
+        const uint4 ro = resid_add(ld16(rk.out[r] + off + v * 16), ld16(rk.resid + off + v * 16), ss);
+        st16(rk.out2[r] + off + v * 16, ro);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      if ((T0 & 31) == 0) s_red[T0 >> 5] = ss;
+      __syncthreads();
+      if (T0 < 32) {
+        float t = T0 < (NT + 31) / 32 ? s_red[T0] : 0.f;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        if (T0 == 0) s_red[0] = t;
+      }
+      __syncthreads();
+      const float inv = rsqrtf(s_red[0] / (float)a.hidden + a.eps);
+      __syncthreads();   // s_red is reused by the next row
+#pragma unroll
+      for (int i = 0; i < kCache; i++)
+        if (T0 + i * NT < nv) st16(rk.out[r] + off + (T0 + i * NT) * 16, normed(hc[i], wc[i], inv));
+      for (size_t v = T0 + kCache * NT; v < nv; v += NT)
+        st16(rk.out[r] + off + v * 16, normed(ld16(rk.out2[r] + off + v * 16), ld16(rk.weight + v * 16), inv));
+      TS_MARK();
+    }
   }
   if (!push && !a.single_launch) handshake(rk, n, e * kPhases + 2, true, a.gpu_scope);
   end_call(rk, e);
