@@ -19,7 +19,7 @@ def main():
     w = make_world(1, n, devices=[0] * n)
     dev = w.device(0)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-    for nb in [1 << k for k in range(10, 23, 2)]:
+    for nb in [int(x) for x in os.environ.get("SIZES", ",".join(str(1 << k) for k in range(10, 23, 2))).split(",")]:
         c = nb // es
         xs = [torch.randn(c, device=dev).to(tdt) for _ in range(n)]
         ys = [torch.empty_like(x) for x in xs]
