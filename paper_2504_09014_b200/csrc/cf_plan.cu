@@ -1144,6 +1144,16 @@ cfStatus finalize(cfPlan* pl) {
     }
   fuse_packet_reads(pl);
   drop_redundant_syncs(pl);
+  // each data op's CTA slice: ceil(size / K) elements rounded up to whole
+  // 16-byte vectors (the interpreter multiplies, never divides)
+  {
+    const uint64_t V = 16 / (uint64_t)pl->es, Kk = (uint64_t)K;
+    for (auto& prog : pl->prog_ops)
+      for (auto& d : prog)
+        if (d.code == D_MULTI || d.code == D_COPY || d.code == D_PUT_PACKETS || d.code == D_READ_PACKETS ||
+            d.code == D_PORT_PUT)
+          d.per = ((d.size + Kk - 1) / Kk + V - 1) / V * V;
+  }
   // device tables per device group
   for (size_t gi = 0; gi < c->groups.size(); gi++) {
     Group G;
@@ -1285,6 +1295,7 @@ DevOp* bound_ops(const cfPlan* pl, Group& G, const PlanArgs& a, cudaStream_t st)
       if (data) {
         const int ns = (d.code == D_PUT_PACKETS && !(d.flags & F_PAIRED)) ? 1 : std::min<int>(d.nsrc, 8);
         h.size = d.size;
+        h.per = d.per;
         h.es = (uint32_t)pl->es;
         for (int k = 0; k < ns; k++)
           if (!((d.pkt_mask >> k) & 1u) && d.src[k].buf == kAbsolute) h.src[h.nsrc++] = (const char*)d.src[k].off;

@@ -116,7 +116,9 @@ struct DevOp {
   DRef dst[kMaxDst];
   uint32_t llflag_k[kMaxSrc];  // plan flag of packet source k (READ_PACKETS batch, MULTI pkt_mask)
   uint32_t pkt_mask;           // D_MULTI: sources read straight from LL16 packet areas
-  uint32_t pad_[3];
+  uint32_t pad_;
+  uint64_t per;                // data ops: elements per CTA slice, whole 16-byte vectors (set at
+                               // load time from K, so the interpreter never divides)
 };
 
 // Per-rank execution state of one loaded plan (in the plan heap of the rank).
@@ -164,7 +166,7 @@ struct PlanArgs {
   int npf;
   struct Prefetch {
     const char* src[8];
-    uint64_t size;       // the op's elements (sliced over the K CTAs like the op)
+    uint64_t size, per;  // the op's elements and its CTA slice (DevOp::per)
     uint32_t nsrc, es;   // sources; bytes per element of the ranges (packet ranges: 2 x)
   } pf[32];
 };

@@ -153,10 +153,8 @@ template <typename T>
 __device__ __noinline__ void multi_fast(const DevOp& op, uint64_t lo, uint64_t hi);
 
 // This CTA's slice [lo, hi) of an op's elements: contiguous, whole vectors.
-template <typename T>
-__device__ __forceinline__ void slice(uint64_t size, int K, int j, uint64_t& lo, uint64_t& hi) {
-  constexpr int V = 16 / sizeof(T);
-  const uint64_t per = ((size + K - 1) / K + V - 1) / V * V;
+// (`per` = DevOp::per, computed at load time: no division on the device)
+__device__ __forceinline__ void slice(uint64_t size, uint64_t per, int j, uint64_t& lo, uint64_t& hi) {
   lo = min((uint64_t)j * per, size);
   hi = min(lo + per, size);
 }
@@ -164,7 +162,7 @@ __device__ __forceinline__ void slice(uint64_t size, int K, int j, uint64_t& lo,
 template <typename T>
 __device__ __forceinline__ void data_op(const PlanArgs& a, const DevOp& op, int j, uint64_t e, RankState* rs) {
   uint64_t lo, hi;
-  slice<T>(op.size, a.K, j, lo, hi);
+  slice(op.size, op.per, j, lo, hi);
   if (lo >= hi) return;
   if ((op.flags & F_VEC) && op.code == D_MULTI && op.nsrc <= 8 && !op.pkt_mask) {
     constexpr int V = 16 / sizeof(T);
@@ -323,10 +321,8 @@ constexpr int kPktU = CF_PLAN_PKT_U;
 // packet {d0, f, d1, f}; LL8: one reference packet {d, f} per 4 payload bytes.
 template <typename T>
 __device__ __noinline__ void packet_op(const DevOp& op, int K, int j, uint32_t fstride, uint64_t e, RankState* rs) {
-  constexpr int V = 16 / sizeof(T);
-  const uint64_t size = op.size;
-  const uint64_t per = ((size + K - 1) / K + V - 1) / V * V;
-  const uint64_t lo = min((uint64_t)j * per, size), hi = min(lo + per, size);
+  uint64_t lo, hi;
+  slice(op.size, op.per, j, lo, hi);
   if (lo >= hi) return;
   const bool put = op.code == D_PUT_PACKETS;
   // batched ops: a put sends one payload to ndst packet ranges (one plan op
@@ -343,6 +339,7 @@ __device__ __noinline__ void packet_op(const DevOp& op, int K, int j, uint32_t f
     const uint32_t nu = (uint32_t)(u1 - u0), items = nu * (uint32_t)nb;
     const bool paired = op.flags & F_PAIRED;
     constexpr int U = kPktU;
+    const float rnu = 1.0f / (float)nu;   // item w -> range w / nu without an integer division
     if (nu >= 4 * blockDim.x || (put && !paired)) {
       // enough units to keep every thread busy (or one payload to many
       // ranges): one unit per thread, all nb ranges' accesses in flight
@@ -355,7 +352,10 @@ __device__ __noinline__ void packet_op(const DevOp& op, int K, int j, uint32_t f
 #pragma unroll
       for (int i = 0; i < U; i++) {
         const uint32_t w = w0 + (uint32_t)i * blockDim.x;
-        kk[i] = w < items ? w / nu : (uint32_t)kMaxDst;
+        uint32_t q = (uint32_t)((float)w * rnu);   // exact after one correction (w < 2^24)
+        q -= q * nu > w;
+        q += (q + 1) * nu <= w;
+        kk[i] = w < items ? q : (uint32_t)kMaxDst;
         uu[i] = u0 + (w - kk[i] * nu);
       }
       if (put) {
@@ -423,11 +423,8 @@ __device__ __noinline__ void port_op(const PlanArgs& a, const DevOp& op, int ran
   if (threadIdx.x != 0) return;
   uint64_t src = 0, dst = 0, bytes = 0;
   if (op.code == D_PORT_PUT) {
-    const int K = a.K;
-    constexpr int V = 16 / sizeof(T);
-    const uint64_t size = op.size;
-    const uint64_t per = ((size + K - 1) / K + V - 1) / V * V;
-    const uint64_t lo = min((uint64_t)j * per, size), hi = min(lo + per, size);
+    uint64_t lo, hi;
+    slice(op.size, op.per, j, lo, hi);
     if (hi > lo) {
       src = (uint64_t)(ptr(op.src[0]) + lo * sizeof(T));
       dst = (uint64_t)(ptr(op.dst[0]) + lo * sizeof(T));
@@ -536,7 +533,7 @@ __global__ void __launch_bounds__(CF_PLAN_THREADS) plan_kernel(const __grid_cons
   if (pid < a.npf) {   // the first data op's source lines, requested while its op is staged
     const PlanArgs::Prefetch& h = a.pf[pid];
     uint64_t lo, hi;
-    slice<T>(h.size, a.K, j, lo, hi);
+    slice(h.size, h.per, j, lo, hi);
     for (uint32_t k = 0; k < h.nsrc; k++)
       for (uint64_t b = lo * h.es + threadIdx.x * 128ull; b < hi * h.es; b += blockDim.x * 128ull)
         asm volatile("prefetch.global.L2 [%0];" ::"l"(h.src[k] + b));
@@ -594,7 +591,7 @@ __global__ void __launch_bounds__(CF_PLAN_THREADS) plan_kernel(const __grid_cons
         if constexpr (CLS == kClsHB) {
           // plain vectors only in this class: no packet sources
           uint64_t lo, hi;
-          slice<T>(op.size, a.K, j, lo, hi);
+          slice(op.size, op.per, j, lo, hi);
           constexpr int V = 16 / sizeof(T);
           const uint64_t full = lo + (hi > lo ? (hi - lo) / V * V : 0);
           if ((op.flags & F_VEC) && op.code == D_MULTI && op.nsrc <= 8) {
