@@ -400,7 +400,13 @@ def run_gpu_arm(args):
     del outs
 
     sweep = []
+    tuned = None
     if not args.no_sweep:
+        # measured selection on this box (World.tune): AUTO rows of the sweep follow it
+        tr = w.tune(kind="allreduce", dtype="bf16", iters=10)
+        tuned = {"table": [[int(b), a] for b, a in tr["table"]],
+                 "note": "fastest AllReduce per size, CUDA graphs on this box (World.tune -> cfCommSetSelection); "
+                         "the sweep's 'auto' rows use it"}
         sweep = run_sweep(w, args)
     cpu = cpu_baseline(n, count, HEAD_DTYPE, "2pa")
     line = {"metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": 1,
@@ -415,7 +421,7 @@ def run_gpu_arm(args):
             "latency_us": round(t * 1e6, 2), "algbw_gbs": round(HEAD_BYTES / t / 1e9, 2),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": args.steps, "clocks": clk.summary(),
-            "wall_s_timed": round(wall, 4), "sweep": sweep}
+            "wall_s_timed": round(wall, 4), "tuned_selection": tuned, "sweep": sweep}
     print(json.dumps(line))
     w.close()
     return 0
@@ -835,7 +841,7 @@ def run_multi_gpu(args):
     big = GiB if not one_gpu else 64 * MiB
     nvls_err = None
     try:
-        sym_mode = comm.setup_symmetric(2 * big + 2 * HEAD_BYTES + 64 * MiB, mode="emulate" if one_gpu else "auto")
+        sym_mode = comm.setup_symmetric(2 * big + 2 * HEAD_BYTES + 192 * MiB, mode="emulate" if one_gpu else "auto")
     except Exception as e:
         sym_mode, nvls_err = -1, f"{type(e).__name__}: {e}"[:200]
     nvls = sym_mode in (1, 2)
@@ -859,6 +865,20 @@ def run_multi_gpu(args):
     # the selector's pick for the headline (AUTO: in-place NVLS on a multicast
     # heap, else the two-shot HB kernel)
     head_algo = "switch_2pa" if (nvls and sym_mode == 1) else "2pa"
+    # measured selection over NVLink (Communicator.tune, max over ranks, one
+    # table on every rank; NVLS start size on a multicast heap): the sweep's
+    # 'auto' rows follow it
+    tuned = None
+    if not args.no_sweep:
+        try:
+            tr = comm.tune(kind="allreduce", dtype="bf16", iters=10, nvls=nvls and sym_mode == 1)
+            tuned = {"table": [[int(b), a] for b, a in tr["table"]], "nvls_min_bytes": tr["nvls_min_bytes"],
+                     "times_us": {a: [None if v is None else round(v * 1e6, 2) for v in ts]
+                                  for a, ts in tr["times"].items()},
+                     "sizes": tr["sizes"]}
+        except Exception as e:   # the line still prints with the built-in table
+            tuned = {"error": f"{type(e).__name__}: {e}"[:200]}
+            comm.clear_device_error()
     for _ in range(args.warmup):
         comm.all_reduce(send, recv, algo=head_algo)
     torch.cuda.synchronize(dev)
@@ -912,7 +932,7 @@ def run_multi_gpu(args):
                     "h2d_bytes_per_step": HEAD_BYTES, "d2h_bytes_per_step": HEAD_BYTES,
                     "ms_per_step": round(te * 1e3, 3),
                     "api": "Communicator.all_reduce_host (cfAllReduceHostStaged), pinned host tensors"},
-            "gpu_launches": args.steps, "clocks": clk.summary(),
+            "gpu_launches": args.steps, "clocks": clk.summary(), "tuned_selection": tuned,
             "sweep": {"config": "bf16 AllReduce (+ C5 DSL plans, AllGather, ReduceScatter, NVLS when the "
                                 "box builds a multicast object): libcf (selector's pick) in a CUDA graph and "
                                 "eager vs NCCL 2.28 in a CUDA graph on default buffers (nccl_graph) and on "

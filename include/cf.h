@@ -294,6 +294,22 @@ CF_API cfStatus cfAllReduceAddRMSNorm(cfComm_t comm, const void* const* send, co
  * a partner that is not scheduled. */
 CF_API cfStatus cfCommSetCtaBudget(cfComm_t comm, int algo, int ctas);
 
+/* Measured selection table ("measured crossover table per
+ * (collective, dtype, n) from the sweep"; the Python Communicator.tune /
+ * World.tune measure it on the live GPUs and install the same table on every
+ * rank).  CF_ALGO_AUTO then picks algos[i] for the first i with
+ * nbytes <= max_bytes[i] (the last entry also covers every larger size); LL
+ * picks beyond cfConfig.ll_max_bytes fall back to CF_ALGO_2PA.  coll: 0
+ * AllReduce (per-rank bytes), 1 AllGather (output bytes), 2 ReduceScatter
+ * (input bytes).  nentries = 0 restores the built-in table.  The table must be
+ * the same on every rank (AUTO is then rank-uniform). */
+CF_API cfStatus cfCommSetSelection(cfComm_t comm, int coll, cfDtype dtype, int nentries, const size_t* max_bytes,
+                                   const int* algos);
+/* Smallest per-rank AllReduce that AUTO runs in place on the NVLS switch when
+ * the buffers are symmetric and multicast-bound (default 1 MiB; SIZE_MAX =
+ * never).  Same on every rank. */
+CF_API cfStatus cfCommSetNvlsMinBytes(cfComm_t comm, size_t bytes);
+
 /* The algorithm the measured selector picks (cf/collectives.py:473-491).
  * collective: 0 = allreduce, 1 = allgather, 2 = reducescatter; nbytes as the
  * reference counts them (AG: output bytes). */

@@ -43,6 +43,7 @@ EXPORTS = (
     "cfPlanInfo", "cfPlanLastDeviceError", "cfPlanClearDeviceError", "cfPlanGetHandle", "cfPlanConnect", "cfPlanDestroy",
     "cfDslBuild", "cfDslLower", "cfSymHeapCreate", "cfSymHeapMapPeer", "cfSymHeapMulticast",
     "cfSymHeapInfo", "cfMemAlloc", "cfMemFree", "cfSwitchChannelCreate", "cfCommSetCtaBudget",
+    "cfCommSetSelection", "cfCommSetNvlsMinBytes",
 )
 
 
@@ -96,6 +97,8 @@ _PROTOS = {
     "cfPlanLastDeviceError": ([vp, P(i32)], i32),
     "cfPlanClearDeviceError": ([vp], i32),
     "cfCommSetCtaBudget": ([vp, i32, i32], i32),
+    "cfCommSetSelection": ([vp, i32, i32, i32, P(sz), P(i32)], i32),
+    "cfCommSetNvlsMinBytes": ([vp, sz], i32),
     "cfSymHeapCreate": ([vp, sz, i32, P(i32)], i32),
     "cfSymHeapMapPeer": ([vp, i32, i32], i32),
     "cfSymHeapMulticast": ([vp, i32, P(i32)], i32),

@@ -15,7 +15,7 @@ import ctypes
 from . import _lib
 from .collectives import _algo_id
 from .dtypes import CODES, from_torch
-from .errors import ShapeError
+from .errors import BadSizeError, ShapeError
 
 
 def all_gather_bytes(blob: bytes, group=None) -> list:
@@ -308,6 +308,78 @@ class Communicator:
                 _lib.check(L.cfSymHeapMulticast(self._comm, 3, ctypes.byref(mfd)))
                 self._sym_mode = 0
         return self._sym_mode
+
+    def tune(self, kind: str = "allreduce", dtype: str = "bf16", sizes=None, algos=None, iters: int = 10,
+             install: bool = True, nvls: bool = True) -> dict:
+        """Collective: time every candidate algorithm at each size on this
+        rank's GPU (CUDA graphs, every replay preceded by a bootstrap barrier),
+        take the max over ranks, and install the same fastest-per-size table on
+        every rank (cfCommSetSelection; see tune.py).  On a multicast heap the
+        smallest size from which in-place NVLS wins is measured and installed
+        too (cfCommSetNvlsMinBytes).  Buffers come from the symmetric heap when
+        there is one, else they are registered for the call.  Returns
+        {"table", "sizes", "times", "nvls_min_bytes"}."""
+        import torch
+        import torch.distributed as dist
+        from . import tune as T
+        from .dtypes import ELEM_SIZE, torch_dtype
+        L = _lib.lib()
+        sizes = sorted(sizes or T.DEFAULT_SIZES)
+        n, es, tdt = self.nranks, ELEM_SIZE[dtype], torch_dtype(dtype)
+        ll_max = (4 << 20)
+        sym = getattr(self, "_sym_mode", -1)
+        per_in = max(sizes) // es if kind == "allreduce" else max(1, max(sizes) // es // n)
+        per_out = per_in if kind == "allreduce" else per_in * n
+        if sym >= 0:
+            x, y = self.alloc_symmetric(per_in, tdt), self.alloc_symmetric(per_out, tdt)
+        else:
+            x = torch.empty(per_in, device=self.device, dtype=tdt)
+            y = torch.empty(per_out, device=self.device, dtype=tdt)
+            self.register(x)
+            self.register(y)
+        x.copy_(torch.randn(per_in, device=self.device).to(tdt))
+        fn = {"allreduce": L.cfAllReduce, "allgather": L.cfAllGather}[kind]
+        barrier = lambda: dist.barrier(group=self.group)   # noqa: E731
+        names = list(algos or T.CANDIDATES[kind])
+        if nvls and kind == "allreduce" and sym == 1:
+            names.append("switch_2pa")
+        local = torch.full((len(names), len(sizes)), -1.0, dtype=torch.float64)
+        for i, nb in enumerate(sizes):
+            cnt = max(1, nb // es) if kind == "allreduce" else max(1, nb // es // n)
+            oc = cnt if kind == "allreduce" else cnt * n
+            for k, a in enumerate(names):
+                if a not in T.candidates(kind, ll_max, nb, [a]):
+                    continue
+                aid = T.algo_id(a)
+                xi, yi = x[:cnt], y[:oc]
+                try:   # validation errors are raised before any launch, identically on every rank
+                    local[k, i] = T.time_graph(self.device, lambda: self._call(fn, xi, yi, cnt, aid, None), iters,
+                                               before=barrier)
+                except BadSizeError:   # beyond this algorithm's capacity (e.g. the LL scratch)
+                    pass
+        self.check_device_error()
+        dist.all_reduce(local, op=dist.ReduceOp.MAX, group=self.group)   # slowest rank, same on all ranks
+        times = {a: [None if v < 0 else float(v) for v in local[k].tolist()] for k, a in enumerate(names)}
+        nv = times.pop("switch_2pa", None)
+        table = T.selection_from_times(sizes, times)
+        nvls_min = None
+        if nv is not None:
+            best = [min((t[i] for t in times.values() if t[i] is not None), default=None) for i in range(len(sizes))]
+            nvls_min = T.nvls_min_from_times(sizes, nv, best)
+        if install:
+            T.install(self._comm, kind, dtype, table)
+            if nv is not None:
+                _lib.check(L.cfCommSetNvlsMinBytes(self._comm, ctypes.c_size_t(nvls_min if nvls_min else
+                                                                              (1 << 64) - 1)))
+        if sym >= 0:
+            self.free_symmetric(x)
+            self.free_symmetric(y)
+        else:
+            self.deregister(x)
+            self.deregister(y)
+        if nv is not None:
+            times["switch_2pa"] = nv
+        return {"table": table, "sizes": sizes, "times": times, "nvls_min_bytes": nvls_min}
 
     def disable_switch(self) -> None:
         """Collective: stop using the NVLS switch on this heap (every rank calls

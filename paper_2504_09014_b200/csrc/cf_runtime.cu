@@ -178,12 +178,20 @@ static bool ag_bulk_enabled() {
   return on;
 }
 
-// AUTO picks the in-place NVLS kernel for symmetric buffers from this size up
-// (per rank; provisional until measured on a multicast-capable box)
-constexpr size_t kNvlsAutoBytes = (size_t)1 << 20;
-
 static int select_algo(const cfComm* c, int coll, size_t nbytes, int dtype) {
-  (void)dtype;
+  // a measured table (cfCommSetSelection: Communicator.tune / World.tune)
+  // wins over the built-in one; LL picks beyond the LL capacity fall back
+  if (coll >= 0 && coll < 3 && dtype >= 0 && dtype < 4 && !c->select_table[coll][dtype].empty()) {
+    const auto& t = c->select_table[coll][dtype];
+    int algo = t.back().second;
+    for (const auto& e : t)
+      if (nbytes <= e.first) {
+        algo = e.second;
+        break;
+      }
+    if ((algo == CF_ALGO_1PA || algo == CF_ALGO_2PA_LL) && nbytes > c->cfg.ll_max_bytes) algo = CF_ALGO_2PA;
+    return algo;
+  }
   const bool coresident = c->groups.size() == 1 && c->local.size() > 1;
   if (coll == 1) return CF_ALGO_ALLPAIRS_AG;
   if (coll == 2) return CF_ALGO_RS_DIRECT;
@@ -582,6 +590,35 @@ extern "C" cfStatus cfCommSetCtaBudget(cfComm_t c, int algo, int ctas) {
   return CF_OK;
 }
 
+extern "C" cfStatus cfCommSetSelection(cfComm_t c, int coll, cfDtype dtype, int nentries, const size_t* max_bytes,
+                                       const int* algos) {
+  if (!c) return fail(CF_E_CONFIG, "null communicator");
+  if (coll < 0 || coll > 2) return fail(CF_E_CONFIG, "collective must be 0 (AllReduce), 1 (AllGather), 2 (ReduceScatter)");
+  if ((int)dtype < 0 || (int)dtype > 3) return fail(CF_E_SHAPE, "unknown dtype %d", (int)dtype);
+  if (nentries < 0 || (nentries > 0 && (!max_bytes || !algos))) return fail(CF_E_CONFIG, "bad selection table");
+  std::vector<std::pair<size_t, int>> t;
+  for (int i = 0; i < nentries; i++) {
+    const int base = algos[i] & ~CF_ALGO_RING_LINKS;
+    const bool ring = base == CF_ALGO_2PR || base == CF_ALGO_RING_AG || base == CF_ALGO_RING_RS;
+    if ((algos[i] & CF_ALGO_RING_LINKS) && !ring) return fail(CF_E_NO_ALGO, "CF_ALGO_RING_LINKS on algorithm %d", base);
+    const bool ok = coll == 0 ? (base == CF_ALGO_1PA || base == CF_ALGO_1PA_HB || base == CF_ALGO_2PA ||
+                                 base == CF_ALGO_2PA_LL || base == CF_ALGO_2PR)
+                  : coll == 1 ? (base == CF_ALGO_ALLPAIRS_AG || base == CF_ALGO_RING_AG)
+                              : (base == CF_ALGO_RS_DIRECT || base == CF_ALGO_RING_RS);
+    if (!ok) return fail(CF_E_NO_ALGO, "algorithm %d cannot serve collective %d from a selection table", algos[i], coll);
+    if (i && max_bytes[i] <= max_bytes[i - 1]) return fail(CF_E_CONFIG, "selection table sizes must increase");
+    t.push_back({max_bytes[i], algos[i]});
+  }
+  c->select_table[coll][(int)dtype] = t;
+  return CF_OK;
+}
+
+extern "C" cfStatus cfCommSetNvlsMinBytes(cfComm_t c, size_t bytes) {
+  if (!c) return fail(CF_E_CONFIG, "null communicator");
+  c->nvls_min_bytes = bytes;
+  return CF_OK;
+}
+
 extern "C" cfStatus cfSelectAlgorithm(cfComm_t c, int coll, size_t nbytes, cfDtype dtype, int* algo) {
   if (!c || !algo) return fail(CF_E_CONFIG, "null argument");
   if (coll < 0 || coll > 2) return fail(CF_E_NO_ALGO, "unknown collective %d", coll);
@@ -894,7 +931,7 @@ extern "C" cfStatus cfAllReduce(cfComm_t c, const void* const* send, void* const
     // symmetric buffers on a real multicast heap: the in-place NVLS kernel
     // moves S per rank per direction on NVLink instead of 2(n-1)/n S
     // (provisional crossover until an NVLink sweep measures it)
-    if (sym_switch && c->sym.mode == 1 && bytes >= kNvlsAutoBytes) algo = CF_ALGO_SWITCH_2PA;
+    if (sym_switch && c->sym.mode == 1 && bytes >= c->nvls_min_bytes) algo = CF_ALGO_SWITCH_2PA;
   }
   if (algo == CF_ALGO_SWITCH_2PA && sym_switch) return nvls_direct(c, count, dtype, oi, oo, streams);
   if (algo == CF_ALGO_SWITCH_2PA && c->nvls.enabled) return nvls_allreduce(c, send, recv, count, dtype, streams);

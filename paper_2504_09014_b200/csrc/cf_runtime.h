@@ -162,6 +162,11 @@ struct cfComm {
   // the fused K13 kernel; budget_all applies to every algorithm without its own)
   int budget[CF_ALGO_COUNT + 1] = {};
   int budget_all = 0;
+  // measured selection tables (cfCommSetSelection) per (collective, dtype):
+  // {max bytes inclusive, algo}, the last entry covering every larger size;
+  // empty = the built-in table
+  std::vector<std::pair<size_t, int>> select_table[3][4];
+  size_t nvls_min_bytes = (size_t)1 << 20;   // AUTO: in-place NVLS from here (symmetric, multicast)
   cf::Nvls nvls;
   cf::SymHeap sym;
   cf::Proxy* proxy = nullptr;          // PortChannel proxy thread (started on demand)

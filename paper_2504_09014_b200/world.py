@@ -170,6 +170,43 @@ class World:
         aid = -1 if algo is None else (_lib.CF_ALGO_COUNT if algo == "fused" else _lib.ALGOS[algo])
         _lib.check(_lib.lib().cfCommSetCtaBudget(self.comm, aid, int(ctas)))
 
+    def tune(self, kind: str = "allreduce", dtype: str = "bf16", sizes=None, algos=None, iters: int = 10,
+             install: bool = True) -> dict:
+        """Measure every candidate algorithm at each size (CUDA graphs, L2 not
+        flushed) and install the fastest-per-size table for ``algo="auto"``
+        (cfCommSetSelection; see tune.py).  Ranks must share one device (the
+        co-resident world); returns {"table", "sizes", "times"}."""
+        import torch
+        from . import collectives as C
+        from . import tune as T
+        from .dtypes import ELEM_SIZE, torch_dtype
+        from .timing import _measure
+        if len(set(self.devices)) != 1:
+            raise TopologyError("World.tune times ranks that share one GPU; use Communicator.tune per GPU")
+        sizes = sorted(sizes or T.DEFAULT_SIZES)
+        n, es, tdt = self.num_ranks, ELEM_SIZE[dtype], torch_dtype(dtype)
+        ll_max = self.config.ll_max_bytes or (4 << 20)
+        per_in = max(sizes) // es if kind == "allreduce" else max(1, max(sizes) // es // n)
+        per_out = per_in if kind == "allreduce" else per_in * n
+        xs = [torch.randn(per_in, device=self.device(r)).to(tdt) for r in range(n)]
+        ys = [torch.empty(per_out, device=self.device(r), dtype=tdt) for r in range(n)]
+        names = list(algos or T.CANDIDATES[kind])
+        times = {a: [None] * len(sizes) for a in names}
+        for i, nb in enumerate(sizes):
+            cnt = max(1, nb // es) if kind == "allreduce" else max(1, nb // es // n)
+            oc = cnt if kind == "allreduce" else cnt * n
+            for a in T.candidates(kind, ll_max, nb, names):
+                aid = T.algo_id(a)
+                xi, yi = [x[:cnt] for x in xs], [y[:oc] for y in ys]
+                try:
+                    times[a][i] = _measure(self, lambda: C.run(kind, xi, yi, cnt, dtype, aid, self), iters, 3)
+                except BadSizeError:   # beyond this algorithm's capacity (e.g. the LL scratch)
+                    pass
+        table = T.selection_from_times(sizes, times)
+        if install:
+            T.install(self.comm, kind, dtype, table)
+        return {"table": table, "sizes": sizes, "times": times}
+
     # -- symmetric heap (cfSymHeapCreate / cfMemAlloc) ----------------------
 
     def symmetric_heap(self, nbytes: int, mode=None) -> int:

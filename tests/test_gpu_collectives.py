@@ -584,3 +584,45 @@ def test_host_buffer_allreduce_every_algorithm():
             for r in range(8):
                 assert not got[r].is_cuda
                 assert torch.equal(got[r].view(torch.int16), dev[r].cpu().view(torch.int16)), (elems, algo, var, r)
+
+
+def test_tune_installs_measured_selection():
+    """World.tune times every AllReduce candidate per size on the GPU, installs
+    the fastest-per-size table (cfCommSetSelection), AUTO and
+    Selector(measured=True) follow it, results stay exact; an empty table
+    restores the built-in one."""
+    import ctypes
+    from paper_2504_09014_b200 import Selector, _lib, collective
+    from paper_2504_09014_b200 import tune as T
+    from paper_2504_09014_b200.collectives import _COLL, _algo_id
+    from paper_2504_09014_b200.dtypes import CODES
+    n = 8
+    w = world(n)
+    sizes = [4096, 65536, 1 << 20, 4 << 20]
+
+    def pick(nb):
+        algo = ctypes.c_int()
+        _lib.check(_lib.lib().cfSelectAlgorithm(w.comm, _COLL["allreduce"], nb, CODES["bf16"],
+                                                ctypes.byref(algo)))
+        return algo.value
+
+    try:
+        res = w.tune(sizes=sizes, iters=5)
+        table = res["table"]
+        assert table and table[-1][0] == sizes[-1]
+        for i, nb in enumerate(sizes):   # the installed pick is the fastest measured at that size
+            best = min((t[i], a) for a, t in res["times"].items() if t[i] is not None)[1]
+            assert pick(nb) == T.algo_id(best), (nb, best)
+            d = Selector(measured=True).select("allreduce", nb, w.topology, world=w, dtype="bf16")
+            assert _algo_id("allreduce", d.name, d.variant) == pick(nb)
+        rng = np.random.default_rng(3)
+        for nb in sizes:   # AUTO on the tuned bf16 table: integer-valued sums are exact
+            ins = [(rng.integers(-8, 8, nb // 2).astype(np.float32).view(np.uint32) >> 16).astype(np.uint16)
+                   for _ in range(n)]
+            got = collective("allreduce", ins, w, dtype="bf16", selector=Selector(measured=True))
+            want = oracle.allreduce(ins, "oracle", "bf16")
+            for g, x in zip(got, want):
+                assert np.array_equal(g, x), nb
+    finally:
+        T.install(w.comm, "allreduce", "bf16", [])
+    assert pick(4096) == _lib.ALGOS["1pa_hb"]   # the built-in co-resident table again

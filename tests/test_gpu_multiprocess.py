@@ -68,6 +68,18 @@ def _worker(rank, world, port, q):
                 out[("rs", algo, elems)] = rs_out.cpu().numpy().copy()
             for t in (send, recv, ag, rs_in):
                 comm.deregister(t)
+        # measured selection: tuned on both GPUs' worth of ranks, same table on every rank
+        tuned = comm.tune(sizes=[4096, 65536, 1 << 20], iters=3)
+        out[("tune",)] = tuned["table"]
+        tin = torch.from_numpy(gen_inputs(world, 1 << 18, "f32", "int", 3)[rank]).cuda()
+        comm.register(tin)
+        tout = torch.empty_like(tin)
+        comm.register(tout)
+        comm.all_reduce(tin, tout, algo="auto")
+        torch.cuda.synchronize()
+        out[("tune_auto",)] = tout.cpu().numpy().copy()
+        comm.deregister(tin)
+        comm.deregister(tout)
         # pipelined host-buffer AllReduce (windows: >= 32 MiB per rank, ragged)
         he = (40 << 20) // 4 + 3
         hx = torch.from_numpy(gen_inputs(world, he, "f32", "uniform", 9)[rank]).pin_memory()
@@ -143,6 +155,10 @@ def test_two_processes_one_gpu_all_collectives():
             assert np.array_equal(res[r][("rs", "rs_direct", elems)].view(np.uint32), rs_want[r].view(np.uint32))
             for algo in ("ring_rs", "ring_rs+ring"):
                 assert np.array_equal(res[r][("rs", algo, elems)].view(np.uint32), rs_ring[r].view(np.uint32))
+    assert res[0][("tune",)] and res[0][("tune",)] == res[1][("tune",)]   # one table on every rank
+    tsum = oracle.allreduce(gen_inputs(world, 1 << 18, "f32", "int", 3), "oracle", "f32")
+    for r in range(world):
+        assert np.array_equal(res[r][("tune_auto",)], tsum[r])
     hins = gen_inputs(world, (40 << 20) // 4 + 3, "f32", "uniform", 9)
     hwant = oracle.allreduce(hins, "2pa", "f32")
     hsmall = oracle.allreduce([x[:1000] for x in hins], "2pa", "f32")
