@@ -942,6 +942,11 @@ def run_multi_gpu(args):
         if one_gpu:
             line["roofline"] = None
         else:
+            # north_star: every busbw also as a fraction of 900 GB/s per direction per GPU
+            for row in sweep:
+                for v in row.values():
+                    if isinstance(v, dict) and v.get("busbw") is not None:
+                        v["pct_of_900"] = round(100 * v["busbw"] / 900, 2)
             line["pct_of_900"] = round(100 * value / 900, 2)
             line["roofline"] = {"bound": "nvlink", "achieved": round(value, 1), "peak": 900.0,
                                 "unit": "GB/s", "frac": round(value / 900, 4), "traffic": None,
