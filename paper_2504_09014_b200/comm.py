@@ -91,6 +91,7 @@ class Communicator:
         allh = b"".join(handles)
         _lib.check(L.cfCommConnect(h, allh, _lib.CF_HANDLE_BYTES))
         self._registered = {}
+        self._ll_max = int(ll_max_bytes) or (4 << 20)   # libcf's default LL capacity
 
     @property
     def comm(self):
@@ -326,7 +327,7 @@ class Communicator:
         L = _lib.lib()
         sizes = sorted(sizes or T.DEFAULT_SIZES)
         n, es, tdt = self.nranks, ELEM_SIZE[dtype], torch_dtype(dtype)
-        ll_max = (4 << 20)
+        ll_max = self._ll_max
         sym = getattr(self, "_sym_mode", -1)
         per_in = max(sizes) // es if kind == "allreduce" else max(1, max(sizes) // es // n)
         per_out = per_in if kind == "allreduce" else per_in * n
