@@ -7,6 +7,18 @@ hand-written sm_100a kernels in ``libcf.so`` (C ABI: ``include/cf.h``).
 
 __version__ = "0.1.0"
 
+import os as _os
+
+# The PortChannel proxy (a host thread issuing copy-engine DMA on its own
+# stream) must not share a hardware work queue with the caller's stream: with
+# CUDA's default 8 connections, a collective kernel waiting for the proxy's
+# copy and the next kernel queued behind it on the caller's stream can land
+# the copy behind that next kernel -- a deadlock (measured: two back-to-back
+# port-channel plan calls time out with 1 or 8 connections, run with 32).  The
+# setting is read when the CUDA context is created, so it is applied here,
+# before any CUDA use, unless the caller chose a value.
+_os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 from .collectives import AlgoDescriptor, Selector, collective, required_multiple, select_algorithm
 from .errors import CommforgeError
 from .executor import RunResult, Runtime

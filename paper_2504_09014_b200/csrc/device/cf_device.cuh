@@ -22,6 +22,9 @@
 //   - multimem.ld_reduce / multimem.st on NVLS multicast addresses.
 #pragma once
 #include <cstdint>
+#ifdef CF_WAIT_DEBUG
+#include <cstdio>
+#endif
 #include <cuda_fp16.h>
 #include <cuda_bf16.h>
 
@@ -264,6 +267,11 @@ __device__ __forceinline__ bool wait_geq(const uint64_t* sem, uint64_t target, R
     if ((it & 255u) == 0) {
       if (*(volatile uint32_t*)&st->error != kDevOk) return false;
       if (globaltimer() - t0 > limit) {
+#ifdef CF_WAIT_DEBUG
+        printf("wait timeout: block %d thread %d sem %p target %llu value %llu\n", (int)blockIdx.x,
+               (int)threadIdx.x, (const void*)sem, (unsigned long long)target,
+               (unsigned long long)ld_wait(sem, gpu));
+#endif
         atomicExch(&st->error, (uint32_t)kDevTimeout);
         return false;
       }

@@ -130,6 +130,30 @@ def test_port_channel_plans_at_size(algo, var):
         assert np.array_equal(got[r].view(np.uint32), want[r].view(np.uint32)), r
 
 
+def test_port_plan_back_to_back_calls_do_not_deadlock():
+    """Four port-channel plan calls queued back to back (no host sync): the
+    proxy's copies must not queue behind the next plan kernel on a shared
+    hardware queue (the package raises CUDA_DEVICE_MAX_CONNECTIONS before the
+    context exists; with CUDA's default 8 the second call timed out)."""
+    import os
+    import torch
+    from paper_2504_09014_b200 import collectives as C
+    assert int(os.environ.get("CUDA_DEVICE_MAX_CONNECTIONS", "8")) >= 32
+    n = 8
+    w = world(n)
+    ins = gen_inputs(n, 1 << 18, "f32", "int", 8)
+    rt = C._plan_runtime(w, "allreduce", "2pa", "port", 1 << 18, "f32")
+    xs = [torch.from_numpy(x).to(w.device(r)) for r, x in enumerate(ins)]
+    ys = [torch.empty_like(x) for x in xs]
+    for _ in range(4):
+        rt.run_raw(xs, ys)
+    w.synchronize()
+    rt.check_device_error()
+    want = oracle.allreduce(ins, "2pa", "f32")
+    for r in range(n):
+        assert np.array_equal(ys[r].cpu().numpy(), want[r]), r
+
+
 def test_wait_without_signal_raises_deadlock():
     """reference test_executor.py:77-89, as a device spin timeout."""
     from paper_2504_09014_b200 import Runtime, make_world
