@@ -879,6 +879,28 @@ def run_multi_gpu(args):
         except Exception as e:   # the line still prints with the built-in table
             tuned = {"error": f"{type(e).__name__}: {e}"[:200]}
             comm.clear_device_error()
+    head_pick = None
+    if nvls and sym_mode == 1:
+        # the headline size is above the tuning ladder: NVLS in place vs the
+        # two-shot kernel measured here (max over ranks), the faster one is timed
+        cand = {}
+        for name in ("switch_2pa", "2pa"):
+            for _ in range(2):
+                comm.all_reduce(send, recv, algo=name)
+            torch.cuda.synchronize(dev)
+            dist.barrier()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(3):
+                comm.all_reduce(send, recv, algo=name)
+            b.record(stream)
+            b.synchronize()
+            cand[name] = a.elapsed_time(b) / 3
+        allc = [None] * world
+        dist.all_gather_object(allc, cand)
+        worst = {k: max(c[k] for c in allc) for k in cand}
+        head_algo = min(worst, key=worst.get)
+        head_pick = {k: round(v * 1e3, 1) for k, v in worst.items()}   # us per call, max over ranks
     for _ in range(args.warmup):
         comm.all_reduce(send, recv, algo=head_algo)
     torch.cuda.synchronize(dev)
@@ -923,6 +945,7 @@ def run_multi_gpu(args):
             "config": {"workload": f"AllReduce {HEAD_DTYPE}, {where}, {HEAD_BYTES // MiB} MiB per rank "
                                    "(C4 shape)", "ranks": world,
                        "algo": head_algo + (" (in place, symmetric buffers)" if head_algo == "switch_2pa" else ""),
+                       "headline_pick_us": head_pick,
                        "buffers": "symmetric heap (cfMemAlloc)" if sym_mode >= 0 else "registered torch tensors",
                        "parallelism": f"{world} GPUs" if not one_gpu else f"{world} processes / 1 GPU",
                        "l2": "inputs larger than L2 (headline); sweep rows < 64 MiB flush L2 between "
