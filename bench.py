@@ -880,7 +880,7 @@ def run_multi_gpu(args):
             tuned = {"error": f"{type(e).__name__}: {e}"[:200]}
             comm.clear_device_error()
     head_pick = None
-    if nvls and sym_mode == 1:
+    if nvls:   # (emulated switch on a 1-GPU path check: exercises the same selection)
         # the headline size is above the tuning ladder: NVLS in place vs the
         # two-shot kernel measured here (max over ranks), the faster one is timed
         cand = {}
