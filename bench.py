@@ -152,21 +152,23 @@ def run_reference_arm(args):
     from oracle import oracle
     es = 2
     full = HEAD_BYTES // es
-    ins = bench_inputs(N_SIM, full, 78)
+    # the cf arm's rank count: 8 simulated ranks at N=1, one rank per GPU at N>1
+    nr = args.gpus if args.gpus > 1 else N_SIM
+    ins = bench_inputs(nr, full, 78)
     cpu_reference_steps(ins, HEAD_DTYPE, "2pa", max(1, args.warmup))
     ts = cpu_reference_steps(ins, HEAD_DTYPE, "2pa", args.steps)
     t = float(np.mean(ts))
-    v = busbw(HEAD_BYTES, t, N_SIM)
+    v = busbw(HEAD_BYTES, t, nr)
     line = {"impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": "GB/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(t * 1e3, 3), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": HEAD_DTYPE, "data": "synthetic",
-            "config": {"workload": f"AllReduce {HEAD_DTYPE} {N_SIM} ranks, {HEAD_BYTES // MiB} MiB "
+            "config": {"workload": f"AllReduce {HEAD_DTYPE} {nr} ranks, {HEAD_BYTES // MiB} MiB "
                                    "per rank (C4 shape), two-shot (2pa) order",
                        "sample_bytes_per_rank": HEAD_BYTES, "same_config": True},
             "cpu_baseline": {"value": round(v, 4), "unit": "GB/s", "cores": oracle.max_threads(),
                              "kind": "port",
-                             "sample": f"the full workload every step: {N_SIM} x {HEAD_BYTES // MiB} MiB "
+                             "sample": f"the full workload every step: {nr} x {HEAD_BYTES // MiB} MiB "
                                        "(oracle/ C port of the reference arithmetic, pthreads)"},
             "e2e": {"value": round(v, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
