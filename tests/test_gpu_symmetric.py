@@ -330,7 +330,12 @@ def test_nvls_multicast_in_process_world():
     n = min(_ngpus(), 8)
     w = make_world(1, n, devices=list(range(n)), spin_timeout_ms=10000)
     try:
-        if w.symmetric_heap(HEAP, mode=1 if w.multicast_supported() else 0) != 1:
+        from paper_2504_09014_b200.errors import CommforgeError
+        try:
+            mode = w.symmetric_heap(HEAP, mode=1 if w.multicast_supported() else 0)
+        except CommforgeError as e:   # the driver refused the multicast object (no fabric manager / IMEX)
+            pytest.skip(f"no multicast object on this box: {e}")
+        if mode != 1:
             pytest.skip("no multicast object on this box")
         for dt in ("bf16", "f32", "i32"):
             elems = n * 65536 + 3
