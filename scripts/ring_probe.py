@@ -9,7 +9,7 @@ sys.path.insert(0, ROOT)
 
 def main():
     import torch
-    from bench import time_coll
+    from bench import algo_id, time_coll
     from paper_2504_09014_b200 import _lib, make_world
     n = 8
     w = make_world(1, n, devices=[0] * n)
@@ -24,12 +24,12 @@ def main():
         fl = flush if nb < 64 << 20 else None
         it = 20 if nb <= 16 << 20 else 5
         row = []
-        for kind, algo, ins, outs, c in (("reducescatter", "ring_rs", send, rs_out, cnt // n),
+        for kind, algo, ins, outs, c in (("reducescatter", "ring_rs+ring", send, rs_out, cnt // n),
                                          ("reducescatter", "rs_direct", send, rs_out, cnt // n),
-                                         ("allgather", "ring_ag", ag_in, ar_out, cnt // n),
-                                         ("allreduce", "2pr", send, ar_out, cnt),
+                                         ("allgather", "ring_ag+ring", ag_in, ar_out, cnt // n),
+                                         ("allreduce", "2pr+ring", send, ar_out, cnt),
                                          ("allreduce", "2pa", send, ar_out, cnt)):
-            t = time_coll(w, kind, ins, outs, c, "bf16", _lib.ALGOS[algo], it, 3, fl)
+            t = time_coll(w, kind, ins, outs, c, "bf16", algo_id(algo), it, 3, fl)
             row.append(f"{algo} {t * 1e6:8.1f}")
         print(f"{nb:>10} B  " + " | ".join(row), flush=True)
     w.close()
