@@ -25,7 +25,8 @@ from .executor import RunResult, Runtime
 from .fused import allreduce_add_rmsnorm
 from .lowering import LoweringParams, ProgramGraph, lower
 from .plan import ExecutionPlan, parse_plan, serialize_plan, validate_plan
-from .timing import BenchRow, CostParams, algobw, busbw, rows_to_csv, run_benchmark
+from .timing import (BenchRow, CostParams, algobw, busbw, rows_to_csv, run_benchmark, simulate_timed,
+                     transfer_time)
 from .world import Topology, World, make_world
 
 SimWorld = World  # the reference's name for the world type (cf/world.py:80)
@@ -34,5 +35,6 @@ __all__ = [
     "AlgoDescriptor", "BenchRow", "CommforgeError", "CostParams", "allreduce_add_rmsnorm", "algobw", "busbw",
     "ExecutionPlan", "LoweringParams", "ProgramGraph", "RunResult", "Runtime", "Selector", "SimWorld",
     "Topology", "World", "collective", "lower", "make_world", "parse_plan", "required_multiple",
-    "rows_to_csv", "run_benchmark", "select_algorithm", "serialize_plan", "validate_plan",
+    "rows_to_csv", "run_benchmark", "select_algorithm", "serialize_plan", "simulate_timed", "transfer_time",
+    "validate_plan",
 ]

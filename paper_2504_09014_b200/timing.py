@@ -26,10 +26,81 @@ _OTHER = {"allgather": [("allpairs_ag", ""), ("ring_ag", "")],
 
 
 @dataclass
+class LinkParams:
+    """cf/timing.py:26-33: an alpha-beta link (seconds, bytes / second)."""
+    alpha: float
+    beta: float
+
+    def __post_init__(self):
+        if self.alpha < 0 or self.beta <= 0:
+            raise BadTimeError("alpha must be >= 0 and beta positive")
+
+
+@dataclass
 class CostParams:
-    """Placeholder for the reference's cost model parameters (cf/timing.py:36-45):
-    accepted by run_benchmark for compatibility, ignored (latencies are measured)."""
-    params: dict = field(default_factory=dict)
+    """The reference's cost-model parameters (cf/timing.py:36-45), kept for
+    signature compatibility: ``transfer_time`` evaluates them; the benchmark
+    API ignores them (its latencies are measured)."""
+    intra: LinkParams = field(default_factory=lambda: LinkParams(829e-9, 397.5e9))
+    inter: LinkParams = field(default_factory=lambda: LinkParams(4.89e-6, 48.94e9))
+    tb_sync: float = 200e-9
+    sem_op: float = 100e-9
+    proxy_hop: float = 500e-9
+
+    def link(self, link_class: str) -> LinkParams:
+        from .world import INTRA
+        return self.intra if link_class == INTRA else self.inter
+
+
+def transfer_time(link_class: str, nbytes: int, p: CostParams) -> float:
+    """The alpha-beta transfer time of the reference's model (cf/timing.py:48-51)."""
+    lp = p.link(link_class)
+    return lp.alpha + nbytes / lp.beta
+
+
+@dataclass(frozen=True)
+class TimedEvent:
+    """cf/timing.py:61-68."""
+    ctx: str
+    label: str
+    start: float
+    end: float
+    link: tuple | None = None
+    nbytes: int = 0
+
+
+@dataclass
+class TimedTrace:
+    """cf/timing.py:71-79.  From ``simulate_timed`` here: one event per
+    (rank, program) spanning the measured execution, no per-op events."""
+    events: list
+    makespan: float
+
+    def link_bytes(self, link_class: str | None = None) -> int:
+        return sum(e.nbytes for e in self.events
+                   if e.link is not None and (link_class is None or e.link[2] == link_class))
+
+
+def simulate_timed(plan, world, p: CostParams | None = None, dtype: str | None = None, iters: int = 20,
+                   reps: int = 3) -> TimedTrace:
+    """The reference times a plan on its discrete-event model
+    (cf/timing.py:295-298); here the plan runs on the world's GPUs (K10) and
+    the makespan is its measured latency (CUDA graph, best of ``reps``);
+    ``p`` is ignored."""
+    import torch
+    from .executor import Runtime
+    from .dtypes import torch_dtype
+    rt = Runtime(plan, world, dtype=dtype)
+    try:
+        tdt = torch_dtype(rt.dtype)
+        n = world.num_ranks
+        xs = [torch.zeros(rt.in_elems, device=world.device(r), dtype=tdt) for r in range(n)]
+        ys = [torch.empty(rt.out_elems, device=world.device(r), dtype=tdt) for r in range(n)]
+        t = _measure(world, lambda: rt.run_raw(xs, ys), iters, reps)
+    finally:
+        rt.close()
+    events = [TimedEvent(f"r{pr.rank}.tb{pr.tb}", "program", 0.0, t) for pr in plan.programs]
+    return TimedTrace(events, t)
 
 
 @dataclass

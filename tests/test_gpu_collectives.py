@@ -566,6 +566,17 @@ def test_run_benchmark_measured_rows():
     assert rows_to_csv(rows).count("\n") == len(rows) + 1
 
 
+def test_simulate_timed_measures_a_plan():
+    """simulate_timed (cf/timing.py:295-298) runs the plan on the GPUs: the
+    makespan is a measured latency, one event per program."""
+    from paper_2504_09014_b200 import CostParams, parse_plan, simulate_timed
+    with open(os.path.join(GOLD, "plans", "2pa_memory_n8_e64.json"), "rb") as f:
+        plan = parse_plan(f.read())
+    tr = simulate_timed(plan, world(8), CostParams(), iters=5)
+    assert 0 < tr.makespan < 1e-3
+    assert len(tr.events) == len(plan.programs) and tr.link_bytes() == 0
+
+
 def test_host_buffer_allreduce_every_algorithm():
     """Host tensors through collective() for every AllReduce algorithm and the
     selector's pick: same bits as the device-buffer call (the host path copies

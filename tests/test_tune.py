@@ -40,3 +40,19 @@ def test_algo_ids():
         algo_id("auto")
     with pytest.raises(NoAlgoError):
         algo_id("2ph")
+
+
+def test_package_exports_the_reference_surface():
+    """Every name of the reference's ``__all__`` (cf/__init__.py:12-17) imports
+    from the drop-in package; transfer_time keeps the reference's alpha-beta
+    definition (cf/timing.py:48-51)."""
+    import paper_2504_09014_b200 as pkg
+    ref_all = ["CostParams", "ExecutionPlan", "LoweringParams", "ProgramGraph", "Runtime", "RunResult",
+               "Selector", "SimWorld", "algobw", "collective", "lower", "make_world", "parse_plan",
+               "run_benchmark", "select_algorithm", "serialize_plan", "simulate_timed", "transfer_time",
+               "validate_plan"]
+    for name in ref_all:
+        assert hasattr(pkg, name) and name in pkg.__all__, name
+    p = pkg.CostParams()
+    assert pkg.transfer_time("intra", 1 << 20, p) == pytest.approx(829e-9 + (1 << 20) / 397.5e9)
+    assert pkg.transfer_time("inter", 1000, p) == pytest.approx(4.89e-6 + 1000 / 48.94e9)
