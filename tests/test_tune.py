@@ -56,3 +56,12 @@ def test_package_exports_the_reference_surface():
     p = pkg.CostParams()
     assert pkg.transfer_time("intra", 1 << 20, p) == pytest.approx(829e-9 + (1 << 20) / 397.5e9)
     assert pkg.transfer_time("inter", 1000, p) == pytest.approx(4.89e-6 + 1000 / 48.94e9)
+
+
+def test_channel_objects_validate_like_the_reference():
+    """cf/channels.py:159-160: an unknown protocol is E_WRONG_PROTOCOL (raised
+    before any device work)."""
+    from paper_2504_09014_b200.channels import MemoryChannel
+    from paper_2504_09014_b200.errors import WrongProtocolError
+    with pytest.raises(WrongProtocolError):
+        MemoryChannel(None, None, "LL128", 0, 1)
