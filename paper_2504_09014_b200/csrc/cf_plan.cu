@@ -30,6 +30,7 @@ namespace plan {
 cfStatus parse(const char* text, size_t len, int dtype_override, Plan& P);
 const char* op_name(int k);
 const void* plan_kernel_for(int dtype, int cls);
+const void* plan_single_kernel_for(int dtype);
 
 namespace {
 
@@ -99,6 +100,7 @@ struct cfPlan {
   bool uses_port = false;             // port-channel ops go through the proxy
   int cls = 3;                        // interpreter class: bit 0 LL packet ops, bit 1 port ops
   bool has_prologue = false;          // per-call zeroing / private input copy
+  bool single_ok = false;             // every program one plain MULTI / COPY: plan_single_kernel applies
   // one-process-per-GPU: this process runs rank `me`'s programs; the peers'
   // plan heaps are IPC-mapped by cfPlanConnect, which finalizes the plan
   bool mp = false;
@@ -1153,6 +1155,14 @@ cfStatus finalize(cfPlan* pl) {
         if (d.code == D_MULTI || d.code == D_COPY || d.code == D_PUT_PACKETS || d.code == D_READ_PACKETS ||
             d.code == D_PORT_PUT)
           d.per = ((d.size + Kk - 1) / Kk + V - 1) / V * V;
+    pl->single_ok = pl->cls == 0 && !pl->prog_ops.empty() && (int)pl->prog_ops.size() <= kSingleProgs;
+    for (auto& prog : pl->prog_ops) {
+      if (!pl->single_ok) break;
+      const bool one = prog.size() == 1;
+      const DevOp* d = one ? &prog[0] : nullptr;
+      pl->single_ok = one && (d->code == D_MULTI || d->code == D_COPY) && (d->flags & F_VEC) && !d->pkt_mask &&
+                      d->nsrc >= 1 && d->nsrc <= 8 && d->ndst <= 8 && d->size % V == 0;
+    }
   }
   // device tables per device group
   for (size_t gi = 0; gi < c->groups.size(); gi++) {
@@ -1242,6 +1252,14 @@ namespace {
 // resolved (see Group::bound), or nullptr: binding table full, or a stream
 // capture is in progress (the first upload of a binding happens outside
 // capture; a captured launch then reuses it).
+bool single_enabled() {
+  static const bool on = [] {
+    const char* v = getenv("CF_PLAN_SINGLE");   // diagnostic: 0 keeps every plan on the interpreter
+    return !(v && atoi(v) == 0);
+  }();
+  return on;
+}
+
 DevOp* bound_ops(const cfPlan* pl, Group& G, const PlanArgs& a, cudaStream_t st) {
   const int n = pl->ir.nranks;
   std::vector<char*> key(a.io_in, a.io_in + n);
@@ -1413,7 +1431,42 @@ extern "C" cfStatus cfPlanExecute(cfPlan_t pl, const void* const* inputs, void* 
         a.prog_tab[p] = make_int4(pl->prog_rank[G.progs[p]], G.beg[p], G.end[p], 0);
       }
     }
-    if (DevOp* rops = bound_ops(pl, G, a, streams[c->groups[gi][0]])) {
+    DevOp* rops = bound_ops(pl, G, a, streams[c->groups[gi][0]]);
+    if (rops && pl->single_ok && !a.entry_barrier && !a.exit_barrier && !pl->uses_port && single_enabled()) {
+      // the plan compiled to a kernel: each program's resolved op in the parameter space
+      const Group::Bound* bb = nullptr;
+      for (auto& x : G.bound)
+        if (x.d_ops == rops) bb = &x;
+      SingleArgs sa;
+      memset(&sa, 0, sizeof(sa));
+      sa.K = pl->K;
+      sa.nprog = np;
+      for (int p = 0; p < np; p++) {
+        const DevOp& d = bb->h_pin[G.beg[p]];
+        auto& P = sa.p[p];
+        for (int k = 0; k < d.nsrc; k++) P.src[k] = (const char*)d.src[k].off;
+        for (int k = 0; k < d.ndst; k++) P.dst[k] = (char*)d.dst[k].off;
+        P.size = d.size;
+        P.per = d.per;
+        P.nsrc = d.nsrc;
+        P.ndst = d.ndst;
+        P.flags = d.flags | (d.code == D_MULTI ? 0x100 : 0);
+        P.rank = pl->prog_rank[G.progs[p]];
+        sa.rank_ctas[P.rank] += pl->K;
+      }
+      for (int r = 0; r < n; r++) sa.st[r] = &((PlanState*)(pl->heap[r] + pl->state_off))->base;
+      void* sargs[] = {&sa};
+      cudaError_t e = cudaLaunchKernel(plan_single_kernel_for(pl->dtype), dim3(np * pl->K), dim3(pl->threads),
+                                       sargs, 0, streams[c->groups[gi][0]]);
+      if (e != cudaSuccess) {
+        cudaSetDevice(prev);
+        return fail(CF_E_CUDA, "plan kernel launch: %s", cudaGetErrorString(e));
+      }
+      s = join_streams(c, (int)gi, streams, true);
+      if (s != CF_OK) { cudaSetDevice(prev); return s; }
+      continue;
+    }
+    if (rops) {
       a.ops = rops;
       a.resolved = 1;
       for (auto& bb : G.bound)

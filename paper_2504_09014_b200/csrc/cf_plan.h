@@ -172,6 +172,24 @@ struct PlanArgs {
 };
 constexpr int kParamProgs = 128;
 constexpr int kPfProgs = 32;
+
+// Plans whose every program is one plain-vector MULTI / COPY (the fused C5
+// two-shot plan: an n-source pull-reduce pushed to n destinations) run, when
+// one launch holds every rank and the I/O binding is host-resolved, on a
+// specialized kernel that takes each program's resolved op in its parameter
+// space: no op staging, no interpreter -- the plan compiled to a kernel.
+constexpr int kSingleProgs = 8;
+struct SingleArgs {
+  int K, nprog;
+  struct Prog {
+    const char* src[8];
+    char* dst[8];
+    uint64_t size, per;    // elements; CTA slice (DevOp::per)
+    int nsrc, ndst, flags, rank;
+  } p[kSingleProgs];
+  RankState* st[CF_MAX_RANKS];   // &PlanState::base of each rank (the call epoch)
+  int rank_ctas[CF_MAX_RANKS];
+};
 static_assert(sizeof(PlanArgs) <= 32764, "kernel parameter space");
 constexpr int kMaxBufs = 16;
 constexpr int kMaxZero = 16;

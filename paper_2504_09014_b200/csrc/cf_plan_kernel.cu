@@ -642,6 +642,72 @@ __global__ void __launch_bounds__(CF_PLAN_THREADS) plan_kernel(const __grid_cons
   TS_DUMP("plan", rank);
 }
 
+// The single-op plan kernel (see SingleArgs): CTA j of program p reduces its
+// slice of the program's op with every source's load in flight, stores it to
+// every destination, and the rank's last CTA publishes the call epoch.
+template <typename T>
+__global__ void __launch_bounds__(512) plan_single_kernel(const __grid_constant__ SingleArgs a) {
+  using A = typename Vec<T>::Acc;
+  constexpr int V = Vec<T>::N;
+  const int pid = blockIdx.x / a.K, j = blockIdx.x % a.K;
+  const SingleArgs::Prog& P = a.p[pid];
+  RankState* rs = a.st[P.rank];
+  const uint64_t e = threadIdx.x == 0 ? *(volatile uint64_t*)&rs->epoch + 1 : 0;
+  uint64_t lo, hi;
+  slice(P.size, P.per, j, lo, hi);
+  const int nsrc = P.nsrc, ndst = P.ndst;
+  const bool multi = P.flags & 0x100, zero = P.flags & F_ZERO, round_each = P.flags & F_ROUND_EACH;
+  const char* src[8];
+  char* dst[8];
+#pragma unroll
+  for (int i = 0; i < 8; i++) {
+    src[i] = P.src[i];
+    dst[i] = P.dst[i];
+  }
+  for (uint64_t v = lo / V + threadIdx.x; v * V < hi; v += blockDim.x) {
+    const size_t boff = (size_t)v * 16;
+    uint4 x[8];
+#pragma unroll
+    for (int i = 0; i < 8; i++) x[i] = i < nsrc ? ld16(src[i] + boff) : make_uint4(0, 0, 0, 0);
+    uint4 res = x[0];
+    if (multi) {
+      A acc[V];
+      if (zero) {
+#pragma unroll
+        for (int i = 0; i < V; i++) acc[i] = A(0);
+        acc_vec<T>(acc, x[0], round_each);
+      } else {
+        Vec<T>::load(x[0], acc);
+      }
+#pragma unroll
+      for (int i = 1; i < 8; i++)
+        if (i < nsrc) acc_vec<T>(acc, x[i], round_each);
+      res = Vec<T>::store(acc);
+    }
+#pragma unroll
+    for (int d = 0; d < 8; d++)
+      if (d < ndst) st16(dst[d] + boff, res);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t prev = atomicAdd(&rs->arrive, 1u);
+    if (prev == (uint32_t)a.rank_ctas[P.rank] - 1) {
+      *(volatile uint32_t*)&rs->arrive = 0;
+      *(volatile uint64_t*)&rs->epoch = e;
+    }
+  }
+}
+
+const void* plan_single_kernel_for(int dtype) {
+  switch (dtype) {
+    case 0: return (const void*)plan_single_kernel<int32_t>;
+    case 1: return (const void*)plan_single_kernel<float>;
+    case 2: return (const void*)plan_single_kernel<__half>;
+    case 3: return (const void*)plan_single_kernel<__nv_bfloat16>;
+  }
+  return nullptr;
+}
+
 template <int CLS>
 static const void* by_dtype(int dtype) {
   switch (dtype) {
