@@ -31,6 +31,7 @@ cfStatus parse(const char* text, size_t len, int dtype_override, Plan& P);
 const char* op_name(int k);
 const void* plan_kernel_for(int dtype, int cls);
 const void* plan_single_kernel_for(int dtype);
+const void* plan_ll_kernel_for(int dtype);
 
 namespace {
 
@@ -101,6 +102,7 @@ struct cfPlan {
   int cls = 3;                        // interpreter class: bit 0 LL packet ops, bit 1 port ops
   bool has_prologue = false;          // per-call zeroing / private input copy
   bool single_ok = false;             // every program one plain MULTI / COPY: plan_single_kernel applies
+  bool ll_ok = false;                 // every program a short LL16 op sequence: plan_ll_kernel applies
   // one-process-per-GPU: this process runs rank `me`'s programs; the peers'
   // plan heaps are IPC-mapped by cfPlanConnect, which finalizes the plan
   bool mp = false;
@@ -1155,6 +1157,26 @@ cfStatus finalize(cfPlan* pl) {
         if (d.code == D_MULTI || d.code == D_COPY || d.code == D_PUT_PACKETS || d.code == D_READ_PACKETS ||
             d.code == D_PORT_PUT)
           d.per = ((d.size + Kk - 1) / Kk + V - 1) / V * V;
+    // compiled LL plans: put / read packets (LL16), MULTI / COPY on whole
+    // 8-byte units (plain or LL16 packet sources), CTA-local syncs
+    const uint64_t H = 8 / (uint64_t)pl->es;
+    pl->ll_ok = pl->cls == 1 && !pl->prog_ops.empty() && (int)pl->prog_ops.size() <= kLLProgs;
+    for (auto& prog : pl->prog_ops) {
+      if (!pl->ll_ok) break;
+      pl->ll_ok = !prog.empty() && (int)prog.size() <= kLLOps;
+      for (auto& d : prog) {
+        if (!pl->ll_ok) break;
+        if (d.code == D_SYNC_CTA) continue;
+        const bool pk = d.code == D_PUT_PACKETS || d.code == D_READ_PACKETS;
+        const bool dm = d.code == D_MULTI || d.code == D_COPY;
+        pl->ll_ok = (pk && (d.flags & F_LL16)) || (dm && (d.flags & F_VEC) && d.nsrc >= 1);
+        pl->ll_ok = pl->ll_ok && d.nsrc <= 8 && d.ndst <= 8 && d.size % H == 0;
+        // latency regime only: from 64 KiB per op the interpreter's vector
+        // path (two units per thread in flight) wins (1pa plan b=16: 17.0 vs
+        // 18.5 us compiled; 2pa_ll b=64: 23.0 vs 26.2 us)
+        pl->ll_ok = pl->ll_ok && d.size * (uint64_t)pl->es <= ((uint64_t)64 << 10);
+      }
+    }
     pl->single_ok = pl->cls == 0 && !pl->prog_ops.empty() && (int)pl->prog_ops.size() <= kSingleProgs;
     for (auto& prog : pl->prog_ops) {
       if (!pl->single_ok) break;
@@ -1458,6 +1480,50 @@ extern "C" cfStatus cfPlanExecute(cfPlan_t pl, const void* const* inputs, void* 
       void* sargs[] = {&sa};
       cudaError_t e = cudaLaunchKernel(plan_single_kernel_for(pl->dtype), dim3(np * pl->K), dim3(pl->threads),
                                        sargs, 0, streams[c->groups[gi][0]]);
+      if (e != cudaSuccess) {
+        cudaSetDevice(prev);
+        return fail(CF_E_CUDA, "plan kernel launch: %s", cudaGetErrorString(e));
+      }
+      s = join_streams(c, (int)gi, streams, true);
+      if (s != CF_OK) { cudaSetDevice(prev); return s; }
+      continue;
+    }
+    if (rops && pl->ll_ok && !a.entry_barrier && !a.exit_barrier && single_enabled()) {
+      const Group::Bound* bb = nullptr;
+      for (auto& x : G.bound)
+        if (x.d_ops == rops) bb = &x;
+      LLArgs la;
+      memset(&la, 0, sizeof(la));
+      la.K = pl->K;
+      la.nprog = np;
+      la.flag_stride = pl->flag_stride;
+      for (int p = 0; p < np; p++) {
+        auto& P = la.p[p];
+        P.rank = pl->prog_rank[G.progs[p]];
+        P.nops = G.end[p] - G.beg[p];
+        for (int i = 0; i < P.nops; i++) {
+          const DevOp& d = bb->h_pin[G.beg[p] + i];
+          auto& o = P.op[i];
+          for (int k = 0; k < d.nsrc && k < 8; k++) {
+            o.src[k] = (const char*)d.src[k].off;
+            o.llflag_k[k] = d.llflag_k[k];
+          }
+          for (int k = 0; k < d.ndst && k < 8; k++) o.dst[k] = (char*)d.dst[k].off;
+          o.size = d.size;
+          o.per = d.per;
+          o.llflag = d.llflag;
+          o.code = d.code;
+          o.nsrc = d.nsrc;
+          o.ndst = d.ndst;
+          o.flags = d.flags;
+          o.pkt_mask = d.pkt_mask;
+        }
+        la.rank_ctas[P.rank] += pl->K;
+      }
+      for (int r = 0; r < n; r++) la.st[r] = &((PlanState*)(pl->heap[r] + pl->state_off))->base;
+      void* largs[] = {&la};
+      cudaError_t e = cudaLaunchKernel(plan_ll_kernel_for(pl->dtype), dim3(np * pl->K), dim3(pl->threads), largs,
+                                       0, streams[c->groups[gi][0]]);
       if (e != cudaSuccess) {
         cudaSetDevice(prev);
         return fail(CF_E_CUDA, "plan kernel launch: %s", cudaGetErrorString(e));

@@ -190,6 +190,36 @@ struct SingleArgs {
   RankState* st[CF_MAX_RANKS];   // &PlanState::base of each rank (the call epoch)
   int rank_ctas[CF_MAX_RANKS];
 };
+
+// LL plans compiled to a kernel: every program a short sequence of LL16
+// packet puts / reads, plain-vector or packet-source MULTI / COPY and
+// CTA-local syncs (the C5 1pa and 2pa_ll plans), one launch holding every
+// rank, binding host-resolved: the resolved ops travel in the parameter
+// space and run on a lean kernel (no staging, no general interpreter, two
+// CTAs per SM) -- packet ops spread their (range, unit) items over the
+// threads, reduces run one 8-byte unit per thread.
+constexpr int kLLProgs = 8;
+constexpr int kLLOps = 7;
+struct LLArgs {
+  int K, nprog;
+  uint32_t flag_stride;
+  struct Op {
+    const char* src[8];
+    char* dst[8];
+    uint32_t llflag_k[8];  // plan flags of packet sources (READ / MULTI)
+    uint64_t size, per;
+    uint32_t llflag;       // PUT
+    uint8_t code, nsrc, ndst, flags;
+    uint32_t pkt_mask;
+  };
+  struct Prog {
+    Op op[kLLOps];
+    int nops, rank;
+  } p[kLLProgs];
+  RankState* st[CF_MAX_RANKS];
+  int rank_ctas[CF_MAX_RANKS];
+};
+static_assert(sizeof(LLArgs) <= 32764, "kernel parameter space");
 static_assert(sizeof(PlanArgs) <= 32764, "kernel parameter space");
 constexpr int kMaxBufs = 16;
 constexpr int kMaxZero = 16;

@@ -698,6 +698,121 @@ __global__ void __launch_bounds__(512) plan_single_kernel(const __grid_constant_
   }
 }
 
+// The compiled LL plan kernel (see LLArgs).  Op fields are read from the
+// parameter space (uniform per CTA); every thread reads the call epoch itself.
+template <typename T>
+__global__ void __launch_bounds__(512, 2) plan_ll_kernel(const __grid_constant__ LLArgs a) {
+  using A = typename Vec<T>::Acc;
+  constexpr int V = Vec<T>::N;
+  constexpr int H = 8 / sizeof(T);   // elements per 8-byte payload unit
+  const int pid = blockIdx.x / a.K, j = blockIdx.x % a.K;
+  const LLArgs::Prog& P = a.p[pid];
+  RankState* rs = a.st[P.rank];
+  const uint64_t e = *(volatile uint64_t*)&rs->epoch + 1;
+  const uint32_t fs = a.flag_stride;
+  for (int oi = 0; oi < P.nops; oi++) {
+    const LLArgs::Op& op = P.op[oi];
+    if (op.code == D_SYNC_CTA) {
+      __syncthreads();
+      continue;
+    }
+    uint64_t lo, hi;
+    slice(op.size, op.per, j, lo, hi);
+    if (lo >= hi) continue;
+    const uint64_t u0 = lo / H, u1 = (hi + H - 1) / H;
+    const uint32_t nu = (uint32_t)(u1 - u0);
+    if (op.code == D_PUT_PACKETS || op.code == D_READ_PACKETS) {
+      const bool put = op.code == D_PUT_PACKETS;
+      const int nb = put ? op.ndst : op.nsrc;
+      const bool paired = op.flags & F_PAIRED;
+      const uint32_t pflag = put ? runtime_flag(e, fs, op.llflag) : 0u;
+      const uint32_t items = nu * (uint32_t)nb;
+      const float rnu = 1.0f / (float)nu;
+      for (uint32_t w = threadIdx.x; w < items; w += blockDim.x) {
+        uint32_t k = (uint32_t)((float)w * rnu);
+        k -= k * nu > w;
+        k += (k + 1) * nu <= w;
+        const uint64_t u = u0 + (w - k * nu);
+        if (put) {
+          const uint2 d = *reinterpret_cast<const uint2*>(op.src[paired ? k : 0] + u * 8);
+          ll16_put(op.dst[k] + u * 16, d, pflag);
+        } else {
+          const uint32_t f = runtime_flag(e, fs, op.llflag_k[k]);
+          const uint4 raw = ld16_volatile(op.src[k] + u * 16);
+          uint2 d = make_uint2(raw.x, raw.z);
+          if (raw.y != f || raw.w != f) d = ll16_get(op.src[k] + u * 16, f, rs);
+          *reinterpret_cast<uint2*>(op.dst[k] + u * 8) = d;
+        }
+      }
+      continue;
+    }
+    // MULTI / COPY, one 8-byte payload unit per thread: every source (plain
+    // unit or LL16 packet) in flight, then the plan's order and rounding
+    const int nsrc = op.nsrc, ndst = op.ndst;
+    const bool multi = op.code == D_MULTI, zero = op.flags & F_ZERO, round_each = op.flags & F_ROUND_EACH;
+    const uint32_t pkt = op.pkt_mask;
+    for (uint64_t u = u0 + threadIdx.x; u < u1; u += blockDim.x) {
+      uint4 x[8];
+#pragma unroll
+      for (int i = 0; i < 8; i++)
+        if (i < nsrc) {
+          if ((pkt >> i) & 1u) {
+            x[i] = ld16_volatile(op.src[i] + u * 16);
+          } else {
+            const uint2 d = *reinterpret_cast<const uint2*>(op.src[i] + u * 8);
+            x[i] = make_uint4(d.x, 0u, d.y, 0u);
+          }
+        }
+#pragma unroll
+      for (int i = 0; i < 8; i++)
+        if (i < nsrc && ((pkt >> i) & 1u)) {
+          const uint32_t f = runtime_flag(e, fs, op.llflag_k[i]);
+          if (x[i].y != f || x[i].w != f) {
+            const uint2 d = ll16_get(op.src[i] + u * 16, f, rs);
+            x[i] = make_uint4(d.x, f, d.y, f);
+          }
+        }
+      uint2 res = make_uint2(x[0].x, x[0].z);
+      if (multi) {
+        A acc[V];
+        if (zero) {
+#pragma unroll
+          for (int i = 0; i < V; i++) acc[i] = A(0);
+          acc_vec<T>(acc, make_uint4(x[0].x, x[0].z, 0u, 0u), round_each);
+        } else {
+          Vec<T>::load(make_uint4(x[0].x, x[0].z, 0u, 0u), acc);
+        }
+#pragma unroll
+        for (int i = 1; i < 8; i++)
+          if (i < nsrc) acc_vec<T>(acc, make_uint4(x[i].x, x[i].z, 0u, 0u), round_each);
+        const uint4 r4 = Vec<T>::store(acc);
+        res = make_uint2(r4.x, r4.y);
+      }
+#pragma unroll
+      for (int d = 0; d < 8; d++)
+        if (d < ndst) *reinterpret_cast<uint2*>(op.dst[d] + u * 8) = res;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t prev = atomicAdd(&rs->arrive, 1u);
+    if (prev == (uint32_t)a.rank_ctas[P.rank] - 1) {
+      *(volatile uint32_t*)&rs->arrive = 0;
+      *(volatile uint64_t*)&rs->epoch = e;
+    }
+  }
+}
+
+const void* plan_ll_kernel_for(int dtype) {
+  switch (dtype) {
+    case 0: return (const void*)plan_ll_kernel<int32_t>;
+    case 1: return (const void*)plan_ll_kernel<float>;
+    case 2: return (const void*)plan_ll_kernel<__half>;
+    case 3: return (const void*)plan_ll_kernel<__nv_bfloat16>;
+  }
+  return nullptr;
+}
+
 const void* plan_single_kernel_for(int dtype) {
   switch (dtype) {
     case 0: return (const void*)plan_single_kernel<int32_t>;
