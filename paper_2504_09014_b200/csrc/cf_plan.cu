@@ -1174,7 +1174,11 @@ cfStatus finalize(cfPlan* pl) {
         // latency regime only: from 64 KiB per op the interpreter's vector
         // path (two units per thread in flight) wins (1pa plan b=16: 17.0 vs
         // 18.5 us compiled; 2pa_ll b=64: 23.0 vs 26.2 us)
-        pl->ll_ok = pl->ll_ok && d.size * (uint64_t)pl->es <= ((uint64_t)64 << 10);
+        static const uint64_t ll_max = [] {
+          const char* v = getenv("CF_PLAN_LL_MAX");   // diagnostic: largest op (bytes) compiled
+          return v ? (uint64_t)atoll(v) : ~(uint64_t)0;
+        }();
+        pl->ll_ok = pl->ll_ok && d.size * (uint64_t)pl->es <= ll_max;
       }
     }
     pl->single_ok = pl->cls == 0 && !pl->prog_ops.empty() && (int)pl->prog_ops.size() <= kSingleProgs;
@@ -1494,7 +1498,22 @@ extern "C" cfStatus cfPlanExecute(cfPlan_t pl, const void* const* inputs, void* 
         if (x.d_ops == rops) bb = &x;
       LLArgs la;
       memset(&la, 0, sizeof(la));
-      la.K = pl->K;
+      // the compiled kernel runs 2 CTAs per SM: up to twice the interpreter's
+      // CTAs per program (slices recomputed for that count)
+      // (only as many as the largest op keeps busy: small plans keep K, their
+      // extra CTAs would only add launch and barrier cost)
+      uint64_t busiest = 0;   // largest op's items: 8-byte units x flattened ranges
+      for (int p = 0; p < np; p++)
+        for (int i = G.beg[p]; i < G.end[p]; i++) {
+          const DevOp& d = bb->h_pin[i];
+          const uint64_t units = d.size * (uint64_t)pl->es / 8;
+          const bool flat = d.code == D_READ_PACKETS || (d.code == D_PUT_PACKETS && (d.flags & F_PAIRED));
+          busiest = std::max(busiest, units * (flat ? (uint64_t)std::max<int>(d.nsrc, d.ndst) : 1));
+        }
+      const int K2 = (int)std::min<uint64_t>(2ull * pl->K, std::max<uint64_t>(
+          pl->K, (busiest + pl->threads - 1) / pl->threads));
+      const uint64_t V2 = 16 / (uint64_t)pl->es;
+      la.K = K2;
       la.nprog = np;
       la.flag_stride = pl->flag_stride;
       for (int p = 0; p < np; p++) {
@@ -1510,7 +1529,7 @@ extern "C" cfStatus cfPlanExecute(cfPlan_t pl, const void* const* inputs, void* 
           }
           for (int k = 0; k < d.ndst && k < 8; k++) o.dst[k] = (char*)d.dst[k].off;
           o.size = d.size;
-          o.per = d.per;
+          o.per = ((d.size + K2 - 1) / K2 + V2 - 1) / V2 * V2;
           o.llflag = d.llflag;
           o.code = d.code;
           o.nsrc = d.nsrc;
@@ -1518,11 +1537,11 @@ extern "C" cfStatus cfPlanExecute(cfPlan_t pl, const void* const* inputs, void* 
           o.flags = d.flags;
           o.pkt_mask = d.pkt_mask;
         }
-        la.rank_ctas[P.rank] += pl->K;
+        la.rank_ctas[P.rank] += K2;
       }
       for (int r = 0; r < n; r++) la.st[r] = &((PlanState*)(pl->heap[r] + pl->state_off))->base;
       void* largs[] = {&la};
-      cudaError_t e = cudaLaunchKernel(plan_ll_kernel_for(pl->dtype), dim3(np * pl->K), dim3(pl->threads), largs,
+      cudaError_t e = cudaLaunchKernel(plan_ll_kernel_for(pl->dtype), dim3(np * K2), dim3(pl->threads), largs,
                                        0, streams[c->groups[gi][0]]);
       if (e != cudaSuccess) {
         cudaSetDevice(prev);

@@ -721,6 +721,18 @@ __global__ void __launch_bounds__(512, 2) plan_ll_kernel(const __grid_constant__
     if (lo >= hi) continue;
     const uint64_t u0 = lo / H, u1 = (hi + H - 1) / H;
     const uint32_t nu = (uint32_t)(u1 - u0);
+    if (op.code == D_PUT_PACKETS && !(op.flags & F_PAIRED)) {
+      // one payload to ndst ranges: one load per unit, every range's packet
+      const uint32_t pflag = runtime_flag(e, fs, op.llflag);
+      const int nb = op.ndst;
+      for (uint64_t u = u0 + threadIdx.x; u < u1; u += blockDim.x) {
+        const uint2 d = *reinterpret_cast<const uint2*>(op.src[0] + u * 8);
+#pragma unroll
+        for (int k = 0; k < 8; k++)
+          if (k < nb) ll16_put(op.dst[k] + u * 16, d, pflag);
+      }
+      continue;
+    }
     if (op.code == D_PUT_PACKETS || op.code == D_READ_PACKETS) {
       const bool put = op.code == D_PUT_PACKETS;
       const int nb = put ? op.ndst : op.nsrc;

@@ -26,6 +26,8 @@ KERNELS = [   # (file tag, substring of the demangled name)
     ("k10_plan_hb_bf16", "plan_kernel<__nv_bfloat16, 0>"),
     ("k10_plan_ll_bf16", "plan_kernel<__nv_bfloat16, 1>"),
     ("k10_plan_all_bf16", "plan_kernel<__nv_bfloat16, 3>"),
+    ("k10_plan_single_bf16", "plan_single_kernel<__nv_bfloat16>"),
+    ("k10_plan_ll_compiled_bf16", "plan_ll_kernel<__nv_bfloat16>"),
 ]
 PATTERNS = {
     "LDG.128": r"LDG\.E\.128\b(?!\.STRONG)", "STG.128": r"STG\.E\.128\b(?!\.STRONG)",
