@@ -1458,7 +1458,20 @@ extern "C" cfStatus cfPlanExecute(cfPlan_t pl, const void* const* inputs, void* 
       }
     }
     DevOp* rops = bound_ops(pl, G, a, streams[c->groups[gi][0]]);
-    if (rops && pl->single_ok && !a.entry_barrier && !a.exit_barrier && !pl->uses_port && single_enabled()) {
+    // rank barriers of the compiled launches: the interpreter's (same CTAs per
+    // rank, same numbering), so calls may alternate between the two paths
+    PlanBarriers pb;
+    memset(&pb, 0, sizeof(pb));
+    for (int r = 0; r < n; r++) {
+      pb.pst[r] = a.st[r];
+      pb.leader[r] = a.rank_leader[r];
+    }
+    pb.n = n;
+    pb.gpu_scope = a.gpu_scope;
+    pb.entry = a.entry_barrier;
+    pb.exit = a.exit_barrier;
+    const bool compiled_ok = rops && !pl->has_prologue && !pl->uses_port && single_enabled();
+    if (compiled_ok && pl->single_ok) {
       // the plan compiled to a kernel: each program's resolved op in the parameter space
       const Group::Bound* bb = nullptr;
       for (auto& x : G.bound)
@@ -1480,7 +1493,8 @@ extern "C" cfStatus cfPlanExecute(cfPlan_t pl, const void* const* inputs, void* 
         P.rank = pl->prog_rank[G.progs[p]];
         sa.rank_ctas[P.rank] += pl->K;
       }
-      for (int r = 0; r < n; r++) sa.st[r] = &((PlanState*)(pl->heap[r] + pl->state_off))->base;
+      for (int r = 0; r < n; r++) sa.st[r] = &a.st[r]->base;
+      sa.bar = pb;
       void* sargs[] = {&sa};
       cudaError_t e = cudaLaunchKernel(plan_single_kernel_for(pl->dtype), dim3(np * pl->K), dim3(pl->threads),
                                        sargs, 0, streams[c->groups[gi][0]]);
@@ -1492,7 +1506,7 @@ extern "C" cfStatus cfPlanExecute(cfPlan_t pl, const void* const* inputs, void* 
       if (s != CF_OK) { cudaSetDevice(prev); return s; }
       continue;
     }
-    if (rops && pl->ll_ok && !a.entry_barrier && !a.exit_barrier && single_enabled()) {
+    if (compiled_ok && pl->ll_ok) {
       const Group::Bound* bb = nullptr;
       for (auto& x : G.bound)
         if (x.d_ops == rops) bb = &x;
@@ -1510,8 +1524,9 @@ extern "C" cfStatus cfPlanExecute(cfPlan_t pl, const void* const* inputs, void* 
           const bool flat = d.code == D_READ_PACKETS || (d.code == D_PUT_PACKETS && (d.flags & F_PAIRED));
           busiest = std::max(busiest, units * (flat ? (uint64_t)std::max<int>(d.nsrc, d.ndst) : 1));
         }
-      const int K2 = (int)std::min<uint64_t>(2ull * pl->K, std::max<uint64_t>(
-          pl->K, (busiest + pl->threads - 1) / pl->threads));
+      const int K2 = (pb.entry || pb.exit) ? pl->K   // barrier counts assume the interpreter's CTAs per rank
+                   : (int)std::min<uint64_t>(2ull * pl->K, std::max<uint64_t>(
+                         pl->K, (busiest + pl->threads - 1) / pl->threads));
       const uint64_t V2 = 16 / (uint64_t)pl->es;
       la.K = K2;
       la.nprog = np;
@@ -1539,7 +1554,10 @@ extern "C" cfStatus cfPlanExecute(cfPlan_t pl, const void* const* inputs, void* 
         }
         la.rank_ctas[P.rank] += K2;
       }
-      for (int r = 0; r < n; r++) la.st[r] = &((PlanState*)(pl->heap[r] + pl->state_off))->base;
+      for (int r = 0; r < n; r++) la.st[r] = &a.st[r]->base;
+      la.bar = pb;
+      for (int r = 0; r < n; r++)   // the leader CTA of each rank at this launch's CTAs per program
+        if (pb.leader[r] >= 0) la.bar.leader[r] = pb.leader[r] / pl->K * K2;
       void* largs[] = {&la};
       cudaError_t e = cudaLaunchKernel(plan_ll_kernel_for(pl->dtype), dim3(np * K2), dim3(pl->threads), largs,
                                        0, streams[c->groups[gi][0]]);

@@ -179,6 +179,14 @@ constexpr int kPfProgs = 32;
 // specialized kernel that takes each program's resolved op in its parameter
 // space: no op staging, no interpreter -- the plan compiled to a kernel.
 constexpr int kSingleProgs = 8;
+// Rank barriers of a compiled plan launch (one process per GPU: entry = the
+// peers' inputs are produced and outputs free, exit = nobody still reads this
+// rank's buffers), numbered like the interpreter's.
+struct PlanBarriers {
+  PlanState* pst[CF_MAX_RANKS];
+  int leader[CF_MAX_RANKS];
+  int n, gpu_scope, entry, exit;
+};
 struct SingleArgs {
   int K, nprog;
   struct Prog {
@@ -189,6 +197,7 @@ struct SingleArgs {
   } p[kSingleProgs];
   RankState* st[CF_MAX_RANKS];   // &PlanState::base of each rank (the call epoch)
   int rank_ctas[CF_MAX_RANKS];
+  PlanBarriers bar;
 };
 
 // LL plans compiled to a kernel: every program a short sequence of LL16
@@ -218,6 +227,7 @@ struct LLArgs {
   } p[kLLProgs];
   RankState* st[CF_MAX_RANKS];
   int rank_ctas[CF_MAX_RANKS];
+  PlanBarriers bar;
 };
 static_assert(sizeof(LLArgs) <= 32764, "kernel parameter space");
 static_assert(sizeof(PlanArgs) <= 32764, "kernel parameter space");

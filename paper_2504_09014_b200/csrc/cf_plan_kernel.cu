@@ -63,19 +63,22 @@ __device__ __forceinline__ void counter_barrier(uint64_t* ctr, uint64_t target, 
 
 // All CTAs of `rank` meet; the rank's leader CTA exchanges `k` with every
 // other rank's leader, then releases its rank.
-__device__ __noinline__ void rank_barrier(const PlanArgs& a, int rank, uint64_t k) {
-  PlanState* ps = a.st[rank];
-  const bool gpu = a.gpu_scope;
+// (`st`: every rank's PlanState as this device addresses it; the rank's CTAs
+// count `rank_ctas` arrivals per barrier, so every launch path of a plan --
+// interpreter or compiled -- must run the same CTAs per rank)
+__device__ __noinline__ void rank_barrier_raw(PlanState* const* st, int n, int rank, int leader, int rank_ctas,
+                                              uint64_t k, bool gpu) {
+  PlanState* ps = st[rank];
   fence_publish(gpu);
   __syncthreads();
   if (threadIdx.x == 0) atomicAdd((unsigned long long*)&ps->bar_arrive, 1ull);
-  if ((int)blockIdx.x == a.rank_leader[rank]) {
-    if (threadIdx.x == 0) wait_geq(&ps->bar_arrive, k * (uint64_t)a.rank_ctas[rank], &ps->base, true);
+  if ((int)blockIdx.x == leader) {
+    if (threadIdx.x == 0) wait_geq(&ps->bar_arrive, k * (uint64_t)rank_ctas, &ps->base, true);
     __syncthreads();
     const int t = threadIdx.x;
-    if (t < a.n && t != rank) {
+    if (t < n && t != rank) {
       fence_publish(gpu);
-      st_release(&a.st[t]->rankbar[rank], k, gpu);
+      st_release(&st[t]->rankbar[rank], k, gpu);
       wait_geq(&ps->rankbar[t], k, &ps->base, gpu);
     }
     __syncthreads();
@@ -84,6 +87,9 @@ __device__ __noinline__ void rank_barrier(const PlanArgs& a, int rank, uint64_t 
     wait_geq(&ps->bar_release, k, &ps->base, true);
   }
   __syncthreads();
+}
+__device__ __forceinline__ void rank_barrier(const PlanArgs& a, int rank, uint64_t k) {
+  rank_barrier_raw(a.st, a.n, rank, a.rank_leader[rank], a.rank_ctas[rank], k, a.gpu_scope);
 }
 
 // ---------------------------------------------------------------- element helpers
@@ -652,7 +658,12 @@ __global__ void __launch_bounds__(512) plan_single_kernel(const __grid_constant_
   const int pid = blockIdx.x / a.K, j = blockIdx.x % a.K;
   const SingleArgs::Prog& P = a.p[pid];
   RankState* rs = a.st[P.rank];
-  const uint64_t e = threadIdx.x == 0 ? *(volatile uint64_t*)&rs->epoch + 1 : 0;
+  const bool bars = a.bar.entry | a.bar.exit;
+  const uint64_t e = (threadIdx.x == 0 || bars) ? *(volatile uint64_t*)&rs->epoch + 1 : 0;
+  const uint64_t per_call = (uint64_t)(a.bar.entry + a.bar.exit);
+  if (a.bar.entry)   // one process per GPU: the peers' inputs are produced, their outputs free
+    rank_barrier_raw(a.bar.pst, a.bar.n, P.rank, a.bar.leader[P.rank], a.rank_ctas[P.rank], (e - 1) * per_call + 1,
+                     a.bar.gpu_scope);
   uint64_t lo, hi;
   slice(P.size, P.per, j, lo, hi);
   const int nsrc = P.nsrc, ndst = P.ndst;
@@ -688,6 +699,9 @@ __global__ void __launch_bounds__(512) plan_single_kernel(const __grid_constant_
     for (int d = 0; d < 8; d++)
       if (d < ndst) st16(dst[d] + boff, res);
   }
+  if (a.bar.exit)    // nobody reads this rank's buffers once it returns
+    rank_barrier_raw(a.bar.pst, a.bar.n, P.rank, a.bar.leader[P.rank], a.rank_ctas[P.rank], e * per_call,
+                     a.bar.gpu_scope);
   __syncthreads();
   if (threadIdx.x == 0) {
     const uint32_t prev = atomicAdd(&rs->arrive, 1u);
@@ -710,6 +724,10 @@ __global__ void __launch_bounds__(512, 2) plan_ll_kernel(const __grid_constant__
   RankState* rs = a.st[P.rank];
   const uint64_t e = *(volatile uint64_t*)&rs->epoch + 1;
   const uint32_t fs = a.flag_stride;
+  const uint64_t per_call = (uint64_t)(a.bar.entry + a.bar.exit);
+  if (a.bar.entry)
+    rank_barrier_raw(a.bar.pst, a.bar.n, P.rank, a.bar.leader[P.rank], a.rank_ctas[P.rank], (e - 1) * per_call + 1,
+                     a.bar.gpu_scope);
   for (int oi = 0; oi < P.nops; oi++) {
     const LLArgs::Op& op = P.op[oi];
     if (op.code == D_SYNC_CTA) {
@@ -805,6 +823,9 @@ __global__ void __launch_bounds__(512, 2) plan_ll_kernel(const __grid_constant__
         if (d < ndst) *reinterpret_cast<uint2*>(op.dst[d] + u * 8) = res;
     }
   }
+  if (a.bar.exit)
+    rank_barrier_raw(a.bar.pst, a.bar.n, P.rank, a.bar.leader[P.rank], a.rank_ctas[P.rank], e * per_call,
+                     a.bar.gpu_scope);
   __syncthreads();
   if (threadIdx.x == 0) {
     const uint32_t prev = atomicAdd(&rs->arrive, 1u);
