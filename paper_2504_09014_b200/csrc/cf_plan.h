@@ -178,7 +178,7 @@ constexpr int kPfProgs = 32;
 // one launch holds every rank and the I/O binding is host-resolved, on a
 // specialized kernel that takes each program's resolved op in its parameter
 // space: no op staging, no interpreter -- the plan compiled to a kernel.
-constexpr int kSingleProgs = 8;
+constexpr int kSingleProgs = 16;
 // Rank barriers of a compiled plan launch (one process per GPU: entry = the
 // peers' inputs are produced and outputs free, exit = nobody still reads this
 // rank's buffers), numbered like the interpreter's.
