@@ -873,8 +873,11 @@ def run_multi_gpu(args):
     tuned = None
     if not args.no_sweep:
         try:
-            tr = comm.tune(kind="allreduce", dtype="bf16", iters=10, nvls=nvls and sym_mode == 1)
+            # (the bench runs no compute beside the collectives: budgets up to 128 CTAs)
+            tr = comm.tune(kind="allreduce", dtype="bf16", iters=10, nvls=nvls and sym_mode == 1,
+                           budgets=(32, 64, 96, 128))
             tuned = {"table": [[int(b), a] for b, a in tr["table"]], "nvls_min_bytes": tr["nvls_min_bytes"],
+                     "cta_budget_2pa": tr["cta_budget_2pa"], "cta_budget_times_us": tr["cta_budget_times_us"],
                      "times_us": {a: [None if v is None else round(v * 1e6, 2) for v in ts]
                                   for a, ts in tr["times"].items()},
                      "sizes": tr["sizes"]}

@@ -311,15 +311,20 @@ class Communicator:
         return self._sym_mode
 
     def tune(self, kind: str = "allreduce", dtype: str = "bf16", sizes=None, algos=None, iters: int = 10,
-             install: bool = True, nvls: bool = True) -> dict:
+             install: bool = True, nvls: bool = True, budgets=(32, 64)) -> dict:
         """Collective: time every candidate algorithm at each size on this
         rank's GPU (CUDA graphs, every replay preceded by a bootstrap barrier),
         take the max over ranks, and install the same fastest-per-size table on
         every rank (cfCommSetSelection; see tune.py).  On a multicast heap the
         smallest size from which in-place NVLS wins is measured and installed
-        too (cfCommSetNvlsMinBytes).  Buffers come from the symmetric heap when
-        there is one, else they are registered for the call.  Returns
-        {"table", "sizes", "times", "nvls_min_bytes"}."""
+        too (cfCommSetNvlsMinBytes).  For AllReduce the two-shot kernel's CTA
+        budget is measured at the largest size over ``budgets`` and the
+        fastest installed (cfCommSetCtaBudget; budgets above half the SMs give
+        up the guarantee that a collective stays resident next to a compute
+        kernel holding the other half -- the default candidates stay below).  Buffers come from the
+        symmetric heap when there is one, else they are registered for the
+        call.  Returns {"table", "sizes", "times", "nvls_min_bytes",
+        "cta_budget_2pa"}."""
         import torch
         import torch.distributed as dist
         from . import tune as T
@@ -358,7 +363,19 @@ class Communicator:
                                                before=barrier)
                 except BadSizeError:   # beyond this algorithm's capacity (e.g. the LL scratch)
                     pass
+        # CTA budget of the two-shot kernel at the largest size (NVLink saturates
+        # well below 148 SMs; the default is 64 per rank)
+        bt = torch.full((len(budgets),), -1.0, dtype=torch.float64)
+        if kind == "allreduce" and budgets:
+            cnt = max(sizes) // es
+            aid = _lib.ALGOS["2pa"]
+            for k, b in enumerate(budgets):
+                self.set_cta_budget(int(b), "2pa")
+                bt[k] = T.time_graph(self.device, lambda: self._call(fn, x[:cnt], y[:cnt], cnt, aid, None), iters,
+                                     before=barrier)
+            self.set_cta_budget(0, "2pa")
         self.check_device_error()
+        dist.all_reduce(bt, op=dist.ReduceOp.MAX, group=self.group)
         dist.all_reduce(local, op=dist.ReduceOp.MAX, group=self.group)   # slowest rank, same on all ranks
         times = {a: [None if v < 0 else float(v) for v in local[k].tolist()] for k, a in enumerate(names)}
         nv = times.pop("switch_2pa", None)
@@ -367,8 +384,13 @@ class Communicator:
         if nv is not None:
             best = [min((t[i] for t in times.values() if t[i] is not None), default=None) for i in range(len(sizes))]
             nvls_min = T.nvls_min_from_times(sizes, nv, best)
+        best_budget = None
+        if kind == "allreduce" and budgets:
+            best_budget = int(budgets[int(torch.argmin(bt).item())])
         if install:
             T.install(self._comm, kind, dtype, table)
+            if best_budget is not None:
+                self.set_cta_budget(best_budget, "2pa")
             if nv is not None:
                 _lib.check(L.cfCommSetNvlsMinBytes(self._comm, ctypes.c_size_t(nvls_min if nvls_min else
                                                                               (1 << 64) - 1)))
@@ -380,7 +402,9 @@ class Communicator:
             self.deregister(y)
         if nv is not None:
             times["switch_2pa"] = nv
-        return {"table": table, "sizes": sizes, "times": times, "nvls_min_bytes": nvls_min}
+        return {"table": table, "sizes": sizes, "times": times, "nvls_min_bytes": nvls_min,
+                "cta_budget_2pa": best_budget,
+                "cta_budget_times_us": {int(b): round(float(t) * 1e6, 2) for b, t in zip(budgets, bt.tolist())}}
 
     def disable_switch(self) -> None:
         """Collective: stop using the NVLS switch on this heap (every rank calls
