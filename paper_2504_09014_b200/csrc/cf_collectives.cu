@@ -656,6 +656,14 @@ __global__ void __launch_bounds__(32) push_gather_bulk_kernel(const __grid_const
 // NVLS switch primitives (multimem_ld_reduce / multimem_st16) live in
 // device/cf_device.cuh with the SwitchChannelDevice they back.
 
+// Switch reductions each thread keeps in flight in the NVLS kernels: one
+// multimem.ld_reduce is a round trip through NVSwitch, so a single one per
+// thread caps a rank far below its NVLink rate.
+#ifndef CF_NVLS_U
+#define CF_NVLS_U 4
+#endif
+constexpr int kNvlsU = CF_NVLS_U;
+
 // K5 NVLS AllReduce (build_switch_2pa, cf/collectives.py:235-250; switch_reduce /
 // switch_broadcast, cf/channels.py:367-409), one launch per call.  The message
 // runs in pieces of the staging half; per piece:
@@ -699,9 +707,19 @@ __global__ void __launch_bounds__(512) nvls_kernel(const __grid_constant__ CollA
       }
     handshake(rk, n, e * kPhases + ph, true, a.gpu_scope);
     // B: reduce chunk r across the members, broadcast the result
-    for (size_t w = w0 + threadIdx.x; w < w1; w += blockDim.x) {
-      const size_t v = (size_t)r * cv + w;
-      if (v >= pv) break;
+    const size_t base = (size_t)r * cv;
+    const size_t we = pv > base ? min(w1, pv - base) : 0;
+    size_t w = w0 + threadIdx.x;
+    if (!a.emul)   // kNvlsU switch reductions in flight per thread
+      for (; w + (kNvlsU - 1) * blockDim.x < we; w += kNvlsU * blockDim.x) {
+        uint4 x[kNvlsU];
+#pragma unroll
+        for (int u = 0; u < kNvlsU; u++) x[u] = multimem_ld_reduce<T>(rk.nv_mc + (base + w + u * blockDim.x) * 16);
+#pragma unroll
+        for (int u = 0; u < kNvlsU; u++) multimem_st16(rk.nv_mc + a.half + (base + w + u * blockDim.x) * 16, x[u]);
+      }
+    for (; w < we; w += blockDim.x) {
+      const size_t v = base + w;
       if (!a.emul) {
         multimem_st16(rk.nv_mc + a.half + v * 16, multimem_ld_reduce<T>(rk.nv_mc + v * 16));
       } else {
@@ -750,8 +768,18 @@ __global__ void __launch_bounds__(512) nvls_direct_kernel(const __grid_constant_
   const size_t v0 = min((size_t)r * cv, full), v1 = min(v0 + cv, full);
   const size_t stride = (size_t)gridDim.x * blockDim.x;
   if (!a.emul) {
-    for (size_t v = v0 + (size_t)blockIdx.x * blockDim.x + threadIdx.x; v < v1; v += stride)
-      multimem_st16(rk.mc_out + v * 16, multimem_ld_reduce<T>(rk.mc_in + v * 16));
+    // kNvlsU switch reductions in flight per thread: one multimem.ld_reduce
+    // is a round trip through the switch, so a thread issuing one at a time
+    // would move 16 bytes per round trip
+    size_t v = v0 + (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; v + (kNvlsU - 1) * stride < v1; v += kNvlsU * stride) {
+      uint4 x[kNvlsU];
+#pragma unroll
+      for (int u = 0; u < kNvlsU; u++) x[u] = multimem_ld_reduce<T>(rk.mc_in + (v + u * stride) * 16);
+#pragma unroll
+      for (int u = 0; u < kNvlsU; u++) multimem_st16(rk.mc_out + (v + u * stride) * 16, x[u]);
+    }
+    for (; v < v1; v += stride) multimem_st16(rk.mc_out + v * 16, multimem_ld_reduce<T>(rk.mc_in + v * 16));
   } else {
     for (size_t v = v0 + (size_t)blockIdx.x * blockDim.x + threadIdx.x; v < v1; v += stride) {
       const uint4 s = switch_sum_unicast<T>((char* const*)rk.in, n, v * 16);

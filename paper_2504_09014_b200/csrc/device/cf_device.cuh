@@ -654,7 +654,16 @@ struct SwitchChannelDevice {
   // of `bytes` (multiple of 16).
   template <typename T>
   __device__ void reduce(char* dst, size_t src_off, size_t bytes, int tid, int nthreads) const {
-    for (size_t v = tid; v < bytes / 16; v += nthreads)
+    size_t v = tid;
+    if (mc)   // four switch reductions in flight per thread
+      for (; v + 3 * (size_t)nthreads < bytes / 16; v += 4 * (size_t)nthreads) {
+        uint4 x[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) x[u] = multimem_ld_reduce<T>(mc + src_off + (v + u * nthreads) * 16);
+#pragma unroll
+        for (int u = 0; u < 4; u++) st16(dst + (v + u * nthreads) * 16, x[u]);
+      }
+    for (; v < bytes / 16; v += nthreads)
       st16(dst + v * 16, mc ? multimem_ld_reduce<T>(mc + src_off + v * 16)
                             : switch_sum_unicast<T>(uc, n, src_off + v * 16));
   }
@@ -674,7 +683,16 @@ struct SwitchChannelDevice {
   // (one pass, the NVLS AllReduce of one chunk)
   template <typename T>
   __device__ void reduce_broadcast(size_t dst_off, size_t src_off, size_t bytes, int tid, int nthreads) const {
-    for (size_t v = tid; v < bytes / 16; v += nthreads) {
+    size_t v = tid;
+    if (mc)
+      for (; v + 3 * (size_t)nthreads < bytes / 16; v += 4 * (size_t)nthreads) {
+        uint4 x[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) x[u] = multimem_ld_reduce<T>(mc + src_off + (v + u * nthreads) * 16);
+#pragma unroll
+        for (int u = 0; u < 4; u++) multimem_st16(mc + dst_off + (v + u * nthreads) * 16, x[u]);
+      }
+    for (; v < bytes / 16; v += nthreads) {
       if (mc) {
         multimem_st16(mc + dst_off + v * 16, multimem_ld_reduce<T>(mc + src_off + v * 16));
       } else {
