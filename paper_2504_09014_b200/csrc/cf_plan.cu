@@ -103,6 +103,7 @@ struct cfPlan {
   bool has_prologue = false;          // per-call zeroing / private input copy
   bool single_ok = false;             // every program one plain MULTI / COPY: plan_single_kernel applies
   bool ll_ok = false;                 // every program a short LL16 op sequence: plan_ll_kernel applies
+  std::vector<int> ll_stream;         // per program: PUT_PACKETS op streamed with the MULTI after it (-1: none)
   // one-process-per-GPU: this process runs rank `me`'s programs; the peers'
   // plan heaps are IPC-mapped by cfPlanConnect, which finalizes the plan
   bool mp = false;
@@ -1121,6 +1122,93 @@ void drop_redundant_syncs(cfPlan* pl) {
   }
 }
 
+// Streamed packet pairs of the compiled LL kernel.  A program's unpaired
+// PUT_PACKETS followed by a MULTI of the same size that reduces LL16 packets
+// may run interleaved (a thread reduces unit u one iteration after putting
+// it) when the pairs form a closed, symmetric exchange:
+//  - every pair has the same size (same CTA slices, same unit -> thread map);
+//  - each packet source of a pair's MULTI is exactly the range one pair's
+//    PUT writes (same location and base, same plan flag);
+//  - nothing else in the plan touches the ranges the pair PUTs write;
+//  - the PUT's source and the MULTI's I/O destinations start at the same
+//    offset (a thread only overwrites units it already put when in place).
+// Then the thread that puts unit u on every rank has the same index and
+// iteration, and the thread waiting for unit u at iteration k depends only on
+// puts of iteration k - 1 (the hand one-shot's argument); without these
+// conditions the plan runs op by op.
+void compute_ll_stream(cfPlan* pl) {
+  const size_t np = pl->prog_ops.size();
+  pl->ll_stream.assign(np, -1);
+  if (!pl->ll_ok) return;
+  if (const char* ev = getenv("CF_PLAN_LL_STREAM"))   // diagnostic: 0 runs op by op
+    if (atoi(ev) == 0) return;
+  const int es = pl->es;
+  std::vector<int> cand(np, -1);
+  uint64_t size = 0;
+  bool any = false;
+  for (size_t p = 0; p < np; p++) {
+    const auto& ops = pl->prog_ops[p];
+    for (size_t i = 0; i + 1 < ops.size(); i++) {
+      const DevOp &u = ops[i], &m = ops[i + 1];
+      if (u.code != D_PUT_PACKETS || (u.flags & F_PAIRED) || !(u.flags & F_LL16)) continue;
+      if (m.code != D_MULTI || !(m.flags & F_VEC) || !m.pkt_mask || m.size != u.size) continue;
+      if (any && u.size != size) return;
+      bool io_ok = true;
+      for (int d = 0; d < m.ndst; d++)
+        if (m.dst[d].buf != kAbsolute && u.src[0].buf != kAbsolute && m.dst[d].off != u.src[0].off) io_ok = false;
+      if (!io_ok) return;
+      cand[p] = (int)i;
+      size = u.size;
+      any = true;
+      break;
+    }
+  }
+  if (!any) return;
+  struct Range {
+    size_t p;
+    int k;
+    DRef loc;
+    uint64_t lo, hi;
+    uint32_t flag;
+  };
+  std::vector<Range> put_ranges;
+  for (size_t p = 0; p < np; p++) {
+    if (cand[p] < 0) continue;
+    const DevOp& u = pl->prog_ops[p][cand[p]];
+    for (int k = 0; k < u.ndst; k++) {
+      uint64_t lo, hi;
+      dref_span(u, u.dst[k], true, es, lo, hi);
+      put_ranges.push_back({p, k, u.dst[k], lo, hi, u.llflag});
+    }
+  }
+  for (size_t p = 0; p < np; p++)
+    for (size_t i = 0; i < pl->prog_ops[p].size(); i++) {
+      const DevOp& d = pl->prog_ops[p][i];
+      if (!data_code(d.code)) continue;
+      const bool pair_put = cand[p] == (int)i, pair_multi = cand[p] >= 0 && cand[p] + 1 == (int)i;
+      for (int k = 0; k < d.nsrc + d.ndst; k++) {
+        const bool is_src = k < d.nsrc;
+        const DRef& r = is_src ? d.src[k] : d.dst[k - d.nsrc];
+        const bool packet = (d.code == D_READ_PACKETS && is_src) || (d.code == D_PUT_PACKETS && !is_src) ||
+                            (d.code == D_MULTI && is_src && ((d.pkt_mask >> k) & 1u));
+        uint64_t lo, hi;
+        dref_span(d, r, packet, es, lo, hi);
+        bool matched = false;
+        for (const Range& R : put_ranges) {
+          if (!same_loc(r, R.loc) || !(lo < R.hi && R.lo < hi)) continue;
+          if (pair_put && !is_src && R.p == p && R.k == k - d.nsrc) continue;   // the range itself
+          if (pair_multi && packet && lo == R.lo && hi == R.hi && d.llflag_k[k] == R.flag) {
+            matched = true;
+            continue;
+          }
+          return;   // touched by something outside the exchange
+        }
+        if (pair_multi && packet && !matched) return;   // a packet source no pair writes
+      }
+    }
+  for (size_t p = 0; p < np; p++) pl->ll_stream[p] = cand[p];
+}
+
 // Bake plan-owned buffer addresses into the device ops, fuse packet reads,
 // upload the per-device tables, start the proxy (port channels).
 cfStatus finalize(cfPlan* pl) {
@@ -1181,6 +1269,7 @@ cfStatus finalize(cfPlan* pl) {
         pl->ll_ok = pl->ll_ok && d.size * (uint64_t)pl->es <= ll_max;
       }
     }
+    compute_ll_stream(pl);
     pl->single_ok = pl->cls == 0 && !pl->prog_ops.empty() && (int)pl->prog_ops.size() <= kSingleProgs;
     for (auto& prog : pl->prog_ops) {
       if (!pl->single_ok) break;
@@ -1535,6 +1624,8 @@ extern "C" cfStatus cfPlanExecute(cfPlan_t pl, const void* const* inputs, void* 
         auto& P = la.p[p];
         P.rank = pl->prog_rank[G.progs[p]];
         P.nops = G.end[p] - G.beg[p];
+        // streamed pairs need the same CTAs per program on every rank
+        P.stream = (K2 == pl->K || np == (int)pl->prog_ops.size()) ? pl->ll_stream[G.progs[p]] : -1;
         for (int i = 0; i < P.nops; i++) {
           const DevOp& d = bb->h_pin[G.beg[p] + i];
           auto& o = P.op[i];
@@ -1552,6 +1643,9 @@ extern "C" cfStatus cfPlanExecute(cfPlan_t pl, const void* const* inputs, void* 
           o.flags = d.flags;
           o.pkt_mask = d.pkt_mask;
         }
+        // streaming pays from a few units per thread (one or two: op by op
+        // is as fast; 1pa plan b=4 7.7 vs 8.8 us, b=64 57.8 vs 49.1 us)
+        if (P.stream >= 0 && P.op[P.stream].per * pl->es / 8 <= 2ull * pl->threads) P.stream = -1;
         la.rank_ctas[P.rank] += K2;
       }
       for (int r = 0; r < n; r++) la.st[r] = &a.st[r]->base;

@@ -224,6 +224,7 @@ struct LLArgs {
   struct Prog {
     Op op[kLLOps];
     int nops, rank;
+    int stream;            // op index of a PUT_PACKETS run streamed with the MULTI after it (-1: none)
   } p[kLLProgs];
   RankState* st[CF_MAX_RANKS];
   int rank_ctas[CF_MAX_RANKS];

@@ -712,12 +712,70 @@ __global__ void __launch_bounds__(512) plan_single_kernel(const __grid_constant_
   }
 }
 
+// One payload unit of an unpaired PUT_PACKETS: one load, every range's packet.
+// (`gpu`: every rank on this GPU, plain stores meet in its L2)
+__device__ __forceinline__ void ll_bcast_unit(const LLArgs::Op& op, uint64_t u, uint32_t pflag, int nb, bool gpu) {
+  const uint2 d = *reinterpret_cast<const uint2*>(op.src[0] + u * 8);
+#pragma unroll
+  for (int k = 0; k < 8; k++)
+    if (k < nb) ll16_put_scoped(op.dst[k] + u * 16, d, pflag, gpu);
+}
+
+// One 8-byte unit of a MULTI / COPY: every source (plain unit or LL16
+// packet) in flight, then the plan's order and rounding.
+template <typename T>
+__device__ __forceinline__ void ll_multi_unit(const LLArgs::Op& op, uint64_t u, uint64_t e, uint32_t fs,
+                                              RankState* rs) {
+  using A = typename Vec<T>::Acc;
+  constexpr int V = Vec<T>::N;
+  const int nsrc = op.nsrc, ndst = op.ndst;
+  const uint32_t pkt = op.pkt_mask;
+  uint4 x[8];
+#pragma unroll
+  for (int i = 0; i < 8; i++)
+    if (i < nsrc) {
+      if ((pkt >> i) & 1u) {
+        x[i] = ld16_volatile(op.src[i] + u * 16);
+      } else {
+        const uint2 d = *reinterpret_cast<const uint2*>(op.src[i] + u * 8);
+        x[i] = make_uint4(d.x, 0u, d.y, 0u);
+      }
+    }
+#pragma unroll
+  for (int i = 0; i < 8; i++)
+    if (i < nsrc && ((pkt >> i) & 1u)) {
+      const uint32_t f = runtime_flag(e, fs, op.llflag_k[i]);
+      if (x[i].y != f || x[i].w != f) {
+        const uint2 d = ll16_get(op.src[i] + u * 16, f, rs);
+        x[i] = make_uint4(d.x, f, d.y, f);
+      }
+    }
+  uint2 res = make_uint2(x[0].x, x[0].z);
+  if (op.code == D_MULTI) {
+    const bool round_each = op.flags & F_ROUND_EACH;
+    A acc[V];
+    if (op.flags & F_ZERO) {
+#pragma unroll
+      for (int i = 0; i < V; i++) acc[i] = A(0);
+      acc_vec<T>(acc, make_uint4(x[0].x, x[0].z, 0u, 0u), round_each);
+    } else {
+      Vec<T>::load(make_uint4(x[0].x, x[0].z, 0u, 0u), acc);
+    }
+#pragma unroll
+    for (int i = 1; i < 8; i++)
+      if (i < nsrc) acc_vec<T>(acc, make_uint4(x[i].x, x[i].z, 0u, 0u), round_each);
+    const uint4 r4 = Vec<T>::store(acc);
+    res = make_uint2(r4.x, r4.y);
+  }
+#pragma unroll
+  for (int d = 0; d < 8; d++)
+    if (d < ndst) *reinterpret_cast<uint2*>(op.dst[d] + u * 8) = res;
+}
+
 // The compiled LL plan kernel (see LLArgs).  Op fields are read from the
 // parameter space (uniform per CTA); every thread reads the call epoch itself.
 template <typename T>
 __global__ void __launch_bounds__(512, 2) plan_ll_kernel(const __grid_constant__ LLArgs a) {
-  using A = typename Vec<T>::Acc;
-  constexpr int V = Vec<T>::N;
   constexpr int H = 8 / sizeof(T);   // elements per 8-byte payload unit
   const int pid = blockIdx.x / a.K, j = blockIdx.x % a.K;
   const LLArgs::Prog& P = a.p[pid];
@@ -739,19 +797,15 @@ __global__ void __launch_bounds__(512, 2) plan_ll_kernel(const __grid_constant__
     if (lo >= hi) continue;
     const uint64_t u0 = lo / H, u1 = (hi + H - 1) / H;
     const uint32_t nu = (uint32_t)(u1 - u0);
-    if (op.code == D_PUT_PACKETS && !(op.flags & F_PAIRED)) {
+    const bool streamed = oi == P.stream;   // host-checked pair: this PUT, then the MULTI after it
+    if (op.code == D_PUT_PACKETS && !(op.flags & F_PAIRED) && !streamed) {
       // one payload to ndst ranges: one load per unit, every range's packet
       const uint32_t pflag = runtime_flag(e, fs, op.llflag);
       const int nb = op.ndst;
-      for (uint64_t u = u0 + threadIdx.x; u < u1; u += blockDim.x) {
-        const uint2 d = *reinterpret_cast<const uint2*>(op.src[0] + u * 8);
-#pragma unroll
-        for (int k = 0; k < 8; k++)
-          if (k < nb) ll16_put(op.dst[k] + u * 16, d, pflag);
-      }
+      for (uint64_t u = u0 + threadIdx.x; u < u1; u += blockDim.x) ll_bcast_unit(op, u, pflag, nb, a.bar.gpu_scope);
       continue;
     }
-    if (op.code == D_PUT_PACKETS || op.code == D_READ_PACKETS) {
+    if ((op.code == D_PUT_PACKETS || op.code == D_READ_PACKETS) && !streamed) {
       const bool put = op.code == D_PUT_PACKETS;
       const int nb = put ? op.ndst : op.nsrc;
       const bool paired = op.flags & F_PAIRED;
@@ -765,7 +819,7 @@ __global__ void __launch_bounds__(512, 2) plan_ll_kernel(const __grid_constant__
         const uint64_t u = u0 + (w - k * nu);
         if (put) {
           const uint2 d = *reinterpret_cast<const uint2*>(op.src[paired ? k : 0] + u * 8);
-          ll16_put(op.dst[k] + u * 16, d, pflag);
+          ll16_put_scoped(op.dst[k] + u * 16, d, pflag, a.bar.gpu_scope);
         } else {
           const uint32_t f = runtime_flag(e, fs, op.llflag_k[k]);
           const uint4 raw = ld16_volatile(op.src[k] + u * 16);
@@ -776,52 +830,25 @@ __global__ void __launch_bounds__(512, 2) plan_ll_kernel(const __grid_constant__
       }
       continue;
     }
-    // MULTI / COPY, one 8-byte payload unit per thread: every source (plain
-    // unit or LL16 packet) in flight, then the plan's order and rounding
-    const int nsrc = op.nsrc, ndst = op.ndst;
-    const bool multi = op.code == D_MULTI, zero = op.flags & F_ZERO, round_each = op.flags & F_ROUND_EACH;
-    const uint32_t pkt = op.pkt_mask;
-    for (uint64_t u = u0 + threadIdx.x; u < u1; u += blockDim.x) {
-      uint4 x[8];
-#pragma unroll
-      for (int i = 0; i < 8; i++)
-        if (i < nsrc) {
-          if ((pkt >> i) & 1u) {
-            x[i] = ld16_volatile(op.src[i] + u * 16);
-          } else {
-            const uint2 d = *reinterpret_cast<const uint2*>(op.src[i] + u * 8);
-            x[i] = make_uint4(d.x, 0u, d.y, 0u);
-          }
-        }
-#pragma unroll
-      for (int i = 0; i < 8; i++)
-        if (i < nsrc && ((pkt >> i) & 1u)) {
-          const uint32_t f = runtime_flag(e, fs, op.llflag_k[i]);
-          if (x[i].y != f || x[i].w != f) {
-            const uint2 d = ll16_get(op.src[i] + u * 16, f, rs);
-            x[i] = make_uint4(d.x, f, d.y, f);
-          }
-        }
-      uint2 res = make_uint2(x[0].x, x[0].z);
-      if (multi) {
-        A acc[V];
-        if (zero) {
-#pragma unroll
-          for (int i = 0; i < V; i++) acc[i] = A(0);
-          acc_vec<T>(acc, make_uint4(x[0].x, x[0].z, 0u, 0u), round_each);
-        } else {
-          Vec<T>::load(make_uint4(x[0].x, x[0].z, 0u, 0u), acc);
-        }
-#pragma unroll
-        for (int i = 1; i < 8; i++)
-          if (i < nsrc) acc_vec<T>(acc, make_uint4(x[i].x, x[i].z, 0u, 0u), round_each);
-        const uint4 r4 = Vec<T>::store(acc);
-        res = make_uint2(r4.x, r4.y);
-      }
-#pragma unroll
-      for (int d = 0; d < 8; d++)
-        if (d < ndst) *reinterpret_cast<uint2*>(op.dst[d] + u * 8) = res;
+    // MULTI / COPY, one 8-byte payload unit per thread.  A streamed pair
+    // (PUT_PACKETS + the MULTI reducing the packets the peers' puts land)
+    // runs interleaved: a thread reduces unit u one iteration after putting
+    // it, and the peers' threads with the same index put it at about the same
+    // time, so packets are read while still in L2 (the hand one-shot's
+    // schedule; the host checked the pair's symmetry).  One call site of the
+    // unit body keeps its in-flight sources in registers.
+    const LLArgs::Op& m = P.op[oi + streamed];
+    const uint32_t pflag = streamed ? runtime_flag(e, fs, op.llflag) : 0u;
+    uint64_t prev = ~(uint64_t)0;
+    for (uint64_t u = u0 + threadIdx.x;; u += blockDim.x) {
+      const bool has = u < u1;
+      if (streamed && has) ll_bcast_unit(op, u, pflag, op.ndst, a.bar.gpu_scope);
+      const uint64_t mu = streamed ? prev : (has ? u : ~(uint64_t)0);
+      if (mu != ~(uint64_t)0) ll_multi_unit<T>(m, mu, e, fs, rs);
+      if (!has) break;
+      prev = u;
     }
+    oi += streamed;
   }
   if (a.bar.exit)
     rank_barrier_raw(a.bar.pst, a.bar.n, P.rank, a.bar.leader[P.rank], a.rank_ctas[P.rank], e * per_call,

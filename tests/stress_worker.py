@@ -68,11 +68,52 @@ def run_inproc(iters: int) -> dict:
     return out
 
 
+PLANS = (("1pa_n8_e64", 128 * 16), ("2pa_ll_n8_e64", 128 * 4), ("2pa_memory_n8_e64", 128 * 16))
+
+
+def _plan_runtimes(w):
+    """DSL plans on the compiled K10 kernels (the 1pa plan's streamed packet
+    pairs, the LL two-shot plan, the single-op HB plan), i32."""
+    from paper_2504_09014_b200 import Runtime, parse_plan
+    from paper_2504_09014_b200.plan import scale_plan
+    rts = []
+    for name, factor in PLANS:
+        with open(os.path.join(ROOT, "tests", "golden", "plans", name + ".json"), "rb") as f:
+            rts.append((name, Runtime(scale_plan(parse_plan(f.read()), factor), w, dtype="i32")))
+    return rts
+
+
+def _check_plans(rts, n, it, out):
+    import torch
+    from paper_2504_09014_b200.errors import DeadlockError
+    for name, rt in rts:
+        ins = gen_inputs(n, rt.in_elems, "i32", "int", 13 * it + rt.in_elems)
+        xs = [torch.from_numpy(x).cuda() for x in ins]
+        ys = [torch.empty(rt.out_elems, dtype=torch.int32, device="cuda") for _ in range(n)]
+        try:
+            rt.run_raw(xs, ys)
+            rt.check_device_error()
+            want = np.sum(np.stack(ins), axis=0, dtype=np.int32)   # i32: exact in any order
+            _record(out, f"plan:{name}:{it}", all(np.array_equal(ys[r].cpu().numpy(), want) for r in range(n)))
+        except DeadlockError:
+            _deadlock(out)
+
+
 def _inproc_loop(w, n, iters, out):
+    rts = _plan_runtimes(w)
+    try:
+        _inproc_iters(w, n, iters, out, rts)
+    finally:
+        for _, rt in rts:
+            rt.close()
+
+
+def _inproc_iters(w, n, iters, out, rts):
     import torch
     from paper_2504_09014_b200 import collective
     from paper_2504_09014_b200.errors import DeadlockError
     for it in range(iters):
+        _check_plans(rts, n, it, out)
         for elems in SIZES:
             ins = gen_inputs(n, elems, "i32", "int", 1000 * it + elems)
             for name, var, oname in AR:

@@ -77,6 +77,8 @@ def _scaled(doc: bytes, factor: int, dtype: str) -> bytes:
 
 
 @pytest.mark.parametrize("name,factor", [("2pa_memory_n8_e64", 128), ("1pa_n8_e64", 128),
+                                         ("1pa_n8_e64", 128 * 64), ("1pa_n8_e64", 128 * 37 + 8),
+                                         ("2pa_ll_n8_e64", 128 * 16),
                                          ("2pa_memory_n8_e64", 128 * 64),
                                          ("2pa_memory_n8_e64_i2", 512),
                                          ("switch_2pa_n8_e64", 1024), ("allpairs_ag_n8_e64", 256)])
@@ -214,3 +216,34 @@ def test_dsl_path_low_precision_vs_plan_oracle(algo, var, dtype):
     want = oracle.run_plan(doc, ins, dtype=dtype)
     for r in range(n):
         assert np.array_equal(got[r].view(np.uint8), want[r][:elems].view(np.uint8)), r
+
+
+@pytest.mark.parametrize("factor", [128 * 4, 128 * 64, 128 * 37 + 8])
+def test_1pa_plan_streamed_pairs_in_place(factor, monkeypatch):
+    """The compiled LL kernel streams the 1pa plan's packet scatter with its
+    read-reduce (a thread reduces unit u one iteration after putting it).
+    Streamed and op-by-op runs give the oracle's bits, out of place and in
+    place (output = input: a thread only overwrites units it already put),
+    on consecutive calls (alternating LL flag epochs)."""
+    import torch
+    from paper_2504_09014_b200 import Runtime, parse_plan
+    doc = _scaled(_load("1pa_n8_e64"), factor, "f32")
+    plan = parse_plan(doc)
+    e = next(b.elems for b in plan.buffers if b.kind == "input")
+    for stream in ("1", "0"):
+        monkeypatch.setenv("CF_PLAN_LL_STREAM", stream)
+        rt = Runtime(plan, world(8), dtype="f32")
+        for it in range(3):
+            ins = gen_inputs(8, e, "f32", "normal", factor + it, scale=0.02)
+            want = oracle.run_plan(doc, ins, dtype="f32")
+            xs = [torch.from_numpy(x).cuda() for x in ins]
+            ys = [torch.empty_like(x) for x in xs]
+            rt.run_raw(xs, ys)
+            rt.check_device_error()
+            for r in range(8):
+                assert np.array_equal(ys[r].cpu().numpy().view(np.uint32), want[r].view(np.uint32)), (stream, it, r)
+            rt.run_raw(xs, xs)   # in place
+            rt.check_device_error()
+            for r in range(8):
+                assert np.array_equal(xs[r].cpu().numpy().view(np.uint32), want[r].view(np.uint32)), (stream, it, r)
+        rt.close()
