@@ -104,6 +104,7 @@ struct cfPlan {
   bool single_ok = false;             // every program one plain MULTI / COPY: plan_single_kernel applies
   bool ll_ok = false;                 // every program a short LL16 op sequence: plan_ll_kernel applies
   std::vector<int> ll_stream;         // per program: PUT_PACKETS op streamed with the MULTI after it (-1: none)
+  std::vector<int> ll_fuse_put;       // per program: MULTI whose result the PUT_PACKETS two ops on broadcasts (-1: none)
   // one-process-per-GPU: this process runs rank `me`'s programs; the peers'
   // plan heaps are IPC-mapped by cfPlanConnect, which finalizes the plan
   bool mp = false;
@@ -541,12 +542,12 @@ bool touched_elsewhere(const cfPlan* pl, const DRef& loc, uint64_t lo, uint64_t 
 // when T_k is scratch nobody else touches: the reduction reads the LL16
 // packets directly (one pass, no temporary), exactly the one-shot LL kernel.
 void fuse_packet_reads(cfPlan* pl) {
-  // Below ~8 KiB of payload per range the separate batched read (its items
-  // spread over every thread) and a plain-source reduce beat the fused
-  // reduce, whose threads each chase 2 packets per source (2pa_ll plan b=1:
-  // 12.1 -> 11.4 us); from there on fusing wins (b=16: 16.2 -> 15.1 us,
-  // b=256: 101 -> 80 us; one box, A/B).
-  long long min_bytes = 8 << 10;
+  // Always fused: on the compiled LL kernel (one unit per thread, every
+  // source in flight) the fused reduce wins at every size (2pa_ll plan b=1
+  // 8.9 -> 8.3 us: no sync, no scratch round trip).  (The interpreter, which
+  // runs what does not compile, preferred the separate batched read below
+  // 8 KiB per range: b=1 12.1 -> 11.4 us.)
+  long long min_bytes = 0;
   if (const char* ev = getenv("CF_PLAN_FUSE_READS_MIN")) min_bytes = atoll(ev);   // diagnostic
   if (const char* ev = getenv("CF_PLAN_FUSE_READS"))   // diagnostic: 0 keeps read_packets separate
     if (atoi(ev) == 0) return;
@@ -1054,6 +1055,27 @@ cfStatus load(cfComm* c, const char* json, size_t len, int dtype_override, cfPla
   return CF_OK;
 }
 
+// Do data ops x and y touch a common byte with at least one of them writing it?
+bool ops_conflict(const DevOp& x, const DevOp& y, int es) {
+  for (int i = 0; i < x.nsrc + x.ndst; i++)
+    for (int k = 0; k < y.nsrc + y.ndst; k++) {
+      const bool xw = i >= x.nsrc, yw = k >= y.nsrc;
+      if (!xw && !yw) continue;
+      const DRef& rx = xw ? x.dst[i - x.nsrc] : x.src[i];
+      const DRef& ry = yw ? y.dst[k - y.nsrc] : y.src[k];
+      if (!same_loc(rx, ry)) continue;
+      auto pkt = [](const DevOp& d, int j, bool w) {
+        return (d.code == D_READ_PACKETS && !w) || (d.code == D_PUT_PACKETS && w) ||
+               (d.code == D_MULTI && !w && ((d.pkt_mask >> j) & 1u));
+      };
+      uint64_t a0, a1, b0, b1;
+      dref_span(x, rx, pkt(x, i, xw), es, a0, a1);
+      dref_span(y, ry, pkt(y, k, yw), es, b0, b1);
+      if (a0 < b1 && b0 < a1) return true;
+    }
+  return false;
+}
+
 // CTA-local syncs that another barrier already provides: first / last op of a
 // program (the staging barrier / the end-of-call barrier), next to an op that
 // starts with a block barrier (signal, port ops, group / device barriers,
@@ -1084,25 +1106,7 @@ void drop_redundant_syncs(cfPlan* pl) {
   // side orders nothing (e.g. the 1pa plan's packet scatter vs its fused
   // read-reduce: packets written by peers are ordered by their flags).
   const int es = pl->es;
-  auto refs_conflict = [&](const DevOp& x, const DevOp& y) {
-    for (int i = 0; i < x.nsrc + x.ndst; i++)
-      for (int k = 0; k < y.nsrc + y.ndst; k++) {
-        const bool xw = i >= x.nsrc, yw = k >= y.nsrc;
-        if (!xw && !yw) continue;
-        const DRef& rx = xw ? x.dst[i - x.nsrc] : x.src[i];
-        const DRef& ry = yw ? y.dst[k - y.nsrc] : y.src[k];
-        if (!same_loc(rx, ry)) continue;
-        auto pkt = [](const DevOp& d, int j, bool w) {
-          return (d.code == D_READ_PACKETS && !w) || (d.code == D_PUT_PACKETS && w) ||
-                 (d.code == D_MULTI && !w && ((d.pkt_mask >> j) & 1u));
-        };
-        uint64_t a0, a1, b0, b1;
-        dref_span(x, rx, pkt(x, i, xw), es, a0, a1);
-        dref_span(y, ry, pkt(y, k, yw), es, b0, b1);
-        if (a0 < b1 && b0 < a1) return true;
-      }
-    return false;
-  };
+  auto refs_conflict = [&](const DevOp& x, const DevOp& y) { return ops_conflict(x, y, es); };
   auto is_data = [](uint8_t c) { return c == D_MULTI || c == D_COPY || c == D_PUT_PACKETS || c == D_READ_PACKETS; };
   for (auto& ops : pl->prog_ops) {
     for (size_t i = 0; i < ops.size(); i++) {
@@ -1209,6 +1213,53 @@ void compute_ll_stream(cfPlan* pl) {
   for (size_t p = 0; p < np; p++) pl->ll_stream[p] = cand[p];
 }
 
+// Reduce-then-broadcast of the compiled LL kernel: MULTI m ; sync ; an
+// unpaired PUT_PACKETS whose source is m's destination (same location, base
+// and size) -- the two-shot LL plan's phase-2 scatter of the reduced chunk.
+// Both ops map unit u to the same thread, so the thread broadcasts the value
+// it just reduced (no sync, no reload) when m and the PUT are the only
+// conflicting pair across that sync.
+void compute_ll_fuse_put(cfPlan* pl) {
+  const size_t np = pl->prog_ops.size();
+  pl->ll_fuse_put.assign(np, -1);
+  if (!pl->ll_ok) return;
+  if (const char* ev = getenv("CF_PLAN_LL_FUSE_PUT"))   // diagnostic: 0 keeps the sync and the reload
+    if (atoi(ev) == 0) return;
+  const int es = pl->es;
+  auto is_data = [](uint8_t c) { return c == D_MULTI || c == D_COPY || c == D_PUT_PACKETS || c == D_READ_PACKETS; };
+  for (size_t p = 0; p < np; p++) {
+    const auto& ops = pl->prog_ops[p];
+    for (size_t i = 0; i + 2 < ops.size(); i++) {
+      const DevOp &m = ops[i], &u = ops[i + 2];
+      if ((m.code != D_MULTI && m.code != D_COPY) || !(m.flags & F_VEC) || ops[i + 1].code != D_SYNC_CTA) continue;
+      if (u.code != D_PUT_PACKETS || (u.flags & F_PAIRED) || !(u.flags & F_LL16) || u.size != m.size) continue;
+      bool src_is_dst = false, misaligned = false;
+      for (int d = 0; d < m.ndst; d++) {
+        const bool same = same_loc(m.dst[d], u.src[0]) && m.dst[d].off == u.src[0].off;
+        src_is_dst |= same;
+        uint64_t a0, a1, b0, b1;
+        dref_span(m, m.dst[d], false, es, a0, a1);
+        dref_span(u, u.src[0], false, es, b0, b1);
+        misaligned |= !same && same_loc(m.dst[d], u.src[0]) && a0 < b1 && b0 < a1;
+      }
+      if (!src_is_dst || misaligned) continue;
+      DevOp writes = u;   // the PUT's packet stores against everything m touches
+      writes.nsrc = 0;
+      if (ops_conflict(m, writes, es)) continue;
+      size_t a = i, b = i + 2;
+      while (a > 0 && is_data(ops[a - 1].code)) a--;
+      while (b < ops.size() && is_data(ops[b].code)) b++;
+      bool other = false;
+      for (size_t x = a; x <= i && !other; x++)
+        for (size_t y = i + 2; y < b && !other; y++)
+          if (!(x == i && y == i + 2)) other = ops_conflict(ops[x], ops[y], es);
+      if (other) continue;
+      pl->ll_fuse_put[p] = (int)i;
+      break;
+    }
+  }
+}
+
 // Bake plan-owned buffer addresses into the device ops, fuse packet reads,
 // upload the per-device tables, start the proxy (port channels).
 cfStatus finalize(cfPlan* pl) {
@@ -1270,6 +1321,7 @@ cfStatus finalize(cfPlan* pl) {
       }
     }
     compute_ll_stream(pl);
+    compute_ll_fuse_put(pl);
     pl->single_ok = pl->cls == 0 && !pl->prog_ops.empty() && (int)pl->prog_ops.size() <= kSingleProgs;
     for (auto& prog : pl->prog_ops) {
       if (!pl->single_ok) break;
@@ -1626,6 +1678,7 @@ extern "C" cfStatus cfPlanExecute(cfPlan_t pl, const void* const* inputs, void* 
         P.nops = G.end[p] - G.beg[p];
         // streamed pairs need the same CTAs per program on every rank
         P.stream = (K2 == pl->K || np == (int)pl->prog_ops.size()) ? pl->ll_stream[G.progs[p]] : -1;
+        P.fuse_put = pl->ll_fuse_put[G.progs[p]];
         for (int i = 0; i < P.nops; i++) {
           const DevOp& d = bb->h_pin[G.beg[p] + i];
           auto& o = P.op[i];

@@ -225,6 +225,7 @@ struct LLArgs {
     Op op[kLLOps];
     int nops, rank;
     int stream;            // op index of a PUT_PACKETS run streamed with the MULTI after it (-1: none)
+    int fuse_put;          // op index of a MULTI whose units the PUT_PACKETS at +2 broadcasts (-1: none)
   } p[kLLProgs];
   RankState* st[CF_MAX_RANKS];
   int rank_ctas[CF_MAX_RANKS];

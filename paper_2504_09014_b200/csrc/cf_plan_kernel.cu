@@ -724,8 +724,8 @@ __device__ __forceinline__ void ll_bcast_unit(const LLArgs::Op& op, uint64_t u, 
 // One 8-byte unit of a MULTI / COPY: every source (plain unit or LL16
 // packet) in flight, then the plan's order and rounding.
 template <typename T>
-__device__ __forceinline__ void ll_multi_unit(const LLArgs::Op& op, uint64_t u, uint64_t e, uint32_t fs,
-                                              RankState* rs) {
+__device__ __forceinline__ uint2 ll_multi_unit(const LLArgs::Op& op, uint64_t u, uint64_t e, uint32_t fs,
+                                               RankState* rs) {
   using A = typename Vec<T>::Acc;
   constexpr int V = Vec<T>::N;
   const int nsrc = op.nsrc, ndst = op.ndst;
@@ -741,15 +741,36 @@ __device__ __forceinline__ void ll_multi_unit(const LLArgs::Op& op, uint64_t u, 
         x[i] = make_uint4(d.x, 0u, d.y, 0u);
       }
     }
+  // unstamped packets are re-polled together, one round trip per round for
+  // all of them (not one per late source)
+  uint32_t pend = 0;
 #pragma unroll
   for (int i = 0; i < 8; i++)
     if (i < nsrc && ((pkt >> i) & 1u)) {
       const uint32_t f = runtime_flag(e, fs, op.llflag_k[i]);
-      if (x[i].y != f || x[i].w != f) {
-        const uint2 d = ll16_get(op.src[i] + u * 16, f, rs);
-        x[i] = make_uint4(d.x, f, d.y, f);
+      if (x[i].y != f || x[i].w != f) pend |= 1u << i;
+    }
+  if (pend) {
+    const uint64_t t0 = globaltimer();
+    for (uint32_t it = 1; pend; ++it) {
+#pragma unroll
+      for (int i = 0; i < 8; i++)
+        if ((pend >> i) & 1u) x[i] = ld16_volatile(op.src[i] + u * 16);
+#pragma unroll
+      for (int i = 0; i < 8; i++)
+        if ((pend >> i) & 1u) {
+          const uint32_t f = runtime_flag(e, fs, op.llflag_k[i]);
+          if (x[i].y == f && x[i].w == f) pend &= ~(1u << i);
+        }
+      if ((it & 255u) == 0 && pend) {
+        if (*(volatile uint32_t*)&rs->error != kDevOk) break;
+        if (globaltimer() - t0 > rs->timeout_ns) {
+          atomicExch(&rs->error, (uint32_t)kDevTimeout);
+          break;
+        }
       }
     }
+  }
   uint2 res = make_uint2(x[0].x, x[0].z);
   if (op.code == D_MULTI) {
     const bool round_each = op.flags & F_ROUND_EACH;
@@ -770,6 +791,7 @@ __device__ __forceinline__ void ll_multi_unit(const LLArgs::Op& op, uint64_t u, 
 #pragma unroll
   for (int d = 0; d < 8; d++)
     if (d < ndst) *reinterpret_cast<uint2*>(op.dst[d] + u * 8) = res;
+  return res;
 }
 
 // The compiled LL plan kernel (see LLArgs).  Op fields are read from the
@@ -777,6 +799,8 @@ __device__ __forceinline__ void ll_multi_unit(const LLArgs::Op& op, uint64_t u, 
 template <typename T>
 __global__ void __launch_bounds__(512, 2) plan_ll_kernel(const __grid_constant__ LLArgs a) {
   constexpr int H = 8 / sizeof(T);   // elements per 8-byte payload unit
+  TS_DECL
+  TS_MARK();
   const int pid = blockIdx.x / a.K, j = blockIdx.x % a.K;
   const LLArgs::Prog& P = a.p[pid];
   RankState* rs = a.st[P.rank];
@@ -786,8 +810,10 @@ __global__ void __launch_bounds__(512, 2) plan_ll_kernel(const __grid_constant__
   if (a.bar.entry)
     rank_barrier_raw(a.bar.pst, a.bar.n, P.rank, a.bar.leader[P.rank], a.rank_ctas[P.rank], (e - 1) * per_call + 1,
                      a.bar.gpu_scope);
+  TS_MARK();
   for (int oi = 0; oi < P.nops; oi++) {
     const LLArgs::Op& op = P.op[oi];
+    TS_MARK();
     if (op.code == D_SYNC_CTA) {
       __syncthreads();
       continue;
@@ -837,19 +863,32 @@ __global__ void __launch_bounds__(512, 2) plan_ll_kernel(const __grid_constant__
     // time, so packets are read while still in L2 (the hand one-shot's
     // schedule; the host checked the pair's symmetry).  One call site of the
     // unit body keeps its in-flight sources in registers.
+    // A fused broadcast (host-checked: the PUT_PACKETS two ops on sends this
+    // MULTI's destination, the sync between them orders only that) takes the
+    // reduced unit straight from registers.
+    const bool fput = oi == P.fuse_put;
     const LLArgs::Op& m = P.op[oi + streamed];
-    const uint32_t pflag = streamed ? runtime_flag(e, fs, op.llflag) : 0u;
+    const LLArgs::Op& bp = P.op[oi + 2 * fput];
+    const uint32_t pflag = streamed ? runtime_flag(e, fs, op.llflag) : fput ? runtime_flag(e, fs, bp.llflag) : 0u;
     uint64_t prev = ~(uint64_t)0;
     for (uint64_t u = u0 + threadIdx.x;; u += blockDim.x) {
       const bool has = u < u1;
       if (streamed && has) ll_bcast_unit(op, u, pflag, op.ndst, a.bar.gpu_scope);
       const uint64_t mu = streamed ? prev : (has ? u : ~(uint64_t)0);
-      if (mu != ~(uint64_t)0) ll_multi_unit<T>(m, mu, e, fs, rs);
+      if (mu != ~(uint64_t)0) {
+        const uint2 r = ll_multi_unit<T>(m, mu, e, fs, rs);
+        if (fput) {
+#pragma unroll
+          for (int k = 0; k < 8; k++)
+            if (k < bp.ndst) ll16_put_scoped(bp.dst[k] + mu * 16, r, pflag, a.bar.gpu_scope);
+        }
+      }
       if (!has) break;
       prev = u;
     }
-    oi += streamed;
+    oi += streamed + 2 * fput;
   }
+  TS_MARK();
   if (a.bar.exit)
     rank_barrier_raw(a.bar.pst, a.bar.n, P.rank, a.bar.leader[P.rank], a.rank_ctas[P.rank], e * per_call,
                      a.bar.gpu_scope);
@@ -861,6 +900,8 @@ __global__ void __launch_bounds__(512, 2) plan_ll_kernel(const __grid_constant__
       *(volatile uint64_t*)&rs->epoch = e;
     }
   }
+  TS_MARK();
+  TS_DUMP("planll", P.rank);
 }
 
 const void* plan_ll_kernel_for(int dtype) {
