@@ -2,12 +2,15 @@
 usage: python scripts/ncu_hot.py report.ncu-rep [N]"""
 import csv
 import io
+import os
 import subprocess
 import sys
 
+NCU = "/usr/local/cuda/bin/ncu" if os.path.exists("/usr/local/cuda/bin/ncu") else "ncu"
+
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 20
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+out = subprocess.run([NCU, "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 hdr = next(i for i, r in enumerate(rows) if r and r[0] == "Address")
