@@ -794,6 +794,14 @@ __device__ __forceinline__ uint2 ll_multi_unit(const LLArgs::Op& op, uint64_t u,
   return res;
 }
 
+// Streamed packet pairs: a thread reduces unit u this many of its iterations
+// after putting it (the peers' packets for u then had as long to land).
+#ifndef CF_PLL_LAG
+#define CF_PLL_LAG 2
+#endif
+constexpr int kStreamLag = CF_PLL_LAG;
+static_assert(kStreamLag == 1 || kStreamLag == 2, "stream lag of 1 or 2 iterations");
+
 // The compiled LL plan kernel (see LLArgs).  Op fields are read from the
 // parameter space (uniform per CTA); every thread reads the call epoch itself.
 template <typename T>
@@ -858,8 +866,8 @@ __global__ void __launch_bounds__(512, 2) plan_ll_kernel(const __grid_constant__
     }
     // MULTI / COPY, one 8-byte payload unit per thread.  A streamed pair
     // (PUT_PACKETS + the MULTI reducing the packets the peers' puts land)
-    // runs interleaved: a thread reduces unit u one iteration after putting
-    // it, and the peers' threads with the same index put it at about the same
+    // runs interleaved: a thread reduces unit u kStreamLag iterations after
+    // putting it, and the peers' threads with the same index put it at about the same
     // time, so packets are read while still in L2 (the hand one-shot's
     // schedule; the host checked the pair's symmetry).  One call site of the
     // unit body keeps its in-flight sources in registers.
@@ -870,12 +878,13 @@ __global__ void __launch_bounds__(512, 2) plan_ll_kernel(const __grid_constant__
     const LLArgs::Op& m = P.op[oi + streamed];
     const LLArgs::Op& bp = P.op[oi + 2 * fput];
     const uint32_t pflag = streamed ? runtime_flag(e, fs, op.llflag) : fput ? runtime_flag(e, fs, bp.llflag) : 0u;
-    uint64_t prev = ~(uint64_t)0;
+    constexpr uint64_t kNone = ~(uint64_t)0;
+    uint64_t q0 = kNone, q1 = kNone;   // units put and not yet reduced (streamed)
     for (uint64_t u = u0 + threadIdx.x;; u += blockDim.x) {
       const bool has = u < u1;
       if (streamed && has) ll_bcast_unit(op, u, pflag, op.ndst, a.bar.gpu_scope);
-      const uint64_t mu = streamed ? prev : (has ? u : ~(uint64_t)0);
-      if (mu != ~(uint64_t)0) {
+      const uint64_t mu = streamed ? (kStreamLag == 2 ? q1 : q0) : (has ? u : kNone);
+      if (mu != kNone) {
         const uint2 r = ll_multi_unit<T>(m, mu, e, fs, rs);
         if (fput) {
 #pragma unroll
@@ -883,8 +892,9 @@ __global__ void __launch_bounds__(512, 2) plan_ll_kernel(const __grid_constant__
             if (k < bp.ndst) ll16_put_scoped(bp.dst[k] + mu * 16, r, pflag, a.bar.gpu_scope);
         }
       }
-      if (!has) break;
-      prev = u;
+      if (kStreamLag == 2) q1 = q0;
+      q0 = has ? u : kNone;
+      if (!has && (!streamed || (q0 == kNone && q1 == kNone))) break;
     }
     oi += streamed + 2 * fput;
   }
