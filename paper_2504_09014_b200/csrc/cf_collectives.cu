@@ -282,6 +282,9 @@ constexpr int kLL2U = CF_LL2U;
 #ifndef CF_LL1_STREAM
 #define CF_LL1_STREAM 1
 #endif
+#ifndef CF_LL1_LAG
+#define CF_LL1_LAG 2
+#endif
 template <typename T, int NR>
 __global__ void __launch_bounds__(512, 2) ll_oneshot_kernel(const __grid_constant__ CollArgs a) {
   const RankCtx& rk = a.rk[blockIdx.y];
@@ -319,13 +322,30 @@ __global__ void __launch_bounds__(512, 2) ll_oneshot_kernel(const __grid_constan
     store_unit<T>(rk.out[r], u, reduce_units<T, NR>(x, n), a.count);
   };
 #if CF_LL1_STREAM
-  // Streamed: every thread reads unit u one iteration after putting it (the
-  // peers' threads with the same index put it at about the same time), so
-  // packets are consumed while they are still in L2 instead of after the
-  // whole message was scattered (lag 1 hides the flag round trip).  Every rank
-  // launches the same grid (same count, same occupancy on a homogeneous box),
-  // so the unit a thread waits for was put, one iteration earlier, by a
-  // thread that is itself never waiting on a later unit.
+  // Streamed: every thread reads unit u CF_LL1_LAG iterations after putting
+  // it (the peers' threads with the same index put it at about the same
+  // time), so packets are consumed while they are still in L2 instead of after
+  // the whole message was scattered.  Every rank launches the same grid (same
+  // count, same occupancy on a homogeneous box), so the unit a thread waits
+  // for was put, iterations earlier, by a thread that is itself never waiting
+  // on a later unit.  Lag 2 (default) vs 1: the peers' packets had two put
+  // rounds to land, fewer re-polls (1 MiB 42.0 -> 37.2 us, 4 MiB 166 -> 162 us,
+  // 16 KiB 5.1 -> 4.9 us; 8 co-resident ranks, bf16).
+#if CF_LL1_LAG == 2
+  uint2 prev = first, prev2 = make_uint2(0u, 0u);
+  for (size_t u = t0; u < nunit; u += stride) {
+    const uint2 x = u == t0 ? first : load_unit<T>(rk.in[r], u, a.count);
+    put(u, x);
+    if (u >= t0 + 2 * stride) read(u - 2 * stride, prev2);
+    prev2 = prev;
+    prev = x;
+  }
+  if (t0 < nunit) {
+    const size_t last = t0 + (nunit - 1 - t0) / stride * stride;
+    if (last >= t0 + stride) read(last - stride, prev2);
+    read(last, prev);
+  }
+#else
   uint2 prev = first;
   for (size_t u = t0; u < nunit; u += stride) {
     const uint2 x = u == t0 ? first : load_unit<T>(rk.in[r], u, a.count);
@@ -334,6 +354,7 @@ __global__ void __launch_bounds__(512, 2) ll_oneshot_kernel(const __grid_constan
     prev = x;
   }
   if (t0 < nunit) read(t0 + (nunit - 1 - t0) / stride * stride, prev);
+#endif
 #else
   for (size_t u = t0; u < nunit; u += stride) put(u, u == t0 ? first : load_unit<T>(rk.in[r], u, a.count));
   TS_MARK();
