@@ -51,10 +51,11 @@ def main():
         rs = [torch.randn(rows, 256, device="cuda") for _ in range(n)]
         for algo in ("1pa_hb", "2pa"):
             allreduce_add_rmsnorm(w, xs, rs, torch.ones(256, device="cuda"), algo=algo)
-    # K10: LL plans at a small scale (batched packet items over every thread,
-    # unfused reads) and a larger one (fused reads, prefetch hints), HB plan
+    # K10: LL plans at a small scale (batched packet items over every thread)
+    # and larger ones (fused reads, the 2pa_ll reduce broadcast from registers,
+    # the 1pa scatter / read-reduce streamed), HB plan
     for name, scale in (("1pa_n4_e8", 3), ("2pa_ll_n4_e8", 3), ("1pa_n4_e8", 4096), ("2pa_ll_n4_e8", 4096),
-                        ("2pa_memory_n4_e8", 1000)):
+                        ("1pa_n4_e8", 65536 + 8), ("2pa_memory_n4_e8", 1000)):
         with open(os.path.join(ROOT, "tests", "golden", "plans", name + ".json"), "rb") as f:
             rt = Runtime(scale_plan(parse_plan(f.read()), scale), w, dtype="f32")
         ins = gen_inputs(n, rt.in_elems, "f32", "normal", scale)
