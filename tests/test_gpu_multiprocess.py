@@ -184,7 +184,10 @@ def test_two_processes_one_gpu_all_collectives():
 
 PLAN_CASES = [("2pa", "memory", 2048, "f32"), ("2pa", "ll", 1024, "f32"), ("1pa", "", 512, "bf16"),
               ("ring_rs", "", 4096, "f32"), ("allpairs_ag", "", 1000, "f32"), ("2pr", "", 4096, "bf16"),
-              ("2pa", "port", 4096, "f32")]
+              ("2pa", "port", 4096, "f32"),
+              # compiled LL kernel across processes: the 1pa scatter / read-reduce
+              # streamed, the 2pa_ll reduce broadcast from registers
+              ("1pa", "", 1 << 20, "f32"), ("2pa", "ll", 65536, "bf16")]
 
 
 def _plan_doc(name, var, elems, dtype, n):
@@ -225,8 +228,8 @@ def _plan_worker(rank, world, port, q):
             torch.cuda.synchronize()
             rt.check_device_error()
             got = recv.cpu()
-            out[(name, var)] = (got.view(torch.int16).numpy().view(np.uint16) if dtype == "bf16"
-                                else got.numpy()).copy()
+            out[(name, var, elems)] = (got.view(torch.int16).numpy().view(np.uint16) if dtype == "bf16"
+                                       else got.numpy()).copy()
             comm.deregister(send)
             comm.deregister(recv)
             rt.close()
@@ -266,7 +269,7 @@ def test_two_processes_one_gpu_plans():
         ins = gen_inputs(world, in_elems, dtype, "normal", 31 + elems)
         want = oracle.run_plan(doc, ins, dtype=dtype)
         for r in range(world):
-            assert np.array_equal(res[r][(name, var)].view(np.uint8), want[r].view(np.uint8)), (name, var, r)
+            assert np.array_equal(res[r][(name, var, elems)].view(np.uint8), want[r].view(np.uint8)), (name, var, r)
 
 
 def _worker4(rank, world, port, q):
