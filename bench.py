@@ -158,7 +158,9 @@ def run_reference_arm(args):
     cpu_reference_steps(ins, HEAD_DTYPE, "2pa", max(1, args.warmup))
     ts = cpu_reference_steps(ins, HEAD_DTYPE, "2pa", args.steps)
     t = float(np.mean(ts))
-    v = busbw(HEAD_BYTES, t, nr)
+    # the cf arm's definition: at N>1 the aggregate over the N ranks' GPUs
+    # (N x busbw of the same-sized job), at N=1 the one GPU's busbw
+    v = busbw(HEAD_BYTES, t, nr) * (args.gpus if args.gpus > 1 else 1)
     line = {"impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": "GB/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(t * 1e3, 3), "higher_is_better": True, "scaling": "weak",
@@ -939,11 +941,18 @@ def run_multi_gpu(args):
     t, te, sweep = gather_max_over_ranks(t_local, float(np.mean(e2e_local)), rows_local, world)
     ok = all(v is True for v in parity.values())
     if rank == 0:
-        value = busbw(HEAD_BYTES, t, world)
+        # `value` is the whole-job aggregate (the contract): the bus bandwidth
+        # of every GPU summed, N x the per-GPU busbw (nccl-tests definition,
+        # reported beside it; the roofline and % of 900 GB/s are per GPU)
+        per_gpu = busbw(HEAD_BYTES, t, world)
+        value = world * per_gpu
+        e2e_gpu = busbw(HEAD_BYTES, te, world)
         where = (f"{world} ranks sharing cuda:0 (time-sliced path check; not an NVLink measurement)"
                  if one_gpu else f"{world} ranks, one per GPU, peer loads/stores over NVLink 5 / NVSwitch")
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
+            "busbw_per_gpu": round(per_gpu, 2),
+            "value_definition": "aggregate over GPUs: n_gpus x per-GPU busbw (max-over-ranks time)",
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t * 1e3, 4),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": HEAD_DTYPE,
             "data": "synthetic",
@@ -956,8 +965,9 @@ def run_multi_gpu(args):
                        "l2": "inputs larger than L2 (headline); sweep rows < 64 MiB flush L2 between "
                              "timed iterations (both arms)"},
             "parity": parity,
-            "e2e": {"value": round(busbw(HEAD_BYTES, te, world), 3), "unit": "GB/s",
-                    "h2d_bytes_per_step": HEAD_BYTES, "d2h_bytes_per_step": HEAD_BYTES,
+            "e2e": {"value": round(world * e2e_gpu, 3), "unit": "GB/s", "busbw_per_gpu": round(e2e_gpu, 3),
+                    "h2d_bytes_per_step": world * HEAD_BYTES, "d2h_bytes_per_step": world * HEAD_BYTES,
+                    "bytes_note": "all ranks (HEAD_BYTES per rank each way)",
                     "ms_per_step": round(te * 1e3, 3),
                     "api": "Communicator.all_reduce_host (cfAllReduceHostStaged), pinned host tensors"},
             "gpu_launches": args.steps, "clocks": clk.summary(), "tuned_selection": tuned,
@@ -975,9 +985,9 @@ def run_multi_gpu(args):
                 for v in row.values():
                     if isinstance(v, dict) and v.get("busbw") is not None:
                         v["pct_of_900"] = round(100 * v["busbw"] / 900, 2)
-            line["pct_of_900"] = round(100 * value / 900, 2)
-            line["roofline"] = {"bound": "nvlink", "achieved": round(value, 1), "peak": 900.0,
-                                "unit": "GB/s", "frac": round(value / 900, 4), "traffic": None,
+            line["pct_of_900"] = round(100 * per_gpu / 900, 2)
+            line["roofline"] = {"bound": "nvlink", "achieved": round(per_gpu, 1), "peak": 900.0,
+                                "unit": "GB/s", "frac": round(per_gpu / 900, 4), "traffic": None,
                                 "note": "busbw per GPU per direction vs nominal NVLink 5 (no measured "
                                         "NVLink peak in MEASURED_PEAKS.json)"}
         print(json.dumps(line))
