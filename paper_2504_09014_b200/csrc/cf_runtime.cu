@@ -727,10 +727,11 @@ cfStatus launch(cfComm* c, const Job& j, int dtype, const void* const* send, voi
   const bool ring = j.kind == kRing || j.kind == kRingGather;
   int threads = j.kind == kRing ? std::min(c->cfg.threads, 256) : c->cfg.threads;   // ring_kernel's bound
   if (j.threads) threads = j.threads;
-  if (j.kind == kNorm && j.blocks > max_blocks_per_rank(c, kernel, 0, threads, 0, j.algo))
-    // K13 rows per rank beyond one resident round: 256-thread CTAs (2 per SM)
-    // finish them in one round (b=256: 22.3 -> 20.3 us; fewer rows keep 512)
-    threads = std::min(threads, 256);
+  // K13 keeps 512-thread CTAs at every row count: with phase 2 pipelined over
+  // a CTA's rows, a 512-thread CTA holds a whole 8192-wide bf16 row in
+  // registers (no second-pass re-reads) and beats two 256-thread CTAs per SM
+  // even when rows take several rounds (C5 b=64 16.4 -> 14.2 us, b=256 40.9 ->
+  // 35.3 us; scripts/k13_threads_ab.py)
   if (j.kind == kNorm)
     if (const char* env = getenv("CF_K13_THREADS")) threads = atoi(env);   // diagnostics
   for (size_t gi = 0; gi < c->groups.size(); gi++) {
