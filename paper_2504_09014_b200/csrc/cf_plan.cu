@@ -717,9 +717,12 @@ cfStatus load(cfComm* c, const char* json, size_t len, int dtype_override, cfPla
     }
   }
   if (cap < 1) return fail(CF_E_CONFIG, "plan has more programs per device than co-resident CTAs");
-  // one 16-byte vector (LL plans: one 8-byte packet unit) per thread per
-  // source and CTA: latency, not issue, bound (1pa plan b=1 11.6 -> 9.5 us)
-  long long per_cta = (long long)pl->threads * (packets ? 8 : 16);
+  // a quarter of a 16-byte vector (half an 8-byte packet unit) per thread and
+  // CTA: small plans are latency-bound, more CTAs keep more loads in flight
+  // (C5 2pa plan b=4 4.8 -> 3.8 us, b=16 5.1 -> 4.1 us; 2pa_ll b=4 9.2 -> 8.6
+  // us; b >= 64 unchanged: the 32-CTA cap applies; was one vector / unit per
+  // thread, 1pa plan b=1 11.6 -> 9.5 us before that)
+  long long per_cta = (long long)pl->threads * 4;
   if (const char* ev = getenv("CF_PLAN_BYTES_PER_CTA")) per_cta = std::max(1LL, atoll(ev));   // diagnostic
   pl->K = (int)std::max(1LL, std::min<long long>({(max_bytes + per_cta - 1) / per_cta, (long long)cap, 32LL}));
   const int K = pl->K;
