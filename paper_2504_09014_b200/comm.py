@@ -346,7 +346,9 @@ class Communicator:
         x.copy_(torch.randn(per_in, device=self.device).to(tdt))
         fn = {"allreduce": L.cfAllReduce, "allgather": L.cfAllGather}[kind]
         barrier = lambda: dist.barrier(group=self.group)   # noqa: E731
-        names = list(algos or T.CANDIDATES[kind])
+        # AUTO never picks 1pa_hb one process per GPU (cfAllReduce: the
+        # in-place test is not rank-uniform there), so it is not a candidate
+        names = [a for a in (algos or T.CANDIDATES[kind]) if a != "1pa_hb"]
         if nvls and kind == "allreduce" and sym == 1:
             names.append("switch_2pa")
         local = torch.full((len(names), len(sizes)), -1.0, dtype=torch.float64)

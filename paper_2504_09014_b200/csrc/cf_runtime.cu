@@ -926,9 +926,17 @@ extern "C" cfStatus cfAllReduce(cfComm_t c, const void* const* send, void* const
   const bool sym_switch = sym_switch_ok(c, send, recv, bytes, &oi, &oo);
   if (algo == CF_ALGO_AUTO) {
     algo = select_algo(c, 0, bytes, dtype);
+    // 1pa_hb cannot run in place.  In one process every rank is local, so the
+    // in-place test is rank-uniform; one process per GPU cannot see the
+    // peers' pointers, so AUTO there never picks 1pa_hb (ranks running in
+    // place and out of place would launch different kernels on the same
+    // handshake slots): the LL one-shot (in-place safe) when it fits, else
+    // the two-shot pull.  An explicit CF_ALGO_1PA_HB is still honoured.
+    if (algo == CF_ALGO_1PA_HB && c->multiprocess)
+      algo = bytes <= c->cfg.ll_max_bytes ? CF_ALGO_1PA : CF_ALGO_2PA;
     if (algo == CF_ALGO_1PA_HB)
       for (size_t li = 0; li < c->local.size(); li++)
-        if (send[li] == recv[li]) algo = CF_ALGO_2PA;   // 1pa_hb cannot run in place
+        if (send[li] == recv[li]) algo = CF_ALGO_2PA;
     // symmetric buffers on a real multicast heap: the in-place NVLS kernel
     // moves S per rank per direction on NVLink instead of 2(n-1)/n S
     // (provisional crossover until an NVLink sweep measures it)

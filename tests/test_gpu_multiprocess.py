@@ -78,6 +78,16 @@ def _worker(rank, world, port, q):
         comm.all_reduce(tin, tout, algo="auto")
         torch.cuda.synchronize()
         out[("tune_auto",)] = tout.cpu().numpy().copy()
+        # a table that would pick 1pa_hb, rank 0 in place and rank 1 out of
+        # place: AUTO must still launch one kernel on both ranks
+        from paper_2504_09014_b200 import tune as T
+        T.install(comm._comm, "allreduce", "f32", [(1 << 30, "1pa_hb")])
+        mx = tin[:4096].clone()
+        comm.register(mx)
+        comm.all_reduce(mx, mx if rank == 0 else tout[:4096], algo="auto")
+        torch.cuda.synchronize()
+        out[("mixed_inplace",)] = (mx if rank == 0 else tout[:4096]).cpu().numpy().copy()
+        comm.deregister(mx)
         comm.deregister(tin)
         comm.deregister(tout)
         # pipelined host-buffer AllReduce (windows: >= 32 MiB per rank, ragged)
@@ -159,6 +169,7 @@ def test_two_processes_one_gpu_all_collectives():
     tsum = oracle.allreduce(gen_inputs(world, 1 << 18, "f32", "int", 3), "oracle", "f32")
     for r in range(world):
         assert np.array_equal(res[r][("tune_auto",)], tsum[r])
+        assert np.array_equal(res[r][("mixed_inplace",)], tsum[r][:4096])
     hins = gen_inputs(world, (40 << 20) // 4 + 3, "f32", "uniform", 9)
     hwant = oracle.allreduce(hins, "2pa", "f32")
     hsmall = oracle.allreduce([x[:1000] for x in hins], "2pa", "f32")
