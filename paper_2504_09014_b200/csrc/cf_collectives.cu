@@ -89,12 +89,13 @@ __device__ __forceinline__ void handshake(const RankCtx& rk, int n, uint64_t v, 
   __syncthreads();
 }
 
-// Barrier over every CTA of every rank: CTA b of rank r publishes its writes
-// and marks slot (r, b) on every rank (its own included), then waits until
-// all n x G slots of its own rank carry `v`.  The whole grid of every rank
+// Barrier over every CTA of every rank, in two halves: cta_arrive publishes
+// this CTA's writes and marks slot (r, b) on every rank; all_wait returns
+// once all n x G slots of this rank carry `v` (every thread of the CTA calls
+// both, each with the call's epoch in `v`).  The whole grid of every rank
 // must be resident (the CTA budget / co-residency cap guarantees it).
-__device__ __forceinline__ void all_cta_barrier(const RankCtx& rk, int n, uint64_t v, bool gpu) {
-  const int t = threadIdx.x, r = rk.rank, b = blockIdx.x, G = gridDim.x;
+__device__ __forceinline__ void cta_arrive(const RankCtx& rk, int n, uint64_t v, bool gpu) {
+  const int t = threadIdx.x, r = rk.rank, b = blockIdx.x;
 #if CF_DROP_FENCE != 1
   fence_publish(gpu);
 #endif
@@ -107,7 +108,13 @@ __device__ __forceinline__ void all_cta_barrier(const RankCtx& rk, int n, uint64
     st_release(rk.sem[t] + sem_index(r, b), v, gpu);
 #endif
   }
-  for (int i = t; i < n * G; i += blockDim.x) wait_geq(rk.sem[r] + sem_index(i / G, i % G), v, rk.st, gpu);
+}
+// ... or once every CTA of every rank has: one thread per slot, all n x G
+// slots polled in parallel (measured: one warp polling every slot with
+// relaxed loads and one acquire fence is slower, C5 K13 b=256 37.5 vs 36.9 us)
+__device__ __forceinline__ void all_wait(const RankCtx& rk, int n, uint64_t v, bool gpu) {
+  const int G = gridDim.x;
+  for (int i = threadIdx.x; i < n * G; i += blockDim.x) wait_geq(rk.sem[rk.rank] + sem_index(i / G, i % G), v, rk.st, gpu);
   __syncthreads();
 }
 
@@ -1262,11 +1269,13 @@ __global__ void __launch_bounds__(512) ar_rmsnorm_kernel(const __grid_constant__
   constexpr int kCache = (NR >= 8 || sizeof(T) >= 4) ? 2 : 4;   // vectors of a thread's share held in registers between the passes
   const int n = a.n, r = rk.rank;
   const bool push = a.push;
-  // The epoch is needed only by the handshaking threads (t < n) and thread 0
-  // at the end: those threads load it themselves, nobody waits for it.
+  // Single launch: the epoch is needed by thread 0 at the end and, two-shot,
+  // by every thread that arrives or waits on the owners' CTAs (t < max(n, G)):
+  // each thread loads it itself (before its CTA's arrival is counted in
+  // end_call), nobody waits for a block barrier.
   uint64_t e;
   if (!a.single_launch) e = begin_call(rk);
-  else if (push) e = (int)threadIdx.x < n ? *(volatile uint64_t*)&rk.st->epoch + 1 : 0;
+  else if (push) e = *(volatile uint64_t*)&rk.st->epoch + 1;
   else e = begin_call_lazy(rk, true);
   if (!a.single_launch) handshake(rk, n, e * kPhases + 1, false, a.gpu_scope);
   const size_t nv = a.hidden / V;
@@ -1280,6 +1289,7 @@ __global__ void __launch_bounds__(512) ar_rmsnorm_kernel(const __grid_constant__
     const size_t G = gridDim.x, stride = G * NT;
     const size_t r0 = min((size_t)r * per, a.rows), r1 = min(r0 + per, a.rows);
     const size_t v1 = r1 * nv;
+    CF_STRESS_AT(11);   // late pushes: phase 2 must wait for the owners' arrivals
     for (size_t v = r0 * nv + blockIdx.x * NT + T0; v < v1; v += 2 * stride) {
       const bool two = v + stride < v1;
       uint4 x0[NR], x1[NR];
@@ -1302,7 +1312,13 @@ __global__ void __launch_bounds__(512) ar_rmsnorm_kernel(const __grid_constant__
     }
     TS_MARK();
     // every CTA of every rank pushed: any row may now be finished anywhere
-    all_cta_barrier(rk, n, e * kPhases + 2, a.gpu_scope);
+    // (measured: waiting per row for the CTAs of the row's owner only is
+    // slower, C5 b=256 39.5 vs 36.9 us -- one wait per owner change stalls the
+    // software pipeline of phase 2)
+    cta_arrive(rk, n, e * kPhases + 2, a.gpu_scope);
+#if CF_DROP_FENCE != 7
+    all_wait(rk, n, e * kPhases + 2, a.gpu_scope);
+#endif
     TS_MARK();
   }
   // finish a row on this rank: h (reduced here, or pushed by its owner) +

@@ -208,6 +208,7 @@ __device__ __forceinline__ void st_masked16(char* base, uint4 v, int jlo, int jh
 //   4  LL packets: flags stored before (and apart from) the payload words
 //   5  exit / phase handshakes: signal without waiting for the peers
 //   6  ring credits: the sender does not wait for the receiver's ack
+//   7  K13 two-shot: phase 2 does not wait for the owners' arrivals
 #ifndef CF_DROP_FENCE
 #define CF_DROP_FENCE 0
 #endif

@@ -68,6 +68,7 @@ MUTATIONS = {
     4: "LL packets: flags stored apart from (before) the payload",
     5: "exit / phase handshakes: signal without waiting",
     6: "ring credits: sender skips the receiver's ack",
+    7: "K13 two-shot: phase 2 reads the pushed rows without waiting for the owners' arrivals",
 }
 
 
